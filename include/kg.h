@@ -1,0 +1,188 @@
+/*
+ * kg.h -- C-ABI of libkg.so: one training step of batched multi-hop
+ * query-embedding models on a B200 (sm_100a), after SMORE (arXiv 2110.14890).
+ *
+ * Citations: P:Lnnn = /root/reference/PAPER.md line nnn.  The readings A1-A24
+ * referred to below are listed in DESIGN.md §3.
+ *
+ * Conventions for every call
+ *   - Every call returns kg_status (KG_OK = 0).  No C++ exception crosses the
+ *     ABI.  On error, kg_last_error(handle) returns a NUL-terminated message
+ *     owned by the handle (valid until the next call on that handle).
+ *   - Memory ownership: the CALLER owns all table memory (theta_E shard, its
+ *     Adam moments, theta_D and its moments), allocated on the handle's device
+ *     and bound with kg_bind; the library never frees it.  The library owns the
+ *     handle, its device workspace, pinned staging buffers, cuBLAS handle and
+ *     NCCL communicator, all released by kg_destroy.
+ *   - Host input arrays need only stay valid until the call returns (they are
+ *     staged before return).  Device input arrays (kg_batch.on_device = 1)
+ *     must stay valid until the step has executed on the bound stream.
+ *   - All device work is enqueued on the stream given to kg_bind, in order.
+ *   - Transactional: on a validation error nothing is enqueued; when the loss
+ *     of a step is non-finite, the update kernels see a device flag and leave
+ *     every table untouched (KG_ENONFINITE is reported by the call that reads
+ *     the loss: kg_step with info != NULL, or kg_sync).
+ *   - A CUDA / NCCL failure moves the handle to a sticky error state: later
+ *     calls return KG_ESTATE.
+ *   - world > 1: every rank calls kg_step / kg_score / kg_read_rows with the
+ *     same structure, M and K (collective calls).
+ */
+#ifndef KG_H_
+#define KG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  KG_OK = 0,
+  KG_EINVAL = 1,        /* null pointer, out-of-range id / size / config value */
+  KG_EUNSUPPORTED = 2,  /* e.g. a multi-hop structure for a single-hop model */
+  KG_ENOMEM = 3,        /* device / pinned allocation failed */
+  KG_ECUDA = 4,         /* CUDA runtime / cuBLAS error (handle -> sticky state) */
+  KG_ENCCL = 5,         /* NCCL error (handle -> sticky state) */
+  KG_ENONFINITE = 6,    /* the step's loss was not finite; the step was not applied */
+  KG_ESTATE = 7         /* handle unusable (earlier CUDA/NCCL error, or not bound) */
+} kg_status;
+
+/* Models of Table 1 and Table 2. */
+typedef enum {
+  KG_GQE = 0, KG_Q2B = 1, KG_BETAE = 2,                  /* multi-hop, all 9 structures */
+  KG_TRANSE = 3, KG_ROTATE = 4, KG_DISTMULT = 5, KG_COMPLEX = 6  /* single-hop: 1p only */
+} kg_model_kind;
+
+/* Query structures, DNF for unions. */
+typedef enum {
+  KG_1P = 0, KG_2P = 1, KG_3P = 2, KG_2I = 3, KG_3I = 4,
+  KG_IP = 5, KG_PI = 6, KG_2U = 7, KG_UP = 8
+} kg_structure;
+
+/* Number of anchor / relation slots of a structure (execution order, A21):
+ * anchors 1p,2p,3p:1  2i:2  3i:3  ip,pi,2u,up:2
+ * relations 1p:1 2p:2 3p:3 2i:2 3i:3 ip:3 pi:3 2u:2 up:3                  */
+
+typedef struct {
+  int32_t kind;          /* kg_model_kind */
+  int32_t dim;           /* d: fp32 values per entity row (A1); must be a multiple of 8, <= 2048 */
+  int64_t n_entities;    /* |V|: 1 <= n_entities < 2^31 */
+  int32_t n_relations;   /* |R| >= 1 */
+  int32_t hidden;        /* BetaE projection MLP width H (A9), multiple of 8; ignored otherwise */
+  float gamma;           /* margin of Eq. 1 */
+  float box_alpha;       /* Q2B in-box weight alpha (Table 1, A7) */
+  float beta1, beta2, eps; /* Adam (A15) */
+  int32_t max_M;         /* workspace sizing: queries per step */
+  int32_t max_K;         /* workspace sizing: shared negatives per step */
+  int32_t max_cand;      /* workspace sizing: candidates per kg_score call */
+  int32_t rank, world;   /* this process's rank in [0, world); theta_E is row-sharded, owner(id) = id % world */
+  const void *nccl_id;   /* world > 1: pointer to a 128-byte ncclUniqueId shared by all ranks; NULL if world == 1 */
+} kg_config;
+
+/* Caller-owned device tables (fp32, row-major).
+ * ent, ent_m, ent_v : [kg_shard_rows() x dim]  theta_E row shard + Adam moments
+ *                     local row of global id g is g / world (owner g % world).
+ * dense, dense_m, dense_v : [kg_dense_size()]  theta_D = relation tables + operator weights
+ *                     (P:L300), layout of DESIGN.md §5 (= kggen.dense_layout).             */
+typedef struct {
+  float *ent, *ent_m, *ent_v;
+  float *dense, *dense_m, *dense_v;
+} kg_tables;
+
+/* One mini-batch (N, {(q_i, V_qi, A_qi)}_{i=1..M}, Mask) of P:L389, one structure.
+ * anchors   int64 [M][n_anchors(structure)]  anchor entity ids (leaves of the plan)
+ * relations int32 [M][n_relations(structure)] relation ids in execution order (A21)
+ * answers   int64 [M]                         the single positive a_q per query
+ * negatives int64 [K]                         the shared pool N, duplicates allowed (A20)
+ * mask      uint32 [M][ceil(K/32)]            bit (j%32) of word j/32 set <=> negatives[j] is a
+ *                                             negative of query i (Mask_ij of P:L389)
+ * on_device 0: host pointers; 1: device pointers on the handle's device.
+ * For kg_score only structure, M, anchors and relations are read.                               */
+typedef struct {
+  int32_t structure;
+  int32_t M;
+  int32_t K;
+  const int64_t *anchors;
+  const int32_t *relations;
+  const int64_t *answers;
+  const int64_t *negatives;
+  const uint32_t *mask;
+  int32_t on_device;
+} kg_batch;
+
+typedef struct {
+  double loss;           /* global Eq. 1 loss of the step (mean over queries and ranks, A12, A18) */
+  int32_t n_touched;     /* distinct entity ids touched by this rank's batch (A16) */
+  int64_t step;          /* Adam step counter t after the step */
+} kg_step_info;
+
+typedef struct kg_handle kg_handle;   /* opaque; one per (process, device) */
+
+/* Create a handle on the current CUDA device: validates cfg, allocates the
+ * workspace for (max_M, max_K, max_cand), creates cuBLAS (and NCCL when
+ * world > 1).  EINVAL on a bad config (dim % 8 != 0, odd sizes, ...). */
+kg_status kg_create(const kg_config *cfg, kg_handle **out);
+
+/* Rows of the local theta_E shard: ceil(n_entities / world). */
+int64_t kg_shard_rows(const kg_handle *h);
+
+/* Floats in theta_D for this model (relation tables + operator weights). */
+int64_t kg_dense_size(const kg_handle *h);
+
+/* Record the caller's table pointers and the CUDA stream (cudaStream_t, may be NULL). */
+kg_status kg_bind(kg_handle *h, const kg_tables *tables, void *cuda_stream);
+
+/* Parameter init (A23): counter-based U(lo, hi) of (seed, stream, index) into ent and dense,
+ * zero Adam moments, t = 0.  Identical to kggen.counter_uniform. */
+kg_status kg_init_params(kg_handle *h, uint64_t seed);
+
+/* One training step (stages 2-4, synchronous; A18):
+ * dedup -> fused gather + query DAG forward (Tables 1-2) -> DNF min (A11)
+ * -> positive + shared-negative scoring with Eq. 1 -> backward
+ * -> deterministic segment-reduce of row gradients + sparse Adam on touched rows
+ * -> [world > 1: NCCL all-reduce of dL/dtheta_D] -> dense Adam on theta_D (A17).
+ * lr > 0.  info == NULL: fully asynchronous (nothing waits on the GPU; read the loss
+ * later with kg_sync).  info != NULL: waits for the step and fills info.
+ * Errors: EINVAL (bad pointer/size/id/relation/structure), EUNSUPPORTED (multi-hop
+ * structure for a single-hop kind), ENONFINITE (info != NULL and loss not finite). */
+kg_status kg_step(kg_handle *h, const kg_batch *batch, float lr, kg_step_info *info);
+
+/* Wait for the last enqueued step and report it (ENONFINITE if its loss was not finite). */
+kg_status kg_sync(kg_handle *h, kg_step_info *info);
+
+/* Dist(f(q_i), f(v_c)) for every query of `queries` (forward DAG only) and every
+ * shared candidate cand[c] (n_cand <= max_cand): out_dist host [M][n_cand], lower = closer,
+ * unions = DNF min (A11). */
+kg_status kg_score(kg_handle *h, const kg_batch *queries, const int64_t *cand, int32_t n_cand,
+                   float *out_dist);
+
+/* Test / checkpoint hooks.  which: 0 parameter, 1 Adam m, 2 Adam v.
+ * Rows are global ids owned by this rank (world == 1: any id); out/in host [n][dim]. */
+kg_status kg_read_rows(kg_handle *h, int32_t which, const int64_t *ids, int32_t n, float *out);
+kg_status kg_write_rows(kg_handle *h, int32_t which, const int64_t *ids, int32_t n, const float *in);
+kg_status kg_read_dense(kg_handle *h, int32_t which, float *out);          /* out [kg_dense_size()] */
+kg_status kg_write_dense(kg_handle *h, int32_t which, const float *in);
+
+/* Gradients of the last step, before the optimizer (parity stage (i) of SURVEY §8(c)):
+ * uniq host int64 [cap] = touched ids ascending (A16), grad_rows host [cap][dim] = merged
+ * dL/dtheta_E rows, grad_dense host [kg_dense_size()] = dL/dtheta_D (relation rows
+ * not used by the step are 0).  *n_uniq receives U; EINVAL if U > cap.
+ * Also: if d_neg != NULL, host [M][K] distances D_ij (DNF min, unmasked) and d_pos host [M]. */
+kg_status kg_last_grads(kg_handle *h, int64_t *uniq, float *grad_rows, float *grad_dense,
+                        int32_t cap, int32_t *n_uniq, float *d_pos, float *d_neg);
+
+/* Test hook.  flags bit 0 (default 1): apply the optimizers; 0 computes loss and
+ * gradients but skips both optimizers and t.  bit 1 (default 0): keep the merged
+ * theta_E gradient rows of each step for kg_last_grads (one extra U x dim write). */
+kg_status kg_set_apply(kg_handle *h, int32_t flags);
+
+const char *kg_last_error(const kg_handle *h);
+
+/* Release everything the library owns; never frees caller memory.  NULL is a no-op. */
+void kg_destroy(kg_handle *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KG_H_ */

@@ -1,0 +1,639 @@
+// k_score.cu -- shared-negative scoring, Eq. 1 loss and the scoring backward.
+//
+// PAPER.md §4.3: M queries x |N| shared negatives, "M x |N| pairs of
+// distances ... box or beta ... KL divergence ... customized CUDA kernel ...
+// operation fusion"; Eq. 1; Dist per Table 1 and
+// Table 2; DNF min over disjuncts (A11).
+//
+// Three CUDA-core "generalised GEMM" kernels, all deterministic (no atomics):
+//   pair_fwd   out (i, j), reduce over units k:  D_ij, Eq. 1 epilogue -> per-pair
+//              adjoint coefficient C[t][i][j], loss partials per (j-tile, i)
+//   pair_bwd_q out (r, k), reduce over pool j:   dQ[r][k] += sum_j C_rj dD/dq_rk
+//   pair_bwd_v out (j, k), reduce over rows r:   dV[j][k]  = sum_r C_rj dD/dv_jk
+// plus the per-query positive kernel (D+, its adjoint, its gradients) and the
+// BetaE digamma / lgamma precomputations.
+//
+// Feature layout (A1): row r of Q holds QF features of U units each,
+// Q[r][f*U + k]; raw entity rows are d floats; the BetaE entity feature row is
+// 9 planes of m = d/2: [Pa | Pb | A | B | TA | TB | TAB | GA | GB] with
+// A = e(x_alpha), B = e(x_beta), Pa = psi(A) - psi(A+B), Pb = psi(B) - psi(A+B),
+// TA = psi'(A), TB = psi'(B), TAB = psi'(A+B), GA/GB = d e / d x (clamp mask).
+#include "kg_common.cuh"
+#include "kg_launch.h"
+
+namespace kg {
+
+// ---------------------------------------------------------------- models
+struct ML2 {   // GQE, TransE: ||q - v||_2 (A2)
+  static constexpr int QF = 1, EF = 1, EOFF = 0, BQ_EF = 1, BQ_EOFF = 0, BV_EF = 1, BV_EOFF = 0, AV = 1, OUTF = 1;
+  static constexpr bool kL2 = true, kBeta = false;
+  __device__ static float acc(const float *q, const float *e, float) { const float t = q[0] - e[0]; return t * t; }
+  __device__ static float fin(float s, float, float) { return sqrtf(s); }
+  __device__ static void bq(const float *q, const float *e, float c, float, float *dq) { dq[0] += c * (q[0] - e[0]); }
+  __device__ static void bv(const float *q, const float *e, float c, float, float *a) { a[0] += c * (e[0] - q[0]); }
+};
+struct MBox {  // Q2B: sum ReLU(|v-c| - o) + alpha * min(|v-c|, o) (A7)
+  static constexpr int QF = 2, EF = 1, EOFF = 0, BQ_EF = 1, BQ_EOFF = 0, BV_EF = 1, BV_EOFF = 0, AV = 1, OUTF = 1;
+  static constexpr bool kL2 = false, kBeta = false;
+  __device__ static float acc(const float *q, const float *e, float al) {
+    const float dl = fabsf(e[0] - q[0]);
+    return fmaxf(dl - q[1], 0.f) + al * fminf(dl, q[1]);
+  }
+  __device__ static float fin(float s, float, float) { return s; }
+  __device__ static void bq(const float *q, const float *e, float c, float al, float *dq) {
+    const float dl = e[0] - q[0], a = fabsf(dl), o = q[1];
+    const float s = (dl > 0.f) ? 1.f : ((dl < 0.f) ? -1.f : 0.f);
+    const float outb = a > o ? 1.f : 0.f, inb = a < o ? 1.f : 0.f;
+    dq[0] -= c * s * (outb + al * inb);                 // dD/dc = -s([a>o] + alpha[a<o])
+    dq[1] += c * (-outb + al * (a >= o ? 1.f : 0.f));   // dD/do = -[a>o] + alpha[a>=o]  (A19)
+  }
+  __device__ static void bv(const float *q, const float *e, float c, float al, float *acc_) {
+    const float dl = e[0] - q[0], a = fabsf(dl), o = q[1];
+    const float s = (dl > 0.f) ? 1.f : ((dl < 0.f) ? -1.f : 0.f);
+    acc_[0] += c * s * ((a > o ? 1.f : 0.f) + al * (a < o ? 1.f : 0.f));
+  }
+};
+struct MBeta {  // KL(Beta(entity) || Beta(query)) summed over m (A10), direct per-unit differences (A22)
+  static constexpr int QF = 2, EF = 4, EOFF = 0, BQ_EF = 2, BQ_EOFF = 0, BV_EF = 7, BV_EOFF = 2, AV = 2, OUTF = 2;
+  static constexpr bool kL2 = false, kBeta = true;
+  // e = [Pa, Pb, A, B]
+  __device__ static float acc(const float *q, const float *e, float) { return (e[2] - q[0]) * e[0] + (e[3] - q[1]) * e[1]; }
+  __device__ static float fin(float s, float cq, float cv) { return s + cq - cv; }
+  __device__ static void bq(const float *, const float *e, float c, float, float *dq) { dq[0] -= c * e[0]; dq[1] -= c * e[1]; }
+  __device__ static void bv(const float *q, const float *, float c, float, float *a) { a[0] += c * q[0]; a[1] += c * q[1]; }
+};
+struct MRot {  // RotatE: sum_k |q_k - t_k| (A3)
+  static constexpr int QF = 2, EF = 2, EOFF = 0, BQ_EF = 2, BQ_EOFF = 0, BV_EF = 2, BV_EOFF = 0, AV = 2, OUTF = 2;
+  static constexpr bool kL2 = false, kBeta = false;
+  __device__ static float acc(const float *q, const float *e, float) {
+    const float a = q[0] - e[0], b = q[1] - e[1];
+    return sqrtf(a * a + b * b);
+  }
+  __device__ static float fin(float s, float, float) { return s; }
+  __device__ static void bq(const float *q, const float *e, float c, float, float *dq) {
+    const float a = q[0] - e[0], b = q[1] - e[1], n = sqrtf(a * a + b * b);
+    if (n > 0.f) { const float w = c / n; dq[0] += w * a; dq[1] += w * b; }
+  }
+  __device__ static void bv(const float *q, const float *e, float c, float, float *acc_) {
+    const float a = q[0] - e[0], b = q[1] - e[1], n = sqrtf(a * a + b * b);
+    if (n > 0.f) { const float w = c / n; acc_[0] -= w * a; acc_[1] -= w * b; }
+  }
+};
+struct MDot {  // DistMult: -<q, t> (A13)
+  static constexpr int QF = 1, EF = 1, EOFF = 0, BQ_EF = 1, BQ_EOFF = 0, BV_EF = 1, BV_EOFF = 0, AV = 1, OUTF = 1;
+  static constexpr bool kL2 = false, kBeta = false;
+  __device__ static float acc(const float *q, const float *e, float) { return q[0] * e[0]; }
+  __device__ static float fin(float s, float, float) { return -s; }
+  __device__ static void bq(const float *, const float *e, float c, float, float *dq) { dq[0] -= c * e[0]; }
+  __device__ static void bv(const float *q, const float *, float c, float, float *a) { a[0] -= c * q[0]; }
+};
+struct MCpx {  // ComplEx: -Re<q, conj(t)> = -sum(q_re t_re + q_im t_im) (A13)
+  static constexpr int QF = 2, EF = 2, EOFF = 0, BQ_EF = 2, BQ_EOFF = 0, BV_EF = 2, BV_EOFF = 0, AV = 2, OUTF = 2;
+  static constexpr bool kL2 = false, kBeta = false;
+  __device__ static float acc(const float *q, const float *e, float) { return q[0] * e[0] + q[1] * e[1]; }
+  __device__ static float fin(float s, float, float) { return -s; }
+  __device__ static void bq(const float *, const float *e, float c, float, float *dq) { dq[0] -= c * e[0]; dq[1] -= c * e[1]; }
+  __device__ static void bv(const float *q, const float *, float c, float, float *a) { a[0] -= c * q[0]; a[1] -= c * q[1]; }
+};
+
+__device__ __forceinline__ float4 ld4(const float *p) { return *reinterpret_cast<const float4 *>(p); }
+
+// ---------------------------------------------------------------- pair_fwd
+template <class Mdl, int NOUT, bool TRAIN>
+__global__ void __launch_bounds__(256) pair_fwd_kernel(ScoreArgs a) {
+  constexpr int BI = 64, BJ = 64, KC = 16, PAD = 4;
+  __shared__ __align__(16) float sQ[NOUT][Mdl::QF][KC][BI + PAD];
+  __shared__ __align__(16) float sE[Mdl::EF][KC][BJ + PAD];
+  __shared__ int64_t sRow[BJ];
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  const int i0 = blockIdx.y * BI, j0 = blockIdx.x * BJ;
+  const int M = a.M, K = a.K, U = a.U;
+  const int qstride = Mdl::QF * U;
+  if (t < BJ) {
+    const int j = j0 + t;
+    sRow[t] = (j < K) ? (a.eidx ? a.eidx[j] : (int64_t)j) : 0;
+  }
+  float acc[NOUT][4][4];
+#pragma unroll
+  for (int tt = 0; tt < NOUT; ++tt)
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) acc[tt][x][y] = 0.f;
+  __syncthreads();
+
+  for (int k0 = 0; k0 < U; k0 += KC) {
+    constexpr int NQ4 = NOUT * Mdl::QF * BI * (KC / 4);
+    for (int e = t; e < NQ4; e += 256) {
+      const int q4 = e % (KC / 4);
+      int rest = e / (KC / 4);
+      const int row = rest % BI; rest /= BI;
+      const int f = rest % Mdl::QF, tt = rest / Mdl::QF;
+      const int i = i0 + row, k = k0 + q4 * 4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < M && k < U) v = ld4(a.Q + (size_t)(tt * M + i) * qstride + f * U + k);
+      sQ[tt][f][q4 * 4 + 0][row] = v.x; sQ[tt][f][q4 * 4 + 1][row] = v.y;
+      sQ[tt][f][q4 * 4 + 2][row] = v.z; sQ[tt][f][q4 * 4 + 3][row] = v.w;
+    }
+    constexpr int NE4 = Mdl::EF * BJ * (KC / 4);
+    for (int e = t; e < NE4; e += 256) {
+      const int q4 = e % (KC / 4);
+      const int rest = e / (KC / 4);
+      const int row = rest % BJ, f = rest / BJ;
+      const int j = j0 + row, k = k0 + q4 * 4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (j < K && k < U) v = ld4(a.E + sRow[row] * a.estride + (Mdl::EOFF + f) * U + k);
+      sE[f][q4 * 4 + 0][row] = v.x; sE[f][q4 * 4 + 1][row] = v.y;
+      sE[f][q4 * 4 + 2][row] = v.z; sE[f][q4 * 4 + 3][row] = v.w;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < KC; ++kk) {
+      float ev[4][Mdl::EF];
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int f = 0; f < Mdl::EF; ++f) ev[b][f] = sE[f][kk][tx + 16 * b];
+#pragma unroll
+      for (int tt = 0; tt < NOUT; ++tt)
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          float qv[Mdl::QF];
+#pragma unroll
+          for (int f = 0; f < Mdl::QF; ++f) qv[f] = sQ[tt][f][kk][ty + 16 * x];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[tt][x][b] += Mdl::acc(qv, ev[b], a.alpha);
+        }
+    }
+    __syncthreads();
+  }
+
+  // ---- epilogue
+  float inv_n[4], lrow[4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    lrow[x] = 0.f;
+    inv_n[x] = 0.f;
+    const int i = i0 + ty + 16 * x;
+    if (TRAIN && i < M) {
+      int n = 0;
+      for (int w = 0; w < a.W; ++w) n += __popc(a.mask[(size_t)i * a.W + w]);
+      inv_n[x] = n ? 1.f / (float)n : 0.f;
+    }
+  }
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int i = i0 + ty + 16 * x;
+    if (i >= M) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int j = j0 + tx + 16 * b;
+      if (j >= a.Kp) continue;
+      if (j >= K) {  // zero padding columns of C (read by the backward kernels)
+        if (TRAIN)
+#pragma unroll
+          for (int tt = 0; tt < NOUT; ++tt) a.C[(size_t)(tt * M + i) * a.Kp + j] = 0.f;
+        continue;
+      }
+      float D[NOUT];
+#pragma unroll
+      for (int tt = 0; tt < NOUT; ++tt)
+        D[tt] = Mdl::fin(acc[tt][x][b], Mdl::kBeta ? a.Cq[tt * M + i] : 0.f, Mdl::kBeta ? a.Cv[j] : 0.f);
+      int tm = 0;
+      float Dm = D[0];
+      if (NOUT == 2 && D[1] < D[0]) { tm = 1; Dm = D[1]; }   // DNF min, ties -> lowest (A11)
+      if (TRAIN) {
+        const bool bit = (a.mask[(size_t)i * a.W + (j >> 5)] >> (j & 31)) & 1u;
+        float c = 0.f;
+        if (bit) {
+          c = -sigm_(a.gamma - Dm) * inv_n[x] * a.scale;     // dl/dD_ij of Eq. 1 (A12)
+          lrow[x] += softplusf_(a.gamma - Dm) * inv_n[x];
+        }
+#pragma unroll
+        for (int tt = 0; tt < NOUT; ++tt) {
+          float coef = (tt == tm) ? c : 0.f;
+          if (Mdl::kL2) coef = (coef != 0.f && D[tt] > 0.f) ? coef / D[tt] : 0.f;
+          a.C[(size_t)(tt * M + i) * a.Kp + j] = coef;
+        }
+        if (a.Dmin) a.Dmin[(size_t)i * K + j] = Dm;
+      } else {
+        a.Dmin[(size_t)i * a.ldo + j] = Dm;
+      }
+    }
+  }
+  if (TRAIN) {
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const float s = half_warp_sum<16>(lrow[x]);
+      const int i = i0 + ty + 16 * x;
+      if (tx == 0 && i < M) a.loss_part[(size_t)blockIdx.x * M + i] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- pair_bwd_q
+template <class Mdl>
+__global__ void __launch_bounds__(256) pair_bwd_q_kernel(ScoreArgs a) {
+  constexpr int BR = 64, BK = 32, JC = 32, PAD = 4, QF = Mdl::QF, EF = Mdl::BQ_EF;
+  __shared__ __align__(16) float sC[JC][BR + PAD];
+  __shared__ __align__(16) float sE[EF][JC][BK + PAD];
+  __shared__ int64_t sRow[JC];
+  const int t = threadIdx.x, tx = t & 7, ty = t >> 3;
+  const int r0 = blockIdx.y * BR, k0 = blockIdx.x * BK;
+  const int NQ = a.NQ, K = a.K, U = a.U, qstride = QF * U;
+  float qv[2][4][QF], acc[2][4][QF], rs[2] = {0.f, 0.f};
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int r = r0 + ty + 32 * x, k = k0 + tx + 8 * b;
+#pragma unroll
+      for (int f = 0; f < QF; ++f) {
+        qv[x][b][f] = (r < NQ && k < U) ? a.Q[(size_t)r * qstride + f * U + k] : 0.f;
+        acc[x][b][f] = 0.f;
+      }
+    }
+  for (int j0 = 0; j0 < K; j0 += JC) {
+    if (t < JC) {
+      const int j = j0 + t;
+      sRow[t] = (j < K) ? (a.eidx ? a.eidx[j] : (int64_t)j) : 0;
+    }
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int e = t + 256 * s, row = e >> 3, c4 = e & 7;
+      const int r = r0 + row;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < NQ) v = ld4(a.C + (size_t)r * a.Kp + j0 + c4 * 4);   // Kp % 64 == 0, padding is 0
+      sC[c4 * 4 + 0][row] = v.x; sC[c4 * 4 + 1][row] = v.y;
+      sC[c4 * 4 + 2][row] = v.z; sC[c4 * 4 + 3][row] = v.w;
+    }
+    __syncthreads();
+    for (int e = t; e < EF * JC * (BK / 4); e += 256) {
+      const int c4 = e % (BK / 4);
+      const int rest = e / (BK / 4);
+      const int row = rest % JC, f = rest / JC;
+      const int j = j0 + row, k = k0 + c4 * 4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (j < K && k < U) v = ld4(a.E + sRow[row] * a.estride + (Mdl::BQ_EOFF + f) * U + k);
+      *reinterpret_cast<float4 *>(&sE[f][row][c4 * 4]) = v;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int jj = 0; jj < JC; ++jj) {
+      float c[2], ev[4][EF];
+#pragma unroll
+      for (int x = 0; x < 2; ++x) { c[x] = sC[jj][ty + 32 * x]; rs[x] += c[x]; }
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int f = 0; f < EF; ++f) ev[b][f] = sE[f][jj][tx + 8 * b];
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) Mdl::bq(qv[x][b], ev[b], c[x], a.alpha, acc[x][b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int r = r0 + ty + 32 * x, k = k0 + tx + 8 * b;
+      if (r >= NQ || k >= U) continue;
+#pragma unroll
+      for (int f = 0; f < QF; ++f) {
+        float v = acc[x][b][f];
+        if (Mdl::kBeta) v += rs[x] * a.QP[(size_t)r * 2 * U + f * U + k];   // sum_j C_rj * (psi(a2)-psi(a2+b2))
+        a.dQ[(size_t)r * qstride + f * U + k] += v;
+      }
+    }
+}
+
+// ---------------------------------------------------------------- pair_bwd_v
+template <class Mdl>
+__global__ void __launch_bounds__(256) pair_bwd_v_kernel(ScoreArgs a) {
+  constexpr int BJ = 64, BK = 32, RC = 32, PAD = 4, QF = Mdl::QF, EF = Mdl::BV_EF, AV = Mdl::AV;
+  __shared__ __align__(16) float sC[RC][BJ + PAD];
+  __shared__ __align__(16) float sQ[QF][RC][BK + PAD];
+  const int t = threadIdx.x, tx = t & 7, ty = t >> 3;
+  const int j0 = blockIdx.y * BJ, k0 = blockIdx.x * BK;
+  const int NQ = a.NQ, K = a.K, U = a.U, qstride = QF * U;
+  float ev[2][4][EF], acc[2][4][AV], cs[2] = {0.f, 0.f};
+#pragma unroll
+  for (int x = 0; x < 2; ++x) {
+    const int j = j0 + ty + 32 * x;
+    const int64_t er = (j < K) ? (a.eidx ? a.eidx[j] : (int64_t)j) : 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int k = k0 + tx + 8 * b;
+#pragma unroll
+      for (int f = 0; f < EF; ++f)
+        ev[x][b][f] = (j < K && k < U) ? a.E[er * a.estride + (Mdl::BV_EOFF + f) * U + k] : 0.f;
+#pragma unroll
+      for (int f = 0; f < AV; ++f) acc[x][b][f] = 0.f;
+    }
+  }
+  for (int r0 = 0; r0 < NQ; r0 += RC) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int e = t + 256 * s, row = e >> 4, c4 = e & 15;
+      const int r = r0 + row;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < NQ) v = ld4(a.C + (size_t)r * a.Kp + j0 + c4 * 4);
+      *reinterpret_cast<float4 *>(&sC[row][c4 * 4]) = v;
+    }
+    for (int e = t; e < QF * RC * (BK / 4); e += 256) {
+      const int c4 = e % (BK / 4);
+      const int rest = e / (BK / 4);
+      const int row = rest % RC, f = rest / RC;
+      const int r = r0 + row, k = k0 + c4 * 4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < NQ && k < U) v = ld4(a.Q + (size_t)r * qstride + f * U + k);
+      *reinterpret_cast<float4 *>(&sQ[f][row][c4 * 4]) = v;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int rr = 0; rr < RC; ++rr) {
+      float c[2], qv[4][QF];
+#pragma unroll
+      for (int x = 0; x < 2; ++x) { c[x] = sC[rr][ty + 32 * x]; cs[x] += c[x]; }
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int f = 0; f < QF; ++f) qv[b][f] = sQ[f][rr][tx + 8 * b];
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) Mdl::bv(qv[b], ev[x][b], c[x], a.alpha, acc[x][b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int j = j0 + ty + 32 * x, k = k0 + tx + 8 * b;
+      if (j >= K || k >= U) continue;
+      float *out = a.dV + (size_t)j * a.d;
+      if (Mdl::kBeta) {
+        // ev = [A, B, TA, TB, TAB, GA, GB]; acc = [sum C a2, sum C b2]; cs = sum C
+        const float A = ev[x][b][0], B = ev[x][b][1], S1 = acc[x][b][0], S2 = acc[x][b][1], Cj = cs[x];
+        const float S = (A + B) * Cj - S1 - S2;
+        out[k] = (ev[x][b][2] * (A * Cj - S1) - ev[x][b][4] * S) * ev[x][b][5];
+        out[U + k] = (ev[x][b][3] * (B * Cj - S2) - ev[x][b][4] * S) * ev[x][b][6];
+      } else {
+#pragma unroll
+        for (int f = 0; f < Mdl::OUTF; ++f) out[f * U + k] = acc[x][b][f];
+      }
+    }
+}
+
+// ---------------------------------------------------------------- positives
+// One CTA per query i: D+ for each disjunct, DNF min, Eq. 1 positive term and
+// its adjoint sigma(D+ - gamma)/(M G); initialises dQ (all disjuncts) and
+// writes the raw-row gradient of the answer occurrence.
+template <int KIND, int NOUT>
+__global__ void __launch_bounds__(128) pos_kernel(PosArgs p) {
+  __shared__ float red[32];
+  const int i = blockIdx.x, M = p.M, U = p.U, d = p.d;
+  constexpr int QF = (KIND == GQE || KIND == TRANSE || KIND == DISTMULT) ? 1 : 2;
+  const float *x = p.ent + p.ans_rows[i] * (int64_t)d;
+  float part[NOUT + 1];
+#pragma unroll
+  for (int tt = 0; tt <= NOUT; ++tt) part[tt] = 0.f;
+  for (int k = threadIdx.x; k < U; k += blockDim.x) {
+    float A = 0.f, B = 0.f, Pa = 0.f, Pb = 0.f;
+    if (KIND == BETAE) {
+      A = beta_act(x[k]); B = beta_act(x[U + k]);
+      const float pab = digammaf_(A + B);
+      Pa = digammaf_(A) - pab; Pb = digammaf_(B) - pab;
+      part[NOUT] += lnbetaf_(A, B);
+    }
+#pragma unroll
+    for (int tt = 0; tt < NOUT; ++tt) {
+      const float *q = p.Q + (size_t)(tt * M + i) * QF * U;
+      float v;
+      if (KIND == GQE || KIND == TRANSE) { const float z = q[k] - x[k]; v = z * z; }
+      else if (KIND == Q2B) { const float dl = fabsf(x[k] - q[k]); v = fmaxf(dl - q[U + k], 0.f) + p.alpha * fminf(dl, q[U + k]); }
+      else if (KIND == BETAE) { v = (A - q[k]) * Pa + (B - q[U + k]) * Pb; }
+      else if (KIND == ROTATE) { const float a = q[k] - x[k], b = q[U + k] - x[U + k]; v = sqrtf(a * a + b * b); }
+      else if (KIND == DISTMULT) { v = q[k] * x[k]; }
+      else { v = q[k] * x[k] + q[U + k] * x[U + k]; }
+      part[tt] += v;
+    }
+  }
+  float D[NOUT], cv = 0.f;
+  if (KIND == BETAE) cv = block_sum(part[NOUT], red);
+#pragma unroll
+  for (int tt = 0; tt < NOUT; ++tt) {
+    const float s = block_sum(part[tt], red);
+    if (KIND == GQE || KIND == TRANSE) D[tt] = sqrtf(s);
+    else if (KIND == BETAE) D[tt] = s + p.Cq[tt * M + i] - cv;
+    else if (KIND == DISTMULT || KIND == COMPLEX) D[tt] = -s;
+    else D[tt] = s;
+  }
+  int tm = 0;
+  float Dm = D[0];
+  if (NOUT == 2 && D[1] < D[0]) { tm = 1; Dm = D[1]; }
+  const float c = sigm_(Dm - p.gamma) * p.scale;                  // dl/dD+ (Eq. 1)
+  if (threadIdx.x == 0) {
+    p.loss_pos[i] = softplusf_(Dm - p.gamma);
+    if (p.Dpos) p.Dpos[i] = Dm;
+  }
+  const float *q = p.Q + (size_t)(tm * M + i) * QF * U;
+  float *og = p.dV + (size_t)i * d;
+  const float invD = (Dm > 0.f) ? 1.f / Dm : 0.f;
+  for (int k = threadIdx.x; k < U; k += blockDim.x) {
+    float gq[2] = {0.f, 0.f}, gv[2] = {0.f, 0.f};
+    if (KIND == GQE || KIND == TRANSE) {
+      const float z = (q[k] - x[k]) * invD * c; gq[0] = z; gv[0] = -z;
+    } else if (KIND == Q2B) {
+      const float dl = x[k] - q[k], a = fabsf(dl), o = q[U + k];
+      const float s = (dl > 0.f) ? 1.f : ((dl < 0.f) ? -1.f : 0.f);
+      const float outb = a > o ? 1.f : 0.f, inb = a < o ? 1.f : 0.f;
+      gq[0] = -c * s * (outb + p.alpha * inb);
+      gq[1] = c * (-outb + p.alpha * (a >= o ? 1.f : 0.f));
+      gv[0] = c * s * (outb + p.alpha * inb);
+    } else if (KIND == BETAE) {
+      const float A = beta_act(x[k]), B = beta_act(x[U + k]);
+      const float pab = digammaf_(A + B), Pa = digammaf_(A) - pab, Pb = digammaf_(B) - pab;
+      const float a2 = q[k], b2 = q[U + k];
+      gq[0] = c * (-Pa + p.QP[(size_t)(tm * M + i) * 2 * U + k]);
+      gq[1] = c * (-Pb + p.QP[(size_t)(tm * M + i) * 2 * U + U + k]);
+      const float tab = trigammaf_(A + B), S = A + B - a2 - b2;
+      gv[0] = c * ((A - a2) * trigammaf_(A) - S * tab) * beta_act_grad(x[k]);
+      gv[1] = c * ((B - b2) * trigammaf_(B) - S * tab) * beta_act_grad(x[U + k]);
+    } else if (KIND == ROTATE) {
+      const float a = q[k] - x[k], b = q[U + k] - x[U + k], n = sqrtf(a * a + b * b);
+      if (n > 0.f) { gq[0] = c * a / n; gq[1] = c * b / n; gv[0] = -gq[0]; gv[1] = -gq[1]; }
+    } else if (KIND == DISTMULT) {
+      gq[0] = -c * x[k]; gv[0] = -c * q[k];
+    } else {
+      gq[0] = -c * x[k]; gq[1] = -c * x[U + k]; gv[0] = -c * q[k]; gv[1] = -c * q[U + k];
+    }
+#pragma unroll
+    for (int tt = 0; tt < NOUT; ++tt) {
+      float *dq = p.dQ + (size_t)(tt * M + i) * QF * U;
+#pragma unroll
+      for (int f = 0; f < QF; ++f) dq[f * U + k] = (tt == tm) ? gq[f] : 0.f;
+    }
+    og[k] = gv[0];
+    if (QF == 2 && KIND != Q2B) og[U + k] = gv[1];
+  }
+}
+
+// ---------------------------------------------------------------- BetaE precompute
+// Entity features of the pool (9 planes of m, layout above) and Cv_j = sum_k lnB(A, B).
+__global__ void __launch_bounds__(128) beta_entity_kernel(const float *ent, const int64_t *rows, int K, int m,
+                                                          float *F, float *Cv) {
+  __shared__ float red[32];
+  const int j = blockIdx.x;
+  const float *x = ent + rows[j] * (int64_t)(2 * m);
+  float *f = F + (size_t)j * 9 * m;
+  float s = 0.f;
+  for (int k = threadIdx.x; k < m; k += blockDim.x) {
+    const float xa = x[k], xb = x[m + k];
+    const float A = beta_act(xa), B = beta_act(xb);
+    const float pab = digammaf_(A + B);
+    f[k] = digammaf_(A) - pab;
+    f[m + k] = digammaf_(B) - pab;
+    f[2 * m + k] = A;
+    f[3 * m + k] = B;
+    f[4 * m + k] = trigammaf_(A);
+    f[5 * m + k] = trigammaf_(B);
+    f[6 * m + k] = trigammaf_(A + B);
+    f[7 * m + k] = beta_act_grad(xa);
+    f[8 * m + k] = beta_act_grad(xb);
+    s += lnbetaf_(A, B);
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) Cv[j] = s;
+}
+
+// Query features: QP[r] = [psi(a2) - psi(a2+b2) | psi(b2) - psi(a2+b2)], Cq[r] = sum_k lnB(a2, b2).
+__global__ void __launch_bounds__(128) beta_query_kernel(const float *Q, int NQ, int m, float *QP, float *Cq) {
+  __shared__ float red[32];
+  const int r = blockIdx.x;
+  const float *q = Q + (size_t)r * 2 * m;
+  float s = 0.f;
+  for (int k = threadIdx.x; k < m; k += blockDim.x) {
+    const float a2 = q[k], b2 = q[m + k], pab = digammaf_(a2 + b2);
+    QP[(size_t)r * 2 * m + k] = digammaf_(a2) - pab;
+    QP[(size_t)r * 2 * m + m + k] = digammaf_(b2) - pab;
+    s += lnbetaf_(a2, b2);
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) Cq[r] = s;
+}
+
+// ---------------------------------------------------------------- loss
+// Deterministic sum of the per-query terms; finite check; Adam step counter and
+// bias corrections on device (so a step needs no host round trip).
+__global__ void __launch_bounds__(256) loss_finalize_kernel(const float *loss_pos, const float *loss_part, int M,
+                                                            int njt, double scale, double *loss_out,
+                                                            int *flags, int64_t *t_dev, float *bc,
+                                                            float beta1, float beta2, int apply) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < M; i += 256) {
+    double v = loss_pos[i];
+    for (int jt = 0; jt < njt; ++jt) v += loss_part[(size_t)jt * M + i];
+    s += v;
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double loss = red[0] * scale;
+    // flags[1]: an input id / relation was out of range (device-side validation);
+    // flags[0]: skip every update of this step (non-finite loss or bad input).
+    const int bad = !isfinite(loss) || flags[1];
+    *loss_out = loss;
+    flags[0] = bad;
+    if (!bad && apply) {
+      const int64_t t = *t_dev + 1;
+      *t_dev = t;
+      bc[0] = (float)(1.0 - pow((double)beta1, (double)t));
+      bc[1] = (float)(1.0 - pow((double)beta2, (double)t));
+    }
+  }
+}
+
+// ---------------------------------------------------------------- launchers
+template <class Mdl>
+static void launch_pair(const ScoreArgs &a, int nout, bool train, cudaStream_t st) {
+  dim3 gf((a.K + 63) / 64, (a.M + 63) / 64);
+  if (nout == 1) {
+    if (train) pair_fwd_kernel<Mdl, 1, true><<<gf, 256, 0, st>>>(a);
+    else pair_fwd_kernel<Mdl, 1, false><<<gf, 256, 0, st>>>(a);
+  } else {
+    if (train) pair_fwd_kernel<Mdl, 2, true><<<gf, 256, 0, st>>>(a);
+    else pair_fwd_kernel<Mdl, 2, false><<<gf, 256, 0, st>>>(a);
+  }
+}
+
+void launch_pair_fwd(int kind, const ScoreArgs &a, int nout, bool train, cudaStream_t st) {
+  switch (kind) {
+    case GQE: case TRANSE: launch_pair<ML2>(a, nout, train, st); break;
+    case Q2B: launch_pair<MBox>(a, nout, train, st); break;
+    case BETAE: launch_pair<MBeta>(a, nout, train, st); break;
+    case ROTATE: launch_pair<MRot>(a, nout, train, st); break;
+    case DISTMULT: launch_pair<MDot>(a, nout, train, st); break;
+    case COMPLEX: launch_pair<MCpx>(a, nout, train, st); break;
+  }
+}
+
+template <class Mdl>
+static void launch_bwd(const ScoreArgs &a, cudaStream_t st) {
+  dim3 gq((a.U + 31) / 32, (a.NQ + 63) / 64);
+  pair_bwd_q_kernel<Mdl><<<gq, 256, 0, st>>>(a);
+  dim3 gv((a.U + 31) / 32, (a.K + 63) / 64);
+  pair_bwd_v_kernel<Mdl><<<gv, 256, 0, st>>>(a);
+}
+
+void launch_pair_bwd(int kind, const ScoreArgs &a, cudaStream_t st) {
+  switch (kind) {
+    case GQE: case TRANSE: launch_bwd<ML2>(a, st); break;
+    case Q2B: launch_bwd<MBox>(a, st); break;
+    case BETAE: launch_bwd<MBeta>(a, st); break;
+    case ROTATE: launch_bwd<MRot>(a, st); break;
+    case DISTMULT: launch_bwd<MDot>(a, st); break;
+    case COMPLEX: launch_bwd<MCpx>(a, st); break;
+  }
+}
+
+template <int KIND>
+static void launch_pos_k(const PosArgs &p, int nout, cudaStream_t st) {
+  if (nout == 1) pos_kernel<KIND, 1><<<p.M, 128, 0, st>>>(p);
+  else pos_kernel<KIND, 2><<<p.M, 128, 0, st>>>(p);
+}
+
+void launch_pos(int kind, const PosArgs &p, int nout, cudaStream_t st) {
+  switch (kind) {
+    case GQE: launch_pos_k<GQE>(p, nout, st); break;
+    case TRANSE: launch_pos_k<TRANSE>(p, nout, st); break;
+    case Q2B: launch_pos_k<Q2B>(p, nout, st); break;
+    case BETAE: launch_pos_k<BETAE>(p, nout, st); break;
+    case ROTATE: launch_pos_k<ROTATE>(p, nout, st); break;
+    case DISTMULT: launch_pos_k<DISTMULT>(p, nout, st); break;
+    case COMPLEX: launch_pos_k<COMPLEX>(p, nout, st); break;
+  }
+}
+
+void launch_beta_entity(const float *ent, const int64_t *rows, int K, int m, float *F, float *Cv, cudaStream_t st) {
+  if (K > 0) beta_entity_kernel<<<K, 128, 0, st>>>(ent, rows, K, m, F, Cv);
+}
+void launch_beta_query(const float *Q, int NQ, int m, float *QP, float *Cq, cudaStream_t st) {
+  beta_query_kernel<<<NQ, 128, 0, st>>>(Q, NQ, m, QP, Cq);
+}
+void launch_loss_finalize(const float *loss_pos, const float *loss_part, int M, int njt, double scale,
+                          double *loss_out, int *flags, int64_t *t_dev, float *bc, float beta1, float beta2,
+                          int apply, cudaStream_t st) {
+  loss_finalize_kernel<<<1, 256, 0, st>>>(loss_pos, loss_part, M, njt, scale, loss_out, flags, t_dev, bc,
+                                          beta1, beta2, apply);
+}
+
+}  // namespace kg

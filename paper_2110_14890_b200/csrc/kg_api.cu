@@ -1,0 +1,979 @@
+// kg_api.cu -- host implementation of the C-ABI in include/kg.h.
+//
+// Owns the handle: validation, the static per-structure DAG plans (SURVEY
+// App. A.3), the device workspace, pinned staging, cuBLAS, and the order in
+// which the sm_100a kernels of k_*.cu are enqueued for one training step
+// (§4.1, §4.2, §4.3).
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/kg.h"
+#include "kg_launch.h"
+
+using namespace kg;
+
+namespace {
+
+// ------------------------------------------------------------------ plans
+struct PNode {
+  int type;       // 0 projection, 1 intersection
+  int in;         // projection input node (-1: anchor slot)
+  int anchor;     // anchor slot (when in == -1)
+  int rel;        // relation slot (execution order, A21)
+  int ins[3];
+  int nin;
+};
+struct Plan {
+  int na, nr, nn, nout, nproj;
+  PNode n[6];
+  int outs[2];
+  int inter;      // index of the intersection node or -1
+};
+
+PNode P(int in, int anchor, int rel) { return PNode{0, in, anchor, rel, {0, 0, 0}, 0}; }
+PNode I2(int a, int b) { return PNode{1, -1, -1, -1, {a, b, 0}, 2}; }
+PNode I3(int a, int b, int c) { return PNode{1, -1, -1, -1, {a, b, c}, 3}; }
+
+Plan make_plan(int s) {
+  Plan p{};
+  p.inter = -1;
+  auto set = [&](std::initializer_list<PNode> nodes, std::initializer_list<int> outs, int na, int nr) {
+    p.nn = 0;
+    for (auto &x : nodes) p.n[p.nn++] = x;
+    p.nout = 0;
+    for (int o : outs) p.outs[p.nout++] = o;
+    p.na = na;
+    p.nr = nr;
+  };
+  switch (s) {
+    case KG_1P: set({P(-1, 0, 0)}, {0}, 1, 1); break;
+    case KG_2P: set({P(-1, 0, 0), P(0, -1, 1)}, {1}, 1, 2); break;
+    case KG_3P: set({P(-1, 0, 0), P(0, -1, 1), P(1, -1, 2)}, {2}, 1, 3); break;
+    case KG_2I: set({P(-1, 0, 0), P(-1, 1, 1), I2(0, 1)}, {2}, 2, 2); break;
+    case KG_3I: set({P(-1, 0, 0), P(-1, 1, 1), P(-1, 2, 2), I3(0, 1, 2)}, {3}, 3, 3); break;
+    case KG_IP: set({P(-1, 0, 0), P(-1, 1, 1), I2(0, 1), P(2, -1, 2)}, {3}, 2, 3); break;
+    case KG_PI: set({P(-1, 0, 0), P(0, -1, 1), P(-1, 1, 2), I2(1, 2)}, {3}, 2, 3); break;
+    case KG_2U: set({P(-1, 0, 0), P(-1, 1, 1)}, {0, 1}, 2, 2); break;
+    case KG_UP: set({P(-1, 0, 0), P(0, -1, 2), P(-1, 1, 1), P(2, -1, 2)}, {1, 3}, 2, 3); break;
+  }
+  p.nproj = 0;
+  for (int i = 0; i < p.nn; ++i) {
+    if (p.n[i].type == 0) p.nproj++;
+    else p.inter = i;
+  }
+  return p;
+}
+
+int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct Seg {
+  std::string name;
+  int64_t off, n;
+  int rows, cols;
+  float lo, hi;
+};
+
+struct Arena {
+  char *base = nullptr;
+  size_t off = 0;
+  template <class T>
+  T *take(int64_t n) {
+    off = (size_t)align_up((int64_t)off, 256);
+    T *p = base ? reinterpret_cast<T *>(base + off) : nullptr;
+    off += (size_t)std::max<int64_t>(n, 1) * sizeof(T);
+    return p;
+  }
+};
+
+}  // namespace
+
+struct kg_handle {
+  kg_config cfg{};
+  std::string err;
+  bool broken = false, bound = false;
+  int kind = 0, d = 0, m = 0, H = 0, R = 0, world = 1, rank = 0;
+  int64_t n_ent = 0, shard = 0;
+  int dq = 0, dr = 0, ent_bits = 1, rel_bits = 1;
+  std::vector<Seg> segs;
+  int64_t dense_size = 0, w_off = 0;
+  kg_tables t{};
+  cudaStream_t st = nullptr;
+  cublasHandle_t blas = nullptr;
+  int device = 0;
+
+  // workspace
+  char *ws = nullptr;
+  size_t ws_bytes = 0;
+  int Mx = 0, Kx = 0, Cx = 0, Lx = 0, Lrx = 0, Kpx = 0;
+  int64_t *b_anchors = nullptr, *b_answers = nullptr, *b_negs = nullptr;
+  int32_t *b_rels = nullptr;
+  uint32_t *b_mask = nullptr;
+  int64_t *ids = nullptr, *rows = nullptr, *uniq = nullptr;
+  int32_t *inv = nullptr, *perm = nullptr, *seg = nullptr, *Udev = nullptr, *bad = nullptr;
+  int32_t *rocc = nullptr, *rinv = nullptr, *rperm = nullptr, *rseg = nullptr, *rU = nullptr;
+  int64_t *runiq = nullptr;
+  int32_t *rel_seg_map = nullptr;
+  int64_t *rel_stamp = nullptr;
+  float *OG = nullptr, *RG = nullptr, *RGU = nullptr, *Gc = nullptr, *gdense = nullptr;
+  float *Q = nullptr, *dQ = nullptr, *C = nullptr, *Dmin = nullptr, *Dpos = nullptr, *loss_part = nullptr,
+        *loss_pos = nullptr;
+  float *F = nullptr, *Cv = nullptr, *QP = nullptr, *Cq = nullptr;
+  double *loss_dev = nullptr;
+  int *flags = nullptr;
+  int64_t *t_dev = nullptr;
+  float *bc = nullptr;
+  float *nval[6] = {}, *ngrad[6] = {};
+  float *stack_v = nullptr, *stack_g = nullptr;
+  float *T[12] = {};
+  int8_t *amin = nullptr;
+  float *pX = nullptr, *pH1 = nullptr, *pH2 = nullptr, *pZp1 = nullptr, *pdZ = nullptr, *pdH2 = nullptr,
+        *pdH1 = nullptr, *pZ = nullptr, *pdX = nullptr;
+  float *Dscore = nullptr;
+
+  // pinned staging (double-buffered) + host mirrors of the step results
+  char *pin[2] = {nullptr, nullptr};
+  size_t pin_bytes = 0;
+  cudaEvent_t pin_ev[2] = {nullptr, nullptr};
+  int pin_cur = 0;
+  struct HostOut {
+    double loss;
+    int flags[2];
+    int32_t U;
+    int64_t t;
+  } *hout = nullptr;
+  cudaEvent_t step_done = nullptr;
+
+  int64_t stamp = 0;
+  int apply = 1, keep_grads = 0;
+  int last_M = 0, last_K = 0, last_U_valid = 0;
+  bool step_pending = false;
+};
+
+namespace {
+
+kg_status fail(kg_handle *h, kg_status s, const std::string &msg) {
+  if (h) {
+    h->err = msg;
+    if (s == KG_ECUDA || s == KG_ENCCL) h->broken = true;
+  }
+  return s;
+}
+
+#define CK(call)                                                                               \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess)                                                                     \
+      return fail(h, KG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));            \
+  } while (0)
+#define CKB(call)                                                                              \
+  do {                                                                                         \
+    cublasStatus_t e_ = (call);                                                                \
+    if (e_ != CUBLAS_STATUS_SUCCESS)                                                           \
+      return fail(h, KG_ECUDA, std::string(#call) + ": cublas status " + std::to_string(e_));  \
+  } while (0)
+
+bool single_hop(int k) { return k == KG_TRANSE || k == KG_ROTATE || k == KG_DISTMULT || k == KG_COMPLEX; }
+int bits_for(int64_t n) {
+  int b = 1;
+  while (b < 31 && ((int64_t)1 << b) < n) ++b;
+  return b;
+}
+
+// theta_D layout -- identical to kggen.dense_layout.
+void build_layout(kg_handle *h) {
+  const int d = h->d, R = h->R, H = h->H, m = h->m;
+  const double rho = ((double)h->cfg.gamma + 2.0) / (double)d;
+  const double w = 1.0 / std::sqrt((double)d);
+  auto add = [&](const char *name, int rows, int cols, double lo, double hi) {
+    Seg s{name, 0, (int64_t)rows * cols, rows, cols, (float)lo, (float)hi};
+    h->segs.push_back(s);
+  };
+  const int k = h->kind;
+  if (k == KG_GQE || k == KG_TRANSE || k == KG_DISTMULT || k == KG_COMPLEX) add("rel", R, d, -rho, rho);
+  else if (k == KG_Q2B) { add("rel_center", R, d, -rho, rho); add("rel_offset", R, d, 0.0, rho); }
+  else if (k == KG_BETAE) add("rel", R, d, -rho, rho);
+  else if (k == KG_ROTATE) add("rel_phase", R, m, -M_PI, M_PI);
+  const size_t nrel = h->segs.size();
+  if (k == KG_GQE) {
+    add("ds_W1", d, d, -w, w); add("ds_b1", 1, d, -w, w); add("ds_W2", d, d, -w, w); add("ds_b2", 1, d, -w, w);
+  } else if (k == KG_Q2B) {
+    add("att_W1", d, d, -w, w); add("att_b1", 1, d, -w, w); add("att_W2", d, d, -w, w); add("att_b2", 1, d, -w, w);
+    add("off_W1", d, d, -w, w); add("off_b1", 1, d, -w, w); add("off_W2", d, d, -w, w); add("off_b2", 1, d, -w, w);
+  } else if (k == KG_BETAE) {
+    const double w1 = 1.0 / std::sqrt(2.0 * d), wh = 1.0 / std::sqrt((double)H);
+    add("prj_W1", H, 2 * d, -w1, w1); add("prj_b1", 1, H, -w1, w1);
+    add("prj_W2", H, H, -wh, wh); add("prj_b2", 1, H, -wh, wh);
+    add("prj_W0", d, H, -wh, wh); add("prj_b0", 1, d, -wh, wh);
+    add("att_U1", d, d, -w, w); add("att_c1", 1, d, -w, w); add("att_U2", m, d, -w, w); add("att_c2", 1, m, -w, w);
+  }
+  int64_t off = 0;
+  for (size_t i = 0; i < h->segs.size(); ++i) {
+    h->segs[i].off = off;
+    off += h->segs[i].n;
+    if (i + 1 == nrel) h->w_off = off;
+  }
+  h->dense_size = off;
+}
+
+const Seg *seg_of(const kg_handle *h, const char *name) {
+  for (auto &s : h->segs)
+    if (s.name == name) return &s;
+  return nullptr;
+}
+float *dp(kg_handle *h, const char *name) { return h->t.dense + seg_of(h, name)->off; }
+float *gp(kg_handle *h, const char *name) { return h->gdense + (seg_of(h, name)->off - h->w_off); }
+
+void carve(kg_handle *h, Arena &A) {
+  const int Mx = h->Mx, Kx = h->Kx, d = h->d, dq = h->dq, H = h->H;
+  const int NQ = 2 * Mx;
+  h->b_anchors = A.take<int64_t>(3 * Mx);
+  h->b_rels = A.take<int32_t>(3 * Mx);
+  h->b_answers = A.take<int64_t>(Mx);
+  h->b_negs = A.take<int64_t>(std::max(Kx, h->Cx));
+  h->b_mask = A.take<uint32_t>((int64_t)Mx * ((Kx + 31) / 32));
+  h->ids = A.take<int64_t>(h->Lx);
+  h->rows = A.take<int64_t>(h->Lx);
+  h->uniq = A.take<int64_t>(h->Lx);
+  h->inv = A.take<int32_t>(h->Lx);
+  h->perm = A.take<int32_t>(h->Lx);
+  h->seg = A.take<int32_t>(h->Lx + 1);
+  h->Udev = A.take<int32_t>(1);
+  h->bad = A.take<int32_t>(1);
+  h->rocc = A.take<int32_t>(h->Lrx);
+  h->runiq = A.take<int64_t>(h->Lrx);
+  h->rinv = A.take<int32_t>(h->Lrx);
+  h->rperm = A.take<int32_t>(h->Lrx);
+  h->rseg = A.take<int32_t>(h->Lrx + 1);
+  h->rU = A.take<int32_t>(1);
+  h->rel_seg_map = A.take<int32_t>(h->R);
+  h->rel_stamp = A.take<int64_t>(h->R);
+  h->RG = A.take<float>((int64_t)h->Lrx * h->dr);
+  h->RGU = A.take<float>((int64_t)h->Lrx * h->dr);
+  h->OG = A.take<float>((int64_t)h->Lx * d);
+  h->Gc = A.take<float>((int64_t)h->Lx * d);
+  h->gdense = A.take<float>(h->dense_size - h->w_off);
+  h->Q = A.take<float>((int64_t)NQ * dq);
+  h->dQ = A.take<float>((int64_t)NQ * dq);
+  h->C = A.take<float>((int64_t)NQ * h->Kpx);
+  h->Dmin = A.take<float>((int64_t)Mx * Kx);
+  h->Dpos = A.take<float>(Mx);
+  h->loss_part = A.take<float>((int64_t)((Kx + 63) / 64) * Mx);
+  h->loss_pos = A.take<float>(Mx);
+  if (h->kind == KG_BETAE) {
+    h->F = A.take<float>((int64_t)std::max(Kx, h->Cx) * 9 * h->m);
+    h->Cv = A.take<float>(std::max(Kx, h->Cx));
+    h->QP = A.take<float>((int64_t)NQ * d);
+    h->Cq = A.take<float>(NQ);
+  }
+  h->loss_dev = A.take<double>(1);
+  h->flags = A.take<int>(2);
+  h->t_dev = A.take<int64_t>(1);
+  h->bc = A.take<float>(2);
+  for (int i = 0; i < 6; ++i) {
+    h->nval[i] = A.take<float>((int64_t)Mx * dq);
+    h->ngrad[i] = A.take<float>((int64_t)Mx * dq);
+  }
+  if (!single_hop(h->kind)) {
+    h->stack_v = A.take<float>((int64_t)3 * Mx * dq);
+    h->stack_g = A.take<float>((int64_t)3 * Mx * dq);
+    for (int i = 0; i < 12; ++i) h->T[i] = A.take<float>((int64_t)3 * Mx * d);
+    h->amin = A.take<int8_t>((int64_t)Mx * d);
+  }
+  if (h->kind == KG_BETAE) {
+    const int64_t P = 4 * (int64_t)Mx;
+    h->pX = A.take<float>(P * 2 * d);
+    h->pH1 = A.take<float>(P * H);
+    h->pH2 = A.take<float>(P * H);
+    h->pZp1 = A.take<float>(P * d);
+    h->pdZ = A.take<float>(P * d);
+    h->pdH2 = A.take<float>(P * H);
+    h->pdH1 = A.take<float>(P * H);
+    h->pZ = A.take<float>((int64_t)Mx * d);
+    h->pdX = A.take<float>((int64_t)Mx * 2 * d);
+  }
+  h->Dscore = A.take<float>((int64_t)Mx * std::max(h->Cx, 1));
+}
+
+// Row-major GEMM: C[m x n] = op(A) op(B) + beta C, op(A) is [m x k].
+kg_status gemm(kg_handle *h, bool ta, bool tb, int m, int n, int k, const float *A, int lda, const float *B, int ldb,
+               float beta, float *C, int ldc) {
+  if (m <= 0 || n <= 0) return KG_OK;
+  const float one = 1.f;
+  CKB(cublasSgemm(h->blas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, n, m, k, &one, B, ldb, A,
+                  lda, &beta, C, ldc));
+  return KG_OK;
+}
+#define G(...)                                   \
+  do {                                           \
+    kg_status s_ = gemm(h, __VA_ARGS__);         \
+    if (s_ != KG_OK) return s_;                  \
+  } while (0)
+
+struct StepBufs {
+  Plan plan;
+  int M, K, Kp, NQ;
+  float *val[6], *grad[6];
+};
+
+// -------------------------------------------------------------- forward DAG
+kg_status dag_forward(kg_handle *h, StepBufs &S) {
+  const Plan &p = S.plan;
+  const int M = S.M, d = h->d, dq = h->dq, m = h->m, HH = h->H;
+  cudaStream_t st = h->st;
+  const float *ent = h->t.ent;
+  int u = 0;
+  for (int ni = 0; ni < p.nn; ++ni) {
+    const PNode &nd = p.n[ni];
+    if (nd.type == 0) {
+      const int64_t *arows = nd.in < 0 ? h->rows + (int64_t)nd.anchor * M : nullptr;
+      const float *in = nd.in < 0 ? nullptr : S.val[nd.in];
+      const int32_t *rel = h->rocc + (int64_t)u * M;
+      if (h->kind == KG_BETAE) {
+        float *X = h->pX + (int64_t)u * M * 2 * d, *H1 = h->pH1 + (int64_t)u * M * HH, *H2 = h->pH2 + (int64_t)u * M * HH;
+        launch_betae_proj_in(M, d, in, arows, ent, rel, 1, dp(h, "rel"), X, st);
+        G(false, true, M, HH, 2 * d, X, 2 * d, dp(h, "prj_W1"), 2 * d, 0.f, H1, HH);
+        launch_bias_act(H1, dp(h, "prj_b1"), M, HH, 1, st);
+        G(false, true, M, HH, HH, H1, HH, dp(h, "prj_W2"), HH, 0.f, H2, HH);
+        launch_bias_act(H2, dp(h, "prj_b2"), M, HH, 1, st);
+        G(false, true, M, d, HH, H2, HH, dp(h, "prj_W0"), HH, 0.f, h->pZ, d);
+        launch_betae_proj_out(h->pZ, dp(h, "prj_b0"), M, d, h->pZp1 + (int64_t)u * M * d, S.val[ni], st);
+      } else {
+        const float *relA = nullptr, *relB = nullptr;
+        if (h->kind == KG_Q2B) { relA = dp(h, "rel_center"); relB = dp(h, "rel_offset"); }
+        else if (h->kind == KG_ROTATE) relA = dp(h, "rel_phase");
+        else relA = dp(h, "rel");
+        launch_proj_fwd(h->kind, M, d, in, dq, arows, ent, rel, 1, relA, relB, S.val[ni], st);
+      }
+      ++u;
+    } else {
+      const int n = nd.nin, NR = n * M;
+      float *out = S.val[ni];
+      float **T = h->T;
+      if (h->kind == KG_GQE) {
+        G(false, true, NR, d, d, h->stack_v, d, dp(h, "ds_W1"), d, 0.f, T[0], d);   // H
+        launch_bias_act(T[0], dp(h, "ds_b1"), NR, d, 1, st);
+        launch_mean_stack(T[0], n, M, d, T[1], st);                                  // Mn
+        G(false, true, M, d, d, T[1], d, dp(h, "ds_W2"), d, 0.f, out, d);
+        launch_bias_act(out, dp(h, "ds_b2"), M, d, 0, st);
+      } else if (h->kind == KG_Q2B) {
+        G(false, true, NR, d, d, h->stack_v, 2 * d, dp(h, "att_W1"), d, 0.f, T[0], d);  // Hc
+        launch_bias_act(T[0], dp(h, "att_b1"), NR, d, 1, st);
+        G(false, true, NR, d, d, T[0], d, dp(h, "att_W2"), d, 0.f, T[1], d);           // Lg
+        launch_bias_act(T[1], dp(h, "att_b2"), NR, d, 0, st);
+        launch_q2b_att_fwd(h->stack_v, T[1], n, M, d, T[2], out, st);                  // a, center
+        G(false, true, NR, d, d, h->stack_v + d, 2 * d, dp(h, "off_W1"), d, 0.f, T[3], d);  // Ho
+        launch_bias_act(T[3], dp(h, "off_b1"), NR, d, 1, st);
+        launch_mean_stack(T[3], n, M, d, T[4], st);                                    // Mo
+        G(false, true, M, d, d, T[4], d, dp(h, "off_W2"), d, 0.f, T[5], d);            // Z
+        launch_bias_act(T[5], dp(h, "off_b2"), M, d, 0, st);
+        launch_q2b_off_fwd(h->stack_v, T[5], n, M, d, T[6], h->amin, out, st);         // sig, amin, offset
+      } else if (h->kind == KG_BETAE) {
+        G(false, true, NR, d, d, h->stack_v, d, dp(h, "att_U1"), d, 0.f, T[0], d);     // Hs
+        launch_bias_act(T[0], dp(h, "att_c1"), NR, d, 1, st);
+        G(false, true, NR, m, d, T[0], d, dp(h, "att_U2"), d, 0.f, T[1], m);           // Lg
+        launch_bias_act(T[1], dp(h, "att_c2"), NR, m, 0, st);
+        launch_beta_att_fwd(h->stack_v, T[1], n, M, d, T[2], out, st);                 // w, out
+      }
+    }
+  }
+  return KG_OK;
+}
+
+// -------------------------------------------------------------- backward DAG
+kg_status dag_backward(kg_handle *h, StepBufs &S) {
+  const Plan &p = S.plan;
+  const int M = S.M, d = h->d, dq = h->dq, m = h->m, HH = h->H;
+  cudaStream_t st = h->st;
+  const float *ent = h->t.ent;
+  // projection-use index of each node
+  int use[6], u = 0;
+  for (int ni = 0; ni < p.nn; ++ni) use[ni] = p.n[ni].type == 0 ? u++ : -1;
+  for (int ni = p.nn - 1; ni >= 0; --ni) {
+    const PNode &nd = p.n[ni];
+    if (nd.type == 0) {
+      const int uu = use[ni];
+      const int64_t *arows = nd.in < 0 ? h->rows + (int64_t)nd.anchor * M : nullptr;
+      const float *in = nd.in < 0 ? nullptr : S.val[nd.in];
+      float *din = nd.in < 0 ? h->OG + (int64_t)nd.anchor * M * d : S.grad[nd.in];
+      const int64_t din_ld = nd.in < 0 ? d : dq;
+      const int32_t *rel = h->rocc + (int64_t)uu * M;
+      float *drel = h->RG + (int64_t)uu * M * h->dr;
+      if (h->kind == KG_BETAE) {
+        float *dZ = h->pdZ + (int64_t)uu * M * d, *dH2 = h->pdH2 + (int64_t)uu * M * HH,
+              *dH1 = h->pdH1 + (int64_t)uu * M * HH;
+        launch_betae_proj_dz(S.grad[ni], h->pZp1 + (int64_t)uu * M * d, M, d, dZ, st);
+        G(false, false, M, HH, d, dZ, d, dp(h, "prj_W0"), HH, 0.f, dH2, HH);
+        launch_relu_mask(dH2, h->pH2 + (int64_t)uu * M * HH, M, HH, st);
+        G(false, false, M, HH, HH, dH2, HH, dp(h, "prj_W2"), HH, 0.f, dH1, HH);
+        launch_relu_mask(dH1, h->pH1 + (int64_t)uu * M * HH, M, HH, st);
+        G(false, false, M, 2 * d, HH, dH1, HH, dp(h, "prj_W1"), 2 * d, 0.f, h->pdX, 2 * d);
+        launch_betae_split(h->pdX, M, d, arows, ent, din, din_ld, drel, st);
+      } else {
+        const float *relA = nullptr, *relB = nullptr;
+        if (h->kind == KG_Q2B) { relA = dp(h, "rel_center"); relB = dp(h, "rel_offset"); }
+        else if (h->kind == KG_ROTATE) relA = dp(h, "rel_phase");
+        else relA = dp(h, "rel");
+        launch_proj_bwd(h->kind, M, d, S.grad[ni], in, dq, arows, ent, rel, 1, relA, relB, S.val[ni], din, din_ld,
+                        drel, st);
+      }
+    } else {
+      const int n = nd.nin, NR = n * M;
+      const float *gout = S.grad[ni];
+      float **T = h->T;
+      if (h->kind == KG_GQE) {
+        // T0 = H, T1 = Mn (forward);  T7 = dMn, T8 = dH
+        G(false, false, M, d, d, gout, d, dp(h, "ds_W2"), d, 0.f, T[7], d);
+        G(true, false, d, d, M, gout, d, T[1], d, 0.f, gp(h, "ds_W2"), d);
+        launch_colsum(gout, M, d, d, gp(h, "ds_b2"), st);
+        launch_gqe_inter_dh(T[7], T[0], n, M, d, T[8], st);
+        G(true, false, d, d, NR, T[8], d, h->stack_v, d, 0.f, gp(h, "ds_W1"), d);
+        launch_colsum(T[8], NR, d, d, gp(h, "ds_b1"), st);
+        G(false, false, NR, d, d, T[8], d, dp(h, "ds_W1"), d, 0.f, h->stack_g, d);
+      } else if (h->kind == KG_Q2B) {
+        // forward: T0 Hc, T1 Lg, T2 a, T3 Ho, T4 Mo, T5 Z, T6 sig.  backward: T7 dLg, T8 dHc, T9 dZ, T10 dMo, T11 dHo
+        launch_q2b_att_bwd(h->stack_v, T[2], gout, n, M, d, T[7], h->stack_g, st);
+        launch_q2b_off_bwd(h->stack_v, T[6], h->amin, gout, n, M, d, T[9], h->stack_g, st);
+        G(false, false, NR, d, d, T[7], d, dp(h, "att_W2"), d, 0.f, T[8], d);
+        launch_relu_mask(T[8], T[0], NR, d, st);
+        G(true, false, d, d, NR, T[7], d, T[0], d, 0.f, gp(h, "att_W2"), d);
+        launch_colsum(T[7], NR, d, d, gp(h, "att_b2"), st);
+        G(true, false, d, d, NR, T[8], d, h->stack_v, 2 * d, 0.f, gp(h, "att_W1"), d);
+        launch_colsum(T[8], NR, d, d, gp(h, "att_b1"), st);
+        G(false, false, NR, d, d, T[8], d, dp(h, "att_W1"), d, 1.f, h->stack_g, 2 * d);
+        G(false, false, M, d, d, T[9], d, dp(h, "off_W2"), d, 0.f, T[10], d);
+        G(true, false, d, d, M, T[9], d, T[4], d, 0.f, gp(h, "off_W2"), d);
+        launch_colsum(T[9], M, d, d, gp(h, "off_b2"), st);
+        launch_gqe_inter_dh(T[10], T[3], n, M, d, T[11], st);
+        G(true, false, d, d, NR, T[11], d, h->stack_v + d, 2 * d, 0.f, gp(h, "off_W1"), d);
+        launch_colsum(T[11], NR, d, d, gp(h, "off_b1"), st);
+        G(false, false, NR, d, d, T[11], d, dp(h, "off_W1"), d, 1.f, h->stack_g + d, 2 * d);
+      } else if (h->kind == KG_BETAE) {
+        // forward: T0 Hs, T1 Lg, T2 w.  backward: T7 dLg, T8 dHs
+        launch_beta_att_bwd(h->stack_v, T[2], gout, n, M, d, T[7], h->stack_g, st);
+        G(false, false, NR, d, m, T[7], m, dp(h, "att_U2"), d, 0.f, T[8], d);
+        launch_relu_mask(T[8], T[0], NR, d, st);
+        G(true, false, m, d, NR, T[7], m, T[0], d, 0.f, gp(h, "att_U2"), d);
+        launch_colsum(T[7], NR, m, m, gp(h, "att_c2"), st);
+        G(true, false, d, d, NR, T[8], d, h->stack_v, d, 0.f, gp(h, "att_U1"), d);
+        launch_colsum(T[8], NR, d, d, gp(h, "att_c1"), st);
+        G(false, false, NR, d, d, T[8], d, dp(h, "att_U1"), d, 1.f, h->stack_g, d);
+      }
+    }
+  }
+  if (h->kind == KG_BETAE) {
+    // projection-MLP weight gradients over all projection uses at once (A9)
+    const int NR = p.nproj * M;
+    G(true, false, d, HH, NR, h->pdZ, d, h->pH2, HH, 0.f, gp(h, "prj_W0"), HH);
+    launch_colsum(h->pdZ, NR, d, d, gp(h, "prj_b0"), st);
+    G(true, false, HH, HH, NR, h->pdH2, HH, h->pH1, HH, 0.f, gp(h, "prj_W2"), HH);
+    launch_colsum(h->pdH2, NR, HH, HH, gp(h, "prj_b2"), st);
+    G(true, false, HH, 2 * d, NR, h->pdH1, HH, h->pX, 2 * d, 0.f, gp(h, "prj_W1"), 2 * d);
+    launch_colsum(h->pdH1, NR, HH, HH, gp(h, "prj_b1"), st);
+  }
+  return KG_OK;
+}
+
+// Assign node value / gradient buffers for the current M (outputs -> Q / dQ slices,
+// intersection inputs -> stack slices).
+void assign_buffers(kg_handle *h, StepBufs &S) {
+  const Plan &p = S.plan;
+  const int64_t Md = (int64_t)S.M * h->dq;
+  for (int ni = 0; ni < p.nn; ++ni) { S.val[ni] = h->nval[ni]; S.grad[ni] = h->ngrad[ni]; }
+  if (p.inter >= 0)
+    for (int k = 0; k < p.n[p.inter].nin; ++k) {
+      S.val[p.n[p.inter].ins[k]] = h->stack_v + k * Md;
+      S.grad[p.n[p.inter].ins[k]] = h->stack_g + k * Md;
+    }
+  for (int t = 0; t < p.nout; ++t) { S.val[p.outs[t]] = h->Q + t * Md; S.grad[p.outs[t]] = h->dQ + t * Md; }
+}
+
+kg_status check_state(kg_handle *h) {
+  if (!h) return KG_EINVAL;
+  if (h->broken) return fail(h, KG_ESTATE, "handle is in an error state: " + h->err);
+  if (!h->bound) return fail(h, KG_ESTATE, "kg_bind has not been called");
+  return KG_OK;
+}
+
+// Validate a batch and stage host inputs into the workspace (H2D on the bound stream).
+kg_status ingest(kg_handle *h, const kg_batch *b, bool train, const Plan &plan) {
+  const int M = b->M, K = train ? b->K : 0, na = plan.na, nr = plan.nr;
+  const int W = (K + 31) / 32;
+  if (M < 1 || M > h->Mx) return fail(h, KG_EINVAL, "M out of range [1, max_M]");
+  if (K < 0 || K > h->Kx) return fail(h, KG_EINVAL, "K out of range [0, max_K]");
+  if (!b->anchors || !b->relations) return fail(h, KG_EINVAL, "null anchors / relations");
+  if (train && (!b->answers || (K > 0 && (!b->negatives || !b->mask))))
+    return fail(h, KG_EINVAL, "null answers / negatives / mask");
+  const size_t sz_a = (size_t)M * na * 8, sz_r = (size_t)M * nr * 4, sz_ans = train ? (size_t)M * 8 : 0,
+               sz_n = (size_t)K * 8, sz_m = (size_t)M * W * 4;
+  if (b->on_device) {
+    CK(cudaMemcpyAsync(h->b_anchors, b->anchors, sz_a, cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaMemcpyAsync(h->b_rels, b->relations, sz_r, cudaMemcpyDeviceToDevice, h->st));
+    if (train) {
+      CK(cudaMemcpyAsync(h->b_answers, b->answers, sz_ans, cudaMemcpyDeviceToDevice, h->st));
+      if (K > 0) {
+        CK(cudaMemcpyAsync(h->b_negs, b->negatives, sz_n, cudaMemcpyDeviceToDevice, h->st));
+        CK(cudaMemcpyAsync(h->b_mask, b->mask, sz_m, cudaMemcpyDeviceToDevice, h->st));
+      }
+    }
+    return KG_OK;
+  }
+  // host inputs: validate here (EINVAL before anything is enqueued)
+  for (int64_t i = 0; i < (int64_t)M * na; ++i)
+    if (b->anchors[i] < 0 || b->anchors[i] >= h->n_ent) return fail(h, KG_EINVAL, "anchor id out of range");
+  for (int64_t i = 0; i < (int64_t)M * nr; ++i)
+    if (b->relations[i] < 0 || b->relations[i] >= h->R) return fail(h, KG_EINVAL, "relation id out of range");
+  if (train) {
+    for (int i = 0; i < M; ++i)
+      if (b->answers[i] < 0 || b->answers[i] >= h->n_ent) return fail(h, KG_EINVAL, "answer id out of range");
+    for (int j = 0; j < K; ++j)
+      if (b->negatives[j] < 0 || b->negatives[j] >= h->n_ent) return fail(h, KG_EINVAL, "negative id out of range");
+  }
+  const size_t total = sz_a + sz_r + sz_ans + sz_n + sz_m + 5 * 256;
+  if (total > h->pin_bytes) return fail(h, KG_EINVAL, "batch exceeds staging capacity");
+  const int cur = h->pin_cur;
+  h->pin_cur ^= 1;
+  CK(cudaEventSynchronize(h->pin_ev[cur]));   // the H2D that last read this buffer has finished
+  char *p = h->pin[cur];
+  size_t off = 0;
+  auto put = [&](const void *src, size_t n, void *dst) -> kg_status {
+    if (!n) return KG_OK;
+    std::memcpy(p + off, src, n);
+    CK(cudaMemcpyAsync(dst, p + off, n, cudaMemcpyHostToDevice, h->st));
+    off = (size_t)align_up((int64_t)(off + n), 256);
+    return KG_OK;
+  };
+  kg_status s;
+  if ((s = put(b->anchors, sz_a, h->b_anchors)) != KG_OK) return s;
+  if ((s = put(b->relations, sz_r, h->b_rels)) != KG_OK) return s;
+  if (train) {
+    if ((s = put(b->answers, sz_ans, h->b_answers)) != KG_OK) return s;
+    if ((s = put(b->negatives, sz_n, h->b_negs)) != KG_OK) return s;
+    if ((s = put(b->mask, sz_m, h->b_mask)) != KG_OK) return s;
+  }
+  CK(cudaEventRecord(h->pin_ev[cur], h->st));
+  return KG_OK;
+}
+
+kg_status read_result(kg_handle *h, kg_step_info *info) {
+  CK(cudaEventSynchronize(h->step_done));
+  h->step_pending = false;
+  if (info) {
+    info->loss = h->hout->loss;
+    info->n_touched = h->hout->U;
+    info->step = h->hout->t;
+  }
+  if (h->hout->flags[1]) return fail(h, KG_EINVAL, "an id or relation of the (device) batch was out of range; step not applied");
+  if (h->hout->flags[0]) return fail(h, KG_ENONFINITE, "non-finite loss; step not applied");
+  return KG_OK;
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+kg_status kg_create(const kg_config *cfg, kg_handle **out) {
+  if (!cfg || !out) return KG_EINVAL;
+  *out = nullptr;
+  const kg_config &c = *cfg;
+  if (c.kind < KG_GQE || c.kind > KG_COMPLEX) return KG_EINVAL;
+  if (c.dim < 8 || c.dim > 2048 || c.dim % 8) return KG_EINVAL;
+  if (c.n_entities < 1 || c.n_entities >= ((int64_t)1 << 31) || c.n_relations < 1) return KG_EINVAL;
+  if (c.kind == KG_BETAE && (c.hidden < 8 || c.hidden % 8)) return KG_EINVAL;
+  if (c.max_M < 1 || c.max_K < 0 || c.max_cand < 0) return KG_EINVAL;
+  if (c.world < 1 || c.rank < 0 || c.rank >= c.world) return KG_EINVAL;
+  if (!(c.gamma == c.gamma) || !(c.beta1 >= 0.f && c.beta1 < 1.f) || !(c.beta2 >= 0.f && c.beta2 < 1.f) ||
+      !(c.eps > 0.f))
+    return KG_EINVAL;
+  const int Lx = 3 * c.max_M + c.max_M + std::max(c.max_K, c.max_cand);
+  if (Lx > dedup_capacity()) return KG_EINVAL;
+  if (c.world > 1) return KG_EUNSUPPORTED;   // multi-GPU path: see DESIGN.md §7 (next)
+
+  kg_handle *h = new kg_handle();
+  h->cfg = c;
+  h->kind = c.kind; h->d = c.dim; h->m = c.dim / 2; h->R = c.n_relations; h->n_ent = c.n_entities;
+  h->H = c.kind == KG_BETAE ? c.hidden : 0;
+  h->world = c.world; h->rank = c.rank;
+  h->shard = (c.n_entities + c.world - 1) / c.world;
+  h->dq = c.kind == KG_Q2B ? 2 * c.dim : c.dim;
+  h->dr = c.kind == KG_Q2B ? 2 * c.dim : (c.kind == KG_ROTATE ? c.dim / 2 : c.dim);
+  h->ent_bits = bits_for(c.n_entities);
+  h->rel_bits = bits_for(c.n_relations);
+  h->Mx = c.max_M; h->Kx = std::max(c.max_K, 1); h->Cx = c.max_cand;
+  h->Lx = Lx; h->Lrx = 4 * c.max_M; h->Kpx = (int)align_up(std::max(c.max_K, 1), 64);
+  build_layout(h);
+
+  if (cudaGetDevice(&h->device) != cudaSuccess) { delete h; return KG_ECUDA; }
+  Arena A;
+  carve(h, A);
+  h->ws_bytes = A.off;
+  if (cudaMalloc(&h->ws, h->ws_bytes) != cudaSuccess) { delete h; return KG_ENOMEM; }
+  A = Arena{h->ws, 0};
+  carve(h, A);
+  const int W = (h->Kx + 31) / 32;
+  h->pin_bytes = (size_t)h->Mx * 3 * 8 + (size_t)h->Mx * 3 * 4 + (size_t)h->Mx * 8 + (size_t)h->Kx * 8 +
+                 (size_t)h->Mx * W * 4 + 8 * 256;
+  for (int i = 0; i < 2; ++i) {
+    if (cudaMallocHost(&h->pin[i], h->pin_bytes) != cudaSuccess) { kg_destroy(h); return KG_ENOMEM; }
+    if (cudaEventCreateWithFlags(&h->pin_ev[i], cudaEventDisableTiming) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
+  }
+  if (cudaMallocHost(&h->hout, sizeof(kg_handle::HostOut)) != cudaSuccess) { kg_destroy(h); return KG_ENOMEM; }
+  std::memset(h->hout, 0, sizeof(kg_handle::HostOut));
+  if (cudaEventCreateWithFlags(&h->step_done, cudaEventDisableTiming) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
+  if (cublasCreate(&h->blas) != CUBLAS_STATUS_SUCCESS) { kg_destroy(h); return KG_ECUDA; }
+  cublasSetMathMode(h->blas, CUBLAS_PEDANTIC_MATH);   // true fp32, no TF32 (parity at 1e-5, A24)
+  // device scalars
+  if (cudaMemset(h->ws, 0, h->ws_bytes) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
+  if (cudaMemset(h->rel_stamp, 0xff, sizeof(int64_t) * h->R) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
+  *out = h;
+  return KG_OK;
+}
+
+int64_t kg_shard_rows(const kg_handle *h) { return h ? h->shard : -1; }
+int64_t kg_dense_size(const kg_handle *h) { return h ? h->dense_size : -1; }
+
+kg_status kg_bind(kg_handle *h, const kg_tables *t, void *stream) {
+  if (!h || !t) return KG_EINVAL;
+  if (h->broken) return fail(h, KG_ESTATE, "handle is in an error state: " + h->err);
+  if (!t->ent || !t->ent_m || !t->ent_v || !t->dense || !t->dense_m || !t->dense_v)
+    return fail(h, KG_EINVAL, "null table pointer");
+  const void *ps[6] = {t->ent, t->ent_m, t->ent_v, t->dense, t->dense_m, t->dense_v};
+  for (const void *p : ps)
+    if ((uintptr_t)p % 16) return fail(h, KG_EINVAL, "table pointers must be 16-byte aligned");
+  h->t = *t;
+  h->st = (cudaStream_t)stream;
+  CKB(cublasSetStream(h->blas, h->st));
+  h->bound = true;
+  return KG_OK;
+}
+
+kg_status kg_init_params(kg_handle *h, uint64_t seed) {
+  kg_status s = check_state(h);
+  if (s) return s;
+  const double rho = ((double)h->cfg.gamma + 2.0) / (double)h->d;
+  launch_init_rows(h->t.ent, h->shard, h->d, h->rank, h->world, seed, 0, (float)-rho, (float)rho, h->st);
+  for (size_t i = 0; i < h->segs.size(); ++i)
+    launch_init_flat(h->t.dense + h->segs[i].off, h->segs[i].n, seed, 1 + i, h->segs[i].lo, h->segs[i].hi, h->st);
+  CK(cudaMemsetAsync(h->t.ent_m, 0, sizeof(float) * h->shard * h->d, h->st));
+  CK(cudaMemsetAsync(h->t.ent_v, 0, sizeof(float) * h->shard * h->d, h->st));
+  CK(cudaMemsetAsync(h->t.dense_m, 0, sizeof(float) * h->dense_size, h->st));
+  CK(cudaMemsetAsync(h->t.dense_v, 0, sizeof(float) * h->dense_size, h->st));
+  CK(cudaMemsetAsync(h->t_dev, 0, sizeof(int64_t), h->st));
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(h->st));
+  return KG_OK;
+}
+
+kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info) {
+  kg_status s = check_state(h);
+  if (s) return s;
+  if (!b) return fail(h, KG_EINVAL, "null batch");
+  if (b->structure < KG_1P || b->structure > KG_UP) return fail(h, KG_EINVAL, "bad structure");
+  if (single_hop(h->kind) && b->structure != KG_1P)
+    return fail(h, KG_EUNSUPPORTED, "single-hop models accept only 1p (Table 2, P:L55)");
+  if (!(lr > 0.f)) return fail(h, KG_EINVAL, "lr must be > 0");
+  StepBufs S;
+  S.plan = make_plan(b->structure);
+  if ((s = ingest(h, b, true, S.plan)) != KG_OK) return s;
+  const Plan &p = S.plan;
+  const int M = b->M, K = b->K, d = h->d, na = p.na, nr = p.nr;
+  S.M = M; S.K = K; S.Kp = (int)align_up(std::max(K, 1), 64); S.NQ = p.nout * M;
+  const int L = na * M + M + K, Lr = p.nproj * M;
+  cudaStream_t st = h->st;
+  h->stamp++;
+  h->last_M = M; h->last_K = K;
+
+  // a2: ids + dedup; relation occurrences + dedup
+  CK(cudaMemsetAsync(h->flags, 0, 2 * sizeof(int), st));
+  launch_ids_concat(h->b_anchors, na, M, h->b_answers, M, h->b_negs, K, h->world, h->ids, h->rows, h->flags + 1,
+                    h->n_ent, st);
+  launch_dedup(h->ids, nullptr, L, h->ent_bits, h->uniq, h->inv, h->perm, h->seg, h->Udev, st);
+  Slots4 sl{{0, 0, 0, 0}};
+  {
+    int u = 0;
+    for (int ni = 0; ni < p.nn; ++ni)
+      if (p.n[ni].type == 0) sl.s[u++] = p.n[ni].rel;
+  }
+  launch_rel_occ(h->b_rels, M, nr, sl, p.nproj, h->R, h->rocc, h->flags + 1, st);
+  launch_dedup(nullptr, h->rocc, Lr, h->rel_bits, h->runiq, h->rinv, h->rperm, h->rseg, h->rU, st);
+
+  // a4-a7: fused gather + DAG forward
+  assign_buffers(h, S);
+  if ((s = dag_forward(h, S)) != KG_OK) return s;
+
+  // a8-a10: scoring, Eq. 1, scoring backward
+  const int U = (h->kind == KG_BETAE || h->kind == KG_ROTATE || h->kind == KG_COMPLEX) ? h->m : d;
+  const int64_t *neg_rows = h->rows + (int64_t)na * M + M;
+  const float scale = 1.f / (float)((double)M * h->world);
+  if (h->kind == KG_BETAE) {
+    launch_beta_query(h->Q, S.NQ, h->m, h->QP, h->Cq, st);
+    launch_beta_entity(h->t.ent, neg_rows, K, h->m, h->F, h->Cv, st);
+  }
+  PosArgs pa;
+  pa.M = M; pa.U = U; pa.d = d; pa.ent = h->t.ent; pa.ans_rows = h->rows + (int64_t)na * M; pa.Q = h->Q;
+  pa.alpha = h->cfg.box_alpha; pa.gamma = h->cfg.gamma; pa.scale = scale; pa.Cq = h->Cq; pa.QP = h->QP;
+  pa.loss_pos = h->loss_pos; pa.Dpos = h->Dpos; pa.dQ = h->dQ; pa.dV = h->OG + (int64_t)na * M * d;
+  launch_pos(h->kind, pa, p.nout, st);
+  ScoreArgs sa;
+  sa.Q = h->Q; sa.NQ = S.NQ; sa.M = M; sa.K = K; sa.Kp = S.Kp; sa.U = U; sa.d = d;
+  if (h->kind == KG_BETAE) { sa.E = h->F; sa.eidx = nullptr; sa.estride = 9LL * h->m; }
+  else { sa.E = h->t.ent; sa.eidx = neg_rows; sa.estride = d; }
+  sa.mask = h->b_mask; sa.W = (K + 31) / 32; sa.Cq = h->Cq; sa.Cv = h->Cv; sa.QP = h->QP;
+  sa.gamma = h->cfg.gamma; sa.alpha = h->cfg.box_alpha; sa.scale = scale;
+  sa.C = h->C; sa.Dmin = h->Dmin; sa.loss_part = h->loss_part; sa.dQ = h->dQ;
+  sa.dV = h->OG + (int64_t)(na * M + M) * d;
+  const int njt = (K + 63) / 64;
+  if (K > 0) launch_pair_fwd(h->kind, sa, p.nout, true, st);
+  launch_loss_finalize(h->loss_pos, h->loss_part, M, njt, 1.0 / ((double)M * h->world), h->loss_dev, h->flags,
+                       h->t_dev, h->bc, h->cfg.beta1, h->cfg.beta2, h->apply, st);
+  if (K > 0) launch_pair_bwd(h->kind, sa, st);
+
+  // a11: DAG backward
+  if ((s = dag_backward(h, S)) != KG_OK) return s;
+  if (p.inter < 0 && h->kind != KG_BETAE && h->w_off < h->dense_size)
+    CK(cudaMemsetAsync(h->gdense, 0, sizeof(float) * (h->dense_size - h->w_off), st));
+  if (p.inter < 0 && h->kind == KG_BETAE) {   // attention weights unused by this structure
+    const Seg *a = seg_of(h, "att_U1");
+    CK(cudaMemsetAsync(h->gdense + (a->off - h->w_off), 0, sizeof(float) * (h->dense_size - a->off), st));
+  }
+
+  // a12-a14: relation rows reduce, sparse Adam on touched rows, dense Adam on theta_D
+  launch_rel_reduce(h->rseg, h->rperm, h->rU, Lr, h->RG, h->dr, h->RGU, st);
+  launch_rel_stamp(h->runiq, h->rU, Lr, h->rel_seg_map, h->rel_stamp, h->stamp, st);
+  if (h->apply || h->keep_grads)
+    launch_sparse_adam(h->uniq, h->seg, h->perm, h->Udev, L, h->OG, d, h->world, h->t.ent, h->t.ent_m, h->t.ent_v,
+                       h->keep_grads ? h->Gc : nullptr, lr, h->cfg.beta1, h->cfg.beta2, h->cfg.eps, h->bc, h->flags,
+                       h->apply, st);
+  if (h->apply) {
+    const float b1 = h->cfg.beta1, b2 = h->cfg.beta2, eps = h->cfg.eps;
+    if (h->kind == KG_Q2B) {
+      launch_dense_adam_rel(dp(h, "rel_center"), h->t.dense_m + seg_of(h, "rel_center")->off,
+                            h->t.dense_v + seg_of(h, "rel_center")->off, h->R, d, h->RGU, h->dr, 0, h->rel_seg_map,
+                            h->rel_stamp, h->stamp, lr, b1, b2, eps, h->bc, h->flags, st);
+      launch_dense_adam_rel(dp(h, "rel_offset"), h->t.dense_m + seg_of(h, "rel_offset")->off,
+                            h->t.dense_v + seg_of(h, "rel_offset")->off, h->R, d, h->RGU, h->dr, d, h->rel_seg_map,
+                            h->rel_stamp, h->stamp, lr, b1, b2, eps, h->bc, h->flags, st);
+    } else {
+      const Seg &r = h->segs[0];
+      launch_dense_adam_rel(h->t.dense + r.off, h->t.dense_m + r.off, h->t.dense_v + r.off, h->R, r.cols, h->RGU,
+                            h->dr, 0, h->rel_seg_map, h->rel_stamp, h->stamp, lr, b1, b2, eps, h->bc, h->flags, st);
+    }
+    launch_dense_adam(h->t.dense + h->w_off, h->t.dense_m + h->w_off, h->t.dense_v + h->w_off, h->gdense,
+                      h->dense_size - h->w_off, lr, b1, b2, eps, h->bc, h->flags, st);
+  }
+  CK(cudaGetLastError());
+  // results to pinned host memory (loss, flags, U, t)
+  CK(cudaMemcpyAsync(&h->hout->loss, h->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h->hout->flags, h->flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&h->hout->U, h->Udev, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&h->hout->t, h->t_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(h->step_done, st));
+  h->step_pending = true;
+  h->last_U_valid = 1;
+  if (info) return read_result(h, info);
+  return KG_OK;
+}
+
+kg_status kg_sync(kg_handle *h, kg_step_info *info) {
+  kg_status s = check_state(h);
+  if (s) return s;
+  return read_result(h, info);
+}
+
+kg_status kg_score(kg_handle *h, const kg_batch *q, const int64_t *cand, int32_t n_cand, float *out_dist) {
+  kg_status s = check_state(h);
+  if (s) return s;
+  if (!q || !cand || !out_dist) return fail(h, KG_EINVAL, "null argument");
+  if (q->structure < KG_1P || q->structure > KG_UP) return fail(h, KG_EINVAL, "bad structure");
+  if (single_hop(h->kind) && q->structure != KG_1P) return fail(h, KG_EUNSUPPORTED, "single-hop models accept only 1p");
+  if (n_cand < 1 || n_cand > h->Cx) return fail(h, KG_EINVAL, "n_cand out of range [1, max_cand]");
+  for (int c = 0; c < n_cand; ++c)
+    if (cand[c] < 0 || cand[c] >= h->n_ent) return fail(h, KG_EINVAL, "candidate id out of range");
+  StepBufs S;
+  S.plan = make_plan(q->structure);
+  kg_batch qb = *q;
+  qb.on_device = q->on_device;
+  if ((s = ingest(h, &qb, false, S.plan)) != KG_OK) return s;
+  const Plan &p = S.plan;
+  const int M = q->M, d = h->d, na = p.na, nr = p.nr;
+  S.M = M; S.K = n_cand; S.Kp = n_cand; S.NQ = p.nout * M;
+  cudaStream_t st = h->st;
+  // candidates share the negative slot of the workspace
+  CK(cudaMemcpyAsync(h->b_negs, cand, sizeof(int64_t) * n_cand, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(h->flags, 0, 2 * sizeof(int), st));
+  launch_ids_concat(h->b_anchors, na, M, nullptr, 0, h->b_negs, n_cand, h->world, h->ids, h->rows, h->flags + 1,
+                    h->n_ent, st);
+  Slots4 sl{{0, 0, 0, 0}};
+  {
+    int u = 0;
+    for (int ni = 0; ni < p.nn; ++ni)
+      if (p.n[ni].type == 0) sl.s[u++] = p.n[ni].rel;
+  }
+  launch_rel_occ(h->b_rels, M, nr, sl, p.nproj, h->R, h->rocc, h->flags + 1, st);
+  assign_buffers(h, S);
+  if ((s = dag_forward(h, S)) != KG_OK) return s;
+  const int U = (h->kind == KG_BETAE || h->kind == KG_ROTATE || h->kind == KG_COMPLEX) ? h->m : d;
+  const int64_t *cand_rows = h->rows + (int64_t)na * M;
+  if (h->kind == KG_BETAE) {
+    launch_beta_query(h->Q, S.NQ, h->m, h->QP, h->Cq, st);
+    launch_beta_entity(h->t.ent, cand_rows, n_cand, h->m, h->F, h->Cv, st);
+  }
+  ScoreArgs sa;
+  sa.Q = h->Q; sa.NQ = S.NQ; sa.M = M; sa.K = n_cand; sa.Kp = n_cand; sa.U = U; sa.d = d;
+  if (h->kind == KG_BETAE) { sa.E = h->F; sa.eidx = nullptr; sa.estride = 9LL * h->m; }
+  else { sa.E = h->t.ent; sa.eidx = cand_rows; sa.estride = d; }
+  sa.Cq = h->Cq; sa.Cv = h->Cv; sa.alpha = h->cfg.box_alpha; sa.Dmin = h->Dscore; sa.ldo = n_cand;
+  launch_pair_fwd(h->kind, sa, p.nout, false, st);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out_dist, h->Dscore, sizeof(float) * (size_t)M * n_cand, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return KG_OK;
+}
+
+static float *table_of(kg_handle *h, int which) {
+  return which == 0 ? h->t.ent : (which == 1 ? h->t.ent_m : (which == 2 ? h->t.ent_v : nullptr));
+}
+
+kg_status kg_read_rows(kg_handle *h, int32_t which, const int64_t *ids, int32_t n, float *out) {
+  kg_status s = check_state(h);
+  if (s) return s;
+  float *tab = table_of(h, which);
+  if (!tab || !ids || !out || n < 0) return fail(h, KG_EINVAL, "bad argument");
+  std::vector<int64_t> rows(n);
+  for (int i = 0; i < n; ++i) {
+    if (ids[i] < 0 || ids[i] >= h->n_ent || ids[i] % h->world != h->rank) return fail(h, KG_EINVAL, "id not owned");
+    rows[i] = ids[i] / h->world;
+  }
+  if (n == 0) return KG_OK;
+  int64_t *drows = nullptr;
+  float *buf = nullptr;
+  CK(cudaMalloc(&drows, sizeof(int64_t) * n));
+  CK(cudaMalloc(&buf, sizeof(float) * (size_t)n * h->d));
+  CK(cudaMemcpyAsync(drows, rows.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, h->st));
+  launch_gather_rows(buf, tab, drows, n, h->d, h->st);
+  CK(cudaMemcpyAsync(out, buf, sizeof(float) * (size_t)n * h->d, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  cudaFree(drows);
+  cudaFree(buf);
+  return KG_OK;
+}
+
+kg_status kg_write_rows(kg_handle *h, int32_t which, const int64_t *ids, int32_t n, const float *in) {
+  kg_status s = check_state(h);
+  if (s) return s;
+  float *tab = table_of(h, which);
+  if (!tab || !ids || !in || n < 0) return fail(h, KG_EINVAL, "bad argument");
+  std::vector<int64_t> rows(n);
+  for (int i = 0; i < n; ++i) {
+    if (ids[i] < 0 || ids[i] >= h->n_ent || ids[i] % h->world != h->rank) return fail(h, KG_EINVAL, "id not owned");
+    rows[i] = ids[i] / h->world;
+  }
+  if (n == 0) return KG_OK;
+  int64_t *drows = nullptr;
+  float *buf = nullptr;
+  CK(cudaMalloc(&drows, sizeof(int64_t) * n));
+  CK(cudaMalloc(&buf, sizeof(float) * (size_t)n * h->d));
+  CK(cudaMemcpyAsync(drows, rows.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, h->st));
+  CK(cudaMemcpyAsync(buf, in, sizeof(float) * (size_t)n * h->d, cudaMemcpyHostToDevice, h->st));
+  launch_scatter_rows(tab, buf, drows, n, h->d, h->st);
+  CK(cudaStreamSynchronize(h->st));
+  cudaFree(drows);
+  cudaFree(buf);
+  return KG_OK;
+}
+
+kg_status kg_read_dense(kg_handle *h, int32_t which, float *out) {
+  kg_status s = check_state(h);
+  if (s) return s;
+  float *p = which == 0 ? h->t.dense : (which == 1 ? h->t.dense_m : (which == 2 ? h->t.dense_v : nullptr));
+  if (!p || !out) return fail(h, KG_EINVAL, "bad argument");
+  CK(cudaMemcpyAsync(out, p, sizeof(float) * h->dense_size, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return KG_OK;
+}
+
+kg_status kg_write_dense(kg_handle *h, int32_t which, const float *in) {
+  kg_status s = check_state(h);
+  if (s) return s;
+  float *p = which == 0 ? h->t.dense : (which == 1 ? h->t.dense_m : (which == 2 ? h->t.dense_v : nullptr));
+  if (!p || !in) return fail(h, KG_EINVAL, "bad argument");
+  CK(cudaMemcpyAsync(p, in, sizeof(float) * h->dense_size, cudaMemcpyHostToDevice, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return KG_OK;
+}
+
+kg_status kg_last_grads(kg_handle *h, int64_t *uniq, float *grad_rows, float *grad_dense, int32_t cap,
+                        int32_t *n_uniq, float *d_pos, float *d_neg) {
+  kg_status s = check_state(h);
+  if (s) return s;
+  if (!h->last_U_valid) return fail(h, KG_ESTATE, "no step has run");
+  CK(cudaStreamSynchronize(h->st));
+  int32_t U = 0, rU = 0;
+  CK(cudaMemcpy(&U, h->Udev, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&rU, h->rU, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (n_uniq) *n_uniq = U;
+  if ((uniq || grad_rows) && U > cap) return fail(h, KG_EINVAL, "cap < number of touched rows");
+  if (uniq) CK(cudaMemcpy(uniq, h->uniq, sizeof(int64_t) * U, cudaMemcpyDeviceToHost));
+  if (grad_rows) {
+    if (!h->keep_grads) return fail(h, KG_ESTATE, "enable gradient capture with kg_set_apply(h, flags | 2)");
+    CK(cudaMemcpy(grad_rows, h->Gc, sizeof(float) * (size_t)U * h->d, cudaMemcpyDeviceToHost));
+  }
+  if (grad_dense) {
+    std::memset(grad_dense, 0, sizeof(float) * h->dense_size);
+    if (h->dense_size > h->w_off)
+      CK(cudaMemcpy(grad_dense + h->w_off, h->gdense, sizeof(float) * (h->dense_size - h->w_off),
+                    cudaMemcpyDeviceToHost));
+    std::vector<int64_t> ru(rU);
+    std::vector<float> rg((size_t)rU * h->dr);
+    CK(cudaMemcpy(ru.data(), h->runiq, sizeof(int64_t) * rU, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(rg.data(), h->RGU, sizeof(float) * rg.size(), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < rU; ++k) {
+      const int64_t r = ru[k];
+      if (h->kind == KG_Q2B) {
+        const Seg *c = seg_of(h, "rel_center"), *o = seg_of(h, "rel_offset");
+        std::memcpy(grad_dense + c->off + r * h->d, &rg[(size_t)k * h->dr], sizeof(float) * h->d);
+        std::memcpy(grad_dense + o->off + r * h->d, &rg[(size_t)k * h->dr + h->d], sizeof(float) * h->d);
+      } else {
+        const Seg &s0 = h->segs[0];
+        std::memcpy(grad_dense + s0.off + r * s0.cols, &rg[(size_t)k * h->dr], sizeof(float) * s0.cols);
+      }
+    }
+  }
+  if (d_pos) CK(cudaMemcpy(d_pos, h->Dpos, sizeof(float) * h->last_M, cudaMemcpyDeviceToHost));
+  if (d_neg && h->last_K > 0)
+    CK(cudaMemcpy(d_neg, h->Dmin, sizeof(float) * (size_t)h->last_M * h->last_K, cudaMemcpyDeviceToHost));
+  return KG_OK;
+}
+
+kg_status kg_set_apply(kg_handle *h, int32_t flags) {
+  if (!h) return KG_EINVAL;
+  h->apply = flags & 1;
+  h->keep_grads = (flags >> 1) & 1;
+  return KG_OK;
+}
+
+const char *kg_last_error(const kg_handle *h) { return h ? h->err.c_str() : "null handle"; }
+
+void kg_destroy(kg_handle *h) {
+  if (!h) return;
+  if (h->st) cudaStreamSynchronize(h->st);
+  else cudaDeviceSynchronize();
+  if (h->blas) cublasDestroy(h->blas);
+  for (int i = 0; i < 2; ++i) {
+    if (h->pin[i]) cudaFreeHost(h->pin[i]);
+    if (h->pin_ev[i]) cudaEventDestroy(h->pin_ev[i]);
+  }
+  if (h->hout) cudaFreeHost(h->hout);
+  if (h->step_done) cudaEventDestroy(h->step_done);
+  if (h->ws) cudaFree(h->ws);
+  delete h;
+}
+
+}  // extern "C"

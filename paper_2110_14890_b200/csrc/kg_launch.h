@@ -1,0 +1,113 @@
+// kg_launch.h -- host-side launchers of the sm_100a kernels (internal to libkg.so).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace kg {
+
+struct Slots4 { int s[4]; };
+
+struct ScoreArgs {
+  const float *Q = nullptr;     // [NQ][QF*U] query features (NQ = nout*M)
+  int NQ = 0, M = 0, K = 0, Kp = 0, U = 0, d = 0;
+  const float *E = nullptr;     // entity rows (raw theta_E) or BetaE feature rows
+  const int64_t *eidx = nullptr;  // [K] row index into E (nullptr: identity)
+  int64_t estride = 0;
+  const uint32_t *mask = nullptr;
+  int W = 0;
+  const float *Cq = nullptr, *Cv = nullptr, *QP = nullptr;
+  float gamma = 0.f, alpha = 0.f, scale = 0.f;
+  float *C = nullptr;           // [NQ][Kp] adjoint coefficients
+  float *Dmin = nullptr;        // train: [M][K] (optional); score: [M][ldo]
+  int ldo = 0;
+  float *loss_part = nullptr;   // [ceil(K/64)][M]
+  float *dQ = nullptr;          // [NQ][QF*U]
+  float *dV = nullptr;          // raw-row gradients of the pool, [K][d]
+};
+
+struct PosArgs {
+  int M = 0, U = 0, d = 0;
+  const float *ent = nullptr;
+  const int64_t *ans_rows = nullptr;
+  const float *Q = nullptr;
+  float alpha = 0.f, gamma = 0.f, scale = 0.f;
+  const float *Cq = nullptr, *QP = nullptr;
+  float *loss_pos = nullptr, *Dpos = nullptr, *dQ = nullptr, *dV = nullptr;
+};
+
+// k_score.cu
+void launch_pair_fwd(int kind, const ScoreArgs &a, int nout, bool train, cudaStream_t st);
+void launch_pair_bwd(int kind, const ScoreArgs &a, cudaStream_t st);
+void launch_pos(int kind, const PosArgs &p, int nout, cudaStream_t st);
+void launch_beta_entity(const float *ent, const int64_t *rows, int K, int m, float *F, float *Cv, cudaStream_t st);
+void launch_beta_query(const float *Q, int NQ, int m, float *QP, float *Cq, cudaStream_t st);
+void launch_loss_finalize(const float *loss_pos, const float *loss_part, int M, int njt, double scale,
+                          double *loss_out, int *flags, int64_t *t_dev, float *bc, float beta1, float beta2,
+                          int apply, cudaStream_t st);
+
+// k_dedup.cu: sort keys (ids < 2^end_bit) with their positions; outputs
+// uniq[U] (ascending), inv[L] (position -> unique index), perm[L] (sorted
+// positions), seg[U+1] (segment starts into perm), *U_out.
+int dedup_capacity();
+void launch_dedup(const int64_t *ids64, const int32_t *ids32, int L, int end_bit, int64_t *uniq, int32_t *inv,
+                  int32_t *perm, int32_t *seg, int32_t *U_out, cudaStream_t st);
+
+// k_adam.cu
+void launch_init_rows(float *p, int64_t rows, int d, int64_t row0, int64_t row_step, uint64_t seed, uint64_t stream,
+                      float lo, float hi, cudaStream_t st);
+void launch_init_flat(float *p, int64_t n, uint64_t seed, uint64_t stream, float lo, float hi, cudaStream_t st);
+void launch_sparse_adam(const int64_t *uniq, const int32_t *seg, const int32_t *perm, const int32_t *U_dev, int Lmax,
+                        const float *OG, int d, int world, float *ent, float *m, float *v, float *grad_out, float lr,
+                        float beta1, float beta2, float eps, const float *bc, const int *nonfinite, int apply,
+                        cudaStream_t st);
+void launch_rel_reduce(const int32_t *seg, const int32_t *perm, const int32_t *U_dev, int Lmax, const float *RG,
+                       int dr, float *RGU, cudaStream_t st);
+void launch_rel_stamp(const int64_t *uniq_rel, const int32_t *U_dev, int Lmax, int32_t *rel_seg, int64_t *rel_stamp,
+                      int64_t stamp, cudaStream_t st);
+void launch_dense_adam_rel(float *p, float *m, float *v, int R, int width, const float *RGU, int rg_stride,
+                           int rg_col, const int32_t *rel_seg, const int64_t *rel_stamp, int64_t stamp, float lr,
+                           float beta1, float beta2, float eps, const float *bc, const int *nonfinite, cudaStream_t st);
+void launch_dense_adam(float *p, float *m, float *v, const float *g, int64_t n, float lr, float beta1, float beta2,
+                       float eps, const float *bc, const int *nonfinite, cudaStream_t st);
+void launch_colsum(const float *X, int rows, int cols, int ld, float *out, cudaStream_t st);
+
+// k_dag.cu
+void launch_proj_fwd(int kind, int N, int d, const float *in, int64_t in_ld, const int64_t *anchor_rows,
+                     const float *ent, const int32_t *rel, int rel_ld, const float *relA, const float *relB,
+                     float *out, cudaStream_t st);
+void launch_proj_bwd(int kind, int N, int d, const float *dout, const float *in, int64_t in_ld,
+                     const int64_t *anchor_rows, const float *ent, const int32_t *rel, int rel_ld, const float *relA,
+                     const float *relB, const float *out, float *din, int64_t din_ld, float *drel, cudaStream_t st);
+void launch_betae_proj_in(int N, int d, const float *in, const int64_t *anchor_rows, const float *ent,
+                          const int32_t *rel, int rel_ld, const float *relT, float *X, cudaStream_t st);
+void launch_bias_act(float *Y, const float *b, int rows, int cols, int act, cudaStream_t st);
+void launch_betae_proj_out(const float *Z, const float *b0, int rows, int d, float *Zp1, float *out, cudaStream_t st);
+void launch_betae_proj_dz(const float *dout, const float *Zp1, int rows, int d, float *dZ, cudaStream_t st);
+void launch_relu_mask(float *dY, const float *Y, int rows, int cols, cudaStream_t st);
+void launch_betae_split(const float *dX, int N, int d, const int64_t *anchor_rows, const float *ent, float *din,
+                        int64_t din_ld, float *drel, cudaStream_t st);
+void launch_mean_stack(const float *H, int n, int rows, int cols, float *out, cudaStream_t st);
+void launch_gqe_inter_dh(const float *dMn, const float *H, int n, int rows, int cols, float *dH, cudaStream_t st);
+void launch_q2b_att_fwd(const float *stack, const float *Lg, int n, int M, int d, float *a, float *out,
+                        cudaStream_t st);
+void launch_q2b_off_fwd(const float *stack, const float *Z, int n, int M, int d, float *sig, int8_t *amin,
+                        float *out, cudaStream_t st);
+void launch_q2b_att_bwd(const float *stack, const float *a, const float *dout, int n, int M, int d, float *dLg,
+                        float *dstack, cudaStream_t st);
+void launch_q2b_off_bwd(const float *stack, const float *sig, const int8_t *amin, const float *dout, int n, int M,
+                        int d, float *dZ, float *dstack, cudaStream_t st);
+void launch_beta_att_fwd(const float *stack, const float *Lg, int n, int M, int d, float *w, float *out,
+                         cudaStream_t st);
+void launch_beta_att_bwd(const float *stack, const float *w, const float *dout, int n, int M, int d, float *dLg,
+                         float *dstack, cudaStream_t st);
+void launch_scale_copy(float *dst, const float *src, int64_t n, float s, cudaStream_t st);
+void launch_gather_rows(float *dst, const float *src, const int64_t *rows, int n, int d, cudaStream_t st);
+void launch_scatter_rows(float *dst, const float *src, const int64_t *rows, int n, int d, cudaStream_t st);
+// ids = [anchors slot-major (a*M + i) | answers (n_ans) | negatives (K)], rows = id / world
+void launch_ids_concat(const int64_t *anchors, int na, int M, const int64_t *answers, int n_ans, const int64_t *negs,
+                       int K, int world, int64_t *ids, int64_t *rows_out, int32_t *bad, int64_t n_entities,
+                       cudaStream_t st);
+void launch_rel_occ(const int32_t *relations, int M, int nr, Slots4 slots, int nproj, int n_rel, int32_t *occ,
+                    int32_t *bad, cudaStream_t st);
+
+}  // namespace kg

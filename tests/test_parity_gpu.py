@@ -1,0 +1,262 @@
+"""GPU parity: the CUDA path through the C-ABI vs the fp64 oracle (-m gpu).
+
+Tolerance (BASELINE.json north_star): indices and touched-row sets bit-exact;
+losses, gradients and updated rows within rtol = 1e-5 (fp32), measured per
+tensor as |x - ref| <= rtol*|ref| + rtol*max|ref|.  Parity is checked in the
+three stages of SURVEY §8(c): (i) gradients vs oracle gradients, (ii) Adam as
+a pure function of the GPU's own gradient (1e-6), (iii) end-to-end rows, where
+elements with |g_ref| < 1e-4 max|g_ref| are excluded (Adam's first step is
+~ -lr*sign(g), reading H9) and counted.
+
+Sizes span several CUDA tiles with ragged tails: M = 70 (tiles of 64/32
+rows), K = 100 (tiles of 64/32), d = 40 (chunks of 16/32 units, m = 20).
+"""
+import numpy as np
+import pytest
+
+import kggen
+import oracle
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-5
+
+
+def assert_close(x, ref, rtol=RTOL, what="", mask=None):
+    x = np.asarray(x, np.float64)
+    ref = np.asarray(ref, np.float64)
+    assert x.shape == ref.shape, (what, x.shape, ref.shape)
+    if ref.size == 0:
+        return 0
+    err = np.abs(x - ref)
+    tol = rtol * np.abs(ref) + rtol * np.abs(ref).max()
+    bad = err > tol
+    if mask is not None:
+        bad &= mask
+    if bad.any():
+        k = np.unravel_index(np.argmax(np.where(bad, err / np.maximum(tol, 1e-300), 0)), err.shape)
+        raise AssertionError(f"{what}: {bad.sum()}/{bad.size} out of tolerance; worst at {k}: "
+                             f"got {x[k]!r} ref {ref[k]!r} (max|ref| {np.abs(ref).max():.3g})")
+    return int((~mask).sum()) if mask is not None else 0
+
+
+def _model(cfg, max_M, max_K, max_cand=0, seed=5):
+    from paper_2110_14890_b200 import KGModel
+    m = KGModel(cfg, max_M, max_K, max_cand)
+    m.init_params(seed)
+    m.set_apply(True, keep_grads=True)
+    return m
+
+
+def _check_step(gm, table, cfg, batch, lr, step_no=1):
+    M, K = batch["M"], batch["K"]
+    ref = oracle.oracle_step(cfg, table, [batch], lr, apply=False)
+    p0, m0, v0 = table.get(ref.uniq)
+    info = gm.step(gm.host_batch(batch), lr)
+    assert info.step == step_no
+    g = gm.last_grads(cap=4 * M + M + K + 8, M=M, K=K)
+    # (i) forward values, touched set, gradients
+    assert abs(info.loss - ref.loss) <= RTOL * abs(ref.loss) + 1e-12, (info.loss, ref.loss)
+    assert_close(g["d_pos"], ref.d_pos[0], what="D+")
+    if K:
+        assert_close(g["d_neg"], ref.d_neg[0], what="D")
+    np.testing.assert_array_equal(g["uniq"], ref.uniq)
+    assert info.n_touched == len(ref.uniq)
+    assert_close(g["grad_rows"], ref.grad_rows, what="dL/dtheta_E rows")
+    assert_close(g["grad_dense"], ref.grad_dense, what="dL/dtheta_D")
+    # (ii) Adam as a pure function of the GPU's gradient
+    t = step_no
+    rows_gpu = gm.read_rows(ref.uniq)
+    pa, ma, va = oracle.adam(p0, m0, v0, g["grad_rows"].astype(np.float64), lr, t, cfg.beta1, cfg.beta2, cfg.eps)
+    assert_close(rows_gpu, pa, rtol=1e-6, what="sparse Adam(p | g_gpu)")
+    assert_close(gm.read_rows(ref.uniq, 1), ma, rtol=1e-6, what="sparse Adam(m | g_gpu)")
+    assert_close(gm.read_rows(ref.uniq, 2), va, rtol=1e-6, what="sparse Adam(v | g_gpu)")
+    dense_gpu = gm.read_dense(0)
+    pd, md, vd = oracle.adam(table.dense, table.dense_m, table.dense_v, g["grad_dense"].astype(np.float64), lr, t,
+                             cfg.beta1, cfg.beta2, cfg.eps)
+    assert_close(dense_gpu, pd, rtol=1e-6, what="dense Adam(p | g_gpu)")
+    # (iii) end-to-end updated rows against the oracle's own update
+    ref2 = oracle.oracle_step(cfg, table, [batch], lr, apply=True)
+    # the update direction m_hat/sqrt(v_hat) is ill-conditioned where the first moment is
+    # ~0 relative to its tensor (at t = 1: ~ -lr*sign(g), H9): those elements are excluded
+    keep = np.abs(ref2.m_new) >= 1e-4 * np.abs(ref2.m_new).max()
+    assert_close(rows_gpu, ref2.rows_new, what="theta_E rows after step", mask=keep)
+    keepd = np.abs(ref2.dense_m_new) >= 1e-4 * np.abs(ref2.dense_m_new).max()
+    assert_close(dense_gpu, ref2.dense_new, what="theta_D after step", mask=keepd)
+    return info
+
+
+CASES = [(k, s) for k in ("gqe", "q2b", "betae") for s in kggen.STRUCTURES] + \
+        [(k, "1p") for k in ("transe", "rotate", "distmult", "complex")]
+
+
+@pytest.mark.parametrize("kind,structure", CASES)
+def test_step_parity(kind, structure):
+    cfg = kggen.ModelConfig(kind, 40, 300, 7, hidden=24)
+    gm = _model(cfg, 70, 100)
+    table = oracle.SparseTable(cfg, 5)
+    b = kggen.make_batch(cfg, structure, 70, 100, seed=1, step=0, mask_p=0.9)
+    _check_step(gm, table, cfg, b, lr=0.01, step_no=1)
+    # a second step on another batch (t = 2, non-zero moments)
+    b2 = kggen.make_batch(cfg, structure, 70, 100, seed=1, step=1, mask_p=0.9)
+    _check_step(gm, table, cfg, b2, lr=0.01, step_no=2)
+    gm.close()
+
+
+def test_init_matches_generator_bit_exact():
+    for kind in ("q2b", "betae", "rotate"):
+        cfg = kggen.ModelConfig(kind, 40, 300, 7, hidden=24)
+        gm = _model(cfg, 8, 8, seed=11)
+        ids = np.array([0, 1, 17, 299])
+        np.testing.assert_array_equal(gm.read_rows(ids), kggen.init_entity_rows(cfg, 11, ids))
+        np.testing.assert_array_equal(gm.read_dense(), kggen.init_dense(cfg, 11))
+        assert not gm.read_rows(ids, 1).any() and not gm.read_dense(2).any()
+        gm.close()
+
+
+@pytest.mark.parametrize("kind,structure", [("gqe", "ip"), ("q2b", "up"), ("betae", "pi"), ("rotate", "1p"),
+                                            ("complex", "1p"), ("q2b", "3i")])
+def test_score_parity(kind, structure):
+    cfg = kggen.ModelConfig(kind, 40, 300, 7, hidden=24)
+    gm = _model(cfg, 70, 100, max_cand=90)
+    table = oracle.SparseTable(cfg, 5)
+    b = kggen.make_batch(cfg, structure, 70, 100, seed=3)
+    cand = np.random.default_rng(0).integers(0, 300, size=90)
+    assert_close(gm.score(gm.host_batch(b), cand), oracle.oracle_score(cfg, table, b, cand), what="kg_score")
+    gm.close()
+
+
+def test_determinism_bitwise():
+    cfg = kggen.ModelConfig("q2b", 40, 300, 7)
+    outs = []
+    for _ in range(2):
+        gm = _model(cfg, 70, 100)
+        for s, st in enumerate(["2i", "up", "3p"]):
+            gm.step(gm.host_batch(kggen.make_batch(cfg, st, 70, 100, seed=2, step=s)), 0.01)
+        outs.append((gm.read_rows(np.arange(300)), gm.read_dense()))
+        gm.close()
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+
+
+def test_device_inputs_equal_host_inputs():
+    cfg = kggen.ModelConfig("betae", 40, 300, 7, hidden=24)
+    res = []
+    for on_dev in (False, True):
+        gm = _model(cfg, 70, 100)
+        b = kggen.make_batch(cfg, "ip", 70, 100, seed=4)
+        info = gm.step(gm.device_batch(b) if on_dev else gm.host_batch(b), 0.01, on_device=on_dev)
+        res.append((info.loss, gm.read_rows(np.arange(300)), gm.read_dense()))
+        gm.close()
+    assert res[0][0] == res[1][0]
+    np.testing.assert_array_equal(res[0][1], res[1][1])
+    np.testing.assert_array_equal(res[0][2], res[1][2])
+
+
+def test_async_step_then_sync():
+    cfg = kggen.ModelConfig("gqe", 40, 300, 7)
+    gm = _model(cfg, 70, 100)
+    table = oracle.SparseTable(cfg, 5)
+    b = kggen.make_batch(cfg, "2i", 70, 100, seed=6)
+    assert gm.step(gm.host_batch(b), 0.01, sync=False) is None
+    info = gm.sync()
+    ref = oracle.oracle_step(cfg, table, [b], 0.01, apply=False)
+    assert abs(info.loss - ref.loss) <= RTOL * abs(ref.loss)
+    gm.close()
+
+
+def test_untouched_rows_bit_identical():
+    cfg = kggen.ModelConfig("q2b", 40, 300, 7)
+    gm = _model(cfg, 70, 100)
+    before = gm.read_rows(np.arange(300))
+    b = kggen.make_batch(cfg, "2p", 70, 100, seed=7)
+    gm.step(gm.host_batch(b), 0.01)
+    after = gm.read_rows(np.arange(300))
+    touched = set(np.concatenate([b["anchors"].ravel(), b["answers"], b["negatives"]]).tolist())
+    untouched = np.array(sorted(set(range(300)) - touched))
+    assert len(untouched) > 0
+    np.testing.assert_array_equal(after[untouched], before[untouched])
+    assert not np.array_equal(after[sorted(touched)], before[sorted(touched)])
+    gm.close()
+
+
+def test_validation_errors_leave_tables_untouched():
+    from paper_2110_14890_b200 import KGError
+    cfg = kggen.ModelConfig("rotate", 40, 300, 7)
+    gm = _model(cfg, 70, 100)
+    before = gm.read_dense()
+    b = kggen.make_batch(cfg, "2p", 8, 16, seed=8)
+    with pytest.raises(KGError) as e:
+        gm.step(gm.host_batch(b), 0.01)                     # single-hop model, multi-hop structure
+    assert e.value.status == 2
+    b = kggen.make_batch(cfg, "1p", 8, 16, seed=8)
+    b["negatives"][3] = 300
+    with pytest.raises(KGError) as e:
+        gm.step(gm.host_batch(b), 0.01)
+    assert e.value.status == 1
+    b["negatives"][3] = 0
+    b["relations"][0, 0] = 7
+    with pytest.raises(KGError) as e:
+        gm.step(gm.host_batch(b), 0.01)
+    assert e.value.status == 1
+    with pytest.raises(KGError):
+        gm.step(gm.host_batch(kggen.make_batch(cfg, "1p", 71, 16, seed=8)), 0.01)   # M > max_M
+    np.testing.assert_array_equal(gm.read_dense(), before)
+    gm.close()
+
+
+def test_device_side_validation_of_device_inputs():
+    from paper_2110_14890_b200 import KGError
+    cfg = kggen.ModelConfig("gqe", 40, 300, 7)
+    gm = _model(cfg, 70, 100)
+    before = (gm.read_rows(np.arange(300)), gm.read_dense())
+    b = kggen.make_batch(cfg, "2i", 20, 30, seed=9)
+    b["anchors"][2, 1] = 10_000
+    with pytest.raises(KGError) as e:
+        gm.step(gm.device_batch(b), 0.01, on_device=True)
+    assert e.value.status == 1
+    np.testing.assert_array_equal(gm.read_rows(np.arange(300)), before[0])
+    np.testing.assert_array_equal(gm.read_dense(), before[1])
+    gm.close()
+
+
+def test_nonfinite_loss_is_transactional():
+    from paper_2110_14890_b200 import KGError
+    cfg = kggen.ModelConfig("gqe", 40, 300, 7)
+    gm = _model(cfg, 70, 100)
+    b = kggen.make_batch(cfg, "1p", 10, 20, seed=10)
+    bad = gm.read_rows([b["anchors"][0, 0]])
+    bad[0, 3] = np.nan
+    gm.write_rows([b["anchors"][0, 0]], bad)
+    before = (gm.read_rows(np.arange(300)), gm.read_dense())
+    with pytest.raises(KGError) as e:
+        gm.step(gm.host_batch(b), 0.01)
+    assert e.value.status == 6
+    np.testing.assert_array_equal(gm.read_rows(np.arange(300)), before[0])
+    np.testing.assert_array_equal(gm.read_dense(), before[1])
+    gm.close()
+
+
+@pytest.mark.parametrize("kind", ["q2b", "betae"])
+def test_empty_pool_and_empty_mask_rows(kind):
+    cfg = kggen.ModelConfig(kind, 40, 300, 7, hidden=24)
+    gm = _model(cfg, 70, 100)
+    table = oracle.SparseTable(cfg, 5)
+    b = kggen.make_batch(cfg, "2u", 33, 0, seed=12)          # K = 0: positive term only
+    _check_step(gm, table, cfg, b, 0.01, step_no=1)
+    b = kggen.make_batch(cfg, "2i", 33, 40, seed=13)
+    b["mask"][::2] = 0                                      # half the queries with n_i = 0 (A12)
+    _check_step(gm, table, cfg, b, 0.01, step_no=2)
+    gm.close()
+
+
+def test_all_ids_identical():
+    cfg = kggen.ModelConfig("betae", 40, 300, 7, hidden=24)
+    gm = _model(cfg, 70, 100)
+    table = oracle.SparseTable(cfg, 5)
+    b = kggen.make_batch(cfg, "3i", 64, 64, seed=14)
+    b["anchors"][:] = 5
+    b["negatives"][:] = 5
+    b["answers"][:] = 6
+    b["mask"][:] = 0xFFFFFFFF
+    _check_step(gm, table, cfg, b, 0.01, step_no=1)
+    gm.close()
