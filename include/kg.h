@@ -72,7 +72,7 @@ typedef struct {
   int32_t hidden;        /* BetaE projection MLP width H (A9), multiple of 8; ignored otherwise */
   float gamma;           /* margin of Eq. 1 */
   float box_alpha;       /* Q2B in-box weight alpha (Table 1, A7) */
-  float beta1, beta2, eps; /* Adam (A15) */
+  double beta1, beta2, eps; /* Adam (A15); double so that 1 - beta2 keeps its digits */
   int32_t max_M;         /* workspace sizing: queries per step */
   int32_t max_K;         /* workspace sizing: shared negatives per step */
   int32_t max_cand;      /* workspace sizing: candidates per kg_score call */

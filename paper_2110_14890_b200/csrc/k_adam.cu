@@ -43,18 +43,24 @@ void launch_init_flat(float *p, int64_t n, uint64_t seed, uint64_t stream, float
 }
 
 // ------------------------------------------------------------------ Adam
-__device__ __forceinline__ void adam1(float &p, float &m, float &v, float g, float lr, float b1, float b2, float eps,
-                                      float bc1, float bc2) {
-  m = b1 * m + (1.f - b1) * g;
-  v = b2 * v + (1.f - b2) * g * g;
-  p -= lr * (m / bc1) / (sqrtf(v / bc2) + eps);
+// h = {beta1, 1 - beta1, beta2, 1 - beta2} (the complements formed in double on the host:
+// 1 - beta2 in fp32 would lose ~1e-5 of its value), eps; bc = {1 - beta1^t, 1 - beta2^t}.
+struct AdamHyper { float b1, omb1, b2, omb2, eps; };
+__device__ __forceinline__ void adam1(float &p, float &m, float &v, float g, float lr, const AdamHyper &h, float bc1,
+                                      float bc2) {
+  m = h.b1 * m + h.omb1 * g;
+  v = h.b2 * v + h.omb2 * g * g;
+  p -= lr * (m / bc1) / (sqrtf(v / bc2) + h.eps);
 }
-__device__ __forceinline__ void adam4(float4 &p, float4 &m, float4 &v, const float4 g, float lr, float b1, float b2,
-                                      float eps, float bc1, float bc2) {
-  adam1(p.x, m.x, v.x, g.x, lr, b1, b2, eps, bc1, bc2);
-  adam1(p.y, m.y, v.y, g.y, lr, b1, b2, eps, bc1, bc2);
-  adam1(p.z, m.z, v.z, g.z, lr, b1, b2, eps, bc1, bc2);
-  adam1(p.w, m.w, v.w, g.w, lr, b1, b2, eps, bc1, bc2);
+__device__ __forceinline__ void adam4(float4 &p, float4 &m, float4 &v, const float4 g, float lr, const AdamHyper &h,
+                                      float bc1, float bc2) {
+  adam1(p.x, m.x, v.x, g.x, lr, h, bc1, bc2);
+  adam1(p.y, m.y, v.y, g.y, lr, h, bc1, bc2);
+  adam1(p.z, m.z, v.z, g.z, lr, h, bc1, bc2);
+  adam1(p.w, m.w, v.w, g.w, lr, h, bc1, bc2);
+}
+static AdamHyper hyper(double b1, double b2, double eps) {
+  return AdamHyper{(float)b1, (float)(1.0 - b1), (float)b2, (float)(1.0 - b2), (float)eps};
 }
 
 // One warp per distinct row u: G_u = sum of its occurrence gradients in
@@ -64,7 +70,7 @@ __device__ __forceinline__ void adam4(float4 &p, float4 &m, float4 &v, const flo
 __global__ void __launch_bounds__(256) sparse_adam_kernel(const int64_t *uniq, const int32_t *seg,
                                                           const int32_t *perm, const int32_t *U_dev, const float *OG,
                                                           int d, int world, float *ent, float *m, float *v,
-                                                          float *grad_out, float lr, float b1, float b2, float eps,
+                                                          float *grad_out, float lr, AdamHyper hy,
                                                           const float *bc, const int *flags, int apply) {
   const int u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -86,18 +92,18 @@ __global__ void __launch_bounds__(256) sparse_adam_kernel(const int64_t *uniq, c
     float4 *mp = reinterpret_cast<float4 *>(m + row * d) + c;
     float4 *vp = reinterpret_cast<float4 *>(v + row * d) + c;
     float4 P = *pp, Mm = *mp, V = *vp;
-    adam4(P, Mm, V, g, lr, b1, b2, eps, bc1, bc2);
+    adam4(P, Mm, V, g, lr, hy, bc1, bc2);
     *pp = P; *mp = Mm; *vp = V;
   }
 }
 
 void launch_sparse_adam(const int64_t *uniq, const int32_t *seg, const int32_t *perm, const int32_t *U_dev, int Lmax,
                         const float *OG, int d, int world, float *ent, float *m, float *v, float *grad_out, float lr,
-                        float beta1, float beta2, float eps, const float *bc, const int *flags, int apply,
+                        double beta1, double beta2, double eps, const float *bc, const int *flags, int apply,
                         cudaStream_t st) {
   const int warps = 8;
   sparse_adam_kernel<<<(Lmax + warps - 1) / warps, warps * 32, 0, st>>>(uniq, seg, perm, U_dev, OG, d, world, ent, m,
-                                                                        v, grad_out, lr, beta1, beta2, eps, bc,
+                                                                        v, grad_out, lr, hyper(beta1, beta2, eps), bc,
                                                                         flags, apply);
 }
 
@@ -138,7 +144,7 @@ void launch_rel_stamp(const int64_t *uniq_rel, const int32_t *U_dev, int Lmax, i
 __global__ void __launch_bounds__(256) dense_adam_rel_kernel(float *p, float *m, float *v, int R, int width,
                                                              const float *RGU, int rg_stride, int rg_col,
                                                              const int32_t *rel_seg, const int64_t *rel_stamp,
-                                                             int64_t stamp, float lr, float b1, float b2, float eps,
+                                                             int64_t stamp, float lr, AdamHyper hy,
                                                              const float *bc, const int *flags) {
   if (flags[0]) return;
   const int w4 = width >> 2;
@@ -149,7 +155,7 @@ __global__ void __launch_bounds__(256) dense_adam_rel_kernel(float *p, float *m,
     float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
     if (rel_stamp[r] == stamp) g = *reinterpret_cast<const float4 *>(RGU + (int64_t)rel_seg[r] * rg_stride + rg_col + c4 * 4);
     float4 P = reinterpret_cast<float4 *>(p)[e], Mm = reinterpret_cast<float4 *>(m)[e], V = reinterpret_cast<float4 *>(v)[e];
-    adam4(P, Mm, V, g, lr, b1, b2, eps, bc1, bc2);
+    adam4(P, Mm, V, g, lr, hy, bc1, bc2);
     reinterpret_cast<float4 *>(p)[e] = P;
     reinterpret_cast<float4 *>(m)[e] = Mm;
     reinterpret_cast<float4 *>(v)[e] = V;
@@ -157,29 +163,29 @@ __global__ void __launch_bounds__(256) dense_adam_rel_kernel(float *p, float *m,
 }
 void launch_dense_adam_rel(float *p, float *m, float *v, int R, int width, const float *RGU, int rg_stride,
                            int rg_col, const int32_t *rel_seg, const int64_t *rel_stamp, int64_t stamp, float lr,
-                           float beta1, float beta2, float eps, const float *bc, const int *flags, cudaStream_t st) {
+                           double beta1, double beta2, double eps, const float *bc, const int *flags, cudaStream_t st) {
   const int64_t n4 = (int64_t)R * (width / 4);
   dense_adam_rel_kernel<<<grid_for(n4, 256), 256, 0, st>>>(p, m, v, R, width, RGU, rg_stride, rg_col, rel_seg,
-                                                           rel_stamp, stamp, lr, beta1, beta2, eps, bc, flags);
+                                                           rel_stamp, stamp, lr, hyper(beta1, beta2, eps), bc, flags);
 }
 
 __global__ void __launch_bounds__(256) dense_adam_kernel(float *p, float *m, float *v, const float *g, int64_t n4,
-                                                         float lr, float b1, float b2, float eps, const float *bc,
+                                                         float lr, AdamHyper hy, const float *bc,
                                                          const int *flags) {
   if (flags[0]) return;
   const float bc1 = bc[0], bc2 = bc[1];
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n4; e += (int64_t)gridDim.x * blockDim.x) {
     float4 P = reinterpret_cast<float4 *>(p)[e], Mm = reinterpret_cast<float4 *>(m)[e], V = reinterpret_cast<float4 *>(v)[e];
-    adam4(P, Mm, V, reinterpret_cast<const float4 *>(g)[e], lr, b1, b2, eps, bc1, bc2);
+    adam4(P, Mm, V, reinterpret_cast<const float4 *>(g)[e], lr, hy, bc1, bc2);
     reinterpret_cast<float4 *>(p)[e] = P;
     reinterpret_cast<float4 *>(m)[e] = Mm;
     reinterpret_cast<float4 *>(v)[e] = V;
   }
 }
-void launch_dense_adam(float *p, float *m, float *v, const float *g, int64_t n, float lr, float beta1, float beta2,
-                       float eps, const float *bc, const int *flags, cudaStream_t st) {
+void launch_dense_adam(float *p, float *m, float *v, const float *g, int64_t n, float lr, double beta1, double beta2,
+                       double eps, const float *bc, const int *flags, cudaStream_t st) {
   if (n <= 0) return;
-  dense_adam_kernel<<<grid_for(n / 4, 256), 256, 0, st>>>(p, m, v, g, n / 4, lr, beta1, beta2, eps, bc, flags);
+  dense_adam_kernel<<<grid_for(n / 4, 256), 256, 0, st>>>(p, m, v, g, n / 4, lr, hyper(beta1, beta2, eps), bc, flags);
 }
 
 // out[c] = sum_r X[r*ld + c]; 32 columns x 32 row-lanes per block, fixed-order smem reduce.

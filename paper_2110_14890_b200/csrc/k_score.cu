@@ -532,7 +532,7 @@ __global__ void __launch_bounds__(128) beta_query_kernel(const float *Q, int NQ,
 __global__ void __launch_bounds__(256) loss_finalize_kernel(const float *loss_pos, const float *loss_part, int M,
                                                             int njt, double scale, double *loss_out,
                                                             int *flags, int64_t *t_dev, float *bc,
-                                                            float beta1, float beta2, int apply) {
+                                                            double beta1, double beta2, int apply) {
   __shared__ double red[256];
   double s = 0.0;
   for (int i = threadIdx.x; i < M; i += 256) {
@@ -556,8 +556,8 @@ __global__ void __launch_bounds__(256) loss_finalize_kernel(const float *loss_po
     if (!bad && apply) {
       const int64_t t = *t_dev + 1;
       *t_dev = t;
-      bc[0] = (float)(1.0 - pow((double)beta1, (double)t));
-      bc[1] = (float)(1.0 - pow((double)beta2, (double)t));
+      bc[0] = (float)(1.0 - pow(beta1, (double)t));
+      bc[1] = (float)(1.0 - pow(beta2, (double)t));
     }
   }
 }
@@ -630,7 +630,7 @@ void launch_beta_query(const float *Q, int NQ, int m, float *QP, float *Cq, cuda
   beta_query_kernel<<<NQ, 128, 0, st>>>(Q, NQ, m, QP, Cq);
 }
 void launch_loss_finalize(const float *loss_pos, const float *loss_part, int M, int njt, double scale,
-                          double *loss_out, int *flags, int64_t *t_dev, float *bc, float beta1, float beta2,
+                          double *loss_out, int *flags, int64_t *t_dev, float *bc, double beta1, double beta2,
                           int apply, cudaStream_t st) {
   loss_finalize_kernel<<<1, 256, 0, st>>>(loss_pos, loss_part, M, njt, scale, loss_out, flags, t_dev, bc,
                                           beta1, beta2, apply);

@@ -589,8 +589,8 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
   if (c.kind == KG_BETAE && (c.hidden < 8 || c.hidden % 8)) return KG_EINVAL;
   if (c.max_M < 1 || c.max_K < 0 || c.max_cand < 0) return KG_EINVAL;
   if (c.world < 1 || c.rank < 0 || c.rank >= c.world) return KG_EINVAL;
-  if (!(c.gamma == c.gamma) || !(c.beta1 >= 0.f && c.beta1 < 1.f) || !(c.beta2 >= 0.f && c.beta2 < 1.f) ||
-      !(c.eps > 0.f))
+  if (!(c.gamma == c.gamma) || !(c.beta1 >= 0.0 && c.beta1 < 1.0) || !(c.beta2 >= 0.0 && c.beta2 < 1.0) ||
+      !(c.eps > 0.0))
     return KG_EINVAL;
   const int Lx = 3 * c.max_M + c.max_M + std::max(c.max_K, c.max_cand);
   if (Lx > dedup_capacity()) return KG_EINVAL;
@@ -752,7 +752,7 @@ kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info)
                        h->keep_grads ? h->Gc : nullptr, lr, h->cfg.beta1, h->cfg.beta2, h->cfg.eps, h->bc, h->flags,
                        h->apply, st);
   if (h->apply) {
-    const float b1 = h->cfg.beta1, b2 = h->cfg.beta2, eps = h->cfg.eps;
+    const double b1 = h->cfg.beta1, b2 = h->cfg.beta2, eps = h->cfg.eps;
     if (h->kind == KG_Q2B) {
       launch_dense_adam_rel(dp(h, "rel_center"), h->t.dense_m + seg_of(h, "rel_center")->off,
                             h->t.dense_v + seg_of(h, "rel_center")->off, h->R, d, h->RGU, h->dr, 0, h->rel_seg_map,

@@ -42,7 +42,7 @@ void launch_pos(int kind, const PosArgs &p, int nout, cudaStream_t st);
 void launch_beta_entity(const float *ent, const int64_t *rows, int K, int m, float *F, float *Cv, cudaStream_t st);
 void launch_beta_query(const float *Q, int NQ, int m, float *QP, float *Cq, cudaStream_t st);
 void launch_loss_finalize(const float *loss_pos, const float *loss_part, int M, int njt, double scale,
-                          double *loss_out, int *flags, int64_t *t_dev, float *bc, float beta1, float beta2,
+                          double *loss_out, int *flags, int64_t *t_dev, float *bc, double beta1, double beta2,
                           int apply, cudaStream_t st);
 
 // k_dedup.cu: sort keys (ids < 2^end_bit) with their positions; outputs
@@ -58,7 +58,7 @@ void launch_init_rows(float *p, int64_t rows, int d, int64_t row0, int64_t row_s
 void launch_init_flat(float *p, int64_t n, uint64_t seed, uint64_t stream, float lo, float hi, cudaStream_t st);
 void launch_sparse_adam(const int64_t *uniq, const int32_t *seg, const int32_t *perm, const int32_t *U_dev, int Lmax,
                         const float *OG, int d, int world, float *ent, float *m, float *v, float *grad_out, float lr,
-                        float beta1, float beta2, float eps, const float *bc, const int *nonfinite, int apply,
+                        double beta1, double beta2, double eps, const float *bc, const int *flags, int apply,
                         cudaStream_t st);
 void launch_rel_reduce(const int32_t *seg, const int32_t *perm, const int32_t *U_dev, int Lmax, const float *RG,
                        int dr, float *RGU, cudaStream_t st);
@@ -66,9 +66,9 @@ void launch_rel_stamp(const int64_t *uniq_rel, const int32_t *U_dev, int Lmax, i
                       int64_t stamp, cudaStream_t st);
 void launch_dense_adam_rel(float *p, float *m, float *v, int R, int width, const float *RGU, int rg_stride,
                            int rg_col, const int32_t *rel_seg, const int64_t *rel_stamp, int64_t stamp, float lr,
-                           float beta1, float beta2, float eps, const float *bc, const int *nonfinite, cudaStream_t st);
-void launch_dense_adam(float *p, float *m, float *v, const float *g, int64_t n, float lr, float beta1, float beta2,
-                       float eps, const float *bc, const int *nonfinite, cudaStream_t st);
+                           double beta1, double beta2, double eps, const float *bc, const int *flags, cudaStream_t st);
+void launch_dense_adam(float *p, float *m, float *v, const float *g, int64_t n, float lr, double beta1, double beta2,
+                       double eps, const float *bc, const int *flags, cudaStream_t st);
 void launch_colsum(const float *X, int rows, int cols, int ld, float *out, cudaStream_t st);
 
 // k_dag.cu

@@ -30,7 +30,7 @@ STRUCTS = {"1p": 0, "2p": 1, "3p": 2, "2i": 3, "3i": 4, "ip": 5, "pi": 6, "2u": 
 class kg_config(C.Structure):
     _fields_ = [("kind", C.c_int32), ("dim", C.c_int32), ("n_entities", C.c_int64),
                 ("n_relations", C.c_int32), ("hidden", C.c_int32), ("gamma", C.c_float),
-                ("box_alpha", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
+                ("box_alpha", C.c_float), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
                 ("max_M", C.c_int32), ("max_K", C.c_int32), ("max_cand", C.c_int32),
                 ("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.c_void_p)]
 
