@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""bench.py -- training queries/s of the SMORE training step on B200.
+
+Metric (BASELINE.json): training queries/sec at 1/2/4/8 B200 (Freebase-shaped
+Q2B/BetaE); HBM GB/s vs peak.  One "step" = one pass of the whole hot path
+ over one mini-batch of B queries of one structure
+(scheduled structure sampling), structures round-robin over the 9.
+
+Default workload (`--workload C5-q2b`): Freebase-shaped Q2B, d = 400, |R| =
+14,824, B = 512 queries and K = 1,024 shared negatives per GPU, and a
+theta_E shard of ceil(86,054,151 / 8) rows + Adam state per GPU -- the
+per-GPU shard of the 8-GPU Freebase run (constant shard size
+at G < 8 because 413 GB does not fit one GPU).  Synthetic inputs (kggen).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import kggen  # noqa: E402
+
+METRIC = "training queries/sec at 1/2/4/8 B200 (Freebase-shaped Q2B/BetaE); HBM GB/s vs peak"
+UNIT = "queries/s"
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # SMs x FP32 lanes x FMA x max SM clock
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+# ------------------------------------------------------------------ dist
+def dist_init(gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce_max(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(gpu_index)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        rows = [l.split(", ") for l in out.strip().splitlines() if l.count(",") >= 8]
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ algorithmic work
+def pair_flops_per_unit(kind):
+    """FP32 ops per (query, candidate, unit) of the distance, forward; backward counted as 2x."""
+    return {"q2b": 7, "betae": 6, "gqe": 3, "transe": 3, "rotate": 8, "distmult": 2, "complex": 4}[kind]
+
+
+def stage_work(cfg, M, K, structure, U, d):
+    """Algorithmic bytes (HBM) / FLOPs per launch for the stages we report."""
+    nout = 2 if structure in ("2u", "up") else 1
+    units = cfg.dim // 2 if cfg.kind in ("betae", "rotate", "complex") else cfg.dim
+    offs, size = kggen.dense_offsets(cfg)
+    rel_elems = sum(int(np.prod(s)) for n, (o, s) in offs.items() if n.startswith("rel"))
+    w_elems = size - rel_elems
+    L = M * kggen.N_ANCHORS[structure] + M + K
+    return {
+        # scoring fwd+bwd: M*nout x K x units pair-units, fwd + 2x bwd
+        "scoring": ("alu", 3.0 * pair_flops_per_unit(cfg.kind) * M * nout * K * units, "FLOP"),
+        # dense Adam: read p, m, v (+ g of the weights) and write p, m, v of every theta_D element (A17)
+        "dense_adam": ("hbm", 24.0 * size + 4.0 * w_elems, "B"),
+        # sparse Adam: p, m, v read + write of the U touched rows + the L occurrence gradient rows read
+        "sparse_adam": ("hbm", 24.0 * U * d + 4.0 * L * d, "B"),
+    }
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, world, rank, local):
+    import torch
+    from paper_2110_14890_b200 import KGModel
+
+    w = kggen.WORKLOADS[args.workload]
+    cfg = w.model_config()
+    if args.workload.startswith("C5"):
+        # constant per-GPU shard: each rank holds ceil(|V|/8) rows.
+        # TODO(next): row-sharded all-to-all exchange for world > 1.
+        cfg.n_entities = kggen.shard_rows(w.n_entities, 8)
+    M, K = w.M, w.K
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    gm = KGModel(cfg, M, K)
+    gm.init_params(args.seed)
+    gm.set_apply(True)
+    lr = args.lr
+    structures = w.structures
+    n_distinct = len(structures) * args.distinct
+    hb = [kggen.make_batch(cfg, structures[s % len(structures)], M, K, seed=args.seed, step=s, rank=rank)
+          for s in range(n_distinct)]
+    db = [gm.device_batch(b) for b in hb]
+    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    # warm-up
+    for s in range(args.warmup):
+        gm.step(db[s % n_distinct], lr, sync=False, on_device=True)
+    gm.sync()
+    torch.cuda.synchronize()
+    barrier(world)
+
+    # ---- timed region: device-resident inputs, L2 flushed between steps (outside the events)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        flush.zero_()
+        ev[s][0].record(stream)
+        gm.step(db[(args.warmup + s) % n_distinct], lr, sync=False, on_device=True)
+        ev[s][1].record(stream)
+    info = gm.sync()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    barrier(world)
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = allreduce_max(sum(step_ms), world)
+    value = world * args.steps * M / (total_ms / 1e3)
+    kernels_per_step = info.kernels
+
+    # ---- profiling pass: the same steps with stage events (CUDA events on the bound stream)
+    gm.set_apply(True, stage_timing=True)
+    stage = np.zeros(8)
+    work = {}
+    n_prof = min(args.steps, 9 * 3)
+    for s in range(n_prof):
+        b = hb[(args.warmup + s) % n_distinct]
+        flush.zero_()
+        inf = gm.step(db[(args.warmup + s) % n_distinct], lr, sync=True, on_device=True)
+        stage += np.array(inf.stage_ms[:8])
+        for k, (bound, amount, unit) in stage_work(cfg, M, K, b["structure"], inf.n_touched, cfg.dim).items():
+            work.setdefault(k, [bound, 0.0, unit])[1] += amount
+    gm.set_apply(True)
+    stage /= n_prof
+    stage_names = ["ingest+dedup", "dag_forward", "scoring_forward", "scoring_backward", "dag_backward",
+                   "sparse_adam", "dense_adam"]
+    shares = {stage_names[i]: round(float(stage[i] / stage[7]), 4) for i in range(7)}
+    pk, pk_src = peaks()
+    cand = {"scoring": (stage[2] + stage[3]), "dense_adam": stage[6], "sparse_adam": stage[5]}
+    dom = max(cand, key=cand.get)
+    bound, amount, unit = work[dom]
+    per_launch = amount / n_prof
+    sec = cand[dom] / 1e3
+    if bound == "hbm":
+        achieved = per_launch / sec / 1e9
+        peak = pk.get("hbm_gbs")
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None}
+    else:
+        achieved = per_launch / sec / 1e12
+        roof = {"bound": "alu", "achieved": round(achieved, 2), "peak": round(FP32_PEAK_TFLOPS, 1),
+                "unit": "TFLOP/s", "frac": round(achieved / FP32_PEAK_TFLOPS, 4), "traffic": None}
+    roof.update({"kernel": dom, "peak_source": pk_src if bound == "hbm" else "derived (DESIGN.md §6)",
+                 "stage_ms": {stage_names[i]: round(float(stage[i]), 4) for i in range(7)},
+                 "stage_share": shares, "dominant_share": round(float(cand[dom] / stage[7]), 4)})
+    other = {}
+    for k in cand:
+        b_, a_, u_ = work[k]
+        t_ = cand[k] / 1e3
+        other[k] = (round(a_ / n_prof / t_ / 1e9, 1), "GB/s") if b_ == "hbm" else (round(a_ / n_prof / t_ / 1e12, 2), "TFLOP/s")
+    roof["all"] = other
+
+    # ---- e2e: the public API with HOST (pinned) buffers; H2D of inputs + D2H of the loss every step
+    pinned = []
+    for b in hb:
+        hbb = gm.host_batch(b)
+        pb = dict(structure=b["structure"], M=M, K=K)
+        for k in ("anchors", "relations", "answers", "negatives", "mask"):
+            a = hbb[k]
+            if a.dtype == np.uint32:
+                a = a.view(np.int32)
+            t = torch.from_numpy(a.copy()).pin_memory()
+            pb[k] = t
+        pinned.append(pb)
+    h2d = sum(int(pinned[0][k].numel() * pinned[0][k].element_size()) for k in ("anchors", "relations", "answers",
+                                                                             "negatives", "mask"))
+    n_e2e = min(args.steps, 450)
+    torch.cuda.synchronize()
+    barrier(world)
+    t1 = time.perf_counter()
+    for s in range(n_e2e):
+        gm.step(pinned[s % n_distinct], lr, sync=True)       # copies + loss read inside
+    e2e_s = allreduce_max(time.perf_counter() - t1, world)
+    e2e = {"value": round(world * n_e2e * M / e2e_s, 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": 28, "steps": n_e2e}
+
+    out = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 5), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (kggen, seeded)",
+        "config": {"workload": args.workload, "model": cfg.kind, "dim": cfg.dim,
+                   "entities_per_gpu": cfg.n_entities, "relations": cfg.n_relations,
+                   "global_batch": M * world, "negatives_per_gpu": K, "structures": structures,
+                   "lr": lr, "parallelism": f"dp{world}" if world > 1 else "single",
+                   "l2": "flushed between timed steps (256 MB write outside the step events)",
+                   "note": w.note},
+        "e2e": e2e, "roofline": roof, "gpu_launches": int(kernels_per_step * args.steps),
+        "kernels_per_step": kernels_per_step, "gemms_per_step": info.gemms, "clocks": clk,
+        "wall_s": round(wall, 3), "loss_last": info.loss,
+    }
+    gm.close()
+    return out, cfg, hb
+
+
+# ------------------------------------------------------------------ oracle timing
+def oracle_time(cfg, batches, q_per_step, n_steps, seed):
+    """Time the CPU oracle, as it stands, on the first q_per_step queries of each batch (full pool)."""
+    import torch
+    import oracle
+    table = oracle.SparseTable(cfg, seed)
+    done = 0
+    t0 = time.perf_counter()
+    for s in range(n_steps):
+        b = batches[s % len(batches)]
+        q = q_per_step
+        sub = dict(b, anchors=b["anchors"][:q], relations=b["relations"][:q], answers=b["answers"][:q],
+                   mask=b["mask"][:q], M=q)
+        oracle.oracle_step(cfg, table, [sub], 1e-4)
+        done += q
+    dt = time.perf_counter() - t0
+    return done / dt, torch.get_num_threads(), dt
+
+
+def cpu_baseline(cfg, batches, seed, budget_s=20.0):
+    # ~2 s per step of 16 queries on the 8-core dev box; sized to stay within ~budget_s
+    rate, cores, dt = oracle_time(cfg, batches, 16, 1, seed)
+    n = max(1, min(9, int(budget_s / max(dt, 1e-3))))
+    rate, cores, dt = oracle_time(cfg, batches, 16, n, seed)
+    return {"value": round(rate, 3), "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{n} steps x 16 of the 512 queries (full K pool, full theta_D Adam), structures "
+                      f"round-robin, fp64 torch CPU; {dt:.1f} s"}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the CPU oracle as it stands, on our config/metric (rank 0 only)."""
+    if rank != 0:
+        return None
+    w = kggen.WORKLOADS[args.workload]
+    cfg = w.model_config()
+    if args.workload.startswith("C5"):
+        cfg.n_entities = kggen.shard_rows(w.n_entities, 8)
+    batches = [kggen.make_batch(cfg, w.structures[s % len(w.structures)], w.M, w.K, seed=args.seed, step=s)
+               for s in range(len(w.structures))]
+    q = 4
+    for s in range(min(args.warmup, 1)):
+        oracle_time(cfg, batches, q, 1, args.seed)
+    rate, cores, dt = oracle_time(cfg, batches, q, args.steps if args.steps <= 60 else 60, args.seed)
+    steps_run = args.steps if args.steps <= 60 else 60
+    return {"impl": "reference", "metric": METRIC, "value": round(rate, 3), "unit": UNIT, "n_gpus": 1,
+            "steps": steps_run, "warmup": args.warmup, "ms_per_step": round(dt / steps_run * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (kggen, seeded)",
+            "config": {"workload": args.workload, "model": cfg.kind, "dim": cfg.dim,
+                       "entities_per_gpu": cfg.n_entities, "queries_per_step_sample": q},
+            "cpu_baseline": {"value": round(rate, 3), "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{steps_run} steps x {q} queries of the workload (full pool)"},
+            "e2e": {"value": round(rate, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=900)
+    ap.add_argument("--warmup", type=int, default=18)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C5-q2b", choices=sorted(kggen.WORKLOADS))
+    ap.add_argument("--lr", type=float, default=1e-4)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--distinct", type=int, default=4, help="distinct batches per structure (cycled)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    assert args.warmup >= 3
+    world, rank, local = dist_init(args.gpus)
+    if args.impl == "reference":
+        out = run_reference(args, world, rank)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    out, cfg, hb = run_ours(args, world, rank, local)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(cfg, hb, args.seed)
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -115,6 +115,11 @@ typedef struct {
   double loss;           /* global Eq. 1 loss of the step (mean over queries and ranks, A12, A18) */
   int32_t n_touched;     /* distinct entity ids touched by this rank's batch (A16) */
   int64_t step;          /* Adam step counter t after the step */
+  int32_t kernels;       /* kernels of this library enqueued by the step */
+  int32_t gemms;         /* cuBLAS SGEMM calls enqueued by the step (dense MLP layers) */
+  float stage_ms[8];     /* device time per stage when stage timing is on (kg_set_apply bit 2), else 0:
+                            0 ingest + dedup, 1 DAG forward, 2 scoring forward + Eq. 1, 3 scoring backward,
+                            4 DAG backward, 5 relation reduce + sparse Adam, 6 dense Adam, 7 whole step */
 } kg_step_info;
 
 typedef struct kg_handle kg_handle;   /* opaque; one per (process, device) */
@@ -174,7 +179,8 @@ kg_status kg_last_grads(kg_handle *h, int64_t *uniq, float *grad_rows, float *gr
 
 /* Test hook.  flags bit 0 (default 1): apply the optimizers; 0 computes loss and
  * gradients but skips both optimizers and t.  bit 1 (default 0): keep the merged
- * theta_E gradient rows of each step for kg_last_grads (one extra U x dim write). */
+ * theta_E gradient rows of each step for kg_last_grads (one extra U x dim write).
+ * bit 2 (default 0): record CUDA events between the stages of kg_step (kg_step_info.stage_ms). */
 kg_status kg_set_apply(kg_handle *h, int32_t flags);
 
 const char *kg_last_error(const kg_handle *h);

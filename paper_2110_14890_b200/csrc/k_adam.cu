@@ -35,11 +35,11 @@ static int grid_for(int64_t n, int threads) {
 void launch_init_rows(float *p, int64_t rows, int d, int64_t row0, int64_t row_step, uint64_t seed, uint64_t stream,
                       float lo, float hi, cudaStream_t st) {
   if (rows <= 0) return;
-  init_rows_kernel<<<grid_for(rows * d, 256), 256, 0, st>>>(p, rows, d, row0, row_step, seed, stream, lo, hi);
+  { init_rows_kernel<<<grid_for(rows * d, 256), 256, 0, st>>>(p, rows, d, row0, row_step, seed, stream, lo, hi); ++g_launches; }
 }
 void launch_init_flat(float *p, int64_t n, uint64_t seed, uint64_t stream, float lo, float hi, cudaStream_t st) {
   if (n <= 0) return;
-  init_flat_kernel<<<grid_for(n, 256), 256, 0, st>>>(p, n, seed, stream, lo, hi);
+  { init_flat_kernel<<<grid_for(n, 256), 256, 0, st>>>(p, n, seed, stream, lo, hi); ++g_launches; }
 }
 
 // ------------------------------------------------------------------ Adam
@@ -102,9 +102,9 @@ void launch_sparse_adam(const int64_t *uniq, const int32_t *seg, const int32_t *
                         double beta1, double beta2, double eps, const float *bc, const int *flags, int apply,
                         cudaStream_t st) {
   const int warps = 8;
-  sparse_adam_kernel<<<(Lmax + warps - 1) / warps, warps * 32, 0, st>>>(uniq, seg, perm, U_dev, OG, d, world, ent, m,
+  { sparse_adam_kernel<<<(Lmax + warps - 1) / warps, warps * 32, 0, st>>>(uniq, seg, perm, U_dev, OG, d, world, ent, m,
                                                                         v, grad_out, lr, hyper(beta1, beta2, eps), bc,
-                                                                        flags, apply);
+                                                                        flags, apply); ++g_launches; }
 }
 
 // Relation occurrence gradients -> one row per distinct relation (fixed order).
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(256) rel_reduce_kernel(const int32_t *seg, con
 }
 void launch_rel_reduce(const int32_t *seg, const int32_t *perm, const int32_t *U_dev, int Lmax, const float *RG,
                        int dr, float *RGU, cudaStream_t st) {
-  rel_reduce_kernel<<<(Lmax + 7) / 8, 256, 0, st>>>(seg, perm, U_dev, RG, dr, RGU);
+  { rel_reduce_kernel<<<(Lmax + 7) / 8, 256, 0, st>>>(seg, perm, U_dev, RG, dr, RGU); ++g_launches; }
 }
 
 // rel_seg[r] = index of relation r's reduced gradient row, valid iff rel_stamp[r] == stamp.
@@ -137,7 +137,7 @@ __global__ void rel_stamp_kernel(const int64_t *uniq_rel, const int32_t *U_dev, 
 }
 void launch_rel_stamp(const int64_t *uniq_rel, const int32_t *U_dev, int Lmax, int32_t *rel_seg, int64_t *rel_stamp,
                       int64_t stamp, cudaStream_t st) {
-  rel_stamp_kernel<<<(Lmax + 255) / 256, 256, 0, st>>>(uniq_rel, U_dev, rel_seg, rel_stamp, stamp);
+  { rel_stamp_kernel<<<(Lmax + 255) / 256, 256, 0, st>>>(uniq_rel, U_dev, rel_seg, rel_stamp, stamp); ++g_launches; }
 }
 
 // Dense Adam over a relation table [R][width] (A17: every row, g = 0 if unused).
@@ -165,8 +165,8 @@ void launch_dense_adam_rel(float *p, float *m, float *v, int R, int width, const
                            int rg_col, const int32_t *rel_seg, const int64_t *rel_stamp, int64_t stamp, float lr,
                            double beta1, double beta2, double eps, const float *bc, const int *flags, cudaStream_t st) {
   const int64_t n4 = (int64_t)R * (width / 4);
-  dense_adam_rel_kernel<<<grid_for(n4, 256), 256, 0, st>>>(p, m, v, R, width, RGU, rg_stride, rg_col, rel_seg,
-                                                           rel_stamp, stamp, lr, hyper(beta1, beta2, eps), bc, flags);
+  { dense_adam_rel_kernel<<<grid_for(n4, 256), 256, 0, st>>>(p, m, v, R, width, RGU, rg_stride, rg_col, rel_seg,
+                                                           rel_stamp, stamp, lr, hyper(beta1, beta2, eps), bc, flags); ++g_launches; }
 }
 
 __global__ void __launch_bounds__(256) dense_adam_kernel(float *p, float *m, float *v, const float *g, int64_t n4,
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(256) dense_adam_kernel(float *p, float *m, flo
 void launch_dense_adam(float *p, float *m, float *v, const float *g, int64_t n, float lr, double beta1, double beta2,
                        double eps, const float *bc, const int *flags, cudaStream_t st) {
   if (n <= 0) return;
-  dense_adam_kernel<<<grid_for(n / 4, 256), 256, 0, st>>>(p, m, v, g, n / 4, lr, hyper(beta1, beta2, eps), bc, flags);
+  { dense_adam_kernel<<<grid_for(n / 4, 256), 256, 0, st>>>(p, m, v, g, n / 4, lr, hyper(beta1, beta2, eps), bc, flags); ++g_launches; }
 }
 
 // out[c] = sum_r X[r*ld + c]; 32 columns x 32 row-lanes per block, fixed-order smem reduce.
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(1024) colsum_kernel(const float *X, int rows, 
   }
 }
 void launch_colsum(const float *X, int rows, int cols, int ld, float *out, cudaStream_t st) {
-  colsum_kernel<<<(cols + 31) / 32, 1024, 0, st>>>(X, rows, cols, ld, out);
+  { colsum_kernel<<<(cols + 31) / 32, 1024, 0, st>>>(X, rows, cols, ld, out); ++g_launches; }
 }
 
 }  // namespace kg

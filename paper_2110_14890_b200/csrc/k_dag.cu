@@ -98,12 +98,12 @@ void launch_proj_fwd(int kind, int N, int d, const float *in, int64_t in_ld, con
   const int g = blocks((int64_t)N * U);
 #define ARGS N, d, in, in_ld, anchor_rows, ent, rel, rel_ld, relA, relB, out
   switch (kind) {
-    case GQE: proj_fwd_kernel<GQE><<<g, 256, 0, st>>>(ARGS); break;
-    case TRANSE: proj_fwd_kernel<TRANSE><<<g, 256, 0, st>>>(ARGS); break;
-    case Q2B: proj_fwd_kernel<Q2B><<<g, 256, 0, st>>>(ARGS); break;
-    case DISTMULT: proj_fwd_kernel<DISTMULT><<<g, 256, 0, st>>>(ARGS); break;
-    case COMPLEX: proj_fwd_kernel<COMPLEX><<<g, 256, 0, st>>>(ARGS); break;
-    case ROTATE: proj_fwd_kernel<ROTATE><<<g, 256, 0, st>>>(ARGS); break;
+    case GQE: { proj_fwd_kernel<GQE><<<g, 256, 0, st>>>(ARGS); ++g_launches; } break;
+    case TRANSE: { proj_fwd_kernel<TRANSE><<<g, 256, 0, st>>>(ARGS); ++g_launches; } break;
+    case Q2B: { proj_fwd_kernel<Q2B><<<g, 256, 0, st>>>(ARGS); ++g_launches; } break;
+    case DISTMULT: { proj_fwd_kernel<DISTMULT><<<g, 256, 0, st>>>(ARGS); ++g_launches; } break;
+    case COMPLEX: { proj_fwd_kernel<COMPLEX><<<g, 256, 0, st>>>(ARGS); ++g_launches; } break;
+    case ROTATE: { proj_fwd_kernel<ROTATE><<<g, 256, 0, st>>>(ARGS); ++g_launches; } break;
     default: break;
   }
 #undef ARGS
@@ -116,12 +116,12 @@ void launch_proj_bwd(int kind, int N, int d, const float *dout, const float *in,
   const int g = blocks((int64_t)N * U);
 #define ARGS N, d, dout, in, in_ld, anchor_rows, ent, rel, rel_ld, relA, relB, out, din, din_ld, drel
   switch (kind) {
-    case GQE: proj_bwd_kernel<GQE><<<g, 256, 0, st>>>(ARGS); break;
-    case TRANSE: proj_bwd_kernel<TRANSE><<<g, 256, 0, st>>>(ARGS); break;
-    case Q2B: proj_bwd_kernel<Q2B><<<g, 256, 0, st>>>(ARGS); break;
-    case DISTMULT: proj_bwd_kernel<DISTMULT><<<g, 256, 0, st>>>(ARGS); break;
-    case COMPLEX: proj_bwd_kernel<COMPLEX><<<g, 256, 0, st>>>(ARGS); break;
-    case ROTATE: proj_bwd_kernel<ROTATE><<<g, 256, 0, st>>>(ARGS); break;
+    case GQE: { proj_bwd_kernel<GQE><<<g, 256, 0, st>>>(ARGS); ++g_launches; } break;
+    case TRANSE: { proj_bwd_kernel<TRANSE><<<g, 256, 0, st>>>(ARGS); ++g_launches; } break;
+    case Q2B: { proj_bwd_kernel<Q2B><<<g, 256, 0, st>>>(ARGS); ++g_launches; } break;
+    case DISTMULT: { proj_bwd_kernel<DISTMULT><<<g, 256, 0, st>>>(ARGS); ++g_launches; } break;
+    case COMPLEX: { proj_bwd_kernel<COMPLEX><<<g, 256, 0, st>>>(ARGS); ++g_launches; } break;
+    case ROTATE: { proj_bwd_kernel<ROTATE><<<g, 256, 0, st>>>(ARGS); ++g_launches; } break;
     default: break;
   }
 #undef ARGS
@@ -140,7 +140,7 @@ __global__ void betae_proj_in_kernel(int N, int d, const float *in, const int64_
 }
 void launch_betae_proj_in(int N, int d, const float *in, const int64_t *anchor_rows, const float *ent,
                           const int32_t *rel, int rel_ld, const float *relT, float *X, cudaStream_t st) {
-  betae_proj_in_kernel<<<blocks((int64_t)N * d), 256, 0, st>>>(N, d, in, anchor_rows, ent, rel, rel_ld, relT, X);
+  { betae_proj_in_kernel<<<blocks((int64_t)N * d), 256, 0, st>>>(N, d, in, anchor_rows, ent, rel, rel_ld, relT, X); ++g_launches; }
 }
 
 // Y = act(Y + b) row-wise; act 1 = ReLU, 0 = identity.
@@ -151,7 +151,7 @@ __global__ void bias_act_kernel(float *Y, const float *b, int rows, int cols, in
   Y[e] = act ? fmaxf(v, 0.f) : v;
 }
 void launch_bias_act(float *Y, const float *b, int rows, int cols, int act, cudaStream_t st) {
-  bias_act_kernel<<<blocks((int64_t)rows * cols), 256, 0, st>>>(Y, b, rows, cols, act);
+  { bias_act_kernel<<<blocks((int64_t)rows * cols), 256, 0, st>>>(Y, b, rows, cols, act); ++g_launches; }
 }
 
 __global__ void betae_proj_out_kernel(const float *Z, const float *b0, int rows, int d, float *Zp1, float *out) {
@@ -163,7 +163,7 @@ __global__ void betae_proj_out_kernel(const float *Z, const float *b0, int rows,
 }
 void launch_betae_proj_out(const float *Z, const float *b0, int rows, int d, float *Zp1, float *out,
                            cudaStream_t st) {
-  betae_proj_out_kernel<<<blocks((int64_t)rows * d), 256, 0, st>>>(Z, b0, rows, d, Zp1, out);
+  { betae_proj_out_kernel<<<blocks((int64_t)rows * d), 256, 0, st>>>(Z, b0, rows, d, Zp1, out); ++g_launches; }
 }
 
 __global__ void betae_proj_dz_kernel(const float *dout, const float *Zp1, int rows, int d, float *dZ) {
@@ -173,7 +173,7 @@ __global__ void betae_proj_dz_kernel(const float *dout, const float *Zp1, int ro
   dZ[e] = (z >= kBetaLo && z <= kBetaHi) ? dout[e] : 0.f;
 }
 void launch_betae_proj_dz(const float *dout, const float *Zp1, int rows, int d, float *dZ, cudaStream_t st) {
-  betae_proj_dz_kernel<<<blocks((int64_t)rows * d), 256, 0, st>>>(dout, Zp1, rows, d, dZ);
+  { betae_proj_dz_kernel<<<blocks((int64_t)rows * d), 256, 0, st>>>(dout, Zp1, rows, d, dZ); ++g_launches; }
 }
 
 __global__ void relu_mask_kernel(float *dY, const float *Y, int64_t n) {
@@ -181,7 +181,7 @@ __global__ void relu_mask_kernel(float *dY, const float *Y, int64_t n) {
   if (e < n && !(Y[e] > 0.f)) dY[e] = 0.f;
 }
 void launch_relu_mask(float *dY, const float *Y, int rows, int cols, cudaStream_t st) {
-  relu_mask_kernel<<<blocks((int64_t)rows * cols), 256, 0, st>>>(dY, Y, (int64_t)rows * cols);
+  { relu_mask_kernel<<<blocks((int64_t)rows * cols), 256, 0, st>>>(dY, Y, (int64_t)rows * cols); ++g_launches; }
 }
 
 // dX [N][2d] -> din (query part; raw-row gradient through the clamp for anchors) and drel.
@@ -197,7 +197,7 @@ __global__ void betae_split_kernel(const float *dX, int N, int d, const int64_t 
 }
 void launch_betae_split(const float *dX, int N, int d, const int64_t *anchor_rows, const float *ent, float *din,
                         int64_t din_ld, float *drel, cudaStream_t st) {
-  betae_split_kernel<<<blocks((int64_t)N * d), 256, 0, st>>>(dX, N, d, anchor_rows, ent, din, din_ld, drel);
+  { betae_split_kernel<<<blocks((int64_t)N * d), 256, 0, st>>>(dX, N, d, anchor_rows, ent, din, din_ld, drel); ++g_launches; }
 }
 
 // ------------------------------------------------------------ intersections
@@ -210,7 +210,7 @@ __global__ void mean_stack_kernel(const float *H, int n, int64_t rc, float *out)
 }
 void launch_mean_stack(const float *H, int n, int rows, int cols, float *out, cudaStream_t st) {
   const int64_t rc = (int64_t)rows * cols;
-  mean_stack_kernel<<<blocks(rc), 256, 0, st>>>(H, n, rc, out);
+  { mean_stack_kernel<<<blocks(rc), 256, 0, st>>>(H, n, rc, out); ++g_launches; }
 }
 
 // dH_t = dMn / n * [H_t > 0]   (DeepSet mean pooling + ReLU adjoint, A4)
@@ -221,7 +221,7 @@ __global__ void gqe_inter_dh_kernel(const float *dMn, const float *H, int n, int
 }
 void launch_gqe_inter_dh(const float *dMn, const float *H, int n, int rows, int cols, float *dH, cudaStream_t st) {
   const int64_t rc = (int64_t)rows * cols;
-  gqe_inter_dh_kernel<<<blocks(rc * n), 256, 0, st>>>(dMn, H, n, rc, dH);
+  { gqe_inter_dh_kernel<<<blocks(rc * n), 256, 0, st>>>(dMn, H, n, rc, dH); ++g_launches; }
 }
 
 // Q2B center attention: a_t = softmax_t(Lg_t) per (i, k); c = sum_t a_t c_t (A5).
@@ -244,7 +244,7 @@ __global__ void q2b_att_fwd_kernel(const float *stack, const float *Lg, int n, i
 }
 void launch_q2b_att_fwd(const float *stack, const float *Lg, int n, int M, int d, float *a, float *out,
                         cudaStream_t st) {
-  q2b_att_fwd_kernel<<<blocks((int64_t)M * d), 256, 0, st>>>(stack, Lg, n, M, d, a, out);
+  { q2b_att_fwd_kernel<<<blocks((int64_t)M * d), 256, 0, st>>>(stack, Lg, n, M, d, a, out); ++g_launches; }
 }
 
 // Q2B offset: o = min_t o_t * sigmoid(Z)  (Table 1), argmin ties -> lowest t (A19).
@@ -266,7 +266,7 @@ __global__ void q2b_off_fwd_kernel(const float *stack, const float *Z, int n, in
 }
 void launch_q2b_off_fwd(const float *stack, const float *Z, int n, int M, int d, float *sig, int8_t *amin,
                         float *out, cudaStream_t st) {
-  q2b_off_fwd_kernel<<<blocks((int64_t)M * d), 256, 0, st>>>(stack, Z, n, M, d, sig, amin, out);
+  { q2b_off_fwd_kernel<<<blocks((int64_t)M * d), 256, 0, st>>>(stack, Z, n, M, d, sig, amin, out); ++g_launches; }
 }
 
 __global__ void q2b_att_bwd_kernel(const float *stack, const float *a, const float *dout, int n, int M, int d,
@@ -289,7 +289,7 @@ __global__ void q2b_att_bwd_kernel(const float *stack, const float *a, const flo
 }
 void launch_q2b_att_bwd(const float *stack, const float *a, const float *dout, int n, int M, int d, float *dLg,
                         float *dstack, cudaStream_t st) {
-  q2b_att_bwd_kernel<<<blocks((int64_t)M * d), 256, 0, st>>>(stack, a, dout, n, M, d, dLg, dstack);
+  { q2b_att_bwd_kernel<<<blocks((int64_t)M * d), 256, 0, st>>>(stack, a, dout, n, M, d, dLg, dstack); ++g_launches; }
 }
 
 __global__ void q2b_off_bwd_kernel(const float *stack, const float *sig, const int8_t *amin, const float *dout, int n,
@@ -305,7 +305,7 @@ __global__ void q2b_off_bwd_kernel(const float *stack, const float *sig, const i
 }
 void launch_q2b_off_bwd(const float *stack, const float *sig, const int8_t *amin, const float *dout, int n, int M,
                         int d, float *dZ, float *dstack, cudaStream_t st) {
-  q2b_off_bwd_kernel<<<blocks((int64_t)M * d), 256, 0, st>>>(stack, sig, amin, dout, n, M, d, dZ, dstack);
+  { q2b_off_bwd_kernel<<<blocks((int64_t)M * d), 256, 0, st>>>(stack, sig, amin, dout, n, M, d, dZ, dstack); ++g_launches; }
 }
 
 // BetaE attention: w = softmax_t(Lg_t) (m per row), out = (sum w a_t, sum w b_t) (Table 1, A5).
@@ -332,7 +332,7 @@ __global__ void beta_att_fwd_kernel(const float *stack, const float *Lg, int n, 
 }
 void launch_beta_att_fwd(const float *stack, const float *Lg, int n, int M, int d, float *w, float *out,
                          cudaStream_t st) {
-  beta_att_fwd_kernel<<<blocks((int64_t)M * (d / 2)), 256, 0, st>>>(stack, Lg, n, M, d, w, out);
+  { beta_att_fwd_kernel<<<blocks((int64_t)M * (d / 2)), 256, 0, st>>>(stack, Lg, n, M, d, w, out); ++g_launches; }
 }
 
 __global__ void beta_att_bwd_kernel(const float *stack, const float *w, const float *dout, int n, int M, int d,
@@ -359,7 +359,7 @@ __global__ void beta_att_bwd_kernel(const float *stack, const float *w, const fl
 }
 void launch_beta_att_bwd(const float *stack, const float *w, const float *dout, int n, int M, int d, float *dLg,
                          float *dstack, cudaStream_t st) {
-  beta_att_bwd_kernel<<<blocks((int64_t)M * (d / 2)), 256, 0, st>>>(stack, w, dout, n, M, d, dLg, dstack);
+  { beta_att_bwd_kernel<<<blocks((int64_t)M * (d / 2)), 256, 0, st>>>(stack, w, dout, n, M, d, dLg, dstack); ++g_launches; }
 }
 
 // ------------------------------------------------------------ misc
@@ -368,7 +368,7 @@ __global__ void scale_copy_kernel(float *dst, const float *src, int64_t n, float
   if (e < n) dst[e] = src[e] * s;
 }
 void launch_scale_copy(float *dst, const float *src, int64_t n, float s, cudaStream_t st) {
-  if (n > 0) scale_copy_kernel<<<blocks(n), 256, 0, st>>>(dst, src, n, s);
+  if (n > 0) { scale_copy_kernel<<<blocks(n), 256, 0, st>>>(dst, src, n, s); ++g_launches; }
 }
 
 __global__ void gather_rows_kernel(float *dst, const float *src, const int64_t *rows, int n, int d) {
@@ -378,7 +378,7 @@ __global__ void gather_rows_kernel(float *dst, const float *src, const int64_t *
   dst[e] = src[rows[i] * (int64_t)d + k];
 }
 void launch_gather_rows(float *dst, const float *src, const int64_t *rows, int n, int d, cudaStream_t st) {
-  if (n > 0) gather_rows_kernel<<<blocks((int64_t)n * d), 256, 0, st>>>(dst, src, rows, n, d);
+  if (n > 0) { gather_rows_kernel<<<blocks((int64_t)n * d), 256, 0, st>>>(dst, src, rows, n, d); ++g_launches; }
 }
 __global__ void scatter_rows_kernel(float *dst, const float *src, const int64_t *rows, int n, int d) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -387,7 +387,7 @@ __global__ void scatter_rows_kernel(float *dst, const float *src, const int64_t 
   dst[rows[i] * (int64_t)d + k] = src[e];
 }
 void launch_scatter_rows(float *dst, const float *src, const int64_t *rows, int n, int d, cudaStream_t st) {
-  if (n > 0) scatter_rows_kernel<<<blocks((int64_t)n * d), 256, 0, st>>>(dst, src, rows, n, d);
+  if (n > 0) { scatter_rows_kernel<<<blocks((int64_t)n * d), 256, 0, st>>>(dst, src, rows, n, d); ++g_launches; }
 }
 
 // ids = concat(anchors (slot-major: position a*M + i), answers, negatives) -- the
@@ -412,8 +412,8 @@ void launch_ids_concat(const int64_t *anchors, int na, int M, const int64_t *ans
                        cudaStream_t st) {
   const int L = na * M + n_ans + K;
   if (L > 0)
-    ids_concat_kernel<<<blocks(L), 256, 0, st>>>(anchors, na, M, answers, n_ans, negs, K, world, ids, rows_out, bad,
-                                                 n_entities);
+    { ids_concat_kernel<<<blocks(L), 256, 0, st>>>(anchors, na, M, answers, n_ans, negs, K, world, ids, rows_out, bad,
+                                                 n_entities); ++g_launches; }
 }
 
 // occ[u*M + i] = relations[i][slot_u] (one relation occurrence per projection use).
@@ -428,7 +428,7 @@ __global__ void rel_occ_kernel(const int32_t *relations, int M, int nr, Slots4 s
 }
 void launch_rel_occ(const int32_t *relations, int M, int nr, Slots4 slots, int nproj, int n_rel, int32_t *occ,
                     int32_t *bad, cudaStream_t st) {
-  rel_occ_kernel<<<blocks((int64_t)nproj * M), 256, 0, st>>>(relations, M, nr, slots, nproj, n_rel, occ, bad);
+  { rel_occ_kernel<<<blocks((int64_t)nproj * M), 256, 0, st>>>(relations, M, nr, slots, nproj, n_rel, occ, bad); ++g_launches; }
 }
 
 }  // namespace kg

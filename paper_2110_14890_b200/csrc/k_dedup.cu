@@ -90,7 +90,7 @@ static void run_dedup(const int64_t *ids64, const int32_t *ids32, int L, int end
     cudaFuncSetAttribute(dedup_kernel<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     configured = true;
   }
-  dedup_kernel<ITEMS><<<1, kDedupThreads, bytes, st>>>(ids64, ids32, L, end_bit, uniq, inv, perm, seg, U_out);
+  { dedup_kernel<ITEMS><<<1, kDedupThreads, bytes, st>>>(ids64, ids32, L, end_bit, uniq, inv, perm, seg, U_out); ++g_launches; }
 }
 
 void launch_dedup(const int64_t *ids64, const int32_t *ids32, int L, int end_bit, int64_t *uniq, int32_t *inv,

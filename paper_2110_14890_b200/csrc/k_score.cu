@@ -567,11 +567,11 @@ template <class Mdl>
 static void launch_pair(const ScoreArgs &a, int nout, bool train, cudaStream_t st) {
   dim3 gf((a.K + 63) / 64, (a.M + 63) / 64);
   if (nout == 1) {
-    if (train) pair_fwd_kernel<Mdl, 1, true><<<gf, 256, 0, st>>>(a);
-    else pair_fwd_kernel<Mdl, 1, false><<<gf, 256, 0, st>>>(a);
+    if (train) { pair_fwd_kernel<Mdl, 1, true><<<gf, 256, 0, st>>>(a); ++g_launches; }
+    else { pair_fwd_kernel<Mdl, 1, false><<<gf, 256, 0, st>>>(a); ++g_launches; }
   } else {
-    if (train) pair_fwd_kernel<Mdl, 2, true><<<gf, 256, 0, st>>>(a);
-    else pair_fwd_kernel<Mdl, 2, false><<<gf, 256, 0, st>>>(a);
+    if (train) { pair_fwd_kernel<Mdl, 2, true><<<gf, 256, 0, st>>>(a); ++g_launches; }
+    else { pair_fwd_kernel<Mdl, 2, false><<<gf, 256, 0, st>>>(a); ++g_launches; }
   }
 }
 
@@ -589,9 +589,9 @@ void launch_pair_fwd(int kind, const ScoreArgs &a, int nout, bool train, cudaStr
 template <class Mdl>
 static void launch_bwd(const ScoreArgs &a, cudaStream_t st) {
   dim3 gq((a.U + 31) / 32, (a.NQ + 63) / 64);
-  pair_bwd_q_kernel<Mdl><<<gq, 256, 0, st>>>(a);
+  { pair_bwd_q_kernel<Mdl><<<gq, 256, 0, st>>>(a); ++g_launches; }
   dim3 gv((a.U + 31) / 32, (a.K + 63) / 64);
-  pair_bwd_v_kernel<Mdl><<<gv, 256, 0, st>>>(a);
+  { pair_bwd_v_kernel<Mdl><<<gv, 256, 0, st>>>(a); ++g_launches; }
 }
 
 void launch_pair_bwd(int kind, const ScoreArgs &a, cudaStream_t st) {
@@ -607,8 +607,8 @@ void launch_pair_bwd(int kind, const ScoreArgs &a, cudaStream_t st) {
 
 template <int KIND>
 static void launch_pos_k(const PosArgs &p, int nout, cudaStream_t st) {
-  if (nout == 1) pos_kernel<KIND, 1><<<p.M, 128, 0, st>>>(p);
-  else pos_kernel<KIND, 2><<<p.M, 128, 0, st>>>(p);
+  if (nout == 1) { pos_kernel<KIND, 1><<<p.M, 128, 0, st>>>(p); ++g_launches; }
+  else { pos_kernel<KIND, 2><<<p.M, 128, 0, st>>>(p); ++g_launches; }
 }
 
 void launch_pos(int kind, const PosArgs &p, int nout, cudaStream_t st) {
@@ -624,16 +624,16 @@ void launch_pos(int kind, const PosArgs &p, int nout, cudaStream_t st) {
 }
 
 void launch_beta_entity(const float *ent, const int64_t *rows, int K, int m, float *F, float *Cv, cudaStream_t st) {
-  if (K > 0) beta_entity_kernel<<<K, 128, 0, st>>>(ent, rows, K, m, F, Cv);
+  if (K > 0) { beta_entity_kernel<<<K, 128, 0, st>>>(ent, rows, K, m, F, Cv); ++g_launches; }
 }
 void launch_beta_query(const float *Q, int NQ, int m, float *QP, float *Cq, cudaStream_t st) {
-  beta_query_kernel<<<NQ, 128, 0, st>>>(Q, NQ, m, QP, Cq);
+  { beta_query_kernel<<<NQ, 128, 0, st>>>(Q, NQ, m, QP, Cq); ++g_launches; }
 }
 void launch_loss_finalize(const float *loss_pos, const float *loss_part, int M, int njt, double scale,
                           double *loss_out, int *flags, int64_t *t_dev, float *bc, double beta1, double beta2,
                           int apply, cudaStream_t st) {
-  loss_finalize_kernel<<<1, 256, 0, st>>>(loss_pos, loss_part, M, njt, scale, loss_out, flags, t_dev, bc,
-                                          beta1, beta2, apply);
+  { loss_finalize_kernel<<<1, 256, 0, st>>>(loss_pos, loss_part, M, njt, scale, loss_out, flags, t_dev, bc,
+                                          beta1, beta2, apply); ++g_launches; }
 }
 
 }  // namespace kg

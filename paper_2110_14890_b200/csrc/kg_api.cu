@@ -19,6 +19,10 @@
 
 using namespace kg;
 
+namespace kg {
+int64_t g_launches = 0;
+}
+
 namespace {
 
 // ------------------------------------------------------------------ plans
@@ -151,7 +155,10 @@ struct kg_handle {
   cudaEvent_t step_done = nullptr;
 
   int64_t stamp = 0;
-  int apply = 1, keep_grads = 0;
+  int apply = 1, keep_grads = 0, timing = 0;
+  cudaEvent_t sev[8] = {};
+  int64_t launches0 = 0;
+  int last_kernels = 0, last_gemms = 0, gemm_count = 0;
   int last_M = 0, last_K = 0, last_U_valid = 0;
   bool step_pending = false;
 };
@@ -306,6 +313,7 @@ kg_status gemm(kg_handle *h, bool ta, bool tb, int m, int n, int k, const float 
                float beta, float *C, int ldc) {
   if (m <= 0 || n <= 0) return KG_OK;
   const float one = 1.f;
+  h->gemm_count++;
   CKB(cublasSgemm(h->blas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, n, m, k, &one, B, ldb, A,
                   lda, &beta, C, ldc));
   return KG_OK;
@@ -561,6 +569,10 @@ kg_status ingest(kg_handle *h, const kg_batch *b, bool train, const Plan &plan) 
   return KG_OK;
 }
 
+void mark(kg_handle *h, int i) {
+  if (h->timing) cudaEventRecord(h->sev[i], h->st);
+}
+
 kg_status read_result(kg_handle *h, kg_step_info *info) {
   CK(cudaEventSynchronize(h->step_done));
   h->step_pending = false;
@@ -568,6 +580,13 @@ kg_status read_result(kg_handle *h, kg_step_info *info) {
     info->loss = h->hout->loss;
     info->n_touched = h->hout->U;
     info->step = h->hout->t;
+    info->kernels = h->last_kernels;
+    info->gemms = h->last_gemms;
+    for (int i = 0; i < 8; ++i) info->stage_ms[i] = 0.f;
+    if (h->timing) {
+      for (int i = 0; i < 7; ++i) CK(cudaEventElapsedTime(&info->stage_ms[i], h->sev[i], h->sev[i + 1]));
+      CK(cudaEventElapsedTime(&info->stage_ms[7], h->sev[0], h->sev[7]));
+    }
   }
   if (h->hout->flags[1]) return fail(h, KG_EINVAL, "an id or relation of the (device) batch was out of range; step not applied");
   if (h->hout->flags[0]) return fail(h, KG_ENONFINITE, "non-finite loss; step not applied");
@@ -627,6 +646,8 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
   if (cudaMallocHost(&h->hout, sizeof(kg_handle::HostOut)) != cudaSuccess) { kg_destroy(h); return KG_ENOMEM; }
   std::memset(h->hout, 0, sizeof(kg_handle::HostOut));
   if (cudaEventCreateWithFlags(&h->step_done, cudaEventDisableTiming) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
+  for (int i = 0; i < 8; ++i)
+    if (cudaEventCreate(&h->sev[i]) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
   if (cublasCreate(&h->blas) != CUBLAS_STATUS_SUCCESS) { kg_destroy(h); return KG_ECUDA; }
   cublasSetMathMode(h->blas, CUBLAS_PEDANTIC_MATH);   // true fp32, no TF32 (parity at 1e-5, A24)
   // device scalars
@@ -681,6 +702,9 @@ kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info)
   if (!(lr > 0.f)) return fail(h, KG_EINVAL, "lr must be > 0");
   StepBufs S;
   S.plan = make_plan(b->structure);
+  h->launches0 = g_launches;
+  h->gemm_count = 0;
+  mark(h, 0);
   if ((s = ingest(h, b, true, S.plan)) != KG_OK) return s;
   const Plan &p = S.plan;
   const int M = b->M, K = b->K, d = h->d, na = p.na, nr = p.nr;
@@ -705,8 +729,10 @@ kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info)
   launch_dedup(nullptr, h->rocc, Lr, h->rel_bits, h->runiq, h->rinv, h->rperm, h->rseg, h->rU, st);
 
   // a4-a7: fused gather + DAG forward
+  mark(h, 1);
   assign_buffers(h, S);
   if ((s = dag_forward(h, S)) != KG_OK) return s;
+  mark(h, 2);
 
   // a8-a10: scoring, Eq. 1, scoring backward
   const int U = (h->kind == KG_BETAE || h->kind == KG_ROTATE || h->kind == KG_COMPLEX) ? h->m : d;
@@ -733,7 +759,9 @@ kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info)
   if (K > 0) launch_pair_fwd(h->kind, sa, p.nout, true, st);
   launch_loss_finalize(h->loss_pos, h->loss_part, M, njt, 1.0 / ((double)M * h->world), h->loss_dev, h->flags,
                        h->t_dev, h->bc, h->cfg.beta1, h->cfg.beta2, h->apply, st);
+  mark(h, 3);
   if (K > 0) launch_pair_bwd(h->kind, sa, st);
+  mark(h, 4);
 
   // a11: DAG backward
   if ((s = dag_backward(h, S)) != KG_OK) return s;
@@ -745,12 +773,14 @@ kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info)
   }
 
   // a12-a14: relation rows reduce, sparse Adam on touched rows, dense Adam on theta_D
+  mark(h, 5);
   launch_rel_reduce(h->rseg, h->rperm, h->rU, Lr, h->RG, h->dr, h->RGU, st);
   launch_rel_stamp(h->runiq, h->rU, Lr, h->rel_seg_map, h->rel_stamp, h->stamp, st);
   if (h->apply || h->keep_grads)
     launch_sparse_adam(h->uniq, h->seg, h->perm, h->Udev, L, h->OG, d, h->world, h->t.ent, h->t.ent_m, h->t.ent_v,
                        h->keep_grads ? h->Gc : nullptr, lr, h->cfg.beta1, h->cfg.beta2, h->cfg.eps, h->bc, h->flags,
                        h->apply, st);
+  mark(h, 6);
   if (h->apply) {
     const double b1 = h->cfg.beta1, b2 = h->cfg.beta2, eps = h->cfg.eps;
     if (h->kind == KG_Q2B) {
@@ -768,6 +798,9 @@ kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info)
     launch_dense_adam(h->t.dense + h->w_off, h->t.dense_m + h->w_off, h->t.dense_v + h->w_off, h->gdense,
                       h->dense_size - h->w_off, lr, b1, b2, eps, h->bc, h->flags, st);
   }
+  mark(h, 7);
+  h->last_kernels = (int)(g_launches - h->launches0);
+  h->last_gemms = h->gemm_count;
   CK(cudaGetLastError());
   // results to pinned host memory (loss, flags, U, t)
   CK(cudaMemcpyAsync(&h->hout->loss, h->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -956,6 +989,7 @@ kg_status kg_set_apply(kg_handle *h, int32_t flags) {
   if (!h) return KG_EINVAL;
   h->apply = flags & 1;
   h->keep_grads = (flags >> 1) & 1;
+  h->timing = (flags >> 2) & 1;
   return KG_OK;
 }
 
@@ -972,6 +1006,8 @@ void kg_destroy(kg_handle *h) {
   }
   if (h->hout) cudaFreeHost(h->hout);
   if (h->step_done) cudaEventDestroy(h->step_done);
+  for (int i = 0; i < 8; ++i)
+    if (h->sev[i]) cudaEventDestroy(h->sev[i]);
   if (h->ws) cudaFree(h->ws);
   delete h;
 }

@@ -7,6 +7,8 @@ namespace kg {
 
 struct Slots4 { int s[4]; };
 
+extern int64_t g_launches;   // kernels of this library enqueued so far (per process)
+
 struct ScoreArgs {
   const float *Q = nullptr;     // [NQ][QF*U] query features (NQ = nout*M)
   int NQ = 0, M = 0, K = 0, Kp = 0, U = 0, d = 0;

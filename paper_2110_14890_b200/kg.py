@@ -46,7 +46,8 @@ class kg_batch(C.Structure):
 
 
 class kg_step_info(C.Structure):
-    _fields_ = [("loss", C.c_double), ("n_touched", C.c_int32), ("step", C.c_int64)]
+    _fields_ = [("loss", C.c_double), ("n_touched", C.c_int32), ("step", C.c_int64),
+                ("kernels", C.c_int32), ("gemms", C.c_int32), ("stage_ms", C.c_float * 8)]
 
 
 _H = C.c_void_p
@@ -134,8 +135,8 @@ class KGModel:
     def init_params(self, seed):
         check(kg_init_params(self.h, seed), self.h)
 
-    def set_apply(self, apply=True, keep_grads=False):
-        check(kg_set_apply(self.h, int(apply) | (int(keep_grads) << 1)), self.h)
+    def set_apply(self, apply=True, keep_grads=False, stage_timing=False):
+        check(kg_set_apply(self.h, int(apply) | (int(keep_grads) << 1) | (int(stage_timing) << 2)), self.h)
 
     @staticmethod
     def batch_struct(b, on_device=False) -> kg_batch:
