@@ -63,80 +63,135 @@ static AdamHyper hyper(double b1, double b2, double eps) {
   return AdamHyper{(float)b1, (float)(1.0 - b1), (float)b2, (float)(1.0 - b2), (float)eps};
 }
 
-// One warp per distinct row u: G_u = sum of its occurrence gradients in
-// ascending position order (anchors, answers, pool, A16), then Adam on
-// (p, m, v) of the row (local row = id / world).  Every touched row is updated,
+// ---------------------------------------------------------------- segment reduce
+// Occurrence rows X[L][w] are grouped by the dedup's sorted positions s (perm[s] =
+// occurrence, inv[perm[s]] = its distinct index u, seg[u] = first sorted position
+// of u).  Hot ids (Zipf anchors / relations) have long segments, so a segment is
+// cut into "pieces": a piece starts at every segment head and at every multiple
+// of kPiece.  Phase 1 sums each piece (kPiece independent loads in flight per
+// thread) into PS[piece start]; phase 2 sums the pieces of a segment in
+// ascending order.  The order of every sum is a fixed function of the sorted
+// positions: deterministic, no atomics (P:L343 merge).  Segments of length 1
+// skip phase 1.
+constexpr int kPiece = 16;
+
+__global__ void __launch_bounds__(128) seg_piece_kernel(const int32_t *perm, const int32_t *inv, const int32_t *seg,
+                                                        int L, const float *X, int w4, float *PS) {
+  __shared__ int s_row[kPiece], s_beg[kPiece], s_len[kPiece];
+  const int c0 = blockIdx.x * kPiece;
+  const int n = min(kPiece, L - c0);
+  if (threadIdx.x < n) {
+    const int s = c0 + threadIdx.x, r = perm[s], u = inv[r];
+    s_row[threadIdx.x] = r;
+    s_beg[threadIdx.x] = seg[u];
+    s_len[threadIdx.x] = seg[u + 1] - seg[u];
+  }
+  __syncthreads();
+  const float4 *X4 = reinterpret_cast<const float4 *>(X);
+  float4 *P4 = reinterpret_cast<float4 *>(PS);
+  for (int c = threadIdx.x; c < w4; c += blockDim.x) {
+    float4 v[kPiece];
+#pragma unroll
+    for (int i = 0; i < kPiece; ++i)
+      if (i < n && s_len[i] > 1) v[i] = X4[(int64_t)s_row[i] * w4 + c];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int start = -1;
+#pragma unroll
+    for (int i = 0; i < kPiece; ++i) {
+      if (i >= n || s_len[i] <= 1) continue;
+      const int s = c0 + i;
+      if (s == s_beg[i] || start < 0) {           // a new piece (segment head or chunk start)
+        if (start >= 0) P4[(int64_t)start * w4 + c] = acc;
+        acc = v[i];
+        start = s;
+      } else {
+        acc.x += v[i].x; acc.y += v[i].y; acc.z += v[i].z; acc.w += v[i].w;
+      }
+    }
+    if (start >= 0) P4[(int64_t)start * w4 + c] = acc;
+  }
+}
+
+__device__ __forceinline__ float4 segment_sum(const int32_t *perm, const float4 *X4, const float4 *P4, int s0, int s1,
+                                              int w4, int c) {
+  if (s1 - s0 == 1) return X4[(int64_t)perm[s0] * w4 + c];
+  float4 g = P4[(int64_t)s0 * w4 + c];
+  for (int s = (s0 / kPiece + 1) * kPiece; s < s1; s += kPiece) {
+    const float4 o = P4[(int64_t)s * w4 + c];
+    g.x += o.x; g.y += o.y; g.z += o.z; g.w += o.w;
+  }
+  return g;
+}
+
+// Phase 2 for theta_E: one thread per (distinct row u, float4 column): G_u, then Adam
+// on (p, m, v) of the row (local row = id / world).  Every touched row is updated,
 // including rows whose gradient is zero (A16).
 __global__ void __launch_bounds__(256) sparse_adam_kernel(const int64_t *uniq, const int32_t *seg,
                                                           const int32_t *perm, const int32_t *U_dev, const float *OG,
-                                                          int d, int world, float *ent, float *m, float *v,
-                                                          float *grad_out, float lr, AdamHyper hy,
+                                                          const float *PS, int d, int world, float *ent, float *m,
+                                                          float *v, float *grad_out, const float *lr_dev, AdamHyper hy,
                                                           const float *bc, const int *flags, int apply) {
-  const int u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (u >= *U_dev) return;
-  const int s0 = seg[u], s1 = seg[u + 1];
-  const bool upd = apply && !flags[0];
-  const int64_t row = uniq[u] / world;
-  const float bc1 = bc[0], bc2 = bc[1];
   const int d4 = d >> 2;
-  for (int c = lane; c < d4; c += 32) {
-    float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s = s0; s < s1; ++s) {
-      const float4 o = reinterpret_cast<const float4 *>(OG + (int64_t)perm[s] * d)[c];
-      g.x += o.x; g.y += o.y; g.z += o.z; g.w += o.w;
-    }
-    if (grad_out) reinterpret_cast<float4 *>(grad_out + (int64_t)u * d)[c] = g;
-    if (!upd) continue;
-    float4 *pp = reinterpret_cast<float4 *>(ent + row * d) + c;
-    float4 *mp = reinterpret_cast<float4 *>(m + row * d) + c;
-    float4 *vp = reinterpret_cast<float4 *>(v + row * d) + c;
-    float4 P = *pp, Mm = *mp, V = *vp;
-    adam4(P, Mm, V, g, lr, hy, bc1, bc2);
-    *pp = P; *mp = Mm; *vp = V;
-  }
-}
-
-void launch_sparse_adam(const int64_t *uniq, const int32_t *seg, const int32_t *perm, const int32_t *U_dev, int Lmax,
-                        const float *OG, int d, int world, float *ent, float *m, float *v, float *grad_out, float lr,
-                        double beta1, double beta2, double eps, const float *bc, const int *flags, int apply,
-                        cudaStream_t st) {
-  const int warps = 8;
-  { sparse_adam_kernel<<<(Lmax + warps - 1) / warps, warps * 32, 0, st>>>(uniq, seg, perm, U_dev, OG, d, world, ent, m,
-                                                                        v, grad_out, lr, hyper(beta1, beta2, eps), bc,
-                                                                        flags, apply); ++g_launches; }
-}
-
-// Relation occurrence gradients -> one row per distinct relation (fixed order).
-__global__ void __launch_bounds__(256) rel_reduce_kernel(const int32_t *seg, const int32_t *perm,
-                                                         const int32_t *U_dev, const float *RG, int dr, float *RGU) {
-  const int u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int u = (int)(e / d4), c = (int)(e - (int64_t)u * d4);
   if (u >= *U_dev) return;
-  const int s0 = seg[u], s1 = seg[u + 1];
-  for (int c = lane; c < dr; c += 32) {
-    float g = 0.f;
-    for (int s = s0; s < s1; ++s) g += RG[(int64_t)perm[s] * dr + c];
-    RGU[(int64_t)u * dr + c] = g;
-  }
+  const float4 g = segment_sum(perm, reinterpret_cast<const float4 *>(OG), reinterpret_cast<const float4 *>(PS),
+                               seg[u], seg[u + 1], d4, c);
+  if (grad_out) reinterpret_cast<float4 *>(grad_out)[(int64_t)u * d4 + c] = g;
+  if (!apply || flags[0]) return;
+  const int64_t off = (uniq[u] / world) * d4 + c;
+  float4 P = reinterpret_cast<float4 *>(ent)[off], Mm = reinterpret_cast<float4 *>(m)[off],
+         V = reinterpret_cast<float4 *>(v)[off];
+  adam4(P, Mm, V, g, *lr_dev, hy, bc[0], bc[1]);
+  reinterpret_cast<float4 *>(ent)[off] = P;
+  reinterpret_cast<float4 *>(m)[off] = Mm;
+  reinterpret_cast<float4 *>(v)[off] = V;
 }
-void launch_rel_reduce(const int32_t *seg, const int32_t *perm, const int32_t *U_dev, int Lmax, const float *RG,
-                       int dr, float *RGU, cudaStream_t st) {
-  { rel_reduce_kernel<<<(Lmax + 7) / 8, 256, 0, st>>>(seg, perm, U_dev, RG, dr, RGU); ++g_launches; }
+
+void launch_sparse_adam(const int64_t *uniq, const int32_t *seg, const int32_t *perm, const int32_t *inv,
+                        const int32_t *U_dev, int L, const float *OG, float *PS, int d, int world, float *ent,
+                        float *m, float *v, float *grad_out, const float *lr, double beta1, double beta2, double eps,
+                        const float *bc, const int *flags, int apply, cudaStream_t st) {
+  if (L <= 0) return;
+  { seg_piece_kernel<<<(L + kPiece - 1) / kPiece, 128, 0, st>>>(perm, inv, seg, L, OG, d / 4, PS); ++g_launches; }
+  const int64_t n = (int64_t)L * (d / 4);
+  { sparse_adam_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(uniq, seg, perm, U_dev, OG, PS, d, world, ent, m, v,
+                                                              grad_out, lr, hyper(beta1, beta2, eps), bc, flags,
+                                                              apply); ++g_launches; }
+}
+
+// Phase 2 for the relation rows: RGU[u] = sum of the occurrence rows of relation u.
+__global__ void __launch_bounds__(256) rel_reduce_kernel(const int32_t *seg, const int32_t *perm,
+                                                         const int32_t *U_dev, const float *RG, const float *PS,
+                                                         int dr, float *RGU) {
+  const int w4 = dr >> 2;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int u = (int)(e / w4), c = (int)(e - (int64_t)u * w4);
+  if (u >= *U_dev) return;
+  reinterpret_cast<float4 *>(RGU)[(int64_t)u * w4 + c] =
+      segment_sum(perm, reinterpret_cast<const float4 *>(RG), reinterpret_cast<const float4 *>(PS), seg[u],
+                  seg[u + 1], w4, c);
+}
+void launch_rel_reduce(const int32_t *seg, const int32_t *perm, const int32_t *inv, const int32_t *U_dev, int Lr,
+                       const float *RG, float *PS, int dr, float *RGU, cudaStream_t st) {
+  if (Lr <= 0) return;
+  { seg_piece_kernel<<<(Lr + kPiece - 1) / kPiece, 128, 0, st>>>(perm, inv, seg, Lr, RG, dr / 4, PS); ++g_launches; }
+  const int64_t n = (int64_t)Lr * (dr / 4);
+  { rel_reduce_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(seg, perm, U_dev, RG, PS, dr, RGU); ++g_launches; }
 }
 
 // rel_seg[r] = index of relation r's reduced gradient row, valid iff rel_stamp[r] == stamp.
 // (Avoids zeroing / reading a dense |R| x d gradient for the untouched relation rows.)
 __global__ void rel_stamp_kernel(const int64_t *uniq_rel, const int32_t *U_dev, int32_t *rel_seg,
-                                 int64_t *rel_stamp, int64_t stamp) {
+                                 int64_t *rel_stamp, const int64_t *stamp) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= *U_dev) return;
   const int64_t r = uniq_rel[u];
   rel_seg[r] = u;
-  rel_stamp[r] = stamp;
+  rel_stamp[r] = *stamp;
 }
 void launch_rel_stamp(const int64_t *uniq_rel, const int32_t *U_dev, int Lmax, int32_t *rel_seg, int64_t *rel_stamp,
-                      int64_t stamp, cudaStream_t st) {
+                      const int64_t *stamp, cudaStream_t st) {
   { rel_stamp_kernel<<<(Lmax + 255) / 256, 256, 0, st>>>(uniq_rel, U_dev, rel_seg, rel_stamp, stamp); ++g_launches; }
 }
 
@@ -144,9 +199,11 @@ void launch_rel_stamp(const int64_t *uniq_rel, const int32_t *U_dev, int Lmax, i
 __global__ void __launch_bounds__(256) dense_adam_rel_kernel(float *p, float *m, float *v, int R, int width,
                                                              const float *RGU, int rg_stride, int rg_col,
                                                              const int32_t *rel_seg, const int64_t *rel_stamp,
-                                                             int64_t stamp, float lr, AdamHyper hy,
-                                                             const float *bc, const int *flags) {
+                                                             const int64_t *stamp_dev, const float *lr_dev,
+                                                             AdamHyper hy, const float *bc, const int *flags) {
   if (flags[0]) return;
+  const int64_t stamp = *stamp_dev;
+  const float lr = *lr_dev;
   const int w4 = width >> 2;
   const int64_t n4 = (int64_t)R * w4;
   const float bc1 = bc[0], bc2 = bc[1];
@@ -162,17 +219,18 @@ __global__ void __launch_bounds__(256) dense_adam_rel_kernel(float *p, float *m,
   }
 }
 void launch_dense_adam_rel(float *p, float *m, float *v, int R, int width, const float *RGU, int rg_stride,
-                           int rg_col, const int32_t *rel_seg, const int64_t *rel_stamp, int64_t stamp, float lr,
-                           double beta1, double beta2, double eps, const float *bc, const int *flags, cudaStream_t st) {
+                           int rg_col, const int32_t *rel_seg, const int64_t *rel_stamp, const int64_t *stamp,
+                           const float *lr, double beta1, double beta2, double eps, const float *bc, const int *flags, cudaStream_t st) {
   const int64_t n4 = (int64_t)R * (width / 4);
   { dense_adam_rel_kernel<<<grid_for(n4, 256), 256, 0, st>>>(p, m, v, R, width, RGU, rg_stride, rg_col, rel_seg,
                                                            rel_stamp, stamp, lr, hyper(beta1, beta2, eps), bc, flags); ++g_launches; }
 }
 
 __global__ void __launch_bounds__(256) dense_adam_kernel(float *p, float *m, float *v, const float *g, int64_t n4,
-                                                         float lr, AdamHyper hy, const float *bc,
+                                                         const float *lr_dev, AdamHyper hy, const float *bc,
                                                          const int *flags) {
   if (flags[0]) return;
+  const float lr = *lr_dev;
   const float bc1 = bc[0], bc2 = bc[1];
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n4; e += (int64_t)gridDim.x * blockDim.x) {
     float4 P = reinterpret_cast<float4 *>(p)[e], Mm = reinterpret_cast<float4 *>(m)[e], V = reinterpret_cast<float4 *>(v)[e];
@@ -182,7 +240,7 @@ __global__ void __launch_bounds__(256) dense_adam_kernel(float *p, float *m, flo
     reinterpret_cast<float4 *>(v)[e] = V;
   }
 }
-void launch_dense_adam(float *p, float *m, float *v, const float *g, int64_t n, float lr, double beta1, double beta2,
+void launch_dense_adam(float *p, float *m, float *v, const float *g, int64_t n, const float *lr, double beta1, double beta2,
                        double eps, const float *bc, const int *flags, cudaStream_t st) {
   if (n <= 0) return;
   { dense_adam_kernel<<<grid_for(n / 4, 256), 256, 0, st>>>(p, m, v, g, n / 4, lr, hyper(beta1, beta2, eps), bc, flags); ++g_launches; }

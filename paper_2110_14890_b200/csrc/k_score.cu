@@ -18,6 +18,8 @@
 // 9 planes of m = d/2: [Pa | Pb | A | B | TA | TB | TAB | GA | GB] with
 // A = e(x_alpha), B = e(x_beta), Pa = psi(A) - psi(A+B), Pb = psi(B) - psi(A+B),
 // TA = psi'(A), TB = psi'(B), TAB = psi'(A+B), GA/GB = d e / d x (clamp mask).
+#include <algorithm>
+
 #include "kg_common.cuh"
 #include "kg_launch.h"
 
@@ -98,8 +100,12 @@ struct MCpx {  // ComplEx: -Re<q, conj(t)> = -sum(q_re t_re + q_im t_im) (A13)
 
 __device__ __forceinline__ float4 ld4(const float *p) { return *reinterpret_cast<const float4 *>(p); }
 
-// ---------------------------------------------------------------- pair_fwd
-template <class Mdl, int NOUT, bool TRAIN>
+// ---------------------------------------------------------------- pair_fwd (partial)
+// Tile 64 queries x 64 candidates, 256 threads (4x4 pairs each), units in chunks of
+// 16 staged in shared memory.  blockIdx.z selects a contiguous range of units
+// (split reduction: more CTAs than the 148 SMs even at B = 512); the raw partial
+// sums go to Dpart[z][t][i][j] and pair_epi_kernel adds them in the fixed order z.
+template <class Mdl, int NOUT>
 __global__ void __launch_bounds__(256) pair_fwd_kernel(ScoreArgs a) {
   constexpr int BI = 64, BJ = 64, KC = 16, PAD = 4;
   __shared__ __align__(16) float sQ[NOUT][Mdl::QF][KC][BI + PAD];
@@ -109,6 +115,7 @@ __global__ void __launch_bounds__(256) pair_fwd_kernel(ScoreArgs a) {
   const int i0 = blockIdx.y * BI, j0 = blockIdx.x * BJ;
   const int M = a.M, K = a.K, U = a.U;
   const int qstride = Mdl::QF * U;
+  const int ku0 = blockIdx.z * a.ups, ku1 = min(U, ku0 + a.ups);
   if (t < BJ) {
     const int j = j0 + t;
     sRow[t] = (j < K) ? (a.eidx ? a.eidx[j] : (int64_t)j) : 0;
@@ -122,7 +129,7 @@ __global__ void __launch_bounds__(256) pair_fwd_kernel(ScoreArgs a) {
       for (int y = 0; y < 4; ++y) acc[tt][x][y] = 0.f;
   __syncthreads();
 
-  for (int k0 = 0; k0 < U; k0 += KC) {
+  for (int k0 = ku0; k0 < ku1; k0 += KC) {
     constexpr int NQ4 = NOUT * Mdl::QF * BI * (KC / 4);
     for (int e = t; e < NQ4; e += 256) {
       const int q4 = e % (KC / 4);
@@ -131,7 +138,7 @@ __global__ void __launch_bounds__(256) pair_fwd_kernel(ScoreArgs a) {
       const int f = rest % Mdl::QF, tt = rest / Mdl::QF;
       const int i = i0 + row, k = k0 + q4 * 4;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (i < M && k < U) v = ld4(a.Q + (size_t)(tt * M + i) * qstride + f * U + k);
+      if (i < M && k < ku1) v = ld4(a.Q + (size_t)(tt * M + i) * qstride + f * U + k);
       sQ[tt][f][q4 * 4 + 0][row] = v.x; sQ[tt][f][q4 * 4 + 1][row] = v.y;
       sQ[tt][f][q4 * 4 + 2][row] = v.z; sQ[tt][f][q4 * 4 + 3][row] = v.w;
     }
@@ -142,7 +149,7 @@ __global__ void __launch_bounds__(256) pair_fwd_kernel(ScoreArgs a) {
       const int row = rest % BJ, f = rest / BJ;
       const int j = j0 + row, k = k0 + q4 * 4;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (j < K && k < U) v = ld4(a.E + sRow[row] * a.estride + (Mdl::EOFF + f) * U + k);
+      if (j < K && k < ku1) v = ld4(a.E + sRow[row] * a.estride + (Mdl::EOFF + f) * U + k);
       sE[f][q4 * 4 + 0][row] = v.x; sE[f][q4 * 4 + 1][row] = v.y;
       sE[f][q4 * 4 + 2][row] = v.z; sE[f][q4 * 4 + 3][row] = v.w;
     }
@@ -167,71 +174,92 @@ __global__ void __launch_bounds__(256) pair_fwd_kernel(ScoreArgs a) {
     }
     __syncthreads();
   }
-
-  // ---- epilogue
-  float inv_n[4], lrow[4];
+  float *out = a.Dpart + (size_t)blockIdx.z * NOUT * M * a.Kp;
 #pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    lrow[x] = 0.f;
-    inv_n[x] = 0.f;
-    const int i = i0 + ty + 16 * x;
-    if (TRAIN && i < M) {
-      int n = 0;
-      for (int w = 0; w < a.W; ++w) n += __popc(a.mask[(size_t)i * a.W + w]);
-      inv_n[x] = n ? 1.f / (float)n : 0.f;
+  for (int tt = 0; tt < NOUT; ++tt)
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int i = i0 + ty + 16 * x;
+      if (i >= M) continue;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int j = j0 + tx + 16 * b;
+        if (j < K) out[(size_t)(tt * M + i) * a.Kp + j] = acc[tt][x][b];
+      }
     }
+}
+
+// ---------------------------------------------------------------- pair epilogue
+// One CTA per query i: D_t = fin(sum_z Dpart), DNF min (A11), Eq. 1 adjoint
+// coefficients C[t][i][j] (train) or distances (score), the row's negative loss
+// term and sum_j C (BetaE), all reduced in a fixed order.
+template <class Mdl, int NOUT, bool TRAIN>
+__global__ void __launch_bounds__(256) pair_epi_kernel(ScoreArgs a) {
+  __shared__ float red[32];
+  const int i = blockIdx.x, M = a.M, K = a.K;
+  const size_t zs = (size_t)NOUT * M * a.Kp;
+  float inv_n = 0.f;
+  if (TRAIN) {
+    float n = 0.f;
+    for (int w = threadIdx.x; w < a.W; w += blockDim.x) n += (float)__popc(a.mask[(size_t)i * a.W + w]);
+    n = block_sum(n, red);
+    inv_n = n > 0.f ? 1.f / n : 0.f;
   }
+  float lsum = 0.f, csum[NOUT];
 #pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    const int i = i0 + ty + 16 * x;
-    if (i >= M) continue;
+  for (int tt = 0; tt < NOUT; ++tt) csum[tt] = 0.f;
+  const int jend = TRAIN ? a.Kp : K;
+  for (int j = threadIdx.x; j < jend; j += blockDim.x) {
+    if (j >= K) {
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int j = j0 + tx + 16 * b;
-      if (j >= a.Kp) continue;
-      if (j >= K) {  // zero padding columns of C (read by the backward kernels)
-        if (TRAIN)
+      for (int tt = 0; tt < NOUT; ++tt) a.C[(size_t)(tt * M + i) * a.Kp + j] = 0.f;
+      continue;
+    }
+    float D[NOUT];
 #pragma unroll
-          for (int tt = 0; tt < NOUT; ++tt) a.C[(size_t)(tt * M + i) * a.Kp + j] = 0.f;
-        continue;
+    for (int tt = 0; tt < NOUT; ++tt) {
+      float s = 0.f;
+      for (int z = 0; z < a.KS; ++z) s += a.Dpart[z * zs + (size_t)(tt * M + i) * a.Kp + j];
+      D[tt] = Mdl::fin(s, Mdl::kBeta ? a.Cq[tt * M + i] : 0.f, Mdl::kBeta ? a.Cv[j] : 0.f);
+    }
+    int tm = 0;
+    float Dm = D[0];
+    if (NOUT == 2 && D[1] < D[0]) { tm = 1; Dm = D[1]; }   // DNF min, ties -> lowest (A11)
+    if (TRAIN) {
+      const bool bit = (a.mask[(size_t)i * a.W + (j >> 5)] >> (j & 31)) & 1u;
+      float c = 0.f;
+      if (bit) {
+        c = -sigm_(a.gamma - Dm) * inv_n * a.scale;         // dl/dD_ij of Eq. 1 (A12)
+        lsum += softplusf_(a.gamma - Dm) * inv_n;
       }
-      float D[NOUT];
 #pragma unroll
-      for (int tt = 0; tt < NOUT; ++tt)
-        D[tt] = Mdl::fin(acc[tt][x][b], Mdl::kBeta ? a.Cq[tt * M + i] : 0.f, Mdl::kBeta ? a.Cv[j] : 0.f);
-      int tm = 0;
-      float Dm = D[0];
-      if (NOUT == 2 && D[1] < D[0]) { tm = 1; Dm = D[1]; }   // DNF min, ties -> lowest (A11)
-      if (TRAIN) {
-        const bool bit = (a.mask[(size_t)i * a.W + (j >> 5)] >> (j & 31)) & 1u;
-        float c = 0.f;
-        if (bit) {
-          c = -sigm_(a.gamma - Dm) * inv_n[x] * a.scale;     // dl/dD_ij of Eq. 1 (A12)
-          lrow[x] += softplusf_(a.gamma - Dm) * inv_n[x];
-        }
-#pragma unroll
-        for (int tt = 0; tt < NOUT; ++tt) {
-          float coef = (tt == tm) ? c : 0.f;
-          if (Mdl::kL2) coef = (coef != 0.f && D[tt] > 0.f) ? coef / D[tt] : 0.f;
-          a.C[(size_t)(tt * M + i) * a.Kp + j] = coef;
-        }
-        if (a.Dmin) a.Dmin[(size_t)i * K + j] = Dm;
-      } else {
-        a.Dmin[(size_t)i * a.ldo + j] = Dm;
+      for (int tt = 0; tt < NOUT; ++tt) {
+        float coef = (tt == tm) ? c : 0.f;
+        csum[tt] += coef;
+        if (Mdl::kL2) coef = (coef != 0.f && D[tt] > 0.f) ? coef / D[tt] : 0.f;
+        a.C[(size_t)(tt * M + i) * a.Kp + j] = coef;
       }
+      if (a.Dmin) a.Dmin[(size_t)i * K + j] = Dm;
+    } else {
+      a.Dmin[(size_t)i * a.ldo + j] = Dm;
     }
   }
   if (TRAIN) {
+    lsum = block_sum(lsum, red);
+    if (threadIdx.x == 0) a.loss_part[i] = lsum;
+    if (Mdl::kBeta) {
 #pragma unroll
-    for (int x = 0; x < 4; ++x) {
-      const float s = half_warp_sum<16>(lrow[x]);
-      const int i = i0 + ty + 16 * x;
-      if (tx == 0 && i < M) a.loss_part[(size_t)blockIdx.x * M + i] = s;
+      for (int tt = 0; tt < NOUT; ++tt) {
+        const float s = block_sum(csum[tt], red);
+        if (threadIdx.x == 0) a.Csum[tt * M + i] = s;
+      }
     }
   }
 }
 
-// ---------------------------------------------------------------- pair_bwd_q
+// ---------------------------------------------------------------- pair_bwd_q (partial)
+// out (r, k) 64 x 32, reduction over the pool j in chunks of 32; blockIdx.z
+// selects a contiguous j range (split reduction), partials to partQ[z].
 template <class Mdl>
 __global__ void __launch_bounds__(256) pair_bwd_q_kernel(ScoreArgs a) {
   constexpr int BR = 64, BK = 32, JC = 32, PAD = 4, QF = Mdl::QF, EF = Mdl::BQ_EF;
@@ -241,7 +269,8 @@ __global__ void __launch_bounds__(256) pair_bwd_q_kernel(ScoreArgs a) {
   const int t = threadIdx.x, tx = t & 7, ty = t >> 3;
   const int r0 = blockIdx.y * BR, k0 = blockIdx.x * BK;
   const int NQ = a.NQ, K = a.K, U = a.U, qstride = QF * U;
-  float qv[2][4][QF], acc[2][4][QF], rs[2] = {0.f, 0.f};
+  const int jb = blockIdx.z * a.jps, je = min(K, jb + a.jps);
+  float qv[2][4][QF], acc[2][4][QF];
 #pragma unroll
   for (int x = 0; x < 2; ++x)
 #pragma unroll
@@ -253,10 +282,10 @@ __global__ void __launch_bounds__(256) pair_bwd_q_kernel(ScoreArgs a) {
         acc[x][b][f] = 0.f;
       }
     }
-  for (int j0 = 0; j0 < K; j0 += JC) {
+  for (int j0 = jb; j0 < je; j0 += JC) {
     if (t < JC) {
       const int j = j0 + t;
-      sRow[t] = (j < K) ? (a.eidx ? a.eidx[j] : (int64_t)j) : 0;
+      sRow[t] = (j < je) ? (a.eidx ? a.eidx[j] : (int64_t)j) : 0;
     }
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
@@ -264,6 +293,7 @@ __global__ void __launch_bounds__(256) pair_bwd_q_kernel(ScoreArgs a) {
       const int r = r0 + row;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (r < NQ) v = ld4(a.C + (size_t)r * a.Kp + j0 + c4 * 4);   // Kp % 64 == 0, padding is 0
+      if (j0 + c4 * 4 >= je) v = make_float4(0.f, 0.f, 0.f, 0.f);
       sC[c4 * 4 + 0][row] = v.x; sC[c4 * 4 + 1][row] = v.y;
       sC[c4 * 4 + 2][row] = v.z; sC[c4 * 4 + 3][row] = v.w;
     }
@@ -274,7 +304,7 @@ __global__ void __launch_bounds__(256) pair_bwd_q_kernel(ScoreArgs a) {
       const int row = rest % JC, f = rest / JC;
       const int j = j0 + row, k = k0 + c4 * 4;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (j < K && k < U) v = ld4(a.E + sRow[row] * a.estride + (Mdl::BQ_EOFF + f) * U + k);
+      if (j < je && k < U) v = ld4(a.E + sRow[row] * a.estride + (Mdl::BQ_EOFF + f) * U + k);
       *reinterpret_cast<float4 *>(&sE[f][row][c4 * 4]) = v;
     }
     __syncthreads();
@@ -282,7 +312,7 @@ __global__ void __launch_bounds__(256) pair_bwd_q_kernel(ScoreArgs a) {
     for (int jj = 0; jj < JC; ++jj) {
       float c[2], ev[4][EF];
 #pragma unroll
-      for (int x = 0; x < 2; ++x) { c[x] = sC[jj][ty + 32 * x]; rs[x] += c[x]; }
+      for (int x = 0; x < 2; ++x) c[x] = sC[jj][ty + 32 * x];
 #pragma unroll
       for (int b = 0; b < 4; ++b)
 #pragma unroll
@@ -294,6 +324,7 @@ __global__ void __launch_bounds__(256) pair_bwd_q_kernel(ScoreArgs a) {
     }
     __syncthreads();
   }
+  float *out = a.partQ + (size_t)blockIdx.z * NQ * qstride;
 #pragma unroll
   for (int x = 0; x < 2; ++x)
 #pragma unroll
@@ -301,15 +332,26 @@ __global__ void __launch_bounds__(256) pair_bwd_q_kernel(ScoreArgs a) {
       const int r = r0 + ty + 32 * x, k = k0 + tx + 8 * b;
       if (r >= NQ || k >= U) continue;
 #pragma unroll
-      for (int f = 0; f < QF; ++f) {
-        float v = acc[x][b][f];
-        if (Mdl::kBeta) v += rs[x] * a.QP[(size_t)r * 2 * U + f * U + k];   // sum_j C_rj * (psi(a2)-psi(a2+b2))
-        a.dQ[(size_t)r * qstride + f * U + k] += v;
-      }
+      for (int f = 0; f < QF; ++f) out[(size_t)r * qstride + f * U + k] = acc[x][b][f];
     }
 }
 
-// ---------------------------------------------------------------- pair_bwd_v
+// dQ[r][f*U + k] += sum_z partQ[z] (+ BetaE: Csum[r] * QP[r][f][k]); dQ holds the positive term.
+template <bool BETA>
+__global__ void bwd_q_combine_kernel(ScoreArgs a, int qstride) {
+  const int64_t n = (int64_t)a.NQ * qstride;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  float v = 0.f;
+  for (int z = 0; z < a.JS; ++z) v += a.partQ[z * n + e];
+  if (BETA) v += a.Csum[e / qstride] * a.QP[e];
+  a.dQ[e] += v;
+}
+
+// ---------------------------------------------------------------- pair_bwd_v (partial)
+// out (j, k) 64 x 32, reduction over query rows r in chunks of 32; blockIdx.z
+// selects a contiguous r range, partial accumulators to partV[z] (and, BetaE,
+// the partial column sums of C to Cpart[z]).
 template <class Mdl>
 __global__ void __launch_bounds__(256) pair_bwd_v_kernel(ScoreArgs a) {
   constexpr int BJ = 64, BK = 32, RC = 32, PAD = 4, QF = Mdl::QF, EF = Mdl::BV_EF, AV = Mdl::AV;
@@ -318,6 +360,7 @@ __global__ void __launch_bounds__(256) pair_bwd_v_kernel(ScoreArgs a) {
   const int t = threadIdx.x, tx = t & 7, ty = t >> 3;
   const int j0 = blockIdx.y * BJ, k0 = blockIdx.x * BK;
   const int NQ = a.NQ, K = a.K, U = a.U, qstride = QF * U;
+  const int rb = blockIdx.z * a.rps, re = min(NQ, rb + a.rps);
   float ev[2][4][EF], acc[2][4][AV], cs[2] = {0.f, 0.f};
 #pragma unroll
   for (int x = 0; x < 2; ++x) {
@@ -328,18 +371,18 @@ __global__ void __launch_bounds__(256) pair_bwd_v_kernel(ScoreArgs a) {
       const int k = k0 + tx + 8 * b;
 #pragma unroll
       for (int f = 0; f < EF; ++f)
-        ev[x][b][f] = (j < K && k < U) ? a.E[er * a.estride + (Mdl::BV_EOFF + f) * U + k] : 0.f;
+        ev[x][b][f] = (!Mdl::kBeta && j < K && k < U) ? a.E[er * a.estride + (Mdl::BV_EOFF + f) * U + k] : 0.f;
 #pragma unroll
       for (int f = 0; f < AV; ++f) acc[x][b][f] = 0.f;
     }
   }
-  for (int r0 = 0; r0 < NQ; r0 += RC) {
+  for (int r0 = rb; r0 < re; r0 += RC) {
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       const int e = t + 256 * s, row = e >> 4, c4 = e & 15;
       const int r = r0 + row;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (r < NQ) v = ld4(a.C + (size_t)r * a.Kp + j0 + c4 * 4);
+      if (r < re) v = ld4(a.C + (size_t)r * a.Kp + j0 + c4 * 4);
       *reinterpret_cast<float4 *>(&sC[row][c4 * 4]) = v;
     }
     for (int e = t; e < QF * RC * (BK / 4); e += 256) {
@@ -348,7 +391,7 @@ __global__ void __launch_bounds__(256) pair_bwd_v_kernel(ScoreArgs a) {
       const int row = rest % RC, f = rest / RC;
       const int r = r0 + row, k = k0 + c4 * 4;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (r < NQ && k < U) v = ld4(a.Q + (size_t)r * qstride + f * U + k);
+      if (r < re && k < U) v = ld4(a.Q + (size_t)r * qstride + f * U + k);
       *reinterpret_cast<float4 *>(&sQ[f][row][c4 * 4]) = v;
     }
     __syncthreads();
@@ -368,24 +411,55 @@ __global__ void __launch_bounds__(256) pair_bwd_v_kernel(ScoreArgs a) {
     }
     __syncthreads();
   }
+  const size_t zs = (size_t)K * AV * U;
+  float *out = a.partV + blockIdx.z * zs;
 #pragma unroll
-  for (int x = 0; x < 2; ++x)
+  for (int x = 0; x < 2; ++x) {
+    const int j = j0 + ty + 32 * x;
+    if (j >= K) continue;
+    if (Mdl::kBeta && blockIdx.x == 0 && tx == 0) a.Cpart[(size_t)blockIdx.z * K + j] = cs[x];
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int j = j0 + ty + 32 * x, k = k0 + tx + 8 * b;
-      if (j >= K || k >= U) continue;
-      float *out = a.dV + (size_t)j * a.d;
-      if (Mdl::kBeta) {
-        // ev = [A, B, TA, TB, TAB, GA, GB]; acc = [sum C a2, sum C b2]; cs = sum C
-        const float A = ev[x][b][0], B = ev[x][b][1], S1 = acc[x][b][0], S2 = acc[x][b][1], Cj = cs[x];
-        const float S = (A + B) * Cj - S1 - S2;
-        out[k] = (ev[x][b][2] * (A * Cj - S1) - ev[x][b][4] * S) * ev[x][b][5];
-        out[U + k] = (ev[x][b][3] * (B * Cj - S2) - ev[x][b][4] * S) * ev[x][b][6];
-      } else {
+      const int k = k0 + tx + 8 * b;
+      if (k >= U) continue;
 #pragma unroll
-        for (int f = 0; f < Mdl::OUTF; ++f) out[f * U + k] = acc[x][b][f];
-      }
+      for (int f = 0; f < AV; ++f) out[(size_t)j * AV * U + f * U + k] = acc[x][b][f];
     }
+  }
+}
+
+// Raw-row gradient of pool entry j: sum_z partials (+ BetaE epilogue with the
+// entity features [A, B, TA, TB, TAB, GA, GB] = F planes 2..8).
+template <class Mdl>
+__global__ void bwd_v_combine_kernel(ScoreArgs a) {
+  constexpr int AV = Mdl::AV;
+  const int U = a.U, K = a.K;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)K * U) return;
+  const int j = (int)(e / U), k = (int)(e - (int64_t)j * U);
+  const size_t zs = (size_t)K * AV * U;
+  float acc[AV];
+#pragma unroll
+  for (int f = 0; f < AV; ++f) {
+    float s = 0.f;
+    for (int z = 0; z < a.RS; ++z) s += a.partV[z * zs + (size_t)j * AV * U + f * U + k];
+    acc[f] = s;
+  }
+  float *out = a.dV + (size_t)j * a.d;
+  if (Mdl::kBeta) {
+    float Cj = 0.f;
+    for (int z = 0; z < a.RS; ++z) Cj += a.Cpart[(size_t)z * K + j];
+    const float *Fr = a.E + (size_t)j * a.estride;
+    const float A = Fr[2 * U + k], B = Fr[3 * U + k], TA = Fr[4 * U + k], TB = Fr[5 * U + k],
+                TAB = Fr[6 * U + k], GA = Fr[7 * U + k], GB = Fr[8 * U + k];
+    const float S1 = acc[0], S2 = acc[AV - 1];
+    const float S = (A + B) * Cj - S1 - S2;
+    out[k] = (TA * (A * Cj - S1) - TAB * S) * GA;
+    out[U + k] = (TB * (B * Cj - S2) - TAB * S) * GB;
+  } else {
+#pragma unroll
+    for (int f = 0; f < Mdl::OUTF; ++f) out[f * U + k] = acc[f];
+  }
 }
 
 // ---------------------------------------------------------------- positives
@@ -563,15 +637,31 @@ __global__ void __launch_bounds__(256) loss_finalize_kernel(const float *loss_po
 }
 
 // ---------------------------------------------------------------- launchers
+// Split counts: enough CTAs for ~4 per SM (148 SMs), bounded by the partial
+// buffers and by whole chunks per split.
+static int split_for(int tiles, int chunks, int64_t cap_floats, int64_t per_split_floats) {
+  int s = (4 * 148 + tiles - 1) / tiles;
+  s = std::max(1, std::min(s, std::min(8, chunks)));
+  while (s > 1 && (int64_t)s * per_split_floats > cap_floats) --s;
+  return s;
+}
+
 template <class Mdl>
-static void launch_pair(const ScoreArgs &a, int nout, bool train, cudaStream_t st) {
-  dim3 gf((a.K + 63) / 64, (a.M + 63) / 64);
+static void launch_pair(ScoreArgs a, int nout, bool train, cudaStream_t st) {
+  const int tiles = ((a.K + 63) / 64) * ((a.M + 63) / 64);
+  const int chunks = (a.U + 15) / 16;
+  a.KS = split_for(tiles, chunks, a.cap_D, (int64_t)nout * a.M * a.Kp);
+  a.ups = ((chunks + a.KS - 1) / a.KS) * 16;
+  a.KS = (a.U + a.ups - 1) / a.ups;
+  dim3 gf((a.K + 63) / 64, (a.M + 63) / 64, a.KS);
   if (nout == 1) {
-    if (train) { pair_fwd_kernel<Mdl, 1, true><<<gf, 256, 0, st>>>(a); ++g_launches; }
-    else { pair_fwd_kernel<Mdl, 1, false><<<gf, 256, 0, st>>>(a); ++g_launches; }
+    { pair_fwd_kernel<Mdl, 1><<<gf, 256, 0, st>>>(a); ++g_launches; }
+    if (train) { pair_epi_kernel<Mdl, 1, true><<<a.M, 256, 0, st>>>(a); ++g_launches; }
+    else { pair_epi_kernel<Mdl, 1, false><<<a.M, 256, 0, st>>>(a); ++g_launches; }
   } else {
-    if (train) { pair_fwd_kernel<Mdl, 2, true><<<gf, 256, 0, st>>>(a); ++g_launches; }
-    else { pair_fwd_kernel<Mdl, 2, false><<<gf, 256, 0, st>>>(a); ++g_launches; }
+    { pair_fwd_kernel<Mdl, 2><<<gf, 256, 0, st>>>(a); ++g_launches; }
+    if (train) { pair_epi_kernel<Mdl, 2, true><<<a.M, 256, 0, st>>>(a); ++g_launches; }
+    else { pair_epi_kernel<Mdl, 2, false><<<a.M, 256, 0, st>>>(a); ++g_launches; }
   }
 }
 
@@ -587,21 +677,42 @@ void launch_pair_fwd(int kind, const ScoreArgs &a, int nout, bool train, cudaStr
 }
 
 template <class Mdl>
-static void launch_bwd(const ScoreArgs &a, cudaStream_t st) {
-  dim3 gq((a.U + 31) / 32, (a.NQ + 63) / 64);
-  { pair_bwd_q_kernel<Mdl><<<gq, 256, 0, st>>>(a); ++g_launches; }
-  dim3 gv((a.U + 31) / 32, (a.K + 63) / 64);
-  { pair_bwd_v_kernel<Mdl><<<gv, 256, 0, st>>>(a); ++g_launches; }
+static void launch_bwd(ScoreArgs a, cudaStream_t st, cudaStream_t st2) {
+  const int qstride = Mdl::QF * a.U;
+  // dQ: reduction over the pool
+  {
+    const int tiles = ((a.U + 31) / 32) * ((a.NQ + 63) / 64);
+    const int chunks = (a.K + 31) / 32;
+    a.JS = split_for(tiles, chunks, a.cap_Q, (int64_t)a.NQ * qstride);
+    a.jps = ((chunks + a.JS - 1) / a.JS) * 32;
+    a.JS = (a.K + a.jps - 1) / a.jps;
+    dim3 g((a.U + 31) / 32, (a.NQ + 63) / 64, a.JS);
+    { pair_bwd_q_kernel<Mdl><<<g, 256, 0, st>>>(a); ++g_launches; }
+    const int64_t n = (int64_t)a.NQ * qstride;
+    { bwd_q_combine_kernel<Mdl::kBeta><<<(int)((n + 255) / 256), 256, 0, st>>>(a, qstride); ++g_launches; }
+  }
+  // dV: reduction over the query rows (independent of dQ: second stream)
+  {
+    const int tiles = ((a.U + 31) / 32) * ((a.K + 63) / 64);
+    const int chunks = (a.NQ + 31) / 32;
+    a.RS = split_for(tiles, chunks, a.cap_V, (int64_t)a.K * Mdl::AV * a.U);
+    a.rps = ((chunks + a.RS - 1) / a.RS) * 32;
+    a.RS = (a.NQ + a.rps - 1) / a.rps;
+    dim3 g((a.U + 31) / 32, (a.K + 63) / 64, a.RS);
+    { pair_bwd_v_kernel<Mdl><<<g, 256, 0, st2>>>(a); ++g_launches; }
+    const int64_t n = (int64_t)a.K * a.U;
+    { bwd_v_combine_kernel<Mdl><<<(int)((n + 255) / 256), 256, 0, st2>>>(a); ++g_launches; }
+  }
 }
 
-void launch_pair_bwd(int kind, const ScoreArgs &a, cudaStream_t st) {
+void launch_pair_bwd(int kind, const ScoreArgs &a, cudaStream_t st, cudaStream_t st2) {
   switch (kind) {
-    case GQE: case TRANSE: launch_bwd<ML2>(a, st); break;
-    case Q2B: launch_bwd<MBox>(a, st); break;
-    case BETAE: launch_bwd<MBeta>(a, st); break;
-    case ROTATE: launch_bwd<MRot>(a, st); break;
-    case DISTMULT: launch_bwd<MDot>(a, st); break;
-    case COMPLEX: launch_bwd<MCpx>(a, st); break;
+    case GQE: case TRANSE: launch_bwd<ML2>(a, st, st2); break;
+    case Q2B: launch_bwd<MBox>(a, st, st2); break;
+    case BETAE: launch_bwd<MBeta>(a, st, st2); break;
+    case ROTATE: launch_bwd<MRot>(a, st, st2); break;
+    case DISTMULT: launch_bwd<MDot>(a, st, st2); break;
+    case COMPLEX: launch_bwd<MCpx>(a, st, st2); break;
   }
 }
 

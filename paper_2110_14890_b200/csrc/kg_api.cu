@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -125,7 +126,7 @@ struct kg_handle {
   int64_t *runiq = nullptr;
   int32_t *rel_seg_map = nullptr;
   int64_t *rel_stamp = nullptr;
-  float *OG = nullptr, *RG = nullptr, *RGU = nullptr, *Gc = nullptr, *gdense = nullptr;
+  float *OG = nullptr, *RG = nullptr, *RGU = nullptr, *Gc = nullptr, *gdense = nullptr, *PS = nullptr, *PSr = nullptr;
   float *Q = nullptr, *dQ = nullptr, *C = nullptr, *Dmin = nullptr, *Dpos = nullptr, *loss_part = nullptr,
         *loss_pos = nullptr;
   float *F = nullptr, *Cv = nullptr, *QP = nullptr, *Cq = nullptr;
@@ -140,6 +141,20 @@ struct kg_handle {
   float *pX = nullptr, *pH1 = nullptr, *pH2 = nullptr, *pZp1 = nullptr, *pdZ = nullptr, *pdH2 = nullptr,
         *pdH1 = nullptr, *pZ = nullptr, *pdX = nullptr;
   float *Dscore = nullptr;
+  float *Dpart = nullptr, *partQ = nullptr, *partV = nullptr, *Cpart = nullptr, *Csum = nullptr;
+  int64_t cap_D = 0, cap_Q = 0, cap_V = 0;
+  cudaStream_t st2 = nullptr, st_cap = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_fork2 = nullptr, ev_join = nullptr;
+  float *lr_dev = nullptr;
+  int64_t *stamp_dev = nullptr;
+  struct GraphEntry {
+    int structure, M, K, flags, kernels, gemms;
+    cudaGraphExec_t exec;
+  };
+  std::vector<GraphEntry> graphs;
+  bool use_graphs = true;
+  void *blas_ws = nullptr;
+  int flag_key() const { return apply | (keep_grads << 1) | (timing << 2); }
 
   // pinned staging (double-buffered) + host mirrors of the step results
   char *pin[2] = {nullptr, nullptr};
@@ -265,13 +280,28 @@ void carve(kg_handle *h, Arena &A) {
   h->RGU = A.take<float>((int64_t)h->Lrx * h->dr);
   h->OG = A.take<float>((int64_t)h->Lx * d);
   h->Gc = A.take<float>((int64_t)h->Lx * d);
+  h->PS = A.take<float>((int64_t)h->Lx * d);
+  h->PSr = A.take<float>((int64_t)h->Lrx * h->dr);
   h->gdense = A.take<float>(h->dense_size - h->w_off);
   h->Q = A.take<float>((int64_t)NQ * dq);
   h->dQ = A.take<float>((int64_t)NQ * dq);
   h->C = A.take<float>((int64_t)NQ * h->Kpx);
   h->Dmin = A.take<float>((int64_t)Mx * Kx);
   h->Dpos = A.take<float>(Mx);
-  h->loss_part = A.take<float>((int64_t)((Kx + 63) / 64) * Mx);
+  h->loss_part = A.take<float>(Mx);
+  {
+    const int64_t KK = std::max(h->Kpx, (int)align_up(std::max(h->Cx, 1), 4));
+    const int64_t one = 2LL * Mx * KK;
+    int64_t ks = std::max<int64_t>(1, std::min<int64_t>(8, (64LL << 20) / std::max<int64_t>(one, 1)));
+    h->cap_D = one * ks;
+    h->cap_Q = 2LL * Mx * dq * 8;
+    h->cap_V = (int64_t)std::max(Kx, h->Cx) * d * 8;
+    h->Dpart = A.take<float>(h->cap_D);
+    h->partQ = A.take<float>(h->cap_Q);
+    h->partV = A.take<float>(h->cap_V);
+    h->Cpart = A.take<float>(8LL * std::max(Kx, h->Cx));
+    h->Csum = A.take<float>(NQ);
+  }
   h->loss_pos = A.take<float>(Mx);
   if (h->kind == KG_BETAE) {
     h->F = A.take<float>((int64_t)std::max(Kx, h->Cx) * 9 * h->m);
@@ -282,6 +312,9 @@ void carve(kg_handle *h, Arena &A) {
   h->loss_dev = A.take<double>(1);
   h->flags = A.take<int>(2);
   h->t_dev = A.take<int64_t>(1);
+  h->lr_dev = A.take<float>(4);
+  h->stamp_dev = A.take<int64_t>(1);
+  h->blas_ws = A.take<char>(32 << 20);
   h->bc = A.take<float>(2);
   for (int i = 0; i < 6; ++i) {
     h->nval[i] = A.take<float>((int64_t)Mx * dq);
@@ -510,7 +543,7 @@ kg_status check_state(kg_handle *h) {
 }
 
 // Validate a batch and stage host inputs into the workspace (H2D on the bound stream).
-kg_status ingest(kg_handle *h, const kg_batch *b, bool train, const Plan &plan) {
+kg_status ingest(kg_handle *h, const kg_batch *b, bool train, const Plan &plan, float lr = 0.f) {
   const int M = b->M, K = train ? b->K : 0, na = plan.na, nr = plan.nr;
   const int W = (K + 31) / 32;
   if (M < 1 || M > h->Mx) return fail(h, KG_EINVAL, "M out of range [1, max_M]");
@@ -521,6 +554,17 @@ kg_status ingest(kg_handle *h, const kg_batch *b, bool train, const Plan &plan) 
   const size_t sz_a = (size_t)M * na * 8, sz_r = (size_t)M * nr * 4, sz_ans = train ? (size_t)M * 8 : 0,
                sz_n = (size_t)K * 8, sz_m = (size_t)M * W * 4;
   if (b->on_device) {
+    if (train) {   // step scalars (lr, stamp) through the pinned staging buffer
+      const int cur = h->pin_cur;
+      h->pin_cur ^= 1;
+      CK(cudaEventSynchronize(h->pin_ev[cur]));
+      char *p = h->pin[cur];
+      std::memcpy(p, &lr, sizeof(float));
+      std::memcpy(p + 8, &h->stamp, sizeof(int64_t));
+      CK(cudaMemcpyAsync(h->lr_dev, p, sizeof(float), cudaMemcpyHostToDevice, h->st));
+      CK(cudaMemcpyAsync(h->stamp_dev, p + 8, sizeof(int64_t), cudaMemcpyHostToDevice, h->st));
+      CK(cudaEventRecord(h->pin_ev[cur], h->st));
+    }
     CK(cudaMemcpyAsync(h->b_anchors, b->anchors, sz_a, cudaMemcpyDeviceToDevice, h->st));
     CK(cudaMemcpyAsync(h->b_rels, b->relations, sz_r, cudaMemcpyDeviceToDevice, h->st));
     if (train) {
@@ -543,7 +587,7 @@ kg_status ingest(kg_handle *h, const kg_batch *b, bool train, const Plan &plan) 
     for (int j = 0; j < K; ++j)
       if (b->negatives[j] < 0 || b->negatives[j] >= h->n_ent) return fail(h, KG_EINVAL, "negative id out of range");
   }
-  const size_t total = sz_a + sz_r + sz_ans + sz_n + sz_m + 5 * 256;
+  const size_t total = sz_a + sz_r + sz_ans + sz_n + sz_m + 7 * 256;
   if (total > h->pin_bytes) return fail(h, KG_EINVAL, "batch exceeds staging capacity");
   const int cur = h->pin_cur;
   h->pin_cur ^= 1;
@@ -558,6 +602,10 @@ kg_status ingest(kg_handle *h, const kg_batch *b, bool train, const Plan &plan) 
     return KG_OK;
   };
   kg_status s;
+  if (train) {
+    if ((s = put(&lr, sizeof(float), h->lr_dev)) != KG_OK) return s;
+    if ((s = put(&h->stamp, sizeof(int64_t), h->stamp_dev)) != KG_OK) return s;
+  }
   if ((s = put(b->anchors, sz_a, h->b_anchors)) != KG_OK) return s;
   if ((s = put(b->relations, sz_r, h->b_rels)) != KG_OK) return s;
   if (train) {
@@ -570,7 +618,8 @@ kg_status ingest(kg_handle *h, const kg_batch *b, bool train, const Plan &plan) 
 }
 
 void mark(kg_handle *h, int i) {
-  if (h->timing) cudaEventRecord(h->sev[i], h->st);
+  // external: inside a stream capture this becomes an event-record node of the graph
+  if (h->timing) cudaEventRecordWithFlags(h->sev[i], h->st, cudaEventRecordExternal);
 }
 
 kg_status read_result(kg_handle *h, kg_step_info *info) {
@@ -649,6 +698,13 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
   for (int i = 0; i < 8; ++i)
     if (cudaEventCreate(&h->sev[i]) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
   if (cublasCreate(&h->blas) != CUBLAS_STATUS_SUCCESS) { kg_destroy(h); return KG_ECUDA; }
+  if (cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&h->st_cap, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_fork2, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
+  if (cublasSetWorkspace(h->blas, h->blas_ws, 32 << 20) != CUBLAS_STATUS_SUCCESS) { kg_destroy(h); return KG_ECUDA; }
+  if (const char *e = std::getenv("KG_NO_GRAPH")) h->use_graphs = !(e[0] == '1');
   cublasSetMathMode(h->blas, CUBLAS_PEDANTIC_MATH);   // true fp32, no TF32 (parity at 1e-5, A24)
   // device scalars
   if (cudaMemset(h->ws, 0, h->ws_bytes) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
@@ -692,33 +748,24 @@ kg_status kg_init_params(kg_handle *h, uint64_t seed) {
   return KG_OK;
 }
 
-kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info) {
-  kg_status s = check_state(h);
-  if (s) return s;
-  if (!b) return fail(h, KG_EINVAL, "null batch");
-  if (b->structure < KG_1P || b->structure > KG_UP) return fail(h, KG_EINVAL, "bad structure");
-  if (single_hop(h->kind) && b->structure != KG_1P)
-    return fail(h, KG_EUNSUPPORTED, "single-hop models accept only 1p (Table 2, P:L55)");
-  if (!(lr > 0.f)) return fail(h, KG_EINVAL, "lr must be > 0");
-  StepBufs S;
-  S.plan = make_plan(b->structure);
-  h->launches0 = g_launches;
-  h->gemm_count = 0;
-  mark(h, 0);
-  if ((s = ingest(h, b, true, S.plan)) != KG_OK) return s;
+}  // extern "C"
+
+namespace {
+
+// Everything of one step after ingest: enqueued on h->st (directly, or while
+// h->st is a capturing stream -- the sequence is then replayed as a CUDA graph).
+kg_status enqueue_step(kg_handle *h, StepBufs &S) {
+  kg_status s;
   const Plan &p = S.plan;
-  const int M = b->M, K = b->K, d = h->d, na = p.na, nr = p.nr;
-  S.M = M; S.K = K; S.Kp = (int)align_up(std::max(K, 1), 64); S.NQ = p.nout * M;
+  const int M = S.M, K = S.K, d = h->d, na = p.na, nr = p.nr;
   const int L = na * M + M + K, Lr = p.nproj * M;
   cudaStream_t st = h->st;
-  h->stamp++;
-  h->last_M = M; h->last_K = K;
-
-  // a2: ids + dedup; relation occurrences + dedup
+  mark(h, 0);
+  // a2: ids (fused gather indices) on the main stream; dedup of entities and relations
+  // on the side stream -- only the sparse update at the end needs them
   CK(cudaMemsetAsync(h->flags, 0, 2 * sizeof(int), st));
   launch_ids_concat(h->b_anchors, na, M, h->b_answers, M, h->b_negs, K, h->world, h->ids, h->rows, h->flags + 1,
                     h->n_ent, st);
-  launch_dedup(h->ids, nullptr, L, h->ent_bits, h->uniq, h->inv, h->perm, h->seg, h->Udev, st);
   Slots4 sl{{0, 0, 0, 0}};
   {
     int u = 0;
@@ -726,7 +773,10 @@ kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info)
       if (p.n[ni].type == 0) sl.s[u++] = p.n[ni].rel;
   }
   launch_rel_occ(h->b_rels, M, nr, sl, p.nproj, h->R, h->rocc, h->flags + 1, st);
-  launch_dedup(nullptr, h->rocc, Lr, h->rel_bits, h->runiq, h->rinv, h->rperm, h->rseg, h->rU, st);
+  CK(cudaEventRecord(h->ev_fork, st));
+  CK(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
+  launch_dedup(h->ids, nullptr, L, h->ent_bits, h->uniq, h->inv, h->perm, h->seg, h->Udev, h->st2);
+  launch_dedup(nullptr, h->rocc, Lr, h->rel_bits, h->runiq, h->rinv, h->rperm, h->rseg, h->rU, h->st2);
 
   // a4-a7: fused gather + DAG forward
   mark(h, 1);
@@ -754,13 +804,21 @@ kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info)
   sa.mask = h->b_mask; sa.W = (K + 31) / 32; sa.Cq = h->Cq; sa.Cv = h->Cv; sa.QP = h->QP;
   sa.gamma = h->cfg.gamma; sa.alpha = h->cfg.box_alpha; sa.scale = scale;
   sa.C = h->C; sa.Dmin = h->Dmin; sa.loss_part = h->loss_part; sa.dQ = h->dQ;
+  sa.Dpart = h->Dpart; sa.partQ = h->partQ; sa.partV = h->partV; sa.Cpart = h->Cpart; sa.Csum = h->Csum;
+  sa.cap_D = h->cap_D; sa.cap_Q = h->cap_Q; sa.cap_V = h->cap_V;
   sa.dV = h->OG + (int64_t)(na * M + M) * d;
-  const int njt = (K + 63) / 64;
+  const int njt = K > 0 ? 1 : 0;
   if (K > 0) launch_pair_fwd(h->kind, sa, p.nout, true, st);
   launch_loss_finalize(h->loss_pos, h->loss_part, M, njt, 1.0 / ((double)M * h->world), h->loss_dev, h->flags,
                        h->t_dev, h->bc, h->cfg.beta1, h->cfg.beta2, h->apply, st);
   mark(h, 3);
-  if (K > 0) launch_pair_bwd(h->kind, sa, st);
+  if (K > 0) {
+    // dV (pool rows) on the side stream, concurrently with dQ and the DAG backward
+    CK(cudaEventRecord(h->ev_fork2, st));
+    CK(cudaStreamWaitEvent(h->st2, h->ev_fork2, 0));
+  }
+  if (K > 0) launch_pair_bwd(h->kind, sa, st, h->st2);
+  CK(cudaEventRecord(h->ev_join, h->st2));
   mark(h, 4);
 
   // a11: DAG backward
@@ -773,41 +831,104 @@ kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info)
   }
 
   // a12-a14: relation rows reduce, sparse Adam on touched rows, dense Adam on theta_D
+  CK(cudaStreamWaitEvent(st, h->ev_join, 0));
   mark(h, 5);
-  launch_rel_reduce(h->rseg, h->rperm, h->rU, Lr, h->RG, h->dr, h->RGU, st);
-  launch_rel_stamp(h->runiq, h->rU, Lr, h->rel_seg_map, h->rel_stamp, h->stamp, st);
+  launch_rel_reduce(h->rseg, h->rperm, h->rinv, h->rU, Lr, h->RG, h->PSr, h->dr, h->RGU, st);
+  launch_rel_stamp(h->runiq, h->rU, Lr, h->rel_seg_map, h->rel_stamp, h->stamp_dev, st);
   if (h->apply || h->keep_grads)
-    launch_sparse_adam(h->uniq, h->seg, h->perm, h->Udev, L, h->OG, d, h->world, h->t.ent, h->t.ent_m, h->t.ent_v,
-                       h->keep_grads ? h->Gc : nullptr, lr, h->cfg.beta1, h->cfg.beta2, h->cfg.eps, h->bc, h->flags,
-                       h->apply, st);
+    launch_sparse_adam(h->uniq, h->seg, h->perm, h->inv, h->Udev, L, h->OG, h->PS, d, h->world, h->t.ent, h->t.ent_m,
+                       h->t.ent_v, h->keep_grads ? h->Gc : nullptr, h->lr_dev, h->cfg.beta1, h->cfg.beta2,
+                       h->cfg.eps, h->bc, h->flags, h->apply, st);
   mark(h, 6);
   if (h->apply) {
     const double b1 = h->cfg.beta1, b2 = h->cfg.beta2, eps = h->cfg.eps;
+    const float *lr = h->lr_dev;
     if (h->kind == KG_Q2B) {
       launch_dense_adam_rel(dp(h, "rel_center"), h->t.dense_m + seg_of(h, "rel_center")->off,
                             h->t.dense_v + seg_of(h, "rel_center")->off, h->R, d, h->RGU, h->dr, 0, h->rel_seg_map,
-                            h->rel_stamp, h->stamp, lr, b1, b2, eps, h->bc, h->flags, st);
+                            h->rel_stamp, h->stamp_dev, lr, b1, b2, eps, h->bc, h->flags, st);
       launch_dense_adam_rel(dp(h, "rel_offset"), h->t.dense_m + seg_of(h, "rel_offset")->off,
                             h->t.dense_v + seg_of(h, "rel_offset")->off, h->R, d, h->RGU, h->dr, d, h->rel_seg_map,
-                            h->rel_stamp, h->stamp, lr, b1, b2, eps, h->bc, h->flags, st);
+                            h->rel_stamp, h->stamp_dev, lr, b1, b2, eps, h->bc, h->flags, st);
     } else {
       const Seg &r = h->segs[0];
       launch_dense_adam_rel(h->t.dense + r.off, h->t.dense_m + r.off, h->t.dense_v + r.off, h->R, r.cols, h->RGU,
-                            h->dr, 0, h->rel_seg_map, h->rel_stamp, h->stamp, lr, b1, b2, eps, h->bc, h->flags, st);
+                            h->dr, 0, h->rel_seg_map, h->rel_stamp, h->stamp_dev, lr, b1, b2, eps, h->bc, h->flags,
+                            st);
     }
     launch_dense_adam(h->t.dense + h->w_off, h->t.dense_m + h->w_off, h->t.dense_v + h->w_off, h->gdense,
                       h->dense_size - h->w_off, lr, b1, b2, eps, h->bc, h->flags, st);
   }
   mark(h, 7);
-  h->last_kernels = (int)(g_launches - h->launches0);
-  h->last_gemms = h->gemm_count;
   CK(cudaGetLastError());
   // results to pinned host memory (loss, flags, U, t)
   CK(cudaMemcpyAsync(&h->hout->loss, h->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(h->hout->flags, h->flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&h->hout->U, h->Udev, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&h->hout->t, h->t_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaEventRecord(h->step_done, st));
+  return KG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info) {
+  kg_status s = check_state(h);
+  if (s) return s;
+  if (!b) return fail(h, KG_EINVAL, "null batch");
+  if (b->structure < KG_1P || b->structure > KG_UP) return fail(h, KG_EINVAL, "bad structure");
+  if (single_hop(h->kind) && b->structure != KG_1P)
+    return fail(h, KG_EUNSUPPORTED, "single-hop models accept only 1p (Table 2, P:L55)");
+  if (!(lr > 0.f)) return fail(h, KG_EINVAL, "lr must be > 0");
+  StepBufs S;
+  S.plan = make_plan(b->structure);
+  const Plan &p = S.plan;
+  S.M = b->M; S.K = b->K; S.Kp = (int)align_up(std::max(b->K, 1), 64); S.NQ = p.nout * b->M;
+  h->stamp++;
+  if ((s = ingest(h, b, true, p, lr)) != KG_OK) return s;
+  h->last_M = S.M; h->last_K = S.K;
+  if (h->use_graphs) {
+    kg_handle::GraphEntry *g = nullptr;
+    for (auto &e : h->graphs)
+      if (e.structure == b->structure && e.M == S.M && e.K == S.K && e.flags == h->flag_key()) { g = &e; break; }
+    if (!g) {
+      // capture once per (structure, M, K, flags) on the internal stream, then replay
+      cudaStream_t user = h->st;
+      h->st = h->st_cap;
+      CKB(cublasSetStream(h->blas, h->st_cap));
+      const int64_t l0 = g_launches;
+      h->gemm_count = 0;
+      CK(cudaStreamBeginCapture(h->st_cap, cudaStreamCaptureModeThreadLocal));
+      s = enqueue_step(h, S);
+      cudaGraph_t graph = nullptr;
+      cudaError_t ce = cudaStreamEndCapture(h->st_cap, &graph);
+      h->st = user;
+      CKB(cublasSetStream(h->blas, user));
+      if (s != KG_OK) { if (graph) cudaGraphDestroy(graph); return s; }
+      if (ce != cudaSuccess) return fail(h, KG_ECUDA, std::string("stream capture: ") + cudaGetErrorString(ce));
+      kg_handle::GraphEntry e{};
+      e.structure = b->structure; e.M = S.M; e.K = S.K; e.flags = h->flag_key();
+      e.kernels = (int)(g_launches - l0);
+      e.gemms = h->gemm_count;
+      ce = cudaGraphInstantiate(&e.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ce != cudaSuccess) return fail(h, KG_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+      if (h->graphs.size() >= 64) { cudaGraphExecDestroy(h->graphs.front().exec); h->graphs.erase(h->graphs.begin()); }
+      h->graphs.push_back(e);
+      g = &h->graphs.back();
+    }
+    CK(cudaGraphLaunch(g->exec, h->st));
+    h->last_kernels = g->kernels;
+    h->last_gemms = g->gemms;
+  } else {
+    const int64_t l0 = g_launches;
+    h->gemm_count = 0;
+    if ((s = enqueue_step(h, S)) != KG_OK) return s;
+    h->last_kernels = (int)(g_launches - l0);
+    h->last_gemms = h->gemm_count;
+  }
+  CK(cudaEventRecord(h->step_done, h->st));
   h->step_pending = true;
   h->last_U_valid = 1;
   if (info) return read_result(h, info);
@@ -863,6 +984,7 @@ kg_status kg_score(kg_handle *h, const kg_batch *q, const int64_t *cand, int32_t
   if (h->kind == KG_BETAE) { sa.E = h->F; sa.eidx = nullptr; sa.estride = 9LL * h->m; }
   else { sa.E = h->t.ent; sa.eidx = cand_rows; sa.estride = d; }
   sa.Cq = h->Cq; sa.Cv = h->Cv; sa.alpha = h->cfg.box_alpha; sa.Dmin = h->Dscore; sa.ldo = n_cand;
+  sa.Dpart = h->Dpart; sa.cap_D = h->cap_D;
   launch_pair_fwd(h->kind, sa, p.nout, false, st);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out_dist, h->Dscore, sizeof(float) * (size_t)M * n_cand, cudaMemcpyDeviceToHost, st));
@@ -1000,6 +1122,12 @@ void kg_destroy(kg_handle *h) {
   if (h->st) cudaStreamSynchronize(h->st);
   else cudaDeviceSynchronize();
   if (h->blas) cublasDestroy(h->blas);
+  if (h->st2) { cudaStreamSynchronize(h->st2); cudaStreamDestroy(h->st2); }
+  if (h->st_cap) cudaStreamDestroy(h->st_cap);
+  for (auto &g : h->graphs) cudaGraphExecDestroy(g.exec);
+  if (h->ev_fork2) cudaEventDestroy(h->ev_fork2);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   for (int i = 0; i < 2; ++i) {
     if (h->pin[i]) cudaFreeHost(h->pin[i]);
     if (h->pin_ev[i]) cudaEventDestroy(h->pin_ev[i]);

@@ -22,9 +22,13 @@ struct ScoreArgs {
   float *C = nullptr;           // [NQ][Kp] adjoint coefficients
   float *Dmin = nullptr;        // train: [M][K] (optional); score: [M][ldo]
   int ldo = 0;
-  float *loss_part = nullptr;   // [ceil(K/64)][M]
+  float *loss_part = nullptr;   // [M] negative-term sum of each query
   float *dQ = nullptr;          // [NQ][QF*U]
   float *dV = nullptr;          // raw-row gradients of the pool, [K][d]
+  // split-reduction partials (see k_score.cu) and their capacities (floats)
+  float *Dpart = nullptr, *partQ = nullptr, *partV = nullptr, *Cpart = nullptr, *Csum = nullptr;
+  int64_t cap_D = 0, cap_Q = 0, cap_V = 0;
+  int KS = 1, JS = 1, RS = 1, ups = 0, jps = 0, rps = 0;
 };
 
 struct PosArgs {
@@ -39,7 +43,7 @@ struct PosArgs {
 
 // k_score.cu
 void launch_pair_fwd(int kind, const ScoreArgs &a, int nout, bool train, cudaStream_t st);
-void launch_pair_bwd(int kind, const ScoreArgs &a, cudaStream_t st);
+void launch_pair_bwd(int kind, const ScoreArgs &a, cudaStream_t st, cudaStream_t st2);
 void launch_pos(int kind, const PosArgs &p, int nout, cudaStream_t st);
 void launch_beta_entity(const float *ent, const int64_t *rows, int K, int m, float *F, float *Cv, cudaStream_t st);
 void launch_beta_query(const float *Q, int NQ, int m, float *QP, float *Cq, cudaStream_t st);
@@ -58,18 +62,18 @@ void launch_dedup(const int64_t *ids64, const int32_t *ids32, int L, int end_bit
 void launch_init_rows(float *p, int64_t rows, int d, int64_t row0, int64_t row_step, uint64_t seed, uint64_t stream,
                       float lo, float hi, cudaStream_t st);
 void launch_init_flat(float *p, int64_t n, uint64_t seed, uint64_t stream, float lo, float hi, cudaStream_t st);
-void launch_sparse_adam(const int64_t *uniq, const int32_t *seg, const int32_t *perm, const int32_t *U_dev, int Lmax,
-                        const float *OG, int d, int world, float *ent, float *m, float *v, float *grad_out, float lr,
-                        double beta1, double beta2, double eps, const float *bc, const int *flags, int apply,
-                        cudaStream_t st);
-void launch_rel_reduce(const int32_t *seg, const int32_t *perm, const int32_t *U_dev, int Lmax, const float *RG,
-                       int dr, float *RGU, cudaStream_t st);
+void launch_sparse_adam(const int64_t *uniq, const int32_t *seg, const int32_t *perm, const int32_t *inv,
+                        const int32_t *U_dev, int L, const float *OG, float *PS, int d, int world, float *ent,
+                        float *m, float *v, float *grad_out, const float *lr, double beta1, double beta2, double eps,
+                        const float *bc, const int *flags, int apply, cudaStream_t st);
+void launch_rel_reduce(const int32_t *seg, const int32_t *perm, const int32_t *inv, const int32_t *U_dev, int Lr,
+                       const float *RG, float *PS, int dr, float *RGU, cudaStream_t st);
 void launch_rel_stamp(const int64_t *uniq_rel, const int32_t *U_dev, int Lmax, int32_t *rel_seg, int64_t *rel_stamp,
-                      int64_t stamp, cudaStream_t st);
+                      const int64_t *stamp, cudaStream_t st);
 void launch_dense_adam_rel(float *p, float *m, float *v, int R, int width, const float *RGU, int rg_stride,
-                           int rg_col, const int32_t *rel_seg, const int64_t *rel_stamp, int64_t stamp, float lr,
-                           double beta1, double beta2, double eps, const float *bc, const int *flags, cudaStream_t st);
-void launch_dense_adam(float *p, float *m, float *v, const float *g, int64_t n, float lr, double beta1, double beta2,
+                           int rg_col, const int32_t *rel_seg, const int64_t *rel_stamp, const int64_t *stamp,
+                           const float *lr, double beta1, double beta2, double eps, const float *bc, const int *flags, cudaStream_t st);
+void launch_dense_adam(float *p, float *m, float *v, const float *g, int64_t n, const float *lr, double beta1, double beta2,
                        double eps, const float *bc, const int *flags, cudaStream_t st);
 void launch_colsum(const float *X, int rows, int cols, int ld, float *out, cudaStream_t st);
 
