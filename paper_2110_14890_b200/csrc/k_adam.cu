@@ -46,18 +46,21 @@ void launch_init_flat(float *p, int64_t n, uint64_t seed, uint64_t stream, float
 // h = {beta1, 1 - beta1, beta2, 1 - beta2} (the complements formed in double on the host:
 // 1 - beta2 in fp32 would lose ~1e-5 of its value), eps; bc = {1 - beta1^t, 1 - beta2^t}.
 struct AdamHyper { float b1, omb1, b2, omb2, eps; };
-__device__ __forceinline__ void adam1(float &p, float &m, float &v, float g, float lr, const AdamHyper &h, float bc1,
-                                      float bc2) {
-  m = h.b1 * m + h.omb1 * g;
-  v = h.b2 * v + h.omb2 * g * g;
-  p -= lr * (m / bc1) / (sqrtf(v / bc2) + h.eps);
+// ibc = {1 / (1 - beta1^t), 1 / (1 - beta2^t)} (formed in double by the loss kernel);
+// lr1 = lr * ibc[0].  p -= lr * (m / bc1) / (sqrt(v / bc2) + eps) with the divisions by the
+// bias corrections as multiplications and the last one as a 2-ulp reciprocal-divide.
+__device__ __forceinline__ void adam1(float &p, float &m, float &v, float g, float lr1, const AdamHyper &h,
+                                      float ibc2) {
+  m = fmaf(h.b1, m, h.omb1 * g);
+  v = fmaf(h.b2, v, h.omb2 * g * g);
+  p -= lr1 * __fdividef(m, sqrtf(v * ibc2) + h.eps);
 }
-__device__ __forceinline__ void adam4(float4 &p, float4 &m, float4 &v, const float4 g, float lr, const AdamHyper &h,
-                                      float bc1, float bc2) {
-  adam1(p.x, m.x, v.x, g.x, lr, h, bc1, bc2);
-  adam1(p.y, m.y, v.y, g.y, lr, h, bc1, bc2);
-  adam1(p.z, m.z, v.z, g.z, lr, h, bc1, bc2);
-  adam1(p.w, m.w, v.w, g.w, lr, h, bc1, bc2);
+__device__ __forceinline__ void adam4(float4 &p, float4 &m, float4 &v, const float4 g, float lr1, const AdamHyper &h,
+                                      float ibc2) {
+  adam1(p.x, m.x, v.x, g.x, lr1, h, ibc2);
+  adam1(p.y, m.y, v.y, g.y, lr1, h, ibc2);
+  adam1(p.z, m.z, v.z, g.z, lr1, h, ibc2);
+  adam1(p.w, m.w, v.w, g.w, lr1, h, ibc2);
 }
 static AdamHyper hyper(double b1, double b2, double eps) {
   return AdamHyper{(float)b1, (float)(1.0 - b1), (float)b2, (float)(1.0 - b2), (float)eps};
@@ -123,29 +126,31 @@ __device__ __forceinline__ float4 segment_sum(const int32_t *perm, const float4 
   return g;
 }
 
-// Phase 2 for theta_E: one thread per (distinct row u, float4 column): G_u, then Adam
-// on (p, m, v) of the row (local row = id / world).  Every touched row is updated,
-// including rows whose gradient is zero (A16).
+// Phase 2 for theta_E: one warp per distinct row u, lanes over float4 columns:
+// G_u, then Adam on (p, m, v) of the row (local row = id / world).  Every touched
+// row is updated, including rows whose gradient is zero (A16).
 __global__ void __launch_bounds__(256) sparse_adam_kernel(const int64_t *uniq, const int32_t *seg,
                                                           const int32_t *perm, const int32_t *U_dev, const float *OG,
                                                           const float *PS, int d, int world, float *ent, float *m,
                                                           float *v, float *grad_out, const float *lr_dev, AdamHyper hy,
                                                           const float *bc, const int *flags, int apply) {
-  const int d4 = d >> 2;
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int u = (int)(e / d4), c = (int)(e - (int64_t)u * d4);
+  const int u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (u >= *U_dev) return;
-  const float4 g = segment_sum(perm, reinterpret_cast<const float4 *>(OG), reinterpret_cast<const float4 *>(PS),
-                               seg[u], seg[u + 1], d4, c);
-  if (grad_out) reinterpret_cast<float4 *>(grad_out)[(int64_t)u * d4 + c] = g;
-  if (!apply || flags[0]) return;
-  const int64_t off = (uniq[u] / world) * d4 + c;
-  float4 P = reinterpret_cast<float4 *>(ent)[off], Mm = reinterpret_cast<float4 *>(m)[off],
-         V = reinterpret_cast<float4 *>(v)[off];
-  adam4(P, Mm, V, g, *lr_dev, hy, bc[0], bc[1]);
-  reinterpret_cast<float4 *>(ent)[off] = P;
-  reinterpret_cast<float4 *>(m)[off] = Mm;
-  reinterpret_cast<float4 *>(v)[off] = V;
+  const int d4 = d >> 2, s0 = seg[u], s1 = seg[u + 1];
+  const bool upd = apply && !flags[0];
+  const float lr1 = *lr_dev * bc[0], ibc2 = bc[1];
+  const int64_t rowoff = (uniq[u] / world) * d4;
+  const float4 *X4 = reinterpret_cast<const float4 *>(OG), *P4 = reinterpret_cast<const float4 *>(PS);
+  float4 *pe = reinterpret_cast<float4 *>(ent) + rowoff, *pm = reinterpret_cast<float4 *>(m) + rowoff,
+         *pv = reinterpret_cast<float4 *>(v) + rowoff;
+  for (int c = lane; c < d4; c += 32) {
+    const float4 g = segment_sum(perm, X4, P4, s0, s1, d4, c);
+    if (grad_out) reinterpret_cast<float4 *>(grad_out)[(int64_t)u * d4 + c] = g;
+    if (!upd) continue;
+    float4 P = pe[c], Mm = pm[c], V = pv[c];
+    adam4(P, Mm, V, g, lr1, hy, ibc2);
+    pe[c] = P; pm[c] = Mm; pv[c] = V;
+  }
 }
 
 void launch_sparse_adam(const int64_t *uniq, const int32_t *seg, const int32_t *perm, const int32_t *inv,
@@ -154,8 +159,7 @@ void launch_sparse_adam(const int64_t *uniq, const int32_t *seg, const int32_t *
                         const float *bc, const int *flags, int apply, cudaStream_t st) {
   if (L <= 0) return;
   { seg_piece_kernel<<<(L + kPiece - 1) / kPiece, 128, 0, st>>>(perm, inv, seg, L, OG, d / 4, PS); ++g_launches; }
-  const int64_t n = (int64_t)L * (d / 4);
-  { sparse_adam_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(uniq, seg, perm, U_dev, OG, PS, d, world, ent, m, v,
+  { sparse_adam_kernel<<<(L + 7) / 8, 256, 0, st>>>(uniq, seg, perm, U_dev, OG, PS, d, world, ent, m, v,
                                                               grad_out, lr, hyper(beta1, beta2, eps), bc, flags,
                                                               apply); ++g_launches; }
 }
@@ -195,55 +199,103 @@ void launch_rel_stamp(const int64_t *uniq_rel, const int32_t *U_dev, int Lmax, i
   { rel_stamp_kernel<<<(Lmax + 255) / 256, 256, 0, st>>>(uniq_rel, U_dev, rel_seg, rel_stamp, stamp); ++g_launches; }
 }
 
-// Dense Adam over a relation table [R][width] (A17: every row, g = 0 if unused).
-__global__ void __launch_bounds__(256) dense_adam_rel_kernel(float *p, float *m, float *v, int R, int width,
-                                                             const float *RGU, int rg_stride, int rg_col,
-                                                             const int32_t *rel_seg, const int64_t *rel_stamp,
-                                                             const int64_t *stamp_dev, const float *lr_dev,
-                                                             AdamHyper hy, const float *bc, const int *flags) {
+// Dense Adam over theta_D (A17: every element, every step).  Streaming kernel:
+// each thread issues the loads of kE float4 elements (p, m, v, g) before any
+// arithmetic, evict-first cache hints (the 300 MB of Adam state is touched once
+// per step), no grid cap (one pass).
+// REL: the relation tables, nseg segments of [R][width] stored back to back
+// (Q2B: rel_center, rel_offset); the gradient of row r of segment s is
+// RGU[rel_seg[r]][s*width + c] when relation r was used by this step
+// (rel_stamp[r] == stamp), else 0.  !REL: the operator weights, gradient g.
+constexpr int kE = 4;
+
+// Relation tables: one warp per table row (nseg * R rows); the "was this relation
+// used by the step" test is warp-uniform; lanes stream the row's float4 columns.
+__global__ void __launch_bounds__(256) dense_adam_rel_kernel(float4 *p, float4 *m, float4 *v, int R, int w4, int nseg,
+                                                             const float *RGU, const int32_t *rel_seg,
+                                                             const int64_t *rel_stamp, const int64_t *stamp_dev,
+                                                             const float *lr_dev, AdamHyper hy, const float *bc,
+                                                             const int *flags) {
   if (flags[0]) return;
-  const int64_t stamp = *stamp_dev;
-  const float lr = *lr_dev;
-  const int w4 = width >> 2;
-  const int64_t n4 = (int64_t)R * w4;
-  const float bc1 = bc[0], bc2 = bc[1];
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n4; e += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(e / w4), c4 = (int)(e - (int64_t)r * w4);
-    float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (rel_stamp[r] == stamp) g = *reinterpret_cast<const float4 *>(RGU + (int64_t)rel_seg[r] * rg_stride + rg_col + c4 * 4);
-    float4 P = reinterpret_cast<float4 *>(p)[e], Mm = reinterpret_cast<float4 *>(m)[e], V = reinterpret_cast<float4 *>(v)[e];
-    adam4(P, Mm, V, g, lr, hy, bc1, bc2);
-    reinterpret_cast<float4 *>(p)[e] = P;
-    reinterpret_cast<float4 *>(m)[e] = Mm;
-    reinterpret_cast<float4 *>(v)[e] = V;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= nseg * R) return;
+  const int sidx = row >= R ? 1 : 0, r = row - sidx * R;
+  const float lr1 = *lr_dev * bc[0], ibc2 = bc[1];
+  const bool used = rel_stamp[r] == *stamp_dev;
+  const float4 *g4 = used ? reinterpret_cast<const float4 *>(RGU) + (int64_t)rel_seg[r] * nseg * w4 + sidx * w4 : nullptr;
+  float4 *pr = p + (int64_t)row * w4, *mr = m + (int64_t)row * w4, *vr = v + (int64_t)row * w4;
+  float4 P[kE], Mm[kE], V[kE], G[kE];
+#pragma unroll
+  for (int k = 0; k < kE; ++k) {
+    const int c = lane + 32 * k;
+    if (c >= w4) continue;
+    P[k] = __ldcs(pr + c);
+    Mm[k] = __ldcs(mr + c);
+    V[k] = __ldcs(vr + c);
+    G[k] = used ? g4[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int k = 0; k < kE; ++k) {
+    const int c = lane + 32 * k;
+    if (c >= w4) continue;
+    adam4(P[k], Mm[k], V[k], G[k], lr1, hy, ibc2);
+    __stcs(pr + c, P[k]);
+    __stcs(mr + c, Mm[k]);
+    __stcs(vr + c, V[k]);
+  }
+  for (int c = lane + 32 * kE; c < w4; c += 32) {   // rows wider than 4 x 32 float4
+    float4 Pq = pr[c], Mq = mr[c], Vq = vr[c];
+    adam4(Pq, Mq, Vq, used ? g4[c] : make_float4(0.f, 0.f, 0.f, 0.f), lr1, hy, ibc2);
+    pr[c] = Pq; mr[c] = Mq; vr[c] = Vq;
   }
 }
-void launch_dense_adam_rel(float *p, float *m, float *v, int R, int width, const float *RGU, int rg_stride,
-                           int rg_col, const int32_t *rel_seg, const int64_t *rel_stamp, const int64_t *stamp,
-                           const float *lr, double beta1, double beta2, double eps, const float *bc, const int *flags, cudaStream_t st) {
-  const int64_t n4 = (int64_t)R * (width / 4);
-  { dense_adam_rel_kernel<<<grid_for(n4, 256), 256, 0, st>>>(p, m, v, R, width, RGU, rg_stride, rg_col, rel_seg,
-                                                           rel_stamp, stamp, lr, hyper(beta1, beta2, eps), bc, flags); ++g_launches; }
-}
 
-__global__ void __launch_bounds__(256) dense_adam_kernel(float *p, float *m, float *v, const float *g, int64_t n4,
+// Operator weights: flat stream, kE float4 per thread, loads issued first.
+__global__ void __launch_bounds__(256) dense_adam_kernel(float4 *p, float4 *m, float4 *v, const float4 *g, int n4,
                                                          const float *lr_dev, AdamHyper hy, const float *bc,
                                                          const int *flags) {
   if (flags[0]) return;
-  const float lr = *lr_dev;
-  const float bc1 = bc[0], bc2 = bc[1];
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n4; e += (int64_t)gridDim.x * blockDim.x) {
-    float4 P = reinterpret_cast<float4 *>(p)[e], Mm = reinterpret_cast<float4 *>(m)[e], V = reinterpret_cast<float4 *>(v)[e];
-    adam4(P, Mm, V, reinterpret_cast<const float4 *>(g)[e], lr, hy, bc1, bc2);
-    reinterpret_cast<float4 *>(p)[e] = P;
-    reinterpret_cast<float4 *>(m)[e] = Mm;
-    reinterpret_cast<float4 *>(v)[e] = V;
+  const float lr1 = *lr_dev * bc[0], ibc2 = bc[1];
+  const int base = blockIdx.x * (256 * kE) + threadIdx.x;
+  float4 P[kE], Mm[kE], V[kE], G[kE];
+#pragma unroll
+  for (int k = 0; k < kE; ++k) {
+    const int e = base + k * 256;
+    if (e >= n4) continue;
+    P[k] = __ldcs(p + e);
+    Mm[k] = __ldcs(m + e);
+    V[k] = __ldcs(v + e);
+    G[k] = __ldcs(g + e);
+  }
+#pragma unroll
+  for (int k = 0; k < kE; ++k) {
+    const int e = base + k * 256;
+    if (e >= n4) continue;
+    adam4(P[k], Mm[k], V[k], G[k], lr1, hy, ibc2);
+    __stcs(p + e, P[k]);
+    __stcs(m + e, Mm[k]);
+    __stcs(v + e, V[k]);
   }
 }
-void launch_dense_adam(float *p, float *m, float *v, const float *g, int64_t n, const float *lr, double beta1, double beta2,
-                       double eps, const float *bc, const int *flags, cudaStream_t st) {
-  if (n <= 0) return;
-  { dense_adam_kernel<<<grid_for(n / 4, 256), 256, 0, st>>>(p, m, v, g, n / 4, lr, hyper(beta1, beta2, eps), bc, flags); ++g_launches; }
+
+void launch_dense_adam_rel(float *p, float *m, float *v, int R, int width, int nseg, const float *RGU,
+                           const int32_t *rel_seg, const int64_t *rel_stamp, const int64_t *stamp, const float *lr,
+                           double beta1, double beta2, double eps, const float *bc, const int *flags,
+                           cudaStream_t st) {
+  const int rows = nseg * R;
+  if (rows <= 0) return;
+  { dense_adam_rel_kernel<<<(rows + 7) / 8, 256, 0, st>>>(
+        reinterpret_cast<float4 *>(p), reinterpret_cast<float4 *>(m), reinterpret_cast<float4 *>(v), R, width / 4,
+        nseg, RGU, rel_seg, rel_stamp, stamp, lr, hyper(beta1, beta2, eps), bc, flags); ++g_launches; }
+}
+
+void launch_dense_adam(float *p, float *m, float *v, const float *g, int64_t n, const float *lr, double beta1,
+                       double beta2, double eps, const float *bc, const int *flags, cudaStream_t st) {
+  const int n4 = (int)(n / 4);
+  if (n4 <= 0) return;
+  { dense_adam_kernel<<<(n4 + 256 * kE - 1) / (256 * kE), 256, 0, st>>>(
+        reinterpret_cast<float4 *>(p), reinterpret_cast<float4 *>(m), reinterpret_cast<float4 *>(v),
+        reinterpret_cast<const float4 *>(g), n4, lr, hyper(beta1, beta2, eps), bc, flags); ++g_launches; }
 }
 
 // out[c] = sum_r X[r*ld + c]; 32 columns x 32 row-lanes per block, fixed-order smem reduce.

@@ -27,19 +27,29 @@ namespace kg {
 
 // ---------------------------------------------------------------- models
 struct ML2 {   // GQE, TransE: ||q - v||_2 (A2)
+  static constexpr bool kRowAlpha = false;
   static constexpr int QF = 1, EF = 1, EOFF = 0, BQ_EF = 1, BQ_EOFF = 0, BV_EF = 1, BV_EOFF = 0, AV = 1, OUTF = 1;
   static constexpr bool kL2 = true, kBeta = false;
   __device__ static float acc(const float *q, const float *e, float) { const float t = q[0] - e[0]; return t * t; }
   __device__ static float fin(float s, float, float) { return sqrtf(s); }
   __device__ static void bq(const float *q, const float *e, float c, float, float *dq) { dq[0] += c * (q[0] - e[0]); }
   __device__ static void bv(const float *q, const float *e, float c, float, float *a) { a[0] += c * (e[0] - q[0]); }
+  // fused backward: dq += dD/dq * C, dv += dD/dv * C   (C here is c_ij / D_ij, A2 adjoint)
+  static constexpr int BF = 1, BOFF = 0;
+  __device__ static void grad(const float *q, const float *e, float c, float, float *dq, float *dv) {
+    const float ct = c * (q[0] - e[0]);
+    dq[0] += ct;
+    dv[0] -= ct;
+  }
 };
 struct MBox {  // Q2B: sum ReLU(|v-c| - o) + alpha * min(|v-c|, o) (A7)
+  static constexpr bool kRowAlpha = true;   // dq[1] += alpha * sum_j c after the j loop
   static constexpr int QF = 2, EF = 1, EOFF = 0, BQ_EF = 1, BQ_EOFF = 0, BV_EF = 1, BV_EOFF = 0, AV = 1, OUTF = 1;
   static constexpr bool kL2 = false, kBeta = false;
+  // ReLU(d - o) + alpha min(d, o) = d + (alpha - 1) min(d, o), d = |v - c| (o >= 0)
   __device__ static float acc(const float *q, const float *e, float al) {
     const float dl = fabsf(e[0] - q[0]);
-    return fmaxf(dl - q[1], 0.f) + al * fminf(dl, q[1]);
+    return fmaf(al - 1.f, fminf(dl, q[1]), dl);
   }
   __device__ static float fin(float s, float, float) { return s; }
   __device__ static void bq(const float *q, const float *e, float c, float al, float *dq) {
@@ -54,8 +64,22 @@ struct MBox {  // Q2B: sum ReLU(|v-c| - o) + alpha * min(|v-c|, o) (A7)
     const float s = (dl > 0.f) ? 1.f : ((dl < 0.f) ? -1.f : 0.f);
     acc_[0] += c * s * ((a > o ? 1.f : 0.f) + al * (a < o ? 1.f : 0.f));
   }
+  static constexpr int BF = 1, BOFF = 0;
+  __device__ static void grad(const float *q, const float *e, float c, float al, float *dq, float *dv) {
+    // t = v - c, a = |t|, W = [a > o] + alpha [a < o]:  dD/dv = sign(t) W (sign(0) = 0),
+    // dD/dc = -dD/dv, dD/do = alpha - W (= alpha - 1 | 0 | alpha for a > o | a < o | a == o);
+    // the alpha * c part of dD/do is added once per row by the caller (A7, A19).
+    const float t = e[0] - q[0], a = fabsf(t), o = q[1];
+    const float W = (a > o) ? 1.f : ((a < o) ? al : 0.f);
+    const float cw = c * W;
+    const float cg = (t == 0.f) ? 0.f : __int_as_float(__float_as_int(cw) ^ (__float_as_int(t) & 0x80000000));
+    dq[0] -= cg;
+    dv[0] += cg;
+    dq[1] -= cw;
+  }
 };
 struct MBeta {  // KL(Beta(entity) || Beta(query)) summed over m (A10), direct per-unit differences (A22)
+  static constexpr bool kRowAlpha = false;
   static constexpr int QF = 2, EF = 4, EOFF = 0, BQ_EF = 2, BQ_EOFF = 0, BV_EF = 7, BV_EOFF = 2, AV = 2, OUTF = 2;
   static constexpr bool kL2 = false, kBeta = true;
   // e = [Pa, Pb, A, B]
@@ -63,8 +87,17 @@ struct MBeta {  // KL(Beta(entity) || Beta(query)) summed over m (A10), direct p
   __device__ static float fin(float s, float cq, float cv) { return s + cq - cv; }
   __device__ static void bq(const float *, const float *e, float c, float, float *dq) { dq[0] -= c * e[0]; dq[1] -= c * e[1]; }
   __device__ static void bv(const float *q, const float *, float c, float, float *a) { a[0] += c * q[0]; a[1] += c * q[1]; }
+  // e = [Pa, Pb]; dv accumulates sum C a2, sum C b2 (epilogue in the combine kernel)
+  static constexpr int BF = 2, BOFF = 0;
+  __device__ static void grad(const float *q, const float *e, float c, float, float *dq, float *dv) {
+    dq[0] -= c * e[0];
+    dq[1] -= c * e[1];
+    dv[0] += c * q[0];
+    dv[1] += c * q[1];
+  }
 };
 struct MRot {  // RotatE: sum_k |q_k - t_k| (A3)
+  static constexpr bool kRowAlpha = false;
   static constexpr int QF = 2, EF = 2, EOFF = 0, BQ_EF = 2, BQ_EOFF = 0, BV_EF = 2, BV_EOFF = 0, AV = 2, OUTF = 2;
   static constexpr bool kL2 = false, kBeta = false;
   __device__ static float acc(const float *q, const float *e, float) {
@@ -80,22 +113,41 @@ struct MRot {  // RotatE: sum_k |q_k - t_k| (A3)
     const float a = q[0] - e[0], b = q[1] - e[1], n = sqrtf(a * a + b * b);
     if (n > 0.f) { const float w = c / n; acc_[0] -= w * a; acc_[1] -= w * b; }
   }
+  static constexpr int BF = 2, BOFF = 0;
+  __device__ static void grad(const float *q, const float *e, float c, float, float *dq, float *dv) {
+    const float a = q[0] - e[0], b = q[1] - e[1], n = sqrtf(a * a + b * b);
+    const float w = n > 0.f ? c / n : 0.f;
+    dq[0] += w * a; dq[1] += w * b;
+    dv[0] -= w * a; dv[1] -= w * b;
+  }
 };
 struct MDot {  // DistMult: -<q, t> (A13)
+  static constexpr bool kRowAlpha = false;
   static constexpr int QF = 1, EF = 1, EOFF = 0, BQ_EF = 1, BQ_EOFF = 0, BV_EF = 1, BV_EOFF = 0, AV = 1, OUTF = 1;
   static constexpr bool kL2 = false, kBeta = false;
   __device__ static float acc(const float *q, const float *e, float) { return q[0] * e[0]; }
   __device__ static float fin(float s, float, float) { return -s; }
   __device__ static void bq(const float *, const float *e, float c, float, float *dq) { dq[0] -= c * e[0]; }
   __device__ static void bv(const float *q, const float *, float c, float, float *a) { a[0] -= c * q[0]; }
+  static constexpr int BF = 1, BOFF = 0;
+  __device__ static void grad(const float *q, const float *e, float c, float, float *dq, float *dv) {
+    dq[0] -= c * e[0];
+    dv[0] -= c * q[0];
+  }
 };
 struct MCpx {  // ComplEx: -Re<q, conj(t)> = -sum(q_re t_re + q_im t_im) (A13)
+  static constexpr bool kRowAlpha = false;
   static constexpr int QF = 2, EF = 2, EOFF = 0, BQ_EF = 2, BQ_EOFF = 0, BV_EF = 2, BV_EOFF = 0, AV = 2, OUTF = 2;
   static constexpr bool kL2 = false, kBeta = false;
   __device__ static float acc(const float *q, const float *e, float) { return q[0] * e[0] + q[1] * e[1]; }
   __device__ static float fin(float s, float, float) { return -s; }
   __device__ static void bq(const float *, const float *e, float c, float, float *dq) { dq[0] -= c * e[0]; dq[1] -= c * e[1]; }
   __device__ static void bv(const float *q, const float *, float c, float, float *a) { a[0] -= c * q[0]; a[1] -= c * q[1]; }
+  static constexpr int BF = 2, BOFF = 0;
+  __device__ static void grad(const float *q, const float *e, float c, float, float *dq, float *dv) {
+    dq[0] -= c * e[0]; dq[1] -= c * e[1];
+    dv[0] -= c * q[0]; dv[1] -= c * q[1];
+  }
 };
 
 __device__ __forceinline__ float4 ld4(const float *p) { return *reinterpret_cast<const float4 *>(p); }
@@ -107,6 +159,8 @@ __device__ __forceinline__ float4 ld4(const float *p) { return *reinterpret_cast
 // sums go to Dpart[z][t][i][j] and pair_epi_kernel adds them in the fixed order z.
 template <class Mdl, int NOUT>
 __global__ void __launch_bounds__(256) pair_fwd_kernel(ScoreArgs a) {
+  // thread (tx, ty) owns queries i0 + 4*ty + x and candidates j0 + 4*tx + b (x, b < 4):
+  // one 128-bit shared load per operand row per unit.
   constexpr int BI = 64, BJ = 64, KC = 16, PAD = 4;
   __shared__ __align__(16) float sQ[NOUT][Mdl::QF][KC][BI + PAD];
   __shared__ __align__(16) float sE[Mdl::EF][KC][BJ + PAD];
@@ -158,34 +212,38 @@ __global__ void __launch_bounds__(256) pair_fwd_kernel(ScoreArgs a) {
     for (int kk = 0; kk < KC; ++kk) {
       float ev[4][Mdl::EF];
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
+      for (int f = 0; f < Mdl::EF; ++f) {
+        const float4 v = *reinterpret_cast<const float4 *>(&sE[f][kk][4 * tx]);
+        ev[0][f] = v.x; ev[1][f] = v.y; ev[2][f] = v.z; ev[3][f] = v.w;
+      }
 #pragma unroll
-        for (int f = 0; f < Mdl::EF; ++f) ev[b][f] = sE[f][kk][tx + 16 * b];
+      for (int tt = 0; tt < NOUT; ++tt) {
+        float qv[4][Mdl::QF];
 #pragma unroll
-      for (int tt = 0; tt < NOUT; ++tt)
-#pragma unroll
-        for (int x = 0; x < 4; ++x) {
-          float qv[Mdl::QF];
-#pragma unroll
-          for (int f = 0; f < Mdl::QF; ++f) qv[f] = sQ[tt][f][kk][ty + 16 * x];
-#pragma unroll
-          for (int b = 0; b < 4; ++b) acc[tt][x][b] += Mdl::acc(qv, ev[b], a.alpha);
+        for (int f = 0; f < Mdl::QF; ++f) {
+          const float4 v = *reinterpret_cast<const float4 *>(&sQ[tt][f][kk][4 * ty]);
+          qv[0][f] = v.x; qv[1][f] = v.y; qv[2][f] = v.z; qv[3][f] = v.w;
         }
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[tt][x][b] += Mdl::acc(qv[x], ev[b], a.alpha);
+      }
     }
     __syncthreads();
   }
   float *out = a.Dpart + (size_t)blockIdx.z * NOUT * M * a.Kp;
+  const int jb = j0 + 4 * tx;
 #pragma unroll
   for (int tt = 0; tt < NOUT; ++tt)
 #pragma unroll
     for (int x = 0; x < 4; ++x) {
-      const int i = i0 + ty + 16 * x;
+      const int i = i0 + 4 * ty + x;
       if (i >= M) continue;
+      float *o = out + (size_t)(tt * M + i) * a.Kp + jb;
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int j = j0 + tx + 16 * b;
-        if (j < K) out[(size_t)(tt * M + i) * a.Kp + j] = acc[tt][x][b];
-      }
+      for (int b = 0; b < 4; ++b)
+        if (jb + b < K) o[b] = acc[tt][x][b];
     }
 }
 
@@ -247,7 +305,7 @@ __global__ void __launch_bounds__(256) pair_epi_kernel(ScoreArgs a) {
   if (TRAIN) {
     lsum = block_sum(lsum, red);
     if (threadIdx.x == 0) a.loss_part[i] = lsum;
-    if (Mdl::kBeta) {
+    if (Mdl::kBeta || Mdl::kRowAlpha) {   // row sums of C: BetaE psi terms, Q2B alpha * sum_j c (dD/do)
 #pragma unroll
       for (int tt = 0; tt < NOUT; ++tt) {
         const float s = block_sum(csum[tt], red);
@@ -257,87 +315,97 @@ __global__ void __launch_bounds__(256) pair_epi_kernel(ScoreArgs a) {
   }
 }
 
-// ---------------------------------------------------------------- pair_bwd_q (partial)
-// out (r, k) 64 x 32, reduction over the pool j in chunks of 32; blockIdx.z
-// selects a contiguous j range (split reduction), partials to partQ[z].
+// ---------------------------------------------------------------- fused scoring backward
+// One pass over the (query row r, pool entry j, unit k) terms computes both
+// reductions: dQ[r][k] = sum_j C_rj dD/dq and dV[j][k] = sum_r C_rj dD/dv.
+// Lanes = 32 consecutive units k; warp w of the CTA owns JW = 16 pool entries
+// (their entity features and their dV accumulators live in registers for the
+// whole row range); each row's dQ partial over the warp's entries is combined
+// across the NW warps in shared memory in a fixed order and written once per
+// (row, j-block of NW*JW).  blockIdx.z splits the rows; all partial sums are
+// added by the combine kernels in a fixed order (deterministic, no atomics).
+constexpr int kBW = 8, kJW = 16, kIC = 16;
+
 template <class Mdl>
-__global__ void __launch_bounds__(256) pair_bwd_q_kernel(ScoreArgs a) {
-  constexpr int BR = 64, BK = 32, JC = 32, PAD = 4, QF = Mdl::QF, EF = Mdl::BQ_EF;
-  __shared__ __align__(16) float sC[JC][BR + PAD];
-  __shared__ __align__(16) float sE[EF][JC][BK + PAD];
-  __shared__ int64_t sRow[JC];
-  const int t = threadIdx.x, tx = t & 7, ty = t >> 3;
-  const int r0 = blockIdx.y * BR, k0 = blockIdx.x * BK;
-  const int NQ = a.NQ, K = a.K, U = a.U, qstride = QF * U;
-  const int jb = blockIdx.z * a.jps, je = min(K, jb + a.jps);
-  float qv[2][4][QF], acc[2][4][QF];
+__global__ void __launch_bounds__(kBW * 32, 2) pair_bwd_kernel(ScoreArgs a) {
+  constexpr int QF = Mdl::QF, BF = Mdl::BF, AV = Mdl::AV, JB = kBW * kJW;
+  extern __shared__ __align__(16) float smem[];
+  float *sC = smem;                                   // [kIC][JB]
+  float *sQ = sC + kIC * JB;                          // [kIC][QF][32]
+  float *sDQ = sQ + kIC * QF * 32;                    // [kBW][kIC][QF][32]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int U = a.U, K = a.K, NQ = a.NQ, qstride = QF * U;
+  const int k = blockIdx.x * 32 + lane;
+  const bool kval = k < U;
+  const int jb0 = blockIdx.y * JB, jw0 = jb0 + w * kJW;
+  const int rb = blockIdx.z * a.rps, re = min(NQ, rb + a.rps);
+  float ev[kJW][BF], dv[kJW][AV];
 #pragma unroll
-  for (int x = 0; x < 2; ++x)
+  for (int jj = 0; jj < kJW; ++jj) {
+    const int j = jw0 + jj;
+    const int64_t er = (j < K) ? (a.eidx ? a.eidx[j] : (int64_t)j) : 0;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int r = r0 + ty + 32 * x, k = k0 + tx + 8 * b;
+    for (int f = 0; f < BF; ++f) ev[jj][f] = (j < K && kval) ? a.E[er * a.estride + (Mdl::BOFF + f) * U + k] : 0.f;
 #pragma unroll
-      for (int f = 0; f < QF; ++f) {
-        qv[x][b][f] = (r < NQ && k < U) ? a.Q[(size_t)r * qstride + f * U + k] : 0.f;
-        acc[x][b][f] = 0.f;
+    for (int f = 0; f < AV; ++f) dv[jj][f] = 0.f;
+  }
+  for (int r0 = rb; r0 < re; r0 += kIC) {
+    // stage C[r0 .. r0+kIC][jb0 .. jb0+JB) and the query features of the chunk
+    for (int e = threadIdx.x; e < kIC * JB / 4; e += blockDim.x) {
+      const int ii = e / (JB / 4), c4 = e - ii * (JB / 4);
+      const int r = r0 + ii, j = jb0 + c4 * 4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < re && j < a.Kp) v = ld4(a.C + (size_t)r * a.Kp + j);   // Kp % 64 == 0, padding is 0
+      *reinterpret_cast<float4 *>(sC + ii * JB + c4 * 4) = v;
+    }
+    for (int e = threadIdx.x; e < kIC * QF * 32; e += blockDim.x) {
+      const int ii = e / (QF * 32), f = (e / 32) % QF, l = e & 31;
+      const int r = r0 + ii, kk = blockIdx.x * 32 + l;
+      sQ[e] = (r < re && kk < U) ? a.Q[(size_t)r * qstride + f * U + kk] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int ii = 0; ii < kIC; ++ii) {
+      float q[QF], dq[QF], dq2[QF];
+#pragma unroll
+      for (int f = 0; f < QF; ++f) { q[f] = sQ[(ii * QF + f) * 32 + lane]; dq[f] = 0.f; dq2[f] = 0.f; }
+      const float4 *crow = reinterpret_cast<const float4 *>(sC + ii * JB + w * kJW);
+#pragma unroll
+      for (int j4 = 0; j4 < kJW / 4; ++j4) {
+        const float4 c4 = crow[j4];
+        Mdl::grad(q, ev[j4 * 4 + 0], c4.x, a.alpha, dq, dv[j4 * 4 + 0]);
+        Mdl::grad(q, ev[j4 * 4 + 1], c4.y, a.alpha, dq2, dv[j4 * 4 + 1]);
+        Mdl::grad(q, ev[j4 * 4 + 2], c4.z, a.alpha, dq, dv[j4 * 4 + 2]);
+        Mdl::grad(q, ev[j4 * 4 + 3], c4.w, a.alpha, dq2, dv[j4 * 4 + 3]);
       }
-    }
-  for (int j0 = jb; j0 < je; j0 += JC) {
-    if (t < JC) {
-      const int j = j0 + t;
-      sRow[t] = (j < je) ? (a.eidx ? a.eidx[j] : (int64_t)j) : 0;
-    }
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const int e = t + 256 * s, row = e >> 3, c4 = e & 7;
-      const int r = r0 + row;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (r < NQ) v = ld4(a.C + (size_t)r * a.Kp + j0 + c4 * 4);   // Kp % 64 == 0, padding is 0
-      if (j0 + c4 * 4 >= je) v = make_float4(0.f, 0.f, 0.f, 0.f);
-      sC[c4 * 4 + 0][row] = v.x; sC[c4 * 4 + 1][row] = v.y;
-      sC[c4 * 4 + 2][row] = v.z; sC[c4 * 4 + 3][row] = v.w;
+      for (int f = 0; f < QF; ++f) sDQ[((w * kIC + ii) * QF + f) * 32 + lane] = dq[f] + dq2[f];
     }
     __syncthreads();
-    for (int e = t; e < EF * JC * (BK / 4); e += 256) {
-      const int c4 = e % (BK / 4);
-      const int rest = e / (BK / 4);
-      const int row = rest % JC, f = rest / JC;
-      const int j = j0 + row, k = k0 + c4 * 4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (j < je && k < U) v = ld4(a.E + sRow[row] * a.estride + (Mdl::BQ_EOFF + f) * U + k);
-      *reinterpret_cast<float4 *>(&sE[f][row][c4 * 4]) = v;
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (int jj = 0; jj < JC; ++jj) {
-      float c[2], ev[4][EF];
+    // fixed-order combine over the warps; one partial per (row, j-block)
+    for (int e = threadIdx.x; e < kIC * QF * 32; e += blockDim.x) {
+      const int ii = e / (QF * 32), f = (e / 32) % QF, l = e & 31;
+      const int r = r0 + ii, kk = blockIdx.x * 32 + l;
+      float s = 0.f;
 #pragma unroll
-      for (int x = 0; x < 2; ++x) c[x] = sC[jj][ty + 32 * x];
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-#pragma unroll
-        for (int f = 0; f < EF; ++f) ev[b][f] = sE[f][jj][tx + 8 * b];
-#pragma unroll
-      for (int x = 0; x < 2; ++x)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) Mdl::bq(qv[x][b], ev[b], c[x], a.alpha, acc[x][b]);
+      for (int ww = 0; ww < kBW; ++ww) s += sDQ[ww * kIC * QF * 32 + e];
+      if (r < re && kk < U) a.partQ[((size_t)blockIdx.y * NQ + r) * qstride + f * U + kk] = s;
     }
     __syncthreads();
   }
-  float *out = a.partQ + (size_t)blockIdx.z * NQ * qstride;
+  const size_t zs = (size_t)K * AV * U;
 #pragma unroll
-  for (int x = 0; x < 2; ++x)
+  for (int jj = 0; jj < kJW; ++jj) {
+    const int j = jw0 + jj;
+    if (j >= K || !kval) continue;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int r = r0 + ty + 32 * x, k = k0 + tx + 8 * b;
-      if (r >= NQ || k >= U) continue;
-#pragma unroll
-      for (int f = 0; f < QF; ++f) out[(size_t)r * qstride + f * U + k] = acc[x][b][f];
-    }
+    for (int f = 0; f < AV; ++f) a.partV[blockIdx.z * zs + (size_t)j * AV * U + f * U + k] = dv[jj][f];
+  }
 }
 
-// dQ[r][f*U + k] += sum_z partQ[z] (+ BetaE: Csum[r] * QP[r][f][k]); dQ holds the positive term.
-template <bool BETA>
+// dQ[r][f*U + k] += sum_z partQ[z] (+ BetaE: Csum[r] * QP[r][f][k]; Q2B offset: alpha * Csum[r]);
+// dQ already holds the positive term.
+template <bool BETA, bool BOX>
 __global__ void bwd_q_combine_kernel(ScoreArgs a, int qstride) {
   const int64_t n = (int64_t)a.NQ * qstride;
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -345,87 +413,8 @@ __global__ void bwd_q_combine_kernel(ScoreArgs a, int qstride) {
   float v = 0.f;
   for (int z = 0; z < a.JS; ++z) v += a.partQ[z * n + e];
   if (BETA) v += a.Csum[e / qstride] * a.QP[e];
+  if (BOX && (e % qstride) >= a.U) v = fmaf(a.alpha, a.Csum[e / qstride], v);
   a.dQ[e] += v;
-}
-
-// ---------------------------------------------------------------- pair_bwd_v (partial)
-// out (j, k) 64 x 32, reduction over query rows r in chunks of 32; blockIdx.z
-// selects a contiguous r range, partial accumulators to partV[z] (and, BetaE,
-// the partial column sums of C to Cpart[z]).
-template <class Mdl>
-__global__ void __launch_bounds__(256) pair_bwd_v_kernel(ScoreArgs a) {
-  constexpr int BJ = 64, BK = 32, RC = 32, PAD = 4, QF = Mdl::QF, EF = Mdl::BV_EF, AV = Mdl::AV;
-  __shared__ __align__(16) float sC[RC][BJ + PAD];
-  __shared__ __align__(16) float sQ[QF][RC][BK + PAD];
-  const int t = threadIdx.x, tx = t & 7, ty = t >> 3;
-  const int j0 = blockIdx.y * BJ, k0 = blockIdx.x * BK;
-  const int NQ = a.NQ, K = a.K, U = a.U, qstride = QF * U;
-  const int rb = blockIdx.z * a.rps, re = min(NQ, rb + a.rps);
-  float ev[2][4][EF], acc[2][4][AV], cs[2] = {0.f, 0.f};
-#pragma unroll
-  for (int x = 0; x < 2; ++x) {
-    const int j = j0 + ty + 32 * x;
-    const int64_t er = (j < K) ? (a.eidx ? a.eidx[j] : (int64_t)j) : 0;
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int k = k0 + tx + 8 * b;
-#pragma unroll
-      for (int f = 0; f < EF; ++f)
-        ev[x][b][f] = (!Mdl::kBeta && j < K && k < U) ? a.E[er * a.estride + (Mdl::BV_EOFF + f) * U + k] : 0.f;
-#pragma unroll
-      for (int f = 0; f < AV; ++f) acc[x][b][f] = 0.f;
-    }
-  }
-  for (int r0 = rb; r0 < re; r0 += RC) {
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const int e = t + 256 * s, row = e >> 4, c4 = e & 15;
-      const int r = r0 + row;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (r < re) v = ld4(a.C + (size_t)r * a.Kp + j0 + c4 * 4);
-      *reinterpret_cast<float4 *>(&sC[row][c4 * 4]) = v;
-    }
-    for (int e = t; e < QF * RC * (BK / 4); e += 256) {
-      const int c4 = e % (BK / 4);
-      const int rest = e / (BK / 4);
-      const int row = rest % RC, f = rest / RC;
-      const int r = r0 + row, k = k0 + c4 * 4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (r < re && k < U) v = ld4(a.Q + (size_t)r * qstride + f * U + k);
-      *reinterpret_cast<float4 *>(&sQ[f][row][c4 * 4]) = v;
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (int rr = 0; rr < RC; ++rr) {
-      float c[2], qv[4][QF];
-#pragma unroll
-      for (int x = 0; x < 2; ++x) { c[x] = sC[rr][ty + 32 * x]; cs[x] += c[x]; }
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-#pragma unroll
-        for (int f = 0; f < QF; ++f) qv[b][f] = sQ[f][rr][tx + 8 * b];
-#pragma unroll
-      for (int x = 0; x < 2; ++x)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) Mdl::bv(qv[b], ev[x][b], c[x], a.alpha, acc[x][b]);
-    }
-    __syncthreads();
-  }
-  const size_t zs = (size_t)K * AV * U;
-  float *out = a.partV + blockIdx.z * zs;
-#pragma unroll
-  for (int x = 0; x < 2; ++x) {
-    const int j = j0 + ty + 32 * x;
-    if (j >= K) continue;
-    if (Mdl::kBeta && blockIdx.x == 0 && tx == 0) a.Cpart[(size_t)blockIdx.z * K + j] = cs[x];
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int k = k0 + tx + 8 * b;
-      if (k >= U) continue;
-#pragma unroll
-      for (int f = 0; f < AV; ++f) out[(size_t)j * AV * U + f * U + k] = acc[x][b][f];
-    }
-  }
 }
 
 // Raw-row gradient of pool entry j: sum_z partials (+ BetaE epilogue with the
@@ -447,8 +436,7 @@ __global__ void bwd_v_combine_kernel(ScoreArgs a) {
   }
   float *out = a.dV + (size_t)j * a.d;
   if (Mdl::kBeta) {
-    float Cj = 0.f;
-    for (int z = 0; z < a.RS; ++z) Cj += a.Cpart[(size_t)z * K + j];
+    const float Cj = a.Cpart[j];   // column sum of C over all query rows
     const float *Fr = a.E + (size_t)j * a.estride;
     const float A = Fr[2 * U + k], B = Fr[3 * U + k], TA = Fr[4 * U + k], TB = Fr[5 * U + k],
                 TAB = Fr[6 * U + k], GA = Fr[7 * U + k], GB = Fr[8 * U + k];
@@ -630,8 +618,8 @@ __global__ void __launch_bounds__(256) loss_finalize_kernel(const float *loss_po
     if (!bad && apply) {
       const int64_t t = *t_dev + 1;
       *t_dev = t;
-      bc[0] = (float)(1.0 - pow(beta1, (double)t));
-      bc[1] = (float)(1.0 - pow(beta2, (double)t));
+      bc[0] = (float)(1.0 / (1.0 - pow(beta1, (double)t)));   // reciprocal bias corrections (A15)
+      bc[1] = (float)(1.0 / (1.0 - pow(beta2, (double)t)));
     }
   }
 }
@@ -678,31 +666,30 @@ void launch_pair_fwd(int kind, const ScoreArgs &a, int nout, bool train, cudaStr
 
 template <class Mdl>
 static void launch_bwd(ScoreArgs a, cudaStream_t st, cudaStream_t st2) {
+  (void)st2;
+  constexpr int JB = kBW * kJW;
   const int qstride = Mdl::QF * a.U;
-  // dQ: reduction over the pool
-  {
-    const int tiles = ((a.U + 31) / 32) * ((a.NQ + 63) / 64);
-    const int chunks = (a.K + 31) / 32;
-    a.JS = split_for(tiles, chunks, a.cap_Q, (int64_t)a.NQ * qstride);
-    a.jps = ((chunks + a.JS - 1) / a.JS) * 32;
-    a.JS = (a.K + a.jps - 1) / a.jps;
-    dim3 g((a.U + 31) / 32, (a.NQ + 63) / 64, a.JS);
-    { pair_bwd_q_kernel<Mdl><<<g, 256, 0, st>>>(a); ++g_launches; }
-    const int64_t n = (int64_t)a.NQ * qstride;
-    { bwd_q_combine_kernel<Mdl::kBeta><<<(int)((n + 255) / 256), 256, 0, st>>>(a, qstride); ++g_launches; }
+  const int kt = (a.U + 31) / 32, jt = (a.K + JB - 1) / JB;
+  a.JS = jt;                                   // dQ partials: one per j-block
+  const int chunks = (a.NQ + kIC - 1) / kIC;
+  int is = (4 * 148 + kt * jt - 1) / (kt * jt);
+  is = std::max(1, std::min(is, std::min(16, chunks)));
+  while (is > 1 && (int64_t)is * a.K * Mdl::AV * a.U > a.cap_V) --is;
+  a.rps = ((chunks + is - 1) / is) * kIC;
+  a.RS = (a.NQ + a.rps - 1) / a.rps;
+  if (Mdl::kBeta) launch_colsum(a.C, a.NQ, a.K, a.Kp, a.Cpart, st);   // sum_r C_rj
+  const size_t smem = sizeof(float) * (kIC * JB + kIC * Mdl::QF * 32 + kBW * kIC * Mdl::QF * 32);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(pair_bwd_kernel<Mdl>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
   }
-  // dV: reduction over the query rows (independent of dQ: second stream)
-  {
-    const int tiles = ((a.U + 31) / 32) * ((a.K + 63) / 64);
-    const int chunks = (a.NQ + 31) / 32;
-    a.RS = split_for(tiles, chunks, a.cap_V, (int64_t)a.K * Mdl::AV * a.U);
-    a.rps = ((chunks + a.RS - 1) / a.RS) * 32;
-    a.RS = (a.NQ + a.rps - 1) / a.rps;
-    dim3 g((a.U + 31) / 32, (a.K + 63) / 64, a.RS);
-    { pair_bwd_v_kernel<Mdl><<<g, 256, 0, st2>>>(a); ++g_launches; }
-    const int64_t n = (int64_t)a.K * a.U;
-    { bwd_v_combine_kernel<Mdl><<<(int)((n + 255) / 256), 256, 0, st2>>>(a); ++g_launches; }
-  }
+  dim3 g(kt, jt, a.RS);
+  { pair_bwd_kernel<Mdl><<<g, kBW * 32, smem, st>>>(a); ++g_launches; }
+  const int64_t nq = (int64_t)a.NQ * qstride;
+  { bwd_q_combine_kernel<Mdl::kBeta, Mdl::kRowAlpha><<<(int)((nq + 255) / 256), 256, 0, st>>>(a, qstride); ++g_launches; }
+  const int64_t nv = (int64_t)a.K * a.U;
+  { bwd_v_combine_kernel<Mdl><<<(int)((nv + 255) / 256), 256, 0, st>>>(a); ++g_launches; }
 }
 
 void launch_pair_bwd(int kind, const ScoreArgs &a, cudaStream_t st, cudaStream_t st2) {

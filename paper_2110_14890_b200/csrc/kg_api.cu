@@ -294,7 +294,7 @@ void carve(kg_handle *h, Arena &A) {
     const int64_t one = 2LL * Mx * KK;
     int64_t ks = std::max<int64_t>(1, std::min<int64_t>(8, (64LL << 20) / std::max<int64_t>(one, 1)));
     h->cap_D = one * ks;
-    h->cap_Q = 2LL * Mx * dq * 8;
+    h->cap_Q = 2LL * Mx * dq * std::max<int64_t>(1, (std::max(Kx, h->Cx) + 63) / 64);   // one dQ partial per >= 64 pool entries
     h->cap_V = (int64_t)std::max(Kx, h->Cx) * d * 8;
     h->Dpart = A.take<float>(h->cap_D);
     h->partQ = A.take<float>(h->cap_Q);
@@ -843,18 +843,12 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   if (h->apply) {
     const double b1 = h->cfg.beta1, b2 = h->cfg.beta2, eps = h->cfg.eps;
     const float *lr = h->lr_dev;
-    if (h->kind == KG_Q2B) {
-      launch_dense_adam_rel(dp(h, "rel_center"), h->t.dense_m + seg_of(h, "rel_center")->off,
-                            h->t.dense_v + seg_of(h, "rel_center")->off, h->R, d, h->RGU, h->dr, 0, h->rel_seg_map,
-                            h->rel_stamp, h->stamp_dev, lr, b1, b2, eps, h->bc, h->flags, st);
-      launch_dense_adam_rel(dp(h, "rel_offset"), h->t.dense_m + seg_of(h, "rel_offset")->off,
-                            h->t.dense_v + seg_of(h, "rel_offset")->off, h->R, d, h->RGU, h->dr, d, h->rel_seg_map,
-                            h->rel_stamp, h->stamp_dev, lr, b1, b2, eps, h->bc, h->flags, st);
-    } else {
+    {
+      // relation tables: segs[0] (and segs[1] for Q2B: rel_offset right after rel_center)
       const Seg &r = h->segs[0];
-      launch_dense_adam_rel(h->t.dense + r.off, h->t.dense_m + r.off, h->t.dense_v + r.off, h->R, r.cols, h->RGU,
-                            h->dr, 0, h->rel_seg_map, h->rel_stamp, h->stamp_dev, lr, b1, b2, eps, h->bc, h->flags,
-                            st);
+      const int nseg = h->kind == KG_Q2B ? 2 : 1;
+      launch_dense_adam_rel(h->t.dense + r.off, h->t.dense_m + r.off, h->t.dense_v + r.off, h->R, r.cols, nseg,
+                            h->RGU, h->rel_seg_map, h->rel_stamp, h->stamp_dev, lr, b1, b2, eps, h->bc, h->flags, st);
     }
     launch_dense_adam(h->t.dense + h->w_off, h->t.dense_m + h->w_off, h->t.dense_v + h->w_off, h->gdense,
                       h->dense_size - h->w_off, lr, b1, b2, eps, h->bc, h->flags, st);

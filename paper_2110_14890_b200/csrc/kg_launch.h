@@ -70,11 +70,12 @@ void launch_rel_reduce(const int32_t *seg, const int32_t *perm, const int32_t *i
                        const float *RG, float *PS, int dr, float *RGU, cudaStream_t st);
 void launch_rel_stamp(const int64_t *uniq_rel, const int32_t *U_dev, int Lmax, int32_t *rel_seg, int64_t *rel_stamp,
                       const int64_t *stamp, cudaStream_t st);
-void launch_dense_adam_rel(float *p, float *m, float *v, int R, int width, const float *RGU, int rg_stride,
-                           int rg_col, const int32_t *rel_seg, const int64_t *rel_stamp, const int64_t *stamp,
-                           const float *lr, double beta1, double beta2, double eps, const float *bc, const int *flags, cudaStream_t st);
-void launch_dense_adam(float *p, float *m, float *v, const float *g, int64_t n, const float *lr, double beta1, double beta2,
-                       double eps, const float *bc, const int *flags, cudaStream_t st);
+void launch_dense_adam_rel(float *p, float *m, float *v, int R, int width, int nseg, const float *RGU,
+                           const int32_t *rel_seg, const int64_t *rel_stamp, const int64_t *stamp, const float *lr,
+                           double beta1, double beta2, double eps, const float *bc, const int *flags,
+                           cudaStream_t st);
+void launch_dense_adam(float *p, float *m, float *v, const float *g, int64_t n, const float *lr, double beta1,
+                       double beta2, double eps, const float *bc, const int *flags, cudaStream_t st);
 void launch_colsum(const float *X, int rows, int cols, int ld, float *out, cudaStream_t st);
 
 // k_dag.cu
