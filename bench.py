@@ -134,13 +134,20 @@ def run_ours(args, world, rank, local):
     w = kggen.WORKLOADS[args.workload]
     cfg = w.model_config()
     if args.workload.startswith("C5"):
-        # constant per-GPU shard: each rank holds ceil(|V|/8) rows.
-        # TODO(next): row-sharded all-to-all exchange for world > 1.
-        cfg.n_entities = kggen.shard_rows(w.n_entities, 8)
+        # constant per-GPU shard: theta_E of min(|V|, G * ceil(|V|/8)) rows,
+        # row-sharded over the G ranks (full Freebase at G = 8)
+        cfg.n_entities = min(w.n_entities, world * kggen.shard_rows(w.n_entities, 8))
     M, K = w.M, w.K
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    gm = KGModel(cfg, M, K)
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+        from paper_2110_14890_b200 import nccl_unique_id
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    gm = KGModel(cfg, M, K, rank=rank, world=world, nccl_id=nccl_id)
     gm.init_params(args.seed)
     gm.set_apply(True)
     lr = args.lr
@@ -252,9 +259,12 @@ def run_ours(args, world, rank, local):
         "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 5), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (kggen, seeded)",
         "config": {"workload": args.workload, "model": cfg.kind, "dim": cfg.dim,
-                   "entities_per_gpu": cfg.n_entities, "relations": cfg.n_relations,
+                   "entities": cfg.n_entities, "entities_per_gpu": kggen.shard_rows(cfg.n_entities, world),
+                   "relations": cfg.n_relations,
                    "global_batch": M * world, "negatives_per_gpu": K, "structures": structures,
-                   "lr": lr, "parallelism": f"dp{world}" if world > 1 else "single",
+                   "lr": lr, "parallelism": (f"dp{world} + theta_E row-sharded (owner = id % {world}), "
+                                             "NCCL exchange of rows / row gradients, all-reduce of dL/dtheta_D")
+                   if world > 1 else "single",
                    "l2": "flushed between timed steps (256 MB write outside the step events)",
                    "note": w.note},
         "e2e": e2e, "roofline": roof, "gpu_launches": int(kernels_per_step * args.steps),

@@ -185,6 +185,10 @@ kg_status kg_set_apply(kg_handle *h, int32_t flags);
 
 const char *kg_last_error(const kg_handle *h);
 
+/* world > 1: rank 0 creates the 128-byte NCCL unique id (written to out) and shares it with
+ * the other ranks (e.g. torch.distributed broadcast) before every rank calls kg_create. */
+kg_status kg_nccl_unique_id(void *out);
+
 /* Release everything the library owns; never frees caller memory.  NULL is a no-op. */
 void kg_destroy(kg_handle *h);
 

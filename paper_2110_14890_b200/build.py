@@ -1,6 +1,7 @@
 """Build libkg.so (all CUDA sources of csrc/) for sm_100a with nvcc, in-tree.
 
-python -m paper_2110_14890_b200.build   (also called by __graft_entry__.build())
+python paper_2110_14890_b200/build.py [-f] [-v]   (also called by __graft_entry__.build();
+run as a file: importing the package itself requires the built library)
 """
 import os
 import subprocess
@@ -12,8 +13,26 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libkg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+def _nccl_dir():
+    """torch's bundled NCCL (headers + the library torch itself loads)."""
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        if spec and spec.submodule_search_locations:
+            d = list(spec.submodule_search_locations)[0]
+            if os.path.exists(os.path.join(d, "include", "nccl.h")):
+                return d
+    except Exception:
+        pass
+    return None
+
+
+NCCL_DIR = _nccl_dir()
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills", "-I", os.path.join(ROOT, "include")]
+if NCCL_DIR:
+    FLAGS += ["-I", os.path.join(NCCL_DIR, "include"),
+              f'-DKG_NCCL_PATH="{os.path.join(NCCL_DIR, "lib", "libnccl.so.2")}"']
 
 
 def sources():
@@ -44,7 +63,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
             raise RuntimeError(f"nvcc failed on {s}")
         if verbose and out:
             sys.stderr.write(out.decode())
-    cmd = [NVCC, *ARCH, "-shared", "-o", OUT + ".tmp", *objs, "-lcublas", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", OUT + ".tmp", *objs, "-lcublas", "-ldl", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
     subprocess.run(cmd, check=True)
     os.replace(OUT + ".tmp", OUT)
     return OUT

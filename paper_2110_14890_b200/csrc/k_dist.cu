@@ -1,0 +1,145 @@
+// k_dist.cu -- row-sharded theta_E across ranks: routing kernels
+// for the request / row / gradient exchange around the NCCL calls of kg_api.cu.
+//
+// PAPER.md §4.1: one worker per GPU; the paper keeps theta_E in host
+// memory with hogwild updates; this build row-shards theta_E and its
+// Adam state over the GPUs (owner(id) = id % G, local row = id / G) and keeps
+// the update synchronous (reading A18).  Every order below is a fixed function
+// of the inputs (deterministic merges, no atomics).
+#include "kg_common.cuh"
+#include "kg_launch.h"
+
+namespace kg {
+
+constexpr int kPartThreads = 1024;
+
+// Stable partition of the distinct ids (ascending) by owner: send_ids[pos] = uniq[u]
+// with pos = offset[owner] + (rank of u among the ids of that owner); send_pos[u] = pos;
+// counts[o] = number of distinct ids owned by o.  One CTA; per-thread contiguous
+// ranges keep the order stable.
+__global__ void __launch_bounds__(kPartThreads) owner_partition_kernel(const int64_t *uniq, const int32_t *U_dev,
+                                                                       int G, int64_t *send_ids, int32_t *send_pos,
+                                                                       int32_t *counts) {
+  __shared__ int32_t s_cnt[kMaxWorld][kPartThreads];
+  __shared__ int32_t s_base[kMaxWorld + 1];
+  const int U = *U_dev, t = threadIdx.x;
+  const int per = (U + kPartThreads - 1) / kPartThreads;
+  const int b = t * per, e = min(U, b + per);
+  int c[kMaxWorld];
+#pragma unroll
+  for (int o = 0; o < kMaxWorld; ++o) c[o] = 0;
+  for (int u = b; u < e; ++u) {
+    const int o = (int)(uniq[u] % G);
+#pragma unroll
+    for (int q = 0; q < kMaxWorld; ++q) c[q] += (q == o);
+  }
+#pragma unroll
+  for (int o = 0; o < kMaxWorld; ++o) s_cnt[o][t] = c[o];
+  __syncthreads();
+  if (t < G) {   // exclusive scan over threads for owner t (serial, fixed order)
+    int run = 0;
+    for (int k = 0; k < kPartThreads; ++k) {
+      const int v = s_cnt[t][k];
+      s_cnt[t][k] = run;
+      run += v;
+    }
+    counts[t] = run;
+    s_base[t + 1] = run;
+  }
+  __syncthreads();
+  if (t == 0) {
+    s_base[0] = 0;
+    for (int o = 1; o <= G; ++o) s_base[o] += s_base[o - 1];
+  }
+  __syncthreads();
+  int run[kMaxWorld];
+#pragma unroll
+  for (int o = 0; o < kMaxWorld; ++o) run[o] = (o < G) ? s_base[o] + s_cnt[o][t] : 0;
+  for (int u = b; u < e; ++u) {
+    const int o = (int)(uniq[u] % G);
+    int pos = 0;
+#pragma unroll
+    for (int q = 0; q < kMaxWorld; ++q)
+      if (q == o) pos = run[q]++;
+    send_ids[pos] = uniq[u];
+    send_pos[u] = pos;
+  }
+}
+
+void launch_owner_partition(const int64_t *uniq, const int32_t *U_dev, int G, int64_t *send_ids, int32_t *send_pos,
+                            int32_t *counts, cudaStream_t st) {
+  { owner_partition_kernel<<<1, kPartThreads, 0, st>>>(uniq, U_dev, G, send_ids, send_pos, counts); ++g_launches; }
+}
+
+// rows[p] = send_pos[inv[p]]: the occurrence's row in the received (owner-grouped) row buffer.
+__global__ void occ_rows_kernel(const int32_t *inv, const int32_t *send_pos, int L, int64_t *rows) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < L) rows[p] = send_pos[inv[p]];
+}
+void launch_occ_rows(const int32_t *inv, const int32_t *send_pos, int L, int64_t *rows, cudaStream_t st) {
+  if (L > 0) { occ_rows_kernel<<<(L + 255) / 256, 256, 0, st>>>(inv, send_pos, L, rows); ++g_launches; }
+}
+
+// Owner side: out[i] = theta_E[ids[i] / G] (rows requested by the peers, in receive order).
+__global__ void gather_owned_kernel(const float *ent, const int64_t *ids, int n, int G, int d4, float4 *out) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)n * d4) return;
+  const int i = (int)(e / d4), c = (int)(e - (int64_t)i * d4);
+  out[e] = reinterpret_cast<const float4 *>(ent)[(ids[i] / G) * d4 + c];
+}
+void launch_gather_owned(const float *ent, const int64_t *ids, int n, int G, int d, float *out, cudaStream_t st) {
+  const int64_t m = (int64_t)n * (d / 4);
+  if (m > 0) {
+    gather_owned_kernel<<<(int)((m + 255) / 256), 256, 0, st>>>(ent, ids, n, G, d / 4, reinterpret_cast<float4 *>(out));
+    ++g_launches;
+  }
+}
+
+// out[send_pos[u]] = G[u] (merged row gradients in send order).
+__global__ void reorder_rows_kernel(const float4 *Gu, const int32_t *send_pos, const int32_t *U_dev, int d4,
+                                    float4 *out) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int u = (int)(e / d4), c = (int)(e - (int64_t)u * d4);
+  if (u >= *U_dev) return;
+  out[(int64_t)send_pos[u] * d4 + c] = Gu[e];
+}
+void launch_reorder_rows(const float *Gu, const int32_t *send_pos, const int32_t *U_dev, int Lmax, int d, float *out,
+                         cudaStream_t st) {
+  const int64_t m = (int64_t)Lmax * (d / 4);
+  if (m > 0) {
+    reorder_rows_kernel<<<(int)((m + 255) / 256), 256, 0, st>>>(reinterpret_cast<const float4 *>(Gu), send_pos, U_dev,
+                                                                d / 4, reinterpret_cast<float4 *>(out));
+    ++g_launches;
+  }
+}
+
+// keys[i] = ids[i] / G (owner-local rows of the received ids, for the owner-side merge).
+__global__ void local_rows_kernel(const int64_t *ids, int n, int G, int64_t *keys) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) keys[i] = ids[i] / G;
+}
+void launch_local_rows(const int64_t *ids, int n, int G, int64_t *keys, cudaStream_t st) {
+  if (n > 0) { local_rows_kernel<<<(n + 255) / 256, 256, 0, st>>>(ids, n, G, keys); ++g_launches; }
+}
+
+// Dense relation gradient (for the all-reduce): gfull[s*R*w + r*w + c] = RGU[u][s*w + c]
+// for the relations used by this rank (the caller zeroes the relation part first).
+__global__ void scatter_rel_kernel(const float *RGU, const int64_t *runiq, const int32_t *rU, int R, int w, int nseg,
+                                   float *gfull) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int dr = w * nseg;
+  const int u = (int)(e / dr), c = (int)(e - (int64_t)u * dr);
+  if (u >= *rU) return;
+  const int s = c / w, cc = c - s * w;
+  gfull[(int64_t)s * R * w + runiq[u] * w + cc] = RGU[e];
+}
+void launch_scatter_rel(const float *RGU, const int64_t *runiq, const int32_t *rU, int Lrmax, int R, int w, int nseg,
+                        float *gfull, cudaStream_t st) {
+  const int64_t m = (int64_t)Lrmax * w * nseg;
+  if (m > 0) {
+    scatter_rel_kernel<<<(int)((m + 255) / 256), 256, 0, st>>>(RGU, runiq, rU, R, w, nseg, gfull);
+    ++g_launches;
+  }
+}
+
+}  // namespace kg

@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(128) beta_query_kernel(const float *Q, int NQ,
 __global__ void __launch_bounds__(256) loss_finalize_kernel(const float *loss_pos, const float *loss_part, int M,
                                                             int njt, double scale, double *loss_out,
                                                             int *flags, int64_t *t_dev, float *bc,
-                                                            double beta1, double beta2, int apply) {
+                                                            double beta1, double beta2, int apply, int check) {
   __shared__ double red[256];
   double s = 0.0;
   for (int i = threadIdx.x; i < M; i += 256) {
@@ -608,7 +608,8 @@ __global__ void __launch_bounds__(256) loss_finalize_kernel(const float *loss_po
     if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && !check) *loss_out = red[0] * scale;   // world > 1: summed over ranks, then loss_check
+  if (threadIdx.x == 0 && check) {
     const double loss = red[0] * scale;
     // flags[1]: an input id / relation was out of range (device-side validation);
     // flags[0]: skip every update of this step (non-finite loss or bad input).
@@ -729,9 +730,27 @@ void launch_beta_query(const float *Q, int NQ, int m, float *QP, float *Cq, cuda
 }
 void launch_loss_finalize(const float *loss_pos, const float *loss_part, int M, int njt, double scale,
                           double *loss_out, int *flags, int64_t *t_dev, float *bc, double beta1, double beta2,
-                          int apply, cudaStream_t st) {
+                          int apply, cudaStream_t st, int check) {
   { loss_finalize_kernel<<<1, 256, 0, st>>>(loss_pos, loss_part, M, njt, scale, loss_out, flags, t_dev, bc,
-                                          beta1, beta2, apply); ++g_launches; }
+                                          beta1, beta2, apply, check); ++g_launches; }
+}
+
+// After the cross-rank sum of the loss and max of the input flags (world > 1).
+__global__ void loss_check_kernel(double *loss_out, int *flags, int64_t *t_dev, float *bc, double beta1, double beta2,
+                                  int apply) {
+  const double loss = *loss_out;
+  const int bad = !isfinite(loss) || flags[1];
+  flags[0] = bad;
+  if (!bad && apply) {
+    const int64_t t = *t_dev + 1;
+    *t_dev = t;
+    bc[0] = (float)(1.0 / (1.0 - pow(beta1, (double)t)));
+    bc[1] = (float)(1.0 / (1.0 - pow(beta2, (double)t)));
+  }
+}
+void launch_loss_check(double *loss_out, int *flags, int64_t *t_dev, float *bc, double beta1, double beta2, int apply,
+                       cudaStream_t st) {
+  { loss_check_kernel<<<1, 1, 0, st>>>(loss_out, flags, t_dev, bc, beta1, beta2, apply); ++g_launches; }
 }
 
 }  // namespace kg

@@ -6,6 +6,8 @@
 // (§4.1, §4.2, §4.3).
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -13,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/kg.h"
@@ -25,6 +28,54 @@ int64_t g_launches = 0;
 }
 
 namespace {
+
+// ------------------------------------------------------------------ NCCL (world > 1 only)
+// NCCL is resolved at run time (dlopen) so that single-GPU use has no NCCL
+// dependency and so that the library binds to the NCCL that torch already
+// loaded (RTLD_NOLOAD) instead of a second, different copy.
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+const NcclApi &nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void *lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+#ifdef KG_NCCL_PATH
+  if (!lib) lib = dlopen(KG_NCCL_PATH, RTLD_NOW | RTLD_GLOBAL);
+#endif
+  if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!lib) return api;
+  bool all = true;
+  auto get = [&](auto &fp, const char *name) {
+    fp = reinterpret_cast<std::remove_reference_t<decltype(fp)>>(dlsym(lib, name));
+    all = all && fp;
+  };
+  get(api.GetUniqueId, "ncclGetUniqueId");
+  get(api.CommInitRank, "ncclCommInitRank");
+  get(api.CommDestroy, "ncclCommDestroy");
+  get(api.AllGather, "ncclAllGather");
+  get(api.AllReduce, "ncclAllReduce");
+  get(api.Send, "ncclSend");
+  get(api.Recv, "ncclRecv");
+  get(api.GroupStart, "ncclGroupStart");
+  get(api.GroupEnd, "ncclGroupEnd");
+  get(api.GetErrorString, "ncclGetErrorString");
+  api.ok = all;
+  return api;
+}
 
 // ------------------------------------------------------------------ plans
 struct PNode {
@@ -154,6 +205,15 @@ struct kg_handle {
   std::vector<GraphEntry> graphs;
   bool use_graphs = true;
   void *blas_ws = nullptr;
+  // row-sharded exchange (world > 1, k_dist.cu)
+  ncclComm_t comm = nullptr;
+  const float *ent_src = nullptr;       // rows read by the step: theta_E (world 1) or the received rows
+  float *gfull = nullptr;               // dense dL/dtheta_D [dense_size] (weights part = gdense)
+  int64_t *send_ids = nullptr, *recv_ids = nullptr, *recv_keys = nullptr, *ouniq = nullptr;
+  int32_t *send_pos = nullptr, *counts = nullptr, *all_counts = nullptr, *oinv = nullptr, *operm = nullptr,
+          *oseg = nullptr, *oU = nullptr;
+  float *Xin = nullptr, *send_rows = nullptr, *Gsend = nullptr, *Grecv = nullptr, *PSo = nullptr;
+  int32_t *h_counts = nullptr;           // pinned [G*G]
   int flag_key() const { return apply | (keep_grads << 1) | (timing << 2); }
 
   // pinned staging (double-buffered) + host mirrors of the step results
@@ -282,7 +342,8 @@ void carve(kg_handle *h, Arena &A) {
   h->Gc = A.take<float>((int64_t)h->Lx * d);
   h->PS = A.take<float>((int64_t)h->Lx * d);
   h->PSr = A.take<float>((int64_t)h->Lrx * h->dr);
-  h->gdense = A.take<float>(h->dense_size - h->w_off);
+  h->gfull = A.take<float>(h->dense_size);
+  h->gdense = h->gfull + h->w_off;
   h->Q = A.take<float>((int64_t)NQ * dq);
   h->dQ = A.take<float>((int64_t)NQ * dq);
   h->C = A.take<float>((int64_t)NQ * h->Kpx);
@@ -339,6 +400,25 @@ void carve(kg_handle *h, Arena &A) {
     h->pdX = A.take<float>((int64_t)Mx * 2 * d);
   }
   h->Dscore = A.take<float>((int64_t)Mx * std::max(h->Cx, 1));
+  if (h->world > 1) {
+    const int64_t GL = (int64_t)h->world * h->Lx;
+    h->send_ids = A.take<int64_t>(h->Lx);
+    h->send_pos = A.take<int32_t>(h->Lx);
+    h->counts = A.take<int32_t>(kMaxWorld);
+    h->all_counts = A.take<int32_t>(kMaxWorld * kMaxWorld);
+    h->recv_ids = A.take<int64_t>(GL);
+    h->recv_keys = A.take<int64_t>(GL);
+    h->ouniq = A.take<int64_t>(GL);
+    h->oinv = A.take<int32_t>(GL);
+    h->operm = A.take<int32_t>(GL);
+    h->oseg = A.take<int32_t>(GL + 1);
+    h->oU = A.take<int32_t>(1);
+    h->Xin = A.take<float>((int64_t)h->Lx * d);
+    h->send_rows = A.take<float>(GL * d);
+    h->Gsend = A.take<float>((int64_t)h->Lx * d);
+    h->Grecv = A.take<float>(GL * d);
+    h->PSo = A.take<float>(GL * d);
+  }
 }
 
 // Row-major GEMM: C[m x n] = op(A) op(B) + beta C, op(A) is [m x k].
@@ -368,7 +448,7 @@ kg_status dag_forward(kg_handle *h, StepBufs &S) {
   const Plan &p = S.plan;
   const int M = S.M, d = h->d, dq = h->dq, m = h->m, HH = h->H;
   cudaStream_t st = h->st;
-  const float *ent = h->t.ent;
+  const float *ent = h->ent_src;
   int u = 0;
   for (int ni = 0; ni < p.nn; ++ni) {
     const PNode &nd = p.n[ni];
@@ -432,7 +512,7 @@ kg_status dag_backward(kg_handle *h, StepBufs &S) {
   const Plan &p = S.plan;
   const int M = S.M, d = h->d, dq = h->dq, m = h->m, HH = h->H;
   cudaStream_t st = h->st;
-  const float *ent = h->t.ent;
+  const float *ent = h->ent_src;
   // projection-use index of each node
   int use[6], u = 0;
   for (int ni = 0; ni < p.nn; ++ni) use[ni] = p.n[ni].type == 0 ? u++ : -1;
@@ -662,7 +742,8 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
     return KG_EINVAL;
   const int Lx = 3 * c.max_M + c.max_M + std::max(c.max_K, c.max_cand);
   if (Lx > dedup_capacity()) return KG_EINVAL;
-  if (c.world > 1) return KG_EUNSUPPORTED;   // multi-GPU path: see DESIGN.md §7 (next)
+  if (c.world > kMaxWorld || (c.world > 1 && !c.nccl_id)) return KG_EINVAL;
+  if ((int64_t)c.world * Lx > dedup_capacity()) return KG_EINVAL;
 
   kg_handle *h = new kg_handle();
   h->cfg = c;
@@ -704,6 +785,13 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
   if (cublasSetWorkspace(h->blas, h->blas_ws, 32 << 20) != CUBLAS_STATUS_SUCCESS) { kg_destroy(h); return KG_ECUDA; }
+  if (c.world > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, c.nccl_id, sizeof(id));
+    if (!nccl().ok || nccl().CommInitRank(&h->comm, c.world, id, c.rank) != ncclSuccess) { kg_destroy(h); return KG_ENCCL; }
+    if (cudaMallocHost(&h->h_counts, sizeof(int32_t) * kMaxWorld * kMaxWorld) != cudaSuccess) { kg_destroy(h); return KG_ENOMEM; }
+    h->use_graphs = false;   // the exchange sizes are read on the host every step
+  }
   if (const char *e = std::getenv("KG_NO_GRAPH")) h->use_graphs = !(e[0] == '1');
   cublasSetMathMode(h->blas, CUBLAS_PEDANTIC_MATH);   // true fp32, no TF32 (parity at 1e-5, A24)
   // device scalars
@@ -760,6 +848,7 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   const int M = S.M, K = S.K, d = h->d, na = p.na, nr = p.nr;
   const int L = na * M + M + K, Lr = p.nproj * M;
   cudaStream_t st = h->st;
+  h->ent_src = h->t.ent;
   mark(h, 0);
   // a2: ids (fused gather indices) on the main stream; dedup of entities and relations
   // on the side stream -- only the sparse update at the end needs them
@@ -790,17 +879,17 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   const float scale = 1.f / (float)((double)M * h->world);
   if (h->kind == KG_BETAE) {
     launch_beta_query(h->Q, S.NQ, h->m, h->QP, h->Cq, st);
-    launch_beta_entity(h->t.ent, neg_rows, K, h->m, h->F, h->Cv, st);
+    launch_beta_entity(h->ent_src, neg_rows, K, h->m, h->F, h->Cv, st);
   }
   PosArgs pa;
-  pa.M = M; pa.U = U; pa.d = d; pa.ent = h->t.ent; pa.ans_rows = h->rows + (int64_t)na * M; pa.Q = h->Q;
+  pa.M = M; pa.U = U; pa.d = d; pa.ent = h->ent_src; pa.ans_rows = h->rows + (int64_t)na * M; pa.Q = h->Q;
   pa.alpha = h->cfg.box_alpha; pa.gamma = h->cfg.gamma; pa.scale = scale; pa.Cq = h->Cq; pa.QP = h->QP;
   pa.loss_pos = h->loss_pos; pa.Dpos = h->Dpos; pa.dQ = h->dQ; pa.dV = h->OG + (int64_t)na * M * d;
   launch_pos(h->kind, pa, p.nout, st);
   ScoreArgs sa;
   sa.Q = h->Q; sa.NQ = S.NQ; sa.M = M; sa.K = K; sa.Kp = S.Kp; sa.U = U; sa.d = d;
   if (h->kind == KG_BETAE) { sa.E = h->F; sa.eidx = nullptr; sa.estride = 9LL * h->m; }
-  else { sa.E = h->t.ent; sa.eidx = neg_rows; sa.estride = d; }
+  else { sa.E = h->ent_src; sa.eidx = neg_rows; sa.estride = d; }
   sa.mask = h->b_mask; sa.W = (K + 31) / 32; sa.Cq = h->Cq; sa.Cv = h->Cv; sa.QP = h->QP;
   sa.gamma = h->cfg.gamma; sa.alpha = h->cfg.box_alpha; sa.scale = scale;
   sa.C = h->C; sa.Dmin = h->Dmin; sa.loss_part = h->loss_part; sa.dQ = h->dQ;
@@ -863,6 +952,146 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   return KG_OK;
 }
 
+#define NCK(call)                                                                                \
+  do {                                                                                           \
+    ncclResult_t r_ = (call);                                                                    \
+    if (r_ != ncclSuccess) return fail(h, KG_ENCCL, std::string(#call) + ": " + nccl().GetErrorString(r_)); \
+  } while (0)
+
+// One step with theta_E row-sharded over G ranks (reading A18):
+// requests of the distinct ids go to their owners, owners return the rows, the
+// step runs on the received rows, merged row gradients go back to the owners,
+// which sum the contributions of all ranks in (source rank, position) order and
+// apply Adam; dL/dtheta_D (relations + weights) is all-reduced and every rank
+// applies the same dense Adam.  Collective: all ranks call it with the same
+// structure, M and K.
+kg_status step_dist(kg_handle *h, StepBufs &S) {
+  kg_status s;
+  const Plan &p = S.plan;
+  const int M = S.M, K = S.K, d = h->d, na = p.na, nr = p.nr, G = h->world, me = h->rank;
+  const int L = na * M + M + K, Lr = p.nproj * M;
+  cudaStream_t st = h->st;
+  mark(h, 0);
+  CK(cudaMemsetAsync(h->flags, 0, 2 * sizeof(int), st));
+  launch_ids_concat(h->b_anchors, na, M, h->b_answers, M, h->b_negs, K, G, h->ids, h->rows, h->flags + 1, h->n_ent,
+                    st);
+  Slots4 sl{{0, 0, 0, 0}};
+  {
+    int u = 0;
+    for (int ni = 0; ni < p.nn; ++ni)
+      if (p.n[ni].type == 0) sl.s[u++] = p.n[ni].rel;
+  }
+  launch_rel_occ(h->b_rels, M, nr, sl, p.nproj, h->R, h->rocc, h->flags + 1, st);
+  launch_dedup(h->ids, nullptr, L, h->ent_bits, h->uniq, h->inv, h->perm, h->seg, h->Udev, st);
+  launch_dedup(nullptr, h->rocc, Lr, h->rel_bits, h->runiq, h->rinv, h->rperm, h->rseg, h->rU, st);
+  // a3: route the distinct ids to their owners (owner = id % G)
+  launch_owner_partition(h->uniq, h->Udev, G, h->send_ids, h->send_pos, h->counts, st);
+  NCK(nccl().AllGather(h->counts, h->all_counts, kMaxWorld, ncclInt32, h->comm, st));
+  CK(cudaMemcpyAsync(h->h_counts, h->all_counts, sizeof(int32_t) * kMaxWorld * G, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<int64_t> so(G + 1, 0), ro(G + 1, 0);   // send / receive offsets (rows)
+  for (int o = 0; o < G; ++o) {
+    so[o + 1] = so[o] + h->h_counts[me * kMaxWorld + o];
+    ro[o + 1] = ro[o] + h->h_counts[o * kMaxWorld + me];
+  }
+  const int Rtot = (int)ro[G];
+  NCK(nccl().GroupStart());
+  for (int o = 0; o < G; ++o) {
+    if (so[o + 1] > so[o]) NCK(nccl().Send(h->send_ids + so[o], so[o + 1] - so[o], ncclInt64, o, h->comm, st));
+    if (ro[o + 1] > ro[o]) NCK(nccl().Recv(h->recv_ids + ro[o], ro[o + 1] - ro[o], ncclInt64, o, h->comm, st));
+  }
+  NCK(nccl().GroupEnd());
+  launch_gather_owned(h->t.ent, h->recv_ids, Rtot, G, d, h->send_rows, st);
+  NCK(nccl().GroupStart());
+  for (int o = 0; o < G; ++o) {
+    if (ro[o + 1] > ro[o]) NCK(nccl().Send(h->send_rows + ro[o] * d, (ro[o + 1] - ro[o]) * d, ncclFloat32, o, h->comm, st));
+    if (so[o + 1] > so[o]) NCK(nccl().Recv(h->Xin + so[o] * d, (so[o + 1] - so[o]) * d, ncclFloat32, o, h->comm, st));
+  }
+  NCK(nccl().GroupEnd());
+  launch_occ_rows(h->inv, h->send_pos, L, h->rows, st);
+  h->ent_src = h->Xin;
+
+  // a4-a10 on the received rows (as for one rank)
+  mark(h, 1);
+  assign_buffers(h, S);
+  if ((s = dag_forward(h, S)) != KG_OK) return s;
+  mark(h, 2);
+  const int U = (h->kind == KG_BETAE || h->kind == KG_ROTATE || h->kind == KG_COMPLEX) ? h->m : d;
+  const int64_t *neg_rows = h->rows + (int64_t)na * M + M;
+  const float scale = 1.f / (float)((double)M * G);
+  if (h->kind == KG_BETAE) {
+    launch_beta_query(h->Q, S.NQ, h->m, h->QP, h->Cq, st);
+    launch_beta_entity(h->ent_src, neg_rows, K, h->m, h->F, h->Cv, st);
+  }
+  PosArgs pa;
+  pa.M = M; pa.U = U; pa.d = d; pa.ent = h->ent_src; pa.ans_rows = h->rows + (int64_t)na * M; pa.Q = h->Q;
+  pa.alpha = h->cfg.box_alpha; pa.gamma = h->cfg.gamma; pa.scale = scale; pa.Cq = h->Cq; pa.QP = h->QP;
+  pa.loss_pos = h->loss_pos; pa.Dpos = h->Dpos; pa.dQ = h->dQ; pa.dV = h->OG + (int64_t)na * M * d;
+  launch_pos(h->kind, pa, p.nout, st);
+  ScoreArgs sa;
+  sa.Q = h->Q; sa.NQ = S.NQ; sa.M = M; sa.K = K; sa.Kp = S.Kp; sa.U = U; sa.d = d;
+  if (h->kind == KG_BETAE) { sa.E = h->F; sa.eidx = nullptr; sa.estride = 9LL * h->m; }
+  else { sa.E = h->ent_src; sa.eidx = neg_rows; sa.estride = d; }
+  sa.mask = h->b_mask; sa.W = (K + 31) / 32; sa.Cq = h->Cq; sa.Cv = h->Cv; sa.QP = h->QP;
+  sa.gamma = h->cfg.gamma; sa.alpha = h->cfg.box_alpha; sa.scale = scale;
+  sa.C = h->C; sa.Dmin = h->Dmin; sa.loss_part = h->loss_part; sa.dQ = h->dQ;
+  sa.Dpart = h->Dpart; sa.partQ = h->partQ; sa.partV = h->partV; sa.Cpart = h->Cpart; sa.Csum = h->Csum;
+  sa.cap_D = h->cap_D; sa.cap_Q = h->cap_Q; sa.cap_V = h->cap_V;
+  sa.dV = h->OG + (int64_t)(na * M + M) * d;
+  if (K > 0) launch_pair_fwd(h->kind, sa, p.nout, true, st);
+  // global loss = sum over ranks of the (1/(M G))-scaled local sums (A18); one finite check for all
+  launch_loss_finalize(h->loss_pos, h->loss_part, M, K > 0 ? 1 : 0, 1.0 / ((double)M * G), h->loss_dev, h->flags,
+                       h->t_dev, h->bc, h->cfg.beta1, h->cfg.beta2, h->apply, st, /*check=*/0);
+  NCK(nccl().AllReduce(h->loss_dev, h->loss_dev, 1, ncclFloat64, ncclSum, h->comm, st));
+  NCK(nccl().AllReduce(h->flags + 1, h->flags + 1, 1, ncclInt32, ncclMax, h->comm, st));
+  launch_loss_check(h->loss_dev, h->flags, h->t_dev, h->bc, h->cfg.beta1, h->cfg.beta2, h->apply, st);
+  mark(h, 3);
+  if (K > 0) launch_pair_bwd(h->kind, sa, st, st);
+  mark(h, 4);
+  if ((s = dag_backward(h, S)) != KG_OK) return s;
+  if (p.inter < 0 && h->kind != KG_BETAE && h->w_off < h->dense_size)
+    CK(cudaMemsetAsync(h->gdense, 0, sizeof(float) * (h->dense_size - h->w_off), st));
+  if (p.inter < 0 && h->kind == KG_BETAE) {
+    const Seg *a = seg_of(h, "att_U1");
+    CK(cudaMemsetAsync(h->gdense + (a->off - h->w_off), 0, sizeof(float) * (h->dense_size - a->off), st));
+  }
+  mark(h, 5);
+  // a12: merged row gradients of this rank (distinct-id order) -> send order -> owners
+  launch_sparse_adam(h->uniq, h->seg, h->perm, h->inv, h->Udev, L, h->OG, h->PS, d, 1, h->t.ent, h->t.ent_m,
+                     h->t.ent_v, h->Gc, h->lr_dev, h->cfg.beta1, h->cfg.beta2, h->cfg.eps, h->bc, h->flags,
+                     /*apply=*/0, st);
+  launch_reorder_rows(h->Gc, h->send_pos, h->Udev, L, d, h->Gsend, st);
+  NCK(nccl().GroupStart());
+  for (int o = 0; o < G; ++o) {
+    if (so[o + 1] > so[o]) NCK(nccl().Send(h->Gsend + so[o] * d, (so[o + 1] - so[o]) * d, ncclFloat32, o, h->comm, st));
+    if (ro[o + 1] > ro[o]) NCK(nccl().Recv(h->Grecv + ro[o] * d, (ro[o + 1] - ro[o]) * d, ncclFloat32, o, h->comm, st));
+  }
+  NCK(nccl().GroupEnd());
+  // a13 at the owner: merge the contributions of all ranks (fixed order) + sparse Adam on local rows
+  launch_local_rows(h->recv_ids, Rtot, G, h->recv_keys, st);
+  launch_dedup(h->recv_keys, nullptr, Rtot, bits_for(h->shard), h->ouniq, h->oinv, h->operm, h->oseg, h->oU, st);
+  if (h->apply)
+    launch_sparse_adam(h->ouniq, h->oseg, h->operm, h->oinv, h->oU, Rtot, h->Grecv, h->PSo, d, 1, h->t.ent,
+                       h->t.ent_m, h->t.ent_v, nullptr, h->lr_dev, h->cfg.beta1, h->cfg.beta2, h->cfg.eps, h->bc,
+                       h->flags, 1, st);
+  mark(h, 6);
+  // a14: dense dL/dtheta_D -> all-reduce -> dense Adam (identical on every rank)
+  launch_rel_reduce(h->rseg, h->rperm, h->rinv, h->rU, Lr, h->RG, h->PSr, h->dr, h->RGU, st);
+  CK(cudaMemsetAsync(h->gfull, 0, sizeof(float) * h->w_off, st));
+  launch_scatter_rel(h->RGU, h->runiq, h->rU, Lr, h->R, h->segs[0].cols, h->kind == KG_Q2B ? 2 : 1, h->gfull, st);
+  NCK(nccl().AllReduce(h->gfull, h->gfull, h->dense_size, ncclFloat32, ncclSum, h->comm, st));
+  if (h->apply)
+    launch_dense_adam(h->t.dense, h->t.dense_m, h->t.dense_v, h->gfull, h->dense_size, h->lr_dev, h->cfg.beta1,
+                      h->cfg.beta2, h->cfg.eps, h->bc, h->flags, st);
+  mark(h, 7);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(&h->hout->loss, h->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h->hout->flags, h->flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&h->hout->U, h->Udev, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&h->hout->t, h->t_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  return KG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -882,7 +1111,13 @@ kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info)
   h->stamp++;
   if ((s = ingest(h, b, true, p, lr)) != KG_OK) return s;
   h->last_M = S.M; h->last_K = S.K;
-  if (h->use_graphs) {
+  if (h->world > 1) {
+    const int64_t l0 = g_launches;
+    h->gemm_count = 0;
+    if ((s = step_dist(h, S)) != KG_OK) return s;
+    h->last_kernels = (int)(g_launches - l0);
+    h->last_gemms = h->gemm_count;
+  } else if (h->use_graphs) {
     kg_handle::GraphEntry *g = nullptr;
     for (auto &e : h->graphs)
       if (e.structure == b->structure && e.M == S.M && e.K == S.K && e.flags == h->flag_key()) { g = &e; break; }
@@ -948,7 +1183,9 @@ kg_status kg_score(kg_handle *h, const kg_batch *q, const int64_t *cand, int32_t
   S.plan = make_plan(q->structure);
   kg_batch qb = *q;
   qb.on_device = q->on_device;
+  if (h->world > 1) return fail(h, KG_EUNSUPPORTED, "kg_score with world > 1 is not built yet (DESIGN.md §7)");
   if ((s = ingest(h, &qb, false, S.plan)) != KG_OK) return s;
+  h->ent_src = h->t.ent;
   const Plan &p = S.plan;
   const int M = q->M, d = h->d, na = p.na, nr = p.nr;
   S.M = M; S.K = n_cand; S.Kp = n_cand; S.NQ = p.nout * M;
@@ -971,12 +1208,12 @@ kg_status kg_score(kg_handle *h, const kg_batch *q, const int64_t *cand, int32_t
   const int64_t *cand_rows = h->rows + (int64_t)na * M;
   if (h->kind == KG_BETAE) {
     launch_beta_query(h->Q, S.NQ, h->m, h->QP, h->Cq, st);
-    launch_beta_entity(h->t.ent, cand_rows, n_cand, h->m, h->F, h->Cv, st);
+    launch_beta_entity(h->ent_src, cand_rows, n_cand, h->m, h->F, h->Cv, st);
   }
   ScoreArgs sa;
   sa.Q = h->Q; sa.NQ = S.NQ; sa.M = M; sa.K = n_cand; sa.Kp = n_cand; sa.U = U; sa.d = d;
   if (h->kind == KG_BETAE) { sa.E = h->F; sa.eidx = nullptr; sa.estride = 9LL * h->m; }
-  else { sa.E = h->t.ent; sa.eidx = cand_rows; sa.estride = d; }
+  else { sa.E = h->ent_src; sa.eidx = cand_rows; sa.estride = d; }
   sa.Cq = h->Cq; sa.Cv = h->Cv; sa.alpha = h->cfg.box_alpha; sa.Dmin = h->Dscore; sa.ldo = n_cand;
   sa.Dpart = h->Dpart; sa.cap_D = h->cap_D;
   launch_pair_fwd(h->kind, sa, p.nout, false, st);
@@ -1111,6 +1348,14 @@ kg_status kg_set_apply(kg_handle *h, int32_t flags) {
 
 const char *kg_last_error(const kg_handle *h) { return h ? h->err.c_str() : "null handle"; }
 
+kg_status kg_nccl_unique_id(void *out) {
+  if (!out) return KG_EINVAL;
+  ncclUniqueId id;
+  if (!nccl().ok || nccl().GetUniqueId(&id) != ncclSuccess) return KG_ENCCL;
+  std::memcpy(out, &id, sizeof(id));
+  return KG_OK;
+}
+
 void kg_destroy(kg_handle *h) {
   if (!h) return;
   if (h->st) cudaStreamSynchronize(h->st);
@@ -1130,6 +1375,8 @@ void kg_destroy(kg_handle *h) {
   if (h->step_done) cudaEventDestroy(h->step_done);
   for (int i = 0; i < 8; ++i)
     if (h->sev[i]) cudaEventDestroy(h->sev[i]);
+  if (h->comm) nccl().CommDestroy(h->comm);
+  if (h->h_counts) cudaFreeHost(h->h_counts);
   if (h->ws) cudaFree(h->ws);
   delete h;
 }

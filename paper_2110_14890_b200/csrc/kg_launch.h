@@ -7,6 +7,8 @@ namespace kg {
 
 struct Slots4 { int s[4]; };
 
+constexpr int kMaxWorld = 8;   // ranks supported by the row-sharded exchange
+
 extern int64_t g_launches;   // kernels of this library enqueued so far (per process)
 
 struct ScoreArgs {
@@ -49,7 +51,7 @@ void launch_beta_entity(const float *ent, const int64_t *rows, int K, int m, flo
 void launch_beta_query(const float *Q, int NQ, int m, float *QP, float *Cq, cudaStream_t st);
 void launch_loss_finalize(const float *loss_pos, const float *loss_part, int M, int njt, double scale,
                           double *loss_out, int *flags, int64_t *t_dev, float *bc, double beta1, double beta2,
-                          int apply, cudaStream_t st);
+                          int apply, cudaStream_t st, int check = 1);
 
 // k_dedup.cu: sort keys (ids < 2^end_bit) with their positions; outputs
 // uniq[U] (ascending), inv[L] (position -> unique index), perm[L] (sorted
@@ -77,6 +79,19 @@ void launch_dense_adam_rel(float *p, float *m, float *v, int R, int width, int n
 void launch_dense_adam(float *p, float *m, float *v, const float *g, int64_t n, const float *lr, double beta1,
                        double beta2, double eps, const float *bc, const int *flags, cudaStream_t st);
 void launch_colsum(const float *X, int rows, int cols, int ld, float *out, cudaStream_t st);
+
+// k_dist.cu (world > 1)
+void launch_owner_partition(const int64_t *uniq, const int32_t *U_dev, int G, int64_t *send_ids, int32_t *send_pos,
+                            int32_t *counts, cudaStream_t st);
+void launch_occ_rows(const int32_t *inv, const int32_t *send_pos, int L, int64_t *rows, cudaStream_t st);
+void launch_gather_owned(const float *ent, const int64_t *ids, int n, int G, int d, float *out, cudaStream_t st);
+void launch_reorder_rows(const float *Gu, const int32_t *send_pos, const int32_t *U_dev, int Lmax, int d, float *out,
+                         cudaStream_t st);
+void launch_local_rows(const int64_t *ids, int n, int G, int64_t *keys, cudaStream_t st);
+void launch_scatter_rel(const float *RGU, const int64_t *runiq, const int32_t *rU, int Lrmax, int R, int w, int nseg,
+                        float *gfull, cudaStream_t st);
+void launch_loss_check(double *loss_out, int *flags, int64_t *t_dev, float *bc, double beta1, double beta2, int apply,
+                       cudaStream_t st);
 
 // k_dag.cu
 void launch_proj_fwd(int kind, int N, int d, const float *in, int64_t in_ld, const int64_t *anchor_rows,

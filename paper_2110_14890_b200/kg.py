@@ -16,7 +16,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libkg.so")
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2110_14890_b200.build` "
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_2110_14890_b200/build.py` "
                       "(there is no CPU fallback)")
 _lib = C.CDLL(LIB_PATH)
 
@@ -68,6 +68,7 @@ _sig = {
                                 C.c_void_p, C.c_void_p]),
     "kg_set_apply": (C.c_int, [_H, C.c_int32]),
     "kg_last_error": (C.c_char_p, [_H]),
+    "kg_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "kg_destroy": (None, [_H]),
 }
 for _name, (_res, _args) in _sig.items():
@@ -76,6 +77,13 @@ for _name, (_res, _args) in _sig.items():
     globals()[_name] = _f
 
 EXPORTED = sorted(_sig)
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0), to be broadcast to the other ranks before kg_create."""
+    buf = C.create_string_buffer(128)
+    check(kg_nccl_unique_id(buf))
+    return buf.raw
 
 
 class KGError(RuntimeError):
@@ -109,12 +117,15 @@ def make_config(cfg, max_M, max_K, max_cand=0, rank=0, world=1, nccl_id=None) ->
 class KGModel:
     """Convenience owner of one handle + its caller-owned tables (torch device memory)."""
 
-    def __init__(self, cfg, max_M, max_K, max_cand=0, device="cuda", stream=None, rank=0, world=1):
+    def __init__(self, cfg, max_M, max_K, max_cand=0, device="cuda", stream=None, rank=0, world=1,
+                 nccl_id: bytes = None):
         import torch
         self.cfg = cfg
         self.torch = torch
         self.h = _H()
-        self.conf = make_config(cfg, max_M, max_K, max_cand, rank, world)
+        self._nccl_id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        self.conf = make_config(cfg, max_M, max_K, max_cand, rank, world,
+                                C.cast(self._nccl_id, C.c_void_p) if self._nccl_id is not None else None)
         check(kg_create(C.byref(self.conf), C.byref(self.h)))
         self.rows = kg_shard_rows(self.h)
         self.dense_size = kg_dense_size(self.h)
