@@ -185,6 +185,15 @@ kg_status kg_set_apply(kg_handle *h, int32_t flags);
 
 const char *kg_last_error(const kg_handle *h);
 
+/* Test hook: the tensor-core GEMM of the query-DAG contractions on device pointers,
+ * C[M][N] (ldc) = beta*C + op(A) op(B)^T (+ bias[n]) (ReLU if relu), op(A) = [M][K], op(B) = [N][K];
+ * ta: A stored [K][lda] (else [M][lda]); tb: B stored [K][ldb] (else [N][ldb]).  tcgen05
+ * kind::tf32 with a 3xTF32 split (fp32-level accuracy); a non-transposed operand needs ld % 4 == 0
+ * (else EINVAL).  Synchronises the stream. */
+kg_status kg_test_gemm(int32_t ta, int32_t tb, int32_t M, int32_t N, int32_t K, const float *A, int32_t lda,
+                       const float *B, int32_t ldb, float *C, int32_t ldc, const float *bias, int32_t relu, float beta,
+                       void *stream);
+
 /* world > 1: rank 0 creates the 128-byte NCCL unique id (written to out) and shares it with
  * the other ranks (e.g. torch.distributed broadcast) before every rank calls kg_create. */
 kg_status kg_nccl_unique_id(void *out);

@@ -192,6 +192,8 @@ struct kg_handle {
   float *pX = nullptr, *pH1 = nullptr, *pH2 = nullptr, *pZp1 = nullptr, *pdZ = nullptr, *pdH2 = nullptr,
         *pdH1 = nullptr, *pZ = nullptr, *pdX = nullptr;
   float *Dscore = nullptr;
+  float *gsA = nullptr, *gsB = nullptr, *gsP = nullptr;   // GEMM transpose / split-K scratch
+  int64_t gsP_cap = 0;
   float *Dpart = nullptr, *partQ = nullptr, *partV = nullptr, *Cpart = nullptr, *Csum = nullptr;
   int64_t cap_D = 0, cap_Q = 0, cap_V = 0;
   cudaStream_t st2 = nullptr, st_cap = nullptr;
@@ -204,6 +206,8 @@ struct kg_handle {
   };
   std::vector<GraphEntry> graphs;
   bool use_graphs = true;
+  bool gemm_cublas = false, gemm_tc_all = false;
+  int tc_min_k = 512;
   void *blas_ws = nullptr;
   // row-sharded exchange (world > 1, k_dist.cu)
   ncclComm_t comm = nullptr;
@@ -400,6 +404,14 @@ void carve(kg_handle *h, Arena &A) {
     h->pdX = A.take<float>((int64_t)Mx * 2 * d);
   }
   h->Dscore = A.take<float>((int64_t)Mx * std::max(h->Cx, 1));
+  {
+    const int64_t wide = std::max<int64_t>({(int64_t)H, 2LL * d, (int64_t)dq});
+    const int64_t tall = std::max<int64_t>({4LL * Mx, (int64_t)H, 2LL * d});
+    h->gsA = A.take<float>(wide * (tall + 4));
+    h->gsB = A.take<float>(wide * (tall + 4));
+    h->gsP_cap = std::min<int64_t>(16LL << 20, 8LL * 4 * Mx * wide);
+    h->gsP = A.take<float>(h->gsP_cap);
+  }
   if (h->world > 1) {
     const int64_t GL = (int64_t)h->world * h->Lx;
     h->send_ids = A.take<int64_t>(h->Lx);
@@ -421,14 +433,29 @@ void carve(kg_handle *h, Arena &A) {
   }
 }
 
-// Row-major GEMM: C[m x n] = op(A) op(B) + beta C, op(A) is [m x k].
+// Row-major GEMM: C[m x n] = op(A) op(B) + beta C, op(A) is [m x k]; tb: B given as [n x k].
+// Default: the tcgen05 3xTF32 kernel (k_gemm.cu); KG_GEMM=cublas selects cuBLAS SGEMM (A/B check).
 kg_status gemm(kg_handle *h, bool ta, bool tb, int m, int n, int k, const float *A, int lda, const float *B, int ldb,
-               float beta, float *C, int ldc) {
+               float beta, float *C, int ldc, const float *bias = nullptr, int relu = 0) {
   if (m <= 0 || n <= 0) return KG_OK;
+  // the tcgen05 kernel pays off for long K loops over large outputs (BetaE MLP layers and
+  // their dW over the batch rows); the small d x d contractions go to cuBLAS SGEMM (fp32)
+  if (!h->gemm_cublas && ((k >= h->tc_min_k && (int64_t)m * n >= (1 << 18)) || h->gemm_tc_all)) {
+    // operands the tensor-core kernel reads K-major: transpose [k][m] / [k][n] storage first
+    GemmArgs g;
+    g.A = A; g.B = B; g.C = C; g.M = m; g.N = n; g.K = k; g.lda = lda; g.ldb = ldb; g.ldc = ldc; g.beta = beta;
+    g.bias = bias; g.relu = relu;
+    const int kp = (k + 3) & ~3;
+    if (ta) { launch_transpose(A, k, m, lda, h->gsA, kp, h->st); g.A = h->gsA; g.lda = kp; }
+    if (!tb) { launch_transpose(B, k, n, ldb, h->gsB, kp, h->st); g.B = h->gsB; g.ldb = kp; }
+    launch_gemm_tc(g, h->gsP, h->gsP_cap, h->st);
+    return KG_OK;
+  }
   const float one = 1.f;
   h->gemm_count++;
   CKB(cublasSgemm(h->blas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, n, m, k, &one, B, ldb, A,
                   lda, &beta, C, ldc));
+  if (bias || relu) launch_bias_act(C, bias, m, n, relu, h->st);   // (bias required when relu; ldc == n here)
   return KG_OK;
 }
 #define G(...)                                   \
@@ -459,10 +486,8 @@ kg_status dag_forward(kg_handle *h, StepBufs &S) {
       if (h->kind == KG_BETAE) {
         float *X = h->pX + (int64_t)u * M * 2 * d, *H1 = h->pH1 + (int64_t)u * M * HH, *H2 = h->pH2 + (int64_t)u * M * HH;
         launch_betae_proj_in(M, d, in, arows, ent, rel, 1, dp(h, "rel"), X, st);
-        G(false, true, M, HH, 2 * d, X, 2 * d, dp(h, "prj_W1"), 2 * d, 0.f, H1, HH);
-        launch_bias_act(H1, dp(h, "prj_b1"), M, HH, 1, st);
-        G(false, true, M, HH, HH, H1, HH, dp(h, "prj_W2"), HH, 0.f, H2, HH);
-        launch_bias_act(H2, dp(h, "prj_b2"), M, HH, 1, st);
+        G(false, true, M, HH, 2 * d, X, 2 * d, dp(h, "prj_W1"), 2 * d, 0.f, H1, HH, dp(h, "prj_b1"), 1);
+        G(false, true, M, HH, HH, H1, HH, dp(h, "prj_W2"), HH, 0.f, H2, HH, dp(h, "prj_b2"), 1);
         G(false, true, M, d, HH, H2, HH, dp(h, "prj_W0"), HH, 0.f, h->pZ, d);
         launch_betae_proj_out(h->pZ, dp(h, "prj_b0"), M, d, h->pZp1 + (int64_t)u * M * d, S.val[ni], st);
       } else {
@@ -478,28 +503,20 @@ kg_status dag_forward(kg_handle *h, StepBufs &S) {
       float *out = S.val[ni];
       float **T = h->T;
       if (h->kind == KG_GQE) {
-        G(false, true, NR, d, d, h->stack_v, d, dp(h, "ds_W1"), d, 0.f, T[0], d);   // H
-        launch_bias_act(T[0], dp(h, "ds_b1"), NR, d, 1, st);
+        G(false, true, NR, d, d, h->stack_v, d, dp(h, "ds_W1"), d, 0.f, T[0], d, dp(h, "ds_b1"), 1);   // H
         launch_mean_stack(T[0], n, M, d, T[1], st);                                  // Mn
-        G(false, true, M, d, d, T[1], d, dp(h, "ds_W2"), d, 0.f, out, d);
-        launch_bias_act(out, dp(h, "ds_b2"), M, d, 0, st);
+        G(false, true, M, d, d, T[1], d, dp(h, "ds_W2"), d, 0.f, out, d, dp(h, "ds_b2"), 0);
       } else if (h->kind == KG_Q2B) {
-        G(false, true, NR, d, d, h->stack_v, 2 * d, dp(h, "att_W1"), d, 0.f, T[0], d);  // Hc
-        launch_bias_act(T[0], dp(h, "att_b1"), NR, d, 1, st);
-        G(false, true, NR, d, d, T[0], d, dp(h, "att_W2"), d, 0.f, T[1], d);           // Lg
-        launch_bias_act(T[1], dp(h, "att_b2"), NR, d, 0, st);
+        G(false, true, NR, d, d, h->stack_v, 2 * d, dp(h, "att_W1"), d, 0.f, T[0], d, dp(h, "att_b1"), 1);  // Hc
+        G(false, true, NR, d, d, T[0], d, dp(h, "att_W2"), d, 0.f, T[1], d, dp(h, "att_b2"), 0);           // Lg
         launch_q2b_att_fwd(h->stack_v, T[1], n, M, d, T[2], out, st);                  // a, center
-        G(false, true, NR, d, d, h->stack_v + d, 2 * d, dp(h, "off_W1"), d, 0.f, T[3], d);  // Ho
-        launch_bias_act(T[3], dp(h, "off_b1"), NR, d, 1, st);
+        G(false, true, NR, d, d, h->stack_v + d, 2 * d, dp(h, "off_W1"), d, 0.f, T[3], d, dp(h, "off_b1"), 1);  // Ho
         launch_mean_stack(T[3], n, M, d, T[4], st);                                    // Mo
-        G(false, true, M, d, d, T[4], d, dp(h, "off_W2"), d, 0.f, T[5], d);            // Z
-        launch_bias_act(T[5], dp(h, "off_b2"), M, d, 0, st);
+        G(false, true, M, d, d, T[4], d, dp(h, "off_W2"), d, 0.f, T[5], d, dp(h, "off_b2"), 0);            // Z
         launch_q2b_off_fwd(h->stack_v, T[5], n, M, d, T[6], h->amin, out, st);         // sig, amin, offset
       } else if (h->kind == KG_BETAE) {
-        G(false, true, NR, d, d, h->stack_v, d, dp(h, "att_U1"), d, 0.f, T[0], d);     // Hs
-        launch_bias_act(T[0], dp(h, "att_c1"), NR, d, 1, st);
-        G(false, true, NR, m, d, T[0], d, dp(h, "att_U2"), d, 0.f, T[1], m);           // Lg
-        launch_bias_act(T[1], dp(h, "att_c2"), NR, m, 0, st);
+        G(false, true, NR, d, d, h->stack_v, d, dp(h, "att_U1"), d, 0.f, T[0], d, dp(h, "att_c1"), 1);     // Hs
+        G(false, true, NR, m, d, T[0], d, dp(h, "att_U2"), d, 0.f, T[1], m, dp(h, "att_c2"), 0);           // Lg
         launch_beta_att_fwd(h->stack_v, T[1], n, M, d, T[2], out, st);                 // w, out
       }
     }
@@ -793,6 +810,10 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
     h->use_graphs = false;   // the exchange sizes are read on the host every step
   }
   if (const char *e = std::getenv("KG_NO_GRAPH")) h->use_graphs = !(e[0] == '1');
+  if (const char *e = std::getenv("KG_GEMM")) {
+    h->gemm_cublas = std::string(e) == "cublas";
+    h->gemm_tc_all = std::string(e) == "tc";
+  }
   cublasSetMathMode(h->blas, CUBLAS_PEDANTIC_MATH);   // true fp32, no TF32 (parity at 1e-5, A24)
   // device scalars
   if (cudaMemset(h->ws, 0, h->ws_bytes) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
@@ -1347,6 +1368,39 @@ kg_status kg_set_apply(kg_handle *h, int32_t flags) {
 }
 
 const char *kg_last_error(const kg_handle *h) { return h ? h->err.c_str() : "null handle"; }
+
+kg_status kg_test_gemm(int32_t ta, int32_t tb, int32_t M, int32_t N, int32_t K, const float *A, int32_t lda,
+                       const float *B, int32_t ldb, float *C, int32_t ldc, const float *bias, int32_t relu, float beta,
+                       void *stream) {
+  if (!A || !B || !C || M < 0 || N < 0 || K < 0) return KG_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  GemmArgs g;
+  g.A = A; g.B = B; g.C = C; g.bias = bias; g.M = M; g.N = N; g.K = K; g.lda = lda; g.ldb = ldb; g.ldc = ldc;
+  g.relu = relu; g.beta = beta;
+  const int kp = (K + 3) & ~3;
+  float *sA = nullptr, *sB = nullptr;
+  if ((!ta && (lda & 3)) || (!tb && (ldb & 3))) return KG_EINVAL;   // K-major operands need ld % 4 == 0
+  if (ta) {
+    if (cudaMalloc(&sA, sizeof(float) * (size_t)std::max(M, 1) * kp) != cudaSuccess) return KG_ENOMEM;
+    launch_transpose(A, K, M, lda, sA, kp, st);
+    g.A = sA; g.lda = kp;
+  }
+  if (tb) {
+    if (cudaMalloc(&sB, sizeof(float) * (size_t)std::max(N, 1) * kp) != cudaSuccess) return KG_ENOMEM;
+    launch_transpose(B, K, N, ldb, sB, kp, st);
+    g.B = sB; g.ldb = kp;
+  }
+  float *sP = nullptr;
+  const int64_t pcap = 8LL * std::max(M, 1) * std::max(N, 1);
+  if (cudaMalloc(&sP, sizeof(float) * pcap) != cudaSuccess) return KG_ENOMEM;
+  launch_gemm_tc(g, sP, pcap, st);
+  const cudaError_t e = cudaStreamSynchronize(st);
+  cudaFree(sP);
+  if (sA) cudaFree(sA);
+  if (sB) cudaFree(sB);
+  if (e != cudaSuccess) return KG_ECUDA;
+  return cudaGetLastError() == cudaSuccess ? KG_OK : KG_ECUDA;
+}
 
 kg_status kg_nccl_unique_id(void *out) {
   if (!out) return KG_EINVAL;

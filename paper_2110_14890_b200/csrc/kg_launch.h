@@ -80,6 +80,20 @@ void launch_dense_adam(float *p, float *m, float *v, const float *g, int64_t n, 
                        double beta2, double eps, const float *bc, const int *flags, cudaStream_t st);
 void launch_colsum(const float *X, int rows, int cols, int ld, float *out, cudaStream_t st);
 
+// k_gemm.cu: C[M][N] = beta C + op(A) op(B)^T (+ bias) (ReLU), op(A) [M][K], op(B) [N][K];
+// tcgen05 kind::tf32 with a 3xTF32 split; A stored [M][lda], B stored [N][ldb] (K-major).
+struct GemmArgs {
+  const float *A = nullptr, *B = nullptr;
+  float *C = nullptr;
+  const float *bias = nullptr;
+  int M = 0, N = 0, K = 0, lda = 0, ldb = 0, ldc = 0, relu = 0;
+  float beta = 0.f;
+  float *P = nullptr;   // split-K partials [splits][M][N] (set by launch_gemm_tc)
+  int kbs = 1 << 30;    // k-blocks per split
+};
+void launch_gemm_tc(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st);   // K-major, ld % 4 == 0
+void launch_transpose(const float *in, int R, int Cc, int ld_in, float *out, int ld_out, cudaStream_t st);
+
 // k_dist.cu (world > 1)
 void launch_owner_partition(const int64_t *uniq, const int32_t *U_dev, int G, int64_t *send_ids, int32_t *send_pos,
                             int32_t *counts, cudaStream_t st);

@@ -69,6 +69,9 @@ _sig = {
     "kg_set_apply": (C.c_int, [_H, C.c_int32]),
     "kg_last_error": (C.c_char_p, [_H]),
     "kg_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "kg_test_gemm": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
+                               C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_float,
+                               C.c_void_p]),
     "kg_destroy": (None, [_H]),
 }
 for _name, (_res, _args) in _sig.items():

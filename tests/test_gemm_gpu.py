@@ -1,0 +1,56 @@
+"""The tcgen05 3xTF32 GEMM of the query-DAG contractions vs fp64 numpy (-m gpu).
+
+The contractions are plain linear algebra (Y = X W^T, dX = dY W, dW = dY^T X),
+so the reference is numpy's float64 matmul; the bar is the fp32 parity bar of
+the step (1e-5 relative to the tensor, BASELINE north_star).
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(ta, tb, M, N, K, bias=False, relu=False, beta=0.0, seed=0):
+    import torch
+    import paper_2110_14890_b200 as kgb
+    rng = np.random.default_rng(seed)
+    A = rng.standard_normal((K, M) if ta else (M, K)).astype(np.float32)
+    B = rng.standard_normal((K, N) if tb else (N, K)).astype(np.float32)
+    C0 = rng.standard_normal((M, N)).astype(np.float32)
+    b = rng.standard_normal(N).astype(np.float32)
+    dev = torch.device("cuda")
+    tA, tB, tC, tb_ = (torch.from_numpy(x).to(dev) for x in (A, B, C0, b))
+    st = torch.cuda.current_stream()
+    s = kgb.kg_test_gemm(int(ta), int(tb), M, N, K, tA.data_ptr(), A.shape[1], tB.data_ptr(), B.shape[1],
+                         tC.data_ptr(), N, tb_.data_ptr() if bias else None, int(relu), beta,
+                         C.c_void_p(st.cuda_stream))
+    assert s == 0
+    opA = A.T.astype(np.float64) if ta else A.astype(np.float64)
+    opB = B.astype(np.float64) if tb else B.T.astype(np.float64)
+    ref = opA @ opB
+    if bias:
+        ref = ref + b.astype(np.float64)
+    if relu:
+        ref = np.maximum(ref, 0)
+    if beta:
+        ref = ref + beta * C0.astype(np.float64)
+    got = tC.cpu().numpy().astype(np.float64)
+    err = np.abs(got - ref)
+    tol = 1e-5 * (np.abs(ref) + np.abs(ref).max())
+    assert np.all(err <= tol), (float(err.max()), float(np.abs(ref).max()), np.unravel_index(np.argmax(err / tol), err.shape))
+    return float((err / (np.abs(ref).max())).max())
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
+@pytest.mark.parametrize("M,N,K", [(70, 40, 40), (128, 128, 32), (200, 136, 100), (512, 400, 800)])
+def test_gemm_layouts_and_ragged_shapes(ta, tb, M, N, K):
+    _run(ta, tb, M, N, K)
+
+
+def test_gemm_betae_shapes_and_epilogues():
+    _run(False, False, 1024, 1600, 800, bias=True, relu=True)     # H1 = ReLU(X W1^T + b1)
+    _run(False, True, 1024, 800, 1600)                            # dX = dH1 W1
+    _run(True, True, 1600, 800, 1024)                             # dW1 = dH1^T X
+    _run(False, False, 300, 400, 400, beta=1.0)                   # dstack += dH U1
