@@ -186,17 +186,22 @@ def run_ours(args, world, rank, local):
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = allreduce_max(sum(step_ms), world)
     value = world * args.steps * M / (total_ms / 1e3)
-    kernels_per_step = info.kernels
+    step_structs = [hb[(args.warmup + s) % n_distinct]["structure"] for s in range(args.steps)]
+    per_struct_ms = {st: round(float(np.mean([t for t, x in zip(step_ms, step_structs) if x == st])), 5)
+                     for st in structures}
 
     # ---- profiling pass: the same steps with stage events (CUDA events on the bound stream)
     gm.set_apply(True, stage_timing=True)
     stage = np.zeros(8)
     work = {}
+    kernels_of, gemms_of = {}, {}
     n_prof = min(args.steps, 9 * 3)
     for s in range(n_prof):
         b = hb[(args.warmup + s) % n_distinct]
         flush.zero_()
         inf = gm.step(db[(args.warmup + s) % n_distinct], lr, sync=True, on_device=True)
+        kernels_of[b["structure"]] = inf.kernels
+        gemms_of[b["structure"]] = inf.gemms
         stage += np.array(inf.stage_ms[:8])
         for k, (bound, amount, unit) in stage_work(cfg, M, K, b["structure"], inf.n_touched, cfg.dim).items():
             work.setdefault(k, [bound, 0.0, unit])[1] += amount
@@ -267,8 +272,10 @@ def run_ours(args, world, rank, local):
                    if world > 1 else "single",
                    "l2": "flushed between timed steps (256 MB write outside the step events)",
                    "note": w.note},
-        "e2e": e2e, "roofline": roof, "gpu_launches": int(kernels_per_step * args.steps),
-        "kernels_per_step": kernels_per_step, "gemms_per_step": info.gemms, "clocks": clk,
+        "e2e": e2e, "roofline": roof,
+        "gpu_launches": int(sum(kernels_of.get(st, info.kernels) for st in step_structs)),
+        "kernels_per_step": kernels_of, "cublas_gemms_per_step": gemms_of, "ms_per_step_by_structure": per_struct_ms,
+        "clocks": clk,
         "wall_s": round(wall, 3), "loss_last": info.loss,
     }
     gm.close()

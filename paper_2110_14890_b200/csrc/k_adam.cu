@@ -143,13 +143,26 @@ __global__ void __launch_bounds__(256) sparse_adam_kernel(const int64_t *uniq, c
   const float4 *X4 = reinterpret_cast<const float4 *>(OG), *P4 = reinterpret_cast<const float4 *>(PS);
   float4 *pe = reinterpret_cast<float4 *>(ent) + rowoff, *pm = reinterpret_cast<float4 *>(m) + rowoff,
          *pv = reinterpret_cast<float4 *>(v) + rowoff;
-  for (int c = lane; c < d4; c += 32) {
-    const float4 g = segment_sum(perm, X4, P4, s0, s1, d4, c);
-    if (grad_out) reinterpret_cast<float4 *>(grad_out)[(int64_t)u * d4 + c] = g;
-    if (!upd) continue;
-    float4 P = pe[c], Mm = pm[c], V = pv[c];
-    adam4(P, Mm, V, g, lr1, hy, ibc2);
-    pe[c] = P; pm[c] = Mm; pv[c] = V;
+  // d <= 2048: at most 16 float4 per lane; issue the row's p, m, v loads before the arithmetic
+  constexpr int kMaxIt = 4;
+  for (int c0 = 0; c0 < d4; c0 += 32 * kMaxIt) {
+    float4 P[kMaxIt], Mm[kMaxIt], V[kMaxIt], Gq[kMaxIt];
+#pragma unroll
+    for (int it = 0; it < kMaxIt; ++it) {
+      const int c = c0 + lane + 32 * it;
+      if (c >= d4) continue;
+      Gq[it] = segment_sum(perm, X4, P4, s0, s1, d4, c);
+      if (upd) { P[it] = pe[c]; Mm[it] = pm[c]; V[it] = pv[c]; }
+    }
+#pragma unroll
+    for (int it = 0; it < kMaxIt; ++it) {
+      const int c = c0 + lane + 32 * it;
+      if (c >= d4) continue;
+      if (grad_out) reinterpret_cast<float4 *>(grad_out)[(int64_t)u * d4 + c] = Gq[it];
+      if (!upd) continue;
+      adam4(P[it], Mm[it], V[it], Gq[it], lr1, hy, ibc2);
+      pe[c] = P[it]; pm[c] = Mm[it]; pv[c] = V[it];
+    }
   }
 }
 
@@ -207,46 +220,51 @@ void launch_rel_stamp(const int64_t *uniq_rel, const int32_t *U_dev, int Lmax, i
 // (Q2B: rel_center, rel_offset); the gradient of row r of segment s is
 // RGU[rel_seg[r]][s*width + c] when relation r was used by this step
 // (rel_stamp[r] == stamp), else 0.  !REL: the operator weights, gradient g.
-constexpr int kE = 4;
+constexpr int kE = 2;
 
-// Relation tables: one warp per table row (nseg * R rows); the "was this relation
-// used by the step" test is warp-uniform; lanes stream the row's float4 columns.
-__global__ void __launch_bounds__(256) dense_adam_rel_kernel(float4 *p, float4 *m, float4 *v, int R, int w4, int nseg,
-                                                             const float *RGU, const int32_t *rel_seg,
-                                                             const int64_t *rel_stamp, const int64_t *stamp_dev,
-                                                             const float *lr_dev, AdamHyper hy, const float *bc,
-                                                             const int *flags) {
+// q = n / D for n < 2^32 via a 64-bit reciprocal (exact for n < 2^40 / D).
+struct FastDiv {
+  uint64_t mul;
+  uint32_t d;
+};
+static FastDiv fastdiv(uint32_t d) { return FastDiv{(((uint64_t)1 << 40) + d - 1) / d, d}; }
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, FastDiv f) { return (uint32_t)(((uint64_t)n * f.mul) >> 40); }
+
+// Relation tables: flat stream over nseg * R rows of w4 float4; the gradient of row r
+// of segment s is RGU[rel_seg[r]][s*w4 + c] when relation r was used by this step
+// (rel_stamp[r] == stamp), else 0 (A17).  kE float4 per thread, loads issued first.
+__global__ void __launch_bounds__(256) dense_adam_rel_kernel(float4 *p, float4 *m, float4 *v, int n4, FastDiv fw4,
+                                                             int R, int nseg, const float *RGU,
+                                                             const int32_t *rel_seg, const int64_t *rel_stamp,
+                                                             const int64_t *stamp_dev, const float *lr_dev,
+                                                             AdamHyper hy, const float *bc, const int *flags) {
   if (flags[0]) return;
-  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (row >= nseg * R) return;
-  const int sidx = row >= R ? 1 : 0, r = row - sidx * R;
   const float lr1 = *lr_dev * bc[0], ibc2 = bc[1];
-  const bool used = rel_stamp[r] == *stamp_dev;
-  const float4 *g4 = used ? reinterpret_cast<const float4 *>(RGU) + (int64_t)rel_seg[r] * nseg * w4 + sidx * w4 : nullptr;
-  float4 *pr = p + (int64_t)row * w4, *mr = m + (int64_t)row * w4, *vr = v + (int64_t)row * w4;
+  const int64_t stamp = *stamp_dev;
+  const int w4 = (int)fw4.d;
+  const int base = blockIdx.x * (256 * kE) + threadIdx.x;
   float4 P[kE], Mm[kE], V[kE], G[kE];
 #pragma unroll
   for (int k = 0; k < kE; ++k) {
-    const int c = lane + 32 * k;
-    if (c >= w4) continue;
-    P[k] = __ldcs(pr + c);
-    Mm[k] = __ldcs(mr + c);
-    V[k] = __ldcs(vr + c);
-    G[k] = used ? g4[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int e = base + k * 256;
+    if (e >= n4) continue;
+    P[k] = __ldcs(p + e);
+    Mm[k] = __ldcs(m + e);
+    V[k] = __ldcs(v + e);
+    const int row = (int)fdiv((uint32_t)e, fw4), c4 = e - row * w4;
+    const int sidx = row >= R ? 1 : 0, r = row - sidx * R;
+    G[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (rel_stamp[r] == stamp)
+      G[k] = reinterpret_cast<const float4 *>(RGU)[(int64_t)rel_seg[r] * nseg * w4 + sidx * w4 + c4];
   }
 #pragma unroll
   for (int k = 0; k < kE; ++k) {
-    const int c = lane + 32 * k;
-    if (c >= w4) continue;
+    const int e = base + k * 256;
+    if (e >= n4) continue;
     adam4(P[k], Mm[k], V[k], G[k], lr1, hy, ibc2);
-    __stcs(pr + c, P[k]);
-    __stcs(mr + c, Mm[k]);
-    __stcs(vr + c, V[k]);
-  }
-  for (int c = lane + 32 * kE; c < w4; c += 32) {   // rows wider than 4 x 32 float4
-    float4 Pq = pr[c], Mq = mr[c], Vq = vr[c];
-    adam4(Pq, Mq, Vq, used ? g4[c] : make_float4(0.f, 0.f, 0.f, 0.f), lr1, hy, ibc2);
-    pr[c] = Pq; mr[c] = Mq; vr[c] = Vq;
+    __stcs(p + e, P[k]);
+    __stcs(m + e, Mm[k]);
+    __stcs(v + e, V[k]);
   }
 }
 
@@ -282,11 +300,12 @@ void launch_dense_adam_rel(float *p, float *m, float *v, int R, int width, int n
                            const int32_t *rel_seg, const int64_t *rel_stamp, const int64_t *stamp, const float *lr,
                            double beta1, double beta2, double eps, const float *bc, const int *flags,
                            cudaStream_t st) {
-  const int rows = nseg * R;
-  if (rows <= 0) return;
-  { dense_adam_rel_kernel<<<(rows + 7) / 8, 256, 0, st>>>(
-        reinterpret_cast<float4 *>(p), reinterpret_cast<float4 *>(m), reinterpret_cast<float4 *>(v), R, width / 4,
-        nseg, RGU, rel_seg, rel_stamp, stamp, lr, hyper(beta1, beta2, eps), bc, flags); ++g_launches; }
+  const int n4 = nseg * R * (width / 4);
+  if (n4 <= 0) return;
+  { dense_adam_rel_kernel<<<(n4 + 256 * kE - 1) / (256 * kE), 256, 0, st>>>(
+        reinterpret_cast<float4 *>(p), reinterpret_cast<float4 *>(m), reinterpret_cast<float4 *>(v), n4,
+        fastdiv((uint32_t)(width / 4)), R, nseg, RGU, rel_seg, rel_stamp, stamp, lr, hyper(beta1, beta2, eps), bc,
+        flags); ++g_launches; }
 }
 
 void launch_dense_adam(float *p, float *m, float *v, const float *g, int64_t n, const float *lr, double beta1,

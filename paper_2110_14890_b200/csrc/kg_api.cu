@@ -196,7 +196,8 @@ struct kg_handle {
   int64_t gsP_cap = 0;
   float *Dpart = nullptr, *partQ = nullptr, *partV = nullptr, *Cpart = nullptr, *Csum = nullptr;
   int64_t cap_D = 0, cap_Q = 0, cap_V = 0;
-  cudaStream_t st2 = nullptr, st_cap = nullptr;
+  cudaStream_t st2 = nullptr, st_cap = nullptr, st3 = nullptr;
+  cudaEvent_t ev_i1 = nullptr, ev_i2 = nullptr;   // fork / join of the two Q2B intersection branches
   cudaEvent_t ev_fork = nullptr, ev_fork2 = nullptr, ev_join = nullptr;
   float *lr_dev = nullptr;
   int64_t *stamp_dev = nullptr;
@@ -206,7 +207,9 @@ struct kg_handle {
   };
   std::vector<GraphEntry> graphs;
   bool use_graphs = true;
-  bool gemm_cublas = false, gemm_tc_all = false;
+  bool gemm_cublas = false, gemm_tc_all = false, side = false;
+  cublasHandle_t blas2 = nullptr;
+  void *blas_ws2 = nullptr;
   int tc_min_k = 512;
   void *blas_ws = nullptr;
   // row-sharded exchange (world > 1, k_dist.cu)
@@ -380,6 +383,7 @@ void carve(kg_handle *h, Arena &A) {
   h->lr_dev = A.take<float>(4);
   h->stamp_dev = A.take<int64_t>(1);
   h->blas_ws = A.take<char>(32 << 20);
+  h->blas_ws2 = A.take<char>(32 << 20);
   h->bc = A.take<float>(2);
   for (int i = 0; i < 6; ++i) {
     h->nval[i] = A.take<float>((int64_t)Mx * dq);
@@ -440,7 +444,7 @@ kg_status gemm(kg_handle *h, bool ta, bool tb, int m, int n, int k, const float 
   if (m <= 0 || n <= 0) return KG_OK;
   // the tcgen05 kernel pays off for long K loops over large outputs (BetaE MLP layers and
   // their dW over the batch rows); the small d x d contractions go to cuBLAS SGEMM (fp32)
-  if (!h->gemm_cublas && ((k >= h->tc_min_k && (int64_t)m * n >= (1 << 18)) || h->gemm_tc_all)) {
+  if (!h->gemm_cublas && !h->side && ((k >= h->tc_min_k && (int64_t)m * n >= (1 << 18)) || h->gemm_tc_all)) {
     // operands the tensor-core kernel reads K-major: transpose [k][m] / [k][n] storage first
     GemmArgs g;
     g.A = A; g.B = B; g.C = C; g.M = m; g.N = n; g.K = k; g.lda = lda; g.ldb = ldb; g.ldc = ldc; g.beta = beta;
@@ -458,6 +462,36 @@ kg_status gemm(kg_handle *h, bool ta, bool tb, int m, int n, int k, const float 
   if (bias || relu) launch_bias_act(C, bias, m, n, relu, h->st);   // (bias required when relu; ldc == n here)
   return KG_OK;
 }
+// Run the following GEMMs / kernels on another stream (restored on scope exit).
+// The side stream gets its own cuBLAS handle (own workspace) and never uses the shared
+// tensor-core GEMM scratch, so the two branches cannot race on scratch memory.
+struct OnStream {
+  kg_handle *h;
+  cudaStream_t prev;
+  cublasHandle_t prev_blas;
+  OnStream(kg_handle *hh, cudaStream_t s) : h(hh), prev(hh->st), prev_blas(hh->blas) {
+    h->st = s;
+    h->blas = h->blas2;
+    cublasSetStream(h->blas, s);
+    h->side = true;
+  }
+  ~OnStream() {
+    h->st = prev;
+    h->blas = prev_blas;
+    h->side = false;
+  }
+};
+kg_status fork(kg_handle *h, cudaStream_t from, cudaStream_t to) {
+  CK(cudaEventRecord(h->ev_i1, from));
+  CK(cudaStreamWaitEvent(to, h->ev_i1, 0));
+  return KG_OK;
+}
+kg_status join(kg_handle *h, cudaStream_t from, cudaStream_t to) {
+  CK(cudaEventRecord(h->ev_i2, from));
+  CK(cudaStreamWaitEvent(to, h->ev_i2, 0));
+  return KG_OK;
+}
+
 #define G(...)                                   \
   do {                                           \
     kg_status s_ = gemm(h, __VA_ARGS__);         \
@@ -507,13 +541,20 @@ kg_status dag_forward(kg_handle *h, StepBufs &S) {
         launch_mean_stack(T[0], n, M, d, T[1], st);                                  // Mn
         G(false, true, M, d, d, T[1], d, dp(h, "ds_W2"), d, 0.f, out, d, dp(h, "ds_b2"), 0);
       } else if (h->kind == KG_Q2B) {
+        // the center-attention and offset-DeepSet branches are independent: second stream
+        kg_status fs = fork(h, st, h->st3);
+        if (fs) return fs;
+        {
+          OnStream os(h, h->st3);
+          G(false, true, NR, d, d, h->stack_v + d, 2 * d, dp(h, "off_W1"), d, 0.f, T[3], d, dp(h, "off_b1"), 1);  // Ho
+          launch_mean_stack(T[3], n, M, d, T[4], h->st3);                                                         // Mo
+          G(false, true, M, d, d, T[4], d, dp(h, "off_W2"), d, 0.f, T[5], d, dp(h, "off_b2"), 0);                 // Z
+          launch_q2b_off_fwd(h->stack_v, T[5], n, M, d, T[6], h->amin, out, h->st3);  // sig, amin, offset
+        }
         G(false, true, NR, d, d, h->stack_v, 2 * d, dp(h, "att_W1"), d, 0.f, T[0], d, dp(h, "att_b1"), 1);  // Hc
         G(false, true, NR, d, d, T[0], d, dp(h, "att_W2"), d, 0.f, T[1], d, dp(h, "att_b2"), 0);           // Lg
         launch_q2b_att_fwd(h->stack_v, T[1], n, M, d, T[2], out, st);                  // a, center
-        G(false, true, NR, d, d, h->stack_v + d, 2 * d, dp(h, "off_W1"), d, 0.f, T[3], d, dp(h, "off_b1"), 1);  // Ho
-        launch_mean_stack(T[3], n, M, d, T[4], st);                                    // Mo
-        G(false, true, M, d, d, T[4], d, dp(h, "off_W2"), d, 0.f, T[5], d, dp(h, "off_b2"), 0);            // Z
-        launch_q2b_off_fwd(h->stack_v, T[5], n, M, d, T[6], h->amin, out, st);         // sig, amin, offset
+        if ((fs = join(h, h->st3, st)) != KG_OK) return fs;
       } else if (h->kind == KG_BETAE) {
         G(false, true, NR, d, d, h->stack_v, d, dp(h, "att_U1"), d, 0.f, T[0], d, dp(h, "att_c1"), 1);     // Hs
         G(false, true, NR, m, d, T[0], d, dp(h, "att_U2"), d, 0.f, T[1], m, dp(h, "att_c2"), 0);           // Lg
@@ -576,8 +617,22 @@ kg_status dag_backward(kg_handle *h, StepBufs &S) {
         G(false, false, NR, d, d, T[8], d, dp(h, "ds_W1"), d, 0.f, h->stack_g, d);
       } else if (h->kind == KG_Q2B) {
         // forward: T0 Hc, T1 Lg, T2 a, T3 Ho, T4 Mo, T5 Z, T6 sig.  backward: T7 dLg, T8 dHc, T9 dZ, T10 dMo, T11 dHo
+        // offset branch on the second stream (writes the offset half of stack_g only)
+        kg_status fs = fork(h, st, h->st3);
+        if (fs) return fs;
+        {
+          OnStream os(h, h->st3);
+          cudaStream_t s3 = h->st3;
+          launch_q2b_off_bwd(h->stack_v, T[6], h->amin, gout, n, M, d, T[9], h->stack_g, s3);
+          G(false, false, M, d, d, T[9], d, dp(h, "off_W2"), d, 0.f, T[10], d);
+          G(true, false, d, d, M, T[9], d, T[4], d, 0.f, gp(h, "off_W2"), d);
+          launch_colsum(T[9], M, d, d, gp(h, "off_b2"), s3);
+          launch_gqe_inter_dh(T[10], T[3], n, M, d, T[11], s3);
+          G(true, false, d, d, NR, T[11], d, h->stack_v + d, 2 * d, 0.f, gp(h, "off_W1"), d);
+          launch_colsum(T[11], NR, d, d, gp(h, "off_b1"), s3);
+          G(false, false, NR, d, d, T[11], d, dp(h, "off_W1"), d, 1.f, h->stack_g + d, 2 * d);
+        }
         launch_q2b_att_bwd(h->stack_v, T[2], gout, n, M, d, T[7], h->stack_g, st);
-        launch_q2b_off_bwd(h->stack_v, T[6], h->amin, gout, n, M, d, T[9], h->stack_g, st);
         G(false, false, NR, d, d, T[7], d, dp(h, "att_W2"), d, 0.f, T[8], d);
         launch_relu_mask(T[8], T[0], NR, d, st);
         G(true, false, d, d, NR, T[7], d, T[0], d, 0.f, gp(h, "att_W2"), d);
@@ -585,13 +640,7 @@ kg_status dag_backward(kg_handle *h, StepBufs &S) {
         G(true, false, d, d, NR, T[8], d, h->stack_v, 2 * d, 0.f, gp(h, "att_W1"), d);
         launch_colsum(T[8], NR, d, d, gp(h, "att_b1"), st);
         G(false, false, NR, d, d, T[8], d, dp(h, "att_W1"), d, 1.f, h->stack_g, 2 * d);
-        G(false, false, M, d, d, T[9], d, dp(h, "off_W2"), d, 0.f, T[10], d);
-        G(true, false, d, d, M, T[9], d, T[4], d, 0.f, gp(h, "off_W2"), d);
-        launch_colsum(T[9], M, d, d, gp(h, "off_b2"), st);
-        launch_gqe_inter_dh(T[10], T[3], n, M, d, T[11], st);
-        G(true, false, d, d, NR, T[11], d, h->stack_v + d, 2 * d, 0.f, gp(h, "off_W1"), d);
-        launch_colsum(T[11], NR, d, d, gp(h, "off_b1"), st);
-        G(false, false, NR, d, d, T[11], d, dp(h, "off_W1"), d, 1.f, h->stack_g + d, 2 * d);
+        if ((fs = join(h, h->st3, st)) != KG_OK) return fs;
       } else if (h->kind == KG_BETAE) {
         // forward: T0 Hs, T1 Lg, T2 w.  backward: T7 dLg, T8 dHs
         launch_beta_att_bwd(h->stack_v, T[2], gout, n, M, d, T[7], h->stack_g, st);
@@ -798,10 +847,16 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
   if (cublasCreate(&h->blas) != CUBLAS_STATUS_SUCCESS) { kg_destroy(h); return KG_ECUDA; }
   if (cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->st_cap, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&h->st3, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_i1, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_i2, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork2, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
   if (cublasSetWorkspace(h->blas, h->blas_ws, 32 << 20) != CUBLAS_STATUS_SUCCESS) { kg_destroy(h); return KG_ECUDA; }
+  if (cublasCreate(&h->blas2) != CUBLAS_STATUS_SUCCESS ||
+      cublasSetWorkspace(h->blas2, h->blas_ws2, 32 << 20) != CUBLAS_STATUS_SUCCESS) { kg_destroy(h); return KG_ECUDA; }
+  cublasSetMathMode(h->blas2, CUBLAS_PEDANTIC_MATH);
   if (c.world > 1) {
     ncclUniqueId id;
     std::memcpy(&id, c.nccl_id, sizeof(id));
@@ -1415,8 +1470,12 @@ void kg_destroy(kg_handle *h) {
   if (h->st) cudaStreamSynchronize(h->st);
   else cudaDeviceSynchronize();
   if (h->blas) cublasDestroy(h->blas);
+  if (h->blas2) cublasDestroy(h->blas2);
   if (h->st2) { cudaStreamSynchronize(h->st2); cudaStreamDestroy(h->st2); }
   if (h->st_cap) cudaStreamDestroy(h->st_cap);
+  if (h->st3) { cudaStreamSynchronize(h->st3); cudaStreamDestroy(h->st3); }
+  if (h->ev_i1) cudaEventDestroy(h->ev_i1);
+  if (h->ev_i2) cudaEventDestroy(h->ev_i2);
   for (auto &g : h->graphs) cudaGraphExecDestroy(g.exec);
   if (h->ev_fork2) cudaEventDestroy(h->ev_fork2);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
