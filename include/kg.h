@@ -57,12 +57,17 @@ typedef enum {
 /* Query structures, DNF for unions. */
 typedef enum {
   KG_1P = 0, KG_2P = 1, KG_3P = 2, KG_2I = 3, KG_3I = 4,
-  KG_IP = 5, KG_PI = 6, KG_2U = 7, KG_UP = 8
+  KG_IP = 5, KG_PI = 6, KG_2U = 7, KG_UP = 8,
+  /* negation structures (Table 10), BetaE only: N(q) = 1/q (Table 1) */
+  KG_2IN = 9, KG_3IN = 10, KG_INP = 11, KG_PIN = 12, KG_PNI = 13
 } kg_structure;
 
 /* Number of anchor / relation slots of a structure (execution order, A21):
- * anchors 1p,2p,3p:1  2i:2  3i:3  ip,pi,2u,up:2
- * relations 1p:1 2p:2 3p:3 2i:2 3i:3 ip:3 pi:3 2u:2 up:3                  */
+ * anchors 1p,2p,3p:1  2i:2  3i:3  ip,pi,2u,up:2   2in:2 3in:3 inp,pin,pni:2
+ * relations 1p:1 2p:2 3p:3 2i:2 3i:3 ip:3 pi:3 2u:2 up:3   2in:2 3in:3 inp,pin,pni:3
+ * 2in = I(P(a0,r0), N(P(a1,r1)))         3in = I(P(a0,r0), P(a1,r1), N(P(a2,r2)))
+ * inp = P(I(P(a0,r0), N(P(a1,r1))), r2)   pin = I(P(P(a0,r0),r1), N(P(a1,r2)))
+ * pni = I(N(P(P(a0,r0),r1)), P(a1,r2))                                               */
 
 typedef struct {
   int32_t kind;          /* kg_model_kind */

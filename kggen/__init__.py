@@ -35,10 +35,15 @@ MODEL_ID = {m: i for i, m in enumerate(MODELS)}
 SINGLE_HOP = {"transe", "rotate", "distmult", "complex"}
 
 STRUCTURES = ["1p", "2p", "3p", "2i", "3i", "ip", "pi", "2u", "up"]
-STRUCTURE_ID = {s: i for i, s in enumerate(STRUCTURES)}
+# the 5 structures with negation (Table 10; BetaE only, Table 1 'Negation' column)
+NEG_STRUCTURES = ["2in", "3in", "inp", "pin", "pni"]
+ALL_STRUCTURES = STRUCTURES + NEG_STRUCTURES
+STRUCTURE_ID = {s: i for i, s in enumerate(ALL_STRUCTURES)}
 # slot counts per structure (execution order A21)
-N_ANCHORS = {"1p": 1, "2p": 1, "3p": 1, "2i": 2, "3i": 3, "ip": 2, "pi": 2, "2u": 2, "up": 2}
-N_RELS = {"1p": 1, "2p": 2, "3p": 3, "2i": 2, "3i": 3, "ip": 3, "pi": 3, "2u": 2, "up": 3}
+N_ANCHORS = {"1p": 1, "2p": 1, "3p": 1, "2i": 2, "3i": 3, "ip": 2, "pi": 2, "2u": 2, "up": 2,
+             "2in": 2, "3in": 3, "inp": 2, "pin": 2, "pni": 2}
+N_RELS = {"1p": 1, "2p": 2, "3p": 3, "2i": 2, "3i": 3, "ip": 3, "pi": 3, "2u": 2, "up": 3,
+          "2in": 2, "3in": 3, "inp": 3, "pin": 3, "pni": 3}
 
 # Default margins (reading A14; the paper states no value).
 DEFAULT_GAMMA = {"gqe": 24.0, "q2b": 24.0, "betae": 60.0, "transe": 24.0,

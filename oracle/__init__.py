@@ -34,11 +34,11 @@ differences).  The operator architectures that the paper leaves unstated
 invariants and special cases, not by a printed number ("parity unpinned by the
 paper" for their exact architecture).
 """
-from .model import (anchor_query, embed_entity, project, intersect, distance,
+from .model import (anchor_query, embed_entity, project, intersect, distance, negate,
                     query_disjuncts, dense_views)
 from .step import (dedup, adam, SparseTable, oracle_step, oracle_score, StepResult,
                    softplus, query_loss_terms)
 
-__all__ = ["anchor_query", "embed_entity", "project", "intersect", "distance",
+__all__ = ["anchor_query", "embed_entity", "project", "intersect", "distance", "negate",
            "query_disjuncts", "dense_views", "dedup", "adam", "SparseTable",
            "oracle_step", "oracle_score", "StepResult", "softplus", "query_loss_terms"]

@@ -164,9 +164,18 @@ def distance(kind: str, q: torch.Tensor, v: torch.Tensor, box_alpha: float = 0.0
     raise ValueError(kind)
 
 
+# ------------------------------------------------------------------ negation
+def negate(kind: str, q: torch.Tensor) -> torch.Tensor:
+    """Negation N(q) = 1 / Em(q) on the Beta parameters (Table 1); BetaE only."""
+    if kind != "betae":
+        raise ValueError(f"{kind} has no negation operator (Table 1 'Negation' column is '-')")
+    return 1.0 / q
+
+
 # --------------------------------------------------------------- query DAGs
 def query_disjuncts(structure: str, kind: str, anchors: list, rels: list, P: dict) -> list:
-    """Evaluate the computation plan of a structure bottom-up.
+    """Evaluate the computation plan of a structure bottom-up (the
+    negation structures 2in / 3in / inp / pin / pni of P:L775 use N(q) = 1/q, BetaE only).
 
     anchors: list (per anchor slot, execution order) of RAW rows [M, d];
     rels: list (per relation slot, execution order A21) of int64 [M].
@@ -201,4 +210,19 @@ def query_disjuncts(structure: str, kind: str, anchors: list, rels: list, P: dic
     if s == "up":
         # (p (u (p a0) (p a1))) in DNF: the final relation r2 applies to both branches
         return [p(p(A[0], 0), 2), p(p(A[1], 1), 2)]
+
+    def n(q):
+        return negate(kind, q)
+
+    # negation structures (BetaE): n marks the negated branch
+    if s == "2in":
+        return [i(p(A[0], 0), n(p(A[1], 1)))]
+    if s == "3in":
+        return [i(p(A[0], 0), p(A[1], 1), n(p(A[2], 2)))]
+    if s == "inp":
+        return [p(i(p(A[0], 0), n(p(A[1], 1))), 2)]
+    if s == "pin":
+        return [i(p(p(A[0], 0), 1), n(p(A[1], 2)))]
+    if s == "pni":
+        return [i(n(p(p(A[0], 0), 1)), p(A[1], 2))]
     raise ValueError(s)

@@ -200,6 +200,26 @@ void launch_betae_split(const float *dX, int N, int d, const int64_t *anchor_row
   { betae_split_kernel<<<blocks((int64_t)N * d), 256, 0, st>>>(dX, N, d, anchor_rows, ent, din, din_ld, drel); ++g_launches; }
 }
 
+// ------------------------------------------------------------ negation (BetaE)
+// N(q) = 1/q elementwise on (alpha, beta) (Table 1 'Negation' P:L143); adjoint -g/q^2.
+__global__ void neg_fwd_kernel(const float *in, int64_t n, float *out) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < n) out[e] = 1.f / in[e];
+}
+__global__ void neg_bwd_kernel(const float *dout, const float *in, int64_t n, float *din) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < n) {
+    const float x = in[e];
+    din[e] = -dout[e] / (x * x);
+  }
+}
+void launch_neg_fwd(const float *in, int64_t n, float *out, cudaStream_t st) {
+  if (n > 0) { neg_fwd_kernel<<<blocks(n), 256, 0, st>>>(in, n, out); ++g_launches; }
+}
+void launch_neg_bwd(const float *dout, const float *in, int64_t n, float *din, cudaStream_t st) {
+  if (n > 0) { neg_bwd_kernel<<<blocks(n), 256, 0, st>>>(dout, in, n, din); ++g_launches; }
+}
+
 // ------------------------------------------------------------ intersections
 __global__ void mean_stack_kernel(const float *H, int n, int64_t rc, float *out) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;

@@ -79,7 +79,7 @@ const NcclApi &nccl() {
 
 // ------------------------------------------------------------------ plans
 struct PNode {
-  int type;       // 0 projection, 1 intersection
+  int type;       // 0 projection, 1 intersection, 2 negation (input = `in`)
   int in;         // projection input node (-1: anchor slot)
   int anchor;     // anchor slot (when in == -1)
   int rel;        // relation slot (execution order, A21)
@@ -96,6 +96,7 @@ struct Plan {
 PNode P(int in, int anchor, int rel) { return PNode{0, in, anchor, rel, {0, 0, 0}, 0}; }
 PNode I2(int a, int b) { return PNode{1, -1, -1, -1, {a, b, 0}, 2}; }
 PNode I3(int a, int b, int c) { return PNode{1, -1, -1, -1, {a, b, c}, 3}; }
+PNode Ng(int in) { return PNode{2, in, -1, -1, {0, 0, 0}, 0}; }
 
 Plan make_plan(int s) {
   Plan p{};
@@ -118,11 +119,16 @@ Plan make_plan(int s) {
     case KG_PI: set({P(-1, 0, 0), P(0, -1, 1), P(-1, 1, 2), I2(1, 2)}, {3}, 2, 3); break;
     case KG_2U: set({P(-1, 0, 0), P(-1, 1, 1)}, {0, 1}, 2, 2); break;
     case KG_UP: set({P(-1, 0, 0), P(0, -1, 2), P(-1, 1, 1), P(2, -1, 2)}, {1, 3}, 2, 3); break;
+    case KG_2IN: set({P(-1, 0, 0), P(-1, 1, 1), Ng(1), I2(0, 2)}, {3}, 2, 2); break;
+    case KG_3IN: set({P(-1, 0, 0), P(-1, 1, 1), P(-1, 2, 2), Ng(2), I3(0, 1, 3)}, {4}, 3, 3); break;
+    case KG_INP: set({P(-1, 0, 0), P(-1, 1, 1), Ng(1), I2(0, 2), P(3, -1, 2)}, {4}, 2, 3); break;
+    case KG_PIN: set({P(-1, 0, 0), P(0, -1, 1), P(-1, 1, 2), Ng(2), I2(1, 3)}, {4}, 2, 3); break;
+    case KG_PNI: set({P(-1, 0, 0), P(0, -1, 1), Ng(1), P(-1, 1, 2), I2(2, 3)}, {4}, 2, 3); break;
   }
   p.nproj = 0;
   for (int i = 0; i < p.nn; ++i) {
     if (p.n[i].type == 0) p.nproj++;
-    else p.inter = i;
+    else if (p.n[i].type == 1) p.inter = i;
   }
   return p;
 }
@@ -532,6 +538,8 @@ kg_status dag_forward(kg_handle *h, StepBufs &S) {
         launch_proj_fwd(h->kind, M, d, in, dq, arows, ent, rel, 1, relA, relB, S.val[ni], st);
       }
       ++u;
+    } else if (nd.type == 2) {
+      launch_neg_fwd(S.val[nd.in], (int64_t)M * d, S.val[ni], st);   // N(q) = 1/q (Table 1)
     } else {
       const int n = nd.nin, NR = n * M;
       float *out = S.val[ni];
@@ -602,6 +610,8 @@ kg_status dag_backward(kg_handle *h, StepBufs &S) {
         launch_proj_bwd(h->kind, M, d, S.grad[ni], in, dq, arows, ent, rel, 1, relA, relB, S.val[ni], din, din_ld,
                         drel, st);
       }
+    } else if (nd.type == 2) {
+      launch_neg_bwd(S.grad[ni], S.val[nd.in], (int64_t)M * d, S.grad[nd.in], st);   // d(1/x) = -dx / x^2
     } else {
       const int n = nd.nin, NR = n * M;
       const float *gout = S.grad[ni];
@@ -1176,9 +1186,11 @@ kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info)
   kg_status s = check_state(h);
   if (s) return s;
   if (!b) return fail(h, KG_EINVAL, "null batch");
-  if (b->structure < KG_1P || b->structure > KG_UP) return fail(h, KG_EINVAL, "bad structure");
+  if (b->structure < KG_1P || b->structure > KG_PNI) return fail(h, KG_EINVAL, "bad structure");
   if (single_hop(h->kind) && b->structure != KG_1P)
     return fail(h, KG_EUNSUPPORTED, "single-hop models accept only 1p (Table 2, P:L55)");
+  if (b->structure >= KG_2IN && h->kind != KG_BETAE)
+    return fail(h, KG_EUNSUPPORTED, "negation structures need BetaE (Table 1 'Negation' column)");
   if (!(lr > 0.f)) return fail(h, KG_EINVAL, "lr must be > 0");
   StepBufs S;
   S.plan = make_plan(b->structure);
@@ -1250,8 +1262,10 @@ kg_status kg_score(kg_handle *h, const kg_batch *q, const int64_t *cand, int32_t
   kg_status s = check_state(h);
   if (s) return s;
   if (!q || !cand || !out_dist) return fail(h, KG_EINVAL, "null argument");
-  if (q->structure < KG_1P || q->structure > KG_UP) return fail(h, KG_EINVAL, "bad structure");
+  if (q->structure < KG_1P || q->structure > KG_PNI) return fail(h, KG_EINVAL, "bad structure");
   if (single_hop(h->kind) && q->structure != KG_1P) return fail(h, KG_EUNSUPPORTED, "single-hop models accept only 1p");
+  if (q->structure >= KG_2IN && h->kind != KG_BETAE)
+    return fail(h, KG_EUNSUPPORTED, "negation structures need BetaE (Table 1 'Negation' column)");
   if (n_cand < 1 || n_cand > h->Cx) return fail(h, KG_EINVAL, "n_cand out of range [1, max_cand]");
   for (int c = 0; c < n_cand; ++c)
     if (cand[c] < 0 || cand[c] >= h->n_ent) return fail(h, KG_EINVAL, "candidate id out of range");

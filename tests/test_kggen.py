@@ -43,7 +43,7 @@ def test_mask_roundtrip():
         assert np.array_equal(kggen.unpack_mask(words, K), bits)
 
 
-@pytest.mark.parametrize("structure", kggen.STRUCTURES)
+@pytest.mark.parametrize("structure", kggen.ALL_STRUCTURES)
 def test_make_batch_shapes(structure):
     cfg = kggen.ModelConfig("betae", 8, 1000, 10)
     b = kggen.make_batch(cfg, structure, 40, 70, seed=3, step=2)

@@ -392,3 +392,42 @@ def test_finite_differences(kind, structure):
         assert abs(fd - an) <= 1e-6 * abs(an) + 1e-7 * scale, (fd, an)
         checked += 1
     assert checked == 24
+
+
+# ------------------------------------------------- negation
+def test_negation_closed_forms():
+    # Table 1 P:L143 N(q) = 1/Em(q): (alpha, beta) = (2, 4) -> (0.5, 0.25); N(N(q)) = q
+    q = torch.tensor([[2.0, 4.0]], dtype=F64)
+    torch.testing.assert_close(oracle.negate("betae", q), torch.tensor([[0.5, 0.25]], dtype=F64))
+    r = torch.tensor(np.random.default_rng(8).uniform(0.05, 5, size=(3, 6)), dtype=F64)
+    torch.testing.assert_close(oracle.negate("betae", oracle.negate("betae", r)), r, rtol=1e-15, atol=0)
+    for kind in ("gqe", "q2b"):
+        with pytest.raises(ValueError):
+            oracle.negate(kind, q)
+
+
+def test_negated_beta_kl_closed_form():
+    # KL(B(2,5) || N(B(1/3, 1/3))) = KL(B(2,5) || B(3,3)) = 43/60
+    q = oracle.negate("betae", torch.tensor([1 / 3, 1 / 3], dtype=F64))
+    v = torch.tensor([1.0, 4.0], dtype=F64)        # raw row of Beta(2, 5) (A8)
+    assert float(oracle.distance("betae", q, v)) == pytest.approx(43 / 60, rel=1e-13)
+
+
+def test_2in_with_identical_inputs_negates_one_branch():
+    # with identical attention logits the 2in output is the mean of q and 1/q (A5)
+    cfg = kggen.ModelConfig("betae", 4, 12, 3, hidden=8)
+    dense = kggen.init_dense(cfg, 1).astype(np.float64)
+    offs, _ = kggen.dense_offsets(cfg)
+    o, shape = offs["att_U2"]
+    dense[o:o + int(np.prod(shape))] = 0.0           # U2 = 0 -> equal logits whatever the input
+    o, shape = offs["att_c2"]
+    dense[o:o + int(np.prod(shape))] = 0.0
+    P = dense_views(cfg, torch.tensor(dense))
+    q = torch.tensor([[0.5, 2.0, 1.5, 0.25]], dtype=F64)
+    out = oracle.intersect("betae", [q, oracle.negate("betae", q)], P)
+    torch.testing.assert_close(out, (q + 1.0 / q) / 2, rtol=1e-14, atol=0)
+
+
+@pytest.mark.parametrize("structure", kggen.NEG_STRUCTURES)
+def test_finite_differences_negation(structure):
+    test_finite_differences("betae", structure)

@@ -87,7 +87,8 @@ def _check_step(gm, table, cfg, batch, lr, step_no=1):
 
 
 CASES = [(k, s) for k in ("gqe", "q2b", "betae") for s in kggen.STRUCTURES] + \
-        [(k, "1p") for k in ("transe", "rotate", "distmult", "complex")]
+        [(k, "1p") for k in ("transe", "rotate", "distmult", "complex")] + \
+        [("betae", s) for s in kggen.NEG_STRUCTURES]          # negation, BetaE only (f1)
 
 
 @pytest.mark.parametrize("kind,structure", CASES)
@@ -117,7 +118,8 @@ def test_init_matches_generator_bit_exact():
 
 
 @pytest.mark.parametrize("kind,structure", [("gqe", "ip"), ("q2b", "up"), ("betae", "pi"), ("rotate", "1p"),
-                                            ("complex", "1p"), ("q2b", "3i")])
+                                            ("complex", "1p"), ("q2b", "3i"), ("betae", "pni"),
+                                            ("betae", "3in")])
 def test_score_parity(kind, structure):
     cfg = kggen.ModelConfig(kind, 40, 300, 7, hidden=24)
     gm = _model(cfg, 70, 100, max_cand=90)
@@ -203,6 +205,24 @@ def test_validation_errors_leave_tables_untouched():
     assert e.value.status == 1
     with pytest.raises(KGError):
         gm.step(gm.host_batch(kggen.make_batch(cfg, "1p", 71, 16, seed=8)), 0.01)   # M > max_M
+    np.testing.assert_array_equal(gm.read_dense(), before)
+    gm.close()
+
+
+@pytest.mark.parametrize("kind", ["gqe", "q2b"])
+def test_negation_structures_need_betae(kind):
+    """Table 1 'Negation' column: only BetaE has N(q); other kinds get KG_EUNSUPPORTED."""
+    from paper_2110_14890_b200 import KGError
+    cfg = kggen.ModelConfig(kind, 40, 300, 7)
+    gm = _model(cfg, 70, 100, max_cand=10)
+    before = gm.read_dense()
+    b = kggen.make_batch(cfg, "2in", 8, 16, seed=8)
+    with pytest.raises(KGError) as e:
+        gm.step(gm.host_batch(b), 0.01)
+    assert e.value.status == 2
+    with pytest.raises(KGError) as e:
+        gm.score(gm.host_batch(b), np.arange(10))
+    assert e.value.status == 2
     np.testing.assert_array_equal(gm.read_dense(), before)
     gm.close()
 
