@@ -192,9 +192,9 @@ const char *kg_last_error(const kg_handle *h);
 
 /* Test hook: the tensor-core GEMM of the query-DAG contractions on device pointers,
  * C[M][N] (ldc) = beta*C + op(A) op(B)^T (+ bias[n]) (ReLU if relu), op(A) = [M][K], op(B) = [N][K];
- * ta: A stored [K][lda] (else [M][lda]); tb: B stored [K][ldb] (else [N][ldb]).  tcgen05
- * kind::tf32 with a 3xTF32 split (fp32-level accuracy); a non-transposed operand needs ld % 4 == 0
- * (else EINVAL).  Synchronises the stream. */
+ * ta: A stored [K][lda] (else [M][lda]); tb: B stored [K][ldb] (else [N][ldb]); both layouts are
+ * read in place by TMA.  tcgen05 kind::tf32 with a 3xTF32 split (fp32-level accuracy).  Needs
+ * K >= 1, 16-byte aligned A / B and lda % 4 == ldb % 4 == 0 (else EINVAL).  Synchronises the stream. */
 kg_status kg_test_gemm(int32_t ta, int32_t tb, int32_t M, int32_t N, int32_t K, const float *A, int32_t lda,
                        const float *B, int32_t ldb, float *C, int32_t ldc, const float *bias, int32_t relu, float beta,
                        void *stream);

@@ -30,6 +30,7 @@ def _nccl_dir():
 NCCL_DIR = _nccl_dir()
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills", "-I", os.path.join(ROOT, "include")]
+FLAGS += os.environ.get("KG_NVCC_EXTRA", "").split()   # experiments (e.g. -DKG_G2CW=12)
 if NCCL_DIR:
     FLAGS += ["-I", os.path.join(NCCL_DIR, "include"),
               f'-DKG_NCCL_PATH="{os.path.join(NCCL_DIR, "lib", "libnccl.so.2")}"']
@@ -39,13 +40,14 @@ def sources():
     return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, out: str = None) -> str:
+    OUT_ = out or OUT
     srcs = sources()
     deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     deps.append(os.path.join(ROOT, "include", "kg.h"))
-    if not force and os.path.exists(OUT) and all(os.path.getmtime(OUT) >= os.path.getmtime(d) for d in deps):
-        return OUT
-    objdir = os.path.join(HERE, "build")
+    if not force and os.path.exists(OUT_) and all(os.path.getmtime(OUT_) >= os.path.getmtime(d) for d in deps):
+        return OUT_
+    objdir = os.path.join(HERE, "build" if out is None else "build_" + os.path.basename(out))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
@@ -63,11 +65,12 @@ def build(verbose: bool = False, force: bool = False) -> str:
             raise RuntimeError(f"nvcc failed on {s}")
         if verbose and out:
             sys.stderr.write(out.decode())
-    cmd = [NVCC, *ARCH, "-shared", "-o", OUT + ".tmp", *objs, "-lcublas", "-ldl", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", OUT_ + ".tmp", *objs, "-lcublas", "-ldl", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
     subprocess.run(cmd, check=True)
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    os.replace(OUT_ + ".tmp", OUT_)
+    return OUT_
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    o = [a[6:] for a in sys.argv if a.startswith("--out=")]
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, out=o[0] if o else None))

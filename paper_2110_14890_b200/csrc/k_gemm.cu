@@ -1,63 +1,31 @@
 // k_gemm.cu -- dense contractions of the query DAG on the 5th-generation tensor
-// cores (tcgen05, TMEM accumulators), fp32-accurate through a 3xTF32 split.
+// cores (tcgen05, TMEM accumulators, TMA), fp32-accurate through a 3xTF32 split.
 //
 // The BetaE projection MLP (reading A9; Table 1 'MLP') and the d x d
 // DeepSet / attention MLPs (A4, A5; Table 1) are plain dense
 // contractions Y = X W^T, dX = dY W, dW = dY^T X over the batch rows: they
 // belong on the tensor cores.  kind::tf32 reads 19 significant bits; fp32
 // parity (1e-5, BASELINE north_star) needs the classic split
-//     x = hi + lo,  hi = rna_tf32(x),  lo = x - hi (exact),
+//     x = hi + lo,  hi = trunc_tf32(x),  lo = x - hi (exact),
 //     x.y ~= hi_x.hi_y + hi_x.lo_y + lo_x.hi_y        (error ~ 2^-21 |x||y|)
 // i.e. three tcgen05.mma per K-step into the same fp32 TMEM accumulator.
-//
-// Tile 128 (M) x 128 (N) x 32 (K), one CTA of 4 warps per output tile:
-//   * cp.async copies the raw fp32 operand tiles (K-major; transposed
-//     operands are transposed by a separate kernel first) straight into their
-//     128-byte-swizzled 8-row atoms (the SWIZZLE_128B canonical layout the UMMA
-//     smem descriptors read), 3 stages in flight; all threads then split each
-//     landed tile in place into hi and a separate lo tile;
-//   * one elected thread issues 4 K-steps x 3 MMAs per stage and commits them
-//     to the stage's mbarrier, which gates the refill of that stage;
-//   * epilogue: tcgen05.ld (32 lanes x 32 columns per warp and load) ->
-//     optional bias, ReLU, C += -> global.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "kg_common.cuh"
 #include "kg_launch.h"
 
 namespace kg {
 
-constexpr int GBM = 128, GBN = 128, GBK = 32, GSTAGES = 3, GTHREADS = 256;
-constexpr int GCH = GBM * GBK / 4 / GTHREADS;   // 16-byte chunks per thread per tile
-constexpr int GTILE = GBM * GBK * 4;          // 16 KB: one operand tile (hi or lo)
-constexpr int GSTAGE = 4 * GTILE;             // A_hi, A_lo, B_hi, B_lo
-constexpr int GSMEM = GSTAGES * GSTAGE + 1024;  // + alignment slack
+constexpr int GBM = 128;
 
 __device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B apart.
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)1 << 16;                   // leading byte offset (unused for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;         // stride byte offset
-  d |= (uint64_t)1 << 46;                   // descriptor version (sm_100)
-  d |= (uint64_t)2 << 61;                   // SWIZZLE_128B
-  return d;
-}
-
-// Instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = 128.
-constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(GBN >> 3) << 17) |
-                            ((uint32_t)(GBM >> 4) << 24);
-
-__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-      "l"(a), "l"(b), "r"(kIdesc), "r"(acc));
-}
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar)));
 }
@@ -68,159 +36,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
         : "r"(su32(bar)), "r"(parity));
-}
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
-// byte offset of 16-byte chunk ch (k = 4 ch .. 4 ch + 3) of row `row` in a K-major SW128 tile
-__device__ __forceinline__ uint32_t sw_chunk(int row, int ch) {
-  return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((ch ^ (row & 7)) << 4));
-}
-
-// cp.async the raw fp32 128 x 32 tile rows [r0, r0+128) x k [k0, k0+32) of a K-major operand
-// (stored [rows][ld], ld % 4 == 0) into its swizzled position (zero-filled outside).
-__device__ __forceinline__ void load_tile_async(const float *__restrict__ G, int ld, int rows, int K, int r0, int k0,
-                                                uint8_t *dst, int tid) {
-#pragma unroll
-  for (int j = 0; j < GCH; ++j) {
-    const int f = tid + GTHREADS * j, row = f >> 3, ch = f & 7;
-    const int r = r0 + row, k = k0 + ch * 4;
-    const int bytes = (r < rows && k < K) ? min(16, (K - k) * 4) : 0;
-    const float *src = bytes ? G + (int64_t)r * ld + k : G;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(su32(dst + sw_chunk(row, ch))), "l"(src),
-                 "r"(bytes));
-  }
-}
-// in place: hi slot holds the raw fp32 values -> hi = rna_tf32(x) there, lo = x - hi in the lo tile
-__device__ __forceinline__ void split_tile(uint8_t *hi, uint8_t *lo, int tid) {
-#pragma unroll
-  for (int j = 0; j < GCH; ++j) {
-    const int off = (tid + GTHREADS * j) * 16;
-    float4 v = *reinterpret_cast<float4 *>(hi + off), h, l;
-    h.x = tf32_rna(v.x); h.y = tf32_rna(v.y); h.z = tf32_rna(v.z); h.w = tf32_rna(v.w);
-    l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
-    *reinterpret_cast<float4 *>(hi + off) = h;
-    *reinterpret_cast<float4 *>(lo + off) = l;
-  }
-}
-
-// C[M][N] (ldc) = beta * C + op(A) op(B)^T (+ bias[n]) (ReLU), op(A) = [M][K], op(B) = [N][K].
-__global__ void __launch_bounds__(GTHREADS, 1) gemm_tf32x3_kernel(GemmArgs g) {
-  extern __shared__ uint8_t gsm_raw[];
-  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t empty_bar[GSTAGES];
-  __shared__ __align__(8) uint64_t done_bar;
-  __shared__ uint32_t tmem_base;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * GBN;
-
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)),
-                 "n"(GBN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 0) {
-    for (int s = 0; s < GSTAGES; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&empty_bar[s])));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&done_bar)));
-    asm volatile("fence.mbarrier_init.release.cluster;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = tmem_base;
-
-  const int nkb_all = (g.K + GBK - 1) / GBK;
-  const int kb0 = blockIdx.z * g.kbs, nkb = min(nkb_all, kb0 + g.kbs) - kb0;   // split-K range
-  // prologue: raw tiles of the first GSTAGES - 1 k-blocks in flight
-#pragma unroll
-  for (int p = 0; p < GSTAGES - 1; ++p) {
-    if (p < nkb) {
-      uint8_t *st = sm + p * GSTAGE;
-      load_tile_async(g.A, g.lda, g.M, g.K, m0, (kb0 + p) * GBK, st, tid);
-      load_tile_async(g.B, g.ldb, g.N, g.K, n0, (kb0 + p) * GBK, st + 2 * GTILE, tid);
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-  }
-  for (int kb = 0; kb < nkb; ++kb) {
-    const int s = kb % GSTAGES;
-    // refill the stage of k-block kb + GSTAGES - 1 once the MMAs that read it (kb - 1) are done
-    const int kn = kb + GSTAGES - 1;
-    if (kn < nkb) {
-      const int sn = kn % GSTAGES;
-      if (kb >= 1) mbar_wait(&empty_bar[sn], ((kb - 1) / GSTAGES) & 1);
-      uint8_t *st = sm + sn * GSTAGE;
-      load_tile_async(g.A, g.lda, g.M, g.K, m0, (kb0 + kn) * GBK, st, tid);
-      load_tile_async(g.B, g.ldb, g.N, g.K, n0, (kb0 + kn) * GBK, st + 2 * GTILE, tid);
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(GSTAGES - 1));   // k-block kb has landed (this thread)
-    __syncthreads();                                                  // ... for every thread
-    uint8_t *st = sm + s * GSTAGE;
-    split_tile(st, st + GTILE, tid);
-    split_tile(st + 2 * GTILE, st + 3 * GTILE, tid);
-    asm volatile("fence.proxy.async.shared::cta;");   // generic-proxy stores -> tensor-core (async proxy) reads
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t ah = su32(st), al = su32(st + GTILE), bh = su32(st + 2 * GTILE), bl = su32(st + 3 * GTILE);
-#pragma unroll
-      for (int kk = 0; kk < GBK / 8; ++kk) {          // K = 8 tf32 (32 bytes) per MMA
-        const uint32_t o = kk * 32;
-        const uint64_t dah = sw128_desc(ah + o), dal = sw128_desc(al + o);
-        const uint64_t dbh = sw128_desc(bh + o), dbl = sw128_desc(bl + o);
-        mma_tf32(tmem, dah, dbh, (kb | kk) != 0);
-        mma_tf32(tmem, dah, dbl, 1);
-        mma_tf32(tmem, dal, dbh, 1);
-      }
-      mma_commit(&empty_bar[s]);
-    }
-  }
-  asm volatile("cp.async.wait_group 0;\n" ::);
-  if (tid == 0) mma_commit(&done_bar);
-  mbar_wait(&done_bar, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;");
-
-  // epilogue: warp w owns accumulator lanes (rows) 32 (w % 4) .. + 31 and column half w / 4
-  const int row = m0 + (warp & 3) * 32 + lane;
-#pragma unroll 1
-  for (int c0 = (warp >> 2) * (GBN / 2); c0 < (warp >> 2) * (GBN / 2) + GBN / 2; c0 += 32) {
-    uint32_t r[32];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
-        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0));
-    asm volatile("tcgen05.wait::ld.sync.aligned;");
-    if (row < g.M && g.P) {        // split-K: raw partial sums, combined by gemm_reduce_kernel
-      float *prow = g.P + ((int64_t)blockIdx.z * g.M + row) * g.N;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int n = n0 + c0 + j;
-        if (n < g.N) prow[n] = __uint_as_float(r[j]);
-      }
-    } else if (row < g.M) {
-      float *crow = g.C + (int64_t)row * g.ldc;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int n = n0 + c0 + j;
-        if (n < g.N) {
-          float v = __uint_as_float(r[j]);
-          if (g.bias) v += g.bias[n];
-          if (g.relu) v = fmaxf(v, 0.f);
-          if (g.beta != 0.f) v += g.beta * crow[n];
-          crow[n] = v;
-        }
-      }
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(GBN));
 }
 
 // out[c][r] = in[r][c]: in [R][C] (ld_in), out [C][R] (ld_out); 32 x 32 tiles through shared memory.
@@ -259,31 +74,332 @@ __global__ void gemm_reduce_kernel(const float *__restrict__ P, int splits, int 
   *c = v;
 }
 
-// Operands must be K-major with ld % 4 == 0 (kg_api.cu transposes the others).  When the
-// output has fewer tiles than SMs, K is split over blockIdx.z (at most one wave of CTAs:
-// 192 KB of shared memory per CTA) into `part` (capacity part_cap floats).
-void launch_gemm_tc(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t st) {
-  if (g0.M <= 0 || g0.N <= 0) return;
+
+// ================================================================ v2: TMA + warp specialisation
+// Tile 128 (M) x BN (N) x 16 (K), 6 warps with fixed roles:
+//   warp 0      TMA producer: cp.async.bulk.tensor of the raw fp32 A / B tiles into stage s
+//               (zero fill out of bounds), completion on full[s];
+//   warp 1      TMEM allocator + MMA issuer: per k-block 2 K-steps x 3 tcgen05.mma
+//               (hi.hi, hi.lo, lo.hi), committed to empty[s];
+//   warps 2-5   split + epilogue: lo = x - trunc_tf32(x) of the landed tiles (kind::tf32 reads
+//               the raw fp32 words of a K-major tile as hi = trunc_tf32(x)), then tcgen05.ld of
+//               the accumulator quarter their warp may access (lanes 32 (w % 4) ..) -> per-warp
+//               staging tile -> bias / ReLU / beta C -> coalesced row stores.
+// kind::tf32 reads K-major operands only (the idesc transpose bits give zeros, measured), so
+// an operand stored MN-major (A [K][M], B [K][N], e.g. both operands of dW = dY^T X) is
+// brought in as raw 32 x 16 boxes and the split warps transpose it while splitting, writing
+// hi and lo K-major tiles; no global transpose pass.
+// K-major smem tiles: rows of 16 fp32 (64 B), SWIZZLE_64B, 8-row groups 512 B apart.
+#ifndef KG_G2CW
+#define KG_G2CW 8
+#endif
+constexpr int G2CW = KG_G2CW;                          // split / epilogue warps
+constexpr int G2T = 64 + 32 * G2CW, G2K = 16;
+template <int BN, bool AMN, bool BMN> struct G2Cfg {
+  static constexpr int kA = GBM * G2K * 4, kB = BN * G2K * 4;           // bytes of one tile
+  // stage: A raw, B raw, [A hi if AMN], [B hi if BMN], A lo, B lo
+  static constexpr int kStage = 2 * (kA + kB) + (AMN ? kA : 0) + (BMN ? kB : 0);
+  static constexpr int kStages = (196 * 1024) / kStage < 8 ? (196 * 1024) / kStage : 8;
+  static constexpr int kSmem = kStages * kStage + 1024;
+  static constexpr int oAhi = kA + kB, oBhi = oAhi + (AMN ? kA : 0);
+  static constexpr int oAlo = oBhi + (BMN ? kB : 0), oBlo = oAlo + kA;
+  static constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                     ((uint32_t)(GBM >> 4) << 24);
+};
+__device__ __forceinline__ uint64_t kmajor_desc(uint32_t saddr, int kk) {
+  uint64_t d = (uint64_t)(((saddr + kk * 32) >> 4) & 0x3FFF);   // K-step = 32 B inside the 64 B row
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(512 >> 4) << 32;                              // 8-row groups 512 B apart
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;                                       // SWIZZLE_64B
+  return d;
+}
+// byte offset of 16-byte chunk q (k = 4q .. 4q+3) of row r in a K-major SWIZZLE_64B tile
+__device__ __forceinline__ uint32_t sw64_off(int r, int q) {
+  return (uint32_t)((r >> 3) * 512 + (r & 7) * 64 + ((q ^ ((r >> 1) & 3)) << 4));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *b, int n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap *tm, uint64_t *bar, void *dst, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(su32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+template <uint32_t IDESC>
+__device__ __forceinline__ void mma_tf32_i(uint32_t tmem, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(IDESC), "r"(acc));
+}
+// one operand tile (rows r0 .. r0 + R, k0 .. k0 + 16) into dst: K-major one SWIZZLE_64B box;
+// MN-major R / 32 unswizzled boxes of 32 (rows) x 16 (k), 2048 B each ([k][32 rows])
+template <bool MN, int R>
+__device__ __forceinline__ void load_op(const CUtensorMap *tm, uint64_t *bar, uint8_t *dst, int r0, int k0) {
+  if (MN) {
+#pragma unroll
+    for (int c = 0; c < R / 32; ++c) tma_load_2d(tm, bar, dst + c * 2048, r0 + 32 * c, k0);
+  } else {
+    tma_load_2d(tm, bar, dst, k0, r0);
+  }
+}
+__device__ __forceinline__ float4 tf32_lo(float4 v) {
+  float4 l;
+  l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+  l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+  l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+  l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+  return l;
+}
+// split one landed operand tile of R rows (32 G2CW threads, ct = 0 ..)
+template <bool MN, int R>
+__device__ __forceinline__ void split_op(const uint8_t *raw, uint8_t *hi, uint8_t *lo, int ct) {
+  if (!MN) {   // K-major: same (swizzled) offsets, lo only
+#pragma unroll 4
+    for (int c = ct; c < R * 4; c += 32 * G2CW) {
+      const float4 v = *reinterpret_cast<const float4 *>(raw + c * 16);
+      *reinterpret_cast<float4 *>(lo + c * 16) = tf32_lo(v);
+    }
+  } else {     // MN-major raw [R/32][16 k][32 rows] -> K-major SW64 hi and lo, 4 k per chunk
+#pragma unroll 4
+    for (int c = ct; c < R * 4; c += 32 * G2CW) {
+      const int r = c % R, q = c / R;
+      const float *src = reinterpret_cast<const float *>(raw + (r >> 5) * 2048) + (r & 31);
+      float4 v;
+      v.x = src[(4 * q + 0) * 32];
+      v.y = src[(4 * q + 1) * 32];
+      v.z = src[(4 * q + 2) * 32];
+      v.w = src[(4 * q + 3) * 32];
+      const float4 l = tf32_lo(v);
+      const uint32_t o = sw64_off(r, q);
+      *reinterpret_cast<float4 *>(hi + o) = v;
+      *reinterpret_cast<float4 *>(lo + o) = l;
+    }
+  }
+}
+
+template <int BN, bool AMN, bool BMN>
+__global__ void __launch_bounds__(G2T, 1)
+    gemm_tf32x3_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
+  using Cfg = G2Cfg<BN, AMN, BMN>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ uint8_t gsm_raw[];
+  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full_bar[S], conv_bar[S], empty_bar[S];
+  __shared__ __align__(8) uint64_t done_bar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * BN;
+  const int nkb_all = (g.K + G2K - 1) / G2K;
+  const int kb0 = blockIdx.z * g.kbs, nkb = min(nkb_all, kb0 + g.kbs) - kb0;   // split-K range
+
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)),
+                 "n"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&conv_bar[s], 32 * G2CW);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&done_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % S;
+        if (kb >= S) mbar_wait(&empty_bar[s], ((kb / S) - 1) & 1);
+        uint8_t *st = sm + s * Cfg::kStage;
+        mbar_expect_tx(&full_bar[s], Cfg::kA + Cfg::kB);
+        const int k0 = (kb0 + kb) * G2K;
+        load_op<AMN, GBM>(&tmA, &full_bar[s], st, m0, k0);
+        load_op<BMN, BN>(&tmB, &full_bar[s], st + Cfg::kA, n0, k0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % S;
+        mbar_wait(&conv_bar[s], (kb / S) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t st = su32(sm + s * Cfg::kStage);
+        const uint32_t ah = AMN ? st + Cfg::oAhi : st, bh = BMN ? st + Cfg::oBhi : st + Cfg::kA;
+        const uint32_t al = st + Cfg::oAlo, bl = st + Cfg::oBlo;
+#pragma unroll
+        for (int kk = 0; kk < G2K / 8; ++kk) {   // K = 8 tf32 per MMA
+          const uint64_t dah = kmajor_desc(ah, kk), dal = kmajor_desc(al, kk);
+          const uint64_t dbh = kmajor_desc(bh, kk), dbl = kmajor_desc(bl, kk);
+          mma_tf32_i<Cfg::kIdesc>(tmem, dah, dbh, (kb | kk) != 0);
+          mma_tf32_i<Cfg::kIdesc>(tmem, dah, dbl, 1);
+          mma_tf32_i<Cfg::kIdesc>(tmem, dal, dbh, 1);
+        }
+        mma_commit(&empty_bar[s]);
+      }
+      mma_commit(&done_bar);
+    }
+  } else {
+    // ---- split (and transpose the MN-major operands)
+    const int ct = tid - 64;
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % S;
+      mbar_wait(&full_bar[s], (kb / S) & 1);
+      uint8_t *st = sm + s * Cfg::kStage;
+      split_op<AMN, GBM>(st, st + Cfg::oAhi, st + Cfg::oAlo, ct);
+      split_op<BMN, BN>(st + Cfg::kA, st + Cfg::oBhi, st + Cfg::oBlo, ct);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic stores -> tensor-core reads
+      mbar_arrive(&conv_bar[s]);
+    }
+    // ---- epilogue: TMEM -> registers (thread = accumulator row) -> per-warp 32 x 33 staging
+    // tile in the (now idle) pipeline smem -> coalesced row stores (lane = column)
+    mbar_wait(&done_bar, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    // warp w may read TMEM lanes 32 (w % 4) ..; the G2CW / 4 warps of a quarter take turns on
+    // its 32-column chunks
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    float *T = reinterpret_cast<float *>(sm) + (warp - 2) * 32 * 33;
+#pragma unroll 1
+    for (int c0 = 32 * half; c0 < BN; c0 += 32 * (G2CW / 4)) {
+      if (n0 + c0 >= g.N) break;
+      uint32_t r[32];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+          "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+            "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+            "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+          : "r"(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0));
+      asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+      for (int j = 0; j < 32; ++j) T[lane * 33 + j] = __uint_as_float(r[j]);
+      __syncwarp();
+      const int n = n0 + c0 + lane;
+      if (n < g.N) {
+        const float bn = g.bias ? g.bias[n] : 0.f;
+        const int rlim = min(32, g.M - (m0 + q * 32));
+#pragma unroll 4
+        for (int i = 0; i < rlim; ++i) {
+          const int row = m0 + q * 32 + i;
+          float v = T[i * 33 + lane];
+          if (g.P) {   // split-K: raw partial sums, combined by gemm_reduce_kernel
+            g.P[((int64_t)blockIdx.z * g.M + row) * g.N + n] = v;
+          } else {
+            float *c = g.C + (int64_t)row * g.ldc + n;
+            v += bn;
+            if (g.relu) v = fmaxf(v, 0.f);
+            if (g.beta != 0.f) v += g.beta * *c;
+            *c = v;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN));
+}
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+// fp32 operand with `rows` GEMM rows (M or N) and K columns, stored with leading dimension ld:
+//   K-major  [rows][ld]: dims {K, rows}, box {16, box_rows}, SWIZZLE_64B
+//   MN-major [K][ld]:    dims {rows, K}, box {32, 16},       no swizzle (one box per 32 rows)
+bool make_tmap(CUtensorMap *tm, const float *base, int rows, int K, int ld, int box_rows, bool mn) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)(mn ? rows : K), (cuuint64_t)(mn ? K : rows)};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  const cuuint32_t box[2] = {mn ? 32u : (cuuint32_t)G2K, mn ? (cuuint32_t)G2K : (cuuint32_t)box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, mn ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_64B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN, bool AMN, bool BMN>
+bool launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t st) {
+  using Cfg = G2Cfg<BN, AMN, BMN>;
+  CUtensorMap ta, tb;
+  if (!make_tmap(&ta, g0.A, g0.M, g0.K, g0.lda, GBM, AMN) || !make_tmap(&tb, g0.B, g0.N, g0.K, g0.ldb, BN, BMN))
+    return false;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GSMEM);
+    cudaFuncSetAttribute(gemm_tf32x3_tma_kernel<BN, AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg::kSmem);
     configured = true;
   }
   GemmArgs g = g0;
-  const int tiles = ((g.N + GBN - 1) / GBN) * ((g.M + GBM - 1) / GBM);
-  const int nkb = (g.K + GBK - 1) / GBK;
-  int splits = std::max(1, std::min(148 / std::max(tiles, 1), nkb / 4));
+  const int tiles = ((g.N + BN - 1) / BN) * ((g.M + GBM - 1) / GBM);
+  const int nkb = (g.K + G2K - 1) / G2K;
+  int splits = std::max(1, std::min(148 / std::max(tiles, 1), nkb / 8));
   while (splits > 1 && (!part || (int64_t)splits * g.M * g.N > part_cap)) --splits;
   g.kbs = (nkb + splits - 1) / splits;
   splits = (nkb + g.kbs - 1) / g.kbs;
   g.P = splits > 1 ? part : nullptr;
-  dim3 grid((g.N + GBN - 1) / GBN, (g.M + GBM - 1) / GBM, splits);
-  { gemm_tf32x3_kernel<<<grid, GTHREADS, GSMEM, st>>>(g); ++g_launches; }
+  dim3 grid((g.N + BN - 1) / BN, (g.M + GBM - 1) / GBM, splits);
+  { gemm_tf32x3_tma_kernel<BN, AMN, BMN><<<grid, G2T, Cfg::kSmem, st>>>(ta, tb, g); ++g_launches; }
   if (splits > 1) {
     const int64_t n = (int64_t)g.M * g.N;
     { gemm_reduce_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(part, splits, g.M, g.N, g.C, g.ldc, g.bias, g.relu,
                                                                 g.beta); ++g_launches; }
   }
+  return true;
+}
+template <int BN>
+bool launch_v2_any(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st) {
+  if (g.a_mn) return g.b_mn ? launch_v2<BN, true, true>(g, part, part_cap, st)
+                            : launch_v2<BN, true, false>(g, part, part_cap, st);
+  return g.b_mn ? launch_v2<BN, false, true>(g, part, part_cap, st) : launch_v2<BN, false, false>(g, part, part_cap, st);
+}
+}  // namespace
+
+bool gemm_tc_accepts(const GemmArgs &g) {
+  return g.M > 0 && g.N > 0 && g.K > 0 && !(reinterpret_cast<uintptr_t>(g.A) & 15) &&
+         !(reinterpret_cast<uintptr_t>(g.B) & 15) && !(g.lda & 3) && !(g.ldb & 3) && tmap_encoder() != nullptr;
+}
+
+// C = beta C + op(A) op(B)^T (+ bias) (ReLU) on the tensor cores.  A is [M][K] (a_mn: [K][M]),
+// B is [N][K] (b_mn: [K][N]), 16-byte aligned with ld % 4 == 0 (gemm_tc_accepts).  When the
+// output has fewer tiles than SMs, K is split over blockIdx.z (at most one wave of CTAs: 192 KB
+// of shared memory per CTA) into `part` (capacity part_cap floats).
+bool launch_gemm_tc(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st) {
+  if (!gemm_tc_accepts(g)) return false;
+  const int64_t t256 = (int64_t)((g.N + 255) / 256) * ((g.M + GBM - 1) / GBM);
+  const bool wide = g.N > 128 && t256 >= 100;   // enough 128 x 256 tiles to fill the GPU
+  return wide ? launch_v2_any<256>(g, part, part_cap, st) : launch_v2_any<128>(g, part, part_cap, st);
 }
 
 }  // namespace kg

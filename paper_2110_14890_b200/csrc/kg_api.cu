@@ -198,7 +198,7 @@ struct kg_handle {
   float *pX = nullptr, *pH1 = nullptr, *pH2 = nullptr, *pZp1 = nullptr, *pdZ = nullptr, *pdH2 = nullptr,
         *pdH1 = nullptr, *pZ = nullptr, *pdX = nullptr;
   float *Dscore = nullptr;
-  float *gsA = nullptr, *gsB = nullptr, *gsP = nullptr;   // GEMM transpose / split-K scratch
+  float *gsP = nullptr;   // GEMM split-K scratch
   int64_t gsP_cap = 0;
   float *Dpart = nullptr, *partQ = nullptr, *partV = nullptr, *Cpart = nullptr, *Csum = nullptr;
   int64_t cap_D = 0, cap_Q = 0, cap_V = 0;
@@ -417,8 +417,6 @@ void carve(kg_handle *h, Arena &A) {
   {
     const int64_t wide = std::max<int64_t>({(int64_t)H, 2LL * d, (int64_t)dq});
     const int64_t tall = std::max<int64_t>({4LL * Mx, (int64_t)H, 2LL * d});
-    h->gsA = A.take<float>(wide * (tall + 4));
-    h->gsB = A.take<float>(wide * (tall + 4));
     h->gsP_cap = std::min<int64_t>(16LL << 20, 8LL * 4 * Mx * wide);
     h->gsP = A.take<float>(h->gsP_cap);
   }
@@ -451,15 +449,11 @@ kg_status gemm(kg_handle *h, bool ta, bool tb, int m, int n, int k, const float 
   // the tcgen05 kernel pays off for long K loops over large outputs (BetaE MLP layers and
   // their dW over the batch rows); the small d x d contractions go to cuBLAS SGEMM (fp32)
   if (!h->gemm_cublas && !h->side && ((k >= h->tc_min_k && (int64_t)m * n >= (1 << 18)) || h->gemm_tc_all)) {
-    // operands the tensor-core kernel reads K-major: transpose [k][m] / [k][n] storage first
+    // the tensor-core kernel reads either operand layout directly ([k][m] / [k][n] = MN-major)
     GemmArgs g;
     g.A = A; g.B = B; g.C = C; g.M = m; g.N = n; g.K = k; g.lda = lda; g.ldb = ldb; g.ldc = ldc; g.beta = beta;
-    g.bias = bias; g.relu = relu;
-    const int kp = (k + 3) & ~3;
-    if (ta) { launch_transpose(A, k, m, lda, h->gsA, kp, h->st); g.A = h->gsA; g.lda = kp; }
-    if (!tb) { launch_transpose(B, k, n, ldb, h->gsB, kp, h->st); g.B = h->gsB; g.ldb = kp; }
-    launch_gemm_tc(g, h->gsP, h->gsP_cap, h->st);
-    return KG_OK;
+    g.bias = bias; g.relu = relu; g.a_mn = ta; g.b_mn = !tb;
+    if (k > 0 && launch_gemm_tc(g, h->gsP, h->gsP_cap, h->st)) return KG_OK;
   }
   const float one = 1.f;
   h->gemm_count++;
@@ -1441,32 +1435,19 @@ const char *kg_last_error(const kg_handle *h) { return h ? h->err.c_str() : "nul
 kg_status kg_test_gemm(int32_t ta, int32_t tb, int32_t M, int32_t N, int32_t K, const float *A, int32_t lda,
                        const float *B, int32_t ldb, float *C, int32_t ldc, const float *bias, int32_t relu, float beta,
                        void *stream) {
-  if (!A || !B || !C || M < 0 || N < 0 || K < 0) return KG_EINVAL;
+  if (!A || !B || !C || M < 0 || N < 0 || K < 1) return KG_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   GemmArgs g;
   g.A = A; g.B = B; g.C = C; g.bias = bias; g.M = M; g.N = N; g.K = K; g.lda = lda; g.ldb = ldb; g.ldc = ldc;
-  g.relu = relu; g.beta = beta;
-  const int kp = (K + 3) & ~3;
-  float *sA = nullptr, *sB = nullptr;
-  if ((!ta && (lda & 3)) || (!tb && (ldb & 3))) return KG_EINVAL;   // K-major operands need ld % 4 == 0
-  if (ta) {
-    if (cudaMalloc(&sA, sizeof(float) * (size_t)std::max(M, 1) * kp) != cudaSuccess) return KG_ENOMEM;
-    launch_transpose(A, K, M, lda, sA, kp, st);
-    g.A = sA; g.lda = kp;
-  }
-  if (tb) {
-    if (cudaMalloc(&sB, sizeof(float) * (size_t)std::max(N, 1) * kp) != cudaSuccess) return KG_ENOMEM;
-    launch_transpose(B, K, N, ldb, sB, kp, st);
-    g.B = sB; g.ldb = kp;
-  }
+  g.relu = relu; g.beta = beta; g.a_mn = ta != 0; g.b_mn = tb != 0;
+  if (!gemm_tc_accepts(g)) return KG_EINVAL;   // 16-byte aligned operands with ld % 4 == 0
   float *sP = nullptr;
   const int64_t pcap = 8LL * std::max(M, 1) * std::max(N, 1);
   if (cudaMalloc(&sP, sizeof(float) * pcap) != cudaSuccess) return KG_ENOMEM;
-  launch_gemm_tc(g, sP, pcap, st);
+  const bool launched = launch_gemm_tc(g, sP, pcap, st);
   const cudaError_t e = cudaStreamSynchronize(st);
   cudaFree(sP);
-  if (sA) cudaFree(sA);
-  if (sB) cudaFree(sB);
+  if (!launched) return KG_EUNSUPPORTED;   // tensor map encoding failed
   if (e != cudaSuccess) return KG_ECUDA;
   return cudaGetLastError() == cudaSuccess ? KG_OK : KG_ECUDA;
 }

@@ -89,9 +89,12 @@ struct GemmArgs {
   int M = 0, N = 0, K = 0, lda = 0, ldb = 0, ldc = 0, relu = 0;
   float beta = 0.f;
   float *P = nullptr;   // split-K partials [splits][M][N] (set by launch_gemm_tc)
+  bool a_mn = false;    // A stored [K][M] (lda) instead of [M][K]
+  bool b_mn = false;    // B stored [K][N] (ldb) instead of [N][K]
   int kbs = 1 << 30;    // k-blocks per split
 };
-void launch_gemm_tc(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st);   // K-major, ld % 4 == 0
+bool gemm_tc_accepts(const GemmArgs &g);   // 16-byte aligned operands, ld % 4 == 0
+bool launch_gemm_tc(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st);   // false: not launched
 void launch_transpose(const float *in, int R, int Cc, int ld_in, float *out, int ld_out, cudaStream_t st);
 
 // k_dist.cu (world > 1)

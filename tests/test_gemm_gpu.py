@@ -21,9 +21,17 @@ def _run(ta, tb, M, N, K, bias=False, relu=False, beta=0.0, seed=0):
     C0 = rng.standard_normal((M, N)).astype(np.float32)
     b = rng.standard_normal(N).astype(np.float32)
     dev = torch.device("cuda")
-    tA, tB, tC, tb_ = (torch.from_numpy(x).to(dev) for x in (A, B, C0, b))
+
+    def padded(x):   # leading dimension rounded up to 4 floats; the padding is NaN and must be ignored
+        ld = (x.shape[1] + 3) // 4 * 4
+        y = np.full((x.shape[0], ld), np.nan, dtype=np.float32)
+        y[:, :x.shape[1]] = x
+        return y
+
+    Ap, Bp = padded(A), padded(B)
+    tA, tB, tC, tb_ = (torch.from_numpy(x).to(dev) for x in (Ap, Bp, C0, b))
     st = torch.cuda.current_stream()
-    s = kgb.kg_test_gemm(int(ta), int(tb), M, N, K, tA.data_ptr(), A.shape[1], tB.data_ptr(), B.shape[1],
+    s = kgb.kg_test_gemm(int(ta), int(tb), M, N, K, tA.data_ptr(), Ap.shape[1], tB.data_ptr(), Bp.shape[1],
                          tC.data_ptr(), N, tb_.data_ptr() if bias else None, int(relu), beta,
                          C.c_void_p(st.cuda_stream))
     assert s == 0
@@ -44,7 +52,8 @@ def _run(ta, tb, M, N, K, bias=False, relu=False, beta=0.0, seed=0):
 
 
 @pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
-@pytest.mark.parametrize("M,N,K", [(70, 40, 40), (128, 128, 32), (200, 136, 100), (512, 400, 800)])
+@pytest.mark.parametrize("M,N,K", [(70, 40, 40), (128, 128, 32), (200, 136, 100), (512, 400, 800),
+                                   (33, 257, 17), (1, 1, 1), (300, 600, 1500)])
 def test_gemm_layouts_and_ragged_shapes(ta, tb, M, N, K):
     _run(ta, tb, M, N, K)
 
@@ -54,3 +63,13 @@ def test_gemm_betae_shapes_and_epilogues():
     _run(False, True, 1024, 800, 1600)                            # dX = dH1 W1
     _run(True, True, 1600, 800, 1024)                             # dW1 = dH1^T X
     _run(False, False, 300, 400, 400, beta=1.0)                   # dstack += dH U1
+
+
+def test_gemm_rejects_unaligned_leading_dimension():
+    import torch
+    import paper_2110_14890_b200 as kgb
+    A = torch.zeros((8, 10), device="cuda")
+    st = torch.cuda.current_stream()
+    s = kgb.kg_test_gemm(0, 0, 8, 8, 10, A.data_ptr(), 10, A.data_ptr(), 10, A.data_ptr(), 8, None, 0, 0.0,
+                         C.c_void_p(st.cuda_stream))
+    assert s == 1   # lda % 4 != 0 -> KG_EINVAL
