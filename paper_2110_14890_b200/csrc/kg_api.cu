@@ -87,6 +87,7 @@ struct PNode {
   int nin;
 };
 struct Plan {
+  int gs[6], ge[6];   // projection group [gs, ge) of each projection node
   int na, nr, nn, nout, nproj;
   PNode n[6];
   int outs[2];
@@ -116,14 +117,23 @@ Plan make_plan(int s) {
     case KG_2I: set({P(-1, 0, 0), P(-1, 1, 1), I2(0, 1)}, {2}, 2, 2); break;
     case KG_3I: set({P(-1, 0, 0), P(-1, 1, 1), P(-1, 2, 2), I3(0, 1, 2)}, {3}, 3, 3); break;
     case KG_IP: set({P(-1, 0, 0), P(-1, 1, 1), I2(0, 1), P(2, -1, 2)}, {3}, 2, 3); break;
-    case KG_PI: set({P(-1, 0, 0), P(0, -1, 1), P(-1, 1, 2), I2(1, 2)}, {3}, 2, 3); break;
+    // projections of the same depth are consecutive nodes (one batched MLP for BetaE)
+    case KG_PI: set({P(-1, 0, 0), P(-1, 1, 2), P(0, -1, 1), I2(2, 1)}, {3}, 2, 3); break;
     case KG_2U: set({P(-1, 0, 0), P(-1, 1, 1)}, {0, 1}, 2, 2); break;
-    case KG_UP: set({P(-1, 0, 0), P(0, -1, 2), P(-1, 1, 1), P(2, -1, 2)}, {1, 3}, 2, 3); break;
+    case KG_UP: set({P(-1, 0, 0), P(-1, 1, 1), P(0, -1, 2), P(1, -1, 2)}, {2, 3}, 2, 3); break;
     case KG_2IN: set({P(-1, 0, 0), P(-1, 1, 1), Ng(1), I2(0, 2)}, {3}, 2, 2); break;
     case KG_3IN: set({P(-1, 0, 0), P(-1, 1, 1), P(-1, 2, 2), Ng(2), I3(0, 1, 3)}, {4}, 3, 3); break;
     case KG_INP: set({P(-1, 0, 0), P(-1, 1, 1), Ng(1), I2(0, 2), P(3, -1, 2)}, {4}, 2, 3); break;
-    case KG_PIN: set({P(-1, 0, 0), P(0, -1, 1), P(-1, 1, 2), Ng(2), I2(1, 3)}, {4}, 2, 3); break;
-    case KG_PNI: set({P(-1, 0, 0), P(0, -1, 1), Ng(1), P(-1, 1, 2), I2(2, 3)}, {4}, 2, 3); break;
+    case KG_PIN: set({P(-1, 0, 0), P(-1, 1, 2), P(0, -1, 1), Ng(1), I2(2, 3)}, {4}, 2, 3); break;
+    case KG_PNI: set({P(-1, 0, 0), P(-1, 1, 2), P(0, -1, 1), Ng(2), I2(3, 1)}, {4}, 2, 3); break;
+  }
+  // groups of consecutive, mutually independent projection nodes [gs, ge)
+  for (int i = 0; i < p.nn;) {
+    if (p.n[i].type != 0) { ++i; continue; }
+    int j = i + 1;
+    while (j < p.nn && p.n[j].type == 0 && p.n[j].in < i) ++j;
+    for (int k = i; k < j; ++k) { p.gs[k] = i; p.ge[k] = j; }
+    i = j;
   }
   p.nproj = 0;
   for (int i = 0; i < p.nn; ++i) {
@@ -198,7 +208,7 @@ struct kg_handle {
   float *pX = nullptr, *pH1 = nullptr, *pH2 = nullptr, *pZp1 = nullptr, *pdZ = nullptr, *pdH2 = nullptr,
         *pdH1 = nullptr, *pZ = nullptr, *pdX = nullptr;
   float *Dscore = nullptr;
-  float *gsP = nullptr;   // GEMM split-K scratch
+  float *gsP = nullptr, *gsP2 = nullptr;   // GEMM split-K scratch (main / side stream)
   int64_t gsP_cap = 0;
   float *Dpart = nullptr, *partQ = nullptr, *partV = nullptr, *Cpart = nullptr, *Csum = nullptr;
   int64_t cap_D = 0, cap_Q = 0, cap_V = 0;
@@ -213,10 +223,9 @@ struct kg_handle {
   };
   std::vector<GraphEntry> graphs;
   bool use_graphs = true;
-  bool gemm_cublas = false, gemm_tc_all = false, side = false;
+  bool gemm_cublas = false, side = false;
   cublasHandle_t blas2 = nullptr;
   void *blas_ws2 = nullptr;
-  int tc_min_k = 512;
   void *blas_ws = nullptr;
   // row-sharded exchange (world > 1, k_dist.cu)
   ncclComm_t comm = nullptr;
@@ -410,8 +419,8 @@ void carve(kg_handle *h, Arena &A) {
     h->pdZ = A.take<float>(P * d);
     h->pdH2 = A.take<float>(P * H);
     h->pdH1 = A.take<float>(P * H);
-    h->pZ = A.take<float>((int64_t)Mx * d);
-    h->pdX = A.take<float>((int64_t)Mx * 2 * d);
+    h->pZ = A.take<float>(P * d);
+    h->pdX = A.take<float>(P * 2 * d);
   }
   h->Dscore = A.take<float>((int64_t)Mx * std::max(h->Cx, 1));
   {
@@ -419,6 +428,7 @@ void carve(kg_handle *h, Arena &A) {
     const int64_t tall = std::max<int64_t>({4LL * Mx, (int64_t)H, 2LL * d});
     h->gsP_cap = std::min<int64_t>(16LL << 20, 8LL * 4 * Mx * wide);
     h->gsP = A.take<float>(h->gsP_cap);
+    h->gsP2 = A.take<float>(h->gsP_cap);
   }
   if (h->world > 1) {
     const int64_t GL = (int64_t)h->world * h->Lx;
@@ -446,14 +456,15 @@ void carve(kg_handle *h, Arena &A) {
 kg_status gemm(kg_handle *h, bool ta, bool tb, int m, int n, int k, const float *A, int lda, const float *B, int ldb,
                float beta, float *C, int ldc, const float *bias = nullptr, int relu = 0) {
   if (m <= 0 || n <= 0) return KG_OK;
-  // the tcgen05 kernel pays off for long K loops over large outputs (BetaE MLP layers and
-  // their dW over the batch rows); the small d x d contractions go to cuBLAS SGEMM (fp32)
-  if (!h->gemm_cublas && !h->side && ((k >= h->tc_min_k && (int64_t)m * n >= (1 << 18)) || h->gemm_tc_all)) {
+  // every contraction of the DAG goes to the tcgen05 kernel (measured faster than cuBLAS SGEMM
+  // from the d x d DeepSet / attention layers up to the BetaE MLP); the side stream has its
+  // own split-K scratch
+  if (!h->gemm_cublas) {
     // the tensor-core kernel reads either operand layout directly ([k][m] / [k][n] = MN-major)
     GemmArgs g;
     g.A = A; g.B = B; g.C = C; g.M = m; g.N = n; g.K = k; g.lda = lda; g.ldb = ldb; g.ldc = ldc; g.beta = beta;
     g.bias = bias; g.relu = relu; g.a_mn = ta; g.b_mn = !tb;
-    if (k > 0 && launch_gemm_tc(g, h->gsP, h->gsP_cap, h->st)) return KG_OK;
+    if (k > 0 && launch_gemm_tc(g, h->side ? h->gsP2 : h->gsP, h->gsP_cap, h->st)) return KG_OK;
   }
   const float one = 1.f;
   h->gemm_count++;
@@ -463,8 +474,8 @@ kg_status gemm(kg_handle *h, bool ta, bool tb, int m, int n, int k, const float 
   return KG_OK;
 }
 // Run the following GEMMs / kernels on another stream (restored on scope exit).
-// The side stream gets its own cuBLAS handle (own workspace) and never uses the shared
-// tensor-core GEMM scratch, so the two branches cannot race on scratch memory.
+// The side stream gets its own cuBLAS handle (own workspace) and its own tensor-core GEMM
+// split-K scratch, so the two branches cannot race on scratch memory.
 struct OnStream {
   kg_handle *h;
   cudaStream_t prev;
@@ -513,18 +524,31 @@ kg_status dag_forward(kg_handle *h, StepBufs &S) {
   int u = 0;
   for (int ni = 0; ni < p.nn; ++ni) {
     const PNode &nd = p.n[ni];
+    if (nd.type == 0 && h->kind == KG_BETAE) {
+      // one MLP over the rows of all projections of the group (same weights, A9)
+      const int nj = p.ge[ni], GM = (nj - ni) * M;
+      float *X = h->pX + (int64_t)u * M * 2 * d, *H1 = h->pH1 + (int64_t)u * M * HH, *H2 = h->pH2 + (int64_t)u * M * HH;
+      for (int k = ni; k < nj; ++k) {
+        const PNode &nk = p.n[k];
+        const int64_t *arows = nk.in < 0 ? h->rows + (int64_t)nk.anchor * M : nullptr;
+        launch_betae_proj_in(M, d, nk.in < 0 ? nullptr : S.val[nk.in], arows, ent, h->rocc + (int64_t)(u + k - ni) * M,
+                             1, dp(h, "rel"), X + (int64_t)(k - ni) * M * 2 * d, st);
+      }
+      G(false, true, GM, HH, 2 * d, X, 2 * d, dp(h, "prj_W1"), 2 * d, 0.f, H1, HH, dp(h, "prj_b1"), 1);
+      G(false, true, GM, HH, HH, H1, HH, dp(h, "prj_W2"), HH, 0.f, H2, HH, dp(h, "prj_b2"), 1);
+      G(false, true, GM, d, HH, H2, HH, dp(h, "prj_W0"), HH, 0.f, h->pZ, d);
+      for (int k = ni; k < nj; ++k)
+        launch_betae_proj_out(h->pZ + (int64_t)(k - ni) * M * d, dp(h, "prj_b0"), M, d,
+                              h->pZp1 + (int64_t)(u + k - ni) * M * d, S.val[k], st);
+      u += nj - ni;
+      ni = nj - 1;
+      continue;
+    }
     if (nd.type == 0) {
       const int64_t *arows = nd.in < 0 ? h->rows + (int64_t)nd.anchor * M : nullptr;
       const float *in = nd.in < 0 ? nullptr : S.val[nd.in];
       const int32_t *rel = h->rocc + (int64_t)u * M;
-      if (h->kind == KG_BETAE) {
-        float *X = h->pX + (int64_t)u * M * 2 * d, *H1 = h->pH1 + (int64_t)u * M * HH, *H2 = h->pH2 + (int64_t)u * M * HH;
-        launch_betae_proj_in(M, d, in, arows, ent, rel, 1, dp(h, "rel"), X, st);
-        G(false, true, M, HH, 2 * d, X, 2 * d, dp(h, "prj_W1"), 2 * d, 0.f, H1, HH, dp(h, "prj_b1"), 1);
-        G(false, true, M, HH, HH, H1, HH, dp(h, "prj_W2"), HH, 0.f, H2, HH, dp(h, "prj_b2"), 1);
-        G(false, true, M, d, HH, H2, HH, dp(h, "prj_W0"), HH, 0.f, h->pZ, d);
-        launch_betae_proj_out(h->pZ, dp(h, "prj_b0"), M, d, h->pZp1 + (int64_t)u * M * d, S.val[ni], st);
-      } else {
+      {
         const float *relA = nullptr, *relB = nullptr;
         if (h->kind == KG_Q2B) { relA = dp(h, "rel_center"); relB = dp(h, "rel_offset"); }
         else if (h->kind == KG_ROTATE) relA = dp(h, "rel_phase");
@@ -578,6 +602,28 @@ kg_status dag_backward(kg_handle *h, StepBufs &S) {
   for (int ni = 0; ni < p.nn; ++ni) use[ni] = p.n[ni].type == 0 ? u++ : -1;
   for (int ni = p.nn - 1; ni >= 0; --ni) {
     const PNode &nd = p.n[ni];
+    if (nd.type == 0 && h->kind == KG_BETAE) {
+      // the group [gs, ge) ends here: its output gradients are complete (consumers come later)
+      const int n0 = p.gs[ni], u0 = use[n0], GM = (ni + 1 - n0) * M;
+      float *dZ = h->pdZ + (int64_t)u0 * M * d, *dH2 = h->pdH2 + (int64_t)u0 * M * HH,
+            *dH1 = h->pdH1 + (int64_t)u0 * M * HH;
+      for (int k = n0; k <= ni; ++k)
+        launch_betae_proj_dz(S.grad[k], h->pZp1 + (int64_t)use[k] * M * d, M, d, h->pdZ + (int64_t)use[k] * M * d, st);
+      G(false, false, GM, HH, d, dZ, d, dp(h, "prj_W0"), HH, 0.f, dH2, HH);
+      launch_relu_mask(dH2, h->pH2 + (int64_t)u0 * M * HH, GM, HH, st);
+      G(false, false, GM, HH, HH, dH2, HH, dp(h, "prj_W2"), HH, 0.f, dH1, HH);
+      launch_relu_mask(dH1, h->pH1 + (int64_t)u0 * M * HH, GM, HH, st);
+      G(false, false, GM, 2 * d, HH, dH1, HH, dp(h, "prj_W1"), 2 * d, 0.f, h->pdX, 2 * d);
+      for (int k = n0; k <= ni; ++k) {
+        const PNode &nk = p.n[k];
+        const int64_t *arows = nk.in < 0 ? h->rows + (int64_t)nk.anchor * M : nullptr;
+        float *din = nk.in < 0 ? h->OG + (int64_t)nk.anchor * M * d : S.grad[nk.in];
+        launch_betae_split(h->pdX + (int64_t)(k - n0) * M * 2 * d, M, d, arows, ent, din, nk.in < 0 ? d : dq,
+                           h->RG + (int64_t)use[k] * M * h->dr, st);
+      }
+      ni = n0;   // the loop's --ni moves past the group
+      continue;
+    }
     if (nd.type == 0) {
       const int uu = use[ni];
       const int64_t *arows = nd.in < 0 ? h->rows + (int64_t)nd.anchor * M : nullptr;
@@ -586,17 +632,7 @@ kg_status dag_backward(kg_handle *h, StepBufs &S) {
       const int64_t din_ld = nd.in < 0 ? d : dq;
       const int32_t *rel = h->rocc + (int64_t)uu * M;
       float *drel = h->RG + (int64_t)uu * M * h->dr;
-      if (h->kind == KG_BETAE) {
-        float *dZ = h->pdZ + (int64_t)uu * M * d, *dH2 = h->pdH2 + (int64_t)uu * M * HH,
-              *dH1 = h->pdH1 + (int64_t)uu * M * HH;
-        launch_betae_proj_dz(S.grad[ni], h->pZp1 + (int64_t)uu * M * d, M, d, dZ, st);
-        G(false, false, M, HH, d, dZ, d, dp(h, "prj_W0"), HH, 0.f, dH2, HH);
-        launch_relu_mask(dH2, h->pH2 + (int64_t)uu * M * HH, M, HH, st);
-        G(false, false, M, HH, HH, dH2, HH, dp(h, "prj_W2"), HH, 0.f, dH1, HH);
-        launch_relu_mask(dH1, h->pH1 + (int64_t)uu * M * HH, M, HH, st);
-        G(false, false, M, 2 * d, HH, dH1, HH, dp(h, "prj_W1"), 2 * d, 0.f, h->pdX, 2 * d);
-        launch_betae_split(h->pdX, M, d, arows, ent, din, din_ld, drel, st);
-      } else {
+      {
         const float *relA = nullptr, *relB = nullptr;
         if (h->kind == KG_Q2B) { relA = dp(h, "rel_center"); relB = dp(h, "rel_offset"); }
         else if (h->kind == KG_ROTATE) relA = dp(h, "rel_phase");
@@ -869,10 +905,7 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
     h->use_graphs = false;   // the exchange sizes are read on the host every step
   }
   if (const char *e = std::getenv("KG_NO_GRAPH")) h->use_graphs = !(e[0] == '1');
-  if (const char *e = std::getenv("KG_GEMM")) {
-    h->gemm_cublas = std::string(e) == "cublas";
-    h->gemm_tc_all = std::string(e) == "tc";
-  }
+  if (const char *e = std::getenv("KG_GEMM")) h->gemm_cublas = std::string(e) == "cublas";   // A/B comparison
   cublasSetMathMode(h->blas, CUBLAS_PEDANTIC_MATH);   // true fp32, no TF32 (parity at 1e-5, A24)
   // device scalars
   if (cudaMemset(h->ws, 0, h->ws_bytes) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }

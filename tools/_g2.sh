@@ -1,2 +1,4 @@
-cp paper_2110_14890_b200/libkg.so variants/libkg_8.so
-for w in 4 8 12 16; do cp variants/libkg_$w.so paper_2110_14890_b200/libkg.so; timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/gemm_w$w.csv python tools/gemm_probe.py > /dev/null 2>&1; done
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+for wl in C4 C5-q2b; do
+python bench.py --workload $wl --steps 200 --warmup 10 2>&1 | tail -1 > gpurun_out/b_${wl}_def.json
+done
