@@ -15,6 +15,8 @@ structures and the single-hop TransE / RotatE / DistMult / ComplEx models:
             intersection I, DNF union, distance Dist      (Table 1 P:L137-143,
             Table 2, App. B, App. A, Def. 1
             P:L96-100; readings A1-A13, A19 in DESIGN.md)
+  eval.py   filtered ranks and MRR / Hit@k of the evaluation path (App. F
+            P:L700-705, reading A26)
   step.py   Eq. 1 loss, gradients, duplicate-row merge,
             sparse Adam on touched rows, dense Adam on theta_D
             (P:L307, L314), multi-worker semantics (reading A18),
@@ -38,7 +40,9 @@ from .model import (anchor_query, embed_entity, project, intersect, distance, ne
                     query_disjuncts, dense_views)
 from .step import (dedup, adam, SparseTable, oracle_step, oracle_score, StepResult,
                    softplus, query_loss_terms)
+from .eval import ranks_from_distances, metrics_from_ranks, oracle_eval
 
 __all__ = ["anchor_query", "embed_entity", "project", "intersect", "distance", "negate",
            "query_disjuncts", "dense_views", "dedup", "adam", "SparseTable",
-           "oracle_step", "oracle_score", "StepResult", "softplus", "query_loss_terms"]
+           "oracle_step", "oracle_score", "StepResult", "softplus", "query_loss_terms",
+           "ranks_from_distances", "metrics_from_ranks", "oracle_eval"]
