@@ -167,6 +167,20 @@ kg_status kg_sync(kg_handle *h, kg_step_info *info);
 kg_status kg_score(kg_handle *h, const kg_batch *queries, const int64_t *cand, int32_t n_cand,
                    float *out_dist);
 
+/* Evaluation path (App. F, reading A26): filtered rank of every missing
+ * answer of every query and the per-query metrics.  queries: structure, M (<= max_M),
+ * anchors, relations (host or device per on_device).  ans_off host [M+1] (ans_off[0] = 0,
+ * every query >= 1 answer), ans_ids host [ans_off[M]]: the missing answers
+ * A_q^{G_test} \ A_q^{G_valid}; negatives host [M][n_neg]: per-query negatives the caller
+ * sampled from V \ A_q^{G_test} (already filtered; "1000 negative answers ... for each
+ * query").  Rank(v) = 1 + #{j : D(q, v_j) <= D(q, v)} (ties count against v), D the model
+ * distance with the DNF min over disjuncts.  Outputs (host): ranks [ans_off[M]] and
+ * metrics [M][4] = MRR, Hit@1, Hit@3, Hit@10 of each query (mean over its answers).
+ * Needs (max answers per query + n_neg) <= 51200.  Errors: EINVAL (pointer / size / id),
+ * EUNSUPPORTED (structure not valid for the kind, world > 1).  Synchronises the stream. */
+kg_status kg_eval(kg_handle *h, const kg_batch *queries, const int64_t *ans_off, const int64_t *ans_ids,
+                  int32_t n_neg, const int64_t *negatives, int32_t *ranks, float *metrics);
+
 /* Test / checkpoint hooks.  which: 0 parameter, 1 Adam m, 2 Adam v.
  * Rows are global ids owned by this rank (world == 1: any id); out/in host [n][dim]. */
 kg_status kg_read_rows(kg_handle *h, int32_t which, const int64_t *ids, int32_t n, float *out);

@@ -1285,30 +1285,24 @@ kg_status kg_sync(kg_handle *h, kg_step_info *info) {
   return read_result(h, info);
 }
 
-kg_status kg_score(kg_handle *h, const kg_batch *q, const int64_t *cand, int32_t n_cand, float *out_dist) {
-  kg_status s = check_state(h);
-  if (s) return s;
-  if (!q || !cand || !out_dist) return fail(h, KG_EINVAL, "null argument");
+// Validate a query batch for kg_score / kg_eval and compute its embeddings into h->Q
+// (ingest, relation occurrences, DAG forward); n_cand candidate ids (device, in b_negs)
+// get their rows in h->rows after the anchors.
+static kg_status embed_queries(kg_handle *h, const kg_batch *q, StepBufs &S, int n_cand) {
   if (q->structure < KG_1P || q->structure > KG_PNI) return fail(h, KG_EINVAL, "bad structure");
   if (single_hop(h->kind) && q->structure != KG_1P) return fail(h, KG_EUNSUPPORTED, "single-hop models accept only 1p");
   if (q->structure >= KG_2IN && h->kind != KG_BETAE)
     return fail(h, KG_EUNSUPPORTED, "negation structures need BetaE (Table 1 'Negation' column)");
-  if (n_cand < 1 || n_cand > h->Cx) return fail(h, KG_EINVAL, "n_cand out of range [1, max_cand]");
-  for (int c = 0; c < n_cand; ++c)
-    if (cand[c] < 0 || cand[c] >= h->n_ent) return fail(h, KG_EINVAL, "candidate id out of range");
-  StepBufs S;
+  if (h->world > 1) return fail(h, KG_EUNSUPPORTED, "kg_score / kg_eval with world > 1 are not built yet (DESIGN.md §7)");
   S.plan = make_plan(q->structure);
   kg_batch qb = *q;
-  qb.on_device = q->on_device;
-  if (h->world > 1) return fail(h, KG_EUNSUPPORTED, "kg_score with world > 1 is not built yet (DESIGN.md §7)");
+  kg_status s;
   if ((s = ingest(h, &qb, false, S.plan)) != KG_OK) return s;
   h->ent_src = h->t.ent;
   const Plan &p = S.plan;
-  const int M = q->M, d = h->d, na = p.na, nr = p.nr;
+  const int M = q->M, na = p.na, nr = p.nr;
   S.M = M; S.K = n_cand; S.Kp = n_cand; S.NQ = p.nout * M;
   cudaStream_t st = h->st;
-  // candidates share the negative slot of the workspace
-  CK(cudaMemcpyAsync(h->b_negs, cand, sizeof(int64_t) * n_cand, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(h->flags, 0, 2 * sizeof(int), st));
   launch_ids_concat(h->b_anchors, na, M, nullptr, 0, h->b_negs, n_cand, h->world, h->ids, h->rows, h->flags + 1,
                     h->n_ent, st);
@@ -1320,7 +1314,23 @@ kg_status kg_score(kg_handle *h, const kg_batch *q, const int64_t *cand, int32_t
   }
   launch_rel_occ(h->b_rels, M, nr, sl, p.nproj, h->R, h->rocc, h->flags + 1, st);
   assign_buffers(h, S);
-  if ((s = dag_forward(h, S)) != KG_OK) return s;
+  return dag_forward(h, S);
+}
+
+kg_status kg_score(kg_handle *h, const kg_batch *q, const int64_t *cand, int32_t n_cand, float *out_dist) {
+  kg_status s = check_state(h);
+  if (s) return s;
+  if (!q || !cand || !out_dist) return fail(h, KG_EINVAL, "null argument");
+  if (n_cand < 1 || n_cand > h->Cx) return fail(h, KG_EINVAL, "n_cand out of range [1, max_cand]");
+  for (int c = 0; c < n_cand; ++c)
+    if (cand[c] < 0 || cand[c] >= h->n_ent) return fail(h, KG_EINVAL, "candidate id out of range");
+  cudaStream_t st = h->st;
+  // candidates share the negative slot of the workspace
+  CK(cudaMemcpyAsync(h->b_negs, cand, sizeof(int64_t) * n_cand, cudaMemcpyHostToDevice, st));
+  StepBufs S;
+  if ((s = embed_queries(h, q, S, n_cand)) != KG_OK) return s;
+  const Plan &p = S.plan;
+  const int M = q->M, d = h->d, na = p.na;
   const int U = (h->kind == KG_BETAE || h->kind == KG_ROTATE || h->kind == KG_COMPLEX) ? h->m : d;
   const int64_t *cand_rows = h->rows + (int64_t)na * M;
   if (h->kind == KG_BETAE) {
@@ -1336,6 +1346,59 @@ kg_status kg_score(kg_handle *h, const kg_batch *q, const int64_t *cand, int32_t
   launch_pair_fwd(h->kind, sa, p.nout, false, st);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out_dist, h->Dscore, sizeof(float) * (size_t)M * n_cand, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return KG_OK;
+}
+
+kg_status kg_eval(kg_handle *h, const kg_batch *q, const int64_t *ans_off, const int64_t *ans_ids, int32_t n_neg,
+                  const int64_t *negatives, int32_t *ranks, float *metrics) {
+  kg_status s = check_state(h);
+  if (s) return s;
+  if (!q || !ans_off || !ans_ids || !ranks || !metrics || n_neg < 0 || (n_neg > 0 && !negatives))
+    return fail(h, KG_EINVAL, "null argument");
+  const int M = q->M;
+  if (M < 1 || M > h->Mx) return fail(h, KG_EINVAL, "M out of range [1, max_M]");
+  if (ans_off[0] != 0) return fail(h, KG_EINVAL, "ans_off[0] must be 0");
+  int64_t max_ans = 0;
+  for (int i = 0; i < M; ++i) {
+    const int64_t n = ans_off[i + 1] - ans_off[i];
+    if (n < 1) return fail(h, KG_EINVAL, "every query needs at least one missing answer");
+    max_ans = std::max(max_ans, n);
+  }
+  const int64_t n_ans = ans_off[M];
+  if ((max_ans + n_neg) * 4 > 200 * 1024) return fail(h, KG_EINVAL, "answers + negatives per query exceed 51200");
+  for (int64_t k = 0; k < n_ans; ++k)
+    if (ans_ids[k] < 0 || ans_ids[k] >= h->n_ent) return fail(h, KG_EINVAL, "answer id out of range");
+  for (int64_t k = 0; k < (int64_t)M * n_neg; ++k)
+    if (negatives[k] < 0 || negatives[k] >= h->n_ent) return fail(h, KG_EINVAL, "negative id out of range");
+  StepBufs S;
+  if ((s = embed_queries(h, q, S, 0)) != KG_OK) return s;
+  cudaStream_t st = h->st;
+  // per-call buffers (the evaluation path is not part of the captured training step)
+  int64_t *d_off = nullptr, *d_ans = nullptr, *d_neg = nullptr;
+  int32_t *d_ranks = nullptr;
+  float *d_met = nullptr;
+  CK(cudaMallocAsync(&d_off, sizeof(int64_t) * (M + 1), st));
+  CK(cudaMallocAsync(&d_ans, sizeof(int64_t) * n_ans, st));
+  CK(cudaMallocAsync(&d_neg, sizeof(int64_t) * std::max<int64_t>(1, (int64_t)M * n_neg), st));
+  CK(cudaMallocAsync(&d_ranks, sizeof(int32_t) * n_ans, st));
+  CK(cudaMallocAsync(&d_met, sizeof(float) * 4 * M, st));
+  CK(cudaMemcpyAsync(d_off, ans_off, sizeof(int64_t) * (M + 1), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_ans, ans_ids, sizeof(int64_t) * n_ans, cudaMemcpyHostToDevice, st));
+  if (n_neg > 0) CK(cudaMemcpyAsync(d_neg, negatives, sizeof(int64_t) * M * n_neg, cudaMemcpyHostToDevice, st));
+  EvalArgs a;
+  a.Q = h->Q; a.ent = h->ent_src; a.ans_off = d_off; a.ans_ids = d_ans; a.negatives = d_neg;
+  a.M = M; a.d = h->d; a.U = (h->kind == KG_BETAE || h->kind == KG_ROTATE || h->kind == KG_COMPLEX) ? h->m : h->d;
+  a.n_neg = n_neg; a.max_ans = (int)max_ans; a.alpha = h->cfg.box_alpha; a.ranks = d_ranks; a.metrics = d_met;
+  launch_eval(h->kind, a, S.plan.nout, st);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(ranks, d_ranks, sizeof(int32_t) * n_ans, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(metrics, d_met, sizeof(float) * 4 * M, cudaMemcpyDeviceToHost, st));
+  CK(cudaFreeAsync(d_off, st));
+  CK(cudaFreeAsync(d_ans, st));
+  CK(cudaFreeAsync(d_neg, st));
+  CK(cudaFreeAsync(d_ranks, st));
+  CK(cudaFreeAsync(d_met, st));
   CK(cudaStreamSynchronize(st));
   return KG_OK;
 }

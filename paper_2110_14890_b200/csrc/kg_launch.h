@@ -97,6 +97,18 @@ bool gemm_tc_accepts(const GemmArgs &g);   // 16-byte aligned operands, ld % 4 =
 bool launch_gemm_tc(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st);   // false: not launched
 void launch_transpose(const float *in, int R, int Cc, int ld_in, float *out, int ld_out, cudaStream_t st);
 
+// k_eval.cu (evaluation path, App. F)
+struct EvalArgs {
+  const float *Q = nullptr;       // query embeddings [nout][M][qstride]
+  const float *ent = nullptr;     // raw entity rows [n][d]
+  const int64_t *ans_off = nullptr, *ans_ids = nullptr, *negatives = nullptr;
+  int M = 0, d = 0, U = 0, n_neg = 0, max_ans = 0;
+  float alpha = 0.f;
+  int32_t *ranks = nullptr;
+  float *metrics = nullptr;       // [M][4]
+};
+void launch_eval(int kind, const EvalArgs &a, int nout, cudaStream_t st);
+
 // k_dist.cu (world > 1)
 void launch_owner_partition(const int64_t *uniq, const int32_t *U_dev, int G, int64_t *send_ids, int32_t *send_pos,
                             int32_t *counts, cudaStream_t st);

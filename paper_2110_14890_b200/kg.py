@@ -61,6 +61,8 @@ _sig = {
     "kg_step": (C.c_int, [_H, C.POINTER(kg_batch), C.c_float, C.POINTER(kg_step_info)]),
     "kg_sync": (C.c_int, [_H, C.POINTER(kg_step_info)]),
     "kg_score": (C.c_int, [_H, C.POINTER(kg_batch), C.c_void_p, C.c_int32, C.c_void_p]),
+    "kg_eval": (C.c_int, [_H, C.POINTER(kg_batch), C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                          C.c_void_p]),
     "kg_read_rows": (C.c_int, [_H, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
     "kg_write_rows": (C.c_int, [_H, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
     "kg_read_dense": (C.c_int, [_H, C.c_int32, C.c_void_p]),
@@ -200,6 +202,20 @@ class KGModel:
         out = np.empty((int(b["M"]), len(cand)), np.float32)
         check(kg_score(self.h, C.byref(bs), cand.ctypes.data, len(cand), out.ctypes.data), self.h)
         return out
+
+    def eval(self, b, ans_off, ans_ids, negatives):
+        """kg_eval: (ranks [n_ans] int32, metrics [M][4] = MRR, Hit@1, Hit@3, Hit@10)."""
+        ans_off = np.ascontiguousarray(ans_off, np.int64)
+        ans_ids = np.ascontiguousarray(ans_ids, np.int64)
+        negatives = np.ascontiguousarray(negatives, np.int64)
+        M = int(b["M"])
+        n_neg = negatives.shape[1] if negatives.ndim == 2 else 0
+        bs = self.batch_struct(dict(b, K=0, answers=None, negatives=None, mask=None))
+        ranks = np.empty(int(ans_off[-1]), np.int32)
+        metrics = np.empty((M, 4), np.float32)
+        check(kg_eval(self.h, C.byref(bs), ans_off.ctypes.data, ans_ids.ctypes.data, n_neg,
+                      negatives.ctypes.data if n_neg else None, ranks.ctypes.data, metrics.ctypes.data), self.h)
+        return ranks, metrics
 
     def read_rows(self, ids, which=0):
         ids = np.ascontiguousarray(ids, np.int64)
