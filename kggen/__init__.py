@@ -30,9 +30,11 @@ import numpy as np
 # --------------------------------------------------------------------------
 # Model kinds and structures (ids match include/kg.h)
 # --------------------------------------------------------------------------
-MODELS = ["gqe", "q2b", "betae", "transe", "rotate", "distmult", "complex"]
+MODELS = ["gqe", "q2b", "betae", "transe", "rotate", "distmult", "complex",
+          "rotate-m", "distmult-m", "complex-m"]     # App. B P:L629-638 multi-hop extensions (f4)
 MODEL_ID = {m: i for i, m in enumerate(MODELS)}
 SINGLE_HOP = {"transe", "rotate", "distmult", "complex"}
+M_VARIANTS = {"rotate-m": "rotate", "distmult-m": "distmult", "complex-m": "complex"}
 
 STRUCTURES = ["1p", "2p", "3p", "2i", "3i", "ip", "pi", "2u", "up"]
 # the 5 structures with negation (Table 10; BetaE only, Table 1 'Negation' column)
@@ -47,7 +49,8 @@ N_RELS = {"1p": 1, "2p": 2, "3p": 3, "2i": 2, "3i": 3, "ip": 3, "pi": 3, "2u": 2
 
 # Default margins (reading A14; the paper states no value).
 DEFAULT_GAMMA = {"gqe": 24.0, "q2b": 24.0, "betae": 60.0, "transe": 24.0,
-                 "rotate": 24.0, "distmult": 24.0, "complex": 24.0}
+                 "rotate": 24.0, "distmult": 24.0, "complex": 24.0,
+                 "rotate-m": 24.0, "distmult-m": 24.0, "complex-m": 24.0}
 
 
 @dataclass
@@ -88,7 +91,7 @@ def dense_layout(cfg: ModelConfig):
     m = d // 2
     rho = cfg.rho
     w = 1.0 / math.sqrt(d)
-    k = cfg.kind
+    k = M_VARIANTS.get(cfg.kind, cfg.kind)   # an -m variant keeps its base model's relation table
     segs = []
     if k in ("gqe", "transe", "distmult", "complex"):
         segs.append(("rel", (R, d), -rho, rho))
@@ -101,7 +104,7 @@ def dense_layout(cfg: ModelConfig):
         segs.append(("rel_phase", (R, m), -math.pi, math.pi))
     else:
         raise ValueError(k)
-    if k == "gqe":        # DeepSet intersection (A4)
+    if k == "gqe" or cfg.kind in M_VARIANTS:   # DeepSet intersection (A4; GQE, and the -m variants P:L632)
         segs += [("ds_W1", (d, d), -w, w), ("ds_b1", (d,), -w, w),
                  ("ds_W2", (d, d), -w, w), ("ds_b2", (d,), -w, w)]
     elif k == "q2b":      # center attention (A5) + offset DeepSet (A4)

@@ -40,6 +40,23 @@ def _halves(x):
     return x[..., :m], x[..., m:]
 
 
+def _base(kind: str) -> str:
+    """The -m multi-hop variants (App. B) project and score like their base model."""
+    return kggen.M_VARIANTS.get(kind, kind)
+
+
+def normalize(kind: str, q: torch.Tensor) -> torch.Tensor:
+    """App. B: DistMult-m q / ||q||_2; ComplEx-m Re and Im parts each to the unit
+    sphere; identity for every other kind (RotatE-m is not normalised, reading A27)."""
+    if kind == "distmult-m":
+        return q / torch.linalg.vector_norm(q, dim=-1, keepdim=True)
+    if kind == "complex-m":
+        re, im = _halves(q)
+        return torch.cat([re / torch.linalg.vector_norm(re, dim=-1, keepdim=True),
+                          im / torch.linalg.vector_norm(im, dim=-1, keepdim=True)], dim=-1)
+    return q
+
+
 # ---------------------------------------------------------------- embeddings
 def embed_entity(kind: str, x: torch.Tensor) -> torch.Tensor:
     """Entity embedding Em(v) from a raw row (Table 1/2 'Embedding Space')."""
@@ -63,6 +80,8 @@ def project(kind: str, q: torch.Tensor, r: torch.Tensor, P: dict) -> torch.Tenso
 
     q: [M, dq] query embeddings, r: int64 [M] relation ids.
     """
+    if kind in kggen.M_VARIANTS:   # base projection, then the -m normalisation (P:L632-638)
+        return normalize(kind, project(_base(kind), q, r, P))
     if kind in ("gqe", "transe"):
         return q + P["rel"][r]                                  # Em(q) + Em(r)
     if kind == "q2b":
@@ -95,6 +114,10 @@ def project(kind: str, q: torch.Tensor, r: torch.Tensor, P: dict) -> torch.Tenso
 def intersect(kind: str, qs: list, P: dict) -> torch.Tensor:
     """Intersection I({q_i}) (Table 1 'Intersection'; A4, A5)."""
     X = torch.stack(qs, dim=0)                                  # [n, M, dq]
+    if kind in kggen.M_VARIANTS:
+        # GQE's DeepSet on the d-float rows ([re | im] for the complex ones), P:L632, L636
+        h = torch.relu(_linear(X, P["ds_W1"], P["ds_b1"])).mean(dim=0)
+        return normalize(kind, _linear(h, P["ds_W2"], P["ds_b2"]))
     if kind == "gqe":
         # A4 DeepSet: W2 * mean_i ReLU(W1 q_i + b1) + b2
         h = torch.relu(_linear(X, P["ds_W1"], P["ds_b1"])).mean(dim=0)
@@ -135,6 +158,7 @@ def beta_kl(a1, b1, a2, b2):
 def distance(kind: str, q: torch.Tensor, v: torch.Tensor, box_alpha: float = 0.02) -> torch.Tensor:
     """Dist(q, Em(v)) for query embeddings q [..., dq] and RAW entity rows v [..., d]
     (broadcasting over leading dims).  Lower = closer (A13 for the semantic-matching kinds)."""
+    kind = _base(kind)
     if kind in ("gqe", "transe"):
         # App. B P:L624 ||q - v||_2 ; Table 2 ||h + r - t|| (A2: L2)
         return torch.linalg.vector_norm(q - v, dim=-1)

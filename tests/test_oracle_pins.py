@@ -344,9 +344,68 @@ def test_untouched_rows_unchanged_and_zero_grad_rows_decay():
     np.testing.assert_array_equal(p, kggen.init_entity_rows(cfg, 4, untouched))
 
 
+# ---------------------------------------- -m multi-hop variants (App. B, f4)
+def test_m_variants_against_numpy_complex():
+    """RotatE-m: h o e^{i theta} (no normalisation); DistMult-m: (h o r) / ||h o r||;
+    ComplEx-m: h o r with Re and Im parts each normalised; distances of the base models."""
+    rng = np.random.default_rng(3)
+    m = 5
+    h = rng.normal(size=m) + 1j * rng.normal(size=m)
+    t = rng.normal(size=m) + 1j * rng.normal(size=m)
+    r1, r2 = (rng.normal(size=m) + 1j * rng.normal(size=m) for _ in range(2))
+    th1, th2 = (rng.uniform(-np.pi, np.pi, size=m) for _ in range(2))
+    cat = lambda z: np.r_[z.real, z.imag]
+    T = lambda x: torch.tensor(np.asarray(x)[None], dtype=F64)
+    unit_parts = lambda z: z.real / np.linalg.norm(z.real) + 1j * z.imag / np.linalg.norm(z.imag)
+    # 2p of each variant, written with numpy complex arithmetic
+    P = {"rel_phase": torch.tensor(np.stack([th1, th2]), dtype=F64)}
+    q = oracle.query_disjuncts("2p", "rotate-m", [T(cat(h))], [torch.tensor([0]), torch.tensor([1])], P)[0]
+    assert float(oracle.distance("rotate-m", q[0], torch.tensor(cat(t)))) == pytest.approx(
+        np.abs(h * np.exp(1j * th1) * np.exp(1j * th2) - t).sum(), rel=1e-12)
+    P = {"rel": torch.tensor(np.stack([cat(r1), cat(r2)]), dtype=F64)}
+    q = oracle.query_disjuncts("2p", "complex-m", [T(cat(h))], [torch.tensor([0]), torch.tensor([1])], P)[0]
+    z = unit_parts(unit_parts(h * r1) * r2)
+    assert float(oracle.distance("complex-m", q[0], torch.tensor(cat(t)))) == pytest.approx(
+        -(z * np.conj(t)).real.sum(), rel=1e-12)
+    hr, a, b, tr = h.real, r1.real, r2.real, t.real
+    P = {"rel": torch.tensor(np.stack([a, b]), dtype=F64)}
+    q = oracle.query_disjuncts("2p", "distmult-m", [T(hr)], [torch.tensor([0]), torch.tensor([1])], P)[0]
+    y = hr * a / np.linalg.norm(hr * a)
+    y = y * b / np.linalg.norm(y * b)
+    assert float(oracle.distance("distmult-m", q[0], torch.tensor(tr))) == pytest.approx(-(y * tr).sum(), rel=1e-12)
+
+
+@pytest.mark.parametrize("kind", ["distmult-m", "complex-m", "rotate-m"])
+def test_m_variants_unit_norm_and_deepset(kind):
+    """Every projection / intersection output of DistMult-m is a unit vector, of ComplEx-m
+    has unit Re and Im parts; the intersection is GQE's DeepSet followed
+    by that normalisation, checked against numpy."""
+    cfg = kggen.ModelConfig(kind, 8, 40, 5)
+    tab = oracle.SparseTable(cfg, 2)
+    P = dense_views(cfg, torch.tensor(tab.dense, dtype=F64))
+    rng = np.random.default_rng(4)
+    X = [torch.tensor(rng.normal(size=(3, 8))) for _ in range(2)]
+    out = oracle.intersect(kind, X, P).numpy()
+    W1, b1, W2, b2 = (P[k].numpy() for k in ("ds_W1", "ds_b1", "ds_W2", "ds_b2"))
+    ref = np.mean([np.maximum(x.numpy() @ W1.T + b1, 0) for x in X], axis=0) @ W2.T + b2
+    if kind == "distmult-m":
+        ref = ref / np.linalg.norm(ref, axis=1, keepdims=True)
+    elif kind == "complex-m":
+        ref = np.concatenate([ref[:, :4] / np.linalg.norm(ref[:, :4], axis=1, keepdims=True),
+                              ref[:, 4:] / np.linalg.norm(ref[:, 4:], axis=1, keepdims=True)], axis=1)
+    np.testing.assert_allclose(out, ref, rtol=1e-12)
+    q = oracle.project(kind, X[0], torch.tensor([0, 1, 2]), P).numpy()
+    if kind == "distmult-m":
+        np.testing.assert_allclose(np.linalg.norm(q, axis=1), 1.0, rtol=1e-12)
+    elif kind == "complex-m":
+        np.testing.assert_allclose(np.linalg.norm(q[:, :4], axis=1), 1.0, rtol=1e-12)
+        np.testing.assert_allclose(np.linalg.norm(q[:, 4:], axis=1), 1.0, rtol=1e-12)
+
+
 # ------------------------------------------------------- P9 finite differences
 CASES = [(k, s) for k in ("gqe", "q2b", "betae") for s in kggen.STRUCTURES] + \
-        [(k, "1p") for k in ("transe", "rotate", "distmult", "complex")]
+        [(k, "1p") for k in ("transe", "rotate", "distmult", "complex")] + \
+        [(k, s) for k in ("rotate-m", "distmult-m", "complex-m") for s in kggen.STRUCTURES]
 
 
 @pytest.mark.parametrize("kind,structure", CASES)
