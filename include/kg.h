@@ -51,7 +51,11 @@ typedef enum {
 /* Models of Table 1 and Table 2. */
 typedef enum {
   KG_GQE = 0, KG_Q2B = 1, KG_BETAE = 2,                  /* multi-hop, all 9 structures */
-  KG_TRANSE = 3, KG_ROTATE = 4, KG_DISTMULT = 5, KG_COMPLEX = 6  /* single-hop: 1p only */
+  KG_TRANSE = 3, KG_ROTATE = 4, KG_DISTMULT = 5, KG_COMPLEX = 6,  /* single-hop: 1p only */
+  /* multi-hop extensions (App. B; reading A27), all 9 structures: projection and
+   * distance of the base model, GQE's DeepSet intersection; DistMult-m / ComplEx-m normalise
+   * the query (whole / Re and Im parts) after every projection and intersection */
+  KG_ROTATE_M = 7, KG_DISTMULT_M = 8, KG_COMPLEX_M = 9
 } kg_model_kind;
 
 /* Query structures, DNF for unions. */

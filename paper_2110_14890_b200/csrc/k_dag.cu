@@ -200,6 +200,44 @@ void launch_betae_split(const float *dX, int N, int d, const int64_t *anchor_row
   { betae_split_kernel<<<blocks((int64_t)N * d), 256, 0, st>>>(dX, N, d, anchor_rows, ent, din, din_ld, drel); ++g_launches; }
 }
 
+// ------------------------------------------------------------ -m query normalisation (A27)
+// App. B: DistMult-m q <- q / ||q||_2 (parts = 1); ComplEx-m Re and Im halves each to the
+// unit sphere (parts = 2).  One warp per (row, part), in place; the norms are kept for the
+// adjoint g <- (g - y (y . g)) / ||x|| (y the normalised value).
+__global__ void qnorm_fwd_kernel(float *X, int M, int d, int parts, float *nrm) {
+  const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (w >= M * parts) return;
+  const int L = d / parts;
+  float *x = X + (int64_t)(w / parts) * d + (w % parts) * L;
+  float s = 0.f;
+  for (int k = lane; k < L; k += 32) s = fmaf(x[k], x[k], s);
+  const float n = sqrtf(warp_sum(s));
+  const float inv = 1.f / n;
+  for (int k = lane; k < L; k += 32) x[k] *= inv;
+  if (lane == 0) nrm[2 * (w / parts) + (w % parts)] = n;
+}
+__global__ void qnorm_bwd_kernel(float *G, const float *Y, int M, int d, int parts, const float *nrm) {
+  const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (w >= M * parts) return;
+  const int L = d / parts;
+  const int64_t o = (int64_t)(w / parts) * d + (w % parts) * L;
+  float *g = G + o;
+  const float *y = Y + o;
+  float s = 0.f;
+  for (int k = lane; k < L; k += 32) s = fmaf(y[k], g[k], s);
+  s = warp_sum(s);
+  const float inv = 1.f / nrm[2 * (w / parts) + (w % parts)];
+  for (int k = lane; k < L; k += 32) g[k] = (g[k] - y[k] * s) * inv;
+}
+void launch_qnorm_fwd(float *X, int M, int d, int parts, float *nrm, cudaStream_t st) {
+  const int64_t threads = (int64_t)M * parts * 32;
+  { qnorm_fwd_kernel<<<blocks(threads), 256, 0, st>>>(X, M, d, parts, nrm); ++g_launches; }
+}
+void launch_qnorm_bwd(float *G, const float *Y, int M, int d, int parts, const float *nrm, cudaStream_t st) {
+  const int64_t threads = (int64_t)M * parts * 32;
+  { qnorm_bwd_kernel<<<blocks(threads), 256, 0, st>>>(G, Y, M, d, parts, nrm); ++g_launches; }
+}
+
 // ------------------------------------------------------------ negation (BetaE)
 // N(q) = 1/q elementwise on (alpha, beta) (Table 1 'Negation' P:L143); adjoint -g/q^2.
 __global__ void neg_fwd_kernel(const float *in, int64_t n, float *out) {

@@ -171,6 +171,9 @@ struct kg_handle {
   std::string err;
   bool broken = false, bound = false;
   int kind = 0, d = 0, m = 0, H = 0, R = 0, world = 1, rank = 0;
+  int sk = 0;            // projection / scoring kind: the base model of an -m variant (A27), else kind
+  int qnorm = 0;         // query normalisation after projection / intersection: 0 none, 1 L2, 2 Re and Im (A27)
+  bool deepset = false;  // GQE DeepSet intersection (GQE and the -m variants)
   int64_t n_ent = 0, shard = 0;
   int dq = 0, dr = 0, ent_bits = 1, rel_bits = 1;
   std::vector<Seg> segs;
@@ -203,6 +206,7 @@ struct kg_handle {
   float *bc = nullptr;
   float *nval[6] = {}, *ngrad[6] = {};
   float *stack_v = nullptr, *stack_g = nullptr;
+  float *qn = nullptr;   // [6 nodes][Mx][2] norms of the -m query normalisation
   float *T[12] = {};
   int8_t *amin = nullptr;
   float *pX = nullptr, *pH1 = nullptr, *pH2 = nullptr, *pZp1 = nullptr, *pdZ = nullptr, *pdH2 = nullptr,
@@ -284,6 +288,9 @@ kg_status fail(kg_handle *h, kg_status s, const std::string &msg) {
   } while (0)
 
 bool single_hop(int k) { return k == KG_TRANSE || k == KG_ROTATE || k == KG_DISTMULT || k == KG_COMPLEX; }
+int base_kind(int k) {
+  return k == KG_ROTATE_M ? KG_ROTATE : (k == KG_DISTMULT_M ? KG_DISTMULT : (k == KG_COMPLEX_M ? KG_COMPLEX : k));
+}
 int bits_for(int64_t n) {
   int b = 1;
   while (b < 31 && ((int64_t)1 << b) < n) ++b;
@@ -299,13 +306,13 @@ void build_layout(kg_handle *h) {
     Seg s{name, 0, (int64_t)rows * cols, rows, cols, (float)lo, (float)hi};
     h->segs.push_back(s);
   };
-  const int k = h->kind;
+  const int k = h->sk;   // an -m variant keeps its base model's relation table (A27)
   if (k == KG_GQE || k == KG_TRANSE || k == KG_DISTMULT || k == KG_COMPLEX) add("rel", R, d, -rho, rho);
   else if (k == KG_Q2B) { add("rel_center", R, d, -rho, rho); add("rel_offset", R, d, 0.0, rho); }
   else if (k == KG_BETAE) add("rel", R, d, -rho, rho);
   else if (k == KG_ROTATE) add("rel_phase", R, m, -M_PI, M_PI);
   const size_t nrel = h->segs.size();
-  if (k == KG_GQE) {
+  if (h->deepset) {
     add("ds_W1", d, d, -w, w); add("ds_b1", 1, d, -w, w); add("ds_W2", d, d, -w, w); add("ds_b2", 1, d, -w, w);
   } else if (k == KG_Q2B) {
     add("att_W1", d, d, -w, w); add("att_b1", 1, d, -w, w); add("att_W2", d, d, -w, w); add("att_b2", 1, d, -w, w);
@@ -404,6 +411,7 @@ void carve(kg_handle *h, Arena &A) {
     h->nval[i] = A.take<float>((int64_t)Mx * dq);
     h->ngrad[i] = A.take<float>((int64_t)Mx * dq);
   }
+  h->qn = A.take<float>((int64_t)6 * 2 * Mx);   // per-node query norms (A27)
   if (!single_hop(h->kind)) {
     h->stack_v = A.take<float>((int64_t)3 * Mx * dq);
     h->stack_g = A.take<float>((int64_t)3 * Mx * dq);
@@ -551,9 +559,10 @@ kg_status dag_forward(kg_handle *h, StepBufs &S) {
       {
         const float *relA = nullptr, *relB = nullptr;
         if (h->kind == KG_Q2B) { relA = dp(h, "rel_center"); relB = dp(h, "rel_offset"); }
-        else if (h->kind == KG_ROTATE) relA = dp(h, "rel_phase");
+        else if (h->sk == KG_ROTATE) relA = dp(h, "rel_phase");
         else relA = dp(h, "rel");
-        launch_proj_fwd(h->kind, M, d, in, dq, arows, ent, rel, 1, relA, relB, S.val[ni], st);
+        launch_proj_fwd(h->sk, M, d, in, dq, arows, ent, rel, 1, relA, relB, S.val[ni], st);
+        if (h->qnorm) launch_qnorm_fwd(S.val[ni], M, d, h->qnorm, h->qn + (int64_t)ni * 2 * h->Mx, st);   // A27
       }
       ++u;
     } else if (nd.type == 2) {
@@ -562,10 +571,11 @@ kg_status dag_forward(kg_handle *h, StepBufs &S) {
       const int n = nd.nin, NR = n * M;
       float *out = S.val[ni];
       float **T = h->T;
-      if (h->kind == KG_GQE) {
+      if (h->deepset) {
         G(false, true, NR, d, d, h->stack_v, d, dp(h, "ds_W1"), d, 0.f, T[0], d, dp(h, "ds_b1"), 1);   // H
         launch_mean_stack(T[0], n, M, d, T[1], st);                                  // Mn
         G(false, true, M, d, d, T[1], d, dp(h, "ds_W2"), d, 0.f, out, d, dp(h, "ds_b2"), 0);
+        if (h->qnorm) launch_qnorm_fwd(out, M, d, h->qnorm, h->qn + (int64_t)ni * 2 * h->Mx, st);   // A27
       } else if (h->kind == KG_Q2B) {
         // the center-attention and offset-DeepSet branches are independent: second stream
         kg_status fs = fork(h, st, h->st3);
@@ -635,9 +645,10 @@ kg_status dag_backward(kg_handle *h, StepBufs &S) {
       {
         const float *relA = nullptr, *relB = nullptr;
         if (h->kind == KG_Q2B) { relA = dp(h, "rel_center"); relB = dp(h, "rel_offset"); }
-        else if (h->kind == KG_ROTATE) relA = dp(h, "rel_phase");
+        else if (h->sk == KG_ROTATE) relA = dp(h, "rel_phase");
         else relA = dp(h, "rel");
-        launch_proj_bwd(h->kind, M, d, S.grad[ni], in, dq, arows, ent, rel, 1, relA, relB, S.val[ni], din, din_ld,
+        if (h->qnorm) launch_qnorm_bwd(S.grad[ni], S.val[ni], M, d, h->qnorm, h->qn + (int64_t)ni * 2 * h->Mx, st);
+        launch_proj_bwd(h->sk, M, d, S.grad[ni], in, dq, arows, ent, rel, 1, relA, relB, S.val[ni], din, din_ld,
                         drel, st);
       }
     } else if (nd.type == 2) {
@@ -646,8 +657,9 @@ kg_status dag_backward(kg_handle *h, StepBufs &S) {
       const int n = nd.nin, NR = n * M;
       const float *gout = S.grad[ni];
       float **T = h->T;
-      if (h->kind == KG_GQE) {
+      if (h->deepset) {
         // T0 = H, T1 = Mn (forward);  T7 = dMn, T8 = dH
+        if (h->qnorm) launch_qnorm_bwd(S.grad[ni], S.val[ni], M, d, h->qnorm, h->qn + (int64_t)ni * 2 * h->Mx, st);
         G(false, false, M, d, d, gout, d, dp(h, "ds_W2"), d, 0.f, T[7], d);
         G(true, false, d, d, M, gout, d, T[1], d, 0.f, gp(h, "ds_W2"), d);
         launch_colsum(gout, M, d, d, gp(h, "ds_b2"), st);
@@ -837,7 +849,7 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
   if (!cfg || !out) return KG_EINVAL;
   *out = nullptr;
   const kg_config &c = *cfg;
-  if (c.kind < KG_GQE || c.kind > KG_COMPLEX) return KG_EINVAL;
+  if (c.kind < KG_GQE || c.kind > KG_COMPLEX_M) return KG_EINVAL;
   if (c.dim < 8 || c.dim > 2048 || c.dim % 8) return KG_EINVAL;
   if (c.n_entities < 1 || c.n_entities >= ((int64_t)1 << 31) || c.n_relations < 1) return KG_EINVAL;
   if (c.kind == KG_BETAE && (c.hidden < 8 || c.hidden % 8)) return KG_EINVAL;
@@ -854,11 +866,14 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
   kg_handle *h = new kg_handle();
   h->cfg = c;
   h->kind = c.kind; h->d = c.dim; h->m = c.dim / 2; h->R = c.n_relations; h->n_ent = c.n_entities;
+  h->sk = base_kind(c.kind);
+  h->qnorm = c.kind == KG_DISTMULT_M ? 1 : (c.kind == KG_COMPLEX_M ? 2 : 0);
+  h->deepset = c.kind == KG_GQE || c.kind >= KG_ROTATE_M;
   h->H = c.kind == KG_BETAE ? c.hidden : 0;
   h->world = c.world; h->rank = c.rank;
   h->shard = (c.n_entities + c.world - 1) / c.world;
   h->dq = c.kind == KG_Q2B ? 2 * c.dim : c.dim;
-  h->dr = c.kind == KG_Q2B ? 2 * c.dim : (c.kind == KG_ROTATE ? c.dim / 2 : c.dim);
+  h->dr = c.kind == KG_Q2B ? 2 * c.dim : (h->sk == KG_ROTATE ? c.dim / 2 : c.dim);
   h->ent_bits = bits_for(c.n_entities);
   h->rel_bits = bits_for(c.n_relations);
   h->Mx = c.max_M; h->Kx = std::max(c.max_K, 1); h->Cx = c.max_cand;
@@ -987,7 +1002,7 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   mark(h, 2);
 
   // a8-a10: scoring, Eq. 1, scoring backward
-  const int U = (h->kind == KG_BETAE || h->kind == KG_ROTATE || h->kind == KG_COMPLEX) ? h->m : d;
+  const int U = (h->sk == KG_BETAE || h->sk == KG_ROTATE || h->sk == KG_COMPLEX) ? h->m : d;
   const int64_t *neg_rows = h->rows + (int64_t)na * M + M;
   const float scale = 1.f / (float)((double)M * h->world);
   if (h->kind == KG_BETAE) {
@@ -998,7 +1013,7 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   pa.M = M; pa.U = U; pa.d = d; pa.ent = h->ent_src; pa.ans_rows = h->rows + (int64_t)na * M; pa.Q = h->Q;
   pa.alpha = h->cfg.box_alpha; pa.gamma = h->cfg.gamma; pa.scale = scale; pa.Cq = h->Cq; pa.QP = h->QP;
   pa.loss_pos = h->loss_pos; pa.Dpos = h->Dpos; pa.dQ = h->dQ; pa.dV = h->OG + (int64_t)na * M * d;
-  launch_pos(h->kind, pa, p.nout, st);
+  launch_pos(h->sk, pa, p.nout, st);
   ScoreArgs sa;
   sa.Q = h->Q; sa.NQ = S.NQ; sa.M = M; sa.K = K; sa.Kp = S.Kp; sa.U = U; sa.d = d;
   if (h->kind == KG_BETAE) { sa.E = h->F; sa.eidx = nullptr; sa.estride = 9LL * h->m; }
@@ -1010,7 +1025,7 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   sa.cap_D = h->cap_D; sa.cap_Q = h->cap_Q; sa.cap_V = h->cap_V;
   sa.dV = h->OG + (int64_t)(na * M + M) * d;
   const int njt = K > 0 ? 1 : 0;
-  if (K > 0) launch_pair_fwd(h->kind, sa, p.nout, true, st);
+  if (K > 0) launch_pair_fwd(h->sk, sa, p.nout, true, st);
   launch_loss_finalize(h->loss_pos, h->loss_part, M, njt, 1.0 / ((double)M * h->world), h->loss_dev, h->flags,
                        h->t_dev, h->bc, h->cfg.beta1, h->cfg.beta2, h->apply, st);
   mark(h, 3);
@@ -1019,7 +1034,7 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
     CK(cudaEventRecord(h->ev_fork2, st));
     CK(cudaStreamWaitEvent(h->st2, h->ev_fork2, 0));
   }
-  if (K > 0) launch_pair_bwd(h->kind, sa, st, h->st2);
+  if (K > 0) launch_pair_bwd(h->sk, sa, st, h->st2);
   CK(cudaEventRecord(h->ev_join, h->st2));
   mark(h, 4);
 
@@ -1129,7 +1144,7 @@ kg_status step_dist(kg_handle *h, StepBufs &S) {
   assign_buffers(h, S);
   if ((s = dag_forward(h, S)) != KG_OK) return s;
   mark(h, 2);
-  const int U = (h->kind == KG_BETAE || h->kind == KG_ROTATE || h->kind == KG_COMPLEX) ? h->m : d;
+  const int U = (h->sk == KG_BETAE || h->sk == KG_ROTATE || h->sk == KG_COMPLEX) ? h->m : d;
   const int64_t *neg_rows = h->rows + (int64_t)na * M + M;
   const float scale = 1.f / (float)((double)M * G);
   if (h->kind == KG_BETAE) {
@@ -1140,7 +1155,7 @@ kg_status step_dist(kg_handle *h, StepBufs &S) {
   pa.M = M; pa.U = U; pa.d = d; pa.ent = h->ent_src; pa.ans_rows = h->rows + (int64_t)na * M; pa.Q = h->Q;
   pa.alpha = h->cfg.box_alpha; pa.gamma = h->cfg.gamma; pa.scale = scale; pa.Cq = h->Cq; pa.QP = h->QP;
   pa.loss_pos = h->loss_pos; pa.Dpos = h->Dpos; pa.dQ = h->dQ; pa.dV = h->OG + (int64_t)na * M * d;
-  launch_pos(h->kind, pa, p.nout, st);
+  launch_pos(h->sk, pa, p.nout, st);
   ScoreArgs sa;
   sa.Q = h->Q; sa.NQ = S.NQ; sa.M = M; sa.K = K; sa.Kp = S.Kp; sa.U = U; sa.d = d;
   if (h->kind == KG_BETAE) { sa.E = h->F; sa.eidx = nullptr; sa.estride = 9LL * h->m; }
@@ -1151,7 +1166,7 @@ kg_status step_dist(kg_handle *h, StepBufs &S) {
   sa.Dpart = h->Dpart; sa.partQ = h->partQ; sa.partV = h->partV; sa.Cpart = h->Cpart; sa.Csum = h->Csum;
   sa.cap_D = h->cap_D; sa.cap_Q = h->cap_Q; sa.cap_V = h->cap_V;
   sa.dV = h->OG + (int64_t)(na * M + M) * d;
-  if (K > 0) launch_pair_fwd(h->kind, sa, p.nout, true, st);
+  if (K > 0) launch_pair_fwd(h->sk, sa, p.nout, true, st);
   // global loss = sum over ranks of the (1/(M G))-scaled local sums (A18); one finite check for all
   launch_loss_finalize(h->loss_pos, h->loss_part, M, K > 0 ? 1 : 0, 1.0 / ((double)M * G), h->loss_dev, h->flags,
                        h->t_dev, h->bc, h->cfg.beta1, h->cfg.beta2, h->apply, st, /*check=*/0);
@@ -1159,7 +1174,7 @@ kg_status step_dist(kg_handle *h, StepBufs &S) {
   NCK(nccl().AllReduce(h->flags + 1, h->flags + 1, 1, ncclInt32, ncclMax, h->comm, st));
   launch_loss_check(h->loss_dev, h->flags, h->t_dev, h->bc, h->cfg.beta1, h->cfg.beta2, h->apply, st);
   mark(h, 3);
-  if (K > 0) launch_pair_bwd(h->kind, sa, st, st);
+  if (K > 0) launch_pair_bwd(h->sk, sa, st, st);
   mark(h, 4);
   if ((s = dag_backward(h, S)) != KG_OK) return s;
   if (p.inter < 0 && h->kind != KG_BETAE && h->w_off < h->dense_size)
@@ -1331,7 +1346,7 @@ kg_status kg_score(kg_handle *h, const kg_batch *q, const int64_t *cand, int32_t
   if ((s = embed_queries(h, q, S, n_cand)) != KG_OK) return s;
   const Plan &p = S.plan;
   const int M = q->M, d = h->d, na = p.na;
-  const int U = (h->kind == KG_BETAE || h->kind == KG_ROTATE || h->kind == KG_COMPLEX) ? h->m : d;
+  const int U = (h->sk == KG_BETAE || h->sk == KG_ROTATE || h->sk == KG_COMPLEX) ? h->m : d;
   const int64_t *cand_rows = h->rows + (int64_t)na * M;
   if (h->kind == KG_BETAE) {
     launch_beta_query(h->Q, S.NQ, h->m, h->QP, h->Cq, st);
@@ -1343,7 +1358,7 @@ kg_status kg_score(kg_handle *h, const kg_batch *q, const int64_t *cand, int32_t
   else { sa.E = h->ent_src; sa.eidx = cand_rows; sa.estride = d; }
   sa.Cq = h->Cq; sa.Cv = h->Cv; sa.alpha = h->cfg.box_alpha; sa.Dmin = h->Dscore; sa.ldo = n_cand;
   sa.Dpart = h->Dpart; sa.cap_D = h->cap_D;
-  launch_pair_fwd(h->kind, sa, p.nout, false, st);
+  launch_pair_fwd(h->sk, sa, p.nout, false, st);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out_dist, h->Dscore, sizeof(float) * (size_t)M * n_cand, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -1388,9 +1403,9 @@ kg_status kg_eval(kg_handle *h, const kg_batch *q, const int64_t *ans_off, const
   if (n_neg > 0) CK(cudaMemcpyAsync(d_neg, negatives, sizeof(int64_t) * M * n_neg, cudaMemcpyHostToDevice, st));
   EvalArgs a;
   a.Q = h->Q; a.ent = h->ent_src; a.ans_off = d_off; a.ans_ids = d_ans; a.negatives = d_neg;
-  a.M = M; a.d = h->d; a.U = (h->kind == KG_BETAE || h->kind == KG_ROTATE || h->kind == KG_COMPLEX) ? h->m : h->d;
+  a.M = M; a.d = h->d; a.U = (h->sk == KG_BETAE || h->sk == KG_ROTATE || h->sk == KG_COMPLEX) ? h->m : h->d;
   a.n_neg = n_neg; a.max_ans = (int)max_ans; a.alpha = h->cfg.box_alpha; a.ranks = d_ranks; a.metrics = d_met;
-  launch_eval(h->kind, a, S.plan.nout, st);
+  launch_eval(h->sk, a, S.plan.nout, st);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(ranks, d_ranks, sizeof(int32_t) * n_ans, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(metrics, d_met, sizeof(float) * 4 * M, cudaMemcpyDeviceToHost, st));

@@ -137,6 +137,8 @@ void launch_betae_proj_dz(const float *dout, const float *Zp1, int rows, int d, 
 void launch_relu_mask(float *dY, const float *Y, int rows, int cols, cudaStream_t st);
 void launch_betae_split(const float *dX, int N, int d, const int64_t *anchor_rows, const float *ent, float *din,
                         int64_t din_ld, float *drel, cudaStream_t st);
+void launch_qnorm_fwd(float *X, int M, int d, int parts, float *nrm, cudaStream_t st);
+void launch_qnorm_bwd(float *G, const float *Y, int M, int d, int parts, const float *nrm, cudaStream_t st);
 void launch_neg_fwd(const float *in, int64_t n, float *out, cudaStream_t st);
 void launch_neg_bwd(const float *dout, const float *in, int64_t n, float *din, cudaStream_t st);
 void launch_mean_stack(const float *H, int n, int rows, int cols, float *out, cudaStream_t st);

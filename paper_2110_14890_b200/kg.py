@@ -23,7 +23,8 @@ _lib = C.CDLL(LIB_PATH)
 KG_OK, KG_EINVAL, KG_EUNSUPPORTED, KG_ENOMEM, KG_ECUDA, KG_ENCCL, KG_ENONFINITE, KG_ESTATE = range(8)
 STATUS = {0: "KG_OK", 1: "KG_EINVAL", 2: "KG_EUNSUPPORTED", 3: "KG_ENOMEM", 4: "KG_ECUDA",
           5: "KG_ENCCL", 6: "KG_ENONFINITE", 7: "KG_ESTATE"}
-KINDS = {"gqe": 0, "q2b": 1, "betae": 2, "transe": 3, "rotate": 4, "distmult": 5, "complex": 6}
+KINDS = {"gqe": 0, "q2b": 1, "betae": 2, "transe": 3, "rotate": 4, "distmult": 5, "complex": 6,
+         "rotate-m": 7, "distmult-m": 8, "complex-m": 9}
 STRUCTS = {"1p": 0, "2p": 1, "3p": 2, "2i": 3, "3i": 4, "ip": 5, "pi": 6, "2u": 7, "up": 8,
            "2in": 9, "3in": 10, "inp": 11, "pin": 12, "pni": 13}
 

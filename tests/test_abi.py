@@ -64,7 +64,7 @@ int main(void) {
 
 
 @pytest.mark.parametrize("field,value", [("dim", 12), ("dim", 0), ("n_entities", 0), ("n_relations", 0),
-                                         ("max_M", 0), ("world", 0), ("kind", 9), ("beta1", 1.0),
+                                         ("max_M", 0), ("world", 0), ("kind", 10), ("kind", -1), ("beta1", 1.0),
                                          ("eps", 0.0)])
 def test_create_rejects_bad_config(field, value):
     import kggen

@@ -15,7 +15,8 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 CASES = [("gqe", "1p"), ("gqe", "ip"), ("q2b", "2u"), ("q2b", "pi"), ("betae", "up"), ("betae", "pni"),
-         ("betae", "3i"), ("transe", "1p"), ("rotate", "1p"), ("distmult", "1p"), ("complex", "1p")]
+         ("betae", "3i"), ("transe", "1p"), ("rotate", "1p"), ("distmult", "1p"), ("complex", "1p"),
+         ("rotate-m", "2i"), ("distmult-m", "ip"), ("complex-m", "2u")]
 
 
 def _model(cfg, max_M):

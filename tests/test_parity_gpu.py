@@ -86,9 +86,11 @@ def _check_step(gm, table, cfg, batch, lr, step_no=1):
     return info
 
 
+# multi-hop models x 9 structures, single-hop 1p, BetaE negation (f1), the -m variants (f4)
 CASES = [(k, s) for k in ("gqe", "q2b", "betae") for s in kggen.STRUCTURES] + \
         [(k, "1p") for k in ("transe", "rotate", "distmult", "complex")] + \
-        [("betae", s) for s in kggen.NEG_STRUCTURES]          # negation, BetaE only (f1)
+        [("betae", s) for s in kggen.NEG_STRUCTURES] + \
+        [(k, s) for k in ("rotate-m", "distmult-m", "complex-m") for s in kggen.STRUCTURES]
 
 
 @pytest.mark.parametrize("kind,structure", CASES)
@@ -107,7 +109,7 @@ def test_step_parity(kind, structure):
 
 
 def test_init_matches_generator_bit_exact():
-    for kind in ("q2b", "betae", "rotate"):
+    for kind in ("q2b", "betae", "rotate", "complex-m"):
         cfg = kggen.ModelConfig(kind, 40, 300, 7, hidden=24)
         gm = _model(cfg, 8, 8, seed=11)
         ids = np.array([0, 1, 17, 299])
@@ -119,7 +121,8 @@ def test_init_matches_generator_bit_exact():
 
 @pytest.mark.parametrize("kind,structure", [("gqe", "ip"), ("q2b", "up"), ("betae", "pi"), ("rotate", "1p"),
                                             ("complex", "1p"), ("q2b", "3i"), ("betae", "pni"),
-                                            ("betae", "3in")])
+                                            ("betae", "3in"), ("rotate-m", "ip"), ("distmult-m", "up"),
+                                            ("complex-m", "pi")])
 def test_score_parity(kind, structure):
     cfg = kggen.ModelConfig(kind, 40, 300, 7, hidden=24)
     gm = _model(cfg, 70, 100, max_cand=90)

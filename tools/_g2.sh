@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_eval_gpu.py -x -q 2>&1 | tail -25
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -25
