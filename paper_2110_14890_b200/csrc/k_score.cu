@@ -19,6 +19,7 @@
 // A = e(x_alpha), B = e(x_beta), Pa = psi(A) - psi(A+B), Pb = psi(B) - psi(A+B),
 // TA = psi'(A), TB = psi'(B), TAB = psi'(A+B), GA/GB = d e / d x (clamp mask).
 #include <algorithm>
+#include <type_traits>
 
 #include "kg_common.cuh"
 #include "kg_launch.h"
@@ -181,6 +182,13 @@ __global__ void __launch_bounds__(256) pair_fwd_kernel(ScoreArgs a) {
     for (int x = 0; x < 4; ++x)
 #pragma unroll
       for (int y = 0; y < 4; ++y) acc[tt][x][y] = 0.f;
+  float2 s1[NOUT][4][2], s2[NOUT][4][2];   // Q2B: sum |t| and sum min(|t|, o) per candidate pair
+#pragma unroll
+  for (int tt = 0; tt < NOUT; ++tt)
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y) s1[tt][x][y] = s2[tt][x][y] = make_float2(0.f, 0.f);
   __syncthreads();
 
   for (int k0 = ku0; k0 < ku1; k0 += KC) {
@@ -208,29 +216,66 @@ __global__ void __launch_bounds__(256) pair_fwd_kernel(ScoreArgs a) {
       sE[f][q4 * 4 + 2][row] = v.z; sE[f][q4 * 4 + 3][row] = v.w;
     }
     __syncthreads();
+    if constexpr (std::is_same<Mdl, MBox>::value) {
+      // Q2B: D = sum |t| + (alpha - 1) sum min(|t|, o), t = v - c, on packed f32x2 pairs of
+      // candidates (FADD2 with |.| operands): 2.5 instructions per (query, candidate, unit)
 #pragma unroll 4
-    for (int kk = 0; kk < KC; ++kk) {
-      float ev[4][Mdl::EF];
+      for (int kk = 0; kk < KC; ++kk) {
+        const float4 v = *reinterpret_cast<const float4 *>(&sE[0][kk][4 * tx]);
+        const float2 e01 = make_float2(v.x, v.y), e23 = make_float2(v.z, v.w);
 #pragma unroll
-      for (int f = 0; f < Mdl::EF; ++f) {
-        const float4 v = *reinterpret_cast<const float4 *>(&sE[f][kk][4 * tx]);
-        ev[0][f] = v.x; ev[1][f] = v.y; ev[2][f] = v.z; ev[3][f] = v.w;
+        for (int tt = 0; tt < NOUT; ++tt) {
+          const float4 cq = *reinterpret_cast<const float4 *>(&sQ[tt][0][kk][4 * ty]);
+          const float4 oq = *reinterpret_cast<const float4 *>(&sQ[tt][1][kk][4 * ty]);
+          const float cs[4] = {cq.x, cq.y, cq.z, cq.w}, os[4] = {oq.x, oq.y, oq.z, oq.w};
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            const float2 cc = make_float2(-cs[x], -cs[x]);
+            const float2 t0 = __fadd2_rn(e01, cc), t1 = __fadd2_rn(e23, cc);
+            const float2 a0 = make_float2(fabsf(t0.x), fabsf(t0.y)), a1 = make_float2(fabsf(t1.x), fabsf(t1.y));
+            s1[tt][x][0] = __fadd2_rn(s1[tt][x][0], a0);
+            s1[tt][x][1] = __fadd2_rn(s1[tt][x][1], a1);
+            s2[tt][x][0] = __fadd2_rn(s2[tt][x][0], make_float2(fminf(a0.x, os[x]), fminf(a0.y, os[x])));
+            s2[tt][x][1] = __fadd2_rn(s2[tt][x][1], make_float2(fminf(a1.x, os[x]), fminf(a1.y, os[x])));
+          }
+        }
       }
+    } else {
+#pragma unroll 4
+      for (int kk = 0; kk < KC; ++kk) {
+        float ev[4][Mdl::EF];
 #pragma unroll
-      for (int tt = 0; tt < NOUT; ++tt) {
-        float qv[4][Mdl::QF];
-#pragma unroll
-        for (int f = 0; f < Mdl::QF; ++f) {
-          const float4 v = *reinterpret_cast<const float4 *>(&sQ[tt][f][kk][4 * ty]);
-          qv[0][f] = v.x; qv[1][f] = v.y; qv[2][f] = v.z; qv[3][f] = v.w;
+        for (int f = 0; f < Mdl::EF; ++f) {
+          const float4 v = *reinterpret_cast<const float4 *>(&sE[f][kk][4 * tx]);
+          ev[0][f] = v.x; ev[1][f] = v.y; ev[2][f] = v.z; ev[3][f] = v.w;
         }
 #pragma unroll
-        for (int x = 0; x < 4; ++x)
+        for (int tt = 0; tt < NOUT; ++tt) {
+          float qv[4][Mdl::QF];
 #pragma unroll
-          for (int b = 0; b < 4; ++b) acc[tt][x][b] += Mdl::acc(qv[x], ev[b], a.alpha);
+          for (int f = 0; f < Mdl::QF; ++f) {
+            const float4 v = *reinterpret_cast<const float4 *>(&sQ[tt][f][kk][4 * ty]);
+            qv[0][f] = v.x; qv[1][f] = v.y; qv[2][f] = v.z; qv[3][f] = v.w;
+          }
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[tt][x][b] += Mdl::acc(qv[x], ev[b], a.alpha);
+        }
       }
     }
     __syncthreads();
+  }
+  if constexpr (std::is_same<Mdl, MBox>::value) {
+#pragma unroll
+    for (int tt = 0; tt < NOUT; ++tt)
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        acc[tt][x][0] = fmaf(a.alpha - 1.f, s2[tt][x][0].x, s1[tt][x][0].x);
+        acc[tt][x][1] = fmaf(a.alpha - 1.f, s2[tt][x][0].y, s1[tt][x][0].y);
+        acc[tt][x][2] = fmaf(a.alpha - 1.f, s2[tt][x][1].x, s1[tt][x][1].x);
+        acc[tt][x][3] = fmaf(a.alpha - 1.f, s2[tt][x][1].y, s1[tt][x][1].y);
+      }
   }
   float *out = a.Dpart + (size_t)blockIdx.z * NOUT * M * a.Kp;
   const int jb = j0 + 4 * tx;
@@ -370,13 +415,45 @@ __global__ void __launch_bounds__(kBW * 32, 2) pair_bwd_kernel(ScoreArgs a) {
 #pragma unroll
       for (int f = 0; f < QF; ++f) { q[f] = sQ[(ii * QF + f) * 32 + lane]; dq[f] = 0.f; dq2[f] = 0.f; }
       const float4 *crow = reinterpret_cast<const float4 *>(sC + ii * JB + w * kJW);
+      if constexpr (std::is_same<Mdl, MBox>::value) {
+        // Q2B on packed f32x2 pairs of pool entries: t = v - c, a = |t|, W = [a > o] + alpha [a < o],
+        // cw = C W, cg = sign(t) cw (0 at t = 0, A19): dq_c -= cg, dv += cg, dq_o -= cw
+        const float2 cc = make_float2(-q[0], -q[0]);
+        const float o = q[1];
+        float2 gq0 = make_float2(0.f, 0.f), gq1 = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int j4 = 0; j4 < kJW / 4; ++j4) {
-        const float4 c4 = crow[j4];
-        Mdl::grad(q, ev[j4 * 4 + 0], c4.x, a.alpha, dq, dv[j4 * 4 + 0]);
-        Mdl::grad(q, ev[j4 * 4 + 1], c4.y, a.alpha, dq2, dv[j4 * 4 + 1]);
-        Mdl::grad(q, ev[j4 * 4 + 2], c4.z, a.alpha, dq, dv[j4 * 4 + 2]);
-        Mdl::grad(q, ev[j4 * 4 + 3], c4.w, a.alpha, dq2, dv[j4 * 4 + 3]);
+        for (int j4 = 0; j4 < kJW / 4; ++j4) {
+          const float4 c4 = crow[j4];
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int jp = j4 * 2 + h2;
+            const float2 cf = h2 ? make_float2(c4.z, c4.w) : make_float2(c4.x, c4.y);
+            const float2 t = __fadd2_rn(make_float2(ev[2 * jp][0], ev[2 * jp + 1][0]), cc);
+            const float ax = fabsf(t.x), ay = fabsf(t.y);
+            const float2 W = make_float2(fmaf(a.alpha, ax < o ? 1.f : 0.f, ax > o ? 1.f : 0.f),
+                                         fmaf(a.alpha, ay < o ? 1.f : 0.f, ay > o ? 1.f : 0.f));
+            const float2 cw = __fmul2_rn(cf, W);
+            const float2 cg = make_float2(
+                t.x == 0.f ? 0.f : __int_as_float(__float_as_int(cw.x) ^ (__float_as_int(t.x) & 0x80000000)),
+                t.y == 0.f ? 0.f : __int_as_float(__float_as_int(cw.y) ^ (__float_as_int(t.y) & 0x80000000)));
+            gq0 = __fadd2_rn(gq0, cg);
+            gq1 = __fadd2_rn(gq1, cw);
+            const float2 dvp = __fadd2_rn(make_float2(dv[2 * jp][0], dv[2 * jp + 1][0]), cg);
+            dv[2 * jp][0] = dvp.x;
+            dv[2 * jp + 1][0] = dvp.y;
+          }
+        }
+        dq[0] = -(gq0.x + gq0.y);
+        dq[1] = -(gq1.x + gq1.y);
+      } else {
+#pragma unroll
+        for (int j4 = 0; j4 < kJW / 4; ++j4) {
+          const float4 c4 = crow[j4];
+          Mdl::grad(q, ev[j4 * 4 + 0], c4.x, a.alpha, dq, dv[j4 * 4 + 0]);
+          Mdl::grad(q, ev[j4 * 4 + 1], c4.y, a.alpha, dq2, dv[j4 * 4 + 1]);
+          Mdl::grad(q, ev[j4 * 4 + 2], c4.z, a.alpha, dq, dv[j4 * 4 + 2]);
+          Mdl::grad(q, ev[j4 * 4 + 3], c4.w, a.alpha, dq2, dv[j4 * 4 + 3]);
+        }
       }
 #pragma unroll
       for (int f = 0; f < QF; ++f) sDQ[((w * kIC + ii) * QF + f) * 32 + lane] = dq[f] + dq2[f];
