@@ -136,7 +136,7 @@ def run_ours(args, world, rank, local):
     if args.workload.startswith("C5"):
         # constant per-GPU shard: theta_E of min(|V|, G * ceil(|V|/8)) rows,
         # row-sharded over the G ranks (full Freebase at G = 8)
-        cfg.n_entities = min(w.n_entities, world * kggen.shard_rows(w.n_entities, 8))
+        cfg.n_entities = min(w.n_entities, world * kggen.shard_rows(w.n_entities, args.shard_of))
     M, K = w.M, w.K
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
@@ -147,7 +147,8 @@ def run_ours(args, world, rank, local):
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
-    gm = KGModel(cfg, M, K, rank=rank, world=world, nccl_id=nccl_id)
+    host_tables = tuple(t for t in args.host_tier.split(",") if t)
+    gm = KGModel(cfg, M, K, rank=rank, world=world, nccl_id=nccl_id, host_tables=host_tables)
     gm.init_params(args.seed)
     gm.set_apply(True)
     lr = args.lr
@@ -271,6 +272,7 @@ def run_ours(args, world, rank, local):
                                              "NCCL exchange of rows / row gradients, all-reduce of dL/dtheta_D")
                    if world > 1 else "single",
                    "l2": "flushed between timed steps (256 MB write outside the step events)",
+                   "theta_E": ("pinned host memory (zero-copy): " + args.host_tier) if args.host_tier else "HBM",
                    "note": w.note},
         "e2e": e2e, "roofline": roof,
         "gpu_launches": int(sum(kernels_of.get(st, info.kernels) for st in step_structs)),
@@ -348,6 +350,10 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--distinct", type=int, default=4, help="distinct batches per structure (cycled)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard-of", type=int, default=8,
+                    help="C5: theta_E shard per GPU = ceil(|V| / SHARD_OF) rows (8: the 8-GPU shard)")
+    ap.add_argument("--host-tier", default="",
+                    help="comma list of ent,ent_m,ent_v kept in pinned host memory (kg_bind host tier)")
     args = ap.parse_args()
     assert args.warmup >= 3
     world, rank, local = dist_init(args.gpus)

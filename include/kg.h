@@ -144,7 +144,11 @@ int64_t kg_shard_rows(const kg_handle *h);
 /* Floats in theta_D for this model (relation tables + operator weights). */
 int64_t kg_dense_size(const kg_handle *h);
 
-/* Record the caller's table pointers and the CUDA stream (cudaStream_t, may be NULL). */
+/* Record the caller's table pointers and the CUDA stream (cudaStream_t, may be NULL).
+ * Host tier (the paper keeps theta_E in CPU memory): each of
+ * ent / ent_m / ent_v may be pinned host memory (cudaHostAlloc / cudaHostRegister) instead of
+ * device memory; the kernels then gather and update its rows zero-copy over the host link.
+ * theta_D must be device memory.  EINVAL for pageable or misaligned pointers. */
 kg_status kg_bind(kg_handle *h, const kg_tables *tables, void *cuda_stream);
 
 /* Parameter init (A23): counter-based U(lo, hi) of (seed, stream, index) into ent and dense,

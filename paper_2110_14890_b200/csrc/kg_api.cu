@@ -207,6 +207,7 @@ struct kg_handle {
   float *nval[6] = {}, *ngrad[6] = {};
   float *stack_v = nullptr, *stack_g = nullptr;
   float *qn = nullptr;   // [6 nodes][Mx][2] norms of the -m query normalisation
+  int host_tier = 0;     // bit i: theta_E table i (ent, ent_m, ent_v) is pinned host memory
   float *T[12] = {};
   int8_t *amin = nullptr;
   float *pX = nullptr, *pH1 = nullptr, *pH2 = nullptr, *pZp1 = nullptr, *pdZ = nullptr, *pdH2 = nullptr,
@@ -940,7 +941,28 @@ kg_status kg_bind(kg_handle *h, const kg_tables *t, void *stream) {
   const void *ps[6] = {t->ent, t->ent_m, t->ent_v, t->dense, t->dense_m, t->dense_v};
   for (const void *p : ps)
     if ((uintptr_t)p % 16) return fail(h, KG_EINVAL, "table pointers must be 16-byte aligned");
-  h->t = *t;
+  // theta_E tables may live in device memory or in pinned host memory (the host tier of
+  // SURVEY §8(f) f4): the kernels then read / write the rows zero-copy through
+  // their device-visible address.  Anything else (pageable host memory) is rejected.
+  kg_tables tt = *t;
+  float **ents[3] = {&tt.ent, &tt.ent_m, &tt.ent_v};
+  h->host_tier = 0;
+  for (int i = 0; i < 6; ++i) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, ps[i]) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(h, KG_EINVAL, "table pointer is not CUDA-visible memory");
+    }
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) continue;
+    if (a.type == cudaMemoryTypeHost && i < 3 && a.devicePointer) {
+      *ents[i] = static_cast<float *>(a.devicePointer);
+      h->host_tier |= 1 << i;
+      continue;
+    }
+    return fail(h, KG_EINVAL, i < 3 ? "theta_E tables must be device or pinned host memory"
+                                    : "theta_D tables must be device memory");
+  }
+  h->t = tt;
   h->st = (cudaStream_t)stream;
   CKB(cublasSetStream(h->blas, h->st));
   h->bound = true;
@@ -954,8 +976,12 @@ kg_status kg_init_params(kg_handle *h, uint64_t seed) {
   launch_init_rows(h->t.ent, h->shard, h->d, h->rank, h->world, seed, 0, (float)-rho, (float)rho, h->st);
   for (size_t i = 0; i < h->segs.size(); ++i)
     launch_init_flat(h->t.dense + h->segs[i].off, h->segs[i].n, seed, 1 + i, h->segs[i].lo, h->segs[i].hi, h->st);
-  CK(cudaMemsetAsync(h->t.ent_m, 0, sizeof(float) * h->shard * h->d, h->st));
-  CK(cudaMemsetAsync(h->t.ent_v, 0, sizeof(float) * h->shard * h->d, h->st));
+  // moments start at 0 (A23); a host-tier table is written by a kernel through its mapped address
+  float *mv[2] = {h->t.ent_m, h->t.ent_v};
+  for (int i = 0; i < 2; ++i) {
+    if (h->host_tier & (2 << i)) launch_init_flat(mv[i], h->shard * h->d, 0, 0, 0.f, 0.f, h->st);
+    else CK(cudaMemsetAsync(mv[i], 0, sizeof(float) * h->shard * h->d, h->st));
+  }
   CK(cudaMemsetAsync(h->t.dense_m, 0, sizeof(float) * h->dense_size, h->st));
   CK(cudaMemsetAsync(h->t.dense_v, 0, sizeof(float) * h->dense_size, h->st));
   CK(cudaMemsetAsync(h->t_dev, 0, sizeof(int64_t), h->st));

@@ -125,7 +125,9 @@ class KGModel:
     """Convenience owner of one handle + its caller-owned tables (torch device memory)."""
 
     def __init__(self, cfg, max_M, max_K, max_cand=0, device="cuda", stream=None, rank=0, world=1,
-                 nccl_id: bytes = None):
+                 nccl_id: bytes = None, host_tables=()):
+        """host_tables: names among ("ent", "ent_m", "ent_v") to keep in pinned host memory
+        (the host tier of kg_bind); the others live in device memory."""
         import torch
         self.cfg = cfg
         self.torch = torch
@@ -138,9 +140,11 @@ class KGModel:
         self.dense_size = kg_dense_size(self.h)
         d = cfg.dim
         f32 = torch.float32
-        self.ent = torch.empty((self.rows, d), dtype=f32, device=device)
-        self.ent_m = torch.empty_like(self.ent)
-        self.ent_v = torch.empty_like(self.ent)
+        def table(name):
+            if name in host_tables:
+                return torch.empty((self.rows, d), dtype=f32, pin_memory=True)
+            return torch.empty((self.rows, d), dtype=f32, device=device)
+        self.ent, self.ent_m, self.ent_v = table("ent"), table("ent_m"), table("ent_v")
         self.dense = torch.empty(self.dense_size, dtype=f32, device=device)
         self.dense_m = torch.empty_like(self.dense)
         self.dense_v = torch.empty_like(self.dense)
@@ -182,7 +186,7 @@ class KGModel:
             a = hb[k]
             if a.dtype == np.uint32:
                 a = a.view(np.int32)
-            out[k] = t.from_numpy(a.copy()).to(self.ent.device)
+            out[k] = t.from_numpy(a.copy()).to(self.dense.device)
         return out
 
     def step(self, b, lr, sync=True, on_device=False):

@@ -301,3 +301,43 @@ def test_graph_replay_equals_direct_launches(monkeypatch):
         gm.close()
     for a, b in zip(*res):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("host_tables", [("ent_v",), ("ent", "ent_m", "ent_v")])
+def test_host_tier_equals_device_tables_bitwise(host_tables):
+    """theta_E tables in pinned host memory (kg_bind host tier): the same
+    kernels run zero-copy over the host link, so every result is bit-identical."""
+    from paper_2110_14890_b200 import KGModel
+    cfg = kggen.ModelConfig("q2b", 40, 300, 7)
+    dev = KGModel(cfg, 70, 100)
+    host = KGModel(cfg, 70, 100, host_tables=host_tables)
+    assert not host.ent_v.is_cuda and dev.ent_v.is_cuda
+    losses = []
+    for m in (dev, host):
+        m.init_params(5)
+        m.set_apply(True)
+        out = []
+        for s in range(3):
+            b = kggen.make_batch(cfg, kggen.STRUCTURES[s * 3], 70, 100, seed=1, step=s)
+            out.append(m.step(m.host_batch(b), 0.01).loss)
+        losses.append(out)
+    assert losses[0] == losses[1]
+    ids = np.arange(300)
+    for which in (0, 1, 2):
+        np.testing.assert_array_equal(dev.read_rows(ids, which), host.read_rows(ids, which))
+    np.testing.assert_array_equal(dev.read_dense(), host.read_dense())
+    dev.close()
+    host.close()
+
+
+def test_bind_rejects_pageable_host_memory():
+    import ctypes as C
+    import torch
+    from paper_2110_14890_b200 import KGModel, kg
+    cfg = kggen.ModelConfig("gqe", 16, 100, 5)
+    m = KGModel(cfg, 8, 8)
+    pageable = torch.empty((m.rows, 16), dtype=torch.float32)        # not pinned
+    t = kg.kg_tables(pageable.data_ptr(), m.ent_m.data_ptr(), m.ent_v.data_ptr(), m.dense.data_ptr(),
+                     m.dense_m.data_ptr(), m.dense_v.data_ptr())
+    assert kg.kg_bind(m.h, C.byref(t), C.c_void_p(m.stream.cuda_stream)) == kg.KG_EINVAL
+    m.close()
