@@ -259,6 +259,49 @@ def make_batch(cfg: ModelConfig, structure: str, M: int, K: int, seed: int = 0,
 
 
 # --------------------------------------------------------------------------
+# Synthetic knowledge graph (input of the online sampler)
+# --------------------------------------------------------------------------
+def powerlaw_ranks(rng: np.random.Generator, size: int, n: int, a: float) -> np.ndarray:
+    """Ranks in [0, n) with P(k) ~ (k+1)^-a (continuous inverse CDF on [1, n+1), a != 1)."""
+    u = rng.random(size)
+    e = 1.0 - a
+    x = (((n + 1.0) ** e - 1.0) * u + 1.0) ** (1.0 / e)
+    return np.minimum(np.floor(x).astype(np.int64) - 1, n - 1)
+
+
+def make_kg(n_entities: int, n_relations: int, n_edges: int, seed: int = 0, a: float = 0.8) -> dict:
+    """A seeded synthetic KG G = (V, E, R) shaped like Table 3.
+
+    Heads and tails follow a power law over ranks (exponent `a`) mapped through two
+    fixed affine permutations (heavy-tailed in- and out-degrees, hubs differ), relations
+    are Zipf(1.0).  Duplicate triples are dropped, so |E| <= n_edges.  Returns
+    dict(h int64 [E], r int32 [E], t int64 [E], n_entities, n_relations), triples sorted
+    by (h, r, t).  Input recipe only: no traversal, sampling or index structure here.
+    """
+    rng = np.random.default_rng([seed, 0x6B67])
+    h = _affine_perm(powerlaw_ranks(rng, n_edges, n_entities, a), n_entities, salt=3)
+    t = _affine_perm(powerlaw_ranks(rng, n_edges, n_entities, a), n_entities, salt=4)
+    r = zipf_ids(rng, (n_edges,), n_relations, 1.0, salt=5)
+    hr = h * np.int64(n_relations) + r
+    order = np.lexsort((t, hr))
+    hr, t = hr[order], t[order]
+    keep = np.ones(len(t), dtype=bool)
+    keep[1:] = (hr[1:] != hr[:-1]) | (t[1:] != t[:-1])
+    hr, t = hr[keep], t[keep]
+    return dict(h=(hr // n_relations).astype(np.int64), r=(hr % n_relations).astype(np.int32),
+                t=t.astype(np.int64), n_entities=int(n_entities), n_relations=int(n_relations))
+
+
+# Table 3 shapes (training edges), for the sampler benches and tests
+KG_SHAPES = {
+    "FB15k-237": (14505, 237, 272115),
+    "FB400k": (409829, 918, 1075837),
+    "ogbl-wikikg2": (2500604, 535, 16109182),
+    "Freebase": (86054151, 14824, 304727650),
+}
+
+
+# --------------------------------------------------------------------------
 # BASELINE.json configs C1-C5 (SURVEY §8(d) table)
 # --------------------------------------------------------------------------
 @dataclass
@@ -295,6 +338,12 @@ WORKLOADS = {
                        note="Freebase-shaped Q2B d400, 9 structures, B512, K1024"),
     "C5-betae": Workload("C5-betae", "betae", 400, 86054151, 14824, ALL9, 512, 1024, hidden=1600,
                          note="Freebase-shaped BetaE d400, 9 structures, B512, K1024"),
+    # SURVEY §8(d) "bandwidth-shaped variant for H1": B = K = 4096 per GPU, so the sparse
+    # gather / segment-reduce / sparse-Adam kernels move enough rows to be measured against HBM
+    "C5-q2b-bw": Workload("C5-q2b-bw", "q2b", 400, 86054151, 14824, ALL9, 4096, 4096,
+                          note="bandwidth-shaped Freebase Q2B d400, 9 structures, B4096, K4096"),
+    "C4-bw": Workload("C4-bw", "betae", 400, 409829, 918, ALL9, 4096, 4096, hidden=1600,
+                      note="bandwidth-shaped FB400k BetaE d400, 9 structures, B4096, K4096"),
 }
 
 
