@@ -259,6 +259,12 @@ def run_ours(args, world, rank, local):
     e2e_s = allreduce_max(time.perf_counter() - t1, world)
     e2e = {"value": round(world * n_e2e * M / e2e_s, 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": 28, "steps": n_e2e}
+    e2e_sampler = None
+    if not args.no_sampler:
+        try:
+            e2e_sampler = sampler_e2e(args, gm, cfg, w, M, K, world, rank)
+        except Exception as ex:       # reported, never silently dropped
+            e2e_sampler = {"error": f"{type(ex).__name__}: {ex}"}
 
     out = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -274,7 +280,7 @@ def run_ours(args, world, rank, local):
                    "l2": "flushed between timed steps (256 MB write outside the step events)",
                    "theta_E": ("pinned host memory (zero-copy): " + args.host_tier) if args.host_tier else "HBM",
                    "note": w.note},
-        "e2e": e2e, "roofline": roof,
+        "e2e": e2e, "e2e_sampler": e2e_sampler, "roofline": roof,
         "gpu_launches": int(sum(kernels_of.get(st, info.kernels) for st in step_structs)),
         "kernels_per_step": kernels_of, "cublas_gemms_per_step": gemms_of, "ms_per_step_by_structure": per_struct_ms,
         "clocks": clk,
@@ -282,6 +288,57 @@ def run_ours(args, world, rank, local):
     }
     gm.close()
     return out, cfg, hb
+
+
+# ------------------------------------------------------------------ sampler-fed end to end (f3)
+def sampler_e2e(args, gm, cfg, w, M, K, world, rank):
+    """kg_step fed live by the native online sampler (libkgsample.so, §8(f) f3).
+
+    A seeded synthetic KG with the workload's |V| and |R| and |E| = |V| x the Table 3
+    edge density of the workload's dataset; worker threads run reverse sampling +
+    bidirectional rejection sampling into a ring of batches while the GPU trains.
+    Timed: `pipeline.next()` (the wait for a ready batch) + kg_step with host buffers
+    (H2D inside) + the loss D2H, wall clock over the steps, max over ranks.
+    """
+    import torch
+    from paper_2110_14890_b200.sampler import KGSampler
+
+    shape = {"C2": "FB15k-237", "C3-rotate": "ogbl-wikikg2", "C3-complex": "ogbl-wikikg2", "C4": "FB400k",
+             "C4-bw": "FB400k"}.get(args.workload, "Freebase")
+    V0, R0, E0 = kggen.KG_SHAPES[shape]
+    n_edges = int(round(E0 * cfg.n_entities / V0))
+    t0 = time.perf_counter()
+    kg = kggen.make_kg(cfg.n_entities, cfg.n_relations, n_edges, seed=args.seed, dedup=False)
+    t_gen = time.perf_counter() - t0
+    threads = os.cpu_count() or 2
+    t0 = time.perf_counter()
+    smp = KGSampler(kg, n_threads=threads)
+    t_idx = time.perf_counter() - t0
+    del kg
+    workers = max(1, threads - 1)
+    pipe = smp.pipeline(w.structures, M, K, seed=args.seed, rank=rank, first_step=0, depth=2 * workers,
+                        n_workers=workers)
+    for _ in range(2 * workers):                  # warm-up: fill the ring once
+        gm.step(pipe.next(), args.lr, sync=True)
+    n = min(args.steps, 450)
+    torch.cuda.synchronize()
+    barrier(world)
+    pipe.wait_ms = 0.0
+    t1 = time.perf_counter()
+    for _ in range(n):
+        gm.step(pipe.next(), args.lr, sync=True)
+    el = allreduce_max(time.perf_counter() - t1, world)
+    wait = pipe.wait_ms
+    pipe.close()
+    smp.close()
+    W = (K + 31) // 32
+    return {"value": round(world * n * M / el, 1), "unit": UNIT, "steps": n,
+            "h2d_bytes_per_step": M * 3 * 8 + M * 3 * 4 + M * 8 + K * 8 + M * W * 4, "d2h_bytes_per_step": 28,
+            "sampler_wait_ms_per_step": round(wait / n, 4), "host_threads": threads, "sampler_workers": workers,
+            "kg": {"shape": shape, "entities": cfg.n_entities, "relations": cfg.n_relations,
+                   "edges": int(smp.n_edges), "gen_s": round(t_gen, 1), "index_s": round(t_idx, 1)},
+            "note": "reverse directional sampling + bidirectional rejection sampling (exact masks) on host "
+                    "threads, prefetched; kg_step with host batches; wall clock"}
 
 
 # ------------------------------------------------------------------ oracle timing
@@ -350,6 +407,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--distinct", type=int, default=4, help="distinct batches per structure (cycled)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sampler", action="store_true", help="skip the sampler-fed e2e measurement")
     ap.add_argument("--shard-of", type=int, default=8,
                     help="C5: theta_E shard per GPU = ceil(|V| / SHARD_OF) rows (8: the 8-GPU shard)")
     ap.add_argument("--host-tier", default="",

@@ -269,19 +269,24 @@ def powerlaw_ranks(rng: np.random.Generator, size: int, n: int, a: float) -> np.
     return np.minimum(np.floor(x).astype(np.int64) - 1, n - 1)
 
 
-def make_kg(n_entities: int, n_relations: int, n_edges: int, seed: int = 0, a: float = 0.8) -> dict:
+def make_kg(n_entities: int, n_relations: int, n_edges: int, seed: int = 0, a: float = 0.8,
+            dedup: bool = True) -> dict:
     """A seeded synthetic KG G = (V, E, R) shaped like Table 3.
 
     Heads and tails follow a power law over ranks (exponent `a`) mapped through two
     fixed affine permutations (heavy-tailed in- and out-degrees, hubs differ), relations
     are Zipf(1.0).  Duplicate triples are dropped, so |E| <= n_edges.  Returns
     dict(h int64 [E], r int32 [E], t int64 [E], n_entities, n_relations), triples sorted
-    by (h, r, t).  Input recipe only: no traversal, sampling or index structure here.
+    by (h, r, t).  dedup=False skips the sort (large benches): the triples keep their draw
+    order and may repeat; the samplers' indices drop repeats themselves.  Input recipe
+    only: no traversal, sampling or index structure here.
     """
     rng = np.random.default_rng([seed, 0x6B67])
     h = _affine_perm(powerlaw_ranks(rng, n_edges, n_entities, a), n_entities, salt=3)
     t = _affine_perm(powerlaw_ranks(rng, n_edges, n_entities, a), n_entities, salt=4)
     r = zipf_ids(rng, (n_edges,), n_relations, 1.0, salt=5)
+    if not dedup:
+        return dict(h=h, r=r.astype(np.int32), t=t, n_entities=int(n_entities), n_relations=int(n_relations))
     hr = h * np.int64(n_relations) + r
     order = np.lexsort((t, hr))
     hr, t = hr[order], t[order]

@@ -40,7 +40,28 @@ def sources():
     return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
 
 
+SAMPLER_OUT = os.path.join(HERE, "libkgsample.so")
+CXX = os.environ.get("CXX", "g++")
+
+
+def build_sampler(verbose: bool = False, force: bool = False) -> str:
+    """libkgsample.so: the host-side online sampler (csrc/sampler.cpp, include/kg_sample.h)."""
+    src = os.path.join(CSRC, "sampler.cpp")
+    deps = [src, os.path.join(ROOT, "include", "kg_sample.h")]
+    if not force and os.path.exists(SAMPLER_OUT) and all(os.path.getmtime(SAMPLER_OUT) >= os.path.getmtime(d)
+                                                         for d in deps):
+        return SAMPLER_OUT
+    cmd = [CXX, "-O3", "-g", "-std=c++17", "-fPIC", "-shared", "-pthread", "-Wall", "-I", os.path.join(ROOT, "include"),
+           src, "-o", SAMPLER_OUT + ".tmp"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    os.replace(SAMPLER_OUT + ".tmp", SAMPLER_OUT)
+    return SAMPLER_OUT
+
+
 def build(verbose: bool = False, force: bool = False, out: str = None) -> str:
+    build_sampler(verbose, force)
     OUT_ = out or OUT
     srcs = sources()
     deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
