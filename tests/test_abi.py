@@ -83,3 +83,14 @@ def test_create_rejects_odd_hidden_for_betae():
     cfg = kggen.ModelConfig("betae", 16, 100, 5, hidden=12)
     h = C.c_void_p()
     assert kgb.kg_create(C.byref(kgb.make_config(cfg, 8, 8)), C.byref(h)) == kgb.kg.KG_EINVAL
+
+
+def test_sampler_library_exports_every_declared_symbol():
+    from paper_2110_14890_b200 import sampler as kgs
+    txt = open(os.path.join(ROOT, "include", "kg_sample.h")).read()
+    declared = sorted(set(re.findall(r"^\s*(?:const\s+)?[\w\s\*]*?\b(kgs_\w+)\s*\(", txt, re.M)))
+    assert len(declared) >= 10
+    lib = C.CDLL(kgs.SAMPLER_LIB_PATH)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert sorted(kgs.SAMPLER_EXPORTED) == declared
