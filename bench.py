@@ -193,7 +193,7 @@ def run_ours(args, world, rank, local):
 
     # ---- profiling pass: the same steps with stage events (CUDA events on the bound stream)
     gm.set_apply(True, stage_timing=True)
-    stage = np.zeros(8)
+    stage = np.zeros(10)
     work = {}
     kernels_of, gemms_of = {}, {}
     n_prof = min(args.steps, 9 * 3)
@@ -203,7 +203,7 @@ def run_ours(args, world, rank, local):
         inf = gm.step(db[(args.warmup + s) % n_distinct], lr, sync=True, on_device=True)
         kernels_of[b["structure"]] = inf.kernels
         gemms_of[b["structure"]] = inf.gemms
-        stage += np.array(inf.stage_ms[:8])
+        stage += np.array(inf.stage_ms[:10])
         for k, (bound, amount, unit) in stage_work(cfg, M, K, b["structure"], inf.n_touched, cfg.dim).items():
             work.setdefault(k, [bound, 0.0, unit])[1] += amount
     gm.set_apply(True)
@@ -212,7 +212,10 @@ def run_ours(args, world, rank, local):
                    "sparse_adam", "dense_adam"]
     shares = {stage_names[i]: round(float(stage[i] / stage[7]), 4) for i in range(7)}
     pk, pk_src = peaks()
-    cand = {"scoring": (stage[2] + stage[3]), "dense_adam": stage[6], "sparse_adam": stage[5]}
+    # the dense update (relation reduce + dense Adam) runs on a second stream concurrently with the
+    # sparse update: its own duration is stage 8; stage 6 is only what it adds to the critical path
+    cand = {"scoring": (stage[2] + stage[3]), "dense_adam": stage[8] if stage[8] > 0 else stage[6],
+            "sparse_adam": stage[5]}
     dom = max(cand, key=cand.get)
     bound, amount, unit = work[dom]
     per_launch = amount / n_prof
@@ -228,7 +231,11 @@ def run_ours(args, world, rank, local):
                 "unit": "TFLOP/s", "frac": round(achieved / FP32_PEAK_TFLOPS, 4), "traffic": None}
     roof.update({"kernel": dom, "peak_source": pk_src if bound == "hbm" else "derived (DESIGN.md §6)",
                  "stage_ms": {stage_names[i]: round(float(stage[i]), 4) for i in range(7)},
-                 "stage_share": shares, "dominant_share": round(float(cand[dom] / stage[7]), 4)})
+                 "stage_share": shares, "dominant_share": round(float(cand[dom] / stage[7]), 4),
+                 "dense_update_path_ms": round(float(stage[8]), 4),
+                 "stage_note": "sparse_adam = stage 5 (critical path); dense_adam stage = what the dense update "
+                               "adds after it; the dense path itself (dense_update_path_ms, concurrent with "
+                               "stage 5) is the time used for its GB/s"})
     other = {}
     for k in cand:
         b_, a_, u_ = work[k]

@@ -126,9 +126,13 @@ typedef struct {
   int64_t step;          /* Adam step counter t after the step */
   int32_t kernels;       /* kernels of this library enqueued by the step */
   int32_t gemms;         /* cuBLAS SGEMM calls enqueued by the step (dense MLP layers) */
-  float stage_ms[8];     /* device time per stage when stage timing is on (kg_set_apply bit 2), else 0:
+  float stage_ms[10];    /* device time per stage when stage timing is on (kg_set_apply bit 2), else 0:
                             0 ingest + dedup, 1 DAG forward, 2 scoring forward + Eq. 1, 3 scoring backward,
-                            4 DAG backward, 5 relation reduce + sparse Adam, 6 dense Adam, 7 whole step */
+                            4 DAG backward, 5 sparse update (segment reduce + sparse Adam), 6 what the dense
+                            update adds after the sparse one, 7 whole step, 8 the dense update path itself
+                            (relation reduce + dense Adam over theta_D, on a second stream concurrently with
+                            stage 5; world = 1), 9 reserved (0).  With world > 1 stage 5 also holds the
+                            relation reduce and 6 the all-reduce + dense Adam, and 8 is 0. */
 } kg_step_info;
 
 typedef struct kg_handle kg_handle;   /* opaque; one per (process, device) */

@@ -258,7 +258,8 @@ struct kg_handle {
 
   int64_t stamp = 0;
   int apply = 1, keep_grads = 0, timing = 0;
-  cudaEvent_t sev[8] = {};
+  cudaEvent_t sev[10] = {};
+  bool side_timed = false;
   int64_t launches0 = 0;
   int last_kernels = 0, last_gemms = 0, gemm_count = 0;
   int last_M = 0, last_K = 0, last_U_valid = 0;
@@ -816,9 +817,9 @@ kg_status ingest(kg_handle *h, const kg_batch *b, bool train, const Plan &plan, 
   return KG_OK;
 }
 
-void mark(kg_handle *h, int i) {
+void mark(kg_handle *h, int i, cudaStream_t s = nullptr) {
   // external: inside a stream capture this becomes an event-record node of the graph
-  if (h->timing) cudaEventRecordWithFlags(h->sev[i], h->st, cudaEventRecordExternal);
+  if (h->timing) cudaEventRecordWithFlags(h->sev[i], s ? s : h->st, cudaEventRecordExternal);
 }
 
 kg_status read_result(kg_handle *h, kg_step_info *info) {
@@ -830,10 +831,11 @@ kg_status read_result(kg_handle *h, kg_step_info *info) {
     info->step = h->hout->t;
     info->kernels = h->last_kernels;
     info->gemms = h->last_gemms;
-    for (int i = 0; i < 8; ++i) info->stage_ms[i] = 0.f;
+    for (int i = 0; i < 10; ++i) info->stage_ms[i] = 0.f;
     if (h->timing) {
       for (int i = 0; i < 7; ++i) CK(cudaEventElapsedTime(&info->stage_ms[i], h->sev[i], h->sev[i + 1]));
       CK(cudaEventElapsedTime(&info->stage_ms[7], h->sev[0], h->sev[7]));
+      if (h->side_timed) CK(cudaEventElapsedTime(&info->stage_ms[8], h->sev[8], h->sev[9]));
     }
   }
   if (h->hout->flags[1]) return fail(h, KG_EINVAL, "an id or relation of the (device) batch was out of range; step not applied");
@@ -898,7 +900,7 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
   if (cudaMallocHost(&h->hout, sizeof(kg_handle::HostOut)) != cudaSuccess) { kg_destroy(h); return KG_ENOMEM; }
   std::memset(h->hout, 0, sizeof(kg_handle::HostOut));
   if (cudaEventCreateWithFlags(&h->step_done, cudaEventDisableTiming) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < 10; ++i)
     if (cudaEventCreate(&h->sev[i]) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
   if (cublasCreate(&h->blas) != CUBLAS_STATUS_SUCCESS) { kg_destroy(h); return KG_ECUDA; }
   if (cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking) != cudaSuccess ||
@@ -1003,6 +1005,7 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   const int L = na * M + M + K, Lr = p.nproj * M;
   cudaStream_t st = h->st;
   h->ent_src = h->t.ent;
+  h->side_timed = true;
   mark(h, 0);
   // a2: ids (fused gather indices) on the main stream; dedup of entities and relations
   // on the side stream -- only the sparse update at the end needs them
@@ -1073,29 +1076,42 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
     CK(cudaMemsetAsync(h->gdense + (a->off - h->w_off), 0, sizeof(float) * (h->dense_size - a->off), st));
   }
 
-  // a12-a14: relation rows reduce, sparse Adam on touched rows, dense Adam on theta_D
+  // a12-a14: the sparse update (segment reduce + sparse Adam, latency-bound random rows) on
+  // the main stream, concurrently with the relation-row reduce and the dense Adam over
+  // theta_D (a streaming, HBM-bound pass) on the side stream; joined before the outputs.
+  // Stage 5-6 = the sparse path, stage 6-7 = what the dense path adds after it.
   CK(cudaStreamWaitEvent(st, h->ev_join, 0));
   mark(h, 5);
-  launch_rel_reduce(h->rseg, h->rperm, h->rinv, h->rU, Lr, h->RG, h->PSr, h->dr, h->RGU, st);
-  launch_rel_stamp(h->runiq, h->rU, Lr, h->rel_seg_map, h->rel_stamp, h->stamp_dev, st);
+  CK(cudaEventRecord(h->ev_fork2, st));
+  CK(cudaStreamWaitEvent(h->st2, h->ev_fork2, 0));
+  {
+    cudaStream_t s2 = h->st2;
+    mark(h, 8, s2);
+    launch_rel_reduce(h->rseg, h->rperm, h->rinv, h->rU, Lr, h->RG, h->PSr, h->dr, h->RGU, s2);
+    launch_rel_stamp(h->runiq, h->rU, Lr, h->rel_seg_map, h->rel_stamp, h->stamp_dev, s2);
+    if (h->apply) {
+      const double b1 = h->cfg.beta1, b2 = h->cfg.beta2, eps = h->cfg.eps;
+      const float *lr = h->lr_dev;
+      {
+        // relation tables: segs[0] (and segs[1] for Q2B: rel_offset right after rel_center)
+        const Seg &r = h->segs[0];
+        const int nseg = h->kind == KG_Q2B ? 2 : 1;
+        launch_dense_adam_rel(h->t.dense + r.off, h->t.dense_m + r.off, h->t.dense_v + r.off, h->R, r.cols, nseg,
+                              h->RGU, h->rel_seg_map, h->rel_stamp, h->stamp_dev, lr, b1, b2, eps, h->bc, h->flags,
+                              s2);
+      }
+      launch_dense_adam(h->t.dense + h->w_off, h->t.dense_m + h->w_off, h->t.dense_v + h->w_off, h->gdense,
+                        h->dense_size - h->w_off, lr, b1, b2, eps, h->bc, h->flags, s2);
+    }
+    mark(h, 9, s2);
+    CK(cudaEventRecord(h->ev_join, s2));
+  }
   if (h->apply || h->keep_grads)
     launch_sparse_adam(h->uniq, h->seg, h->perm, h->inv, h->Udev, L, h->OG, h->PS, d, h->world, h->t.ent, h->t.ent_m,
                        h->t.ent_v, h->keep_grads ? h->Gc : nullptr, h->lr_dev, h->cfg.beta1, h->cfg.beta2,
                        h->cfg.eps, h->bc, h->flags, h->apply, st);
   mark(h, 6);
-  if (h->apply) {
-    const double b1 = h->cfg.beta1, b2 = h->cfg.beta2, eps = h->cfg.eps;
-    const float *lr = h->lr_dev;
-    {
-      // relation tables: segs[0] (and segs[1] for Q2B: rel_offset right after rel_center)
-      const Seg &r = h->segs[0];
-      const int nseg = h->kind == KG_Q2B ? 2 : 1;
-      launch_dense_adam_rel(h->t.dense + r.off, h->t.dense_m + r.off, h->t.dense_v + r.off, h->R, r.cols, nseg,
-                            h->RGU, h->rel_seg_map, h->rel_stamp, h->stamp_dev, lr, b1, b2, eps, h->bc, h->flags, st);
-    }
-    launch_dense_adam(h->t.dense + h->w_off, h->t.dense_m + h->w_off, h->t.dense_v + h->w_off, h->gdense,
-                      h->dense_size - h->w_off, lr, b1, b2, eps, h->bc, h->flags, st);
-  }
+  CK(cudaStreamWaitEvent(st, h->ev_join, 0));
   mark(h, 7);
   CK(cudaGetLastError());
   // results to pinned host memory (loss, flags, U, t)
@@ -1125,6 +1141,7 @@ kg_status step_dist(kg_handle *h, StepBufs &S) {
   const int M = S.M, K = S.K, d = h->d, na = p.na, nr = p.nr, G = h->world, me = h->rank;
   const int L = na * M + M + K, Lr = p.nproj * M;
   cudaStream_t st = h->st;
+  h->side_timed = false;
   mark(h, 0);
   CK(cudaMemsetAsync(h->flags, 0, 2 * sizeof(int), st));
   launch_ids_concat(h->b_anchors, na, M, h->b_answers, M, h->b_negs, K, G, h->ids, h->rows, h->flags + 1, h->n_ent,
@@ -1618,7 +1635,7 @@ void kg_destroy(kg_handle *h) {
   }
   if (h->hout) cudaFreeHost(h->hout);
   if (h->step_done) cudaEventDestroy(h->step_done);
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < 10; ++i)
     if (h->sev[i]) cudaEventDestroy(h->sev[i]);
   if (h->comm) nccl().CommDestroy(h->comm);
   if (h->h_counts) cudaFreeHost(h->h_counts);

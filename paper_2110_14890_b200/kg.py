@@ -49,7 +49,7 @@ class kg_batch(C.Structure):
 
 class kg_step_info(C.Structure):
     _fields_ = [("loss", C.c_double), ("n_touched", C.c_int32), ("step", C.c_int64),
-                ("kernels", C.c_int32), ("gemms", C.c_int32), ("stage_ms", C.c_float * 8)]
+                ("kernels", C.c_int32), ("gemms", C.c_int32), ("stage_ms", C.c_float * 10)]
 
 
 _H = C.c_void_p
