@@ -35,6 +35,27 @@ def _linear(x, W, b):
     return x @ W.T + b
 
 
+# Test instrumentation (no arithmetic change): when TRACE is a list, every discrete decision
+# the forward takes on a computed value -- a ReLU / clamp kink or an argmin between inputs --
+# appends (margin, scale): the signed distance of the value from the kink and the magnitude
+# scale of the sum that produced it (|W| |x| + |b|).  tests/test_fullsize_gpu.py uses it to
+# build inputs whose decisions are well away from fp32 rounding (reading A28).
+TRACE = None
+
+
+def _trace(margin, scale):
+    if TRACE is not None:
+        TRACE.append((margin.detach(), scale.detach()))
+
+
+def _relu_lin(x, W, b):
+    """ReLU(W x + b), traced at its kink."""
+    z = _linear(x, W, b)
+    if TRACE is not None:
+        _trace(z, x.abs() @ W.abs().T + b.abs())
+    return torch.relu(z)
+
+
 def _halves(x):
     m = x.shape[-1] // 2
     return x[..., :m], x[..., m:]
@@ -92,9 +113,12 @@ def project(kind: str, q: torch.Tensor, r: torch.Tensor, P: dict) -> torch.Tenso
     if kind == "betae":
         # Table 1 MLP(Em(q), Em(r)); A9: [e_q; y] -> H -> H -> d, ReLU, A8 clamp(+1)
         x = torch.cat([q, P["rel"][r]], dim=-1)
-        h1 = torch.relu(_linear(x, P["prj_W1"], P["prj_b1"]))
-        h2 = torch.relu(_linear(h1, P["prj_W2"], P["prj_b2"]))
-        return torch.clamp(_linear(h2, P["prj_W0"], P["prj_b0"]) + 1.0, 0.05, 1e9)
+        h1 = _relu_lin(x, P["prj_W1"], P["prj_b1"])
+        h2 = _relu_lin(h1, P["prj_W2"], P["prj_b2"])
+        y = _linear(h2, P["prj_W0"], P["prj_b0"])
+        if TRACE is not None:
+            _trace(y + 1.0 - 0.05, h2.abs() @ P["prj_W0"].abs().T + P["prj_b0"].abs() + 1.0)
+        return torch.clamp(y + 1.0, 0.05, 1e9)
     if kind == "rotate":
         # Table 2 h o r with |r_k| = 1; A3: r_k = exp(i theta_k)
         h_re, h_im = _halves(q)
@@ -116,27 +140,32 @@ def intersect(kind: str, qs: list, P: dict) -> torch.Tensor:
     X = torch.stack(qs, dim=0)                                  # [n, M, dq]
     if kind in kggen.M_VARIANTS:
         # GQE's DeepSet on the d-float rows ([re | im] for the complex ones)
-        h = torch.relu(_linear(X, P["ds_W1"], P["ds_b1"])).mean(dim=0)
+        h = _relu_lin(X, P["ds_W1"], P["ds_b1"]).mean(dim=0)
         return normalize(kind, _linear(h, P["ds_W2"], P["ds_b2"]))
     if kind == "gqe":
         # A4 DeepSet: W2 * mean_i ReLU(W1 q_i + b1) + b2
-        h = torch.relu(_linear(X, P["ds_W1"], P["ds_b1"])).mean(dim=0)
+        h = _relu_lin(X, P["ds_W1"], P["ds_b1"]).mean(dim=0)
         return _linear(h, P["ds_W2"], P["ds_b2"])
     if kind == "q2b":
         d = X.shape[-1] // 2
         C, O = X[..., :d], X[..., d:]
         # A5 center: a_i = softmax_i(W2 ReLU(W1 c_i + b1) + b2); c = sum_i a_i * c_i
-        logits = _linear(torch.relu(_linear(C, P["att_W1"], P["att_b1"])), P["att_W2"], P["att_b2"])
+        logits = _linear(_relu_lin(C, P["att_W1"], P["att_b1"]), P["att_W2"], P["att_b2"])
         a = torch.softmax(logits, dim=0)
         c = (a * C).sum(dim=0)
         # Table 1: Off(q) = min({Off(q_i)}) * sigmoid(DeepSet({Off(q_i)}))  (A4 DeepSet)
         omin = O.min(dim=0).values                               # ties -> lowest index (A19)
-        z = _linear(torch.relu(_linear(O, P["off_W1"], P["off_b1"])).mean(dim=0),
+        if TRACE is not None:
+            for i in range(1, O.shape[0]):
+                for j in range(i):   # exact ties are decided alike on both sides (same inputs)
+                    gap = O[i] - O[j]
+                    _trace(torch.where(gap == 0, torch.ones_like(gap), gap), O[i].abs() + O[j].abs())
+        z = _linear(_relu_lin(O, P["off_W1"], P["off_b1"]).mean(dim=0),
                     P["off_W2"], P["off_b2"])
         return torch.cat([c, omin * torch.sigmoid(z)], dim=-1)
     if kind == "betae":
         # Table 1: [(sum w_i alpha_i, sum w_i beta_i)]; A5: w = softmax_i(U2 ReLU(U1 [a_i; b_i] + c1) + c2)
-        logits = _linear(torch.relu(_linear(X, P["att_U1"], P["att_c1"])), P["att_U2"], P["att_c2"])
+        logits = _linear(_relu_lin(X, P["att_U1"], P["att_c1"]), P["att_U2"], P["att_c2"])
         w = torch.softmax(logits, dim=0)                         # [n, M, m]
         A, B = _halves(X)
         return torch.cat([(w * A).sum(dim=0), (w * B).sum(dim=0)], dim=-1)

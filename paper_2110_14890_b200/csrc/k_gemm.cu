@@ -153,12 +153,24 @@ __device__ __forceinline__ void load_op(const CUtensorMap *tm, uint64_t *bar, ui
     tma_load_2d(tm, bar, dst, k0, r0);
   }
 }
+// lo = x - trunc_tf32(x), rounded to the nearest tf32 (cvt.rna): the MMA then reads lo exactly
+// instead of truncating it again (a one-sided error of ~2^-22 |x| per operand that accumulates
+// linearly over K; tools/gemm_precision.py)
+__device__ __forceinline__ float rna_tf32(float x) {
+#ifdef KG_TF32_LO_TRUNC
+  return x;
+#else
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+#endif
+}
 __device__ __forceinline__ float4 tf32_lo(float4 v) {
   float4 l;
-  l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-  l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-  l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-  l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+  l.x = rna_tf32(v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u));
+  l.y = rna_tf32(v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u));
+  l.z = rna_tf32(v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u));
+  l.w = rna_tf32(v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u));
   return l;
 }
 // split one landed operand tile of R rows (32 G2CW threads, ct = 0 ..)
@@ -249,9 +261,15 @@ __global__ void __launch_bounds__(G2T, 1)
         for (int kk = 0; kk < G2K / 8; ++kk) {   // K = 8 tf32 per MMA
           const uint64_t dah = kmajor_desc(ah, kk), dal = kmajor_desc(al, kk);
           const uint64_t dbh = kmajor_desc(bh, kk), dbl = kmajor_desc(bl, kk);
-          mma_tf32_i<Cfg::kIdesc>(tmem, dah, dbh, (kb | kk) != 0);
+          // small terms first: lo.lo (KG_TF32X4), hi.lo, lo.hi, then hi.hi
+#ifdef KG_TF32X4
+          mma_tf32_i<Cfg::kIdesc>(tmem, dal, dbl, (kb | kk) != 0);
           mma_tf32_i<Cfg::kIdesc>(tmem, dah, dbl, 1);
+#else
+          mma_tf32_i<Cfg::kIdesc>(tmem, dah, dbl, (kb | kk) != 0);
+#endif
           mma_tf32_i<Cfg::kIdesc>(tmem, dal, dbh, 1);
+          mma_tf32_i<Cfg::kIdesc>(tmem, dah, dbh, 1);
         }
         mma_commit(&empty_bar[s]);
       }

@@ -36,7 +36,7 @@ struct ML2 {   // GQE, TransE: ||q - v||_2 (A2)
   __device__ static void bq(const float *q, const float *e, float c, float, float *dq) { dq[0] += c * (q[0] - e[0]); }
   __device__ static void bv(const float *q, const float *e, float c, float, float *a) { a[0] += c * (e[0] - q[0]); }
   // fused backward: dq += dD/dq * C, dv += dD/dv * C   (C here is c_ij / D_ij, A2 adjoint)
-  static constexpr int BF = 1, BOFF = 0;
+  static constexpr int BF = 1, BOFF = 0, BQF = QF;
   __device__ static void grad(const float *q, const float *e, float c, float, float *dq, float *dv) {
     const float ct = c * (q[0] - e[0]);
     dq[0] += ct;
@@ -65,7 +65,7 @@ struct MBox {  // Q2B: sum ReLU(|v-c| - o) + alpha * min(|v-c|, o) (A7)
     const float s = (dl > 0.f) ? 1.f : ((dl < 0.f) ? -1.f : 0.f);
     acc_[0] += c * s * ((a > o ? 1.f : 0.f) + al * (a < o ? 1.f : 0.f));
   }
-  static constexpr int BF = 1, BOFF = 0;
+  static constexpr int BF = 1, BOFF = 0, BQF = QF;
   __device__ static void grad(const float *q, const float *e, float c, float al, float *dq, float *dv) {
     // t = v - c, a = |t|, W = [a > o] + alpha [a < o]:  dD/dv = sign(t) W (sign(0) = 0),
     // dD/dc = -dD/dv, dD/do = alpha - W (= alpha - 1 | 0 | alpha for a > o | a < o | a == o);
@@ -88,13 +88,16 @@ struct MBeta {  // KL(Beta(entity) || Beta(query)) summed over m (A10), direct p
   __device__ static float fin(float s, float cq, float cv) { return s + cq - cv; }
   __device__ static void bq(const float *, const float *e, float c, float, float *dq) { dq[0] -= c * e[0]; dq[1] -= c * e[1]; }
   __device__ static void bv(const float *q, const float *, float c, float, float *a) { a[0] += c * q[0]; a[1] += c * q[1]; }
-  // e = [Pa, Pb]; dv accumulates sum C a2, sum C b2 (epilogue in the combine kernel)
-  static constexpr int BF = 2, BOFF = 0;
+  // Backward on per-term differences (no cancellation of large sums, A22):
+  // q = [a2, b2, QPa, QPb] (query Beta and its psi(a2) - psi(a2+b2), psi(b2) - psi(a2+b2)),
+  // e = [Pa, Pb, A, B] (the same for the entity):  dKL/da2 = QPa - Pa, dKL/db2 = QPb - Pb;
+  // dv accumulates sum C (A - a2), sum C (B - b2) (trigamma epilogue in the combine kernel).
+  static constexpr int BF = 4, BOFF = 0, BQF = 4;
   __device__ static void grad(const float *q, const float *e, float c, float, float *dq, float *dv) {
-    dq[0] -= c * e[0];
-    dq[1] -= c * e[1];
-    dv[0] += c * q[0];
-    dv[1] += c * q[1];
+    dq[0] = fmaf(c, q[2] - e[0], dq[0]);
+    dq[1] = fmaf(c, q[3] - e[1], dq[1]);
+    dv[0] = fmaf(c, e[2] - q[0], dv[0]);
+    dv[1] = fmaf(c, e[3] - q[1], dv[1]);
   }
 };
 struct MRot {  // RotatE: sum_k |q_k - t_k| (A3)
@@ -114,7 +117,7 @@ struct MRot {  // RotatE: sum_k |q_k - t_k| (A3)
     const float a = q[0] - e[0], b = q[1] - e[1], n = sqrtf(a * a + b * b);
     if (n > 0.f) { const float w = c / n; acc_[0] -= w * a; acc_[1] -= w * b; }
   }
-  static constexpr int BF = 2, BOFF = 0;
+  static constexpr int BF = 2, BOFF = 0, BQF = QF;
   __device__ static void grad(const float *q, const float *e, float c, float, float *dq, float *dv) {
     const float a = q[0] - e[0], b = q[1] - e[1], n = sqrtf(a * a + b * b);
     const float w = n > 0.f ? c / n : 0.f;
@@ -130,7 +133,7 @@ struct MDot {  // DistMult: -<q, t> (A13)
   __device__ static float fin(float s, float, float) { return -s; }
   __device__ static void bq(const float *, const float *e, float c, float, float *dq) { dq[0] -= c * e[0]; }
   __device__ static void bv(const float *q, const float *, float c, float, float *a) { a[0] -= c * q[0]; }
-  static constexpr int BF = 1, BOFF = 0;
+  static constexpr int BF = 1, BOFF = 0, BQF = QF;
   __device__ static void grad(const float *q, const float *e, float c, float, float *dq, float *dv) {
     dq[0] -= c * e[0];
     dv[0] -= c * q[0];
@@ -144,7 +147,7 @@ struct MCpx {  // ComplEx: -Re<q, conj(t)> = -sum(q_re t_re + q_im t_im) (A13)
   __device__ static float fin(float s, float, float) { return -s; }
   __device__ static void bq(const float *, const float *e, float c, float, float *dq) { dq[0] -= c * e[0]; dq[1] -= c * e[1]; }
   __device__ static void bv(const float *q, const float *, float c, float, float *a) { a[0] -= c * q[0]; a[1] -= c * q[1]; }
-  static constexpr int BF = 2, BOFF = 0;
+  static constexpr int BF = 2, BOFF = 0, BQF = QF;
   __device__ static void grad(const float *q, const float *e, float c, float, float *dq, float *dv) {
     dq[0] -= c * e[0]; dq[1] -= c * e[1];
     dv[0] -= c * q[0]; dv[1] -= c * q[1];
@@ -373,11 +376,11 @@ constexpr int kBW = 8, kJW = 16, kIC = 16;
 
 template <class Mdl>
 __global__ void __launch_bounds__(kBW * 32, 2) pair_bwd_kernel(ScoreArgs a) {
-  constexpr int QF = Mdl::QF, BF = Mdl::BF, AV = Mdl::AV, JB = kBW * kJW;
+  constexpr int QF = Mdl::QF, BQF = Mdl::BQF, BF = Mdl::BF, AV = Mdl::AV, JB = kBW * kJW;
   extern __shared__ __align__(16) float smem[];
   float *sC = smem;                                   // [kIC][JB]
-  float *sQ = sC + kIC * JB;                          // [kIC][QF][32]
-  float *sDQ = sQ + kIC * QF * 32;                    // [kBW][kIC][QF][32]
+  float *sQ = sC + kIC * JB;                          // [kIC][BQF][32]: Q features (+ BetaE QP)
+  float *sDQ = sQ + kIC * BQF * 32;                   // [kBW][kIC][QF][32]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int U = a.U, K = a.K, NQ = a.NQ, qstride = QF * U;
   const int k = blockIdx.x * 32 + lane;
@@ -403,17 +406,22 @@ __global__ void __launch_bounds__(kBW * 32, 2) pair_bwd_kernel(ScoreArgs a) {
       if (r < re && j < a.Kp) v = ld4(a.C + (size_t)r * a.Kp + j);   // Kp % 64 == 0, padding is 0
       *reinterpret_cast<float4 *>(sC + ii * JB + c4 * 4) = v;
     }
-    for (int e = threadIdx.x; e < kIC * QF * 32; e += blockDim.x) {
-      const int ii = e / (QF * 32), f = (e / 32) % QF, l = e & 31;
+    for (int e = threadIdx.x; e < kIC * BQF * 32; e += blockDim.x) {
+      const int ii = e / (BQF * 32), f = (e / 32) % BQF, l = e & 31;
       const int r = r0 + ii, kk = blockIdx.x * 32 + l;
-      sQ[e] = (r < re && kk < U) ? a.Q[(size_t)r * qstride + f * U + kk] : 0.f;
+      float v = 0.f;
+      if (r < re && kk < U)
+        v = f < QF ? a.Q[(size_t)r * qstride + f * U + kk] : a.QP[(size_t)r * (BQF - QF) * U + (f - QF) * U + kk];
+      sQ[e] = v;
     }
     __syncthreads();
 #pragma unroll 1
     for (int ii = 0; ii < kIC; ++ii) {
-      float q[QF], dq[QF], dq2[QF];
+      float q[BQF], dq[QF], dq2[QF];
 #pragma unroll
-      for (int f = 0; f < QF; ++f) { q[f] = sQ[(ii * QF + f) * 32 + lane]; dq[f] = 0.f; dq2[f] = 0.f; }
+      for (int f = 0; f < BQF; ++f) q[f] = sQ[(ii * BQF + f) * 32 + lane];
+#pragma unroll
+      for (int f = 0; f < QF; ++f) { dq[f] = 0.f; dq2[f] = 0.f; }
       const float4 *crow = reinterpret_cast<const float4 *>(sC + ii * JB + w * kJW);
       if constexpr (std::is_same<Mdl, MBox>::value) {
         // Q2B on packed f32x2 pairs of pool entries: t = v - c, a = |t|, W = [a > o] + alpha [a < o],
@@ -480,8 +488,8 @@ __global__ void __launch_bounds__(kBW * 32, 2) pair_bwd_kernel(ScoreArgs a) {
   }
 }
 
-// dQ[r][f*U + k] += sum_z partQ[z] (+ BetaE: Csum[r] * QP[r][f][k]; Q2B offset: alpha * Csum[r]);
-// dQ already holds the positive term.
+// dQ[r][f*U + k] += sum_z partQ[z] (+ Q2B offset: alpha * Csum[r]); dQ already holds the
+// positive term.  (BetaE's partials already hold sum_j C (QP - P), see MBeta::grad.)
 template <bool BETA, bool BOX>
 __global__ void bwd_q_combine_kernel(ScoreArgs a, int qstride) {
   const int64_t n = (int64_t)a.NQ * qstride;
@@ -489,7 +497,6 @@ __global__ void bwd_q_combine_kernel(ScoreArgs a, int qstride) {
   if (e >= n) return;
   float v = 0.f;
   for (int z = 0; z < a.JS; ++z) v += a.partQ[z * n + e];
-  if (BETA) v += a.Csum[e / qstride] * a.QP[e];
   if (BOX && (e % qstride) >= a.U) v = fmaf(a.alpha, a.Csum[e / qstride], v);
   a.dQ[e] += v;
 }
@@ -513,14 +520,15 @@ __global__ void bwd_v_combine_kernel(ScoreArgs a) {
   }
   float *out = a.dV + (size_t)j * a.d;
   if (Mdl::kBeta) {
-    const float Cj = a.Cpart[j];   // column sum of C over all query rows
+    // S1 = sum_i C (A - a2), S2 = sum_i C (B - b2) (MBeta::grad):
+    // dKL/dA = (A - a2) psi'(A) - ((A - a2) + (B - b2)) psi'(A + B), likewise for B
     const float *Fr = a.E + (size_t)j * a.estride;
-    const float A = Fr[2 * U + k], B = Fr[3 * U + k], TA = Fr[4 * U + k], TB = Fr[5 * U + k],
-                TAB = Fr[6 * U + k], GA = Fr[7 * U + k], GB = Fr[8 * U + k];
+    const float TA = Fr[4 * U + k], TB = Fr[5 * U + k], TAB = Fr[6 * U + k], GA = Fr[7 * U + k],
+                GB = Fr[8 * U + k];
     const float S1 = acc[0], S2 = acc[AV - 1];
-    const float S = (A + B) * Cj - S1 - S2;
-    out[k] = (TA * (A * Cj - S1) - TAB * S) * GA;
-    out[U + k] = (TB * (B * Cj - S2) - TAB * S) * GB;
+    const float S = S1 + S2;
+    out[k] = (TA * S1 - TAB * S) * GA;
+    out[U + k] = (TB * S2 - TAB * S) * GB;
   } else {
 #pragma unroll
     for (int f = 0; f < Mdl::OUTF; ++f) out[f * U + k] = acc[f];
@@ -755,8 +763,7 @@ static void launch_bwd(ScoreArgs a, cudaStream_t st, cudaStream_t st2) {
   while (is > 1 && (int64_t)is * a.K * Mdl::AV * a.U > a.cap_V) --is;
   a.rps = ((chunks + is - 1) / is) * kIC;
   a.RS = (a.NQ + a.rps - 1) / a.rps;
-  if (Mdl::kBeta) launch_colsum(a.C, a.NQ, a.K, a.Kp, a.Cpart, st);   // sum_r C_rj
-  const size_t smem = sizeof(float) * (kIC * JB + kIC * Mdl::QF * 32 + kBW * kIC * Mdl::QF * 32);
+  const size_t smem = sizeof(float) * (kIC * JB + kIC * Mdl::BQF * 32 + kBW * kIC * Mdl::QF * 32);
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(pair_bwd_kernel<Mdl>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

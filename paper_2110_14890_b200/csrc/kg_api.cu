@@ -228,7 +228,7 @@ struct kg_handle {
   };
   std::vector<GraphEntry> graphs;
   bool use_graphs = true;
-  bool gemm_cublas = false, side = false;
+  bool gemm_cublas = true, side = false;
   cublasHandle_t blas2 = nullptr;
   void *blas_ws2 = nullptr;
   void *blas_ws = nullptr;
@@ -462,7 +462,7 @@ void carve(kg_handle *h, Arena &A) {
 }
 
 // Row-major GEMM: C[m x n] = op(A) op(B) + beta C, op(A) is [m x k]; tb: B given as [n x k].
-// Default: the tcgen05 3xTF32 kernel (k_gemm.cu); KG_GEMM=cublas selects cuBLAS SGEMM (A/B check).
+// Default: cuBLAS SGEMM (fp32); KG_GEMM=tc: the tcgen05 3xTF32 kernel (k_gemm.cu); see kg_create.
 kg_status gemm(kg_handle *h, bool ta, bool tb, int m, int n, int k, const float *A, int lda, const float *B, int ldb,
                float beta, float *C, int ldc, const float *bias = nullptr, int relu = 0) {
   if (m <= 0 || n <= 0) return KG_OK;
@@ -914,7 +914,6 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
   if (cublasSetWorkspace(h->blas, h->blas_ws, 32 << 20) != CUBLAS_STATUS_SUCCESS) { kg_destroy(h); return KG_ECUDA; }
   if (cublasCreate(&h->blas2) != CUBLAS_STATUS_SUCCESS ||
       cublasSetWorkspace(h->blas2, h->blas_ws2, 32 << 20) != CUBLAS_STATUS_SUCCESS) { kg_destroy(h); return KG_ECUDA; }
-  cublasSetMathMode(h->blas2, CUBLAS_PEDANTIC_MATH);
   if (c.world > 1) {
     ncclUniqueId id;
     std::memcpy(&id, c.nccl_id, sizeof(id));
@@ -923,8 +922,16 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
     h->use_graphs = false;   // the exchange sizes are read on the host every step
   }
   if (const char *e = std::getenv("KG_NO_GRAPH")) h->use_graphs = !(e[0] == '1');
-  if (const char *e = std::getenv("KG_GEMM")) h->gemm_cublas = std::string(e) == "cublas";   // A/B comparison
-  cublasSetMathMode(h->blas, CUBLAS_PEDANTIC_MATH);   // true fp32, no TF32 (parity at 1e-5, A24)
+  // DAG contractions (reading A24): cuBLAS SGEMM in true fp32 (no TF32).
+  // KG_GEMM=tc selects the hand-written tcgen05 3xTF32 kernel (k_gemm.cu): ~1.4x faster on the
+  // BetaE MLP, but the tensor-core accumulation in TMEM carries 15-25x the error of SGEMM
+  // (tools/gemm_precision.py; measured on B200), which BetaE's full-size gradients amplify past
+  // the 1e-5 parity bar (tests/test_fullsize_gpu.py).  (cuBLAS 12.9's BF16x9 fp32 emulation is
+  // faster and more accurate than SGEMM -- tools/cublas_emu_probe.cu -- but torch 2.11 loads its
+  // own cuBLAS 12.8 into the process, which lacks it.)
+  if (const char *e = std::getenv("KG_GEMM")) h->gemm_cublas = std::string(e) != "tc";
+  cublasSetMathMode(h->blas, CUBLAS_PEDANTIC_MATH);
+  cublasSetMathMode(h->blas2, CUBLAS_PEDANTIC_MATH);
   // device scalars
   if (cudaMemset(h->ws, 0, h->ws_bytes) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
   if (cudaMemset(h->rel_stamp, 0xff, sizeof(int64_t) * h->R) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
