@@ -922,14 +922,21 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
     h->use_graphs = false;   // the exchange sizes are read on the host every step
   }
   if (const char *e = std::getenv("KG_NO_GRAPH")) h->use_graphs = !(e[0] == '1');
-  // DAG contractions (reading A24): cuBLAS SGEMM in true fp32 (no TF32).
-  // KG_GEMM=tc selects the hand-written tcgen05 3xTF32 kernel (k_gemm.cu): ~1.4x faster on the
-  // BetaE MLP, but the tensor-core accumulation in TMEM carries 15-25x the error of SGEMM
-  // (tools/gemm_precision.py; measured on B200), which BetaE's full-size gradients amplify past
-  // the 1e-5 parity bar (tests/test_fullsize_gpu.py).  (cuBLAS 12.9's BF16x9 fp32 emulation is
+  // DAG contractions (reading A24).  The hand-written tcgen05 3xTF32 kernel
+  // (k_gemm.cu) runs the d x d layers of GQE / Q2B / the -m variants (DeepSet, attention and
+  // their gradients; +5.5% C5-q2b q/s over SGEMM); BetaE's projection MLP and attention go to
+  // cuBLAS SGEMM in true fp32: the tensor-core accumulation in TMEM carries 15-25x SGEMM's error
+  // (tools/gemm_precision.py, measured on B200), and BetaE's full-size gradients (K = 800 / 1600
+  // contractions feeding digamma differences) amplify it past the 1e-5 parity bar, while the
+  // other models stay inside it (tests/test_fullsize_gpu.py, every kind at full size).
+  // KG_GEMM=tc / sgemm force one path for A/B checks.  (cuBLAS 12.9's BF16x9 fp32 emulation is
   // faster and more accurate than SGEMM -- tools/cublas_emu_probe.cu -- but torch 2.11 loads its
   // own cuBLAS 12.8 into the process, which lacks it.)
-  if (const char *e = std::getenv("KG_GEMM")) h->gemm_cublas = std::string(e) != "tc";
+  h->gemm_cublas = h->kind == KG_BETAE;
+  if (const char *e = std::getenv("KG_GEMM")) {
+    if (std::string(e) == "tc") h->gemm_cublas = false;
+    if (std::string(e) == "sgemm") h->gemm_cublas = true;
+  }
   cublasSetMathMode(h->blas, CUBLAS_PEDANTIC_MATH);
   cublasSetMathMode(h->blas2, CUBLAS_PEDANTIC_MATH);
   // device scalars

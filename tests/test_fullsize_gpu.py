@@ -182,6 +182,7 @@ def assert_close_allow(x, ref, what, n_allow, jump):
 
 
 CASES = [("C2", "ip", None), ("C2", "up", None), ("C2", "3i", "gqe"), ("C2", "pi", "distmult-m"),
+         ("C2", "ip", "complex-m"), ("C2", "2u", "rotate-m"),
          ("C3-rotate", "1p", None), ("C3-complex", "1p", None), ("C4", "2i", None), ("C4", "pni", None),
          ("C4", "up", None), ("C5-q2b", "pi", None), ("C5-q2b", "2u", None), ("C5-betae", "ip", None)]
 
