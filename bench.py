@@ -116,14 +116,21 @@ def stage_work(cfg, M, K, structure, U, d):
     rel_elems = sum(int(np.prod(s)) for n, (o, s) in offs.items() if n.startswith("rel"))
     w_elems = size - rel_elems
     L = M * kggen.N_ANCHORS[structure] + M + K
-    return {
+    work = {}
+    if cfg.kind == "betae":
+        # DAG forward + backward: the projection MLP [q; r] (2d) -> H -> H -> d on every projection
+        # row (DNF: 'up' projects both disjuncts), backward = 2x forward (SGEMM, fp32 CUDA cores)
+        n_proj = kggen.N_RELS[structure] + (1 if structure == "up" else 0)
+        H = cfg.hidden
+        work["dag"] = ("alu", 3.0 * 2.0 * (2 * cfg.dim * H + H * H + H * cfg.dim) * n_proj * M, "FLOP")
+    return dict(work, **{
         # scoring fwd+bwd: M*nout x K x units pair-units, fwd + 2x bwd
         "scoring": ("alu", 3.0 * pair_flops_per_unit(cfg.kind) * M * nout * K * units, "FLOP"),
         # dense Adam: read p, m, v (+ g of the weights) and write p, m, v of every theta_D element (A17)
         "dense_adam": ("hbm", 24.0 * size + 4.0 * w_elems, "B"),
         # sparse Adam: p, m, v read + write of the U touched rows + the L occurrence gradient rows read
         "sparse_adam": ("hbm", 24.0 * U * d + 4.0 * L * d, "B"),
-    }
+    })
 
 
 # ------------------------------------------------------------------ our arm
@@ -216,6 +223,8 @@ def run_ours(args, world, rank, local):
     # sparse update: its own duration is stage 8; stage 6 is only what it adds to the critical path
     cand = {"scoring": (stage[2] + stage[3]), "dense_adam": stage[8] if stage[8] > 0 else stage[6],
             "sparse_adam": stage[5]}
+    if "dag" in work:
+        cand["dag"] = stage[1] + stage[4]
     dom = max(cand, key=cand.get)
     bound, amount, unit = work[dom]
     per_launch = amount / n_prof

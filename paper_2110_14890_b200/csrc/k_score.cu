@@ -104,9 +104,11 @@ struct MRot {  // RotatE: sum_k |q_k - t_k| (A3)
   static constexpr bool kRowAlpha = false;
   static constexpr int QF = 2, EF = 2, EOFF = 0, BQ_EF = 2, BQ_EOFF = 0, BV_EF = 2, BV_EOFF = 0, AV = 2, OUTF = 2;
   static constexpr bool kL2 = false, kBeta = false;
+  // |z| = s * rsqrt(s), s = |z|^2 (MUFU.RSQ, <= 2 ulp: ~3e-7 relative per unit, far inside the
+  // 1e-5 bar; the IEEE sqrtf / division sequences made RotatE's pair kernels 3x more instructions)
   __device__ static float acc(const float *q, const float *e, float) {
-    const float a = q[0] - e[0], b = q[1] - e[1];
-    return sqrtf(a * a + b * b);
+    const float a = q[0] - e[0], b = q[1] - e[1], s = fmaf(a, a, b * b);
+    return s * rsqrtf(fmaxf(s, 1e-30f));
   }
   __device__ static float fin(float s, float, float) { return s; }
   __device__ static void bq(const float *q, const float *e, float c, float, float *dq) {
@@ -119,8 +121,8 @@ struct MRot {  // RotatE: sum_k |q_k - t_k| (A3)
   }
   static constexpr int BF = 2, BOFF = 0, BQF = QF;
   __device__ static void grad(const float *q, const float *e, float c, float, float *dq, float *dv) {
-    const float a = q[0] - e[0], b = q[1] - e[1], n = sqrtf(a * a + b * b);
-    const float w = n > 0.f ? c / n : 0.f;
+    const float a = q[0] - e[0], b = q[1] - e[1], s = fmaf(a, a, b * b);
+    const float w = s > 0.f ? c * rsqrtf(s) : 0.f;                  // c / |z| (A19: 0 at z = 0)
     dq[0] += w * a; dq[1] += w * b;
     dv[0] -= w * a; dv[1] -= w * b;
   }
