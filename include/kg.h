@@ -129,10 +129,12 @@ typedef struct {
   float stage_ms[10];    /* device time per stage when stage timing is on (kg_set_apply bit 2), else 0:
                             0 ingest + dedup, 1 DAG forward, 2 scoring forward + Eq. 1, 3 scoring backward,
                             4 DAG backward, 5 sparse update (segment reduce + sparse Adam), 6 what the dense
-                            update adds after the sparse one, 7 whole step, 8 the dense update path itself
-                            (relation reduce + dense Adam over theta_D, on a second stream concurrently with
-                            stage 5; world = 1), 9 reserved (0).  With world > 1 stage 5 also holds the
-                            relation reduce and 6 the all-reduce + dense Adam, and 8 is 0. */
+                            update adds after the sparse one, 7 whole step; world = 1 only (else 0):
+                            8 the late dense path (relation reduce + Adam of the used relation rows and of
+                            the operator weights, on a second stream concurrently with stage 5), 9 the early
+                            dense path (Adam of the relation rows the step does not use, g = 0, on a third
+                            stream from the end of stage 2, concurrently with stages 3-5).  With world > 1
+                            stage 5 also holds the relation reduce and 6 the all-reduce + dense Adam. */
 } kg_step_info;
 
 typedef struct kg_handle kg_handle;   /* opaque; one per (process, device) */

@@ -233,39 +233,69 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t n, FastDiv f) { return (uint32
 // Relation tables: flat stream over nseg * R rows of w4 float4; the gradient of row r
 // of segment s is RGU[rel_seg[r]][s*w4 + c] when relation r was used by this step
 // (rel_stamp[r] == stamp), else 0 (A17).  kE float4 per thread, loads issued first.
+// untouched_only: update only the relation rows this step does not use (g = 0, A17) -- they
+// depend on no gradient of the step, so the update runs early, concurrently with the
+// ALU-bound scoring; the touched rows follow in dense_adam_rel_touched_kernel.
 __global__ void __launch_bounds__(256) dense_adam_rel_kernel(float4 *p, float4 *m, float4 *v, int n4, FastDiv fw4,
                                                              int R, int nseg, const float *RGU,
                                                              const int32_t *rel_seg, const int64_t *rel_stamp,
                                                              const int64_t *stamp_dev, const float *lr_dev,
-                                                             AdamHyper hy, const float *bc, const int *flags) {
+                                                             AdamHyper hy, const float *bc, const int *flags,
+                                                             int untouched_only) {
   if (flags[0]) return;
   const float lr1 = *lr_dev * bc[0], ibc2 = bc[1];
   const int64_t stamp = *stamp_dev;
   const int w4 = (int)fw4.d;
   const int base = blockIdx.x * (256 * kE) + threadIdx.x;
   float4 P[kE], Mm[kE], V[kE], G[kE];
+  bool skip[kE];
 #pragma unroll
   for (int k = 0; k < kE; ++k) {
     const int e = base + k * 256;
-    if (e >= n4) continue;
+    skip[k] = e >= n4;
+    if (skip[k]) continue;
+    const int row = (int)fdiv((uint32_t)e, fw4), c4 = e - row * w4;
+    const int sidx = row >= R ? 1 : 0, r = row - sidx * R;
+    const bool used = rel_stamp[r] == stamp;
+    skip[k] = untouched_only && used;
+    if (skip[k]) continue;
     P[k] = __ldcs(p + e);
     Mm[k] = __ldcs(m + e);
     V[k] = __ldcs(v + e);
-    const int row = (int)fdiv((uint32_t)e, fw4), c4 = e - row * w4;
-    const int sidx = row >= R ? 1 : 0, r = row - sidx * R;
     G[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (rel_stamp[r] == stamp)
-      G[k] = reinterpret_cast<const float4 *>(RGU)[(int64_t)rel_seg[r] * nseg * w4 + sidx * w4 + c4];
+    if (used) G[k] = reinterpret_cast<const float4 *>(RGU)[(int64_t)rel_seg[r] * nseg * w4 + sidx * w4 + c4];
   }
 #pragma unroll
   for (int k = 0; k < kE; ++k) {
     const int e = base + k * 256;
-    if (e >= n4) continue;
+    if (skip[k]) continue;
     adam4(P[k], Mm[k], V[k], G[k], lr1, hy, ibc2);
     __stcs(p + e, P[k]);
     __stcs(m + e, Mm[k]);
     __stcs(v + e, V[k]);
   }
+}
+
+// The relation rows used by this step: row runiq[u] of each of the nseg segments, gradient
+// RGU[u][s][c] (the relation-occurrence reduce), u < *rU.
+__global__ void __launch_bounds__(256) dense_adam_rel_touched_kernel(float4 *p, float4 *m, float4 *v, int R, int w4,
+                                                                     int nseg, const float *RGU,
+                                                                     const int64_t *runiq, const int32_t *rU,
+                                                                     const float *lr_dev, AdamHyper hy,
+                                                                     const float *bc, const int *flags) {
+  if (flags[0]) return;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int per = nseg * w4;
+  const int u = (int)(e / per);
+  if (u >= *rU) return;
+  const int rem = (int)(e - (int64_t)u * per), s = rem / w4, c4 = rem - s * w4;
+  const int64_t idx = ((int64_t)s * R + runiq[u]) * w4 + c4;
+  const float lr1 = *lr_dev * bc[0], ibc2 = bc[1];
+  float4 P = p[idx], Mm = m[idx], V = v[idx];
+  adam4(P, Mm, V, reinterpret_cast<const float4 *>(RGU)[e], lr1, hy, ibc2);
+  p[idx] = P;
+  m[idx] = Mm;
+  v[idx] = V;
 }
 
 // Operator weights: flat stream, kE float4 per thread, loads issued first.
@@ -299,13 +329,22 @@ __global__ void __launch_bounds__(256) dense_adam_kernel(float4 *p, float4 *m, f
 void launch_dense_adam_rel(float *p, float *m, float *v, int R, int width, int nseg, const float *RGU,
                            const int32_t *rel_seg, const int64_t *rel_stamp, const int64_t *stamp, const float *lr,
                            double beta1, double beta2, double eps, const float *bc, const int *flags,
-                           cudaStream_t st) {
+                           cudaStream_t st, int untouched_only) {
   const int n4 = nseg * R * (width / 4);
   if (n4 <= 0) return;
   { dense_adam_rel_kernel<<<(n4 + 256 * kE - 1) / (256 * kE), 256, 0, st>>>(
         reinterpret_cast<float4 *>(p), reinterpret_cast<float4 *>(m), reinterpret_cast<float4 *>(v), n4,
         fastdiv((uint32_t)(width / 4)), R, nseg, RGU, rel_seg, rel_stamp, stamp, lr, hyper(beta1, beta2, eps), bc,
-        flags); ++g_launches; }
+        flags, untouched_only); ++g_launches; }
+}
+void launch_dense_adam_rel_touched(float *p, float *m, float *v, int R, int width, int nseg, const float *RGU,
+                                   const int64_t *runiq, const int32_t *rU, int Lr, const float *lr, double beta1,
+                                   double beta2, double eps, const float *bc, const int *flags, cudaStream_t st) {
+  const int64_t n = (int64_t)Lr * nseg * (width / 4);
+  if (n <= 0) return;
+  { dense_adam_rel_touched_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(
+        reinterpret_cast<float4 *>(p), reinterpret_cast<float4 *>(m), reinterpret_cast<float4 *>(v), R, width / 4,
+        nseg, RGU, runiq, rU, lr, hyper(beta1, beta2, eps), bc, flags); ++g_launches; }
 }
 
 void launch_dense_adam(float *p, float *m, float *v, const float *g, int64_t n, const float *lr, double beta1,

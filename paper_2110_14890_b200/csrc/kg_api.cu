@@ -217,7 +217,8 @@ struct kg_handle {
   int64_t gsP_cap = 0;
   float *Dpart = nullptr, *partQ = nullptr, *partV = nullptr, *Cpart = nullptr, *Csum = nullptr;
   int64_t cap_D = 0, cap_Q = 0, cap_V = 0;
-  cudaStream_t st2 = nullptr, st_cap = nullptr, st3 = nullptr;
+  cudaStream_t st2 = nullptr, st_cap = nullptr, st3 = nullptr, st4 = nullptr;
+  cudaEvent_t ev_rel = nullptr, ev_loss = nullptr, ev_early = nullptr;
   cudaEvent_t ev_i1 = nullptr, ev_i2 = nullptr;   // fork / join of the two Q2B intersection branches
   cudaEvent_t ev_fork = nullptr, ev_fork2 = nullptr, ev_join = nullptr;
   float *lr_dev = nullptr;
@@ -258,7 +259,7 @@ struct kg_handle {
 
   int64_t stamp = 0;
   int apply = 1, keep_grads = 0, timing = 0;
-  cudaEvent_t sev[10] = {};
+  cudaEvent_t sev[12] = {};
   bool side_timed = false;
   int64_t launches0 = 0;
   int last_kernels = 0, last_gemms = 0, gemm_count = 0;
@@ -502,6 +503,12 @@ struct OnStream {
     h->side = false;
   }
 };
+// the lowest stream priority (the early dense-Adam stream yields the SMs to the scoring kernels)
+int kLowPriority() {
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  return lo;
+}
 kg_status fork(kg_handle *h, cudaStream_t from, cudaStream_t to) {
   CK(cudaEventRecord(h->ev_i1, from));
   CK(cudaStreamWaitEvent(to, h->ev_i1, 0));
@@ -835,7 +842,10 @@ kg_status read_result(kg_handle *h, kg_step_info *info) {
     if (h->timing) {
       for (int i = 0; i < 7; ++i) CK(cudaEventElapsedTime(&info->stage_ms[i], h->sev[i], h->sev[i + 1]));
       CK(cudaEventElapsedTime(&info->stage_ms[7], h->sev[0], h->sev[7]));
-      if (h->side_timed) CK(cudaEventElapsedTime(&info->stage_ms[8], h->sev[8], h->sev[9]));
+      if (h->side_timed) {
+        CK(cudaEventElapsedTime(&info->stage_ms[8], h->sev[8], h->sev[9]));
+        if (h->apply) CK(cudaEventElapsedTime(&info->stage_ms[9], h->sev[10], h->sev[11]));
+      }
     }
   }
   if (h->hout->flags[1]) return fail(h, KG_EINVAL, "an id or relation of the (device) batch was out of range; step not applied");
@@ -900,12 +910,16 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
   if (cudaMallocHost(&h->hout, sizeof(kg_handle::HostOut)) != cudaSuccess) { kg_destroy(h); return KG_ENOMEM; }
   std::memset(h->hout, 0, sizeof(kg_handle::HostOut));
   if (cudaEventCreateWithFlags(&h->step_done, cudaEventDisableTiming) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
-  for (int i = 0; i < 10; ++i)
+  for (int i = 0; i < 12; ++i)
     if (cudaEventCreate(&h->sev[i]) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
   if (cublasCreate(&h->blas) != CUBLAS_STATUS_SUCCESS) { kg_destroy(h); return KG_ECUDA; }
   if (cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->st_cap, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->st3, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&h->st4, cudaStreamNonBlocking, kLowPriority()) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_rel, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_loss, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_early, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_i1, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_i2, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork2, cudaEventDisableTiming) != cudaSuccess ||
@@ -1037,6 +1051,7 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   CK(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
   launch_dedup(h->ids, nullptr, L, h->ent_bits, h->uniq, h->inv, h->perm, h->seg, h->Udev, h->st2);
   launch_dedup(nullptr, h->rocc, Lr, h->rel_bits, h->runiq, h->rinv, h->rperm, h->rseg, h->rU, h->st2);
+  CK(cudaEventRecord(h->ev_rel, h->st2));
 
   // a4-a7: fused gather + DAG forward
   mark(h, 1);
@@ -1072,6 +1087,23 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   launch_loss_finalize(h->loss_pos, h->loss_part, M, njt, 1.0 / ((double)M * h->world), h->loss_dev, h->flags,
                        h->t_dev, h->bc, h->cfg.beta1, h->cfg.beta2, h->apply, st);
   mark(h, 3);
+  // a14 (first part): the relation rows this step does not use take their Adam update with
+  // g = 0 (A17) as soon as the step's fate (flags, bias corrections) is known -- a 300 MB
+  // stream overlapped with the ALU-bound scoring backward; the used rows follow at the end.
+  if (h->apply) {
+    CK(cudaEventRecord(h->ev_loss, st));
+    CK(cudaStreamWaitEvent(h->st4, h->ev_loss, 0));
+    CK(cudaStreamWaitEvent(h->st4, h->ev_rel, 0));
+    mark(h, 10, h->st4);
+    launch_rel_stamp(h->runiq, h->rU, Lr, h->rel_seg_map, h->rel_stamp, h->stamp_dev, h->st4);
+    const Seg &r = h->segs[0];
+    const int nseg = h->kind == KG_Q2B ? 2 : 1;
+    launch_dense_adam_rel(h->t.dense + r.off, h->t.dense_m + r.off, h->t.dense_v + r.off, h->R, r.cols, nseg,
+                          h->RGU, h->rel_seg_map, h->rel_stamp, h->stamp_dev, h->lr_dev, h->cfg.beta1,
+                          h->cfg.beta2, h->cfg.eps, h->bc, h->flags, h->st4, /*untouched_only=*/1);
+    mark(h, 11, h->st4);
+    CK(cudaEventRecord(h->ev_early, h->st4));
+  }
   if (K > 0) {
     // dV (pool rows) on the side stream, concurrently with dQ and the DAG backward
     CK(cudaEventRecord(h->ev_fork2, st));
@@ -1102,17 +1134,16 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
     cudaStream_t s2 = h->st2;
     mark(h, 8, s2);
     launch_rel_reduce(h->rseg, h->rperm, h->rinv, h->rU, Lr, h->RG, h->PSr, h->dr, h->RGU, s2);
-    launch_rel_stamp(h->runiq, h->rU, Lr, h->rel_seg_map, h->rel_stamp, h->stamp_dev, s2);
     if (h->apply) {
       const double b1 = h->cfg.beta1, b2 = h->cfg.beta2, eps = h->cfg.eps;
       const float *lr = h->lr_dev;
+      CK(cudaStreamWaitEvent(s2, h->ev_early, 0));
       {
-        // relation tables: segs[0] (and segs[1] for Q2B: rel_offset right after rel_center)
+        // the relation rows used by this step: segs[0] (and segs[1] for Q2B: rel_offset right after)
         const Seg &r = h->segs[0];
         const int nseg = h->kind == KG_Q2B ? 2 : 1;
-        launch_dense_adam_rel(h->t.dense + r.off, h->t.dense_m + r.off, h->t.dense_v + r.off, h->R, r.cols, nseg,
-                              h->RGU, h->rel_seg_map, h->rel_stamp, h->stamp_dev, lr, b1, b2, eps, h->bc, h->flags,
-                              s2);
+        launch_dense_adam_rel_touched(h->t.dense + r.off, h->t.dense_m + r.off, h->t.dense_v + r.off, h->R, r.cols,
+                                      nseg, h->RGU, h->runiq, h->rU, Lr, lr, b1, b2, eps, h->bc, h->flags, s2);
       }
       launch_dense_adam(h->t.dense + h->w_off, h->t.dense_m + h->w_off, h->t.dense_v + h->w_off, h->gdense,
                         h->dense_size - h->w_off, lr, b1, b2, eps, h->bc, h->flags, s2);
@@ -1637,6 +1668,7 @@ void kg_destroy(kg_handle *h) {
   if (h->st2) { cudaStreamSynchronize(h->st2); cudaStreamDestroy(h->st2); }
   if (h->st_cap) cudaStreamDestroy(h->st_cap);
   if (h->st3) { cudaStreamSynchronize(h->st3); cudaStreamDestroy(h->st3); }
+  if (h->st4) { cudaStreamSynchronize(h->st4); cudaStreamDestroy(h->st4); }
   if (h->ev_i1) cudaEventDestroy(h->ev_i1);
   if (h->ev_i2) cudaEventDestroy(h->ev_i2);
   for (auto &g : h->graphs) cudaGraphExecDestroy(g.exec);
@@ -1649,8 +1681,11 @@ void kg_destroy(kg_handle *h) {
   }
   if (h->hout) cudaFreeHost(h->hout);
   if (h->step_done) cudaEventDestroy(h->step_done);
-  for (int i = 0; i < 10; ++i)
+  for (int i = 0; i < 12; ++i)
     if (h->sev[i]) cudaEventDestroy(h->sev[i]);
+  if (h->ev_rel) cudaEventDestroy(h->ev_rel);
+  if (h->ev_loss) cudaEventDestroy(h->ev_loss);
+  if (h->ev_early) cudaEventDestroy(h->ev_early);
   if (h->comm) nccl().CommDestroy(h->comm);
   if (h->h_counts) cudaFreeHost(h->h_counts);
   if (h->ws) cudaFree(h->ws);

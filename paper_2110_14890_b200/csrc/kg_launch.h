@@ -75,7 +75,10 @@ void launch_rel_stamp(const int64_t *uniq_rel, const int32_t *U_dev, int Lmax, i
 void launch_dense_adam_rel(float *p, float *m, float *v, int R, int width, int nseg, const float *RGU,
                            const int32_t *rel_seg, const int64_t *rel_stamp, const int64_t *stamp, const float *lr,
                            double beta1, double beta2, double eps, const float *bc, const int *flags,
-                           cudaStream_t st);
+                           cudaStream_t st, int untouched_only = 0);
+void launch_dense_adam_rel_touched(float *p, float *m, float *v, int R, int width, int nseg, const float *RGU,
+                                   const int64_t *runiq, const int32_t *rU, int Lr, const float *lr, double beta1,
+                                   double beta2, double eps, const float *bc, const int *flags, cudaStream_t st);
 void launch_dense_adam(float *p, float *m, float *v, const float *g, int64_t n, const float *lr, double beta1,
                        double beta2, double eps, const float *bc, const int *flags, cudaStream_t st);
 void launch_colsum(const float *X, int rows, int cols, int ld, float *out, cudaStream_t st);
