@@ -375,9 +375,12 @@ __global__ void __launch_bounds__(256) pair_epi_kernel(ScoreArgs a) {
 // (row, j-block of NW*JW).  blockIdx.z splits the rows; all partial sums are
 // added by the combine kernels in a fixed order (deterministic, no atomics).
 constexpr int kBW = 8, kJW = 16, kIC = 16;
+// resident CTAs per SM for the fused backward: 4 where the per-term state fits 64 registers
+// without spills (measured +4 % C5-q2b q/s over 2), 2 for the 2- / 4-feature models
+template <class Mdl> struct BwdOcc { static constexpr int v = (Mdl::BF == 1 && Mdl::AV == 1) ? 4 : 2; };
 
 template <class Mdl>
-__global__ void __launch_bounds__(kBW * 32, 2) pair_bwd_kernel(ScoreArgs a) {
+__global__ void __launch_bounds__(kBW * 32, BwdOcc<Mdl>::v) pair_bwd_kernel(ScoreArgs a) {
   constexpr int QF = Mdl::QF, BQF = Mdl::BQF, BF = Mdl::BF, AV = Mdl::AV, JB = kBW * kJW;
   extern __shared__ __align__(16) float smem[];
   float *sC = smem;                                   // [kIC][JB]
