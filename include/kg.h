@@ -219,7 +219,8 @@ kg_status kg_set_apply(kg_handle *h, int32_t flags);
 const char *kg_last_error(const kg_handle *h);
 
 /* Test hook: the tensor-core GEMM of the query-DAG contractions on device pointers,
- * C[M][N] (ldc) = beta*C + op(A) op(B)^T (+ bias[n]) (ReLU if relu), op(A) = [M][K], op(B) = [N][K];
+ * C[M][N] (ldc) = beta*C + op(A) op(B)^T (+ bias[n]) (ReLU if relu & 1), op(A) = [M][K], op(B) = [N][K];
+ * relu & 2 selects the drained (fp32-accurate) accumulation used for BetaE;
  * ta: A stored [K][lda] (else [M][lda]); tb: B stored [K][ldb] (else [N][ldb]); both layouts are
  * read in place by TMA.  tcgen05 kind::tf32 with a 3xTF32 split (fp32-level accuracy).  Needs
  * K >= 1, 16-byte aligned A / B and lda % 4 == ldb % 4 == 0 (else EINVAL).  Synchronises the stream. */

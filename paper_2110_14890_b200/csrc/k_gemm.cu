@@ -200,15 +200,23 @@ __device__ __forceinline__ void split_op(const uint8_t *raw, uint8_t *hi, uint8_
   }
 }
 
-template <int BN, bool AMN, bool BMN>
+// DRAIN (fp32-accurate mode, reading A24): the tensor cores accumulate only kDrainKB k-blocks
+// (K = 64: 24 MMAs) into one of two TMEM accumulators; the split warps then drain that chunk
+// into fp32 registers (round-to-nearest adds) while the MMA warp fills the other one.  The
+// error of the TMEM accumulation grows with the number of MMAs chained into one accumulator
+// (tools/gemm_precision.py: 15-25x SGEMM's at K = 800-1600); chunks of 24 bring it to SGEMM's.
+constexpr int kDrainKB = 4;
+template <int BN, bool AMN, bool BMN, bool DRAIN>
 __global__ void __launch_bounds__(G2T, 1)
     gemm_tf32x3_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
   using Cfg = G2Cfg<BN, AMN, BMN>;
   constexpr int S = Cfg::kStages;
+  constexpr int kCols = DRAIN ? 2 * BN : BN;                     // TMEM columns (power of 2 >= 32)
+  static_assert(!DRAIN || BN == 128, "the drained accumulator is held in registers for BN = 128");
   extern __shared__ uint8_t gsm_raw[];
   uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full_bar[S], conv_bar[S], empty_bar[S];
-  __shared__ __align__(8) uint64_t done_bar;
+  __shared__ __align__(8) uint64_t done_bar, acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * BN;
@@ -217,7 +225,7 @@ __global__ void __launch_bounds__(G2T, 1)
 
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)),
-                 "n"(BN));
+                 "n"(kCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
@@ -229,6 +237,10 @@ __global__ void __launch_bounds__(G2T, 1)
       mbar_init(&empty_bar[s], 1);
     }
     mbar_init(&done_bar, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 32 * G2CW);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -252,8 +264,12 @@ __global__ void __launch_bounds__(G2T, 1)
     if (lane == 0) {
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % S;
+        const int c = kb / kDrainKB;                      // DRAIN: chunk c -> accumulator c & 1
+        const bool chunk0 = DRAIN ? (kb % kDrainKB == 0) : (kb == 0);
+        if (DRAIN && chunk0 && c >= 2) mbar_wait(&acc_empty[c & 1], ((c >> 1) - 1) & 1);   // chunk c-2 drained
         mbar_wait(&conv_bar[s], (kb / S) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t tm = DRAIN ? tmem + (uint32_t)((c & 1) * BN) : tmem;
         const uint32_t st = su32(sm + s * Cfg::kStage);
         const uint32_t ah = AMN ? st + Cfg::oAhi : st, bh = BMN ? st + Cfg::oBhi : st + Cfg::kA;
         const uint32_t al = st + Cfg::oAlo, bl = st + Cfg::oBlo;
@@ -261,23 +277,50 @@ __global__ void __launch_bounds__(G2T, 1)
         for (int kk = 0; kk < G2K / 8; ++kk) {   // K = 8 tf32 per MMA
           const uint64_t dah = kmajor_desc(ah, kk), dal = kmajor_desc(al, kk);
           const uint64_t dbh = kmajor_desc(bh, kk), dbl = kmajor_desc(bl, kk);
-          // small terms first: lo.lo (KG_TF32X4), hi.lo, lo.hi, then hi.hi
-#ifdef KG_TF32X4
-          mma_tf32_i<Cfg::kIdesc>(tmem, dal, dbl, (kb | kk) != 0);
-          mma_tf32_i<Cfg::kIdesc>(tmem, dah, dbl, 1);
-#else
-          mma_tf32_i<Cfg::kIdesc>(tmem, dah, dbl, (kb | kk) != 0);
-#endif
-          mma_tf32_i<Cfg::kIdesc>(tmem, dal, dbh, 1);
-          mma_tf32_i<Cfg::kIdesc>(tmem, dah, dbh, 1);
+          // small terms first: hi.lo, lo.hi, then hi.hi
+          mma_tf32_i<Cfg::kIdesc>(tm, dah, dbl, !(chunk0 && kk == 0));
+          mma_tf32_i<Cfg::kIdesc>(tm, dal, dbh, 1);
+          mma_tf32_i<Cfg::kIdesc>(tm, dah, dbh, 1);
         }
         mma_commit(&empty_bar[s]);
+        if (DRAIN && (kb % kDrainKB == kDrainKB - 1 || kb == nkb - 1)) mma_commit(&acc_full[c & 1]);
       }
       mma_commit(&done_bar);
     }
   } else {
     // ---- split (and transpose the MN-major operands)
     const int ct = tid - 64;
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    // DRAIN: this thread's share of the accumulator tile -- row 32 q + lane, columns
+    // 32 half + 64 i + j (i < 2, j < 32): the same columns its epilogue writes
+    float acc[DRAIN ? 2 : 1][32];
+    if (DRAIN) {
+#pragma unroll
+      for (int i = 0; i < (DRAIN ? 2 : 1); ++i)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[i][j] = 0.f;
+    }
+    auto drain = [&](int c) {
+      mbar_wait(&acc_full[c & 1], (c >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int i = 0; i < (DRAIN ? 2 : 1); ++i) {
+        uint32_t r[32];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+            "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+              "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+            : "r"(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((c & 1) * BN + 32 * half + 64 * i)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[i][j] += __uint_as_float(r[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      mbar_arrive(&acc_empty[c & 1]);
+    };
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % S;
       mbar_wait(&full_bar[s], (kb / S) & 1);
@@ -286,19 +329,26 @@ __global__ void __launch_bounds__(G2T, 1)
       split_op<BMN, BN>(st + Cfg::kA, st + Cfg::oBhi, st + Cfg::oBlo, ct);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic stores -> tensor-core reads
       mbar_arrive(&conv_bar[s]);
+      // DRAIN: once chunk c's operands are all released, the previous chunk is drained
+      if (DRAIN && (kb % kDrainKB == kDrainKB - 1 || kb == nkb - 1) && kb / kDrainKB >= 1) drain(kb / kDrainKB - 1);
     }
+    if (DRAIN && nkb > 0) drain((nkb - 1) / kDrainKB);
     // ---- epilogue: TMEM -> registers (thread = accumulator row) -> per-warp 32 x 33 staging
     // tile in the (now idle) pipeline smem -> coalesced row stores (lane = column)
     mbar_wait(&done_bar, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
     // warp w may read TMEM lanes 32 (w % 4) ..; the G2CW / 4 warps of a quarter take turns on
     // its 32-column chunks
-    const int q = warp & 3, half = (warp - 2) >> 2;
     float *T = reinterpret_cast<float *>(sm) + (warp - 2) * 32 * 33;
-#pragma unroll 1
-    for (int c0 = 32 * half; c0 < BN; c0 += 32 * (G2CW / 4)) {
+#pragma unroll
+    for (int ci = 0; ci < BN / (32 * (G2CW / 4)); ++ci) {
+      const int c0 = 32 * half + ci * 32 * (G2CW / 4);
       if (n0 + c0 >= g.N) break;
       uint32_t r[32];
+      if (DRAIN) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(acc[DRAIN ? ci : 0][j]);
+      } else {
       asm volatile(
           "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
           "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -308,6 +358,7 @@ __global__ void __launch_bounds__(G2T, 1)
             "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
           : "r"(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0));
       asm volatile("tcgen05.wait::ld.sync.aligned;");
+      }
 #pragma unroll
       for (int j = 0; j < 32; ++j) T[lane * 33 + j] = __uint_as_float(r[j]);
       __syncwarp();
@@ -335,7 +386,7 @@ __global__ void __launch_bounds__(G2T, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
 }
 
 namespace {
@@ -367,7 +418,7 @@ bool make_tmap(CUtensorMap *tm, const float *base, int rows, int K, int ld, int 
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, bool AMN, bool BMN>
+template <int BN, bool AMN, bool BMN, bool DRAIN>
 bool launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t st) {
   using Cfg = G2Cfg<BN, AMN, BMN>;
   CUtensorMap ta, tb;
@@ -375,7 +426,7 @@ bool launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t s
     return false;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(gemm_tf32x3_tma_kernel<BN, AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(gemm_tf32x3_tma_kernel<BN, AMN, BMN, DRAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Cfg::kSmem);
     configured = true;
   }
@@ -389,7 +440,7 @@ bool launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t s
   splits = (nkb + g.kbs - 1) / g.kbs;
   g.P = splits > 1 ? part : nullptr;
   dim3 grid((g.N + BN - 1) / BN, (g.M + GBM - 1) / GBM, splits);
-  { gemm_tf32x3_tma_kernel<BN, AMN, BMN><<<grid, G2T, Cfg::kSmem, st>>>(ta, tb, g); ++g_launches; }
+  { gemm_tf32x3_tma_kernel<BN, AMN, BMN, DRAIN><<<grid, G2T, Cfg::kSmem, st>>>(ta, tb, g); ++g_launches; }
   if (splits > 1) {
     const int64_t n = (int64_t)g.M * g.N;
     { gemm_reduce_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(part, splits, g.M, g.N, g.C, g.ldc, g.bias, g.relu,
@@ -397,11 +448,12 @@ bool launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t s
   }
   return true;
 }
-template <int BN>
+template <int BN, bool DRAIN>
 bool launch_v2_any(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st) {
-  if (g.a_mn) return g.b_mn ? launch_v2<BN, true, true>(g, part, part_cap, st)
-                            : launch_v2<BN, true, false>(g, part, part_cap, st);
-  return g.b_mn ? launch_v2<BN, false, true>(g, part, part_cap, st) : launch_v2<BN, false, false>(g, part, part_cap, st);
+  if (g.a_mn) return g.b_mn ? launch_v2<BN, true, true, DRAIN>(g, part, part_cap, st)
+                            : launch_v2<BN, true, false, DRAIN>(g, part, part_cap, st);
+  return g.b_mn ? launch_v2<BN, false, true, DRAIN>(g, part, part_cap, st)
+                : launch_v2<BN, false, false, DRAIN>(g, part, part_cap, st);
 }
 }  // namespace
 
@@ -418,7 +470,8 @@ bool launch_gemm_tc(const GemmArgs &g, float *part, int64_t part_cap, cudaStream
   if (!gemm_tc_accepts(g)) return false;
   const int64_t t256 = (int64_t)((g.N + 255) / 256) * ((g.M + GBM - 1) / GBM);
   const bool wide = g.N > 128 && t256 >= 100;   // enough 128 x 256 tiles to fill the GPU
-  return wide ? launch_v2_any<256>(g, part, part_cap, st) : launch_v2_any<128>(g, part, part_cap, st);
+  if (g.drain) return launch_v2_any<128, true>(g, part, part_cap, st);
+  return wide ? launch_v2_any<256, false>(g, part, part_cap, st) : launch_v2_any<128, false>(g, part, part_cap, st);
 }
 
 }  // namespace kg

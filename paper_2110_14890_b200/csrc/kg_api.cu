@@ -229,7 +229,7 @@ struct kg_handle {
   };
   std::vector<GraphEntry> graphs;
   bool use_graphs = true;
-  bool gemm_cublas = true, side = false;
+  bool gemm_cublas = false, gemm_drain = false, side = false;
   cublasHandle_t blas2 = nullptr;
   void *blas_ws2 = nullptr;
   void *blas_ws = nullptr;
@@ -463,7 +463,7 @@ void carve(kg_handle *h, Arena &A) {
 }
 
 // Row-major GEMM: C[m x n] = op(A) op(B) + beta C, op(A) is [m x k]; tb: B given as [n x k].
-// Default: cuBLAS SGEMM (fp32); KG_GEMM=tc: the tcgen05 3xTF32 kernel (k_gemm.cu); see kg_create.
+// The tcgen05 3xTF32 kernel (k_gemm.cu; drained accumulation for BetaE) or cuBLAS SGEMM; see kg_create.
 kg_status gemm(kg_handle *h, bool ta, bool tb, int m, int n, int k, const float *A, int lda, const float *B, int ldb,
                float beta, float *C, int ldc, const float *bias = nullptr, int relu = 0) {
   if (m <= 0 || n <= 0) return KG_OK;
@@ -474,7 +474,7 @@ kg_status gemm(kg_handle *h, bool ta, bool tb, int m, int n, int k, const float 
     // the tensor-core kernel reads either operand layout directly ([k][m] / [k][n] = MN-major)
     GemmArgs g;
     g.A = A; g.B = B; g.C = C; g.M = m; g.N = n; g.K = k; g.lda = lda; g.ldb = ldb; g.ldc = ldc; g.beta = beta;
-    g.bias = bias; g.relu = relu; g.a_mn = ta; g.b_mn = !tb;
+    g.bias = bias; g.relu = relu; g.a_mn = ta; g.b_mn = !tb; g.drain = h->gemm_drain;
     if (k > 0 && launch_gemm_tc(g, h->side ? h->gsP2 : h->gsP, h->gsP_cap, h->st)) return KG_OK;
   }
   const float one = 1.f;
@@ -936,20 +936,22 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
     h->use_graphs = false;   // the exchange sizes are read on the host every step
   }
   if (const char *e = std::getenv("KG_NO_GRAPH")) h->use_graphs = !(e[0] == '1');
-  // DAG contractions (reading A24).  The hand-written tcgen05 3xTF32 kernel
-  // (k_gemm.cu) runs the d x d layers of GQE / Q2B / the -m variants (DeepSet, attention and
-  // their gradients; +5.5% C5-q2b q/s over SGEMM); BetaE's projection MLP and attention go to
-  // cuBLAS SGEMM in true fp32: the tensor-core accumulation in TMEM carries 15-25x SGEMM's error
-  // (tools/gemm_precision.py, measured on B200), and BetaE's full-size gradients (K = 800 / 1600
-  // contractions feeding digamma differences) amplify it past the 1e-5 parity bar, while the
-  // other models stay inside it (tests/test_fullsize_gpu.py, every kind at full size).
-  // KG_GEMM=tc / sgemm force one path for A/B checks.  (cuBLAS 12.9's BF16x9 fp32 emulation is
-  // faster and more accurate than SGEMM -- tools/cublas_emu_probe.cu -- but torch 2.11 loads its
-  // own cuBLAS 12.8 into the process, which lacks it.)
-  h->gemm_cublas = h->kind == KG_BETAE;
+  // DAG contractions (reading A24): the hand-written tcgen05 3xTF32 kernel
+  // (k_gemm.cu).  GQE / Q2B / the -m variants use its fast form (one TMEM accumulator per tile;
+  // full-size parity green).  BetaE uses the drained form: its projection MLP contractions
+  // (K = 800 / 1600) feed differences of digammas, which amplify the error of a long TMEM
+  // accumulation (15-25x SGEMM's, tools/gemm_precision.py) past the 1e-5 bar, so TMEM holds only
+  // 4 k-blocks at a time and the chunks are summed in fp32 registers.  KG_GEMM=sgemm: cuBLAS
+  // SGEMM everywhere; =tc: fast form everywhere; =drain: drained form everywhere (A/B checks).
+  // (cuBLAS 12.9's BF16x9 fp32 emulation is faster and more accurate than SGEMM --
+  // tools/cublas_emu_probe.cu -- but torch 2.11 loads its own cuBLAS 12.8 into the process.)
+  h->gemm_cublas = false;
+  h->gemm_drain = h->kind == KG_BETAE;
   if (const char *e = std::getenv("KG_GEMM")) {
-    if (std::string(e) == "tc") h->gemm_cublas = false;
-    if (std::string(e) == "sgemm") h->gemm_cublas = true;
+    const std::string v = e;
+    if (v == "sgemm") h->gemm_cublas = true;
+    if (v == "tc") h->gemm_drain = false;
+    if (v == "drain") h->gemm_drain = true;
   }
   cublasSetMathMode(h->blas, CUBLAS_PEDANTIC_MATH);
   cublasSetMathMode(h->blas2, CUBLAS_PEDANTIC_MATH);
@@ -1638,7 +1640,7 @@ kg_status kg_test_gemm(int32_t ta, int32_t tb, int32_t M, int32_t N, int32_t K, 
   cudaStream_t st = (cudaStream_t)stream;
   GemmArgs g;
   g.A = A; g.B = B; g.C = C; g.bias = bias; g.M = M; g.N = N; g.K = K; g.lda = lda; g.ldb = ldb; g.ldc = ldc;
-  g.relu = relu; g.beta = beta; g.a_mn = ta != 0; g.b_mn = tb != 0;
+  g.relu = relu & 1; g.beta = beta; g.a_mn = ta != 0; g.b_mn = tb != 0; g.drain = (relu & 2) != 0;
   if (!gemm_tc_accepts(g)) return KG_EINVAL;   // 16-byte aligned operands with ld % 4 == 0
   float *sP = nullptr;
   const int64_t pcap = 8LL * std::max(M, 1) * std::max(N, 1);

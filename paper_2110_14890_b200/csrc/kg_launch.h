@@ -95,6 +95,7 @@ struct GemmArgs {
   bool a_mn = false;    // A stored [K][M] (lda) instead of [M][K]
   bool b_mn = false;    // B stored [K][N] (ldb) instead of [N][K]
   int kbs = 1 << 30;    // k-blocks per split
+  bool drain = false;   // fp32-accurate accumulation: TMEM chunks of kDrainKB k-blocks summed in registers
 };
 bool gemm_tc_accepts(const GemmArgs &g);   // 16-byte aligned operands, ld % 4 == 0
 bool launch_gemm_tc(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st);   // false: not launched
