@@ -937,16 +937,16 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
   }
   if (const char *e = std::getenv("KG_NO_GRAPH")) h->use_graphs = !(e[0] == '1');
   // DAG contractions (reading A24): the hand-written tcgen05 3xTF32 kernel
-  // (k_gemm.cu).  GQE / Q2B / the -m variants use its fast form (one TMEM accumulator per tile;
-  // full-size parity green).  BetaE uses the drained form: its projection MLP contractions
-  // (K = 800 / 1600) feed differences of digammas, which amplify the error of a long TMEM
-  // accumulation (15-25x SGEMM's, tools/gemm_precision.py) past the 1e-5 bar, so TMEM holds only
-  // 4 k-blocks at a time and the chunks are summed in fp32 registers.  KG_GEMM=sgemm: cuBLAS
-  // SGEMM everywhere; =tc: fast form everywhere; =drain: drained form everywhere (A/B checks).
+  // (k_gemm.cu) in its drained form: TMEM accumulates 4 k-blocks at a time and the chunks are
+  // summed in fp32 registers -- a long TMEM accumulation carries 15-25x SGEMM's error
+  // (tools/gemm_precision.py), which BetaE's full-size gradients (K = 800 / 1600 contractions
+  // feeding differences of digammas) amplify past the 1e-5 bar; drained, the error is SGEMM's.
+  // GQE / Q2B would pass undrained too (1 % faster); one accurate path is kept for all.
+  // KG_GEMM=sgemm: cuBLAS SGEMM everywhere; =tc: undrained tcgen05 (A/B checks).
   // (cuBLAS 12.9's BF16x9 fp32 emulation is faster and more accurate than SGEMM --
   // tools/cublas_emu_probe.cu -- but torch 2.11 loads its own cuBLAS 12.8 into the process.)
   h->gemm_cublas = false;
-  h->gemm_drain = h->kind == KG_BETAE;
+  h->gemm_drain = true;
   if (const char *e = std::getenv("KG_GEMM")) {
     const std::string v = e;
     if (v == "sgemm") h->gemm_cublas = true;
