@@ -168,8 +168,12 @@ __global__ void __launch_bounds__(256) pair_fwd_kernel(ScoreArgs a) {
   // thread (tx, ty) owns queries i0 + 4*ty + x and candidates j0 + 4*tx + b (x, b < 4):
   // one 128-bit shared load per operand row per unit.
   constexpr int BI = 64, BJ = 64, KC = 16, PAD = 4;
-  __shared__ __align__(16) float sQ[NOUT][Mdl::QF][KC][BI + PAD];
-  __shared__ __align__(16) float sE[Mdl::EF][KC][BJ + PAD];
+  // double-buffered staging (the small 1-output models): chunk c + 1 is loaded into registers
+  // while chunk c is computed; otherwise one buffer and a barrier after the compute
+  constexpr bool DB = NOUT == 1 && Mdl::QF * (BI + PAD) + Mdl::EF * (BJ + PAD) <= 3 * 68;
+  constexpr int NB = DB ? 2 : 1;
+  __shared__ __align__(16) float sQ2[NB][NOUT][Mdl::QF][KC][BI + PAD];
+  __shared__ __align__(16) float sE2[NB][Mdl::EF][KC][BJ + PAD];
   __shared__ int64_t sRow[BJ];
   const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
   const int i0 = blockIdx.y * BI, j0 = blockIdx.x * BJ;
@@ -196,31 +200,66 @@ __global__ void __launch_bounds__(256) pair_fwd_kernel(ScoreArgs a) {
       for (int y = 0; y < 2; ++y) s1[tt][x][y] = s2[tt][x][y] = make_float2(0.f, 0.f);
   __syncthreads();
 
-  for (int k0 = ku0; k0 < ku1; k0 += KC) {
-    constexpr int NQ4 = NOUT * Mdl::QF * BI * (KC / 4);
-    for (int e = t; e < NQ4; e += 256) {
+  constexpr int NQ4 = NOUT * Mdl::QF * BI * (KC / 4), NE4 = Mdl::EF * BJ * (KC / 4);
+  constexpr int RQ = (NQ4 + 255) / 256, RE = (NE4 + 255) / 256;
+  float4 rq[RQ], re[RE];
+  auto load_chunk = [&](int k0) {
+#pragma unroll
+    for (int r = 0; r < RQ; ++r) {
+      const int e = t + 256 * r;
+      rq[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e >= NQ4) continue;
       const int q4 = e % (KC / 4);
       int rest = e / (KC / 4);
       const int row = rest % BI; rest /= BI;
       const int f = rest % Mdl::QF, tt = rest / Mdl::QF;
       const int i = i0 + row, k = k0 + q4 * 4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (i < M && k < ku1) v = ld4(a.Q + (size_t)(tt * M + i) * qstride + f * U + k);
-      sQ[tt][f][q4 * 4 + 0][row] = v.x; sQ[tt][f][q4 * 4 + 1][row] = v.y;
-      sQ[tt][f][q4 * 4 + 2][row] = v.z; sQ[tt][f][q4 * 4 + 3][row] = v.w;
+      if (i < M && k < ku1) rq[r] = ld4(a.Q + (size_t)(tt * M + i) * qstride + f * U + k);
     }
-    constexpr int NE4 = Mdl::EF * BJ * (KC / 4);
-    for (int e = t; e < NE4; e += 256) {
+#pragma unroll
+    for (int r = 0; r < RE; ++r) {
+      const int e = t + 256 * r;
+      re[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e >= NE4) continue;
       const int q4 = e % (KC / 4);
       const int rest = e / (KC / 4);
       const int row = rest % BJ, f = rest / BJ;
       const int j = j0 + row, k = k0 + q4 * 4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (j < K && k < ku1) v = ld4(a.E + sRow[row] * a.estride + (Mdl::EOFF + f) * U + k);
-      sE[f][q4 * 4 + 0][row] = v.x; sE[f][q4 * 4 + 1][row] = v.y;
-      sE[f][q4 * 4 + 2][row] = v.z; sE[f][q4 * 4 + 3][row] = v.w;
+      if (j < K && k < ku1) re[r] = ld4(a.E + sRow[row] * a.estride + (Mdl::EOFF + f) * U + k);
     }
-    __syncthreads();
+  };
+  auto store_chunk = [&](int buf) {
+#pragma unroll
+    for (int r = 0; r < RQ; ++r) {
+      const int e = t + 256 * r;
+      if (e >= NQ4) continue;
+      const int q4 = e % (KC / 4);
+      int rest = e / (KC / 4);
+      const int row = rest % BI; rest /= BI;
+      const int f = rest % Mdl::QF, tt = rest / Mdl::QF;
+      sQ2[buf][tt][f][q4 * 4 + 0][row] = rq[r].x; sQ2[buf][tt][f][q4 * 4 + 1][row] = rq[r].y;
+      sQ2[buf][tt][f][q4 * 4 + 2][row] = rq[r].z; sQ2[buf][tt][f][q4 * 4 + 3][row] = rq[r].w;
+    }
+#pragma unroll
+    for (int r = 0; r < RE; ++r) {
+      const int e = t + 256 * r;
+      if (e >= NE4) continue;
+      const int q4 = e % (KC / 4);
+      const int rest = e / (KC / 4);
+      const int row = rest % BJ, f = rest / BJ;
+      sE2[buf][f][q4 * 4 + 0][row] = re[r].x; sE2[buf][f][q4 * 4 + 1][row] = re[r].y;
+      sE2[buf][f][q4 * 4 + 2][row] = re[r].z; sE2[buf][f][q4 * 4 + 3][row] = re[r].w;
+    }
+  };
+  if (DB && ku0 < ku1) load_chunk(ku0);
+  int buf = 0;
+  for (int k0 = ku0; k0 < ku1; k0 += KC, buf = DB ? buf ^ 1 : 0) {
+    if (!DB) load_chunk(k0);
+    store_chunk(buf);
+    __syncthreads();   // chunk visible; (DB) every thread is past the compute of chunk - 2
+    if (DB && k0 + KC < ku1) load_chunk(k0 + KC);
+    auto &sQ = sQ2[buf];
+    auto &sE = sE2[buf];
     if constexpr (std::is_same<Mdl, MBox>::value) {
       // Q2B: D = sum |t| + (alpha - 1) sum min(|t|, o), t = v - c, on packed f32x2 pairs of
       // candidates (FADD2 with |.| operands): 2.5 instructions per (query, candidate, unit)
@@ -269,7 +308,7 @@ __global__ void __launch_bounds__(256) pair_fwd_kernel(ScoreArgs a) {
         }
       }
     }
-    __syncthreads();
+    if (!DB) __syncthreads();
   }
   if constexpr (std::is_same<Mdl, MBox>::value) {
 #pragma unroll
