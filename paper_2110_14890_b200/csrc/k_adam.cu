@@ -14,6 +14,7 @@ namespace kg {
 // ------------------------------------------------------------------ init (A23)
 __global__ void init_rows_kernel(float *p, int64_t rows, int d, int64_t row0, int64_t row_step, uint64_t seed,
                                  uint64_t stream, float lo, float hi) {
+  KG_GRID_DEP_WAIT();
   const int64_t n = rows * d;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t lr = e / d, c = e - lr * d;
@@ -22,6 +23,7 @@ __global__ void init_rows_kernel(float *p, int64_t rows, int d, int64_t row0, in
   }
 }
 __global__ void init_flat_kernel(float *p, int64_t n, uint64_t seed, uint64_t stream, float lo, float hi) {
+  KG_GRID_DEP_WAIT();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
     p[e] = counter_uniform(seed, stream, (uint64_t)e, lo, hi);
 }
@@ -80,6 +82,7 @@ constexpr int kPiece = 16;
 
 __global__ void __launch_bounds__(128) seg_piece_kernel(const int32_t *perm, const int32_t *inv, const int32_t *seg,
                                                         int L, const float *X, int w4, float *PS) {
+  KG_GRID_DEP_WAIT();
   __shared__ int s_row[kPiece], s_beg[kPiece], s_len[kPiece];
   const int c0 = blockIdx.x * kPiece;
   const int n = min(kPiece, L - c0);
@@ -134,6 +137,7 @@ __global__ void __launch_bounds__(256) sparse_adam_kernel(const int64_t *uniq, c
                                                           const float *PS, int d, int world, float *ent, float *m,
                                                           float *v, float *grad_out, const float *lr_dev, AdamHyper hy,
                                                           const float *bc, const int *flags, int apply) {
+  KG_GRID_DEP_WAIT();
   const int u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (u >= *U_dev) return;
   const int d4 = d >> 2, s0 = seg[u], s1 = seg[u + 1];
@@ -181,6 +185,7 @@ void launch_sparse_adam(const int64_t *uniq, const int32_t *seg, const int32_t *
 __global__ void __launch_bounds__(256) rel_reduce_kernel(const int32_t *seg, const int32_t *perm,
                                                          const int32_t *U_dev, const float *RG, const float *PS,
                                                          int dr, float *RGU) {
+  KG_GRID_DEP_WAIT();
   const int w4 = dr >> 2;
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int u = (int)(e / w4), c = (int)(e - (int64_t)u * w4);
@@ -201,6 +206,7 @@ void launch_rel_reduce(const int32_t *seg, const int32_t *perm, const int32_t *i
 // (Avoids zeroing / reading a dense |R| x d gradient for the untouched relation rows.)
 __global__ void rel_stamp_kernel(const int64_t *uniq_rel, const int32_t *U_dev, int32_t *rel_seg,
                                  int64_t *rel_stamp, const int64_t *stamp) {
+  KG_GRID_DEP_WAIT();
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= *U_dev) return;
   const int64_t r = uniq_rel[u];
@@ -242,6 +248,7 @@ __global__ void __launch_bounds__(256) dense_adam_rel_kernel(float4 *p, float4 *
                                                              const int64_t *stamp_dev, const float *lr_dev,
                                                              AdamHyper hy, const float *bc, const int *flags,
                                                              int untouched_only) {
+  KG_GRID_DEP_WAIT();
   if (flags[0]) return;
   const float lr1 = *lr_dev * bc[0], ibc2 = bc[1];
   const int64_t stamp = *stamp_dev;
@@ -283,6 +290,7 @@ __global__ void __launch_bounds__(256) dense_adam_rel_touched_kernel(float4 *p, 
                                                                      const int64_t *runiq, const int32_t *rU,
                                                                      const float *lr_dev, AdamHyper hy,
                                                                      const float *bc, const int *flags) {
+  KG_GRID_DEP_WAIT();
   if (flags[0]) return;
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int per = nseg * w4;
@@ -302,6 +310,7 @@ __global__ void __launch_bounds__(256) dense_adam_rel_touched_kernel(float4 *p, 
 __global__ void __launch_bounds__(256) dense_adam_kernel(float4 *p, float4 *m, float4 *v, const float4 *g, int n4,
                                                          const float *lr_dev, AdamHyper hy, const float *bc,
                                                          const int *flags) {
+  KG_GRID_DEP_WAIT();
   if (flags[0]) return;
   const float lr1 = *lr_dev * bc[0], ibc2 = bc[1];
   const int base = blockIdx.x * (256 * kE) + threadIdx.x;
@@ -358,6 +367,7 @@ void launch_dense_adam(float *p, float *m, float *v, const float *g, int64_t n, 
 
 // out[c] = sum_r X[r*ld + c]; 32 columns x 32 row-lanes per block, fixed-order smem reduce.
 __global__ void __launch_bounds__(1024) colsum_kernel(const float *X, int rows, int cols, int ld, float *out) {
+  KG_GRID_DEP_WAIT();
   __shared__ float red[32][33];
   const int cx = threadIdx.x & 31, ry = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + cx;

@@ -20,6 +20,7 @@ template <int KIND>
 __global__ void proj_fwd_kernel(int N, int d, const float *in, int64_t in_ld, const int64_t *anchor_rows,
                                 const float *ent, const int32_t *rel, int rel_ld, const float *relA,
                                 const float *relB, float *out) {
+  KG_GRID_DEP_WAIT();
   const int U = (KIND == COMPLEX || KIND == ROTATE) ? d / 2 : d;
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)N * U) return;
@@ -52,6 +53,7 @@ __global__ void proj_bwd_kernel(int N, int d, const float *dout, const float *in
                                 const int64_t *anchor_rows, const float *ent, const int32_t *rel, int rel_ld,
                                 const float *relA, const float *relB, const float *out, float *din, int64_t din_ld,
                                 float *drel) {
+  KG_GRID_DEP_WAIT();
   const int U = (KIND == COMPLEX || KIND == ROTATE) ? d / 2 : d;
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)N * U) return;
@@ -131,6 +133,7 @@ void launch_proj_bwd(int kind, int N, int d, const float *dout, const float *in,
 // X[i] = [e_q(i) ; y_r(i)]  (A9), e_q = node value or clamp(x_anchor + 1) (A8)
 __global__ void betae_proj_in_kernel(int N, int d, const float *in, const int64_t *anchor_rows, const float *ent,
                                      const int32_t *rel, int rel_ld, const float *relT, float *X) {
+  KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)N * d) return;
   const int i = (int)(e / d), k = (int)(e - (int64_t)i * d);
@@ -145,6 +148,7 @@ void launch_betae_proj_in(int N, int d, const float *in, const int64_t *anchor_r
 
 // Y = act(Y + b) row-wise; act 1 = ReLU, 0 = identity.
 __global__ void bias_act_kernel(float *Y, const float *b, int rows, int cols, int act) {
+  KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)rows * cols) return;
   const float v = Y[e] + b[e % cols];
@@ -155,6 +159,7 @@ void launch_bias_act(float *Y, const float *b, int rows, int cols, int act, cuda
 }
 
 __global__ void betae_proj_out_kernel(const float *Z, const float *b0, int rows, int d, float *Zp1, float *out) {
+  KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)rows * d) return;
   const float z = Z[e] + b0[e % d] + 1.f;
@@ -167,6 +172,7 @@ void launch_betae_proj_out(const float *Z, const float *b0, int rows, int d, flo
 }
 
 __global__ void betae_proj_dz_kernel(const float *dout, const float *Zp1, int rows, int d, float *dZ) {
+  KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)rows * d) return;
   const float z = Zp1[e];
@@ -177,6 +183,7 @@ void launch_betae_proj_dz(const float *dout, const float *Zp1, int rows, int d, 
 }
 
 __global__ void relu_mask_kernel(float *dY, const float *Y, int64_t n) {
+  KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e < n && !(Y[e] > 0.f)) dY[e] = 0.f;
 }
@@ -187,6 +194,7 @@ void launch_relu_mask(float *dY, const float *Y, int rows, int cols, cudaStream_
 // dX [N][2d] -> din (query part; raw-row gradient through the clamp for anchors) and drel.
 __global__ void betae_split_kernel(const float *dX, int N, int d, const int64_t *anchor_rows, const float *ent,
                                    float *din, int64_t din_ld, float *drel) {
+  KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)N * d) return;
   const int i = (int)(e / d), k = (int)(e - (int64_t)i * d);
@@ -205,6 +213,7 @@ void launch_betae_split(const float *dX, int N, int d, const int64_t *anchor_row
 // unit sphere (parts = 2).  One warp per (row, part), in place; the norms are kept for the
 // adjoint g <- (g - y (y . g)) / ||x|| (y the normalised value).
 __global__ void qnorm_fwd_kernel(float *X, int M, int d, int parts, float *nrm) {
+  KG_GRID_DEP_WAIT();
   const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (w >= M * parts) return;
   const int L = d / parts;
@@ -217,6 +226,7 @@ __global__ void qnorm_fwd_kernel(float *X, int M, int d, int parts, float *nrm) 
   if (lane == 0) nrm[2 * (w / parts) + (w % parts)] = n;
 }
 __global__ void qnorm_bwd_kernel(float *G, const float *Y, int M, int d, int parts, const float *nrm) {
+  KG_GRID_DEP_WAIT();
   const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (w >= M * parts) return;
   const int L = d / parts;
@@ -241,10 +251,12 @@ void launch_qnorm_bwd(float *G, const float *Y, int M, int d, int parts, const f
 // ------------------------------------------------------------ negation (BetaE)
 // N(q) = 1/q elementwise on (alpha, beta) (Table 1 'Negation' P:L143); adjoint -g/q^2.
 __global__ void neg_fwd_kernel(const float *in, int64_t n, float *out) {
+  KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e < n) out[e] = 1.f / in[e];
 }
 __global__ void neg_bwd_kernel(const float *dout, const float *in, int64_t n, float *din) {
+  KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e < n) {
     const float x = in[e];
@@ -260,6 +272,7 @@ void launch_neg_bwd(const float *dout, const float *in, int64_t n, float *din, c
 
 // ------------------------------------------------------------ intersections
 __global__ void mean_stack_kernel(const float *H, int n, int64_t rc, float *out) {
+  KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= rc) return;
   float s = 0.f;
@@ -273,6 +286,7 @@ void launch_mean_stack(const float *H, int n, int rows, int cols, float *out, cu
 
 // dH_t = dMn / n * [H_t > 0]   (DeepSet mean pooling + ReLU adjoint, A4)
 __global__ void gqe_inter_dh_kernel(const float *dMn, const float *H, int n, int64_t rc, float *dH) {
+  KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= rc * n) return;
   dH[e] = H[e] > 0.f ? dMn[e % rc] / (float)n : 0.f;
@@ -284,6 +298,7 @@ void launch_gqe_inter_dh(const float *dMn, const float *H, int n, int rows, int 
 
 // Q2B center attention: a_t = softmax_t(Lg_t) per (i, k); c = sum_t a_t c_t (A5).
 __global__ void q2b_att_fwd_kernel(const float *stack, const float *Lg, int n, int M, int d, float *a, float *out) {
+  KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t Md = (int64_t)M * d;
   if (e >= Md) return;
@@ -308,6 +323,7 @@ void launch_q2b_att_fwd(const float *stack, const float *Lg, int n, int M, int d
 // Q2B offset: o = min_t o_t * sigmoid(Z)  (Table 1), argmin ties -> lowest t (A19).
 __global__ void q2b_off_fwd_kernel(const float *stack, const float *Z, int n, int M, int d, float *sig, int8_t *amin,
                                    float *out) {
+  KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)M * d) return;
   const int i = (int)(e / d), k = (int)(e - (int64_t)i * d);
@@ -329,6 +345,7 @@ void launch_q2b_off_fwd(const float *stack, const float *Z, int n, int M, int d,
 
 __global__ void q2b_att_bwd_kernel(const float *stack, const float *a, const float *dout, int n, int M, int d,
                                    float *dLg, float *dstack) {
+  KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t Md = (int64_t)M * d;
   if (e >= Md) return;
@@ -352,6 +369,7 @@ void launch_q2b_att_bwd(const float *stack, const float *a, const float *dout, i
 
 __global__ void q2b_off_bwd_kernel(const float *stack, const float *sig, const int8_t *amin, const float *dout, int n,
                                    int M, int d, float *dZ, float *dstack) {
+  KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)M * d) return;
   const int i = (int)(e / d), k = (int)(e - (int64_t)i * d);
@@ -368,6 +386,7 @@ void launch_q2b_off_bwd(const float *stack, const float *sig, const int8_t *amin
 
 // BetaE attention: w = softmax_t(Lg_t) (m per row), out = (sum w a_t, sum w b_t) (Table 1, A5).
 __global__ void beta_att_fwd_kernel(const float *stack, const float *Lg, int n, int M, int d, float *w, float *out) {
+  KG_GRID_DEP_WAIT();
   const int m = d / 2;
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t Mm = (int64_t)M * m;
@@ -395,6 +414,7 @@ void launch_beta_att_fwd(const float *stack, const float *Lg, int n, int M, int 
 
 __global__ void beta_att_bwd_kernel(const float *stack, const float *w, const float *dout, int n, int M, int d,
                                     float *dLg, float *dstack) {
+  KG_GRID_DEP_WAIT();
   const int m = d / 2;
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t Mm = (int64_t)M * m;
@@ -422,6 +442,7 @@ void launch_beta_att_bwd(const float *stack, const float *w, const float *dout, 
 
 // ------------------------------------------------------------ misc
 __global__ void scale_copy_kernel(float *dst, const float *src, int64_t n, float s) {
+  KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e < n) dst[e] = src[e] * s;
 }
@@ -430,6 +451,7 @@ void launch_scale_copy(float *dst, const float *src, int64_t n, float s, cudaStr
 }
 
 __global__ void gather_rows_kernel(float *dst, const float *src, const int64_t *rows, int n, int d) {
+  KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)n * d) return;
   const int i = (int)(e / d), k = (int)(e - (int64_t)i * d);
@@ -439,6 +461,7 @@ void launch_gather_rows(float *dst, const float *src, const int64_t *rows, int n
   if (n > 0) { gather_rows_kernel<<<blocks((int64_t)n * d), 256, 0, st>>>(dst, src, rows, n, d); ++g_launches; }
 }
 __global__ void scatter_rows_kernel(float *dst, const float *src, const int64_t *rows, int n, int d) {
+  KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)n * d) return;
   const int i = (int)(e / d), k = (int)(e - (int64_t)i * d);
@@ -454,6 +477,7 @@ void launch_scatter_rows(float *dst, const float *src, const int64_t *rows, int 
 __global__ void ids_concat_kernel(const int64_t *anchors, int na, int M, const int64_t *answers, int n_ans,
                                   const int64_t *negs, int K, int world, int64_t *ids, int64_t *rows_out,
                                   int32_t *bad, int64_t n_entities) {
+  KG_GRID_DEP_WAIT();
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   const int nai = na * M, L = nai + n_ans + K;
   if (p >= L) return;
@@ -477,6 +501,7 @@ void launch_ids_concat(const int64_t *anchors, int na, int M, const int64_t *ans
 // occ[u*M + i] = relations[i][slot_u] (one relation occurrence per projection use).
 __global__ void rel_occ_kernel(const int32_t *relations, int M, int nr, Slots4 slots, int nproj, int n_rel,
                                int32_t *occ, int32_t *bad) {
+  KG_GRID_DEP_WAIT();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= nproj * M) return;
   const int u = e / M, i = e - u * M;

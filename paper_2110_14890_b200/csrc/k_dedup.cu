@@ -23,6 +23,7 @@ template <int ITEMS>
 __global__ void __launch_bounds__(kDedupThreads) dedup_kernel(const int64_t *ids64, const int32_t *ids32, int L,
                                                               int end_bit, int64_t *uniq, int32_t *inv,
                                                               int32_t *perm, int32_t *seg, int32_t *U_out) {
+  KG_GRID_DEP_WAIT();
   using Sort = cub::BlockRadixSort<uint32_t, kDedupThreads, ITEMS, uint32_t>;
   using Disc = cub::BlockDiscontinuity<uint32_t, kDedupThreads>;
   using Scan = cub::BlockScan<int, kDedupThreads>;

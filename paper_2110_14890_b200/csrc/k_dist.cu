@@ -20,6 +20,7 @@ constexpr int kPartThreads = 1024;
 __global__ void __launch_bounds__(kPartThreads) owner_partition_kernel(const int64_t *uniq, const int32_t *U_dev,
                                                                        int G, int64_t *send_ids, int32_t *send_pos,
                                                                        int32_t *counts) {
+  KG_GRID_DEP_WAIT();
   __shared__ int32_t s_cnt[kMaxWorld][kPartThreads];
   __shared__ int32_t s_base[kMaxWorld + 1];
   const int U = *U_dev, t = threadIdx.x;
@@ -73,6 +74,7 @@ void launch_owner_partition(const int64_t *uniq, const int32_t *U_dev, int G, in
 
 // rows[p] = send_pos[inv[p]]: the occurrence's row in the received (owner-grouped) row buffer.
 __global__ void occ_rows_kernel(const int32_t *inv, const int32_t *send_pos, int L, int64_t *rows) {
+  KG_GRID_DEP_WAIT();
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p < L) rows[p] = send_pos[inv[p]];
 }
@@ -82,6 +84,7 @@ void launch_occ_rows(const int32_t *inv, const int32_t *send_pos, int L, int64_t
 
 // Owner side: out[i] = theta_E[ids[i] / G] (rows requested by the peers, in receive order).
 __global__ void gather_owned_kernel(const float *ent, const int64_t *ids, int n, int G, int d4, float4 *out) {
+  KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)n * d4) return;
   const int i = (int)(e / d4), c = (int)(e - (int64_t)i * d4);
@@ -98,6 +101,7 @@ void launch_gather_owned(const float *ent, const int64_t *ids, int n, int G, int
 // out[send_pos[u]] = G[u] (merged row gradients in send order).
 __global__ void reorder_rows_kernel(const float4 *Gu, const int32_t *send_pos, const int32_t *U_dev, int d4,
                                     float4 *out) {
+  KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int u = (int)(e / d4), c = (int)(e - (int64_t)u * d4);
   if (u >= *U_dev) return;
@@ -115,6 +119,7 @@ void launch_reorder_rows(const float *Gu, const int32_t *send_pos, const int32_t
 
 // keys[i] = ids[i] / G (owner-local rows of the received ids, for the owner-side merge).
 __global__ void local_rows_kernel(const int64_t *ids, int n, int G, int64_t *keys) {
+  KG_GRID_DEP_WAIT();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) keys[i] = ids[i] / G;
 }
@@ -126,6 +131,7 @@ void launch_local_rows(const int64_t *ids, int n, int G, int64_t *keys, cudaStre
 // for the relations used by this rank (the caller zeroes the relation part first).
 __global__ void scatter_rel_kernel(const float *RGU, const int64_t *runiq, const int32_t *rU, int R, int w, int nseg,
                                    float *gfull) {
+  KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int dr = w * nseg;
   const int u = (int)(e / dr), c = (int)(e - (int64_t)u * dr);

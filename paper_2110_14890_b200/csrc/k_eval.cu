@@ -53,6 +53,7 @@ __device__ __forceinline__ float warp_dist(const float *__restrict__ q, const fl
 
 template <int KIND, int NOUT>
 __global__ void __launch_bounds__(256) eval_rank_kernel(EvalArgs a) {
+  KG_GRID_DEP_WAIT();
   extern __shared__ float sD[];   // [max_ans] answer distances, then [n_neg] negative distances
   __shared__ float red[32];
   const int i = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;

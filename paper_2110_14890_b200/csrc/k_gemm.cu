@@ -41,6 +41,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 // out[c][r] = in[r][c]: in [R][C] (ld_in), out [C][R] (ld_out); 32 x 32 tiles through shared memory.
 __global__ void transpose_kernel(const float *__restrict__ in, int R, int Cc, int ld_in, float *__restrict__ out,
                                  int ld_out) {
+  KG_GRID_DEP_WAIT();
   __shared__ float t[32][33];
   const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
   for (int y = threadIdx.y; y < 32; y += 8) {
@@ -62,6 +63,7 @@ void launch_transpose(const float *in, int R, int Cc, int ld_in, float *out, int
 // C = beta C + sum_z P[z] (+ bias) (ReLU): the fixed-order combine of the split-K partials.
 __global__ void gemm_reduce_kernel(const float *__restrict__ P, int splits, int M, int N, float *C, int ldc,
                                    const float *bias, int relu, float beta) {
+  KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)M * N) return;
   const int row = (int)(e / N), n = (int)(e - (int64_t)row * N);
@@ -209,6 +211,7 @@ constexpr int kDrainKB = 4;
 template <int BN, bool AMN, bool BMN, bool DRAIN>
 __global__ void __launch_bounds__(G2T, 1)
     gemm_tf32x3_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
+  KG_GRID_DEP_WAIT();
   using Cfg = G2Cfg<BN, AMN, BMN>;
   constexpr int S = Cfg::kStages;
   constexpr int kCols = DRAIN ? 2 * BN : BN;                     // TMEM columns (power of 2 >= 32)

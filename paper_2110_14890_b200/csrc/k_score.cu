@@ -165,6 +165,7 @@ __device__ __forceinline__ float4 ld4(const float *p) { return *reinterpret_cast
 // sums go to Dpart[z][t][i][j] and pair_epi_kernel adds them in the fixed order z.
 template <class Mdl, int NOUT>
 __global__ void __launch_bounds__(256) pair_fwd_kernel(ScoreArgs a) {
+  KG_GRID_DEP_WAIT();
   // thread (tx, ty) owns queries i0 + 4*ty + x and candidates j0 + 4*tx + b (x, b < 4):
   // one 128-bit shared load per operand row per unit.
   constexpr int BI = 64, BJ = 64, KC = 16, PAD = 4;
@@ -342,6 +343,7 @@ __global__ void __launch_bounds__(256) pair_fwd_kernel(ScoreArgs a) {
 // term and sum_j C (BetaE), all reduced in a fixed order.
 template <class Mdl, int NOUT, bool TRAIN>
 __global__ void __launch_bounds__(256) pair_epi_kernel(ScoreArgs a) {
+  KG_GRID_DEP_WAIT();
   __shared__ float red[32];
   const int i = blockIdx.x, M = a.M, K = a.K;
   const size_t zs = (size_t)NOUT * M * a.Kp;
@@ -420,6 +422,7 @@ template <class Mdl> struct BwdOcc { static constexpr int v = (Mdl::BF == 1 && M
 
 template <class Mdl>
 __global__ void __launch_bounds__(kBW * 32, BwdOcc<Mdl>::v) pair_bwd_kernel(ScoreArgs a) {
+  KG_GRID_DEP_WAIT();
   constexpr int QF = Mdl::QF, BQF = Mdl::BQF, BF = Mdl::BF, AV = Mdl::AV, JB = kBW * kJW;
   extern __shared__ __align__(16) float smem[];
   float *sC = smem;                                   // [kIC][JB]
@@ -536,6 +539,7 @@ __global__ void __launch_bounds__(kBW * 32, BwdOcc<Mdl>::v) pair_bwd_kernel(Scor
 // positive term.  (BetaE's partials already hold sum_j C (QP - P), see MBeta::grad.)
 template <bool BETA, bool BOX>
 __global__ void bwd_q_combine_kernel(ScoreArgs a, int qstride) {
+  KG_GRID_DEP_WAIT();
   const int64_t n = (int64_t)a.NQ * qstride;
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= n) return;
@@ -549,6 +553,7 @@ __global__ void bwd_q_combine_kernel(ScoreArgs a, int qstride) {
 // entity features [A, B, TA, TB, TAB, GA, GB] = F planes 2..8).
 template <class Mdl>
 __global__ void bwd_v_combine_kernel(ScoreArgs a) {
+  KG_GRID_DEP_WAIT();
   constexpr int AV = Mdl::AV;
   const int U = a.U, K = a.K;
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -585,6 +590,7 @@ __global__ void bwd_v_combine_kernel(ScoreArgs a) {
 // writes the raw-row gradient of the answer occurrence.
 template <int KIND, int NOUT>
 __global__ void __launch_bounds__(128) pos_kernel(PosArgs p) {
+  KG_GRID_DEP_WAIT();
   __shared__ float red[32];
   const int i = blockIdx.x, M = p.M, U = p.U, d = p.d;
   constexpr int QF = (KIND == GQE || KIND == TRANSE || KIND == DISTMULT) ? 1 : 2;
@@ -677,6 +683,7 @@ __global__ void __launch_bounds__(128) pos_kernel(PosArgs p) {
 // Entity features of the pool (9 planes of m, layout above) and Cv_j = sum_k lnB(A, B).
 __global__ void __launch_bounds__(128) beta_entity_kernel(const float *ent, const int64_t *rows, int K, int m,
                                                           float *F, float *Cv) {
+  KG_GRID_DEP_WAIT();
   __shared__ float red[32];
   const int j = blockIdx.x;
   const float *x = ent + rows[j] * (int64_t)(2 * m);
@@ -703,6 +710,7 @@ __global__ void __launch_bounds__(128) beta_entity_kernel(const float *ent, cons
 
 // Query features: QP[r] = [psi(a2) - psi(a2+b2) | psi(b2) - psi(a2+b2)], Cq[r] = sum_k lnB(a2, b2).
 __global__ void __launch_bounds__(128) beta_query_kernel(const float *Q, int NQ, int m, float *QP, float *Cq) {
+  KG_GRID_DEP_WAIT();
   __shared__ float red[32];
   const int r = blockIdx.x;
   const float *q = Q + (size_t)r * 2 * m;
@@ -724,6 +732,7 @@ __global__ void __launch_bounds__(256) loss_finalize_kernel(const float *loss_po
                                                             int njt, double scale, double *loss_out,
                                                             int *flags, int64_t *t_dev, float *bc,
                                                             double beta1, double beta2, int apply, int check) {
+  KG_GRID_DEP_WAIT();
   __shared__ double red[256];
   double s = 0.0;
   for (int i = threadIdx.x; i < M; i += 256) {
@@ -866,6 +875,7 @@ void launch_loss_finalize(const float *loss_pos, const float *loss_part, int M, 
 // After the cross-rank sum of the loss and max of the input flags (world > 1).
 __global__ void loss_check_kernel(double *loss_out, int *flags, int64_t *t_dev, float *bc, double beta1, double beta2,
                                   int apply) {
+  KG_GRID_DEP_WAIT();
   const double loss = *loss_out;
   const int bad = !isfinite(loss) || flags[1];
   flags[0] = bad;

@@ -224,12 +224,12 @@ struct kg_handle {
   float *lr_dev = nullptr;
   int64_t *stamp_dev = nullptr;
   struct GraphEntry {
-    int structure, M, K, flags, kernels, gemms;
+    int structure, M, K, flags, kernels, gemms, pdl_edges;
     cudaGraphExec_t exec;
   };
   std::vector<GraphEntry> graphs;
   bool use_graphs = true;
-  bool gemm_cublas = false, gemm_drain = false, side = false;
+  bool gemm_cublas = false, gemm_drain = false, side = false, use_pdl = true;
   cublasHandle_t blas2 = nullptr;
   void *blas_ws2 = nullptr;
   void *blas_ws = nullptr;
@@ -503,6 +503,47 @@ struct OnStream {
     h->side = false;
   }
 };
+// Programmatic dependent launch inside the step graph: every kernel-to-kernel edge whose
+// downstream kernel is one of this library's (they all begin with griddepcontrol.wait,
+// KG_GRID_DEP_WAIT) becomes a programmatic edge, so the downstream grid is launched as the
+// upstream one drains instead of after it has completed; the wait keeps the data dependence.
+// Edges into library kernels of other modules (cuBLAS) and through event nodes are kept.
+bool ours(cudaGraphNode_t n) {
+  cudaGraphNodeType t;
+  if (cudaGraphNodeGetType(n, &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) return false;
+  cudaKernelNodeParams kp;
+  if (cudaGraphKernelNodeGetParams(n, &kp) != cudaSuccess || !kp.func) { cudaGetLastError(); return false; }
+  Dl_info info;
+  return dladdr(kp.func, &info) && info.dli_fname && std::strstr(info.dli_fname, "libkg") != nullptr;
+}
+bool is_kernel(cudaGraphNode_t n) {
+  cudaGraphNodeType t;
+  return cudaGraphNodeGetType(n, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel;
+}
+int make_programmatic(cudaGraph_t g) {
+  size_t n = 0;
+  if (cudaGraphGetEdges_v2(g, nullptr, nullptr, nullptr, &n) != cudaSuccess || n == 0) return 0;
+  std::vector<cudaGraphNode_t> from(n), to(n);
+  std::vector<cudaGraphEdgeData> ed(n);
+  if (cudaGraphGetEdges_v2(g, from.data(), to.data(), ed.data(), &n) != cudaSuccess) return 0;
+  int converted = 0;
+  for (size_t i = 0; i < n; ++i) {
+    if (ed[i].type != cudaGraphDependencyTypeDefault || ed[i].from_port != 0) continue;
+    if (!is_kernel(from[i]) || !ours(to[i])) continue;
+    if (cudaGraphRemoveDependencies_v2(g, &from[i], &to[i], &ed[i], 1) != cudaSuccess) { cudaGetLastError(); continue; }
+    cudaGraphEdgeData e{};
+    e.from_port = cudaGraphKernelNodePortProgrammatic;
+    e.type = cudaGraphDependencyTypeProgrammatic;
+    if (cudaGraphAddDependencies_v2(g, &from[i], &to[i], &e, 1) != cudaSuccess) {
+      cudaGetLastError();
+      cudaGraphAddDependencies_v2(g, &from[i], &to[i], &ed[i], 1);   // restore the plain edge
+      continue;
+    }
+    ++converted;
+  }
+  return converted;
+}
+
 // the lowest stream priority (the early dense-Adam stream yields the SMs to the scoring kernels)
 int kLowPriority() {
   int lo = 0, hi = 0;
@@ -936,6 +977,7 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
     h->use_graphs = false;   // the exchange sizes are read on the host every step
   }
   if (const char *e = std::getenv("KG_NO_GRAPH")) h->use_graphs = !(e[0] == '1');
+  if (const char *e = std::getenv("KG_PDL")) h->use_pdl = !(e[0] == '0');
   // DAG contractions (reading A24): the hand-written tcgen05 3xTF32 kernel
   // (k_gemm.cu) in its drained form: TMEM accumulates 4 k-blocks at a time and the chunks are
   // summed in fp32 registers -- a long TMEM accumulation carries 15-25x SGEMM's error
@@ -1360,6 +1402,7 @@ kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info)
       e.structure = b->structure; e.M = S.M; e.K = S.K; e.flags = h->flag_key();
       e.kernels = (int)(g_launches - l0);
       e.gemms = h->gemm_count;
+      if (h->use_pdl) e.pdl_edges = make_programmatic(graph);
       ce = cudaGraphInstantiate(&e.exec, graph, 0);
       cudaGraphDestroy(graph);
       if (ce != cudaSuccess) return fail(h, KG_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));

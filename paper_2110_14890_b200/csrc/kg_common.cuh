@@ -4,6 +4,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Programmatic dependent launch: every kernel of the library waits for its predecessor grids
+// (memory visible) before touching their outputs.  In a captured step graph the kernel-to-
+// kernel edges are programmatic (kg_api.cu make_programmatic), so a kernel is launched while
+// its predecessor drains; outside such edges the instruction is a no-op.
+#define KG_GRID_DEP_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+
 namespace kg {
 
 enum Kind { GQE = 0, Q2B = 1, BETAE = 2, TRANSE = 3, ROTATE = 4, DISTMULT = 5, COMPLEX = 6 };
