@@ -12,7 +12,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _run(ta, tb, M, N, K, bias=False, relu=False, beta=0.0, seed=0):
+def _run(ta, tb, M, N, K, bias=False, relu=False, beta=0.0, seed=0, drain=False):
     import torch
     import paper_2110_14890_b200 as kgb
     rng = np.random.default_rng(seed)
@@ -32,7 +32,7 @@ def _run(ta, tb, M, N, K, bias=False, relu=False, beta=0.0, seed=0):
     tA, tB, tC, tb_ = (torch.from_numpy(x).to(dev) for x in (Ap, Bp, C0, b))
     st = torch.cuda.current_stream()
     s = kgb.kg_test_gemm(int(ta), int(tb), M, N, K, tA.data_ptr(), Ap.shape[1], tB.data_ptr(), Bp.shape[1],
-                         tC.data_ptr(), N, tb_.data_ptr() if bias else None, int(relu), beta,
+                         tC.data_ptr(), N, tb_.data_ptr() if bias else None, int(relu) | (2 if drain else 0), beta,
                          C.c_void_p(st.cuda_stream))
     assert s == 0
     opA = A.T.astype(np.float64) if ta else A.astype(np.float64)
@@ -73,3 +73,12 @@ def test_gemm_rejects_unaligned_leading_dimension():
     s = kgb.kg_test_gemm(0, 0, 8, 8, 10, A.data_ptr(), 10, A.data_ptr(), 10, A.data_ptr(), 8, None, 0, 0.0,
                          C.c_void_p(st.cuda_stream))
     assert s == 1   # lda % 4 != 0 -> KG_EINVAL
+
+
+@pytest.mark.parametrize("ta,tb,M,N,K", [(False, True, 1536, 1600, 800),    # H1 = X W1^T: 128 x 160 tiles
+                                         (True, True, 1600, 1600, 1536),    # dW2 = dH2^T H1 (MN-major both)
+                                         (False, False, 1536, 800, 1600),   # dX = dH1 W1
+                                         (False, True, 200, 72, 40), (True, False, 70, 130, 33)])
+def test_gemm_drained_accumulation(ta, tb, M, N, K):
+    """The drained form (fp32-accurate, BetaE's default; 128 x 128 or 128 x 160 tiles)."""
+    _run(ta, tb, M, N, K, bias=not ta, relu=not ta, drain=True)
