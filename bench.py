@@ -344,7 +344,7 @@ def sampler_e2e(args, gm, cfg, w, M, K, world, rank):
     del kg
     workers = max(1, threads - 1)
     pipe = smp.pipeline(w.structures, M, K, seed=args.seed, rank=rank, first_step=0, depth=2 * workers,
-                        n_workers=workers)
+                        n_workers=workers, pin=True)
     for _ in range(2 * workers):                  # warm-up: fill the ring once
         gm.step(pipe.next(), args.lr, sync=True)
     n = min(args.steps, 450)

@@ -116,8 +116,8 @@ class KGSampler:
                           n_threads or self.n_threads))
         return out.astype(bool)
 
-    def pipeline(self, structures, M, K, seed=0, rank=0, first_step=0, depth=None, n_workers=None):
-        return Pipeline(self, structures, M, K, seed, rank, first_step, depth, n_workers)
+    def pipeline(self, structures, M, K, seed=0, rank=0, first_step=0, depth=None, n_workers=None, pin=False):
+        return Pipeline(self, structures, M, K, seed, rank, first_step, depth, n_workers, pin)
 
     def close(self):
         if self.g:
@@ -149,9 +149,15 @@ class Pipeline:
         _check(kgs_pipeline_create(smp.g, _p(self.st), len(self.st), M, K, seed, rank, first_step, depth, n_workers,
                                    C.byref(self.p)))
         W = max(1, (K + 31) // 32)
-        self.buf = dict(anchors=np.zeros((M, 3), np.int64), relations=np.zeros((M, 3), np.int32),
-                        answers=np.zeros(M, np.int64), negatives=np.zeros(max(K, 1), np.int64),
-                        mask=np.zeros((M, W), np.uint32))
+        shapes = dict(anchors=((M, 3), np.int64), relations=((M, 3), np.int32), answers=((M,), np.int64),
+                      negatives=((max(K, 1),), np.int64), mask=((M, W), np.uint32))
+        if pin:   # page-locked buffers (numpy views of pinned torch tensors): kg_step's H2D is a DMA
+            import torch
+            tdt = {np.int64: torch.int64, np.int32: torch.int32, np.uint32: torch.int32}
+            self._pinned = {k: torch.zeros(sh, dtype=tdt[dt], pin_memory=True) for k, (sh, dt) in shapes.items()}
+            self.buf = {k: t.numpy().view(shapes[k][1]) for k, t in self._pinned.items()}
+        else:
+            self.buf = {k: np.zeros(sh, dt) for k, (sh, dt) in shapes.items()}
         self.wait_ms = 0.0
 
     def next(self) -> dict:
