@@ -217,10 +217,11 @@ __global__ void __launch_bounds__(G2T, 1)
   // TMEM columns: a power of 2 >= 32 holding one (or, drained, two) BN-column accumulators
   constexpr int kNeed = DRAIN ? 2 * BN : BN;
   constexpr int kCols = kNeed <= 32 ? 32 : kNeed <= 64 ? 64 : kNeed <= 128 ? 128 : kNeed <= 256 ? 256 : 512;
-  // 32-column chunks of the tile; the two warps of a TMEM lane quarter take alternate chunks
-  constexpr int kChunks = BN / 32, kCI = (kChunks + 1) / 2;
-  static_assert(BN % 32 == 0 && kNeed <= 512, "tile width");
-  static_assert(!DRAIN || (G2CW == 8 && BN <= 160), "the drained accumulator is held in registers");
+  // 32-column chunks of the tile; the NG = G2CW / 4 warps of a TMEM lane quarter take the
+  // chunks round-robin (chunk = grp + NG i)
+  constexpr int NG = G2CW / 4, kChunks = BN / 32, kCI = (kChunks + NG - 1) / NG;
+  static_assert(BN % 32 == 0 && kNeed <= 512 && G2CW % 4 == 0, "tile width / split warps");
+  static_assert(!DRAIN || kCI <= 3, "the drained accumulator is held in registers");
   extern __shared__ uint8_t gsm_raw[];
   uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full_bar[S], conv_bar[S], empty_bar[S];
@@ -298,7 +299,7 @@ __global__ void __launch_bounds__(G2T, 1)
   } else {
     // ---- split (and transpose the MN-major operands)
     const int ct = tid - 64;
-    const int q = warp & 3, half = (warp - 2) >> 2;
+    const int q = warp & 3, half = (warp - 2) >> 2;   // lane quarter, chunk group (0 .. NG-1)
     // DRAIN: this thread's share of the accumulator tile -- row 32 q + lane, columns
     // 32 half + 64 i + j (i < 2, j < 32): the same columns its epilogue writes
     float acc[DRAIN ? kCI : 1][32];
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(G2T, 1)
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
       for (int i = 0; i < (DRAIN ? kCI : 1); ++i) {
-        if (half + 2 * i >= kChunks) continue;
+        if (half + NG * i >= kChunks) continue;
         uint32_t r[32];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
@@ -322,7 +323,7 @@ __global__ void __launch_bounds__(G2T, 1)
               "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
               "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
               "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-            : "r"(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((c & 1) * BN + 32 * (half + 2 * i))));
+            : "r"(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((c & 1) * BN + 32 * (half + NG * i))));
         asm volatile("tcgen05.wait::ld.sync.aligned;");
 #pragma unroll
         for (int j = 0; j < 32; ++j) acc[i][j] += __uint_as_float(r[j]);
@@ -350,9 +351,9 @@ __global__ void __launch_bounds__(G2T, 1)
     // its 32-column chunks
     float *T = reinterpret_cast<float *>(sm) + (warp - 2) * 32 * 33;
 #pragma unroll
-    for (int ci = 0; ci < (DRAIN ? kCI : BN / (32 * (G2CW / 4))); ++ci) {
-      const int c0 = DRAIN ? 32 * (half + 2 * ci) : 32 * half + ci * 32 * (G2CW / 4);
-      if ((DRAIN && half + 2 * ci >= kChunks) || n0 + c0 >= g.N) break;
+    for (int ci = 0; ci < kCI; ++ci) {
+      const int c0 = 32 * (half + NG * ci);
+      if (half + NG * ci >= kChunks || n0 + c0 >= g.N) break;
       uint32_t r[32];
       if (DRAIN) {
 #pragma unroll
