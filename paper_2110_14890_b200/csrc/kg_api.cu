@@ -16,6 +16,10 @@
 #include <cstring>
 #include <string>
 #include <type_traits>
+#include <mutex>
+#include <condition_variable>
+#include <atomic>
+#include <chrono>
 #include <vector>
 
 #include "../../include/kg.h"
@@ -47,11 +51,243 @@ struct NcclApi {
   ncclResult_t (*GroupEnd)() = nullptr;
   const char *(*GetErrorString)(ncclResult_t) = nullptr;
 };
+// ------------------------------------------------------------------ loopback communicator
+// Test hook (KG_NCCL=loopback): the NCCL calls of step_dist for ranks that are threads of
+// ONE process sharing ONE device (the pool gives one GPU; NCCL refuses two ranks per GPU).
+// Every collective is a barrier-synchronised exchange of device buffers with cudaMemcpyAsync
+// between the ranks' streams (cross-stream events), reductions in rank order by a kernel --
+// the same data movement NCCL performs, so the routing kernels and the protocol of
+// step_dist run on the GPU end to end (tests/test_dist_loopback_gpu.py).  Not a transport.
+namespace loop {
+struct Op {
+  bool send;
+  const void *sbuf;
+  void *rbuf;
+  size_t bytes;
+  int peer;
+};
+struct Shared {
+  int world = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  int64_t gen = 0;
+  std::vector<std::vector<Op>> posts;        // per rank: its sends of the current exchange
+  std::vector<cudaEvent_t> ev_ready, ev_done;
+};
+struct Comm {
+  Shared *s;
+  int rank;
+  void *tmp = nullptr;
+  size_t tmp_bytes = 0;
+};
+std::mutex g_reg_mu;
+std::vector<std::pair<std::string, Shared *>> g_reg;
+thread_local std::vector<std::pair<Comm *, Op>> t_group;
+thread_local int t_depth = 0;
+thread_local cudaStream_t t_stream = nullptr;
+thread_local Comm *t_comm = nullptr;   // the calling rank's communicator (an empty group still joins)
+
+void barrier(Shared *s) {
+  std::unique_lock<std::mutex> lk(s->mu);
+  const int64_t g = s->gen;
+  if (++s->arrived == s->world) {
+    s->arrived = 0;
+    ++s->gen;
+    s->cv.notify_all();
+  } else {
+    s->cv.wait(lk, [&] { return s->gen != g; });
+  }
+}
+
+// one exchange: every rank posts its sends, then copies what it receives, then waits for the
+// peers' copies out of its buffers before its stream may overwrite them
+ncclResult_t exchange(Comm *c, const std::vector<Op> &ops, cudaStream_t st) {
+  Shared *s = c->s;
+  const int me = c->rank;
+  if (cudaEventRecord(s->ev_ready[me], st) != cudaSuccess) return ncclUnhandledCudaError;
+  {
+    std::lock_guard<std::mutex> lk(s->mu);
+    s->posts[me].clear();
+    for (auto &o : ops)
+      if (o.send) s->posts[me].push_back(o);
+  }
+  barrier(s);
+  std::vector<int> taken(s->world, 0);
+  for (auto &o : ops) {
+    if (o.send) continue;
+    const auto &src = s->posts[o.peer];
+    int k = -1, seen = 0;
+    for (size_t i = 0; i < src.size(); ++i)
+      if (src[i].peer == me && seen++ == taken[o.peer]) { k = (int)i; break; }
+    if (k < 0 || src[k].bytes != o.bytes) return ncclInvalidUsage;
+    ++taken[o.peer];
+    if (cudaStreamWaitEvent(st, s->ev_ready[o.peer], 0) != cudaSuccess ||
+        cudaMemcpyAsync(o.rbuf, src[k].sbuf, o.bytes, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return ncclUnhandledCudaError;
+  }
+  if (cudaEventRecord(s->ev_done[me], st) != cudaSuccess) return ncclUnhandledCudaError;
+  barrier(s);
+  for (int p = 0; p < s->world; ++p)
+    if (p != me && cudaStreamWaitEvent(st, s->ev_done[p], 0) != cudaSuccess) return ncclUnhandledCudaError;
+  barrier(s);
+  return ncclSuccess;
+}
+
+size_t type_size(ncclDataType_t t) {
+  switch (t) {
+    case ncclInt8: case ncclUint8: return 1;
+    case ncclFloat16: case ncclBfloat16: return 2;
+    case ncclInt32: case ncclUint32: case ncclFloat32: return 4;
+    default: return 8;
+  }
+}
+
+ncclResult_t GetUniqueId(ncclUniqueId *id) {
+  static std::atomic<uint64_t> ctr{1};
+  std::memset(id, 0, sizeof(*id));
+  const uint64_t v = ctr++ ^ (uint64_t)std::chrono::steady_clock::now().time_since_epoch().count();
+  std::memcpy(id->internal, &v, sizeof(v));
+  return ncclSuccess;
+}
+ncclResult_t CommInitRank(ncclComm_t *comm, int world, ncclUniqueId id, int rank) {
+  const std::string key(id.internal, sizeof(id.internal));
+  Shared *s = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    for (auto &e : g_reg)
+      if (e.first == key) s = e.second;
+    if (!s) {
+      s = new Shared();
+      s->world = world;
+      s->posts.resize(world);
+      s->ev_ready.resize(world);
+      s->ev_done.resize(world);
+      for (int r = 0; r < world; ++r)
+        if (cudaEventCreateWithFlags(&s->ev_ready[r], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s->ev_done[r], cudaEventDisableTiming) != cudaSuccess)
+          return ncclUnhandledCudaError;
+      g_reg.emplace_back(key, s);
+    }
+  }
+  if (s->world != world || rank < 0 || rank >= world) return ncclInvalidArgument;
+  Comm *c = new Comm{s, rank};
+  t_comm = c;
+  *comm = reinterpret_cast<ncclComm_t>(c);
+  return ncclSuccess;
+}
+ncclResult_t CommDestroy(ncclComm_t comm) {
+  Comm *c = reinterpret_cast<Comm *>(comm);
+  if (c->tmp) cudaFree(c->tmp);
+  delete c;
+  return ncclSuccess;
+}
+ncclResult_t GroupStart() {
+  ++t_depth;
+  return ncclSuccess;
+}
+ncclResult_t GroupEnd() {
+  if (--t_depth > 0) return ncclSuccess;
+  if (t_group.empty()) return t_comm ? exchange(t_comm, {}, t_stream) : ncclSuccess;
+  Comm *c = t_group.front().first;
+  std::vector<Op> ops;
+  for (auto &e : t_group) ops.push_back(e.second);
+  t_group.clear();
+  return exchange(c, ops, t_stream);
+}
+ncclResult_t p2p(bool send, const void *sb, void *rb, size_t count, ncclDataType_t t, int peer, ncclComm_t comm,
+                 cudaStream_t st) {
+  Comm *c = reinterpret_cast<Comm *>(comm);
+  Op o{send, sb, rb, count * type_size(t), peer};
+  t_stream = st;
+  t_comm = c;
+  if (t_depth > 0) {
+    t_group.emplace_back(c, o);
+    return ncclSuccess;
+  }
+  return exchange(c, {o}, st);
+}
+ncclResult_t Send(const void *b, size_t n, ncclDataType_t t, int peer, ncclComm_t comm, cudaStream_t st) {
+  return p2p(true, b, nullptr, n, t, peer, comm, st);
+}
+ncclResult_t Recv(void *b, size_t n, ncclDataType_t t, int peer, ncclComm_t comm, cudaStream_t st) {
+  return p2p(false, nullptr, b, n, t, peer, comm, st);
+}
+ncclResult_t AllGather(const void *sb, void *rb, size_t n, ncclDataType_t t, ncclComm_t comm, cudaStream_t st) {
+  Comm *c = reinterpret_cast<Comm *>(comm);
+  const size_t bytes = n * type_size(t);
+  std::vector<Op> ops;
+  for (int p = 0; p < c->s->world; ++p) {
+    ops.push_back(Op{true, sb, nullptr, bytes, p});
+    ops.push_back(Op{false, nullptr, static_cast<char *>(rb) + p * bytes, bytes, p});
+  }
+  return exchange(c, ops, st);
+}
+template <class T, bool MAX>
+__global__ void reduce_ranks_kernel(const T *tmp, int world, size_t n, T *out) {
+  const size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  T v = tmp[e];
+  for (int r = 1; r < world; ++r) v = MAX ? (tmp[r * n + e] > v ? tmp[r * n + e] : v) : v + tmp[r * n + e];
+  out[e] = v;
+}
+ncclResult_t AllReduce(const void *sb, void *rb, size_t n, ncclDataType_t t, ncclRedOp_t op, ncclComm_t comm,
+                       cudaStream_t st) {
+  Comm *c = reinterpret_cast<Comm *>(comm);
+  const int W = c->s->world;
+  const size_t bytes = n * type_size(t);
+  if (c->tmp_bytes < W * bytes) {   // (world > 1 steps are not graph-captured)
+    if (c->tmp) cudaFree(c->tmp);
+    if (cudaMalloc(&c->tmp, W * bytes) != cudaSuccess) return ncclSystemError;
+    c->tmp_bytes = W * bytes;
+  }
+  ncclResult_t r = AllGather(sb, c->tmp, n, t, comm, st);   // every rank's input, in rank order
+  if (r != ncclSuccess) return r;
+  const int g = (int)((n + 255) / 256);
+  if (op != ncclSum && op != ncclMax) return ncclInvalidArgument;
+  const bool mx = op == ncclMax;
+  switch (t) {
+    case ncclFloat32:
+      if (mx) reduce_ranks_kernel<float, true><<<g, 256, 0, st>>>((const float *)c->tmp, W, n, (float *)rb);
+      else reduce_ranks_kernel<float, false><<<g, 256, 0, st>>>((const float *)c->tmp, W, n, (float *)rb);
+      break;
+    case ncclFloat64:
+      if (mx) reduce_ranks_kernel<double, true><<<g, 256, 0, st>>>((const double *)c->tmp, W, n, (double *)rb);
+      else reduce_ranks_kernel<double, false><<<g, 256, 0, st>>>((const double *)c->tmp, W, n, (double *)rb);
+      break;
+    case ncclInt32:
+      if (mx) reduce_ranks_kernel<int, true><<<g, 256, 0, st>>>((const int *)c->tmp, W, n, (int *)rb);
+      else reduce_ranks_kernel<int, false><<<g, 256, 0, st>>>((const int *)c->tmp, W, n, (int *)rb);
+      break;
+    default:
+      return ncclInvalidArgument;
+  }
+  return cudaGetLastError() == cudaSuccess ? ncclSuccess : ncclUnhandledCudaError;
+}
+const char *GetErrorString(ncclResult_t) { return "loopback communicator error"; }
+}  // namespace loop
+
 const NcclApi &nccl() {
   static NcclApi api;
   static bool tried = false;
   if (tried) return api;
   tried = true;
+  if (const char *e = std::getenv("KG_NCCL")) {
+    if (std::string(e) == "loopback") {
+      api.GetUniqueId = loop::GetUniqueId;
+      api.CommInitRank = loop::CommInitRank;
+      api.CommDestroy = loop::CommDestroy;
+      api.AllGather = loop::AllGather;
+      api.AllReduce = loop::AllReduce;
+      api.Send = loop::Send;
+      api.Recv = loop::Recv;
+      api.GroupStart = loop::GroupStart;
+      api.GroupEnd = loop::GroupEnd;
+      api.GetErrorString = loop::GetErrorString;
+      api.ok = true;
+      return api;
+    }
+  }
   void *lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
 #ifdef KG_NCCL_PATH
   if (!lib) lib = dlopen(KG_NCCL_PATH, RTLD_NOW | RTLD_GLOBAL);

@@ -1,0 +1,84 @@
+"""Worker for tests/test_dist_loopback_gpu.py: world = 2 kg_step on ONE GPU, the two ranks as
+threads of this process, their collectives through the library's loopback communicator
+(KG_NCCL=loopback, kg_api.cu), checked against the oracle of the concatenated workers."""
+import os
+import sys
+import threading
+
+os.environ["KG_NCCL"] = "loopback"
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import kggen  # noqa: E402
+import oracle  # noqa: E402
+from paper_2110_14890_b200 import KGModel, nccl_unique_id  # noqa: E402
+
+RTOL = 1e-5
+
+
+def close(x, ref, what, mask=None):
+    x = np.asarray(x, np.float64)
+    ref = np.asarray(ref, np.float64)
+    err = np.abs(x - ref)
+    tol = RTOL * np.abs(ref) + RTOL * np.abs(ref).max()
+    bad = err > tol
+    if mask is not None:
+        bad &= mask
+    assert not bad.any(), f"{what}: {bad.sum()}/{bad.size} out of tolerance, max err {err.max():.3g}"
+
+
+def case(kind, structure, G=2, M=70, K=100, steps=2):
+    cfg = kggen.ModelConfig(kind, 40, 300, 7, hidden=24)
+    nid = nccl_unique_id()
+    table = oracle.SparseTable(cfg, 5)
+    models, errs = [None] * G, [None] * G
+    barrier = threading.Barrier(G)
+    for step in range(steps):
+        batches = [kggen.make_batch(cfg, structure, M, K, seed=1, step=step, rank=r, mask_p=0.9) for r in range(G)]
+        lr = 1e-6 if step == 0 else 1e-2          # as test_parity_gpu: step 1 tiny (H9), step 2 real
+        losses = [None] * G
+
+        def run(r):
+            try:
+                torch.cuda.set_device(0)
+                if models[r] is None:
+                    models[r] = KGModel(cfg, M, K, rank=r, world=G, nccl_id=nid)
+                    barrier.wait()
+                    models[r].init_params(5)
+                    models[r].set_apply(True)
+                barrier.wait()
+                losses[r] = models[r].step(models[r].host_batch(batches[r]), lr).loss
+            except Exception as e:   # reported below
+                errs[r] = e
+
+        th = [threading.Thread(target=run, args=(r,)) for r in range(G)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(120)
+        assert not any(t.is_alive() for t in th), "rank thread hung"
+        assert errs == [None] * G, errs
+        ref = oracle.oracle_step(cfg, table, batches, lr, apply=True)
+        for r in range(G):
+            assert abs(losses[r] - ref.loss) <= RTOL * abs(ref.loss) + 1e-12, (step, r, losses[r], ref.loss)
+        keep = np.abs(ref.m_new) >= 1e-4 * np.abs(ref.m_new).max()
+        for r in range(G):      # every rank's shard rows after the owner-side update
+            own = ref.uniq % G == r
+            close(models[r].read_rows(ref.uniq[own]), ref.rows_new[own], f"{kind} {structure} rank {r} rows",
+                  keep[own])
+        dense = [m.read_dense(0) for m in models]
+        assert all(np.array_equal(dense[0], x) for x in dense[1:]), "theta_D differs between ranks"
+        keepd = np.abs(ref.dense_m_new) >= 1e-4 * np.abs(ref.dense_m_new).max()
+        close(dense[0], ref.dense_new, f"{kind} {structure} theta_D", keepd)
+    for m in models:
+        m.close()
+    print("ok", kind, structure, G, flush=True)
+
+
+if __name__ == "__main__":
+    for arg in sys.argv[1:]:
+        parts = arg.split(":")
+        case(parts[0], parts[1], G=int(parts[2]) if len(parts) > 2 else 2)

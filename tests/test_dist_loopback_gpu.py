@@ -1,0 +1,23 @@
+"""The world > 1 training step (kg_api.cu step_dist, k_dist.cu routing kernels) on the GPU:
+two ranks as threads of one process on one B200, their NCCL calls served by the library's
+loopback communicator (KG_NCCL=loopback: the same buffers exchanged with device copies, rank-
+order reductions) -- the pool has one GPU and NCCL refuses two ranks per device.  Checked
+against the fp64 oracle of the concatenated workers (reading A18) over two steps: the loss
+on every rank, every owner's updated rows, and theta_D (bitwise equal on both ranks)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def test_two_ranks_match_the_oracle():
+    cases = ["q2b:ip", "gqe:up", "betae:pni", "betae:3i", "complex:1p", "q2b:3p", "distmult-m:pi",
+             "q2b:2i:4", "betae:ip:4"]
+    r = subprocess.run([sys.executable, os.path.join(HERE, "_loopback_worker.py"), *cases],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("ok ") == len(cases), r.stdout
