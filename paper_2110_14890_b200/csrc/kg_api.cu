@@ -1102,8 +1102,14 @@ kg_status ingest(kg_handle *h, const kg_batch *b, bool train, const Plan &plan, 
 }
 
 void mark(kg_handle *h, int i, cudaStream_t s = nullptr) {
-  // external: inside a stream capture this becomes an event-record node of the graph
-  if (h->timing) cudaEventRecordWithFlags(h->sev[i], s ? s : h->st, cudaEventRecordExternal);
+  if (!h->timing) return;
+  // external: inside a stream capture this becomes an event-record node of the graph; outside a
+  // capture (world > 1, KG_NO_GRAPH) the flag is not allowed and a plain record is used
+  cudaStream_t st = s ? s : h->st;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(h->sev[i], st, cudaEventRecordExternal);
+  else cudaEventRecord(h->sev[i], st);
 }
 
 kg_status read_result(kg_handle *h, kg_step_info *info) {

@@ -48,7 +48,7 @@ def case(kind, structure, G=2, M=70, K=100, steps=2):
                     models[r] = KGModel(cfg, M, K, rank=r, world=G, nccl_id=nid)
                     barrier.wait()
                     models[r].init_params(5)
-                    models[r].set_apply(True)
+                    models[r].set_apply(True, stage_timing=True)   # the eager stage events too
                 barrier.wait()
                 losses[r] = models[r].step(models[r].host_batch(batches[r]), lr).loss
             except Exception as e:   # reported below

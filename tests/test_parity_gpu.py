@@ -341,3 +341,19 @@ def test_bind_rejects_pageable_host_memory():
                      m.dense_m.data_ptr(), m.dense_v.data_ptr())
     assert kg.kg_bind(m.h, C.byref(t), C.c_void_p(m.stream.cuda_stream)) == kg.KG_EINVAL
     m.close()
+
+
+def test_stage_timing_with_and_without_graphs(monkeypatch):
+    """kg_set_apply bit 2 (stage events) works in graph replay and in eager launches (world > 1
+    and KG_NO_GRAPH run eagerly): every stage time is finite and they add up to the step."""
+    cfg = kggen.ModelConfig("q2b", 40, 300, 7)
+    for no_graph in ("0", "1"):
+        monkeypatch.setenv("KG_NO_GRAPH", no_graph)
+        gm = _model(cfg, 70, 100)
+        gm.set_apply(True, stage_timing=True)
+        for s in range(3):
+            info = gm.step(gm.host_batch(kggen.make_batch(cfg, "2i", 70, 100, seed=16, step=s)), 0.01)
+        st = np.array(info.stage_ms[:10])
+        assert np.all(np.isfinite(st)) and np.all(st >= 0) and st[7] > 0, st
+        assert abs(st[:7].sum() - st[7]) <= 0.05 * st[7] + 1e-3, st
+        gm.close()
