@@ -136,10 +136,11 @@ __global__ void __launch_bounds__(256) sparse_adam_kernel(const int64_t *uniq, c
                                                           const int32_t *perm, const int32_t *U_dev, const float *OG,
                                                           const float *PS, int d, int world, float *ent, float *m,
                                                           float *v, float *grad_out, const float *lr_dev, AdamHyper hy,
-                                                          const float *bc, const int *flags, int apply) {
+                                                          const float *bc, const int *flags, int apply,
+                                                          int64_t skip_key) {
   KG_GRID_DEP_WAIT();
   const int u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (u >= *U_dev) return;
+  if (u >= *U_dev || uniq[u] == skip_key) return;   // skip_key: the empty-slot key of bucketed exchanges
   const int d4 = d >> 2, s0 = seg[u], s1 = seg[u + 1];
   const bool upd = apply && !flags[0];
   const float lr1 = *lr_dev * bc[0], ibc2 = bc[1];
@@ -173,12 +174,12 @@ __global__ void __launch_bounds__(256) sparse_adam_kernel(const int64_t *uniq, c
 void launch_sparse_adam(const int64_t *uniq, const int32_t *seg, const int32_t *perm, const int32_t *inv,
                         const int32_t *U_dev, int L, const float *OG, float *PS, int d, int world, float *ent,
                         float *m, float *v, float *grad_out, const float *lr, double beta1, double beta2, double eps,
-                        const float *bc, const int *flags, int apply, cudaStream_t st) {
+                        const float *bc, const int *flags, int apply, cudaStream_t st, int64_t skip_key) {
   if (L <= 0) return;
   { seg_piece_kernel<<<(L + kPiece - 1) / kPiece, 128, 0, st>>>(perm, inv, seg, L, OG, d / 4, PS); ++g_launches; }
   { sparse_adam_kernel<<<(L + 7) / 8, 256, 0, st>>>(uniq, seg, perm, U_dev, OG, PS, d, world, ent, m, v,
                                                               grad_out, lr, hyper(beta1, beta2, eps), bc, flags,
-                                                              apply); ++g_launches; }
+                                                              apply, skip_key); ++g_launches; }
 }
 
 // Phase 2 for the relation rows: RGU[u] = sum of the occurrence rows of relation u.

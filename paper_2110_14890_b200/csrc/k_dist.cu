@@ -16,10 +16,12 @@ constexpr int kPartThreads = 1024;
 // Stable partition of the distinct ids (ascending) by owner: send_ids[pos] = uniq[u]
 // with pos = offset[owner] + (rank of u among the ids of that owner); send_pos[u] = pos;
 // counts[o] = number of distinct ids owned by o.  One CTA; per-thread contiguous
-// ranges keep the order stable.
+// ranges keep the order stable.  cap > 0: fixed-capacity buckets instead (offset[o] =
+// o * cap, the caller pre-fills send_ids with -1 = empty slot); an id ranked >= cap in its
+// bucket is not sent and flags[1] = 2 marks the step as not applicable (bucket overflow).
 __global__ void __launch_bounds__(kPartThreads) owner_partition_kernel(const int64_t *uniq, const int32_t *U_dev,
                                                                        int G, int64_t *send_ids, int32_t *send_pos,
-                                                                       int32_t *counts) {
+                                                                       int32_t *counts, int cap, int *flags) {
   KG_GRID_DEP_WAIT();
   __shared__ int32_t s_cnt[kMaxWorld][kPartThreads];
   __shared__ int32_t s_base[kMaxWorld + 1];
@@ -50,7 +52,11 @@ __global__ void __launch_bounds__(kPartThreads) owner_partition_kernel(const int
   __syncthreads();
   if (t == 0) {
     s_base[0] = 0;
-    for (int o = 1; o <= G; ++o) s_base[o] += s_base[o - 1];
+    if (cap > 0) {
+      for (int o = 0; o <= G; ++o) s_base[o] = o * cap;
+    } else {
+      for (int o = 1; o <= G; ++o) s_base[o] += s_base[o - 1];
+    }
   }
   __syncthreads();
   int run[kMaxWorld];
@@ -62,14 +68,19 @@ __global__ void __launch_bounds__(kPartThreads) owner_partition_kernel(const int
 #pragma unroll
     for (int q = 0; q < kMaxWorld; ++q)
       if (q == o) pos = run[q]++;
-    send_ids[pos] = uniq[u];
+    if (cap > 0 && pos >= (o + 1) * cap) {   // bucket overflow: the step will not be applied
+      flags[1] = 2;
+      pos = o * cap;
+    } else {
+      send_ids[pos] = uniq[u];
+    }
     send_pos[u] = pos;
   }
 }
 
 void launch_owner_partition(const int64_t *uniq, const int32_t *U_dev, int G, int64_t *send_ids, int32_t *send_pos,
-                            int32_t *counts, cudaStream_t st) {
-  { owner_partition_kernel<<<1, kPartThreads, 0, st>>>(uniq, U_dev, G, send_ids, send_pos, counts); ++g_launches; }
+                            int32_t *counts, cudaStream_t st, int cap, int *flags) {
+  { owner_partition_kernel<<<1, kPartThreads, 0, st>>>(uniq, U_dev, G, send_ids, send_pos, counts, cap, flags); ++g_launches; }
 }
 
 // rows[p] = send_pos[inv[p]]: the occurrence's row in the received (owner-grouped) row buffer.
@@ -88,7 +99,9 @@ __global__ void gather_owned_kernel(const float *ent, const int64_t *ids, int n,
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)n * d4) return;
   const int i = (int)(e / d4), c = (int)(e - (int64_t)i * d4);
-  out[e] = reinterpret_cast<const float4 *>(ent)[(ids[i] / G) * d4 + c];
+  const int64_t id = ids[i];
+  if (id < 0) return;   // empty bucket slot
+  out[e] = reinterpret_cast<const float4 *>(ent)[(id / G) * d4 + c];
 }
 void launch_gather_owned(const float *ent, const int64_t *ids, int n, int G, int d, float *out, cudaStream_t st) {
   const int64_t m = (int64_t)n * (d / 4);
@@ -117,14 +130,15 @@ void launch_reorder_rows(const float *Gu, const int32_t *send_pos, const int32_t
   }
 }
 
-// keys[i] = ids[i] / G (owner-local rows of the received ids, for the owner-side merge).
-__global__ void local_rows_kernel(const int64_t *ids, int n, int G, int64_t *keys) {
+// keys[i] = ids[i] / G (owner-local rows of the received ids, for the owner-side merge);
+// empty bucket slots (id < 0) get the key `empty` (one past the last local row).
+__global__ void local_rows_kernel(const int64_t *ids, int n, int G, int64_t *keys, int64_t empty) {
   KG_GRID_DEP_WAIT();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) keys[i] = ids[i] / G;
+  if (i < n) keys[i] = ids[i] < 0 ? empty : ids[i] / G;
 }
-void launch_local_rows(const int64_t *ids, int n, int G, int64_t *keys, cudaStream_t st) {
-  if (n > 0) { local_rows_kernel<<<(n + 255) / 256, 256, 0, st>>>(ids, n, G, keys); ++g_launches; }
+void launch_local_rows(const int64_t *ids, int n, int G, int64_t *keys, cudaStream_t st, int64_t empty) {
+  if (n > 0) { local_rows_kernel<<<(n + 255) / 256, 256, 0, st>>>(ids, n, G, keys, empty); ++g_launches; }
 }
 
 // Dense relation gradient (for the all-reduce): gfull[s*R*w + r*w + c] = RGU[u][s*w + c]

@@ -474,6 +474,9 @@ struct kg_handle {
   const float *ent_src = nullptr;       // rows read by the step: theta_E (world 1) or the received rows
   float *gfull = nullptr;               // dense dL/dtheta_D [dense_size] (weights part = gdense)
   int64_t *send_ids = nullptr, *recv_ids = nullptr, *recv_keys = nullptr, *ouniq = nullptr;
+  int cap = 0;             // bucket capacity per owner (ids) of the fixed-capacity exchange
+  bool buckets = true;     // fixed-capacity exchange (no host round trip); KG_DIST_BUCKETS=0: exact counts
+  bool dist_graph = true;  // capture world > 1 steps (NCCL only); KG_DIST_GRAPH=0: eager
   int32_t *send_pos = nullptr, *counts = nullptr, *all_counts = nullptr, *oinv = nullptr, *operm = nullptr,
           *oseg = nullptr, *oU = nullptr;
   float *Xin = nullptr, *send_rows = nullptr, *Gsend = nullptr, *Grecv = nullptr, *PSo = nullptr;
@@ -679,7 +682,11 @@ void carve(kg_handle *h, Arena &A) {
   }
   if (h->world > 1) {
     const int64_t GL = (int64_t)h->world * h->Lx;
-    h->send_ids = A.take<int64_t>(h->Lx);
+    // fixed-capacity exchange buckets: twice the mean share of distinct ids per
+    // owner + 256, at most all of them
+    h->cap = (int)std::min<int64_t>(h->Lx, 2 * ((h->Lx + h->world - 1) / h->world) + 256);
+    const int64_t SL = std::max<int64_t>(h->Lx, (int64_t)h->world * h->cap);
+    h->send_ids = A.take<int64_t>(SL);
     h->send_pos = A.take<int32_t>(h->Lx);
     h->counts = A.take<int32_t>(kMaxWorld);
     h->all_counts = A.take<int32_t>(kMaxWorld * kMaxWorld);
@@ -690,9 +697,9 @@ void carve(kg_handle *h, Arena &A) {
     h->operm = A.take<int32_t>(GL);
     h->oseg = A.take<int32_t>(GL + 1);
     h->oU = A.take<int32_t>(1);
-    h->Xin = A.take<float>((int64_t)h->Lx * d);
+    h->Xin = A.take<float>(SL * d);
     h->send_rows = A.take<float>(GL * d);
-    h->Gsend = A.take<float>((int64_t)h->Lx * d);
+    h->Gsend = A.take<float>(SL * d);
     h->Grecv = A.take<float>(GL * d);
     h->PSo = A.take<float>(GL * d);
   }
@@ -739,11 +746,11 @@ struct OnStream {
     h->side = false;
   }
 };
-// Programmatic dependent launch inside the step graph: every kernel-to-kernel edge whose
-// downstream kernel is one of this library's (they all begin with griddepcontrol.wait,
-// KG_GRID_DEP_WAIT) becomes a programmatic edge, so the downstream grid is launched as the
-// upstream one drains instead of after it has completed; the wait keeps the data dependence.
-// Edges into library kernels of other modules (cuBLAS) and through event nodes are kept.
+// Programmatic dependent launch inside the step graph: every edge between two of this
+// library's kernels (they all begin with griddepcontrol.wait, KG_GRID_DEP_WAIT) becomes a
+// programmatic edge, so the downstream grid is launched as the upstream one drains instead of
+// after it has completed; the wait keeps the data dependence.  Edges touching kernels of
+// other modules (cuBLAS, NCCL) and event nodes are kept as they are.
 bool ours(cudaGraphNode_t n) {
   cudaGraphNodeType t;
   if (cudaGraphNodeGetType(n, &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) return false;
@@ -751,10 +758,6 @@ bool ours(cudaGraphNode_t n) {
   if (cudaGraphKernelNodeGetParams(n, &kp) != cudaSuccess || !kp.func) { cudaGetLastError(); return false; }
   Dl_info info;
   return dladdr(kp.func, &info) && info.dli_fname && std::strstr(info.dli_fname, "libkg") != nullptr;
-}
-bool is_kernel(cudaGraphNode_t n) {
-  cudaGraphNodeType t;
-  return cudaGraphNodeGetType(n, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel;
 }
 int make_programmatic(cudaGraph_t g) {
   size_t n = 0;
@@ -765,7 +768,7 @@ int make_programmatic(cudaGraph_t g) {
   int converted = 0;
   for (size_t i = 0; i < n; ++i) {
     if (ed[i].type != cudaGraphDependencyTypeDefault || ed[i].from_port != 0) continue;
-    if (!is_kernel(from[i]) || !ours(to[i])) continue;
+    if (!ours(from[i]) || !ours(to[i])) continue;   // library kernels on both ends (not cuBLAS / NCCL)
     if (cudaGraphRemoveDependencies_v2(g, &from[i], &to[i], &ed[i], 1) != cudaSuccess) { cudaGetLastError(); continue; }
     cudaGraphEdgeData e{};
     e.from_port = cudaGraphKernelNodePortProgrammatic;
@@ -1131,6 +1134,9 @@ kg_status read_result(kg_handle *h, kg_step_info *info) {
       }
     }
   }
+  if (h->hout->flags[1] == 2)
+    return fail(h, KG_EINVAL, "row exchange bucket overflow (the batch's distinct ids concentrate on one owner beyond "
+                              "the fixed capacity); step not applied -- KG_DIST_BUCKETS=0 exchanges exact counts");
   if (h->hout->flags[1]) return fail(h, KG_EINVAL, "an id or relation of the (device) batch was out of range; step not applied");
   if (h->hout->flags[0]) return fail(h, KG_ENONFINITE, "non-finite loss; step not applied");
   return KG_OK;
@@ -1220,6 +1226,9 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
   }
   if (const char *e = std::getenv("KG_NO_GRAPH")) h->use_graphs = !(e[0] == '1');
   if (const char *e = std::getenv("KG_PDL")) h->use_pdl = !(e[0] == '0');
+  if (const char *e = std::getenv("KG_DIST_BUCKETS")) h->buckets = !(e[0] == '0');
+  if (const char *e = std::getenv("KG_DIST_GRAPH")) h->dist_graph = !(e[0] == '0');
+  if (const char *e = std::getenv("KG_NCCL")) if (std::string(e) == "loopback") h->dist_graph = false;
   // DAG contractions (reading A24): the hand-written tcgen05 3xTF32 kernel
   // (k_gemm.cu) in its drained form: TMEM accumulates 4 k-blocks at a time and the chunks are
   // summed in fp32 registers -- a long TMEM accumulation carries 15-25x SGEMM's error
@@ -1486,15 +1495,24 @@ kg_status step_dist(kg_handle *h, StepBufs &S) {
   launch_rel_occ(h->b_rels, M, nr, sl, p.nproj, h->R, h->rocc, h->flags + 1, st);
   launch_dedup(h->ids, nullptr, L, h->ent_bits, h->uniq, h->inv, h->perm, h->seg, h->Udev, st);
   launch_dedup(nullptr, h->rocc, Lr, h->rel_bits, h->runiq, h->rinv, h->rperm, h->rseg, h->rU, st);
-  // a3: route the distinct ids to their owners (owner = id % G)
-  launch_owner_partition(h->uniq, h->Udev, G, h->send_ids, h->send_pos, h->counts, st);
-  NCK(nccl().AllGather(h->counts, h->all_counts, kMaxWorld, ncclInt32, h->comm, st));
-  CK(cudaMemcpyAsync(h->h_counts, h->all_counts, sizeof(int32_t) * kMaxWorld * G, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  // a3: route the distinct ids to their owners (owner = id % G).  Buckets: every rank sends
+  // `cap` slots to every owner (empty slots = -1), so no size is read on the host and the
+  // step needs no host round trip; otherwise exact counts are all-gathered and read first.
+  const int cap = h->buckets ? h->cap : 0;
   std::vector<int64_t> so(G + 1, 0), ro(G + 1, 0);   // send / receive offsets (rows)
-  for (int o = 0; o < G; ++o) {
-    so[o + 1] = so[o] + h->h_counts[me * kMaxWorld + o];
-    ro[o + 1] = ro[o] + h->h_counts[o * kMaxWorld + me];
+  if (cap > 0) {
+    CK(cudaMemsetAsync(h->send_ids, 0xff, sizeof(int64_t) * G * cap, st));
+    launch_owner_partition(h->uniq, h->Udev, G, h->send_ids, h->send_pos, h->counts, st, cap, h->flags);
+    for (int o = 0; o <= G; ++o) so[o] = ro[o] = (int64_t)o * cap;
+  } else {
+    launch_owner_partition(h->uniq, h->Udev, G, h->send_ids, h->send_pos, h->counts, st);
+    NCK(nccl().AllGather(h->counts, h->all_counts, kMaxWorld, ncclInt32, h->comm, st));
+    CK(cudaMemcpyAsync(h->h_counts, h->all_counts, sizeof(int32_t) * kMaxWorld * G, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int o = 0; o < G; ++o) {
+      so[o + 1] = so[o] + h->h_counts[me * kMaxWorld + o];
+      ro[o + 1] = ro[o] + h->h_counts[o * kMaxWorld + me];
+    }
   }
   const int Rtot = (int)ro[G];
   NCK(nccl().GroupStart());
@@ -1570,12 +1588,13 @@ kg_status step_dist(kg_handle *h, StepBufs &S) {
   }
   NCK(nccl().GroupEnd());
   // a13 at the owner: merge the contributions of all ranks (fixed order) + sparse Adam on local rows
-  launch_local_rows(h->recv_ids, Rtot, G, h->recv_keys, st);
-  launch_dedup(h->recv_keys, nullptr, Rtot, bits_for(h->shard), h->ouniq, h->oinv, h->operm, h->oseg, h->oU, st);
+  // empty bucket slots carry the key `shard` (one past the last local row), skipped by the update
+  launch_local_rows(h->recv_ids, Rtot, G, h->recv_keys, st, h->shard);
+  launch_dedup(h->recv_keys, nullptr, Rtot, bits_for(h->shard + 1), h->ouniq, h->oinv, h->operm, h->oseg, h->oU, st);
   if (h->apply)
     launch_sparse_adam(h->ouniq, h->oseg, h->operm, h->oinv, h->oU, Rtot, h->Grecv, h->PSo, d, 1, h->t.ent,
                        h->t.ent_m, h->t.ent_v, nullptr, h->lr_dev, h->cfg.beta1, h->cfg.beta2, h->cfg.eps, h->bc,
-                       h->flags, 1, st);
+                       h->flags, 1, st, /*skip_key=*/h->shard);
   mark(h, 6);
   // a14: dense dL/dtheta_D -> all-reduce -> dense Adam (identical on every rank)
   launch_rel_reduce(h->rseg, h->rperm, h->rinv, h->rU, Lr, h->RG, h->PSr, h->dr, h->RGU, st);
@@ -1615,13 +1634,17 @@ kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info)
   h->stamp++;
   if ((s = ingest(h, b, true, p, lr)) != KG_OK) return s;
   h->last_M = S.M; h->last_K = S.K;
-  if (h->world > 1) {
+  // world > 1 is captured too when its exchange has fixed sizes (buckets) and the
+  // communicator is NCCL (the loopback test communicator synchronises on the host)
+  const bool graph_ok = h->use_graphs && (h->world == 1 || (h->buckets && h->dist_graph));
+  if (!graph_ok) {
     const int64_t l0 = g_launches;
     h->gemm_count = 0;
-    if ((s = step_dist(h, S)) != KG_OK) return s;
+    if ((s = h->world > 1 ? step_dist(h, S) : enqueue_step(h, S)) != KG_OK) return s;
     h->last_kernels = (int)(g_launches - l0);
     h->last_gemms = h->gemm_count;
   } else if (h->use_graphs) {
+    bool eager_done = false;   // world > 1 whose capture failed: ran eagerly instead
     kg_handle::GraphEntry *g = nullptr;
     for (auto &e : h->graphs)
       if (e.structure == b->structure && e.M == S.M && e.K == S.K && e.flags == h->flag_key()) { g = &e; break; }
@@ -1633,11 +1656,24 @@ kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info)
       const int64_t l0 = g_launches;
       h->gemm_count = 0;
       CK(cudaStreamBeginCapture(h->st_cap, cudaStreamCaptureModeThreadLocal));
-      s = enqueue_step(h, S);
+      s = h->world > 1 ? step_dist(h, S) : enqueue_step(h, S);
       cudaGraph_t graph = nullptr;
       cudaError_t ce = cudaStreamEndCapture(h->st_cap, &graph);
       h->st = user;
       CKB(cublasSetStream(h->blas, user));
+      if (h->world > 1 && (s != KG_OK || ce != cudaSuccess)) {
+        // the collectives could not be captured: this and later steps run eagerly
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        h->dist_graph = false;
+        const int64_t l0e = g_launches;
+        h->gemm_count = 0;
+        if ((s = step_dist(h, S)) != KG_OK) return s;
+        h->last_kernels = (int)(g_launches - l0e);
+        h->last_gemms = h->gemm_count;
+        eager_done = true;
+      }
+      if (!eager_done) {
       if (s != KG_OK) { if (graph) cudaGraphDestroy(graph); return s; }
       if (ce != cudaSuccess) return fail(h, KG_ECUDA, std::string("stream capture: ") + cudaGetErrorString(ce));
       kg_handle::GraphEntry e{};
@@ -1651,10 +1687,13 @@ kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info)
       if (h->graphs.size() >= 64) { cudaGraphExecDestroy(h->graphs.front().exec); h->graphs.erase(h->graphs.begin()); }
       h->graphs.push_back(e);
       g = &h->graphs.back();
+      }
     }
-    CK(cudaGraphLaunch(g->exec, h->st));
-    h->last_kernels = g->kernels;
-    h->last_gemms = g->gemms;
+    if (!eager_done) {
+      CK(cudaGraphLaunch(g->exec, h->st));
+      h->last_kernels = g->kernels;
+      h->last_gemms = g->gemms;
+    }
   } else {
     const int64_t l0 = g_launches;
     h->gemm_count = 0;

@@ -67,7 +67,7 @@ void launch_init_flat(float *p, int64_t n, uint64_t seed, uint64_t stream, float
 void launch_sparse_adam(const int64_t *uniq, const int32_t *seg, const int32_t *perm, const int32_t *inv,
                         const int32_t *U_dev, int L, const float *OG, float *PS, int d, int world, float *ent,
                         float *m, float *v, float *grad_out, const float *lr, double beta1, double beta2, double eps,
-                        const float *bc, const int *flags, int apply, cudaStream_t st);
+                        const float *bc, const int *flags, int apply, cudaStream_t st, int64_t skip_key = -1);
 void launch_rel_reduce(const int32_t *seg, const int32_t *perm, const int32_t *inv, const int32_t *U_dev, int Lr,
                        const float *RG, float *PS, int dr, float *RGU, cudaStream_t st);
 void launch_rel_stamp(const int64_t *uniq_rel, const int32_t *U_dev, int Lmax, int32_t *rel_seg, int64_t *rel_stamp,
@@ -115,12 +115,12 @@ void launch_eval(int kind, const EvalArgs &a, int nout, cudaStream_t st);
 
 // k_dist.cu (world > 1)
 void launch_owner_partition(const int64_t *uniq, const int32_t *U_dev, int G, int64_t *send_ids, int32_t *send_pos,
-                            int32_t *counts, cudaStream_t st);
+                            int32_t *counts, cudaStream_t st, int cap = 0, int *flags = nullptr);
 void launch_occ_rows(const int32_t *inv, const int32_t *send_pos, int L, int64_t *rows, cudaStream_t st);
 void launch_gather_owned(const float *ent, const int64_t *ids, int n, int G, int d, float *out, cudaStream_t st);
 void launch_reorder_rows(const float *Gu, const int32_t *send_pos, const int32_t *U_dev, int Lmax, int d, float *out,
                          cudaStream_t st);
-void launch_local_rows(const int64_t *ids, int n, int G, int64_t *keys, cudaStream_t st);
+void launch_local_rows(const int64_t *ids, int n, int G, int64_t *keys, cudaStream_t st, int64_t empty = -1);
 void launch_scatter_rel(const float *RGU, const int64_t *runiq, const int32_t *rU, int Lrmax, int R, int w, int nseg,
                         float *gfull, cudaStream_t st);
 void launch_loss_check(double *loss_out, int *flags, int64_t *t_dev, float *bc, double beta1, double beta2, int apply,

@@ -14,10 +14,12 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def test_two_ranks_match_the_oracle():
+@pytest.mark.parametrize("buckets", ["1", "0"])
+def test_ranks_match_the_oracle(buckets):
+    """buckets = 1: fixed-capacity exchange (the default, no host round trip); 0: exact counts."""
     cases = ["q2b:ip", "gqe:up", "betae:pni", "betae:3i", "complex:1p", "q2b:3p", "distmult-m:pi",
              "q2b:2i:4", "betae:ip:4"]
     r = subprocess.run([sys.executable, os.path.join(HERE, "_loopback_worker.py"), *cases],
-                       capture_output=True, text=True, timeout=600)
+                       capture_output=True, text=True, timeout=600, env=dict(os.environ, KG_DIST_BUCKETS=buckets))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("ok ") == len(cases), r.stdout
