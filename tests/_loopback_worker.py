@@ -78,7 +78,53 @@ def case(kind, structure, G=2, M=70, K=100, steps=2):
     print("ok", kind, structure, G, flush=True)
 
 
+def overflow_case(G=4, M=200, K=100):
+    """Distinct ids that all belong to one owner overflow its fixed-capacity bucket: every rank's
+    kg_step fails with the bucket-overflow error and no table changes (transactional)."""
+    cfg = kggen.ModelConfig("q2b", 40, 40000, 7)
+    nid = nccl_unique_id()
+    models, errs, before = [None] * G, [None] * G, [None] * G
+    barrier = threading.Barrier(G)
+    b = kggen.make_batch(cfg, "3i", M, K, seed=1, step=0, mask_p=0.9)
+    ids = 4 * np.arange(M * 3 + M + K, dtype=np.int64)          # all owned by rank 0, all distinct
+    b["anchors"] = ids[:3 * M].reshape(M, 3)
+    b["answers"] = ids[3 * M:4 * M]
+    b["negatives"] = ids[4 * M:]
+
+    def run(r):
+        try:
+            torch.cuda.set_device(0)
+            models[r] = KGModel(cfg, M, K, rank=r, world=G, nccl_id=nid)
+            barrier.wait()
+            models[r].init_params(5)
+            models[r].set_apply(True)
+            own = ids[ids % G == r][:64]
+            before[r] = (own, models[r].read_rows(own) if len(own) else None, models[r].read_dense(0))
+            barrier.wait()
+            models[r].step(models[r].host_batch(b), 0.01)
+        except Exception as e:
+            errs[r] = e
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(120)
+    assert not any(t.is_alive() for t in th), "rank thread hung"
+    assert all(e is not None and "overflow" in str(e) for e in errs), errs
+    for r in range(G):
+        own, rows, dense = before[r]
+        if rows is not None:
+            assert np.array_equal(models[r].read_rows(own), rows)
+        assert np.array_equal(models[r].read_dense(0), dense)
+        models[r].close()
+    print("ok overflow", G, flush=True)
+
+
 if __name__ == "__main__":
     for arg in sys.argv[1:]:
+        if arg == "overflow":
+            overflow_case()
+            continue
         parts = arg.split(":")
         case(parts[0], parts[1], G=int(parts[2]) if len(parts) > 2 else 2)

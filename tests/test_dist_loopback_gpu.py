@@ -23,3 +23,12 @@ def test_ranks_match_the_oracle(buckets):
                        capture_output=True, text=True, timeout=600, env=dict(os.environ, KG_DIST_BUCKETS=buckets))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("ok ") == len(cases), r.stdout
+
+
+def test_bucket_overflow_is_reported_and_transactional():
+    """Fixed-capacity buckets: distinct ids concentrated on one owner beyond its capacity make
+    every rank's kg_step fail with the overflow error, and no table changes."""
+    r = subprocess.run([sys.executable, os.path.join(HERE, "_loopback_worker.py"), "overflow"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "ok overflow" in r.stdout, r.stdout
