@@ -344,7 +344,7 @@ def sampler_e2e(args, gm, cfg, w, M, K, world, rank):
     smp = KGSampler(kg, n_threads=threads)
     t_idx = time.perf_counter() - t0
     del kg
-    workers = max(1, threads - 1)
+    workers = max(1, threads - 2)   # leave the driving thread (kg_step) a core of its own
     pipe = smp.pipeline(w.structures, M, K, seed=args.seed, rank=rank, first_step=0, depth=2 * workers,
                         n_workers=workers, pin=True)
     for _ in range(2 * workers):                  # warm-up: fill the ring once
