@@ -84,6 +84,15 @@ kgs_status kgs_verify(const kgs_graph *g, int32_t structure, int32_t M, const in
                       const int32_t *relations, int32_t n_cand, const int64_t *cand, int32_t shared,
                       uint8_t *is_answer, int32_t n_threads);
 
+/* Answer sets of M given queries by full forward traversal (App. A set semantics; the
+ * evaluation set of App. E, needs A_q on G_train / G_valid / G_test):
+ * offsets [M + 1] (int64) and, when ids is not NULL, ids [offsets[M]] (ascending per query).
+ * Call once with ids = NULL to size the output, then with ids of capacity cap >= offsets[M].
+ * KGS_EINVAL if a query's answer set is a complement (a negation at the root: none of the 14
+ * structures) or cap is too small. */
+kgs_status kgs_answers(const kgs_graph *g, int32_t structure, int32_t M, const int64_t *anchors,
+                       const int32_t *relations, int64_t *offsets, int64_t *ids, int64_t cap, int32_t n_threads);
+
 /* Asynchronous pipeline: n_workers threads produce the batches of steps first_step,
  * first_step + 1, ... (structure of step s = structures[s % n_structures]) into a ring
  * of `depth` >= n_workers slots; the graph must outlive the pipeline. */

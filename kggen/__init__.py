@@ -297,6 +297,22 @@ def make_kg(n_entities: int, n_relations: int, n_edges: int, seed: int = 0, a: f
                 t=t.astype(np.int64), n_entities=int(n_entities), n_relations=int(n_relations))
 
 
+def split_kg(kg: dict, valid_frac: float = 0.06, test_frac: float = 0.07, seed: int = 0):
+    """Random edge split into G_train, G_valid = train + valid, G_test = train + valid + test
+    (App. E; fractions of Table 3's FB15k-237 split).  Returns three KG dicts."""
+    rng = np.random.default_rng([seed, 0x5917])
+    E = len(kg["h"])
+    u = rng.random(E)
+    tr = u >= valid_frac + test_frac
+    va = u < valid_frac + test_frac
+    te = u < test_frac
+
+    def sub(m):
+        return dict(h=kg["h"][m], r=kg["r"][m], t=kg["t"][m], n_entities=kg["n_entities"],
+                    n_relations=kg["n_relations"])
+    return sub(tr), sub(tr | (va & ~te)), sub(np.ones(E, bool))
+
+
 # Table 3 shapes (training edges), for the sampler benches and tests
 KG_SHAPES = {
     "FB15k-237": (14505, 237, 272115),

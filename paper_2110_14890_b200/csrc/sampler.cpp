@@ -653,6 +653,40 @@ kgs_status kgs_verify(const kgs_graph *g, int32_t structure, int32_t M, const in
   return KGS_OK;
 }
 
+kgs_status kgs_answers(const kgs_graph *g, int32_t structure, int32_t M, const int64_t *anchors,
+                       const int32_t *relations, int64_t *offsets, int64_t *ids, int64_t cap, int32_t n_threads) {
+  if (!g || !anchors || !relations || !offsets) return fail(KGS_EINVAL, "null pointer");
+  if (structure < 0 || structure >= 14) return fail(KGS_EINVAL, "structure out of range [0, 14)");
+  if (M < 1) return fail(KGS_EINVAL, "M < 1");
+  const Plan &P = plan_of(structure);
+  for (int64_t k = 0; k < (int64_t)M * P.na; ++k)
+    if (anchors[k] < 0 || anchors[k] >= g->V) return fail(KGS_EINVAL, "anchor id out of range");
+  for (int64_t k = 0; k < (int64_t)M * P.nr; ++k)
+    if (relations[k] < 0 || relations[k] >= g->R) return fail(KGS_EINVAL, "relation out of range");
+  std::vector<Set> ans(M);
+  std::atomic<bool> comp{false};
+  try {
+    parallel_for(M, std::max(1, n_threads), [&](int64_t a, int64_t b) {
+      for (int64_t i = a; i < b; ++i) {
+        Query q(*g, P, anchors + i * P.na, relations + i * P.nr);
+        CSet r = q.eval(0);
+        if (r.neg) comp = true;
+        ans[i].swap(r.s);
+      }
+    });
+  } catch (const std::bad_alloc &) {
+    return fail(KGS_ENOMEM, "answer sets");
+  }
+  if (comp) return fail(KGS_EINVAL, "an answer set is a complement (negation at the root)");
+  offsets[0] = 0;
+  for (int i = 0; i < M; ++i) offsets[i + 1] = offsets[i] + (int64_t)ans[i].size();
+  if (!ids) return KGS_OK;
+  if (cap < offsets[M]) return fail(KGS_EINVAL, "ids capacity below offsets[M]");
+  for (int i = 0; i < M; ++i)
+    for (size_t k = 0; k < ans[i].size(); ++k) ids[offsets[i] + (int64_t)k] = ans[i][k];
+  return KGS_OK;
+}
+
 kgs_status kgs_pipeline_create(const kgs_graph *g, const int32_t *structures, int32_t n_structures, int32_t M,
                                int32_t K, uint64_t seed, int32_t rank, int64_t first_step, int32_t depth,
                                int32_t n_workers, kgs_pipeline **out) {

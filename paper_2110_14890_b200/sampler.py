@@ -35,6 +35,7 @@ _sig = {
     "kgs_sample": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_uint64, C.c_int64, C.c_int32, C.c_int32,
                              _P, _P, _P, _P, _P, _P]),
     "kgs_verify": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, C.c_int32, _P, C.c_int32, _P, C.c_int32]),
+    "kgs_answers": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, _P, _P, C.c_int64, C.c_int32]),
     "kgs_pipeline_create": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_uint64, C.c_int32, C.c_int64,
                                       C.c_int32, C.c_int32, C.POINTER(_P)]),
     "kgs_pipeline_next": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
@@ -116,6 +117,19 @@ class KGSampler:
                           n_threads or self.n_threads))
         return out.astype(bool)
 
+    def answers(self, structure: str, anchors, relations, n_threads: int = None):
+        """Answer sets by forward traversal: (offsets int64 [M + 1], ids int64 [offsets[M]])."""
+        sid = STRUCTS[structure]
+        a = np.ascontiguousarray(anchors, np.int64).reshape(-1, N_ANCHORS[sid])
+        r = np.ascontiguousarray(relations, np.int32).reshape(-1, N_RELS[sid])
+        M = a.shape[0]
+        off = np.zeros(M + 1, np.int64)
+        nt = n_threads or self.n_threads
+        _check(kgs_answers(self.g, sid, M, _p(a), _p(r), _p(off), None, 0, nt))
+        ids = np.zeros(max(1, int(off[-1])), np.int64)
+        _check(kgs_answers(self.g, sid, M, _p(a), _p(r), _p(off), _p(ids), len(ids), nt))
+        return off, ids[:int(off[-1])]
+
     def pipeline(self, structures, M, K, seed=0, rank=0, first_step=0, depth=None, n_workers=None, pin=False):
         return Pipeline(self, structures, M, K, seed, rank, first_step, depth, n_workers, pin)
 
@@ -183,3 +197,54 @@ class Pipeline:
             self.close()
         except Exception:
             pass
+
+
+def build_eval_set(test: KGSampler, valid: KGSampler, structure: str, n_queries: int, n_neg: int = 1000,
+                   seed: int = 0, step: int = 0, max_rounds: int = 16):
+    """Evaluation set of App. E for kg_eval: queries grounded on G_test by reverse
+    sampling, their missing answers A_q(G_test) minus A_q(G_valid) (kept: at least one), and n_neg
+    negatives per query drawn uniformly from V and filtered exactly to V minus A_q(G_test) by the
+    native bidirectional verification.  Traversal and verification run in libkgsample.so; the
+    set differences / selection here are host bookkeeping.  Returns (batch, ans_off, ans_ids,
+    negatives [M][n_neg]) with M = n_queries."""
+    sid = STRUCTS[structure]
+    keep_a, keep_r, hard = [], [], []
+    for rnd in range(max_rounds):
+        b = test.sample(structure, 2 * n_queries, 0, seed=seed, step=step * max_rounds + rnd)
+        ot, it = test.answers(structure, b["anchors"], b["relations"])
+        ov, iv = valid.answers(structure, b["anchors"], b["relations"])
+        for i in range(2 * n_queries):
+            h = np.setdiff1d(it[ot[i]:ot[i + 1]], iv[ov[i]:ov[i + 1]], assume_unique=True)
+            if len(h):
+                keep_a.append(b["anchors"][i])
+                keep_r.append(b["relations"][i])
+                hard.append(h)
+            if len(hard) == n_queries:
+                break
+        if len(hard) == n_queries:
+            break
+    if len(hard) < n_queries:
+        raise KGSError(3, f"only {len(hard)} of {n_queries} {structure} queries have missing answers")
+    anchors = np.ascontiguousarray(np.stack(keep_a), np.int64).reshape(n_queries, N_ANCHORS[sid])
+    relations = np.ascontiguousarray(np.stack(keep_r), np.int32).reshape(n_queries, N_RELS[sid])
+    ans_off = np.zeros(n_queries + 1, np.int64)
+    ans_off[1:] = np.cumsum([len(h) for h in hard])
+    ans_ids = np.concatenate(hard).astype(np.int64)
+    rng = np.random.default_rng([seed, step, sid, 0xE7A1])
+    neg = np.zeros((n_queries, n_neg), np.int64)
+    filled = np.zeros(n_queries, np.int64)
+    for rnd in range(max_rounds):
+        need = n_queries * n_neg - int(filled.sum())
+        if need == 0:
+            break
+        cand = rng.integers(0, test.V, size=(n_queries, 2 * n_neg), dtype=np.int64)
+        is_ans = test.verify(structure, anchors, relations, cand, shared=False)
+        for i in range(n_queries):
+            ok = cand[i][~is_ans[i]]
+            take = min(len(ok), n_neg - filled[i])
+            neg[i, filled[i]:filled[i] + take] = ok[:take]
+            filled[i] += take
+    if int(filled.sum()) < n_queries * n_neg:
+        raise KGSError(3, "could not draw enough non-answers")
+    batch = dict(structure=structure, M=n_queries, anchors=anchors, relations=relations)
+    return batch, ans_off, ans_ids, neg

@@ -122,3 +122,28 @@ def test_eval_large_negative_pool_matches_score():
         tol = 1e-5 * np.abs(d).max()
         assert 1 + np.count_nonzero(d[1:] < d[0] - tol) <= ranks[i] <= 1 + np.count_nonzero(d[1:] <= d[0] + tol)
     gm.close()
+
+
+@pytest.mark.parametrize("kind,structure", [("q2b", "ip"), ("betae", "pin"), ("gqe", "2u")])
+def test_eval_on_a_built_eval_set(kind, structure):
+    """kg_eval on an App. E evaluation set built by the native sampler on a split synthetic KG
+    (queries on G_test, missing answers A(G_test) minus A(G_valid), filtered negatives): ranks
+    decided in fp32 equal the oracle's (same decided / undecided rule as test_eval_parity)."""
+    from paper_2110_14890_b200 import sampler as N
+    kg = kggen.make_kg(300, 7, 3000, seed=9, a=0.6)
+    tr, va, te = kggen.split_kg(kg, valid_frac=0.1, test_frac=0.1, seed=2)
+    b, ans_off, ans_ids, negatives = N.build_eval_set(N.KGSampler(te, 2), N.KGSampler(va, 2), structure, 24,
+                                                      n_neg=120, seed=3)
+    cfg = kggen.ModelConfig(kind, 40, 300, 7, hidden=24)
+    gm = _model(cfg, 24)
+    table = oracle.SparseTable(cfg, 5)
+    ranks, metrics = gm.eval(gm.host_batch(dict(b, K=0, answers=np.zeros(24, np.int64),
+                                                negatives=np.zeros(0, np.int64),
+                                                mask=np.zeros((24, 1), np.uint32))),
+                             ans_off, ans_ids, negatives)
+    ref_ranks, ref_metrics, margin = oracle.oracle_eval(cfg, table, b, ans_off, ans_ids, negatives)
+    decided = margin > 1e-3          # far above the fp32 resolution of these distances (<= ~60)
+    assert decided.mean() > 0.8
+    np.testing.assert_array_equal(ranks[decided], ref_ranks[decided])
+    assert np.all((metrics >= 0) & (metrics <= 1))
+    gm.close()
