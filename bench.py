@@ -125,8 +125,11 @@ def stage_work(cfg, M, K, structure, U, d):
         # on the tcgen05 3xTF32 kernel (drained accumulation): 3 tf32 MMAs per fp32 product
         work["dag"] = ("tensor", 3.0 * 2.0 * (2 * cfg.dim * H + H * H + H * cfg.dim) * n_proj * M, "FLOP")
     return dict(work, **{
-        # scoring fwd+bwd: M*nout x K x units pair-units, fwd + 2x bwd
-        "scoring": ("alu", 3.0 * pair_flops_per_unit(cfg.kind) * M * nout * K * units, "FLOP"),
+        # scoring fwd+bwd: M*nout x K x units pair-units, fwd + 2x bwd (dot-product scorers: three
+        # tensor-core GEMMs, S = Q E^T, C E, C^T Q -- the same 2 FLOP per (query, candidate, float))
+        "scoring": ("tensor" if cfg.kind in ("distmult", "complex", "distmult-m", "complex-m") else "alu",
+                    3.0 * pair_flops_per_unit(kggen.M_VARIANTS.get(cfg.kind, cfg.kind)) * M * nout * K * units,
+                    "FLOP"),
         # dense Adam: read p, m, v (+ g of the weights) and write p, m, v of every theta_D element (A17)
         "dense_adam": ("hbm", 24.0 * size + 4.0 * w_elems, "B"),
         # sparse Adam: p, m, v read + write of the U touched rows + the L occurrence gradient rows read

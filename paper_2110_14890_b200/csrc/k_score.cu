@@ -545,6 +545,7 @@ __global__ void bwd_q_combine_kernel(ScoreArgs a, int qstride) {
   if (e >= n) return;
   float v = 0.f;
   for (int z = 0; z < a.JS; ++z) v += a.partQ[z * n + e];
+  v *= a.gsign;
   if (BOX && (e % qstride) >= a.U) v = fmaf(a.alpha, a.Csum[e / qstride], v);
   a.dQ[e] += v;
 }
@@ -565,7 +566,7 @@ __global__ void bwd_v_combine_kernel(ScoreArgs a) {
   for (int f = 0; f < AV; ++f) {
     float s = 0.f;
     for (int z = 0; z < a.RS; ++z) s += a.partV[z * zs + (size_t)j * AV * U + f * U + k];
-    acc[f] = s;
+    acc[f] = s * a.gsign;
   }
   float *out = a.dV + (size_t)j * a.d;
   if (Mdl::kBeta) {
@@ -828,6 +829,33 @@ static void launch_bwd(ScoreArgs a, cudaStream_t st, cudaStream_t st2) {
   { bwd_q_combine_kernel<Mdl::kBeta, Mdl::kRowAlpha><<<(int)((nq + 255) / 256), 256, 0, st>>>(a, qstride); ++g_launches; }
   const int64_t nv = (int64_t)a.K * a.U;
   { bwd_v_combine_kernel<Mdl><<<(int)((nv + 255) / 256), 256, 0, st>>>(a); ++g_launches; }
+}
+
+template <class Mdl>
+static void launch_epi_only(const ScoreArgs &a, int nout, bool train, cudaStream_t st) {
+  if (nout == 1) {
+    if (train) { pair_epi_kernel<Mdl, 1, true><<<a.M, 256, 0, st>>>(a); ++g_launches; }
+    else { pair_epi_kernel<Mdl, 1, false><<<a.M, 256, 0, st>>>(a); ++g_launches; }
+  } else {
+    if (train) { pair_epi_kernel<Mdl, 2, true><<<a.M, 256, 0, st>>>(a); ++g_launches; }
+    else { pair_epi_kernel<Mdl, 2, false><<<a.M, 256, 0, st>>>(a); ++g_launches; }
+  }
+}
+void launch_pair_epi(int kind, const ScoreArgs &a, int nout, bool train, cudaStream_t st) {
+  if (kind == DISTMULT) launch_epi_only<MDot>(a, nout, train, st);
+  else if (kind == COMPLEX) launch_epi_only<MCpx>(a, nout, train, st);
+}
+template <class Mdl>
+static void launch_combine_only(const ScoreArgs &a, cudaStream_t st) {
+  const int qstride = Mdl::QF * a.U;
+  const int64_t nq = (int64_t)a.NQ * qstride;
+  { bwd_q_combine_kernel<Mdl::kBeta, Mdl::kRowAlpha><<<(int)((nq + 255) / 256), 256, 0, st>>>(a, qstride); ++g_launches; }
+  const int64_t nv = (int64_t)a.K * a.U;
+  { bwd_v_combine_kernel<Mdl><<<(int)((nv + 255) / 256), 256, 0, st>>>(a); ++g_launches; }
+}
+void launch_bwd_combine(int kind, const ScoreArgs &a, cudaStream_t st) {
+  if (kind == DISTMULT) launch_combine_only<MDot>(a, st);
+  else if (kind == COMPLEX) launch_combine_only<MCpx>(a, st);
 }
 
 void launch_pair_bwd(int kind, const ScoreArgs &a, cudaStream_t st, cudaStream_t st2) {

@@ -452,6 +452,8 @@ struct kg_handle {
   float *gsP = nullptr, *gsP2 = nullptr;   // GEMM split-K scratch (main / side stream)
   int64_t gsP_cap = 0;
   float *Dpart = nullptr, *partQ = nullptr, *partV = nullptr, *Cpart = nullptr, *Csum = nullptr;
+  float *Eg = nullptr;     // dot-product scorers: the pool's rows, contiguous (GEMM operand)
+  bool gemm_scores = true; // dot-product scorers on the tensor-core GEMM; KG_GEMM_SCORES=0: pair kernels
   int64_t cap_D = 0, cap_Q = 0, cap_V = 0;
   cudaStream_t st2 = nullptr, st_cap = nullptr, st3 = nullptr, st4 = nullptr;
   cudaEvent_t ev_rel = nullptr, ev_loss = nullptr, ev_early = nullptr;
@@ -633,6 +635,7 @@ void carve(kg_handle *h, Arena &A) {
     h->partV = A.take<float>(h->cap_V);
     h->Cpart = A.take<float>(8LL * std::max(Kx, h->Cx));
     h->Csum = A.take<float>(NQ);
+    if (h->sk == KG_DISTMULT || h->sk == KG_COMPLEX) h->Eg = A.take<float>((int64_t)Kx * d);   // pool rows, gathered
   }
   h->loss_pos = A.take<float>(Mx);
   if (h->kind == KG_BETAE) {
@@ -1227,6 +1230,7 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
   if (const char *e = std::getenv("KG_NO_GRAPH")) h->use_graphs = !(e[0] == '1');
   if (const char *e = std::getenv("KG_PDL")) h->use_pdl = !(e[0] == '0');
   if (const char *e = std::getenv("KG_DIST_BUCKETS")) h->buckets = !(e[0] == '0');
+  if (const char *e = std::getenv("KG_GEMM_SCORES")) h->gemm_scores = !(e[0] == '0');
   if (const char *e = std::getenv("KG_DIST_GRAPH")) h->dist_graph = !(e[0] == '0');
   if (const char *e = std::getenv("KG_NCCL")) if (std::string(e) == "loopback") h->dist_graph = false;
   // DAG contractions (reading A24): the hand-written tcgen05 3xTF32 kernel
@@ -1319,6 +1323,37 @@ kg_status kg_init_params(kg_handle *h, uint64_t seed) {
 
 namespace {
 
+// a8-a10 for the dot-product scorers (DistMult / ComplEx and their -m variants; SURVEY §8(a)
+// a8: "a tcgen05 dense contraction only for dot-product scorers"): with the pool's rows
+// gathered into Eg [K][d], S = Q Eg^T is one GEMM (D = -S, A13; the pair epilogue applies the
+// DNF min and Eq. 1 on it), and the backward is two: dQ = -C Eg, dV = -C^T Q (the sign in the
+// combines).  The other scorers (L1 / box / Beta-KL / RotatE) stay on the CUDA-core pair kernels.
+bool gemm_scoring(const kg_handle *h) { return h->gemm_scores && (h->sk == KG_DISTMULT || h->sk == KG_COMPLEX); }
+kg_status score_forward(kg_handle *h, ScoreArgs &sa, int nout, bool train, const int64_t *neg_rows) {
+  if (!gemm_scoring(h)) {
+    launch_pair_fwd(h->sk, sa, nout, train, h->st);
+    return KG_OK;
+  }
+  launch_gather_rows(h->Eg, h->ent_src, neg_rows, sa.K, h->d, h->st);
+  sa.KS = 1;
+  G(false, true, sa.NQ, sa.K, h->d, sa.Q, h->d, h->Eg, h->d, 0.f, sa.Dpart, sa.Kp);
+  launch_pair_epi(h->sk, sa, nout, train, h->st);
+  return KG_OK;
+}
+kg_status score_backward(kg_handle *h, ScoreArgs &sa, cudaStream_t st2) {
+  if (!gemm_scoring(h)) {
+    launch_pair_bwd(h->sk, sa, h->st, st2);
+    return KG_OK;
+  }
+  G(false, false, sa.NQ, h->d, sa.K, sa.C, sa.Kp, h->Eg, h->d, 0.f, sa.partQ, h->d);   // C Eg
+  G(true, false, sa.K, h->d, sa.NQ, sa.C, sa.Kp, sa.Q, h->d, 0.f, sa.partV, h->d);    // C^T Q
+  sa.JS = 1;
+  sa.RS = 1;
+  sa.gsign = -1.f;
+  launch_bwd_combine(h->sk, sa, h->st);
+  return KG_OK;
+}
+
 // Everything of one step after ingest: enqueued on h->st (directly, or while
 // h->st is a capturing stream -- the sequence is then replayed as a CUDA graph).
 kg_status enqueue_step(kg_handle *h, StepBufs &S) {
@@ -1378,7 +1413,7 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   sa.cap_D = h->cap_D; sa.cap_Q = h->cap_Q; sa.cap_V = h->cap_V;
   sa.dV = h->OG + (int64_t)(na * M + M) * d;
   const int njt = K > 0 ? 1 : 0;
-  if (K > 0) launch_pair_fwd(h->sk, sa, p.nout, true, st);
+  if (K > 0 && (s = score_forward(h, sa, p.nout, true, neg_rows)) != KG_OK) return s;
   launch_loss_finalize(h->loss_pos, h->loss_part, M, njt, 1.0 / ((double)M * h->world), h->loss_dev, h->flags,
                        h->t_dev, h->bc, h->cfg.beta1, h->cfg.beta2, h->apply, st);
   mark(h, 3);
@@ -1404,7 +1439,7 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
     CK(cudaEventRecord(h->ev_fork2, st));
     CK(cudaStreamWaitEvent(h->st2, h->ev_fork2, 0));
   }
-  if (K > 0) launch_pair_bwd(h->sk, sa, st, h->st2);
+  if (K > 0 && (s = score_backward(h, sa, h->st2)) != KG_OK) return s;
   CK(cudaEventRecord(h->ev_join, h->st2));
   mark(h, 4);
 
@@ -1558,7 +1593,7 @@ kg_status step_dist(kg_handle *h, StepBufs &S) {
   sa.Dpart = h->Dpart; sa.partQ = h->partQ; sa.partV = h->partV; sa.Cpart = h->Cpart; sa.Csum = h->Csum;
   sa.cap_D = h->cap_D; sa.cap_Q = h->cap_Q; sa.cap_V = h->cap_V;
   sa.dV = h->OG + (int64_t)(na * M + M) * d;
-  if (K > 0) launch_pair_fwd(h->sk, sa, p.nout, true, st);
+  if (K > 0 && (s = score_forward(h, sa, p.nout, true, neg_rows)) != KG_OK) return s;
   // global loss = sum over ranks of the (1/(M G))-scaled local sums (A18); one finite check for all
   launch_loss_finalize(h->loss_pos, h->loss_part, M, K > 0 ? 1 : 0, 1.0 / ((double)M * G), h->loss_dev, h->flags,
                        h->t_dev, h->bc, h->cfg.beta1, h->cfg.beta2, h->apply, st, /*check=*/0);
@@ -1566,7 +1601,7 @@ kg_status step_dist(kg_handle *h, StepBufs &S) {
   NCK(nccl().AllReduce(h->flags + 1, h->flags + 1, 1, ncclInt32, ncclMax, h->comm, st));
   launch_loss_check(h->loss_dev, h->flags, h->t_dev, h->bc, h->cfg.beta1, h->cfg.beta2, h->apply, st);
   mark(h, 3);
-  if (K > 0) launch_pair_bwd(h->sk, sa, st, st);
+  if (K > 0 && (s = score_backward(h, sa, st)) != KG_OK) return s;
   mark(h, 4);
   if ((s = dag_backward(h, S)) != KG_OK) return s;
   if (p.inter < 0 && h->kind != KG_BETAE && h->w_off < h->dense_size)

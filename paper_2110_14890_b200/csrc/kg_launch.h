@@ -31,6 +31,7 @@ struct ScoreArgs {
   float *Dpart = nullptr, *partQ = nullptr, *partV = nullptr, *Cpart = nullptr, *Csum = nullptr;
   int64_t cap_D = 0, cap_Q = 0, cap_V = 0;
   int KS = 1, JS = 1, RS = 1, ups = 0, jps = 0, rps = 0;
+  float gsign = 1.f;            // sign applied to the summed dQ / dV partials (GEMM-path scoring: -1)
 };
 
 struct PosArgs {
@@ -46,6 +47,10 @@ struct PosArgs {
 // k_score.cu
 void launch_pair_fwd(int kind, const ScoreArgs &a, int nout, bool train, cudaStream_t st);
 void launch_pair_bwd(int kind, const ScoreArgs &a, cudaStream_t st, cudaStream_t st2);
+// The dot-product scorers on the tensor-core GEMM (kg_api.cu): the pair epilogue over
+// Dpart (a.KS partials) and the dQ / dV combines over partQ / partV (a.JS / a.RS partials).
+void launch_pair_epi(int kind, const ScoreArgs &a, int nout, bool train, cudaStream_t st);
+void launch_bwd_combine(int kind, const ScoreArgs &a, cudaStream_t st);
 void launch_pos(int kind, const PosArgs &p, int nout, cudaStream_t st);
 void launch_beta_entity(const float *ent, const int64_t *rows, int K, int m, float *F, float *Cv, cudaStream_t st);
 void launch_beta_query(const float *Q, int NQ, int m, float *QP, float *Cq, cudaStream_t st);
