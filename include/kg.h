@@ -149,6 +149,11 @@ int64_t kg_shard_rows(const kg_handle *h);
 
 /* Floats in theta_D for this model (relation tables + operator weights). */
 int64_t kg_dense_size(const kg_handle *h);
+/* Device bytes of the library's own workspace (staged batch, dedup outputs, occurrence
+ * gradients, DAG activations, scoring partials, exchange buffers), sized once at kg_create
+ * from max_M / max_K / max_cand and the model; allocated and freed by the library (the
+ * caller owns the tables of kg_bind, the library only this scratch).  -1 for a NULL handle. */
+int64_t kg_workspace_size(const kg_handle *h);
 
 /* Record the caller's table pointers and the CUDA stream (cudaStream_t, may be NULL).
  * Host tier (the paper keeps theta_E in CPU memory): each of

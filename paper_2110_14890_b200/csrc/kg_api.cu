@@ -1261,6 +1261,7 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
 
 int64_t kg_shard_rows(const kg_handle *h) { return h ? h->shard : -1; }
 int64_t kg_dense_size(const kg_handle *h) { return h ? h->dense_size : -1; }
+int64_t kg_workspace_size(const kg_handle *h) { return h ? (int64_t)h->ws_bytes : -1; }
 
 kg_status kg_bind(kg_handle *h, const kg_tables *t, void *stream) {
   if (!h || !t) return KG_EINVAL;

@@ -57,6 +57,7 @@ _sig = {
     "kg_create": (C.c_int, [C.POINTER(kg_config), C.POINTER(_H)]),
     "kg_shard_rows": (C.c_int64, [_H]),
     "kg_dense_size": (C.c_int64, [_H]),
+    "kg_workspace_size": (C.c_int64, [_H]),
     "kg_bind": (C.c_int, [_H, C.POINTER(kg_tables), C.c_void_p]),
     "kg_init_params": (C.c_int, [_H, C.c_uint64]),
     "kg_step": (C.c_int, [_H, C.POINTER(kg_batch), C.c_float, C.POINTER(kg_step_info)]),
@@ -138,6 +139,7 @@ class KGModel:
         check(kg_create(C.byref(self.conf), C.byref(self.h)))
         self.rows = kg_shard_rows(self.h)
         self.dense_size = kg_dense_size(self.h)
+        self.workspace_bytes = kg_workspace_size(self.h)
         d = cfg.dim
         f32 = torch.float32
         def table(name):
