@@ -250,6 +250,13 @@ def run_ours(args, world, rank, local):
         achieved = per_launch / sec / 1e12
         roof = {"bound": "alu", "achieved": round(achieved, 2), "peak": round(FP32_PEAK_TFLOPS, 1),
                 "unit": "TFLOP/s", "frac": round(achieved / FP32_PEAK_TFLOPS, 4), "traffic": None}
+    try:   # DRAM traffic of the dominant stage from the committed ncu capture (profiles/ncu_traffic.json)
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(args.workload, {}).get(dom)
+        if tr is not None:
+            roof["traffic"] = round(float(tr))
+            roof["traffic_source"] = "ncu --set full, profiles/r1_ncu_full_top_kernels_final.csv (bytes per step)"
+    except (OSError, ValueError):
+        pass
     roof.update({"kernel": dom, "peak_source": pk_src if bound == "hbm" else (
                  "measured sustained bf16 x tf32/bf16 nominal ratio / 3 (3xTF32)" if bound == "tensor" else "derived (DESIGN.md §6)"),
                  "stage_ms": {stage_names[i]: round(float(stage[i]), 4) for i in range(7)},
