@@ -221,6 +221,12 @@ kg_status kg_last_grads(kg_handle *h, int64_t *uniq, float *grad_rows, float *gr
  * bit 2 (default 0): record CUDA events between the stages of kg_step (kg_step_info.stage_ms). */
 kg_status kg_set_apply(kg_handle *h, int32_t flags);
 
+/* Checkpoint / resume: the tables are the caller's (kg_bind), so a checkpoint is
+ * the caller's copy of them plus the Adam step counter t (A15), read and restored here.
+ * kg_set_step waits for pending work; t >= 0. */
+kg_status kg_get_step(kg_handle *h, int64_t *t);
+kg_status kg_set_step(kg_handle *h, int64_t t);
+
 const char *kg_last_error(const kg_handle *h);
 
 /* Test hook: the tensor-core GEMM of the query-DAG contractions on device pointers,

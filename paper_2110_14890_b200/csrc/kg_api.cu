@@ -2013,6 +2013,26 @@ kg_status kg_test_gemm(int32_t ta, int32_t tb, int32_t M, int32_t N, int32_t K, 
   return cudaGetLastError() == cudaSuccess ? KG_OK : KG_ECUDA;
 }
 
+kg_status kg_get_step(kg_handle *h, int64_t *t) {
+  kg_status s = check_state(h);
+  if (s) return s;
+  if (!t) return fail(h, KG_EINVAL, "null pointer");
+  CK(cudaStreamSynchronize(h->st));
+  h->step_pending = false;
+  CK(cudaMemcpy(t, h->t_dev, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  return KG_OK;
+}
+
+kg_status kg_set_step(kg_handle *h, int64_t t) {
+  kg_status s = check_state(h);
+  if (s) return s;
+  if (t < 0) return fail(h, KG_EINVAL, "negative step");
+  CK(cudaStreamSynchronize(h->st));
+  h->step_pending = false;
+  CK(cudaMemcpy(h->t_dev, &t, sizeof(int64_t), cudaMemcpyHostToDevice));
+  return KG_OK;
+}
+
 kg_status kg_nccl_unique_id(void *out) {
   if (!out) return KG_EINVAL;
   ncclUniqueId id;

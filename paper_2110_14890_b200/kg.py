@@ -74,6 +74,8 @@ _sig = {
     "kg_set_apply": (C.c_int, [_H, C.c_int32]),
     "kg_last_error": (C.c_char_p, [_H]),
     "kg_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "kg_get_step": (C.c_int, [_H, C.POINTER(C.c_int64)]),
+    "kg_set_step": (C.c_int, [_H, C.c_int64]),
     "kg_test_gemm": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
                                C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_float,
                                C.c_void_p]),
@@ -257,6 +259,30 @@ class KGModel:
                             None if dneg is None else dneg.ctypes.data), self.h)
         U = n.value
         return dict(uniq=uniq[:U], grad_rows=g[:U], grad_dense=gd, d_pos=dpos, d_neg=dneg)
+
+    # -- checkpoint / resume (the tables are this object's tensors; t is the library's) --------
+    def get_step(self) -> int:
+        t = C.c_int64()
+        check(kg_get_step(self.h, C.byref(t)), self.h)
+        return t.value
+
+    def save(self, path):
+        """theta_E shard, theta_D, their Adam moments and the Adam step counter, with torch.save."""
+        torch = self.torch
+        state = {k: getattr(self, k).detach().cpu() for k in ("ent", "ent_m", "ent_v", "dense", "dense_m", "dense_v")}
+        state["t"] = self.get_step()
+        state["dim"], state["rows"] = self.cfg.dim, self.rows
+        torch.save(state, path)
+
+    def load(self, path):
+        torch = self.torch
+        state = torch.load(path, weights_only=True)
+        assert state["dim"] == self.cfg.dim and state["rows"] == self.rows, "checkpoint of another shape"
+        torch.cuda.synchronize()
+        for k in ("ent", "ent_m", "ent_v", "dense", "dense_m", "dense_v"):
+            getattr(self, k).copy_(state[k])
+        torch.cuda.synchronize()
+        check(kg_set_step(self.h, int(state["t"])), self.h)
 
     def close(self):
         if self.h:

@@ -357,3 +357,25 @@ def test_stage_timing_with_and_without_graphs(monkeypatch):
         assert np.all(np.isfinite(st)) and np.all(st >= 0) and st[7] > 0, st
         assert abs(st[:7].sum() - st[7]) <= 0.05 * st[7] + 1e-3, st
         gm.close()
+
+
+def test_checkpoint_resume_is_bitwise(tmp_path):
+    """Checkpoint / resume: the tables (caller-owned) and the Adam step counter saved after two
+    steps and loaded into a fresh handle continue bit-identically to the uninterrupted run."""
+    cfg = kggen.ModelConfig("q2b", 40, 300, 7)
+    batches = [kggen.make_batch(cfg, st, 70, 100, seed=17, step=s) for s, st in enumerate(["2i", "up", "3p", "ip"])]
+    a = _model(cfg, 70, 100)
+    for b in batches[:2]:
+        a.step(a.host_batch(b), 0.01)
+    a.save(tmp_path / "ck.pt")
+    assert a.get_step() == 2
+    b_ = _model(cfg, 70, 100, seed=99)          # different init, overwritten by the checkpoint
+    b_.load(tmp_path / "ck.pt")
+    for b in batches[2:]:
+        ia = a.step(a.host_batch(b), 0.01)
+        ib = b_.step(b_.host_batch(b), 0.01)
+        assert ia.loss == ib.loss and ia.step == ib.step
+    np.testing.assert_array_equal(a.read_rows(np.arange(300)), b_.read_rows(np.arange(300)))
+    np.testing.assert_array_equal(a.read_dense(2), b_.read_dense(2))
+    a.close()
+    b_.close()
