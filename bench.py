@@ -137,6 +137,19 @@ def stage_work(cfg, M, K, structure, U, d):
     })
 
 
+def workload_config(args, cfg, w, world):
+    """The `config` object of both arms' JSON lines (the workload, not a model schema)."""
+    return {"workload": args.workload, "kind": cfg.kind, "dim": cfg.dim,
+            "entities": cfg.n_entities, "entities_per_gpu": kggen.shard_rows(cfg.n_entities, world),
+            "relations": cfg.n_relations, "global_batch": w.M * world, "negatives_per_gpu": w.K,
+            "structures": w.structures, "lr": args.lr,
+            "parallelism": (f"dp{world} + theta_E row-sharded (owner = id % {world}), NCCL exchange of rows / "
+                            "row gradients, all-reduce of dL/dtheta_D") if world > 1 else "single",
+            "l2": "flushed between timed steps (256 MB write outside the step events)",
+            "theta_E": ("pinned host memory (zero-copy): " + args.host_tier) if args.host_tier else "HBM",
+            "note": w.note}
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args, world, rank, local):
     import torch
@@ -309,16 +322,7 @@ def run_ours(args, world, rank, local):
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 5), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (kggen, seeded)",
-        "config": {"workload": args.workload, "model": cfg.kind, "dim": cfg.dim,
-                   "entities": cfg.n_entities, "entities_per_gpu": kggen.shard_rows(cfg.n_entities, world),
-                   "relations": cfg.n_relations,
-                   "global_batch": M * world, "negatives_per_gpu": K, "structures": structures,
-                   "lr": lr, "parallelism": (f"dp{world} + theta_E row-sharded (owner = id % {world}), "
-                                             "NCCL exchange of rows / row gradients, all-reduce of dL/dtheta_D")
-                   if world > 1 else "single",
-                   "l2": "flushed between timed steps (256 MB write outside the step events)",
-                   "theta_E": ("pinned host memory (zero-copy): " + args.host_tier) if args.host_tier else "HBM",
-                   "note": w.note},
+        "config": workload_config(args, cfg, w, world),
         "e2e": e2e, "e2e_sampler": e2e_sampler, "roofline": roof,
         "gpu_launches": int(sum(kernels_of.get(st, info.kernels) for st in step_structs)),
         "kernels_per_step": kernels_of, "cublas_gemms_per_step": gemms_of, "ms_per_step_by_structure": per_struct_ms,
@@ -428,8 +432,7 @@ def run_reference(args, world, rank):
             "steps": steps_run, "warmup": args.warmup, "ms_per_step": round(dt / steps_run * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (kggen, seeded)",
-            "config": {"workload": args.workload, "model": cfg.kind, "dim": cfg.dim,
-                       "entities_per_gpu": cfg.n_entities, "queries_per_step_sample": q},
+            "config": dict(workload_config(args, cfg, w, 1), queries_per_step_sample=q),
             "cpu_baseline": {"value": round(rate, 3), "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"{steps_run} steps x {q} queries of the workload (full pool)"},
             "e2e": {"value": round(rate, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
