@@ -179,6 +179,11 @@ kg_status kg_step(kg_handle *h, const kg_batch *batch, float lr, kg_step_info *i
 
 /* Wait for the last enqueued step and report it (ENONFINITE if its loss was not finite). */
 kg_status kg_sync(kg_handle *h, kg_step_info *info);
+/* The OLDEST unread step result (waits for that step only) -- two steps' results are kept,
+ * so a host loop can issue step s + 1 (info = NULL) before reading step s and the device
+ * never idles on the host round trip; a third unread step drops the oldest.  KG_ESTATE if
+ * nothing is unread.  kg_sync instead waits for everything and returns the latest step. */
+kg_status kg_result(kg_handle *h, kg_step_info *info);
 
 /* Dist(f(q_i), f(v_c)) for every query of `queries` (forward DAG only) and every
  * shared candidate cand[c] (n_cand <= max_cand): out_dist host [M][n_cand], lower = closer,

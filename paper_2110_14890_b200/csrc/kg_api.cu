@@ -490,13 +490,16 @@ struct kg_handle {
   size_t pin_bytes = 0;
   cudaEvent_t pin_ev[2] = {nullptr, nullptr};
   int pin_cur = 0;
-  struct HostOut {
+  struct HostOut {       // = the device result block (loss, flags, U, t at 0 / 8 / 16 / 24)
     double loss;
     int flags[2];
     int32_t U;
     int64_t t;
-  } *hout = nullptr;
-  cudaEvent_t step_done = nullptr;
+  } *hout = nullptr;      // [2]: two steps' results may be in flight (pipelined host loop)
+  char *resdev = nullptr;
+  cudaEvent_t step_done = nullptr, res_ev[2] = {nullptr, nullptr};
+  int res_next = 0, res_pending = 0;             // ring of the two result slots
+  int res_kernels[2] = {0, 0}, res_gemms[2] = {0, 0};
 
   int64_t stamp = 0;
   int apply = 1, keep_grads = 0, timing = 0;
@@ -599,7 +602,15 @@ void carve(kg_handle *h, Arena &A) {
   h->inv = A.take<int32_t>(h->Lx);
   h->perm = A.take<int32_t>(h->Lx);
   h->seg = A.take<int32_t>(h->Lx + 1);
-  h->Udev = A.take<int32_t>(1);
+  {
+    // the step's scalar results, contiguous so that one D2H copies them (layout = HostOut)
+    char *res = reinterpret_cast<char *>(A.take<int64_t>(4));
+    h->resdev = res;
+    h->loss_dev = reinterpret_cast<double *>(res);
+    h->flags = reinterpret_cast<int *>(res + 8);
+    h->Udev = reinterpret_cast<int32_t *>(res + 16);
+    h->t_dev = reinterpret_cast<int64_t *>(res + 24);
+  }
   h->bad = A.take<int32_t>(1);
   h->rocc = A.take<int32_t>(h->Lrx);
   h->runiq = A.take<int64_t>(h->Lrx);
@@ -644,9 +655,6 @@ void carve(kg_handle *h, Arena &A) {
     h->QP = A.take<float>((int64_t)NQ * d);
     h->Cq = A.take<float>(NQ);
   }
-  h->loss_dev = A.take<double>(1);
-  h->flags = A.take<int>(2);
-  h->t_dev = A.take<int64_t>(1);
   h->lr_dev = A.take<float>(4);
   h->stamp_dev = A.take<int64_t>(1);
   h->blas_ws = A.take<char>(32 << 20);
@@ -1118,15 +1126,17 @@ void mark(kg_handle *h, int i, cudaStream_t s = nullptr) {
   else cudaEventRecord(h->sev[i], st);
 }
 
-kg_status read_result(kg_handle *h, kg_step_info *info) {
-  CK(cudaEventSynchronize(h->step_done));
-  h->step_pending = false;
+// Result of the step in ring slot `slot` (waits for it); stage times are those of the last
+// step issued (stage timing is meant for synchronous steps).
+kg_status read_result(kg_handle *h, kg_step_info *info, int slot) {
+  CK(cudaEventSynchronize(h->res_ev[slot]));
+  const kg_handle::HostOut &o = h->hout[slot];
   if (info) {
-    info->loss = h->hout->loss;
-    info->n_touched = h->hout->U;
-    info->step = h->hout->t;
-    info->kernels = h->last_kernels;
-    info->gemms = h->last_gemms;
+    info->loss = o.loss;
+    info->n_touched = o.U;
+    info->step = o.t;
+    info->kernels = h->res_kernels[slot];
+    info->gemms = h->res_gemms[slot];
     for (int i = 0; i < 10; ++i) info->stage_ms[i] = 0.f;
     if (h->timing) {
       for (int i = 0; i < 7; ++i) CK(cudaEventElapsedTime(&info->stage_ms[i], h->sev[i], h->sev[i + 1]));
@@ -1137,12 +1147,19 @@ kg_status read_result(kg_handle *h, kg_step_info *info) {
       }
     }
   }
-  if (h->hout->flags[1] == 2)
+  if (o.flags[1] == 2)
     return fail(h, KG_EINVAL, "row exchange bucket overflow (the batch's distinct ids concentrate on one owner beyond "
                               "the fixed capacity); step not applied -- KG_DIST_BUCKETS=0 exchanges exact counts");
-  if (h->hout->flags[1]) return fail(h, KG_EINVAL, "an id or relation of the (device) batch was out of range; step not applied");
-  if (h->hout->flags[0]) return fail(h, KG_ENONFINITE, "non-finite loss; step not applied");
+  if (o.flags[1]) return fail(h, KG_EINVAL, "an id or relation of the (device) batch was out of range; step not applied");
+  if (o.flags[0]) return fail(h, KG_ENONFINITE, "non-finite loss; step not applied");
   return KG_OK;
+}
+// the latest step (drains every pending result)
+kg_status read_latest(kg_handle *h, kg_step_info *info) {
+  const int slot = (h->res_next + 1) & 1;      // the slot written last
+  h->res_pending = 0;
+  h->step_pending = false;
+  return read_result(h, info, slot);
 }
 
 }  // namespace
@@ -1199,9 +1216,11 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
     if (cudaMallocHost(&h->pin[i], h->pin_bytes) != cudaSuccess) { kg_destroy(h); return KG_ENOMEM; }
     if (cudaEventCreateWithFlags(&h->pin_ev[i], cudaEventDisableTiming) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
   }
-  if (cudaMallocHost(&h->hout, sizeof(kg_handle::HostOut)) != cudaSuccess) { kg_destroy(h); return KG_ENOMEM; }
-  std::memset(h->hout, 0, sizeof(kg_handle::HostOut));
-  if (cudaEventCreateWithFlags(&h->step_done, cudaEventDisableTiming) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
+  if (cudaMallocHost(&h->hout, 2 * sizeof(kg_handle::HostOut)) != cudaSuccess) { kg_destroy(h); return KG_ENOMEM; }
+  std::memset(h->hout, 0, 2 * sizeof(kg_handle::HostOut));
+  if (cudaEventCreateWithFlags(&h->step_done, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->res_ev[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->res_ev[1], cudaEventDisableTiming) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
   for (int i = 0; i < 12; ++i)
     if (cudaEventCreate(&h->sev[i]) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
   if (cublasCreate(&h->blas) != CUBLAS_STATUS_SUCCESS) { kg_destroy(h); return KG_ECUDA; }
@@ -1491,10 +1510,6 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   mark(h, 7);
   CK(cudaGetLastError());
   // results to pinned host memory (loss, flags, U, t)
-  CK(cudaMemcpyAsync(&h->hout->loss, h->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(h->hout->flags, h->flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&h->hout->U, h->Udev, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&h->hout->t, h->t_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   return KG_OK;
 }
 
@@ -1642,10 +1657,6 @@ kg_status step_dist(kg_handle *h, StepBufs &S) {
                       h->cfg.beta2, h->cfg.eps, h->bc, h->flags, st);
   mark(h, 7);
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(&h->hout->loss, h->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(h->hout->flags, h->flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&h->hout->U, h->Udev, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&h->hout->t, h->t_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   return KG_OK;
 }
 
@@ -1737,17 +1748,37 @@ kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info)
     h->last_kernels = (int)(g_launches - l0);
     h->last_gemms = h->gemm_count;
   }
+  {
+    // the step's scalar results into its ring slot (one D2H), outside the replayed graph
+    const int slot = h->res_next;
+    h->res_next ^= 1;
+    CK(cudaMemcpyAsync(&h->hout[slot], h->resdev, sizeof(kg_handle::HostOut), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaEventRecord(h->res_ev[slot], h->st));
+    h->res_kernels[slot] = h->last_kernels;
+    h->res_gemms[slot] = h->last_gemms;
+    h->res_pending = std::min(2, h->res_pending + 1);   // a third unread step drops the oldest
+  }
   CK(cudaEventRecord(h->step_done, h->st));
   h->step_pending = true;
   h->last_U_valid = 1;
-  if (info) return read_result(h, info);
+  if (info) return read_latest(h, info);
   return KG_OK;
 }
 
 kg_status kg_sync(kg_handle *h, kg_step_info *info) {
   kg_status s = check_state(h);
   if (s) return s;
-  return read_result(h, info);
+  return read_latest(h, info);
+}
+
+kg_status kg_result(kg_handle *h, kg_step_info *info) {
+  kg_status s = check_state(h);
+  if (s) return s;
+  if (h->res_pending == 0) return fail(h, KG_ESTATE, "no unread step result");
+  const int slot = (h->res_next + 2 - h->res_pending) & 1;   // the oldest unread slot
+  --h->res_pending;
+  if (h->res_pending == 0) h->step_pending = false;
+  return read_result(h, info, slot);
 }
 
 // Validate a query batch for kg_score / kg_eval and compute its embeddings into h->Q
@@ -2063,6 +2094,8 @@ void kg_destroy(kg_handle *h) {
   }
   if (h->hout) cudaFreeHost(h->hout);
   if (h->step_done) cudaEventDestroy(h->step_done);
+  for (int i = 0; i < 2; ++i)
+    if (h->res_ev[i]) cudaEventDestroy(h->res_ev[i]);
   for (int i = 0; i < 12; ++i)
     if (h->sev[i]) cudaEventDestroy(h->sev[i]);
   if (h->ev_rel) cudaEventDestroy(h->ev_rel);

@@ -62,6 +62,7 @@ _sig = {
     "kg_init_params": (C.c_int, [_H, C.c_uint64]),
     "kg_step": (C.c_int, [_H, C.POINTER(kg_batch), C.c_float, C.POINTER(kg_step_info)]),
     "kg_sync": (C.c_int, [_H, C.POINTER(kg_step_info)]),
+    "kg_result": (C.c_int, [_H, C.POINTER(kg_step_info)]),
     "kg_score": (C.c_int, [_H, C.POINTER(kg_batch), C.c_void_p, C.c_int32, C.c_void_p]),
     "kg_eval": (C.c_int, [_H, C.POINTER(kg_batch), C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                           C.c_void_p]),
@@ -203,6 +204,12 @@ class KGModel:
     def sync(self):
         info = kg_step_info()
         check(kg_sync(self.h, C.byref(info)), self.h)
+        return info
+
+    def result(self):
+        """The oldest unread step's result (pipelined loops: issue step s + 1, then read step s)."""
+        info = kg_step_info()
+        check(kg_result(self.h, C.byref(info)), self.h)
         return info
 
     def score(self, b, cand):

@@ -379,3 +379,25 @@ def test_checkpoint_resume_is_bitwise(tmp_path):
     np.testing.assert_array_equal(a.read_dense(2), b_.read_dense(2))
     a.close()
     b_.close()
+
+
+def test_pipelined_results_in_order():
+    """kg_result returns unread step results oldest first (two in flight); the losses equal those
+    of synchronous steps, and a third unread step drops the oldest."""
+    from paper_2110_14890_b200 import KGError
+    cfg = kggen.ModelConfig("gqe", 40, 300, 7)
+    bs = [kggen.make_batch(cfg, "2i", 70, 100, seed=18, step=s) for s in range(4)]
+    a, b_ = _model(cfg, 70, 100), _model(cfg, 70, 100)
+    ref = [a.step(a.host_batch(b), 0.01) for b in bs]
+    b_.step(b_.host_batch(bs[0]), 0.01, sync=False)
+    b_.step(b_.host_batch(bs[1]), 0.01, sync=False)
+    r0 = b_.result()
+    b_.step(b_.host_batch(bs[2]), 0.01, sync=False)
+    b_.step(b_.host_batch(bs[3]), 0.01, sync=False)     # three unread (1, 2, 3): step 1 dropped
+    r2, r3 = b_.result(), b_.result()
+    assert (r0.step, r2.step, r3.step) == (1, 3, 4)
+    assert (r0.loss, r2.loss, r3.loss) == (ref[0].loss, ref[2].loss, ref[3].loss)
+    with pytest.raises(KGError):
+        b_.result()
+    a.close()
+    b_.close()
