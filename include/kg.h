@@ -24,8 +24,9 @@
  *     the loss: kg_step with info != NULL, or kg_sync).
  *   - A CUDA / NCCL failure moves the handle to a sticky error state: later
  *     calls return KG_ESTATE.
- *   - world > 1: every rank calls kg_step / kg_score / kg_read_rows with the
- *     same structure, M and K (collective calls).
+ *   - world > 1: kg_step, kg_score, kg_eval and kg_gather_rows are collective: every
+ *     rank calls them together (kg_step with the same structure, M and K, P:L303,
+ *     L397-398; the others with their own queries / ids, sizes may differ per rank).
  */
 #ifndef KG_H_
 #define KG_H_
@@ -187,7 +188,9 @@ kg_status kg_result(kg_handle *h, kg_step_info *info);
 
 /* Dist(f(q_i), f(v_c)) for every query of `queries` (forward DAG only) and every
  * shared candidate cand[c] (n_cand <= max_cand): out_dist host [M][n_cand], lower = closer,
- * unions = DNF min (A11). */
+ * unions = DNF min (A11).  world > 1: collective (each rank its own queries and candidates;
+ * the anchor and candidate rows are fetched from their owners first); the
+ * distances are bit-identical to those of one rank holding the whole table. */
 kg_status kg_score(kg_handle *h, const kg_batch *queries, const int64_t *cand, int32_t n_cand,
                    float *out_dist);
 
@@ -200,14 +203,20 @@ kg_status kg_score(kg_handle *h, const kg_batch *queries, const int64_t *cand, i
  * query").  Rank(v) = 1 + #{j : D(q, v_j) <= D(q, v)} (ties count against v), D the model
  * distance with the DNF min over disjuncts.  Outputs (host): ranks [ans_off[M]] and
  * metrics [M][4] = MRR, Hit@1, Hit@3, Hit@10 of each query (mean over its answers).
- * Needs (max answers per query + n_neg) <= 51200.  Errors: EINVAL (pointer / size / id),
- * EUNSUPPORTED (structure not valid for the kind, world > 1).  Synchronises the stream. */
+ * Needs (max answers per query + n_neg) <= 51200.  world > 1: collective as kg_score (answer
+ * and negative rows fetched from their owners).  Errors: EINVAL (pointer / size / id),
+ * EUNSUPPORTED (structure not valid for the kind).  Synchronises the stream. */
 kg_status kg_eval(kg_handle *h, const kg_batch *queries, const int64_t *ans_off, const int64_t *ans_ids,
                   int32_t n_neg, const int64_t *negatives, int32_t *ranks, float *metrics);
 
 /* Test / checkpoint hooks.  which: 0 parameter, 1 Adam m, 2 Adam v.
  * Rows are global ids owned by this rank (world == 1: any id); out/in host [n][dim]. */
 kg_status kg_read_rows(kg_handle *h, int32_t which, const int64_t *ids, int32_t n, float *out);
+/* Collective read ("with G>1 it is collective, gathering rows from their owners"):
+ * every rank calls it with its own n >= 0 global ids (any owner) and receives their rows of table
+ * `which` in out host [n][dim].  Exact per-owner counts are all-gathered, ids and rows exchanged
+ * over NCCL (not the captured step: a few host round trips).  world == 1: kg_read_rows. */
+kg_status kg_gather_rows(kg_handle *h, int32_t which, const int64_t *ids, int32_t n, float *out);
 kg_status kg_write_rows(kg_handle *h, int32_t which, const int64_t *ids, int32_t n, const float *in);
 kg_status kg_read_dense(kg_handle *h, int32_t which, float *out);          /* out [kg_dense_size()] */
 kg_status kg_write_dense(kg_handle *h, int32_t which, const float *in);

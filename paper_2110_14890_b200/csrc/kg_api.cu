@@ -1509,7 +1509,6 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   CK(cudaStreamWaitEvent(st, h->ev_join, 0));
   mark(h, 7);
   CK(cudaGetLastError());
-  // results to pinned host memory (loss, flags, U, t)
   return KG_OK;
 }
 
@@ -1660,6 +1659,81 @@ kg_status step_dist(kg_handle *h, StepBufs &S) {
   return KG_OK;
 }
 
+
+// Per-call device buffers of the untimed paths (kg_score / kg_eval / kg_gather_rows with
+// world > 1), freed in stream order when the call returns.
+struct CallBufs {
+  kg_handle *h;
+  std::vector<void *> p;
+  explicit CallBufs(kg_handle *hh) : h(hh) {}
+  template <class T> T *get(int64_t n) {
+    void *q = nullptr;
+    if (cudaMallocAsync(&q, sizeof(T) * (size_t)std::max<int64_t>(n, 1), h->st) != cudaSuccess) return nullptr;
+    p.push_back(q);
+    return static_cast<T *>(q);
+  }
+  ~CallBufs() {
+    for (void *q : p) cudaFreeAsync(q, h->st);
+  }
+};
+
+// Rows of arbitrary global ids from their owners (owner = id % G, local row id / G; SURVEY
+// §8(b) "collective ... gathering rows from their owners"), collective over the ranks: every
+// rank calls it, each with its own n >= 0 ids (host), and receives tab's rows in id order in
+// d_out [n][d] (device).  Exact counts are all-gathered first (these are not the captured
+// training step; one host round trip per phase).  Leaves the stream synchronised.
+kg_status fetch_rows(kg_handle *h, const int64_t *ids, int64_t n, const float *tab, float *d_out, CallBufs &B) {
+  const int G = h->world, me = h->rank, d = h->d;
+  cudaStream_t st = h->st;
+  std::vector<int64_t> send, pos;                // requests grouped by owner, their positions in ids
+  std::vector<int64_t> so(G + 1, 0), ro(G + 1, 0);
+  send.reserve(n);
+  pos.reserve(n);
+  for (int o = 0; o < G; ++o) {
+    for (int64_t i = 0; i < n; ++i)
+      if (ids[i] % G == o) { send.push_back(ids[i]); pos.push_back(i); }
+    so[o + 1] = (int64_t)send.size();
+  }
+  std::vector<int32_t> cnt(kMaxWorld, 0);
+  for (int o = 0; o < G; ++o) cnt[o] = (int32_t)(so[o + 1] - so[o]);
+  CK(cudaMemcpyAsync(h->counts, cnt.data(), sizeof(int32_t) * kMaxWorld, cudaMemcpyHostToDevice, st));
+  NCK(nccl().AllGather(h->counts, h->all_counts, kMaxWorld, ncclInt32, h->comm, st));
+  CK(cudaMemcpyAsync(h->h_counts, h->all_counts, sizeof(int32_t) * kMaxWorld * G, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int o = 0; o < G; ++o) ro[o + 1] = ro[o] + h->h_counts[o * kMaxWorld + me];
+  const int64_t S = so[G], R = ro[G];
+  int64_t *d_send = B.get<int64_t>(S), *d_recv = B.get<int64_t>(R), *d_pos = B.get<int64_t>(S);
+  float *rows_out = B.get<float>(R * d), *rows_in = B.get<float>(S * d);
+  if (!d_send || !d_recv || !d_pos || !rows_out || !rows_in) return fail(h, KG_ENOMEM, "fetch_rows buffers");
+  if (S) CK(cudaMemcpyAsync(d_send, send.data(), sizeof(int64_t) * S, cudaMemcpyHostToDevice, st));
+  if (S) CK(cudaMemcpyAsync(d_pos, pos.data(), sizeof(int64_t) * S, cudaMemcpyHostToDevice, st));
+  NCK(nccl().GroupStart());
+  for (int o = 0; o < G; ++o) {
+    if (so[o + 1] > so[o]) NCK(nccl().Send(d_send + so[o], so[o + 1] - so[o], ncclInt64, o, h->comm, st));
+    if (ro[o + 1] > ro[o]) NCK(nccl().Recv(d_recv + ro[o], ro[o + 1] - ro[o], ncclInt64, o, h->comm, st));
+  }
+  NCK(nccl().GroupEnd());
+  // owner side: the requested global ids -> local rows -> row copies
+  std::vector<int64_t> req(R);
+  if (R) CK(cudaMemcpyAsync(req.data(), d_recv, sizeof(int64_t) * R, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int64_t i = 0; i < R; ++i) req[i] /= G;
+  if (R) {
+    CK(cudaMemcpyAsync(d_recv, req.data(), sizeof(int64_t) * R, cudaMemcpyHostToDevice, st));
+    launch_gather_rows(rows_out, tab, d_recv, (int)R, d, st);
+  }
+  NCK(nccl().GroupStart());
+  for (int o = 0; o < G; ++o) {
+    if (ro[o + 1] > ro[o]) NCK(nccl().Send(rows_out + ro[o] * d, (ro[o + 1] - ro[o]) * d, ncclFloat32, o, h->comm, st));
+    if (so[o + 1] > so[o]) NCK(nccl().Recv(rows_in + so[o] * d, (so[o + 1] - so[o]) * d, ncclFloat32, o, h->comm, st));
+  }
+  NCK(nccl().GroupEnd());
+  if (S) launch_scatter_rows(d_out, rows_in, d_pos, (int)S, d, st);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
+  return KG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1784,12 +1858,14 @@ kg_status kg_result(kg_handle *h, kg_step_info *info) {
 // Validate a query batch for kg_score / kg_eval and compute its embeddings into h->Q
 // (ingest, relation occurrences, DAG forward); n_cand candidate ids (device, in b_negs)
 // get their rows in h->rows after the anchors.
-static kg_status embed_queries(kg_handle *h, const kg_batch *q, StepBufs &S, int n_cand) {
+// Forward DAG of the queries; with world > 1 the rows of the anchors and the n_cand candidates
+// (already in b_negs) are first fetched from their owners (collective) into a per-call buffer,
+// and rows[] indexes that buffer.
+static kg_status embed_queries(kg_handle *h, const kg_batch *q, StepBufs &S, int n_cand, CallBufs &B) {
   if (q->structure < KG_1P || q->structure > KG_PNI) return fail(h, KG_EINVAL, "bad structure");
   if (single_hop(h->kind) && q->structure != KG_1P) return fail(h, KG_EUNSUPPORTED, "single-hop models accept only 1p");
   if (q->structure >= KG_2IN && h->kind != KG_BETAE)
     return fail(h, KG_EUNSUPPORTED, "negation structures need BetaE (Table 1 'Negation' column)");
-  if (h->world > 1) return fail(h, KG_EUNSUPPORTED, "kg_score / kg_eval with world > 1 are not built yet (DESIGN.md §7)");
   S.plan = make_plan(q->structure);
   kg_batch qb = *q;
   kg_status s;
@@ -1809,6 +1885,20 @@ static kg_status embed_queries(kg_handle *h, const kg_batch *q, StepBufs &S, int
       if (p.n[ni].type == 0) sl.s[u++] = p.n[ni].rel;
   }
   launch_rel_occ(h->b_rels, M, nr, sl, p.nproj, h->R, h->rocc, h->flags + 1, st);
+  if (h->world > 1) {
+    const int64_t L = (int64_t)na * M + n_cand;
+    std::vector<int64_t> ids(L), iota(L);
+    CK(cudaMemcpyAsync(ids.data(), h->ids, sizeof(int64_t) * L, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int64_t i = 0; i < L; ++i) iota[i] = i;
+    float *X = B.get<float>(L * h->d);
+    if (!X) return fail(h, KG_ENOMEM, "score row buffer");
+    kg_status s;
+    if ((s = fetch_rows(h, ids.data(), L, h->t.ent, X, B)) != KG_OK) return s;
+    CK(cudaMemcpyAsync(h->rows, iota.data(), sizeof(int64_t) * L, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));   // iota is a host temporary
+    h->ent_src = X;
+  }
   assign_buffers(h, S);
   return dag_forward(h, S);
 }
@@ -1824,7 +1914,8 @@ kg_status kg_score(kg_handle *h, const kg_batch *q, const int64_t *cand, int32_t
   // candidates share the negative slot of the workspace
   CK(cudaMemcpyAsync(h->b_negs, cand, sizeof(int64_t) * n_cand, cudaMemcpyHostToDevice, st));
   StepBufs S;
-  if ((s = embed_queries(h, q, S, n_cand)) != KG_OK) return s;
+  CallBufs B(h);
+  if ((s = embed_queries(h, q, S, n_cand, B)) != KG_OK) return s;
   const Plan &p = S.plan;
   const int M = q->M, d = h->d, na = p.na;
   const int U = (h->sk == KG_BETAE || h->sk == KG_ROTATE || h->sk == KG_COMPLEX) ? h->m : d;
@@ -1868,8 +1959,27 @@ kg_status kg_eval(kg_handle *h, const kg_batch *q, const int64_t *ans_off, const
   for (int64_t k = 0; k < (int64_t)M * n_neg; ++k)
     if (negatives[k] < 0 || negatives[k] >= h->n_ent) return fail(h, KG_EINVAL, "negative id out of range");
   StepBufs S;
-  if ((s = embed_queries(h, q, S, 0)) != KG_OK) return s;
+  CallBufs B(h);
+  if ((s = embed_queries(h, q, S, 0, B)) != KG_OK) return s;
   cudaStream_t st = h->st;
+  // world > 1: the answer and negative rows come from their owners (collective); the kernel
+  // then reads them by position in the fetched buffer
+  const float *ent = h->ent_src;
+  std::vector<int64_t> pos_ids;
+  if (h->world > 1) {
+    const int64_t nc = n_ans + (int64_t)M * n_neg;
+    std::vector<int64_t> all(nc);
+    std::copy(ans_ids, ans_ids + n_ans, all.begin());
+    if (n_neg > 0) std::copy(negatives, negatives + (int64_t)M * n_neg, all.begin() + n_ans);
+    float *X = B.get<float>(nc * h->d);
+    if (!X) return fail(h, KG_ENOMEM, "eval row buffer");
+    if ((s = fetch_rows(h, all.data(), nc, h->t.ent, X, B)) != KG_OK) return s;
+    pos_ids.resize(nc);
+    for (int64_t i = 0; i < nc; ++i) pos_ids[i] = i;
+    ans_ids = pos_ids.data();
+    negatives = pos_ids.data() + n_ans;
+    ent = X;
+  }
   // per-call buffers (the evaluation path is not part of the captured training step)
   int64_t *d_off = nullptr, *d_ans = nullptr, *d_neg = nullptr;
   int32_t *d_ranks = nullptr;
@@ -1883,7 +1993,7 @@ kg_status kg_eval(kg_handle *h, const kg_batch *q, const int64_t *ans_off, const
   CK(cudaMemcpyAsync(d_ans, ans_ids, sizeof(int64_t) * n_ans, cudaMemcpyHostToDevice, st));
   if (n_neg > 0) CK(cudaMemcpyAsync(d_neg, negatives, sizeof(int64_t) * M * n_neg, cudaMemcpyHostToDevice, st));
   EvalArgs a;
-  a.Q = h->Q; a.ent = h->ent_src; a.ans_off = d_off; a.ans_ids = d_ans; a.negatives = d_neg;
+  a.Q = h->Q; a.ent = ent; a.ans_off = d_off; a.ans_ids = d_ans; a.negatives = d_neg;
   a.M = M; a.d = h->d; a.U = (h->sk == KG_BETAE || h->sk == KG_ROTATE || h->sk == KG_COMPLEX) ? h->m : h->d;
   a.n_neg = n_neg; a.max_ans = (int)max_ans; a.alpha = h->cfg.box_alpha; a.ranks = d_ranks; a.metrics = d_met;
   launch_eval(h->sk, a, S.plan.nout, st);
@@ -1924,6 +2034,23 @@ kg_status kg_read_rows(kg_handle *h, int32_t which, const int64_t *ids, int32_t 
   CK(cudaStreamSynchronize(h->st));
   cudaFree(drows);
   cudaFree(buf);
+  return KG_OK;
+}
+
+kg_status kg_gather_rows(kg_handle *h, int32_t which, const int64_t *ids, int32_t n, float *out) {
+  kg_status s = check_state(h);
+  if (s) return s;
+  float *tab = table_of(h, which);
+  if (!tab || (n > 0 && (!ids || !out)) || n < 0) return fail(h, KG_EINVAL, "bad argument");
+  for (int i = 0; i < n; ++i)
+    if (ids[i] < 0 || ids[i] >= h->n_ent) return fail(h, KG_EINVAL, "id out of range");
+  if (h->world == 1) return n ? kg_read_rows(h, which, ids, n, out) : KG_OK;
+  CallBufs B(h);
+  float *X = B.get<float>((int64_t)n * h->d);
+  if (!X) return fail(h, KG_ENOMEM, "gather buffer");
+  if ((s = fetch_rows(h, ids, n, tab, X, B)) != KG_OK) return s;
+  if (n) CK(cudaMemcpyAsync(out, X, sizeof(float) * (size_t)n * h->d, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
   return KG_OK;
 }
 

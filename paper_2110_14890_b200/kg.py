@@ -67,6 +67,7 @@ _sig = {
     "kg_eval": (C.c_int, [_H, C.POINTER(kg_batch), C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                           C.c_void_p]),
     "kg_read_rows": (C.c_int, [_H, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
+    "kg_gather_rows": (C.c_int, [_H, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
     "kg_write_rows": (C.c_int, [_H, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
     "kg_read_dense": (C.c_int, [_H, C.c_int32, C.c_void_p]),
     "kg_write_dense": (C.c_int, [_H, C.c_int32, C.c_void_p]),
@@ -237,6 +238,14 @@ class KGModel:
         ids = np.ascontiguousarray(ids, np.int64)
         out = np.empty((len(ids), self.cfg.dim), np.float32)
         check(kg_read_rows(self.h, which, ids.ctypes.data, len(ids), out.ctypes.data), self.h)
+        return out
+
+    def gather_rows(self, ids, which=0):
+        """Collective (world > 1: every rank calls it): rows of any global ids, from their owners."""
+        ids = np.ascontiguousarray(ids, np.int64)
+        out = np.empty((len(ids), self.cfg.dim), np.float32)
+        check(kg_gather_rows(self.h, which, ids.ctypes.data if len(ids) else None, len(ids),
+                             out.ctypes.data if len(ids) else None), self.h)
         return out
 
     def write_rows(self, ids, rows, which=0):

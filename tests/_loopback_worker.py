@@ -121,10 +121,71 @@ def overflow_case(G=4, M=200, K=100):
     print("ok overflow", G, flush=True)
 
 
+def collective_case(kind, structure, G=2):
+    """kg_score / kg_eval / kg_gather_rows with world = G (rows fetched from their owners) are
+    bit-identical to one rank holding the whole table (same init, same kernels, same inputs)."""
+    cfg = kggen.ModelConfig(kind, 40, 300, 7, hidden=24)
+    nid = nccl_unique_id()
+    torch.cuda.set_device(0)
+    one = KGModel(cfg, 70, 100, max_cand=90)
+    one.init_params(5)
+    models, outs, errs = [None] * G, [None] * G, [None] * G
+    barrier = threading.Barrier(G)
+    ins = []
+    for r in range(G):
+        rng = np.random.default_rng(40 + r)
+        b = kggen.make_batch(cfg, structure, 70 - 9 * r, 100, seed=3, rank=r)
+        cand = rng.integers(0, 300, size=90 - 17 * r)
+        M = int(b["M"])
+        counts = rng.integers(1, 4, size=M)
+        ans_off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        ans_ids = rng.integers(0, 300, size=int(ans_off[-1]))
+        negs = rng.integers(0, 300, size=(M, 50))
+        ids = rng.integers(0, 300, size=0 if r == 1 else 33)          # rank 1 asks for nothing
+        ins.append((b, cand, ans_off, ans_ids, negs, ids))
+
+    def run(r):
+        try:
+            torch.cuda.set_device(0)
+            models[r] = KGModel(cfg, 70, 100, max_cand=90, rank=r, world=G, nccl_id=nid)
+            barrier.wait()
+            models[r].init_params(5)
+            barrier.wait()
+            b, cand, ans_off, ans_ids, negs, ids = ins[r]
+            hb = models[r].host_batch(b)
+            outs[r] = (models[r].score(hb, cand), models[r].eval(hb, ans_off, ans_ids, negs),
+                       models[r].gather_rows(ids), models[r].gather_rows(ids, which=2))
+        except Exception as e:   # reported below
+            errs[r] = e
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(120)
+    assert not any(t.is_alive() for t in th), "rank thread hung"
+    assert errs == [None] * G, errs
+    for r in range(G):
+        b, cand, ans_off, ans_ids, negs, ids = ins[r]
+        hb = one.host_batch(b)
+        score, (ranks, metrics), rows, vrows = outs[r]
+        assert np.array_equal(score, one.score(hb, cand)), f"{kind} {structure} rank {r} kg_score"
+        ranks1, metrics1 = one.eval(hb, ans_off, ans_ids, negs)
+        assert np.array_equal(ranks, ranks1) and np.array_equal(metrics, metrics1), f"rank {r} kg_eval"
+        assert np.array_equal(rows, one.read_rows(ids)), f"rank {r} kg_gather_rows"
+        assert np.array_equal(vrows, one.read_rows(ids, which=2)), f"rank {r} kg_gather_rows (v)"
+    for m in models + [one]:
+        m.close()
+    print("ok collective", kind, structure, G, flush=True)
+
+
 if __name__ == "__main__":
     for arg in sys.argv[1:]:
         if arg == "overflow":
             overflow_case()
             continue
         parts = arg.split(":")
+        if parts[0] == "collective":
+            collective_case(parts[1], parts[2], G=int(parts[3]) if len(parts) > 3 else 2)
+            continue
         case(parts[0], parts[1], G=int(parts[2]) if len(parts) > 2 else 2)

@@ -32,3 +32,15 @@ def test_bucket_overflow_is_reported_and_transactional():
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "ok overflow" in r.stdout, r.stdout
+
+
+def test_collective_score_eval_gather_match_one_rank():
+    """kg_score / kg_eval / kg_gather_rows at world = 2 and 3 (each rank its own queries,
+    candidates and ids, of different sizes; one rank asks for no rows) equal, bit for bit, the
+    same calls on one rank holding the whole table."""
+    cases = ["collective:q2b:ip", "collective:betae:pni", "collective:complex:1p", "collective:gqe:up:3",
+             "collective:rotate-m:pi"]
+    r = subprocess.run([sys.executable, os.path.join(HERE, "_loopback_worker.py"), *cases],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("ok collective") == len(cases), r.stdout
