@@ -88,7 +88,13 @@ typedef struct {
   int32_t max_cand;      /* workspace sizing: candidates per kg_score call */
   int32_t rank, world;   /* this process's rank in [0, world); theta_E is row-sharded, owner(id) = id % world */
   const void *nccl_id;   /* world > 1: pointer to a 128-byte ncclUniqueId shared by all ranks; NULL if world == 1 */
+  int32_t score_precision; /* KG_SCORE_FP32 (0, default) or KG_SCORE_BF16 (1): the dot-product scorers'
+                            * (DistMult / ComplEx and their -m variants; SURVEY §8(a) a8 "bf16 opt-in") three
+                            * scoring contractions of kg_step with operands rounded to bf16 and fp32
+                            * accumulation (tolerance 2e-2, §8(c)); kg_score / kg_eval stay fp32.
+                            * EUNSUPPORTED for the other kinds, EINVAL for other values. */
 } kg_config;
+enum { KG_SCORE_FP32 = 0, KG_SCORE_BF16 = 1 };
 
 /* Caller-owned device tables (fp32, row-major).
  * ent, ent_m, ent_v : [kg_shard_rows() x dim]  theta_E row shard + Adam moments

@@ -11,6 +11,7 @@
 // i.e. three tcgen05.mma per K-step into the same fp32 TMEM accumulator.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -175,9 +176,21 @@ __device__ __forceinline__ float4 tf32_lo(float4 v) {
   l.w = rna_tf32(v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u));
   return l;
 }
-// split one landed operand tile of R rows (32 G2CW threads, ct = 0 ..)
-template <bool MN, int R>
-__device__ __forceinline__ void split_op(const uint8_t *raw, uint8_t *hi, uint8_t *lo, int ct) {
+__device__ __forceinline__ float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+__device__ __forceinline__ float4 bf16r4(float4 v) { return make_float4(bf16r(v.x), bf16r(v.y), bf16r(v.z), bf16r(v.w)); }
+// split one landed operand tile of R rows (32 G2CW threads, ct = 0 ..).  LOWP (the bf16 score
+// mode): the operand is rounded to bf16 (RNE) instead -- K-major in place, MN-major into hi --
+// and the one MMA per K-step multiplies bf16-exact values (exact products, fp32 accumulation)
+template <bool MN, int R, bool LOWP = false>
+__device__ __forceinline__ void split_op(uint8_t *raw, uint8_t *hi, uint8_t *lo, int ct) {
+  if (LOWP && !MN) {
+#pragma unroll 4
+    for (int c = ct; c < R * 4; c += 32 * G2CW) {
+      float4 *p = reinterpret_cast<float4 *>(raw + c * 16);
+      *p = bf16r4(*p);
+    }
+    return;
+  }
   if (!MN) {   // K-major: same (swizzled) offsets, lo only
 #pragma unroll 4
     for (int c = ct; c < R * 4; c += 32 * G2CW) {
@@ -194,8 +207,12 @@ __device__ __forceinline__ void split_op(const uint8_t *raw, uint8_t *hi, uint8_
       v.y = src[(4 * q + 1) * 32];
       v.z = src[(4 * q + 2) * 32];
       v.w = src[(4 * q + 3) * 32];
-      const float4 l = tf32_lo(v);
       const uint32_t o = sw64_off(r, q);
+      if (LOWP) {
+        *reinterpret_cast<float4 *>(hi + o) = bf16r4(v);
+        continue;
+      }
+      const float4 l = tf32_lo(v);
       *reinterpret_cast<float4 *>(hi + o) = v;
       *reinterpret_cast<float4 *>(lo + o) = l;
     }
@@ -208,7 +225,7 @@ __device__ __forceinline__ void split_op(const uint8_t *raw, uint8_t *hi, uint8_
 // error of the TMEM accumulation grows with the number of MMAs chained into one accumulator
 // (tools/gemm_precision.py: 15-25x SGEMM's at K = 800-1600); chunks of 24 bring it to SGEMM's.
 constexpr int kDrainKB = 4;
-template <int BN, bool AMN, bool BMN, bool DRAIN>
+template <int BN, bool AMN, bool BMN, bool DRAIN, bool LOWP = false>
 __global__ void __launch_bounds__(G2T, 1)
     gemm_tf32x3_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
   KG_GRID_DEP_WAIT();
@@ -286,6 +303,10 @@ __global__ void __launch_bounds__(G2T, 1)
         for (int kk = 0; kk < G2K / 8; ++kk) {   // K = 8 tf32 per MMA
           const uint64_t dah = kmajor_desc(ah, kk), dal = kmajor_desc(al, kk);
           const uint64_t dbh = kmajor_desc(bh, kk), dbl = kmajor_desc(bl, kk);
+          if (LOWP) {   // bf16-rounded operands: one MMA
+            mma_tf32_i<Cfg::kIdesc>(tm, dah, dbh, !(chunk0 && kk == 0));
+            continue;
+          }
           // small terms first: hi.lo, lo.hi, then hi.hi
           mma_tf32_i<Cfg::kIdesc>(tm, dah, dbl, !(chunk0 && kk == 0));
           mma_tf32_i<Cfg::kIdesc>(tm, dal, dbh, 1);
@@ -335,8 +356,8 @@ __global__ void __launch_bounds__(G2T, 1)
       const int s = kb % S;
       mbar_wait(&full_bar[s], (kb / S) & 1);
       uint8_t *st = sm + s * Cfg::kStage;
-      split_op<AMN, GBM>(st, st + Cfg::oAhi, st + Cfg::oAlo, ct);
-      split_op<BMN, BN>(st + Cfg::kA, st + Cfg::oBhi, st + Cfg::oBlo, ct);
+      split_op<AMN, GBM, LOWP>(st, st + Cfg::oAhi, st + Cfg::oAlo, ct);
+      split_op<BMN, BN, LOWP>(st + Cfg::kA, st + Cfg::oBhi, st + Cfg::oBlo, ct);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic stores -> tensor-core reads
       mbar_arrive(&conv_bar[s]);
       // DRAIN: once chunk c's operands are all released, the previous chunk is drained
@@ -428,7 +449,7 @@ bool make_tmap(CUtensorMap *tm, const float *base, int rows, int K, int ld, int 
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, bool AMN, bool BMN, bool DRAIN>
+template <int BN, bool AMN, bool BMN, bool DRAIN, bool LOWP = false>
 bool launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t st) {
   using Cfg = G2Cfg<BN, AMN, BMN>;
   CUtensorMap ta, tb;
@@ -436,7 +457,7 @@ bool launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t s
     return false;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(gemm_tf32x3_tma_kernel<BN, AMN, BMN, DRAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(gemm_tf32x3_tma_kernel<BN, AMN, BMN, DRAIN, LOWP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Cfg::kSmem);
     configured = true;
   }
@@ -450,7 +471,7 @@ bool launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t s
   splits = (nkb + g.kbs - 1) / g.kbs;
   g.P = splits > 1 ? part : nullptr;
   dim3 grid((g.N + BN - 1) / BN, (g.M + GBM - 1) / GBM, splits);
-  { gemm_tf32x3_tma_kernel<BN, AMN, BMN, DRAIN><<<grid, G2T, Cfg::kSmem, st>>>(ta, tb, g); ++g_launches; }
+  { gemm_tf32x3_tma_kernel<BN, AMN, BMN, DRAIN, LOWP><<<grid, G2T, Cfg::kSmem, st>>>(ta, tb, g); ++g_launches; }
   if (splits > 1) {
     const int64_t n = (int64_t)g.M * g.N;
     { gemm_reduce_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(part, splits, g.M, g.N, g.C, g.ldc, g.bias, g.relu,
@@ -458,12 +479,12 @@ bool launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t s
   }
   return true;
 }
-template <int BN, bool DRAIN>
+template <int BN, bool DRAIN, bool LOWP = false>
 bool launch_v2_any(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st) {
-  if (g.a_mn) return g.b_mn ? launch_v2<BN, true, true, DRAIN>(g, part, part_cap, st)
-                            : launch_v2<BN, true, false, DRAIN>(g, part, part_cap, st);
-  return g.b_mn ? launch_v2<BN, false, true, DRAIN>(g, part, part_cap, st)
-                : launch_v2<BN, false, false, DRAIN>(g, part, part_cap, st);
+  if (g.a_mn) return g.b_mn ? launch_v2<BN, true, true, DRAIN, LOWP>(g, part, part_cap, st)
+                            : launch_v2<BN, true, false, DRAIN, LOWP>(g, part, part_cap, st);
+  return g.b_mn ? launch_v2<BN, false, true, DRAIN, LOWP>(g, part, part_cap, st)
+                : launch_v2<BN, false, false, DRAIN, LOWP>(g, part, part_cap, st);
 }
 }  // namespace
 
@@ -480,6 +501,7 @@ bool launch_gemm_tc(const GemmArgs &g, float *part, int64_t part_cap, cudaStream
   if (!gemm_tc_accepts(g)) return false;
   const int64_t t256 = (int64_t)((g.N + 255) / 256) * ((g.M + GBM - 1) / GBM);
   const bool wide = g.N > 128 && t256 >= 100;   // enough 128 x 256 tiles to fill the GPU
+  if (g.lowp) return launch_v2_any<128, false, true>(g, part, part_cap, st);
   if (g.drain) {
     // wave quantisation: e.g. 1536 x 1600 is 156 tiles of 128 x 128 (two waves on 148 SMs) but
     // 120 tiles of 128 x 160 (one)

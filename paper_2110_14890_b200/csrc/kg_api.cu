@@ -454,6 +454,8 @@ struct kg_handle {
   float *Dpart = nullptr, *partQ = nullptr, *partV = nullptr, *Cpart = nullptr, *Csum = nullptr;
   float *Eg = nullptr;     // dot-product scorers: the pool's rows, contiguous (GEMM operand)
   bool gemm_scores = true; // dot-product scorers on the tensor-core GEMM; KG_GEMM_SCORES=0: pair kernels
+  bool score_bf16 = false;  // kg_config.score_precision == KG_SCORE_BF16
+  bool gemm_lowp = false;   // the GEMMs being enqueued take bf16-rounded operands (scoring, bf16 mode)
   int64_t cap_D = 0, cap_Q = 0, cap_V = 0;
   cudaStream_t st2 = nullptr, st_cap = nullptr, st3 = nullptr, st4 = nullptr;
   cudaEvent_t ev_rel = nullptr, ev_loss = nullptr, ev_early = nullptr;
@@ -728,7 +730,8 @@ kg_status gemm(kg_handle *h, bool ta, bool tb, int m, int n, int k, const float 
     // the tensor-core kernel reads either operand layout directly ([k][m] / [k][n] = MN-major)
     GemmArgs g;
     g.A = A; g.B = B; g.C = C; g.M = m; g.N = n; g.K = k; g.lda = lda; g.ldb = ldb; g.ldc = ldc; g.beta = beta;
-    g.bias = bias; g.relu = relu; g.a_mn = ta; g.b_mn = !tb; g.drain = h->gemm_drain;
+    g.bias = bias; g.relu = relu; g.a_mn = ta; g.b_mn = !tb; g.drain = h->gemm_drain && !h->gemm_lowp;
+    g.lowp = h->gemm_lowp;
     if (k > 0 && launch_gemm_tc(g, h->side ? h->gsP2 : h->gsP, h->gsP_cap, h->st)) return KG_OK;
   }
   const float one = 1.f;
@@ -1184,6 +1187,9 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
   if (Lx > dedup_capacity()) return KG_EINVAL;
   if (c.world > kMaxWorld || (c.world > 1 && !c.nccl_id)) return KG_EINVAL;
   if ((int64_t)c.world * Lx > dedup_capacity()) return KG_EINVAL;
+  if (c.score_precision != KG_SCORE_FP32 && c.score_precision != KG_SCORE_BF16) return KG_EINVAL;
+  if (c.score_precision == KG_SCORE_BF16 && base_kind(c.kind) != KG_DISTMULT && base_kind(c.kind) != KG_COMPLEX)
+    return KG_EUNSUPPORTED;   // bf16 scoring only for the dot-product scorers
 
   kg_handle *h = new kg_handle();
   h->cfg = c;
@@ -1250,6 +1256,8 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
   if (const char *e = std::getenv("KG_PDL")) h->use_pdl = !(e[0] == '0');
   if (const char *e = std::getenv("KG_DIST_BUCKETS")) h->buckets = !(e[0] == '0');
   if (const char *e = std::getenv("KG_GEMM_SCORES")) h->gemm_scores = !(e[0] == '0');
+  h->score_bf16 = c.score_precision == KG_SCORE_BF16;
+  if (h->score_bf16) h->gemm_scores = true;   // the bf16 mode lives on the scoring GEMMs
   if (const char *e = std::getenv("KG_DIST_GRAPH")) h->dist_graph = !(e[0] == '0');
   if (const char *e = std::getenv("KG_NCCL")) if (std::string(e) == "loopback") h->dist_graph = false;
   // DAG contractions (reading A24): the hand-written tcgen05 3xTF32 kernel
@@ -1348,6 +1356,12 @@ namespace {
 // gathered into Eg [K][d], S = Q Eg^T is one GEMM (D = -S, A13; the pair epilogue applies the
 // DNF min and Eq. 1 on it), and the backward is two: dQ = -C Eg, dV = -C^T Q (the sign in the
 // combines).  The other scorers (L1 / box / Beta-KL / RotatE) stay on the CUDA-core pair kernels.
+// bf16 score mode for the GEMMs enqueued in a scope (the scoring contractions only)
+struct LowpScope {
+  kg_handle *h;
+  LowpScope(kg_handle *hh, bool on) : h(hh) { h->gemm_lowp = on; }
+  ~LowpScope() { h->gemm_lowp = false; }
+};
 bool gemm_scoring(const kg_handle *h) { return h->gemm_scores && (h->sk == KG_DISTMULT || h->sk == KG_COMPLEX); }
 kg_status score_forward(kg_handle *h, ScoreArgs &sa, int nout, bool train, const int64_t *neg_rows) {
   if (!gemm_scoring(h)) {
@@ -1356,6 +1370,7 @@ kg_status score_forward(kg_handle *h, ScoreArgs &sa, int nout, bool train, const
   }
   launch_gather_rows(h->Eg, h->ent_src, neg_rows, sa.K, h->d, h->st);
   sa.KS = 1;
+  LowpScope lp(h, train && h->score_bf16);
   G(false, true, sa.NQ, sa.K, h->d, sa.Q, h->d, h->Eg, h->d, 0.f, sa.Dpart, sa.Kp);
   launch_pair_epi(h->sk, sa, nout, train, h->st);
   return KG_OK;
@@ -1365,6 +1380,7 @@ kg_status score_backward(kg_handle *h, ScoreArgs &sa, cudaStream_t st2) {
     launch_pair_bwd(h->sk, sa, h->st, st2);
     return KG_OK;
   }
+  LowpScope lp(h, h->score_bf16);
   G(false, false, sa.NQ, h->d, sa.K, sa.C, sa.Kp, h->Eg, h->d, 0.f, sa.partQ, h->d);   // C Eg
   G(true, false, sa.K, h->d, sa.NQ, sa.C, sa.Kp, sa.Q, h->d, 0.f, sa.partV, h->d);    // C^T Q
   sa.JS = 1;

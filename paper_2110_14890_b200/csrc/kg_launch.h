@@ -101,6 +101,7 @@ struct GemmArgs {
   bool b_mn = false;    // B stored [K][N] (ldb) instead of [N][K]
   int kbs = 1 << 30;    // k-blocks per split
   bool drain = false;   // fp32-accurate accumulation: TMEM chunks of kDrainKB k-blocks summed in registers
+  bool lowp = false;    // bf16 score mode: operands rounded to bf16, one MMA per K-step (no 3xTF32 split)
 };
 bool gemm_tc_accepts(const GemmArgs &g);   // 16-byte aligned operands, ld % 4 == 0
 bool launch_gemm_tc(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st);   // false: not launched

@@ -34,7 +34,8 @@ class kg_config(C.Structure):
                 ("n_relations", C.c_int32), ("hidden", C.c_int32), ("gamma", C.c_float),
                 ("box_alpha", C.c_float), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
                 ("max_M", C.c_int32), ("max_K", C.c_int32), ("max_cand", C.c_int32),
-                ("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.c_void_p)]
+                ("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.c_void_p),
+                ("score_precision", C.c_int32)]
 
 
 class kg_tables(C.Structure):
@@ -119,18 +120,21 @@ def _ptr(a):
     return a.data_ptr()   # torch tensor (device or pinned host)
 
 
-def make_config(cfg, max_M, max_K, max_cand=0, rank=0, world=1, nccl_id=None) -> kg_config:
+SCORE_PRECISIONS = {"fp32": 0, "bf16": 1}
+
+
+def make_config(cfg, max_M, max_K, max_cand=0, rank=0, world=1, nccl_id=None, score_precision="fp32") -> kg_config:
     """kg_config from a kggen.ModelConfig-like object (kind, dim, n_entities, ...)."""
     return kg_config(KINDS[cfg.kind], cfg.dim, cfg.n_entities, cfg.n_relations, cfg.hidden or 0,
                      cfg.gamma, cfg.box_alpha, cfg.beta1, cfg.beta2, cfg.eps, max_M, max_K, max_cand,
-                     rank, world, nccl_id)
+                     rank, world, nccl_id, SCORE_PRECISIONS[score_precision])
 
 
 class KGModel:
     """Convenience owner of one handle + its caller-owned tables (torch device memory)."""
 
     def __init__(self, cfg, max_M, max_K, max_cand=0, device="cuda", stream=None, rank=0, world=1,
-                 nccl_id: bytes = None, host_tables=()):
+                 nccl_id: bytes = None, host_tables=(), score_precision="fp32"):
         """host_tables: names among ("ent", "ent_m", "ent_v") to keep in pinned host memory
         (the host tier of kg_bind); the others live in device memory."""
         import torch
@@ -139,7 +143,8 @@ class KGModel:
         self.h = _H()
         self._nccl_id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         self.conf = make_config(cfg, max_M, max_K, max_cand, rank, world,
-                                C.cast(self._nccl_id, C.c_void_p) if self._nccl_id is not None else None)
+                                C.cast(self._nccl_id, C.c_void_p) if self._nccl_id is not None else None,
+                                score_precision)
         check(kg_create(C.byref(self.conf), C.byref(self.h)))
         self.rows = kg_shard_rows(self.h)
         self.dense_size = kg_dense_size(self.h)

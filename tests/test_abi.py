@@ -43,6 +43,7 @@ int main(void) {
   printf("kg_config %zu\nkg_tables %zu\nkg_batch %zu\nkg_step_info %zu\n", sizeof(kg_config),
          sizeof(kg_tables), sizeof(kg_batch), sizeof(kg_step_info));
   O(kg_config, n_entities); O(kg_config, gamma); O(kg_config, max_M); O(kg_config, nccl_id);
+  O(kg_config, score_precision);
   O(kg_batch, anchors); O(kg_batch, mask); O(kg_batch, on_device); O(kg_step_info, step);
   return 0;
 }'''
@@ -65,7 +66,7 @@ int main(void) {
 
 @pytest.mark.parametrize("field,value", [("dim", 12), ("dim", 0), ("n_entities", 0), ("n_relations", 0),
                                          ("max_M", 0), ("world", 0), ("kind", 10), ("kind", -1), ("beta1", 1.0),
-                                         ("eps", 0.0)])
+                                         ("eps", 0.0), ("score_precision", 2), ("score_precision", -1)])
 def test_create_rejects_bad_config(field, value):
     import kggen
     import paper_2110_14890_b200 as kgb
@@ -83,6 +84,20 @@ def test_create_rejects_odd_hidden_for_betae():
     cfg = kggen.ModelConfig("betae", 16, 100, 5, hidden=12)
     h = C.c_void_p()
     assert kgb.kg_create(C.byref(kgb.make_config(cfg, 8, 8)), C.byref(h)) == kgb.kg.KG_EINVAL
+
+
+@pytest.mark.parametrize("kind,status", [("q2b", "KG_EUNSUPPORTED"), ("betae", "KG_EUNSUPPORTED"),
+                                         ("rotate", "KG_EUNSUPPORTED"), ("gqe", "KG_EUNSUPPORTED")])
+def test_bf16_scoring_only_for_dot_product_scorers(kind, status):
+    """the bf16 score mode on a non-dot-product scorer is EUNSUPPORTED (checked
+    before the device is touched)."""
+    import kggen
+    import paper_2110_14890_b200 as kgb
+    cfg = kggen.ModelConfig(kind, 16, 100, 5, hidden=16)
+    h = C.c_void_p()
+    conf = kgb.make_config(cfg, 8, 8, score_precision="bf16")
+    assert kgb.kg_create(C.byref(conf), C.byref(h)) == getattr(kgb.kg, status)
+    assert not h.value
 
 
 def test_sampler_library_exports_every_declared_symbol():

@@ -401,3 +401,38 @@ def test_pipelined_results_in_order():
         b_.result()
     a.close()
     b_.close()
+
+
+@pytest.mark.parametrize("kind,structure,dim", [("distmult", "1p", 40), ("complex", "1p", 40),
+                                                ("complex", "1p", 200), ("distmult-m", "ip", 400),
+                                                ("complex-m", "pi", 200)])
+def test_bf16_score_mode(kind, structure, dim):
+    """score_precision = bf16 (SURVEY §8(a) a8 opt-in, tolerance 2e-2 of §8(c)): the three
+    scoring contractions take bf16-rounded operands; distances, loss and gradients stay within
+    2e-2 of the fp64 oracle, and the mode is really active (the distances differ from the fp32
+    path's).  No union structures here: the DNF min over disjuncts (A11) is a discrete decision
+    that bf16 distances may take differently from the fp64 oracle on near ties (reading A28)."""
+    from paper_2110_14890_b200 import KGModel
+    cfg = kggen.ModelConfig(kind, dim, 300, 7, hidden=24)
+    M, K = 130, 200
+    table = oracle.SparseTable(cfg, 5)
+    b = kggen.make_batch(cfg, structure, M, K, seed=1, step=0, mask_p=0.9)
+    ref = oracle.oracle_step(cfg, table, [b], 1e-3, apply=False)
+    out = {}
+    for prec in ("bf16", "fp32"):
+        gm = KGModel(cfg, M, K, score_precision=prec)
+        gm.init_params(5)
+        gm.set_apply(True, keep_grads=True)
+        info = gm.step(gm.host_batch(b), 1e-3)
+        out[prec] = (info, gm.last_grads(cap=4 * M + M + K + 8, M=M, K=K))
+        gm.close()
+    info, g = out["bf16"]
+    assert abs(info.loss - ref.loss) <= 2e-2 * abs(ref.loss), (info.loss, ref.loss)
+    assert_close(g["d_neg"], ref.d_neg[0], rtol=2e-2, what="D (bf16)")
+    assert_close(g["d_pos"], ref.d_pos[0], what="D+ (fp32 in both modes)")
+    np.testing.assert_array_equal(g["uniq"], ref.uniq)
+    assert_close(g["grad_rows"], ref.grad_rows, rtol=2e-2, what="dL/dtheta_E rows (bf16)")
+    assert_close(g["grad_dense"], ref.grad_dense, rtol=2e-2, what="dL/dtheta_D (bf16)")
+    err_bf16 = np.abs(g["d_neg"] - ref.d_neg[0]).max()
+    err_fp32 = np.abs(out["fp32"][1]["d_neg"] - ref.d_neg[0]).max()
+    assert err_bf16 > 10 * err_fp32, (err_bf16, err_fp32)
