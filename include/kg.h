@@ -141,7 +141,9 @@ typedef struct {
                             the operator weights, on a second stream concurrently with stage 5), 9 the early
                             dense path (Adam of the relation rows the step does not use, g = 0, on a third
                             stream from the end of stage 2, concurrently with stages 3-5).  With world > 1
-                            stage 5 also holds the relation reduce and 6 the all-reduce + dense Adam. */
+                            stage 5 also holds the relation reduce and the row-gradient exchange, and 6
+                            what the all-reduce + dense Adam (on a second stream and communicator,
+                            overlapped with stage 5) add after it. */
 } kg_step_info;
 
 typedef struct kg_handle kg_handle;   /* opaque; one per (process, device) */

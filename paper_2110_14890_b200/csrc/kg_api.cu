@@ -42,6 +42,7 @@ struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t *, ncclConfig_t *) = nullptr;   // optional
   ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
@@ -176,6 +177,35 @@ ncclResult_t CommInitRank(ncclComm_t *comm, int world, ncclUniqueId id, int rank
   *comm = reinterpret_cast<ncclComm_t>(c);
   return ncclSuccess;
 }
+// a second communicator over the same ranks (its own exchange state), e.g. for a collective on
+// another stream; t_comm (the rank's main communicator) is left as it is
+ncclResult_t CommSplit(ncclComm_t parent, int color, int key, ncclComm_t *out, ncclConfig_t *) {
+  Comm *p = reinterpret_cast<Comm *>(parent);
+  char buf[64];
+  std::snprintf(buf, sizeof(buf), "split:%p:%d", (void *)p->s, color);
+  const std::string k(buf);
+  Shared *s = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    for (auto &e : g_reg)
+      if (e.first == k) s = e.second;
+    if (!s) {
+      s = new Shared();
+      s->world = p->s->world;
+      s->posts.resize(s->world);
+      s->ev_ready.resize(s->world);
+      s->ev_done.resize(s->world);
+      for (int r = 0; r < s->world; ++r)
+        if (cudaEventCreateWithFlags(&s->ev_ready[r], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s->ev_done[r], cudaEventDisableTiming) != cudaSuccess)
+          return ncclUnhandledCudaError;
+      g_reg.emplace_back(k, s);
+    }
+  }
+  (void)key;
+  *out = reinterpret_cast<ncclComm_t>(new Comm{s, p->rank});
+  return ncclSuccess;
+}
 ncclResult_t CommDestroy(ncclComm_t comm) {
   Comm *c = reinterpret_cast<Comm *>(comm);
   if (c->tmp) cudaFree(c->tmp);
@@ -277,6 +307,7 @@ const NcclApi &nccl() {
       api.GetUniqueId = loop::GetUniqueId;
       api.CommInitRank = loop::CommInitRank;
       api.CommDestroy = loop::CommDestroy;
+      api.CommSplit = loop::CommSplit;
       api.AllGather = loop::AllGather;
       api.AllReduce = loop::AllReduce;
       api.Send = loop::Send;
@@ -310,6 +341,7 @@ const NcclApi &nccl() {
   get(api.GroupEnd, "ncclGroupEnd");
   get(api.GetErrorString, "ncclGetErrorString");
   api.ok = all;
+  api.CommSplit = reinterpret_cast<decltype(api.CommSplit)>(dlsym(lib, "ncclCommSplit"));   // NCCL >= 2.18
   return api;
 }
 
@@ -475,6 +507,7 @@ struct kg_handle {
   void *blas_ws = nullptr;
   // row-sharded exchange (world > 1, k_dist.cu)
   ncclComm_t comm = nullptr;
+  ncclComm_t comm2 = nullptr;  // world > 1: the dense all-reduce's own communicator (on st2, overlapped)
   const float *ent_src = nullptr;       // rows read by the step: theta_E (world 1) or the received rows
   float *gfull = nullptr;               // dense dL/dtheta_D [dense_size] (weights part = gdense)
   int64_t *send_ids = nullptr, *recv_ids = nullptr, *recv_keys = nullptr, *ouniq = nullptr;
@@ -1250,7 +1283,13 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
     std::memcpy(&id, c.nccl_id, sizeof(id));
     if (!nccl().ok || nccl().CommInitRank(&h->comm, c.world, id, c.rank) != ncclSuccess) { kg_destroy(h); return KG_ENCCL; }
     if (cudaMallocHost(&h->h_counts, sizeof(int32_t) * kMaxWorld * kMaxWorld) != cudaSuccess) { kg_destroy(h); return KG_ENOMEM; }
-    h->use_graphs = false;   // the exchange sizes are read on the host every step
+    // the dL/dtheta_D all-reduce runs on a second stream, overlapped with
+    // the row-gradient exchange and the owners' sparse Adam -- on a communicator of its own
+    // (collectives of one communicator must not run concurrently); KG_DIST_OVERLAP=0: serial
+    const char *ov = std::getenv("KG_DIST_OVERLAP");
+    if (!(ov && ov[0] == '0') && nccl().CommSplit &&
+        nccl().CommSplit(h->comm, 0, c.rank, &h->comm2, nullptr) != ncclSuccess)
+      h->comm2 = nullptr;
   }
   if (const char *e = std::getenv("KG_NO_GRAPH")) h->use_graphs = !(e[0] == '1');
   if (const char *e = std::getenv("KG_PDL")) h->use_pdl = !(e[0] == '0');
@@ -1642,6 +1681,20 @@ kg_status step_dist(kg_handle *h, StepBufs &S) {
     CK(cudaMemsetAsync(h->gdense + (a->off - h->w_off), 0, sizeof(float) * (h->dense_size - a->off), st));
   }
   mark(h, 5);
+  // a14, first half: the dense dL/dtheta_D of this rank (relation reduce + scatter); with a second
+  // communicator its all-reduce and the dense Adam run on st2 while st exchanges the row
+  // gradients and the owners apply sparse Adam
+  launch_rel_reduce(h->rseg, h->rperm, h->rinv, h->rU, Lr, h->RG, h->PSr, h->dr, h->RGU, st);
+  CK(cudaMemsetAsync(h->gfull, 0, sizeof(float) * h->w_off, st));
+  launch_scatter_rel(h->RGU, h->runiq, h->rU, Lr, h->R, h->segs[0].cols, h->kind == KG_Q2B ? 2 : 1, h->gfull, st);
+  const bool overlap = h->comm2 != nullptr;
+  if (overlap) {
+    if ((s = fork(h, st, h->st2)) != KG_OK) return s;
+    NCK(nccl().AllReduce(h->gfull, h->gfull, h->dense_size, ncclFloat32, ncclSum, h->comm2, h->st2));
+    if (h->apply)
+      launch_dense_adam(h->t.dense, h->t.dense_m, h->t.dense_v, h->gfull, h->dense_size, h->lr_dev, h->cfg.beta1,
+                        h->cfg.beta2, h->cfg.eps, h->bc, h->flags, h->st2);
+  }
   // a12: merged row gradients of this rank (distinct-id order) -> send order -> owners
   launch_sparse_adam(h->uniq, h->seg, h->perm, h->inv, h->Udev, L, h->OG, h->PS, d, 1, h->t.ent, h->t.ent_m,
                      h->t.ent_v, h->Gc, h->lr_dev, h->cfg.beta1, h->cfg.beta2, h->cfg.eps, h->bc, h->flags,
@@ -1662,14 +1715,15 @@ kg_status step_dist(kg_handle *h, StepBufs &S) {
                        h->t.ent_m, h->t.ent_v, nullptr, h->lr_dev, h->cfg.beta1, h->cfg.beta2, h->cfg.eps, h->bc,
                        h->flags, 1, st, /*skip_key=*/h->shard);
   mark(h, 6);
-  // a14: dense dL/dtheta_D -> all-reduce -> dense Adam (identical on every rank)
-  launch_rel_reduce(h->rseg, h->rperm, h->rinv, h->rU, Lr, h->RG, h->PSr, h->dr, h->RGU, st);
-  CK(cudaMemsetAsync(h->gfull, 0, sizeof(float) * h->w_off, st));
-  launch_scatter_rel(h->RGU, h->runiq, h->rU, Lr, h->R, h->segs[0].cols, h->kind == KG_Q2B ? 2 : 1, h->gfull, st);
-  NCK(nccl().AllReduce(h->gfull, h->gfull, h->dense_size, ncclFloat32, ncclSum, h->comm, st));
-  if (h->apply)
-    launch_dense_adam(h->t.dense, h->t.dense_m, h->t.dense_v, h->gfull, h->dense_size, h->lr_dev, h->cfg.beta1,
-                      h->cfg.beta2, h->cfg.eps, h->bc, h->flags, st);
+  // a14, second half: all-reduce -> dense Adam (identical on every rank)
+  if (overlap) {
+    if ((s = join(h, h->st2, st)) != KG_OK) return s;
+  } else {
+    NCK(nccl().AllReduce(h->gfull, h->gfull, h->dense_size, ncclFloat32, ncclSum, h->comm, st));
+    if (h->apply)
+      launch_dense_adam(h->t.dense, h->t.dense_m, h->t.dense_v, h->gfull, h->dense_size, h->lr_dev, h->cfg.beta1,
+                        h->cfg.beta2, h->cfg.eps, h->bc, h->flags, st);
+  }
   mark(h, 7);
   CK(cudaGetLastError());
   return KG_OK;
@@ -2244,6 +2298,7 @@ void kg_destroy(kg_handle *h) {
   if (h->ev_rel) cudaEventDestroy(h->ev_rel);
   if (h->ev_loss) cudaEventDestroy(h->ev_loss);
   if (h->ev_early) cudaEventDestroy(h->ev_early);
+  if (h->comm2) nccl().CommDestroy(h->comm2);
   if (h->comm) nccl().CommDestroy(h->comm);
   if (h->h_counts) cudaFreeHost(h->h_counts);
   if (h->ws) cudaFree(h->ws);

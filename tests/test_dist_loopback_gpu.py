@@ -14,13 +14,16 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-@pytest.mark.parametrize("buckets", ["1", "0"])
-def test_ranks_match_the_oracle(buckets):
-    """buckets = 1: fixed-capacity exchange (the default, no host round trip); 0: exact counts."""
+@pytest.mark.parametrize("buckets,overlap", [("1", "1"), ("0", "1"), ("1", "0")])
+def test_ranks_match_the_oracle(buckets, overlap):
+    """buckets = 1: fixed-capacity exchange (the default, no host round trip); 0: exact counts.
+    overlap = 1 (default): the dL/dtheta_D all-reduce + dense Adam on a second stream and
+    communicator, concurrent with the row-gradient exchange; 0: serial."""
     cases = ["q2b:ip", "gqe:up", "betae:pni", "betae:3i", "complex:1p", "q2b:3p", "distmult-m:pi",
              "q2b:2i:4", "betae:ip:4"]
     r = subprocess.run([sys.executable, os.path.join(HERE, "_loopback_worker.py"), *cases],
-                       capture_output=True, text=True, timeout=600, env=dict(os.environ, KG_DIST_BUCKETS=buckets))
+                       capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, KG_DIST_BUCKETS=buckets, KG_DIST_OVERLAP=overlap))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("ok ") == len(cases), r.stdout
 
