@@ -86,11 +86,11 @@ static void run_dedup(const int64_t *ids64, const int32_t *ids32, int L, int end
   size_t bytes = sizeof(typename Sort::TempStorage);
   if (sizeof(typename Disc::TempStorage) > bytes) bytes = sizeof(typename Disc::TempStorage);
   if (sizeof(typename Scan::TempStorage) > bytes) bytes = sizeof(typename Scan::TempStorage);
-  static bool configured = false;   // per-template attribute, set once
-  if (!configured) {
-    cudaFuncSetAttribute(dedup_kernel<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    configured = true;
-  }
+  // per-template attribute, set once (a function-local static: thread-safe initialisation, the
+  // handles of several host threads may launch concurrently)
+  static const bool configured =
+      cudaFuncSetAttribute(dedup_kernel<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess;
+  (void)configured;
   { dedup_kernel<ITEMS><<<1, kDedupThreads, bytes, st>>>(ids64, ids32, L, end_bit, uniq, inv, perm, seg, U_out); ++g_launches; }
 }
 

@@ -6,6 +6,8 @@
 // Adam state over the GPUs (owner(id) = id % G, local row = id / G) and keeps
 // the update synchronous (reading A18).  Every order below is a fixed function
 // of the inputs (deterministic merges, no atomics).
+#include <cstdio>
+
 #include "kg_common.cuh"
 #include "kg_launch.h"
 
@@ -139,6 +141,94 @@ __global__ void local_rows_kernel(const int64_t *ids, int n, int G, int64_t *key
 }
 void launch_local_rows(const int64_t *ids, int n, int G, int64_t *keys, cudaStream_t st, int64_t empty) {
   if (n > 0) { local_rows_kernel<<<(n + 255) / 256, 256, 0, st>>>(ids, n, G, keys, empty); ++g_launches; }
+}
+
+// ---------------------------------------------------------------- peer-memory exchange
+// KG_XCHG=p2p: the ranks' theta_E shards and owner-side receive buffers are
+// mapped into every rank (CUDA IPC over NVLink / NVSwitch; in-process for the loopback test
+// hook), so the row exchange needs no NCCL call: a rank READS the rows it needs straight from
+// the owners' shards into its bucket-ordered row buffer (the same layout the NCCL path
+// receives), and WRITES its merged row gradients straight into the owners' receive buckets;
+// two flag barriers per step order these one-sided accesses against the owners' updates.
+
+// X[send_pos[u]] = theta_E^{owner(id)}[id / G] for the distinct ids u of this rank.
+__global__ void p2p_gather_kernel(const PeerPtrs *__restrict__ pp, const int64_t *uniq, const int32_t *U_dev,
+                                  const int32_t *send_pos, int G, int d4, float4 *X) {
+  KG_GRID_DEP_WAIT();
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int u = (int)(e / d4), c = (int)(e - (int64_t)u * d4);
+  if (u >= *U_dev) return;
+  const int64_t id = uniq[u];
+  const float4 *src = reinterpret_cast<const float4 *>(pp->ent[id % G]);
+  X[(int64_t)send_pos[u] * d4 + c] = src[(id / G) * d4 + c];
+}
+void launch_p2p_gather(const PeerPtrs *pp, const int64_t *uniq, const int32_t *U_dev, const int32_t *send_pos, int G,
+                       int Lmax, int d, float *X, cudaStream_t st) {
+  const int64_t m = (int64_t)Lmax * (d / 4);
+  if (m > 0) {
+    p2p_gather_kernel<<<(int)((m + 255) / 256), 256, 0, st>>>(pp, uniq, U_dev, send_pos, G, d / 4,
+                                                              reinterpret_cast<float4 *>(X));
+    ++g_launches;
+  }
+}
+
+// Bucket o of this rank (ids, -1 = empty slot, and the gradient rows of the filled slots) into
+// owner o's receive buffers at [me][0 .. cap): the layout the NCCL path's receive produces.
+__global__ void p2p_push_kernel(const PeerPtrs *__restrict__ pp, const int64_t *send_ids, const float4 *Gsend, int G,
+                                int me, int cap, int d4) {
+  KG_GRID_DEP_WAIT();
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t slot = e / d4;
+  if (slot >= (int64_t)G * cap) return;
+  const int c = (int)(e - slot * d4), o = (int)(slot / cap), k = (int)(slot - (int64_t)o * cap);
+  const int64_t id = send_ids[slot], dst = (int64_t)me * cap + k;
+  if (c == 0) pp->rids[o][dst] = id;
+  if (id >= 0) reinterpret_cast<float4 *>(pp->grecv[o])[dst * d4 + c] = Gsend[slot * d4 + c];
+  __threadfence_system();
+}
+void launch_p2p_push(const PeerPtrs *pp, const int64_t *send_ids, const float *Gsend, int G, int me, int cap, int d,
+                     cudaStream_t st) {
+  const int64_t m = (int64_t)G * cap * (d / 4);
+  if (m > 0) {
+    p2p_push_kernel<<<(int)((m + 255) / 256), 256, 0, st>>>(pp, send_ids, reinterpret_cast<const float4 *>(Gsend), G,
+                                                            me, cap, d / 4);
+    ++g_launches;
+  }
+}
+
+// All-rank barrier on flags in peer memory: epoch e = ++(*epoch) (identical on every rank:
+// every rank passes the same barriers in the same order), release-store e into flag `me` of
+// every rank, then acquire-spin until all G flags of this rank reach e.  A peer that does not
+// arrive within 20 s sets flags[1] = 3 (the step is reported failed) instead of hanging.
+__global__ void p2p_barrier_kernel(const PeerPtrs *__restrict__ pp, unsigned long long *mine,
+                                   unsigned long long *epoch, int G, int me, int *flags) {
+  KG_GRID_DEP_WAIT();
+  if (threadIdx.x != 0) return;
+  const unsigned long long e = *epoch + 1;
+  *epoch = e;
+  __threadfence_system();
+  for (int o = 0; o < G; ++o)
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(pp->flags[o] + me), "l"(e) : "memory");
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int o = 0; o < G; ++o) {
+    while (true) {
+      unsigned long long v, now;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine + o) : "memory");
+      if (v >= e) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t0 > 20000000000ull) {
+        flags[1] = 3;
+        printf("kg p2p barrier timeout: rank %d epoch %llu waiting on rank %d (flag %llu)\n", me, e, o, v);
+        return;
+      }
+      __nanosleep(256);
+    }
+  }
+}
+void launch_p2p_barrier(const PeerPtrs *pp, unsigned long long *mine, unsigned long long *epoch, int G, int me,
+                        int *flags, cudaStream_t st) {
+  { p2p_barrier_kernel<<<1, 32, 0, st>>>(pp, mine, epoch, G, me, flags); ++g_launches; }
 }
 
 // Dense relation gradient (for the all-reduce): gfull[s*R*w + r*w + c] = RGU[u][s*w + c]

@@ -422,16 +422,17 @@ __global__ void __launch_bounds__(G2T, 1)
 
 namespace {
 PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  // resolved once; a function-local static is initialised thread-safely (with a plain
+  // "tried" flag a second host thread could see the flag before the pointer and fall back
+  // to cuBLAS for its first GEMM -- different rounding than the other ranks)
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void *p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+  }();
   return fn;
 }
 // fp32 operand with `rows` GEMM rows (M or N) and K columns, stored with leading dimension ld:
@@ -455,12 +456,10 @@ bool launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t s
   CUtensorMap ta, tb;
   if (!make_tmap(&ta, g0.A, g0.M, g0.K, g0.lda, GBM, AMN) || !make_tmap(&tb, g0.B, g0.N, g0.K, g0.ldb, BN, BMN))
     return false;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(gemm_tf32x3_tma_kernel<BN, AMN, BMN, DRAIN, LOWP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         Cfg::kSmem);
-    configured = true;
-  }
+  static const bool configured =   // thread-safe one-time attribute (concurrent host threads)
+      cudaFuncSetAttribute(gemm_tf32x3_tma_kernel<BN, AMN, BMN, DRAIN, LOWP>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) == cudaSuccess;
+  (void)configured;
   GemmArgs g = g0;
   const int tiles = ((g.N + BN - 1) / BN) * ((g.M + GBM - 1) / GBM);
   const int nkb = (g.K + G2K - 1) / G2K;

@@ -818,11 +818,9 @@ static void launch_bwd(ScoreArgs a, cudaStream_t st, cudaStream_t st2) {
   a.rps = ((chunks + is - 1) / is) * kIC;
   a.RS = (a.NQ + a.rps - 1) / a.rps;
   const size_t smem = sizeof(float) * (kIC * JB + kIC * Mdl::BQF * 32 + kBW * kIC * Mdl::QF * 32);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(pair_bwd_kernel<Mdl>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
+  static const bool configured =   // thread-safe one-time attribute (concurrent host threads)
+      cudaFuncSetAttribute(pair_bwd_kernel<Mdl>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
+  (void)configured;
   dim3 g(kt, jt, a.RS);
   { pair_bwd_kernel<Mdl><<<g, kBW * 32, smem, st>>>(a); ++g_launches; }
   const int64_t nq = (int64_t)a.NQ * qstride;

@@ -5,6 +5,7 @@
 // which the sm_100a kernels of k_*.cu are enqueued for one training step
 // (§4.1, §4.2, §4.3).
 #include <cublas_v2.h>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -75,6 +76,7 @@ struct Shared {
   int64_t gen = 0;
   std::vector<std::vector<Op>> posts;        // per rank: its sends of the current exchange
   std::vector<cudaEvent_t> ev_ready, ev_done;
+  std::vector<std::vector<void *>> ptrs;     // share_ptrs
 };
 struct Comm {
   Shared *s;
@@ -295,13 +297,30 @@ ncclResult_t AllReduce(const void *sb, void *rb, size_t n, ncclDataType_t t, ncc
   return cudaGetLastError() == cudaSuccess ? ncclSuccess : ncclUnhandledCudaError;
 }
 const char *GetErrorString(ncclResult_t) { return "loopback communicator error"; }
+// host all-gather of the ranks' buffer addresses (the peer-memory exchange's "mapping" when the
+// ranks are threads of one process on one device)
+std::vector<void *> share_ptrs(ncclComm_t comm, const std::vector<void *> &mine) {
+  Comm *c = reinterpret_cast<Comm *>(comm);
+  Shared *s = c->s;
+  {
+    std::lock_guard<std::mutex> lk(s->mu);
+    s->ptrs.resize(s->world);
+    s->ptrs[c->rank] = mine;
+  }
+  barrier(s);
+  std::vector<void *> all;
+  for (int r = 0; r < s->world; ++r) all.insert(all.end(), s->ptrs[r].begin(), s->ptrs[r].end());
+  barrier(s);
+  return all;
+}
 }  // namespace loop
+bool loopback_nccl() {
+  const char *e = std::getenv("KG_NCCL");
+  return e && std::string(e) == "loopback";
+}
 
-const NcclApi &nccl() {
-  static NcclApi api;
-  static bool tried = false;
-  if (tried) return api;
-  tried = true;
+NcclApi load_nccl() {
+  NcclApi api;
   if (const char *e = std::getenv("KG_NCCL")) {
     if (std::string(e) == "loopback") {
       api.GetUniqueId = loop::GetUniqueId;
@@ -342,6 +361,12 @@ const NcclApi &nccl() {
   get(api.GetErrorString, "ncclGetErrorString");
   api.ok = all;
   api.CommSplit = reinterpret_cast<decltype(api.CommSplit)>(dlsym(lib, "ncclCommSplit"));   // NCCL >= 2.18
+  return api;
+}
+// resolved once, thread-safely (function-local static): the ranks of the loopback test are
+// threads that create their handles concurrently
+const NcclApi &nccl() {
+  static const NcclApi api = load_nccl();
   return api;
 }
 
@@ -513,6 +538,10 @@ struct kg_handle {
   int64_t *send_ids = nullptr, *recv_ids = nullptr, *recv_keys = nullptr, *ouniq = nullptr;
   int cap = 0;             // bucket capacity per owner (ids) of the fixed-capacity exchange
   bool buckets = true;     // fixed-capacity exchange (no host round trip); KG_DIST_BUCKETS=0: exact counts
+  bool p2p = false;        // KG_XCHG=p2p: row exchange over peer memory (one-sided), no NCCL for rows
+  PeerPtrs *pp = nullptr;  // device copy of the mapped peer addresses (workspace)
+  unsigned long long *p2p_flags = nullptr, *p2p_epoch = nullptr;   // barrier flags [kMaxWorld], epoch
+  std::vector<void *> ipc_opened;   // peer allocations mapped with cudaIpcOpenMemHandle
   bool dist_graph = true;  // capture world > 1 steps (NCCL only); KG_DIST_GRAPH=0: eager
   int32_t *send_pos = nullptr, *counts = nullptr, *all_counts = nullptr, *oinv = nullptr, *operm = nullptr,
           *oseg = nullptr, *oU = nullptr;
@@ -561,6 +590,11 @@ kg_status fail(kg_handle *h, kg_status s, const std::string &msg) {
     cudaError_t e_ = (call);                                                                   \
     if (e_ != cudaSuccess)                                                                     \
       return fail(h, KG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));            \
+  } while (0)
+#define NCK(call)                                                                                \
+  do {                                                                                           \
+    ncclResult_t r_ = (call);                                                                    \
+    if (r_ != ncclSuccess) return fail(h, KG_ENCCL, std::string(#call) + ": " + nccl().GetErrorString(r_)); \
   } while (0)
 #define CKB(call)                                                                              \
   do {                                                                                         \
@@ -748,6 +782,9 @@ void carve(kg_handle *h, Arena &A) {
     h->Gsend = A.take<float>(SL * d);
     h->Grecv = A.take<float>(GL * d);
     h->PSo = A.take<float>(GL * d);
+    h->pp = reinterpret_cast<PeerPtrs *>(A.take<char>(sizeof(PeerPtrs)));
+    h->p2p_flags = A.take<unsigned long long>(kMaxWorld + 1);
+    h->p2p_epoch = h->p2p_flags ? h->p2p_flags + kMaxWorld : nullptr;
   }
 }
 
@@ -1183,6 +1220,8 @@ kg_status read_result(kg_handle *h, kg_step_info *info, int slot) {
       }
     }
   }
+  if (o.flags[1] == 3)
+    return fail(h, KG_ESTATE, "peer-memory exchange: a rank did not reach the step barrier within 20 s");
   if (o.flags[1] == 2)
     return fail(h, KG_EINVAL, "row exchange bucket overflow (the batch's distinct ids concentrate on one owner beyond "
                               "the fixed capacity); step not applied -- KG_DIST_BUCKETS=0 exchanges exact counts");
@@ -1198,6 +1237,78 @@ kg_status read_latest(kg_handle *h, kg_step_info *info) {
   return read_result(h, info, slot);
 }
 
+}  // namespace
+
+namespace {
+// KG_XCHG=p2p (collective, at kg_bind): every rank's theta_E shard, receive buckets and barrier
+// flags mapped into every rank -- CUDA IPC handles all-gathered over NCCL (the shard's handle
+// is that of its allocation, plus the offset; the workspace has the same layout on every rank),
+// or the plain addresses for the in-process loopback ranks.
+kg_status map_peers(kg_handle *h) {
+  const int G = h->world, me = h->rank;
+  PeerPtrs hp{};
+  if (loopback_nccl()) {
+    const std::vector<void *> all = loop::share_ptrs(h->comm, {h->t.ent, h->recv_ids, h->Grecv, h->p2p_flags});
+    for (int o = 0; o < G; ++o) {
+      hp.ent[o] = static_cast<const float *>(all[4 * o]);
+      hp.rids[o] = static_cast<int64_t *>(all[4 * o + 1]);
+      hp.grecv[o] = static_cast<float *>(all[4 * o + 2]);
+      hp.flags[o] = static_cast<unsigned long long *>(all[4 * o + 3]);
+    }
+  } else {
+    struct Rec {
+      cudaIpcMemHandle_t ent, ws;
+      int64_t ent_off;
+    } rec{};
+    using AddrRange = CUresult (*)(CUdeviceptr *, size_t *, CUdeviceptr);
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(h, KG_EUNSUPPORTED, "KG_XCHG=p2p: cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t bytes = 0;
+    if (reinterpret_cast<AddrRange>(fn)(&base, &bytes, (CUdeviceptr)h->t.ent) != CUDA_SUCCESS)
+      return fail(h, KG_EUNSUPPORTED, "KG_XCHG=p2p: theta_E allocation not found");
+    rec.ent_off = (int64_t)((CUdeviceptr)h->t.ent - base);
+    if (cudaIpcGetMemHandle(&rec.ent, (void *)base) != cudaSuccess || cudaIpcGetMemHandle(&rec.ws, h->ws) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(h, KG_EUNSUPPORTED, "KG_XCHG=p2p: no IPC handle for theta_E / the workspace (e.g. a VMM allocation)");
+    }
+    char *d = nullptr;
+    CK(cudaMalloc(&d, sizeof(Rec) * (G + 1)));
+    CK(cudaMemcpy(d, &rec, sizeof(Rec), cudaMemcpyHostToDevice));
+    NCK(nccl().AllGather(d, d + sizeof(Rec), sizeof(Rec), ncclInt8, h->comm, h->st));
+    std::vector<Rec> all(G);
+    CK(cudaMemcpyAsync(all.data(), d + sizeof(Rec), sizeof(Rec) * G, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    cudaFree(d);
+    const char *wsb = static_cast<const char *>(h->ws);
+    for (int o = 0; o < G; ++o) {
+      char *ent_base = nullptr, *ws_o = nullptr;
+      if (o == me) {
+        ent_base = reinterpret_cast<char *>(base);
+        ws_o = static_cast<char *>(h->ws);
+      } else {
+        if (cudaIpcOpenMemHandle(reinterpret_cast<void **>(&ent_base), all[o].ent, cudaIpcMemLazyEnablePeerAccess) !=
+                cudaSuccess ||
+            cudaIpcOpenMemHandle(reinterpret_cast<void **>(&ws_o), all[o].ws, cudaIpcMemLazyEnablePeerAccess) !=
+                cudaSuccess) {
+          cudaGetLastError();
+          return fail(h, KG_EUNSUPPORTED, "KG_XCHG=p2p: cudaIpcOpenMemHandle failed (peers not on one node?)");
+        }
+        h->ipc_opened.push_back(ent_base);
+        h->ipc_opened.push_back(ws_o);
+      }
+      hp.ent[o] = reinterpret_cast<const float *>(ent_base + all[o].ent_off);
+      hp.rids[o] = reinterpret_cast<int64_t *>(ws_o + (reinterpret_cast<const char *>(h->recv_ids) - wsb));
+      hp.grecv[o] = reinterpret_cast<float *>(ws_o + (reinterpret_cast<const char *>(h->Grecv) - wsb));
+      hp.flags[o] = reinterpret_cast<unsigned long long *>(ws_o + (reinterpret_cast<const char *>(h->p2p_flags) - wsb));
+    }
+  }
+  CK(cudaMemcpy(h->pp, &hp, sizeof(hp), cudaMemcpyHostToDevice));
+  return KG_OK;
+}
 }  // namespace
 
 // ====================================================================== ABI
@@ -1294,6 +1405,14 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
   if (const char *e = std::getenv("KG_NO_GRAPH")) h->use_graphs = !(e[0] == '1');
   if (const char *e = std::getenv("KG_PDL")) h->use_pdl = !(e[0] == '0');
   if (const char *e = std::getenv("KG_DIST_BUCKETS")) h->buckets = !(e[0] == '0');
+  if (const char *e = std::getenv("KG_XCHG")) h->p2p = c.world > 1 && h->buckets && std::string(e) == "p2p";
+  // zeroed before any rank can reach a barrier (a synchronous copy: the steps run on non-blocking
+  // streams, which do not order against the legacy stream of a plain cudaMemset)
+  static const unsigned long long zeros[kMaxWorld + 1] = {};
+  if (h->p2p_flags && cudaMemcpy(h->p2p_flags, zeros, sizeof(zeros), cudaMemcpyHostToDevice) != cudaSuccess) {
+    kg_destroy(h);
+    return KG_ECUDA;
+  }
   if (const char *e = std::getenv("KG_GEMM_SCORES")) h->gemm_scores = !(e[0] == '0');
   h->score_bf16 = c.score_precision == KG_SCORE_BF16;
   if (h->score_bf16) h->gemm_scores = true;   // the bf16 mode lives on the scoring GEMMs
@@ -1361,6 +1480,11 @@ kg_status kg_bind(kg_handle *h, const kg_tables *t, void *stream) {
   h->t = tt;
   h->st = (cudaStream_t)stream;
   CKB(cublasSetStream(h->blas, h->st));
+  if (h->p2p) {
+    if (h->host_tier) return fail(h, KG_EUNSUPPORTED, "KG_XCHG=p2p needs theta_E in device memory");
+    kg_status s = map_peers(h);
+    if (s != KG_OK) return s;
+  }
   h->bound = true;
   return KG_OK;
 }
@@ -1567,11 +1691,6 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   return KG_OK;
 }
 
-#define NCK(call)                                                                                \
-  do {                                                                                           \
-    ncclResult_t r_ = (call);                                                                    \
-    if (r_ != ncclSuccess) return fail(h, KG_ENCCL, std::string(#call) + ": " + nccl().GetErrorString(r_)); \
-  } while (0)
 
 // One step with theta_E row-sharded over G ranks (reading A18):
 // requests of the distinct ids go to their owners, owners return the rows, the
@@ -1620,19 +1739,26 @@ kg_status step_dist(kg_handle *h, StepBufs &S) {
     }
   }
   const int Rtot = (int)ro[G];
-  NCK(nccl().GroupStart());
-  for (int o = 0; o < G; ++o) {
-    if (so[o + 1] > so[o]) NCK(nccl().Send(h->send_ids + so[o], so[o + 1] - so[o], ncclInt64, o, h->comm, st));
-    if (ro[o + 1] > ro[o]) NCK(nccl().Recv(h->recv_ids + ro[o], ro[o + 1] - ro[o], ncclInt64, o, h->comm, st));
+  if (h->p2p) {
+    // one-sided: every owner's previous update (and init) is done once all ranks pass the
+    // barrier; then the rows are read straight from the owners' shards into bucket order
+    launch_p2p_barrier(h->pp, h->p2p_flags, h->p2p_epoch, G, me, h->flags, st);
+    launch_p2p_gather(h->pp, h->uniq, h->Udev, h->send_pos, G, L, d, h->Xin, st);
+  } else {
+    NCK(nccl().GroupStart());
+    for (int o = 0; o < G; ++o) {
+      if (so[o + 1] > so[o]) NCK(nccl().Send(h->send_ids + so[o], so[o + 1] - so[o], ncclInt64, o, h->comm, st));
+      if (ro[o + 1] > ro[o]) NCK(nccl().Recv(h->recv_ids + ro[o], ro[o + 1] - ro[o], ncclInt64, o, h->comm, st));
+    }
+    NCK(nccl().GroupEnd());
+    launch_gather_owned(h->t.ent, h->recv_ids, Rtot, G, d, h->send_rows, st);
+    NCK(nccl().GroupStart());
+    for (int o = 0; o < G; ++o) {
+      if (ro[o + 1] > ro[o]) NCK(nccl().Send(h->send_rows + ro[o] * d, (ro[o + 1] - ro[o]) * d, ncclFloat32, o, h->comm, st));
+      if (so[o + 1] > so[o]) NCK(nccl().Recv(h->Xin + so[o] * d, (so[o + 1] - so[o]) * d, ncclFloat32, o, h->comm, st));
+    }
+    NCK(nccl().GroupEnd());
   }
-  NCK(nccl().GroupEnd());
-  launch_gather_owned(h->t.ent, h->recv_ids, Rtot, G, d, h->send_rows, st);
-  NCK(nccl().GroupStart());
-  for (int o = 0; o < G; ++o) {
-    if (ro[o + 1] > ro[o]) NCK(nccl().Send(h->send_rows + ro[o] * d, (ro[o + 1] - ro[o]) * d, ncclFloat32, o, h->comm, st));
-    if (so[o + 1] > so[o]) NCK(nccl().Recv(h->Xin + so[o] * d, (so[o + 1] - so[o]) * d, ncclFloat32, o, h->comm, st));
-  }
-  NCK(nccl().GroupEnd());
   launch_occ_rows(h->inv, h->send_pos, L, h->rows, st);
   h->ent_src = h->Xin;
 
@@ -1700,12 +1826,19 @@ kg_status step_dist(kg_handle *h, StepBufs &S) {
                      h->t.ent_v, h->Gc, h->lr_dev, h->cfg.beta1, h->cfg.beta2, h->cfg.eps, h->bc, h->flags,
                      /*apply=*/0, st);
   launch_reorder_rows(h->Gc, h->send_pos, h->Udev, L, d, h->Gsend, st);
-  NCK(nccl().GroupStart());
-  for (int o = 0; o < G; ++o) {
-    if (so[o + 1] > so[o]) NCK(nccl().Send(h->Gsend + so[o] * d, (so[o + 1] - so[o]) * d, ncclFloat32, o, h->comm, st));
-    if (ro[o + 1] > ro[o]) NCK(nccl().Recv(h->Grecv + ro[o] * d, (ro[o + 1] - ro[o]) * d, ncclFloat32, o, h->comm, st));
+  if (h->p2p) {
+    // one-sided: ids + gradient rows straight into the owners' receive buckets, then a barrier
+    // (every rank's writes into this rank's buckets are complete)
+    launch_p2p_push(h->pp, h->send_ids, h->Gsend, G, me, cap, d, st);
+    launch_p2p_barrier(h->pp, h->p2p_flags, h->p2p_epoch, G, me, h->flags, st);
+  } else {
+    NCK(nccl().GroupStart());
+    for (int o = 0; o < G; ++o) {
+      if (so[o + 1] > so[o]) NCK(nccl().Send(h->Gsend + so[o] * d, (so[o + 1] - so[o]) * d, ncclFloat32, o, h->comm, st));
+      if (ro[o + 1] > ro[o]) NCK(nccl().Recv(h->Grecv + ro[o] * d, (ro[o + 1] - ro[o]) * d, ncclFloat32, o, h->comm, st));
+    }
+    NCK(nccl().GroupEnd());
   }
-  NCK(nccl().GroupEnd());
   // a13 at the owner: merge the contributions of all ranks (fixed order) + sparse Adam on local rows
   // empty bucket slots carry the key `shard` (one past the last local row), skipped by the update
   launch_local_rows(h->recv_ids, Rtot, G, h->recv_keys, st, h->shard);
@@ -2298,6 +2431,7 @@ void kg_destroy(kg_handle *h) {
   if (h->ev_rel) cudaEventDestroy(h->ev_rel);
   if (h->ev_loss) cudaEventDestroy(h->ev_loss);
   if (h->ev_early) cudaEventDestroy(h->ev_early);
+  for (void *p : h->ipc_opened) cudaIpcCloseMemHandle(p);
   if (h->comm2) nccl().CommDestroy(h->comm2);
   if (h->comm) nccl().CommDestroy(h->comm);
   if (h->h_counts) cudaFreeHost(h->h_counts);

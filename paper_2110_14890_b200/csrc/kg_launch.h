@@ -127,6 +127,19 @@ void launch_gather_owned(const float *ent, const int64_t *ids, int n, int G, int
 void launch_reorder_rows(const float *Gu, const int32_t *send_pos, const int32_t *U_dev, int Lmax, int d, float *out,
                          cudaStream_t st);
 void launch_local_rows(const int64_t *ids, int n, int G, int64_t *keys, cudaStream_t st, int64_t empty = -1);
+// peer-memory exchange (KG_XCHG=p2p, k_dist.cu): the ranks' buffers mapped into every rank
+struct PeerPtrs {
+  const float *ent[kMaxWorld];            // theta_E shards
+  int64_t *rids[kMaxWorld];               // owner-side receive ids   [G][cap]
+  float *grecv[kMaxWorld];                // owner-side receive rows  [G][cap][d]
+  unsigned long long *flags[kMaxWorld];   // barrier flags            [kMaxWorld]
+};
+void launch_p2p_gather(const PeerPtrs *pp, const int64_t *uniq, const int32_t *U_dev, const int32_t *send_pos, int G,
+                       int Lmax, int d, float *X, cudaStream_t st);
+void launch_p2p_push(const PeerPtrs *pp, const int64_t *send_ids, const float *Gsend, int G, int me, int cap, int d,
+                     cudaStream_t st);
+void launch_p2p_barrier(const PeerPtrs *pp, unsigned long long *mine, unsigned long long *epoch, int G, int me,
+                        int *flags, cudaStream_t st);
 void launch_scatter_rel(const float *RGU, const int64_t *runiq, const int32_t *rU, int Lrmax, int R, int w, int nseg,
                         float *gfull, cudaStream_t st);
 void launch_loss_check(double *loss_out, int *flags, int64_t *t_dev, float *bc, double beta1, double beta2, int apply,

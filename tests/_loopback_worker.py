@@ -1,11 +1,19 @@
 """Worker for tests/test_dist_loopback_gpu.py: world = 2 kg_step on ONE GPU, the two ranks as
 threads of this process, their collectives through the library's loopback communicator
-(KG_NCCL=loopback, kg_api.cu), checked against the oracle of the concatenated workers."""
+(KG_NCCL=loopback, kg_api.cu), checked against the oracle of the concatenated workers.
+Every rank has its own CUDA stream, as separate processes would: the peer-memory exchange's
+device-side barriers (KG_XCHG=p2p) need the ranks' kernels to run concurrently."""
 import os
 import sys
 import threading
 
 os.environ["KG_NCCL"] = "loopback"
+# The ranks share one CUDA context here.  With lazy module loading, the first launch of a kernel
+# in one rank's thread can wait for the context's running kernels -- including the other
+# rank's peer-memory barrier kernel (KG_XCHG=p2p), which spins until this rank arrives.
+# Separate processes (the real deployment) have separate contexts; here everything is loaded
+# up front.
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
@@ -45,7 +53,7 @@ def case(kind, structure, G=2, M=70, K=100, steps=2):
             try:
                 torch.cuda.set_device(0)
                 if models[r] is None:
-                    models[r] = KGModel(cfg, M, K, rank=r, world=G, nccl_id=nid)
+                    models[r] = KGModel(cfg, M, K, rank=r, world=G, nccl_id=nid, stream=torch.cuda.Stream())
                     barrier.wait()
                     models[r].init_params(5)
                     models[r].set_apply(True, stage_timing=True)   # the eager stage events too
@@ -94,7 +102,7 @@ def overflow_case(G=4, M=200, K=100):
     def run(r):
         try:
             torch.cuda.set_device(0)
-            models[r] = KGModel(cfg, M, K, rank=r, world=G, nccl_id=nid)
+            models[r] = KGModel(cfg, M, K, rank=r, world=G, nccl_id=nid, stream=torch.cuda.Stream())
             barrier.wait()
             models[r].init_params(5)
             models[r].set_apply(True)
@@ -147,7 +155,8 @@ def collective_case(kind, structure, G=2):
     def run(r):
         try:
             torch.cuda.set_device(0)
-            models[r] = KGModel(cfg, 70, 100, max_cand=90, rank=r, world=G, nccl_id=nid)
+            models[r] = KGModel(cfg, 70, 100, max_cand=90, rank=r, world=G, nccl_id=nid,
+                                 stream=torch.cuda.Stream())
             barrier.wait()
             models[r].init_params(5)
             barrier.wait()
