@@ -61,15 +61,16 @@ void launch_transpose(const float *in, int R, int Cc, int ld_in, float *out, int
   { transpose_kernel<<<grid, block, 0, st>>>(in, R, Cc, ld_in, out, ld_out); ++g_launches; }
 }
 
-// C = beta C + sum_z P[z] (+ bias) (ReLU): the fixed-order combine of the split-K partials.
+// C = beta C + alpha sum_z P[z] (+ bias) (ReLU): the fixed-order combine of the split-K partials.
 __global__ void gemm_reduce_kernel(const float *__restrict__ P, int splits, int M, int N, float *C, int ldc,
-                                   const float *bias, int relu, float beta) {
+                                   const float *bias, int relu, float beta, float alpha) {
   KG_GRID_DEP_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)M * N) return;
   const int row = (int)(e / N), n = (int)(e - (int64_t)row * N);
   float v = 0.f;
   for (int z = 0; z < splits; ++z) v += P[(int64_t)z * M * N + e];
+  v *= alpha;
   if (bias) v += bias[n];
   if (relu) v = fmaxf(v, 0.f);
   float *c = C + (int64_t)row * ldc + n;
@@ -405,7 +406,7 @@ __global__ void __launch_bounds__(G2T, 1)
             g.P[((int64_t)blockIdx.z * g.M + row) * g.N + n] = v;
           } else {
             float *c = g.C + (int64_t)row * g.ldc + n;
-            v += bn;
+            v = fmaf(g.alpha, v, bn);
             if (g.relu) v = fmaxf(v, 0.f);
             if (g.beta != 0.f) v += g.beta * *c;
             *c = v;
@@ -474,7 +475,7 @@ bool launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t s
   if (splits > 1) {
     const int64_t n = (int64_t)g.M * g.N;
     { gemm_reduce_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(part, splits, g.M, g.N, g.C, g.ldc, g.bias, g.relu,
-                                                                g.beta); ++g_launches; }
+                                                                g.beta, g.alpha); ++g_launches; }
   }
   return true;
 }

@@ -843,18 +843,6 @@ void launch_pair_epi(int kind, const ScoreArgs &a, int nout, bool train, cudaStr
   if (kind == DISTMULT) launch_epi_only<MDot>(a, nout, train, st);
   else if (kind == COMPLEX) launch_epi_only<MCpx>(a, nout, train, st);
 }
-template <class Mdl>
-static void launch_combine_only(const ScoreArgs &a, cudaStream_t st) {
-  const int qstride = Mdl::QF * a.U;
-  const int64_t nq = (int64_t)a.NQ * qstride;
-  { bwd_q_combine_kernel<Mdl::kBeta, Mdl::kRowAlpha><<<(int)((nq + 255) / 256), 256, 0, st>>>(a, qstride); ++g_launches; }
-  const int64_t nv = (int64_t)a.K * a.U;
-  { bwd_v_combine_kernel<Mdl><<<(int)((nv + 255) / 256), 256, 0, st>>>(a); ++g_launches; }
-}
-void launch_bwd_combine(int kind, const ScoreArgs &a, cudaStream_t st) {
-  if (kind == DISTMULT) launch_combine_only<MDot>(a, st);
-  else if (kind == COMPLEX) launch_combine_only<MCpx>(a, st);
-}
 
 void launch_pair_bwd(int kind, const ScoreArgs &a, cudaStream_t st, cudaStream_t st2) {
   switch (kind) {

@@ -791,7 +791,7 @@ void carve(kg_handle *h, Arena &A) {
 // Row-major GEMM: C[m x n] = op(A) op(B) + beta C, op(A) is [m x k]; tb: B given as [n x k].
 // The tcgen05 3xTF32 kernel (k_gemm.cu; drained accumulation for BetaE) or cuBLAS SGEMM; see kg_create.
 kg_status gemm(kg_handle *h, bool ta, bool tb, int m, int n, int k, const float *A, int lda, const float *B, int ldb,
-               float beta, float *C, int ldc, const float *bias = nullptr, int relu = 0) {
+               float beta, float *C, int ldc, const float *bias = nullptr, int relu = 0, float alpha = 1.f) {
   if (m <= 0 || n <= 0) return KG_OK;
   // every contraction of the DAG goes to the tcgen05 kernel (measured faster than cuBLAS SGEMM
   // from the d x d DeepSet / attention layers up to the BetaE MLP); the side stream has its
@@ -802,11 +802,11 @@ kg_status gemm(kg_handle *h, bool ta, bool tb, int m, int n, int k, const float 
     g.A = A; g.B = B; g.C = C; g.M = m; g.N = n; g.K = k; g.lda = lda; g.ldb = ldb; g.ldc = ldc; g.beta = beta;
     g.bias = bias; g.relu = relu; g.a_mn = ta; g.b_mn = !tb; g.drain = h->gemm_drain && !h->gemm_lowp;
     g.lowp = h->gemm_lowp;
+    g.alpha = alpha;
     if (k > 0 && launch_gemm_tc(g, h->side ? h->gsP2 : h->gsP, h->gsP_cap, h->st)) return KG_OK;
   }
-  const float one = 1.f;
   h->gemm_count++;
-  CKB(cublasSgemm(h->blas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, n, m, k, &one, B, ldb, A,
+  CKB(cublasSgemm(h->blas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, n, m, k, &alpha, B, ldb, A,
                   lda, &beta, C, ldc));
   if (bias || relu) launch_bias_act(C, bias, m, n, relu, h->st);   // (bias required when relu; ldc == n here)
   return KG_OK;
@@ -1517,8 +1517,8 @@ namespace {
 // a8-a10 for the dot-product scorers (DistMult / ComplEx and their -m variants; SURVEY §8(a)
 // a8: "a tcgen05 dense contraction only for dot-product scorers"): with the pool's rows
 // gathered into Eg [K][d], S = Q Eg^T is one GEMM (D = -S, A13; the pair epilogue applies the
-// DNF min and Eq. 1 on it), and the backward is two: dQ = -C Eg, dV = -C^T Q (the sign in the
-// combines).  The other scorers (L1 / box / Beta-KL / RotatE) stay on the CUDA-core pair kernels.
+// DNF min and Eq. 1 on it), and the backward is two: dQ += -C Eg, dV = -C^T Q (alpha = -1,
+// written straight into the gradient buffers).  The other scorers (L1 / box / Beta-KL / RotatE) stay on the CUDA-core pair kernels.
 // bf16 score mode for the GEMMs enqueued in a scope (the scoring contractions only)
 struct LowpScope {
   kg_handle *h;
@@ -1544,12 +1544,10 @@ kg_status score_backward(kg_handle *h, ScoreArgs &sa, cudaStream_t st2) {
     return KG_OK;
   }
   LowpScope lp(h, h->score_bf16);
-  G(false, false, sa.NQ, h->d, sa.K, sa.C, sa.Kp, h->Eg, h->d, 0.f, sa.partQ, h->d);   // C Eg
-  G(true, false, sa.K, h->d, sa.NQ, sa.C, sa.Kp, sa.Q, h->d, 0.f, sa.partV, h->d);    // C^T Q
-  sa.JS = 1;
-  sa.RS = 1;
-  sa.gsign = -1.f;
-  launch_bwd_combine(h->sk, sa, h->st);
+  // straight into the gradient buffers (no combine pass): dQ += -C Eg on top of the positive
+  // term, the pool rows' raw gradients dV = -C^T Q (rows of d, the layout of OG)
+  G(false, false, sa.NQ, h->d, sa.K, sa.C, sa.Kp, h->Eg, h->d, 1.f, sa.dQ, h->d, nullptr, 0, -1.f);
+  G(true, false, sa.K, h->d, sa.NQ, sa.C, sa.Kp, sa.Q, h->d, 0.f, sa.dV, h->d, nullptr, 0, -1.f);
   return KG_OK;
 }
 

@@ -50,7 +50,6 @@ void launch_pair_bwd(int kind, const ScoreArgs &a, cudaStream_t st, cudaStream_t
 // The dot-product scorers on the tensor-core GEMM (kg_api.cu): the pair epilogue over
 // Dpart (a.KS partials) and the dQ / dV combines over partQ / partV (a.JS / a.RS partials).
 void launch_pair_epi(int kind, const ScoreArgs &a, int nout, bool train, cudaStream_t st);
-void launch_bwd_combine(int kind, const ScoreArgs &a, cudaStream_t st);
 void launch_pos(int kind, const PosArgs &p, int nout, cudaStream_t st);
 void launch_beta_entity(const float *ent, const int64_t *rows, int K, int m, float *F, float *Cv, cudaStream_t st);
 void launch_beta_query(const float *Q, int NQ, int m, float *QP, float *Cq, cudaStream_t st);
@@ -96,6 +95,7 @@ struct GemmArgs {
   const float *bias = nullptr;
   int M = 0, N = 0, K = 0, lda = 0, ldb = 0, ldc = 0, relu = 0;
   float beta = 0.f;
+  float alpha = 1.f;    // C = beta C + alpha op(A) op(B)^T (+ bias) (ReLU)
   float *P = nullptr;   // split-K partials [splits][M][N] (set by launch_gemm_tc)
   bool a_mn = false;    // A stored [K][M] (lda) instead of [M][K]
   bool b_mn = false;    // B stored [K][N] (ldb) instead of [N][K]
