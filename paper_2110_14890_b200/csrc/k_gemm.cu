@@ -508,6 +508,11 @@ bool launch_gemm_tc(const GemmArgs &g, float *part, int64_t part_cap, cudaStream
     const int64_t t128 = (int64_t)((g.N + 127) / 128) * ((g.M + GBM - 1) / GBM);
     const int64_t t160 = (int64_t)((g.N + 159) / 160) * ((g.M + GBM - 1) / GBM);
     if (t128 > 148 && t160 <= 148) return launch_v2_any<160, true>(g, part, part_cap, st);
+    // under half the SMs with a K too short to split (>= 8 k-blocks per split): 128 x 64
+    // tiles, twice the CTAs (e.g. the ComplEx scores S = Q E^T, 1024 x 1024 x 200: 64 -> 128)
+    const int nkb = (g.K + G2K - 1) / G2K;
+    const int64_t t64 = (int64_t)((g.N + 63) / 64) * ((g.M + GBM - 1) / GBM);
+    if (2 * t128 <= 148 && nkb < 16 && t64 <= 148 && t64 > t128) return launch_v2_any<64, true>(g, part, part_cap, st);
     return launch_v2_any<128, true>(g, part, part_cap, st);
   }
   return wide ? launch_v2_any<256, false>(g, part, part_cap, st) : launch_v2_any<128, false>(g, part, part_cap, st);

@@ -78,7 +78,10 @@ def test_gemm_rejects_unaligned_leading_dimension():
 @pytest.mark.parametrize("ta,tb,M,N,K", [(False, True, 1536, 1600, 800),    # H1 = X W1^T: 128 x 160 tiles
                                          (True, True, 1600, 1600, 1536),    # dW2 = dH2^T H1 (MN-major both)
                                          (False, False, 1536, 800, 1600),   # dX = dH1 W1
-                                         (False, True, 200, 72, 40), (True, False, 70, 130, 33)])
+                                         (False, True, 200, 72, 40), (True, False, 70, 130, 33),
+                                         (False, True, 1024, 1024, 200),    # S = Q E^T (ComplEx C3): 128 x 64
+                                         (True, True, 300, 200, 120)])
 def test_gemm_drained_accumulation(ta, tb, M, N, K):
-    """The drained form (fp32-accurate, BetaE's default; 128 x 128 or 128 x 160 tiles)."""
+    """The drained form (fp32-accurate, the default; 128 x 128, 128 x 160 or, for few tiles and a
+    short K, 128 x 64 tiles)."""
     _run(ta, tb, M, N, K, bias=not ta, relu=not ta, drain=True)
