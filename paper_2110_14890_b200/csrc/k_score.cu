@@ -21,6 +21,8 @@
 #include <algorithm>
 #include <type_traits>
 
+#include <cstdlib>
+
 #include "kg_common.cuh"
 #include "kg_launch.h"
 
@@ -535,6 +537,127 @@ __global__ void __launch_bounds__(kBW * 32, BwdOcc<Mdl>::v) pair_bwd_kernel(Scor
   }
 }
 
+// Q2B unions (NOUT = 2, A11): C[t][i][j] is non-zero only for the argmin disjunct t of the
+// pair (i, j) (or for neither), so one pass per QUERY covers both disjunct rows instead of one
+// pass per disjunct row: t(i, j) = [C[1][i][j] != 0] picks the disjunct's box (bit-mask
+// selects) and its dQ accumulators (x {0, 1} products, exact); c = C[0] + C[1] (one is 0,
+// exact).  The terms and their fp32 arithmetic are those of pair_bwd_kernel<MBox>; it writes
+// the same partials (rows t M + i), so the combines are shared.
+constexpr int kICU = 8;   // query rows per staged chunk (two disjunct rows each; 52 KB of shared memory)
+__global__ void __launch_bounds__(kBW * 32, 3) pair_bwd_union_box_kernel(ScoreArgs a) {
+  KG_GRID_DEP_WAIT();
+  constexpr int JB = kBW * kJW;
+  extern __shared__ __align__(16) float smem[];
+  float *sC = smem;                                             // [kICU][JB] C[0] + C[1]
+  float *sT = sC + kICU * JB;                                    // [kICU][JB] t as 0 / 1
+  float *sN = sT + kICU * JB;                                    // [kICU][JB] 1 - t
+  int *sMk = reinterpret_cast<int *>(sN + kICU * JB);            // [kICU][JB] -t (bit mask)
+  float *sQ = reinterpret_cast<float *>(sMk + kICU * JB);        // [kICU][4][32] cA oA cB oB
+  float *sDQ = sQ + kICU * 4 * 32;                               // [kBW][kICU][4][32]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int U = a.U, K = a.K, M = a.M, qstride = 2 * U;
+  const int k = blockIdx.x * 32 + lane;
+  const bool kval = k < U;
+  const int jb0 = blockIdx.y * JB, jw0 = jb0 + w * kJW;
+  const int rb = blockIdx.z * a.rps, re = min(M, rb + a.rps);
+  float ev[kJW], dv[kJW];
+#pragma unroll
+  for (int jj = 0; jj < kJW; ++jj) {
+    const int j = jw0 + jj;
+    const int64_t er = (j < K) ? (a.eidx ? a.eidx[j] : (int64_t)j) : 0;
+    ev[jj] = (j < K && kval) ? a.E[er * a.estride + k] : 0.f;
+    dv[jj] = 0.f;
+  }
+  for (int r0 = rb; r0 < re; r0 += kICU) {
+    for (int e = threadIdx.x; e < kICU * JB / 4; e += blockDim.x) {
+      const int ii = e / (JB / 4), c4 = e - ii * (JB / 4);
+      const int i = r0 + ii, j = jb0 + c4 * 4;
+      float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+      if (i < re && j < a.Kp) {
+        v0 = ld4(a.C + (size_t)i * a.Kp + j);
+        v1 = ld4(a.C + (size_t)(M + i) * a.Kp + j);
+      }
+      *reinterpret_cast<float4 *>(sC + ii * JB + c4 * 4) = make_float4(v0.x + v1.x, v0.y + v1.y, v0.z + v1.z, v0.w + v1.w);
+      const int4 mk = make_int4(-(int)(v1.x != 0.f), -(int)(v1.y != 0.f), -(int)(v1.z != 0.f), -(int)(v1.w != 0.f));
+      *reinterpret_cast<float4 *>(sT + ii * JB + c4 * 4) = make_float4(-mk.x, -mk.y, -mk.z, -mk.w);
+      *reinterpret_cast<float4 *>(sN + ii * JB + c4 * 4) = make_float4(1 + mk.x, 1 + mk.y, 1 + mk.z, 1 + mk.w);
+      *reinterpret_cast<int4 *>(sMk + ii * JB + c4 * 4) = mk;
+    }
+    for (int e = threadIdx.x; e < kICU * 4 * 32; e += blockDim.x) {
+      const int ii = e / 128, f = (e / 32) & 3, l = e & 31;
+      const int i = r0 + ii, kk = blockIdx.x * 32 + l;
+      float v = 0.f;
+      if (i < re && kk < U) v = a.Q[(size_t)((f >> 1) * M + i) * qstride + (f & 1) * U + kk];
+      sQ[e] = v;
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int ii = 0; ii < kICU; ++ii) {
+      const float cA = sQ[(ii * 4 + 0) * 32 + lane], oA = sQ[(ii * 4 + 1) * 32 + lane];
+      const float cB = sQ[(ii * 4 + 2) * 32 + lane], oB = sQ[(ii * 4 + 3) * 32 + lane];
+      const int icA = __float_as_int(cA), icB = __float_as_int(cB), ioA = __float_as_int(oA), ioB = __float_as_int(oB);
+      float2 gA0 = make_float2(0.f, 0.f), gA1 = gA0, gB0 = gA0, gB1 = gA0;
+      const float4 *crow = reinterpret_cast<const float4 *>(sC + ii * JB + w * kJW);
+      const float4 *trow = reinterpret_cast<const float4 *>(sT + ii * JB + w * kJW);
+      const float4 *nrow = reinterpret_cast<const float4 *>(sN + ii * JB + w * kJW);
+      const int4 *mrow = reinterpret_cast<const int4 *>(sMk + ii * JB + w * kJW);
+#pragma unroll
+      for (int j4 = 0; j4 < kJW / 4; ++j4) {
+        const float4 c4 = crow[j4], t4 = trow[j4], n4 = nrow[j4];
+        const int4 m4 = mrow[j4];
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int jp = j4 * 2 + h2;
+          const float2 cf = h2 ? make_float2(c4.z, c4.w) : make_float2(c4.x, c4.y);
+          const float2 tf = h2 ? make_float2(t4.z, t4.w) : make_float2(t4.x, t4.y);
+          const float2 nt = h2 ? make_float2(n4.z, n4.w) : make_float2(n4.x, n4.y);
+          const int mx = h2 ? m4.z : m4.x, my = h2 ? m4.w : m4.y;   // all ones <=> disjunct 1
+          const float2 cs = make_float2(__int_as_float((icA & ~mx) | (icB & mx)), __int_as_float((icA & ~my) | (icB & my)));
+          const float ox = __int_as_float((ioA & ~mx) | (ioB & mx)), oy = __int_as_float((ioA & ~my) | (ioB & my));
+          const float2 t = __fadd2_rn(make_float2(ev[2 * jp], ev[2 * jp + 1]), make_float2(-cs.x, -cs.y));
+          const float ax = fabsf(t.x), ay = fabsf(t.y);
+          const float2 W = make_float2(fmaf(a.alpha, ax < ox ? 1.f : 0.f, ax > ox ? 1.f : 0.f),
+                                       fmaf(a.alpha, ay < oy ? 1.f : 0.f, ay > oy ? 1.f : 0.f));
+          const float2 cw = __fmul2_rn(cf, W);
+          const float2 cg = make_float2(
+              t.x == 0.f ? 0.f : __int_as_float(__float_as_int(cw.x) ^ (__float_as_int(t.x) & 0x80000000)),
+              t.y == 0.f ? 0.f : __int_as_float(__float_as_int(cw.y) ^ (__float_as_int(t.y) & 0x80000000)));
+          gA0 = __ffma2_rn(cg, nt, gA0);
+          gB0 = __ffma2_rn(cg, tf, gB0);
+          gA1 = __ffma2_rn(cw, nt, gA1);
+          gB1 = __ffma2_rn(cw, tf, gB1);
+          const float2 dvp = __fadd2_rn(make_float2(dv[2 * jp], dv[2 * jp + 1]), cg);
+          dv[2 * jp] = dvp.x;
+          dv[2 * jp + 1] = dvp.y;
+        }
+      }
+      float *o = sDQ + ((w * kICU + ii) * 4) * 32 + lane;
+      o[0] = -(gA0.x + gA0.y);
+      o[32] = -(gA1.x + gA1.y);
+      o[64] = -(gB0.x + gB0.y);
+      o[96] = -(gB1.x + gB1.y);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kICU * 4 * 32; e += blockDim.x) {
+      const int ii = e / 128, f = (e / 32) & 3, l = e & 31;
+      const int i = r0 + ii, kk = blockIdx.x * 32 + l;
+      float sum = 0.f;
+#pragma unroll
+      for (int ww = 0; ww < kBW; ++ww) sum += sDQ[ww * kICU * 4 * 32 + e];
+      if (i < re && kk < U)
+        a.partQ[((size_t)blockIdx.y * a.NQ + (size_t)(f >> 1) * M + i) * qstride + (f & 1) * U + kk] = sum;
+    }
+    __syncthreads();
+  }
+  const size_t zs = (size_t)K * U;
+#pragma unroll
+  for (int jj = 0; jj < kJW; ++jj) {
+    const int j = jw0 + jj;
+    if (j >= K || !kval) continue;
+    a.partV[blockIdx.z * zs + (size_t)j * U + k] = dv[jj];
+  }
+}
+
 // dQ[r][f*U + k] += sum_z partQ[z] (+ Q2B offset: alpha * Csum[r]); dQ already holds the
 // positive term.  (BetaE's partials already hold sum_j C (QP - P), see MBeta::grad.)
 template <bool BETA, bool BOX>
@@ -811,6 +934,28 @@ static void launch_bwd(ScoreArgs a, cudaStream_t st, cudaStream_t st2) {
   const int qstride = Mdl::QF * a.U;
   const int kt = (a.U + 31) / 32, jt = (a.K + JB - 1) / JB;
   a.JS = jt;                                   // dQ partials: one per j-block
+  // Q2B unions: one pass per query over both disjunct rows (pair_bwd_union_box_kernel)
+  const bool union_box = std::is_same<Mdl, MBox>::value && a.NQ == 2 * a.M && !std::getenv("KG_UNION_ROWS");
+  if (union_box) {
+    const int chunks = (a.M + kICU - 1) / kICU;
+    int is = (3 * 148 + kt * jt - 1) / (kt * jt);
+    is = std::max(1, std::min(is, std::min(16, chunks)));
+    while (is > 1 && (int64_t)is * a.K * a.U > a.cap_V) --is;
+    a.rps = ((chunks + is - 1) / is) * kICU;
+    a.RS = (a.M + a.rps - 1) / a.rps;
+    const size_t smem = sizeof(float) * (4 * kICU * JB + kICU * 4 * 32 + kBW * kICU * 4 * 32);
+    static const bool configured =
+        cudaFuncSetAttribute(pair_bwd_union_box_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
+        cudaSuccess;
+    (void)configured;
+    dim3 g(kt, jt, a.RS);
+    { pair_bwd_union_box_kernel<<<g, kBW * 32, smem, st>>>(a); ++g_launches; }
+    const int64_t nq = (int64_t)a.NQ * qstride;
+    { bwd_q_combine_kernel<false, true><<<(int)((nq + 255) / 256), 256, 0, st>>>(a, qstride); ++g_launches; }
+    const int64_t nv = (int64_t)a.K * a.U;
+    { bwd_v_combine_kernel<Mdl><<<(int)((nv + 255) / 256), 256, 0, st>>>(a); ++g_launches; }
+    return;
+  }
   const int chunks = (a.NQ + kIC - 1) / kIC;
   int is = (4 * 148 + kt * jt - 1) / (kt * jt);
   is = std::max(1, std::min(is, std::min(16, chunks)));
