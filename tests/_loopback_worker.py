@@ -13,7 +13,8 @@ os.environ["KG_NCCL"] = "loopback"
 # rank's peer-memory barrier kernel (KG_XCHG=p2p), which spins until this rank arrives.
 # Separate processes (the real deployment) have separate contexts; here everything is loaded
 # up front.
-os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+if os.environ.get("KG_XCHG") == "p2p":     # (eager loading of torch's modules costs ~30 s)
+    os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
