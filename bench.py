@@ -270,7 +270,9 @@ def run_ours(args, world, rank, local):
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(args.workload, {}).get(dom)
         if tr is not None:
             roof["traffic"] = round(float(tr))
-            roof["traffic_source"] = "ncu --set full, profiles/r1_ncu_full_top_kernels_final.csv (bytes per step)"
+            roof["traffic_source"] = ("ncu dram__bytes_read.sum + dram__bytes_write.sum of the stage's kernels, one "
+                                      "step per structure, cold caches (tools/step_traffic.py, profiles/r1_step_traffic/; "
+                                      "bytes per step)")
     except (OSError, ValueError):
         pass
     roof.update({"kernel": dom, "peak_source": pk_src if bound == "hbm" else (
