@@ -436,3 +436,78 @@ def test_bf16_score_mode(kind, structure, dim):
     err_bf16 = np.abs(g["d_neg"] - ref.d_neg[0]).max()
     err_fp32 = np.abs(out["fp32"][1]["d_neg"] - ref.d_neg[0]).max()
     assert err_bf16 > 10 * err_fp32, (err_bf16, err_fp32)
+
+
+def _offsets(cfg):
+    off, out = 0, {}
+    for name, shape, _, _ in kggen.dense_layout(cfg):
+        n = int(np.prod(shape))
+        out[name] = (off, shape)
+        off += n
+    return out
+
+
+@pytest.mark.parametrize("structure", ["1p", "2i", "2u"])
+def test_q2b_exact_kinks_follow_A19(structure):
+    """Hand-built exact ties (reading A19; generated data never hits them): query centers equal
+    to candidate rows (t = v - c = 0, d|t|/dt = 0), candidates exactly on the box boundary
+    (|t| = o: ReLU'(0) = 0, min(|t|, o) -> o), relation offsets exactly 0 and negative
+    (ReLU'(0) = 0 in the projection), identical intersection inputs (min ties -> lowest
+    index) and identical union branches (DNF min ties -> lowest disjunct).  The GPU's
+    gradients equal the oracle's (which applies A19 by construction) within 1e-5."""
+    cfg = kggen.ModelConfig("q2b", 16, 50, 3)
+    M, K = 6, 8
+    b = kggen.make_batch(cfg, structure, M, K, seed=21)
+    na = np.asarray(b["anchors"]).reshape(M, -1).shape[1]
+    b["anchors"] = np.tile(np.arange(na, dtype=np.int64), (M, 1)) + 1          # anchors 1 .. na, every query
+    b["relations"] = np.zeros_like(np.asarray(b["relations"]))                   # relation 0 everywhere
+    b["answers"] = np.full(M, 10, np.int64)
+    b["negatives"] = np.array([1, 11, 12, 13, 1, 11, 14, 15], np.int64)          # duplicates on purpose
+    b["mask"] = np.full_like(np.asarray(b["mask"]), 0xFF)
+    d = cfg.dim
+    lay = _offsets(cfg)
+    dense = kggen.init_dense(cfg, 5)
+    oc, _ = lay["rel_center"]
+    oo, _ = lay["rel_offset"]
+    dense[oc:oc + d] = 0.0                                                       # center shift 0: c = anchor
+    roff = np.full(d, 0.25, np.float32)
+    roff[:4] = 0.0                                                               # ReLU'(0) = 0
+    roff[4:6] = -0.5                                                             # ReLU'(<0) = 0
+    dense[oo:oo + d] = roff
+    base = np.full(d, 0.5, np.float32)
+    rows = {i: base.copy() for i in range(1, na + 1)}                            # identical anchors
+    o_box = np.maximum(roff, 0.0)                                                # the 1p offset
+    rows[10] = base + o_box                                                      # answer on the boundary
+    rows[11] = base.copy()                                                       # t = 0 everywhere
+    rows[12] = base - o_box                                                      # other boundary
+    rows[13] = base + 2 * o_box + 0.125                                          # outside / ties where o = 0
+    rows[14] = base + 0.5 * o_box                                                # inside
+    rows[15] = base - 3.0
+    ids = np.array(sorted(rows), np.int64)
+    R = np.stack([rows[i] for i in ids]).astype(np.float32)
+    table = oracle.SparseTable(cfg, 5, dense=dense)
+    table.set(ids, R, np.zeros_like(R), np.zeros_like(R))
+    gm = _model(cfg, M, K)
+    gm.write_dense(dense)
+    gm.write_rows(ids, R)
+    ref = oracle.oracle_step(cfg, table, [b], 1e-3, apply=False)
+    info = gm.step(gm.host_batch(b), 1e-3)
+    g = gm.last_grads(cap=4 * M + M + K + 8, M=M, K=K)
+    assert abs(info.loss - ref.loss) <= RTOL * abs(ref.loss) + 1e-12, (info.loss, ref.loss)
+    np.testing.assert_array_equal(g["uniq"], ref.uniq)
+    assert_close(g["d_neg"], ref.d_neg[0], what="D (ties)")
+    assert_close(g["grad_rows"], ref.grad_rows, what="dL/dtheta_E rows (ties)")
+    assert_close(g["grad_dense"], ref.grad_dense, what="dL/dtheta_D (ties)")
+    gm.close()
+
+
+@pytest.mark.parametrize("kind,structure", [("q2b", "up"), ("betae", "pin"), ("complex", "1p"), ("gqe", "3i")])
+def test_minimal_sizes(kind, structure):
+    """The degenerate batch sizes: one query against a one-entry pool (every tile a ragged
+    tail, split counts of 1)."""
+    cfg = kggen.ModelConfig(kind, 40, 300, 7, hidden=24)
+    gm = _model(cfg, 1, 1)
+    table = oracle.SparseTable(cfg, 5)
+    b = kggen.make_batch(cfg, structure, 1, 1, seed=2, step=0, mask_p=1.0)
+    _check_step(gm, table, cfg, b, lr=1e-6, step_no=1)
+    gm.close()
