@@ -938,7 +938,7 @@ static void launch_bwd(ScoreArgs a, cudaStream_t st, cudaStream_t st2) {
   const bool union_box = std::is_same<Mdl, MBox>::value && a.NQ == 2 * a.M && !std::getenv("KG_UNION_ROWS");
   if (union_box) {
     const int chunks = (a.M + kICU - 1) / kICU;
-    int is = (3 * 148 + kt * jt - 1) / (kt * jt);
+    int is = (3 * 148) / (kt * jt);   // one wave of the 3 resident CTAs per SM (ncu: 5 splits were 1.17 waves)
     is = std::max(1, std::min(is, std::min(16, chunks)));
     while (is > 1 && (int64_t)is * a.K * a.U > a.cap_V) --is;
     a.rps = ((chunks + is - 1) / is) * kICU;
