@@ -957,7 +957,7 @@ static void launch_bwd(ScoreArgs a, cudaStream_t st, cudaStream_t st2) {
     return;
   }
   const int chunks = (a.NQ + kIC - 1) / kIC;
-  int is = (4 * 148 + kt * jt - 1) / (kt * jt);
+  int is = std::max(1, (BwdOcc<Mdl>::v * 148) / (kt * jt));   // one wave of resident CTAs
   is = std::max(1, std::min(is, std::min(16, chunks)));
   while (is > 1 && (int64_t)is * a.K * Mdl::AV * a.U > a.cap_V) --is;
   a.rps = ((chunks + is - 1) / is) * kIC;
