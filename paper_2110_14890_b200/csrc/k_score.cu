@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <type_traits>
 
+#include <climits>
 #include <cstdlib>
 
 #include "kg_common.cuh"
@@ -890,18 +891,35 @@ __global__ void __launch_bounds__(256) loss_finalize_kernel(const float *loss_po
 // ---------------------------------------------------------------- launchers
 // Split counts: enough CTAs for ~4 per SM (148 SMs), bounded by the partial
 // buffers and by whole chunks per split.
-static int split_for(int tiles, int chunks, int64_t cap_floats, int64_t per_split_floats) {
-  int s = (4 * 148 + tiles - 1) / tiles;
-  s = std::max(1, std::min(s, std::min(8, chunks)));
-  while (s > 1 && (int64_t)s * per_split_floats > cap_floats) --s;
-  return s;
+// Unit-range split of the forward: the count minimising (waves of resident CTAs) x (chunks per
+// CTA), ties to fewer parts -- e.g. Q2B unions (114 registers, 2 CTAs per SM): 5 parts were
+// 2.16 waves, 2 parts fit one.  `slots` = resident CTAs of the kernel on the whole GPU.
+static int split_for(int tiles, int chunks, int slots, int64_t cap_floats, int64_t per_split_floats) {
+  if (tiles >= slots) return 1;   // already a full wave: partials would only add traffic (B = K = 4096)
+  int best = 1;
+  int64_t best_cost = INT64_MAX;
+  for (int s = 1; s <= std::min(8, chunks); ++s) {
+    const int per = (chunks + s - 1) / s, parts = (chunks + per - 1) / per;
+    if ((int64_t)parts * per_split_floats > cap_floats) break;
+    const int64_t cost = (((int64_t)tiles * parts + slots - 1) / slots) * per;
+    if (cost < best_cost) { best_cost = cost; best = parts; }
+  }
+  return best;
+}
+template <class F> static int gpu_slots(F kernel, int threads) {
+  int dev = 0, sms = 148, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, 0);
+  return std::max(1, per) * std::max(1, sms);
 }
 
 template <class Mdl>
 static void launch_pair(ScoreArgs a, int nout, bool train, cudaStream_t st) {
   const int tiles = ((a.K + 63) / 64) * ((a.M + 63) / 64);
   const int chunks = (a.U + 15) / 16;
-  a.KS = split_for(tiles, chunks, a.cap_D, (int64_t)nout * a.M * a.Kp);
+  static const int slots1 = gpu_slots(pair_fwd_kernel<Mdl, 1>, 256), slots2 = gpu_slots(pair_fwd_kernel<Mdl, 2>, 256);
+  a.KS = split_for(tiles, chunks, nout == 1 ? slots1 : slots2, a.cap_D, (int64_t)nout * a.M * a.Kp);
   a.ups = ((chunks + a.KS - 1) / a.KS) * 16;
   a.KS = (a.U + a.ups - 1) / a.ups;
   dim3 gf((a.K + 63) / 64, (a.M + 63) / 64, a.KS);
@@ -957,7 +975,11 @@ static void launch_bwd(ScoreArgs a, cudaStream_t st, cudaStream_t st2) {
     return;
   }
   const int chunks = (a.NQ + kIC - 1) / kIC;
-  int is = std::max(1, (BwdOcc<Mdl>::v * 148) / (kt * jt));   // one wave of resident CTAs
+  // row splits: one wave of resident CTAs (floor) unless that leaves > 15 % of the slots idle,
+  // then the next count up (C5: 5 splits = 520 of 592 slots; B = K = 4096: 416 tiles -> 2)
+  const int slots = BwdOcc<Mdl>::v * 148;
+  int is = std::max(1, slots / (kt * jt));
+  if ((int64_t)is * kt * jt * 100 < 85LL * slots) is = (slots + kt * jt - 1) / (kt * jt);
   is = std::max(1, std::min(is, std::min(16, chunks)));
   while (is > 1 && (int64_t)is * a.K * Mdl::AV * a.U > a.cap_V) --is;
   a.rps = ((chunks + is - 1) / is) * kIC;
