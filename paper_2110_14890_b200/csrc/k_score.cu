@@ -662,10 +662,8 @@ __global__ void __launch_bounds__(kBW * 32, 3) pair_bwd_union_box_kernel(ScoreAr
 // dQ[r][f*U + k] += sum_z partQ[z] (+ Q2B offset: alpha * Csum[r]); dQ already holds the
 // positive term.  (BetaE's partials already hold sum_j C (QP - P), see MBeta::grad.)
 template <bool BETA, bool BOX>
-__global__ void bwd_q_combine_kernel(ScoreArgs a, int qstride) {
-  KG_GRID_DEP_WAIT();
+__device__ __forceinline__ void bwd_q_combine(const ScoreArgs &a, int qstride, int64_t e) {
   const int64_t n = (int64_t)a.NQ * qstride;
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= n) return;
   float v = 0.f;
   for (int z = 0; z < a.JS; ++z) v += a.partQ[z * n + e];
@@ -677,11 +675,9 @@ __global__ void bwd_q_combine_kernel(ScoreArgs a, int qstride) {
 // Raw-row gradient of pool entry j: sum_z partials (+ BetaE epilogue with the
 // entity features [A, B, TA, TB, TAB, GA, GB] = F planes 2..8).
 template <class Mdl>
-__global__ void bwd_v_combine_kernel(ScoreArgs a) {
-  KG_GRID_DEP_WAIT();
+__device__ __forceinline__ void bwd_v_combine(const ScoreArgs &a, int64_t e) {
   constexpr int AV = Mdl::AV;
   const int U = a.U, K = a.K;
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)K * U) return;
   const int j = (int)(e / U), k = (int)(e - (int64_t)j * U);
   const size_t zs = (size_t)K * AV * U;
@@ -707,6 +703,22 @@ __global__ void bwd_v_combine_kernel(ScoreArgs a) {
 #pragma unroll
     for (int f = 0; f < Mdl::OUTF; ++f) out[f * U + k] = acc[f];
   }
+}
+
+// Both combines in one launch: blocks [0, nqb) sum the dQ partials, the rest the dV partials.
+template <class Mdl>
+__global__ void bwd_combine_kernel(ScoreArgs a, int qstride, int nqb) {
+  KG_GRID_DEP_WAIT();
+  if ((int)blockIdx.x < nqb)
+    bwd_q_combine<Mdl::kBeta, Mdl::kRowAlpha>(a, qstride, blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+  else
+    bwd_v_combine<Mdl>(a, (blockIdx.x - nqb) * (int64_t)blockDim.x + threadIdx.x);
+}
+template <class Mdl>
+static void launch_combine(const ScoreArgs &a, int qstride, cudaStream_t st) {
+  const int64_t nq = (int64_t)a.NQ * qstride, nv = (int64_t)a.K * a.U;
+  const int nqb = (int)((nq + 255) / 256), nvb = (int)((nv + 255) / 256);
+  if (nqb + nvb > 0) { bwd_combine_kernel<Mdl><<<nqb + nvb, 256, 0, st>>>(a, qstride, nqb); ++g_launches; }
 }
 
 // ---------------------------------------------------------------- positives
@@ -968,10 +980,7 @@ static void launch_bwd(ScoreArgs a, cudaStream_t st, cudaStream_t st2) {
     (void)configured;
     dim3 g(kt, jt, a.RS);
     { pair_bwd_union_box_kernel<<<g, kBW * 32, smem, st>>>(a); ++g_launches; }
-    const int64_t nq = (int64_t)a.NQ * qstride;
-    { bwd_q_combine_kernel<false, true><<<(int)((nq + 255) / 256), 256, 0, st>>>(a, qstride); ++g_launches; }
-    const int64_t nv = (int64_t)a.K * a.U;
-    { bwd_v_combine_kernel<Mdl><<<(int)((nv + 255) / 256), 256, 0, st>>>(a); ++g_launches; }
+    launch_combine<Mdl>(a, qstride, st);
     return;
   }
   const int chunks = (a.NQ + kIC - 1) / kIC;
@@ -990,10 +999,7 @@ static void launch_bwd(ScoreArgs a, cudaStream_t st, cudaStream_t st2) {
   (void)configured;
   dim3 g(kt, jt, a.RS);
   { pair_bwd_kernel<Mdl><<<g, kBW * 32, smem, st>>>(a); ++g_launches; }
-  const int64_t nq = (int64_t)a.NQ * qstride;
-  { bwd_q_combine_kernel<Mdl::kBeta, Mdl::kRowAlpha><<<(int)((nq + 255) / 256), 256, 0, st>>>(a, qstride); ++g_launches; }
-  const int64_t nv = (int64_t)a.K * a.U;
-  { bwd_v_combine_kernel<Mdl><<<(int)((nv + 255) / 256), 256, 0, st>>>(a); ++g_launches; }
+  launch_combine<Mdl>(a, qstride, st);
 }
 
 template <class Mdl>
