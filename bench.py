@@ -151,6 +151,17 @@ def workload_config(args, cfg, w, world):
             "note": w.note}
 
 
+def cpu_model():
+    """The host CPU's model name (the oracle timing records it)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args, world, rank, local):
     import torch
@@ -426,7 +437,7 @@ def cpu_baseline(cfg, batches, seed, budget_s=20.0):
     rate, cores, dt = oracle_time(cfg, batches, 16, 1, seed)
     n = max(1, min(9, int(budget_s / max(dt, 1e-3))))
     rate, cores, dt = oracle_time(cfg, batches, 16, n, seed)
-    return {"value": round(rate, 3), "unit": UNIT, "cores": cores, "kind": "oracle",
+    return {"value": round(rate, 3), "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"{n} steps x 16 of the 512 queries (full K pool, full theta_D Adam), structures "
                       f"round-robin, fp64 torch CPU; {dt:.1f} s"}
 
@@ -452,6 +463,7 @@ def run_reference(args, world, rank):
             "data": "synthetic (kggen, seeded)",
             "config": dict(workload_config(args, cfg, w, 1), queries_per_step_sample=q),
             "cpu_baseline": {"value": round(rate, 3), "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "cpu_model": cpu_model(),
                              "sample": f"{steps_run} steps x {q} queries of the workload (full pool)"},
             "e2e": {"value": round(rate, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
