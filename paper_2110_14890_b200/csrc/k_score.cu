@@ -103,6 +103,14 @@ struct MBeta {  // KL(Beta(entity) || Beta(query)) summed over m (A10), direct p
     dv[1] = fmaf(c, e[3] - q[1], dv[1]);
   }
 };
+// MUFU.RSQ without the denormal-input fixup of rsqrtf (4 extra instructions per call); every
+// caller passes s >= 1e-30 (normal) or discards the result for s <= 1e-30, where |z| < 1e-15 --
+// not reachable by differences of non-equal floats of the embeddings' magnitude (~0.1)
+__device__ __forceinline__ float rsqrt_n(float s) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s));
+  return r;
+}
 struct MRot {  // RotatE: sum_k |q_k - t_k| (A3)
   static constexpr bool kRowAlpha = false;
   static constexpr int QF = 2, EF = 2, EOFF = 0, BQ_EF = 2, BQ_EOFF = 0, BV_EF = 2, BV_EOFF = 0, AV = 2, OUTF = 2;
@@ -111,7 +119,7 @@ struct MRot {  // RotatE: sum_k |q_k - t_k| (A3)
   // 1e-5 bar; the IEEE sqrtf / division sequences made RotatE's pair kernels 3x more instructions)
   __device__ static float acc(const float *q, const float *e, float) {
     const float a = q[0] - e[0], b = q[1] - e[1], s = fmaf(a, a, b * b);
-    return s * rsqrtf(fmaxf(s, 1e-30f));
+    return s * rsqrt_n(fmaxf(s, 1e-30f));
   }
   __device__ static float fin(float s, float, float) { return s; }
   __device__ static void bq(const float *q, const float *e, float c, float, float *dq) {
@@ -125,7 +133,7 @@ struct MRot {  // RotatE: sum_k |q_k - t_k| (A3)
   static constexpr int BF = 2, BOFF = 0, BQF = QF;
   __device__ static void grad(const float *q, const float *e, float c, float, float *dq, float *dv) {
     const float a = q[0] - e[0], b = q[1] - e[1], s = fmaf(a, a, b * b);
-    const float w = s > 0.f ? c * rsqrtf(s) : 0.f;                  // c / |z| (A19: 0 at z = 0)
+    const float w = s > 1e-30f ? c * rsqrt_n(s) : 0.f;              // c / |z| (A19: 0 at z = 0)
     dq[0] += w * a; dq[1] += w * b;
     dv[0] -= w * a; dv[1] -= w * b;
   }
@@ -285,6 +293,36 @@ __global__ void __launch_bounds__(256) pair_fwd_kernel(ScoreArgs a) {
             s1[tt][x][1] = __fadd2_rn(s1[tt][x][1], a1);
             s2[tt][x][0] = __fadd2_rn(s2[tt][x][0], make_float2(fminf(a0.x, os[x]), fminf(a0.y, os[x])));
             s2[tt][x][1] = __fadd2_rn(s2[tt][x][1], make_float2(fminf(a1.x, os[x]), fminf(a1.y, os[x])));
+          }
+        }
+      }
+    } else if constexpr (std::is_same<Mdl, MRot>::value) {
+      // RotatE on packed f32x2 pairs of candidates: |q - t| = s rsqrt(s), s = a^2 + b^2 (the
+      // generic path's arithmetic, two candidates per instruction; the MUFU.RSQ bounds it)
+#pragma unroll 4
+      for (int kk = 0; kk < KC; ++kk) {
+        const float4 er = *reinterpret_cast<const float4 *>(&sE[0][kk][4 * tx]);
+        const float4 ei = *reinterpret_cast<const float4 *>(&sE[1][kk][4 * tx]);
+        const float2 er01 = make_float2(-er.x, -er.y), er23 = make_float2(-er.z, -er.w);
+        const float2 ei01 = make_float2(-ei.x, -ei.y), ei23 = make_float2(-ei.z, -ei.w);
+#pragma unroll
+        for (int tt = 0; tt < NOUT; ++tt) {
+          const float4 qr = *reinterpret_cast<const float4 *>(&sQ[tt][0][kk][4 * ty]);
+          const float4 qi = *reinterpret_cast<const float4 *>(&sQ[tt][1][kk][4 * ty]);
+          const float qrs[4] = {qr.x, qr.y, qr.z, qr.w}, qis[4] = {qi.x, qi.y, qi.z, qi.w};
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            const float2 qre = make_float2(qrs[x], qrs[x]), qim = make_float2(qis[x], qis[x]);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const float2 a2 = __fadd2_rn(qre, h ? er23 : er01), b2 = __fadd2_rn(qim, h ? ei23 : ei01);
+              const float2 s2 = __ffma2_rn(a2, a2, __fmul2_rn(b2, b2));
+              const float2 r2 = make_float2(rsqrt_n(fmaxf(s2.x, 1e-30f)), rsqrt_n(fmaxf(s2.y, 1e-30f)));
+              const float2 d2 = __fmul2_rn(s2, r2);
+              const float2 o = __fadd2_rn(make_float2(acc[tt][x][2 * h], acc[tt][x][2 * h + 1]), d2);
+              acc[tt][x][2 * h] = o.x;
+              acc[tt][x][2 * h + 1] = o.y;
+            }
           }
         }
       }
@@ -503,6 +541,37 @@ __global__ void __launch_bounds__(kBW * 32, BwdOcc<Mdl>::v) pair_bwd_kernel(Scor
         }
         dq[0] = -(gq0.x + gq0.y);
         dq[1] = -(gq1.x + gq1.y);
+      } else if constexpr (std::is_same<Mdl, MRot>::value) {
+        // RotatE on packed f32x2 pairs of pool entries (even j -> .x, odd j -> .y: the generic
+        // path's dq / dq2 split, so the sums are the same): a = q - t, w = C / |z| (0 at z = 0,
+        // A19); dq += w (a, b), dv -= w (a, b).  The FMA pipe was the limiter at 8 unpacked
+        // instructions per term; packed, the MUFU.RSQ is.
+        const float2 qre = make_float2(q[0], q[0]), qim = make_float2(q[1], q[1]);
+        float2 g0 = make_float2(0.f, 0.f), g1 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int j4 = 0; j4 < kJW / 4; ++j4) {
+          const float4 c4 = crow[j4];
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int jp = j4 * 2 + h2;
+            const float2 cf = h2 ? make_float2(c4.z, c4.w) : make_float2(c4.x, c4.y);
+            const float2 a2 = __fadd2_rn(qre, make_float2(-ev[2 * jp][0], -ev[2 * jp + 1][0]));
+            const float2 b2 = __fadd2_rn(qim, make_float2(-ev[2 * jp][1], -ev[2 * jp + 1][1]));
+            const float2 s2 = __ffma2_rn(a2, a2, __fmul2_rn(b2, b2));
+            float2 w2 = __fmul2_rn(cf, make_float2(rsqrt_n(s2.x), rsqrt_n(s2.y)));
+            w2.x = s2.x > 1e-30f ? w2.x : 0.f;
+            w2.y = s2.y > 1e-30f ? w2.y : 0.f;
+            g0 = __ffma2_rn(w2, a2, g0);
+            g1 = __ffma2_rn(w2, b2, g1);
+            const float2 nw = make_float2(-w2.x, -w2.y);
+            const float2 dre = __ffma2_rn(nw, a2, make_float2(dv[2 * jp][0], dv[2 * jp + 1][0]));
+            const float2 dim = __ffma2_rn(nw, b2, make_float2(dv[2 * jp][1], dv[2 * jp + 1][1]));
+            dv[2 * jp][0] = dre.x; dv[2 * jp + 1][0] = dre.y;
+            dv[2 * jp][1] = dim.x; dv[2 * jp + 1][1] = dim.y;
+          }
+        }
+        dq[0] = g0.x; dq2[0] = g0.y;
+        dq[1] = g1.x; dq2[1] = g1.y;
       } else {
 #pragma unroll
         for (int j4 = 0; j4 < kJW / 4; ++j4) {
