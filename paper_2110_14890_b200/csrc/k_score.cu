@@ -572,6 +572,31 @@ __global__ void __launch_bounds__(kBW * 32, BwdOcc<Mdl>::v) pair_bwd_kernel(Scor
         }
         dq[0] = g0.x; dq2[0] = g0.y;
         dq[1] = g1.x; dq2[1] = g1.y;
+      } else if constexpr (std::is_same<Mdl, MBeta>::value) {
+        // BetaE (MBeta::grad) on packed f32x2 pairs of pool entries, element for element the
+        // same fmaf / subtraction sequence (even j -> .x = dq, odd j -> .y = dq2)
+        const float2 a2 = make_float2(q[0], q[0]), b2 = make_float2(q[1], q[1]);
+        const float2 qa = make_float2(q[2], q[2]), qb = make_float2(q[3], q[3]);
+        float2 g0 = make_float2(0.f, 0.f), g1 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int j4 = 0; j4 < kJW / 4; ++j4) {
+          const float4 c4 = crow[j4];
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int jp = j4 * 2 + h2, j0 = 2 * jp, j1 = 2 * jp + 1;
+            const float2 cf = h2 ? make_float2(c4.z, c4.w) : make_float2(c4.x, c4.y);
+            g0 = __ffma2_rn(cf, __fadd2_rn(qa, make_float2(-ev[j0][0], -ev[j1][0])), g0);
+            g1 = __ffma2_rn(cf, __fadd2_rn(qb, make_float2(-ev[j0][1], -ev[j1][1])), g1);
+            const float2 v0 = __ffma2_rn(cf, __fadd2_rn(make_float2(ev[j0][2], ev[j1][2]), make_float2(-a2.x, -a2.y)),
+                                         make_float2(dv[j0][0], dv[j1][0]));
+            const float2 v1 = __ffma2_rn(cf, __fadd2_rn(make_float2(ev[j0][3], ev[j1][3]), make_float2(-b2.x, -b2.y)),
+                                         make_float2(dv[j0][1], dv[j1][1]));
+            dv[j0][0] = v0.x; dv[j1][0] = v0.y;
+            dv[j0][1] = v1.x; dv[j1][1] = v1.y;
+          }
+        }
+        dq[0] = g0.x; dq2[0] = g0.y;
+        dq[1] = g1.x; dq2[1] = g1.y;
       } else {
 #pragma unroll
         for (int j4 = 0; j4 < kJW / 4; ++j4) {
