@@ -45,9 +45,22 @@ def peaks():
 
 # ------------------------------------------------------------------ dist
 def dist_init(gpus):
+    """One process per GPU.  `--gpus N` without a launcher re-executes this script under
+    torch.distributed.run with N ranks (127.0.0.1 rendezvous); under a launcher WORLD_SIZE
+    must equal N (a mismatch would report an N-GPU line measured on another world size)."""
+    if "WORLD_SIZE" not in os.environ and gpus > 1:
+        import socket
+        with socket.socket() as s_:
+            s_.bind(("127.0.0.1", 0))
+            port = s_.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.run(cmd).returncode)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != gpus:
+        raise SystemExit(f"bench.py: --gpus {gpus} but WORLD_SIZE={world}")
     if world > 1:
         import torch
         import torch.distributed as dist
@@ -197,9 +210,12 @@ def run_ours(args, world, rank, local):
     flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()
 
-    # warm-up
+    # warm-up: every step graph the timed region replays is captured here, whatever --warmup says
+    # (one CUDA graph per (structure, M, K): a capture inside the timed steps would be timed)
     for s in range(args.warmup):
         gm.step(db[s % n_distinct], lr, sync=False, on_device=True)
+    for s in range(len(structures)):
+        gm.step(db[(args.warmup + s) % n_distinct], lr, sync=False, on_device=True)
     gm.sync()
     torch.cuda.synchronize()
     barrier(world)

@@ -112,7 +112,8 @@ typedef struct {
  * answers   int64 [M]                         the single positive a_q per query
  * negatives int64 [K]                         the shared pool N, duplicates allowed (A20)
  * mask      uint32 [M][ceil(K/32)]            bit (j%32) of word j/32 set <=> negatives[j] is a
- *                                             negative of query i (Mask_ij of P:L389)
+ *                                             negative of query i (Mask_ij of P:L389); the padding
+ *                                             bits j >= K of the last word are ignored
  * on_device 0: host pointers; 1: device pointers on the handle's device.
  * For kg_score only structure, M, anchors and relations are read.                               */
 typedef struct {

@@ -218,7 +218,10 @@ __global__ void p2p_barrier_kernel(const PeerPtrs *__restrict__ pp, unsigned lon
       if (v >= e) break;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
       if (now - t0 > 20000000000ull) {
+        // flags[0] too: every update kernel queued after this barrier (the owner's sparse Adam)
+        // checks flags[0] only, so none of them applies a stale bucket
         flags[1] = 3;
+        flags[0] |= 2;
         printf("kg p2p barrier timeout: rank %d epoch %llu waiting on rank %d (flag %llu)\n", me, e, o, v);
         return;
       }

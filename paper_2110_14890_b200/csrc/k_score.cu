@@ -391,7 +391,11 @@ __global__ void __launch_bounds__(256) pair_epi_kernel(ScoreArgs a) {
   float inv_n = 0.f;
   if (TRAIN) {
     float n = 0.f;
-    for (int w = threadIdx.x; w < a.W; w += blockDim.x) n += (float)__popc(a.mask[(size_t)i * a.W + w]);
+    for (int w = threadIdx.x; w < a.W; w += blockDim.x) {
+      uint32_t bits = a.mask[(size_t)i * a.W + w];
+      if (w == a.W - 1 && (K & 31)) bits &= (1u << (K & 31)) - 1u;   // padding bits j >= K are not negatives
+      n += (float)__popc(bits);
+    }
     n = block_sum(n, red);
     inv_n = n > 0.f ? 1.f / n : 0.f;
   }

@@ -269,8 +269,10 @@ ncclResult_t AllReduce(const void *sb, void *rb, size_t n, ncclDataType_t t, ncc
   const int W = c->s->world;
   const size_t bytes = n * type_size(t);
   if (c->tmp_bytes < W * bytes) {   // (world > 1 steps are not graph-captured)
-    if (c->tmp) cudaFree(c->tmp);
-    if (cudaMalloc(&c->tmp, W * bytes) != cudaSuccess) return ncclSystemError;
+    // stream-ordered: cudaFree / cudaMalloc may synchronise the device, which would wait for a
+    // peer rank's spinning p2p barrier kernel (same context here) while that rank waits for us
+    if (c->tmp) cudaFreeAsync(c->tmp, st);
+    if (cudaMallocAsync(&c->tmp, W * bytes, st) != cudaSuccess) return ncclSystemError;
     c->tmp_bytes = W * bytes;
   }
   ncclResult_t r = AllGather(sb, c->tmp, n, t, comm, st);   // every rank's input, in rank order
@@ -1221,7 +1223,8 @@ kg_status read_result(kg_handle *h, kg_step_info *info, int slot) {
     }
   }
   if (o.flags[1] == 3)
-    return fail(h, KG_ESTATE, "peer-memory exchange: a rank did not reach the step barrier within 20 s");
+    return fail(h, KG_ESTATE, "peer-memory exchange: a rank did not reach the step barrier within 20 s (theta_E "
+                              "not updated; a dense update already under way may have run; handle unusable)");
   if (o.flags[1] == 2)
     return fail(h, KG_EINVAL, "row exchange bucket overflow (the batch's distinct ids concentrate on one owner beyond "
                               "the fixed capacity); step not applied -- KG_DIST_BUCKETS=0 exchanges exact counts");
@@ -1476,6 +1479,16 @@ kg_status kg_bind(kg_handle *h, const kg_tables *t, void *stream) {
     }
     return fail(h, KG_EINVAL, i < 3 ? "theta_E tables must be device or pinned host memory"
                                     : "theta_D tables must be device memory");
+  }
+  const bool rebind = h->bound;
+  if (rebind && h->p2p)   // the peers mapped this rank's shard and buckets at the first bind
+    return fail(h, KG_ESTATE, "KG_XCHG=p2p: kg_bind may be called once (peers hold the mapped tables)");
+  if (rebind) {
+    // the cached step graphs baked the old table pointers and stream into their kernel
+    // arguments: finish what is in flight, then drop them (recaptured on the next step)
+    CK(cudaStreamSynchronize(h->st));
+    for (auto &g : h->graphs) cudaGraphExecDestroy(g.exec);
+    h->graphs.clear();
   }
   h->t = tt;
   h->st = (cudaStream_t)stream;
