@@ -6,6 +6,8 @@
 // densely after the AllReduce.  Adam per reading A15 (textbook bias
 // correction; bc = [1 - beta1^t, 1 - beta2^t] computed on device by the loss
 // kernel).  All reductions run in a fixed order (no atomics).
+#include <algorithm>
+
 #include "kg_common.cuh"
 #include "kg_launch.h"
 
@@ -129,57 +131,288 @@ __device__ __forceinline__ float4 segment_sum(const int32_t *perm, const float4 
   return g;
 }
 
-// Phase 2 for theta_E: one warp per distinct row u, lanes over float4 columns:
-// G_u, then Adam on (p, m, v) of the row (local row = id / world).  Every touched
-// row is updated, including rows whose gradient is zero (A16).
-__global__ void __launch_bounds__(256) sparse_adam_kernel(const int64_t *uniq, const int32_t *seg,
-                                                          const int32_t *perm, const int32_t *U_dev, const float *OG,
-                                                          const float *PS, int d, int world, float *ent, float *m,
-                                                          float *v, float *grad_out, const float *lr_dev, AdamHyper hy,
-                                                          const float *bc, const int *flags, int apply,
-                                                          int64_t skip_key) {
-  KG_GRID_DEP_WAIT();
-  const int u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (u >= *U_dev || uniq[u] == skip_key) return;   // skip_key: the empty-slot key of bucketed exchanges
-  const int d4 = d >> 2, s0 = seg[u], s1 = seg[u + 1];
+// Fused segment reduce + sparse Adam for theta_E (a12 + a13): one launch, no atomics on
+// rows, every row staged through shared memory by bulk copies (TMA, cp.async.bulk), so a
+// warp keeps its whole row in flight without holding it in registers.  The sorted
+// occurrence positions are cut into the pieces defined above (a piece starts at every
+// segment head and at every multiple of kPiece).  One warp per item:
+//
+//  * chunk item (c, q), items [0, nch * NS), launched first (the hot rows' chains are the
+//    longest): sorted positions [kPiece c, kPiece c + kPiece) x the q-th of NS column
+//    slices.  The occurrence rows of every repeated segment in the chunk are copied in
+//    together (one bulk copy of the slice per position) and summed into their pieces in
+//    position order.  A segment inside one piece gets its Adam update here, on the slice
+//    (its p, m, v slices were prefetched to L2 with the copies).  A segment of several
+//    pieces (hot Zipf anchors) writes each piece sum to PS[piece start]; the item
+//    completing the last piece of (u, q) -- arrival counter cnt[u * kSlices + q], reset by
+//    that item -- sums the pieces in ascending order and applies Adam to the slice.
+//  * head item u, items [nch * NS, nch * NS + L): a distinct row with ONE occurrence
+//    (every pool row but a few, most answers; hrow[u] >= 0): bulk copies of its p, m, v
+//    rows and of its gradient row into the warp's shared memory, one mbarrier, then Adam
+//    with lanes over float4 columns and coalesced stores.  Repeated rows return at once.
+//
+// Every sum runs in a fixed order (deterministic run to run).  With `early`, index loads
+// and the p / m / v copies go out before griddepcontrol.wait: the row ids come from the
+// dedup at the start of the step and theta_E / m / v are written by no kernel of the step
+// before this one; only the occurrence gradients (and flags) wait for the predecessor.
+constexpr int kSlices = 16;   // column slices per row (counter stride): d <= 16 * 32 * 4
+#ifndef KG_SA_PROBE
+#define KG_SA_PROBE 0         // tools/sparse_probe.py variants: 1 head items only, 2 chunk items only, 3 trace
+#endif
+#if KG_SA_PROBE == 3
+__device__ unsigned long long g_sa_trace[1 << 16][4];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define SA_T(k) do { if (lane == 0 && w < (1 << 16)) g_sa_trace[w][k] = gtime(); } while (0)
+}  // namespace kg
+extern "C" int probe_trace(unsigned long long *out) {
+  return (int)cudaMemcpyFromSymbol(out, kg::g_sa_trace, sizeof(unsigned long long) * (1 << 18));
+}
+extern "C" int probe_trace_clear() {
+  static unsigned long long z[1 << 18];
+  return (int)cudaMemcpyToSymbol(kg::g_sa_trace, z, sizeof(z));
+}
+namespace kg {
+#else
+#define SA_T(k) do {} while (0)
+#endif
+
+__device__ __forceinline__ void add4(float4 &a, const float4 &b) { a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w; }
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint64_t *b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(b)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ void bar_wait0(uint64_t *b) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\nselp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(done)
+                 : "r"(smem_u32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+template <bool EARLY>
+__global__ void __launch_bounds__(128, 8) sparse_adam_fused_kernel(const int64_t *uniq, const int32_t *seg,
+                                                                   const int32_t *perm, const int32_t *sinv,
+                                                                   const int32_t *hrow, const int32_t *U_dev, int L,
+                                                                   const float *OG, float *PS, int32_t *cnt, int d,
+                                                                   int world, int ns, int sw, int wbytes, float *ent,
+                                                                   float *m, float *v, float *grad_out,
+                                                                   const float *lr_dev, AdamHyper hy, const float *bc,
+                                                                   const int *flags, int apply, int64_t skip_key) {
+  extern __shared__ __align__(128) uint8_t sa_smem[];
+  __shared__ __align__(8) uint64_t sa_bar[4];
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w = blockIdx.x * 4 + wi;
+  const int d4 = d >> 2;
+  float4 *sm = reinterpret_cast<float4 *>(sa_smem + (size_t)wi * wbytes);
+  uint64_t *bar = &sa_bar[wi];
+  const float4 *X4 = reinterpret_cast<const float4 *>(OG);
+  float4 *P4 = reinterpret_cast<float4 *>(PS);
+  float4 *E4 = reinterpret_cast<float4 *>(ent), *M4 = reinterpret_cast<float4 *>(m),
+         *V4 = reinterpret_cast<float4 *>(v), *GO4 = reinterpret_cast<float4 *>(grad_out);
+  const int nch = (L + kPiece - 1) / kPiece;
+
+  if (w >= nch * ns) {
+    // ---------------------------------------------------------------- head item
+    const int u = w - nch * ns;
+#if KG_SA_PROBE == 2
+    return;
+#endif
+    SA_T(0);
+    if (!EARLY) KG_GRID_DEP_WAIT();
+    // u < L <= the capacity of hrow / uniq: the three loads go out together, U is checked after
+    const int Ud = *U_dev, r0 = hrow[u];          // r0: the row's one occurrence, -1 if repeated
+    const int64_t key = uniq[u];
+    if (u >= Ud || r0 < 0) return;                // repeated rows: the chunk items
+    if (key == skip_key) return;                  // the empty-slot key of bucketed exchanges
+    const int64_t rowoff = (key / world) * d4;
+    const uint32_t rb = (uint32_t)d * 4u;
+    SA_T(1);
+    if (lane == 0) {
+      bar_init(bar);
+      bar_expect(bar, (apply ? 4u : 1u) * rb);
+      if (apply) {                                // smem: [P | M | V | G]
+        bulk_g2s(sm, E4 + rowoff, rb, bar);
+        bulk_g2s(sm + d4, M4 + rowoff, rb, bar);
+        bulk_g2s(sm + 2 * d4, V4 + rowoff, rb, bar);
+      }
+    }
+    if (EARLY) KG_GRID_DEP_WAIT();
+    if (lane == 0) bulk_g2s(sm + 3 * d4, X4 + (int64_t)r0 * d4, rb, bar);
+    const bool upd = apply && !flags[0];          // the step's go / no-go, after the wait
+    const float lr1 = *lr_dev * bc[0], ibc2 = bc[1];
+    __syncwarp();
+    bar_wait0(bar);
+    SA_T(2);
+    for (int c = lane; c < d4; c += 32) {
+      const float4 G = sm[3 * d4 + c];
+      if (GO4) GO4[(int64_t)u * d4 + c] = G;
+      if (!upd) continue;
+      float4 P = sm[c], Mm = sm[d4 + c], V = sm[2 * d4 + c];
+      adam4(P, Mm, V, G, lr1, hy, ibc2);
+      E4[rowoff + c] = P; M4[rowoff + c] = Mm; V4[rowoff + c] = V;
+    }
+    SA_T(3);
+    return;
+  }
+
+  // ------------------------------------------------------------------ chunk item (c, q)
+#if KG_SA_PROBE == 1
+  return;
+#endif
+  SA_T(0);
+  const int c = w / ns, q = w - c * ns;
+  const int base = c * kPiece;
+  const int n = min(kPiece, L - base);
+  const int c0 = q * sw, cw = min(sw, d4 - c0);   // this slice: float4 columns [c0, c0 + cw)
+  const int col = c0 + lane;
+  const bool cv = lane < cw;
+  // lane j < n: the occurrence at sorted position base + j
+  int pj = 0, uj = 0, s0j = 0, s1j = 0;
+  int64_t kj = 0;
+  if (!EARLY) KG_GRID_DEP_WAIT();
+  if (lane < n) {
+    pj = perm[base + lane];
+    uj = sinv[base + lane];
+    s0j = seg[uj];
+    s1j = seg[uj + 1];
+    kj = uniq[uj];
+  }
+  const bool rep = lane < n && s1j - s0j > 1 && kj != skip_key;
+  const unsigned rep_mask = __ballot_sync(0xffffffffu, rep);
+  if (!rep_mask) return;
+  SA_T(1);
+  // piece starts: a segment head or the chunk's first position; piece ends
+  const unsigned start_mask = __ballot_sync(0xffffffffu, rep && (base + lane == s0j || lane == 0));
+  const unsigned cont_mask = rep_mask & ~start_mask;
+  const unsigned end_mask = rep_mask & ~(cont_mask >> 1);
+  // the p, m, v slices of the segments that finish in this piece (single-piece) to L2 now
+  if (apply && ((start_mask >> lane) & 1u)) {
+    const bool single = (s1j - 1) / kPiece == s0j / kPiece;
+    if (single) {
+      const int64_t off = (kj / world) * d4 + c0;
+      for (int k = 0; k < cw; k += 8) {           // 128-byte lines
+        prefetch_l2(E4 + off + k); prefetch_l2(M4 + off + k); prefetch_l2(V4 + off + k);
+      }
+    }
+  }
+  const uint32_t sb = (uint32_t)cw * 16u;
+  if (lane == 0) {
+    bar_init(bar);
+    bar_expect(bar, (uint32_t)__popc(rep_mask) * sb);
+  }
+  __syncwarp();
+  if (EARLY) KG_GRID_DEP_WAIT();
+  if (rep) bulk_g2s(sm + lane * sw, X4 + (int64_t)pj * d4 + c0, sb, bar);   // slot j = position j
   const bool upd = apply && !flags[0];
   const float lr1 = *lr_dev * bc[0], ibc2 = bc[1];
-  const int64_t rowoff = (uniq[u] / world) * d4;
-  const float4 *X4 = reinterpret_cast<const float4 *>(OG), *P4 = reinterpret_cast<const float4 *>(PS);
-  float4 *pe = reinterpret_cast<float4 *>(ent) + rowoff, *pm = reinterpret_cast<float4 *>(m) + rowoff,
-         *pv = reinterpret_cast<float4 *>(v) + rowoff;
-  // d <= 2048: at most 16 float4 per lane; issue the row's p, m, v loads before the arithmetic
-  constexpr int kMaxIt = 4;
-  for (int c0 = 0; c0 < d4; c0 += 32 * kMaxIt) {
-    float4 P[kMaxIt], Mm[kMaxIt], V[kMaxIt], Gq[kMaxIt];
-#pragma unroll
-    for (int it = 0; it < kMaxIt; ++it) {
-      const int c = c0 + lane + 32 * it;
-      if (c >= d4) continue;
-      Gq[it] = segment_sum(perm, X4, P4, s0, s1, d4, c);
-      if (upd) { P[it] = pe[c]; Mm[it] = pm[c]; V[it] = pv[c]; }
+  bar_wait0(bar);
+  SA_T(2);
+  // (1) pieces in position order: single-piece segments take their update now; the pieces
+  // of longer segments go to PS, and the item completing a segment's last piece keeps it
+  int pend_u[2] = {0, 0}, pend_s0[2] = {0, 0}, pend_s1[2] = {0, 0}, npend = 0;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  int jst = 0;
+  for (int j = 0; j < n; ++j) {
+    if (!((rep_mask >> j) & 1u)) continue;
+    const float4 xv = cv ? sm[j * sw + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+    if ((start_mask >> j) & 1u) { acc = xv; jst = j; }
+    else add4(acc, xv);
+    if (!((end_mask >> j) & 1u)) continue;
+    const int u = __shfl_sync(0xffffffffu, uj, jst), s0 = __shfl_sync(0xffffffffu, s0j, jst),
+              s1 = __shfl_sync(0xffffffffu, s1j, jst);
+    const int64_t key = __shfl_sync(0xffffffffu, kj, jst);
+    const int npieces = (s1 - 1) / kPiece - s0 / kPiece + 1;
+    if (npieces > 1) {
+      if (cv) __stcg(P4 + (int64_t)(base + jst) * d4 + col, acc);
+      __threadfence();
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) last = atomicAdd(cnt + (int64_t)u * kSlices + q, 1) == npieces - 1;
+      if (__shfl_sync(0xffffffffu, last, 0)) {   // at most 2 per chunk: its first and last run
+        if (npend == 0) { pend_u[0] = u; pend_s0[0] = s0; pend_s1[0] = s1; }
+        else { pend_u[1] = u; pend_s0[1] = s0; pend_s1[1] = s1; }
+        ++npend;
+      }
+      continue;
     }
+    if (!cv) continue;
+    if (GO4) GO4[(int64_t)u * d4 + col] = acc;
+    if (!upd) continue;
+    const int64_t off = (key / world) * d4 + col;
+    float4 P = E4[off], Mm = M4[off], V = V4[off];
+    adam4(P, Mm, V, acc, lr1, hy, ibc2);
+    E4[off] = P; M4[off] = Mm; V4[off] = V;
+  }
+  // (2) the segments completed here: all pieces' sums (kB in flight), added in ascending
+  // order, then Adam on the slice
+  SA_T(3);
+  if (!npend) return;
+  __threadfence();
+  for (int pi = 0; pi < npend; ++pi) {
+    const int u = pi ? pend_u[1] : pend_u[0], s0 = pi ? pend_s0[1] : pend_s0[0], s1 = pi ? pend_s1[1] : pend_s1[0];
+    if (lane == 0) cnt[(int64_t)u * kSlices + q] = 0;       // ready for the next step
+    if (!cv) continue;
+    const int64_t off = (uniq[u] / world) * d4 + col;
+    float4 P, Mm, V;
+    if (upd) { P = E4[off]; Mm = M4[off]; V = V4[off]; }  // the row's slice in flight first
+    float4 G = __ldcg(P4 + (int64_t)s0 * d4 + col);
+    constexpr int kB = 8;
+    for (int sp = (s0 / kPiece + 1) * kPiece; sp < s1; sp += kB * kPiece) {
+      const int nk = min(kB, (s1 - sp + kPiece - 1) / kPiece);
+      float4 y[kB];
 #pragma unroll
-    for (int it = 0; it < kMaxIt; ++it) {
-      const int c = c0 + lane + 32 * it;
-      if (c >= d4) continue;
-      if (grad_out) reinterpret_cast<float4 *>(grad_out)[(int64_t)u * d4 + c] = Gq[it];
-      if (!upd) continue;
-      adam4(P[it], Mm[it], V[it], Gq[it], lr1, hy, ibc2);
-      pe[c] = P[it]; pm[c] = Mm[it]; pv[c] = V[it];
+      for (int k = 0; k < kB; ++k)
+        y[k] = k < nk ? __ldcg(P4 + (int64_t)(sp + k * kPiece) * d4 + col) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < kB; ++k)
+        if (k < nk) add4(G, y[k]);
     }
+    if (GO4) GO4[(int64_t)u * d4 + col] = G;
+    if (!upd) continue;
+    adam4(P, Mm, V, G, lr1, hy, ibc2);
+    E4[off] = P; M4[off] = Mm; V4[off] = V;
   }
 }
 
-void launch_sparse_adam(const int64_t *uniq, const int32_t *seg, const int32_t *perm, const int32_t *inv,
-                        const int32_t *U_dev, int L, const float *OG, float *PS, int d, int world, float *ent,
-                        float *m, float *v, float *grad_out, const float *lr, double beta1, double beta2, double eps,
-                        const float *bc, const int *flags, int apply, cudaStream_t st, int64_t skip_key) {
+// cnt: [L][kSlices] int32, zero before the first call (the kernel leaves it zero).
+void launch_sparse_adam(const int64_t *uniq, const int32_t *seg, const int32_t *perm, const int32_t *sinv,
+                        const int32_t *hrow, const int32_t *U_dev, int L, const float *OG, float *PS, int32_t *cnt,
+                        int d, int world, float *ent, float *m, float *v, float *grad_out, const float *lr,
+                        double beta1, double beta2, double eps, const float *bc, const int *flags, int apply,
+                        cudaStream_t st, int64_t skip_key, int early) {
   if (L <= 0) return;
-  { seg_piece_kernel<<<(L + kPiece - 1) / kPiece, 128, 0, st>>>(perm, inv, seg, L, OG, d / 4, PS); ++g_launches; }
-  { sparse_adam_kernel<<<(L + 7) / 8, 256, 0, st>>>(uniq, seg, perm, U_dev, OG, PS, d, world, ent, m, v,
-                                                              grad_out, lr, hyper(beta1, beta2, eps), bc, flags,
-                                                              apply, skip_key); ++g_launches; }
+  const AdamHyper hy = hyper(beta1, beta2, eps);
+  const int d4 = d / 4;
+  const int ns = (d4 + 31) / 32, sw = (d4 + ns - 1) / ns;        // slices of <= 32 float4
+  const int wbytes = (int)((std::max(4 * d4, kPiece * sw) * 16 + 127) / 128 * 128);
+  const int items = (L + kPiece - 1) / kPiece * ns + L;
+  const int smem = 4 * wbytes;
+  auto kern = early ? sparse_adam_fused_kernel<true> : sparse_adam_fused_kernel<false>;
+  static int configured[2] = {0, 0};   // the largest dynamic smem opted into, per instantiation
+  int &cfg = configured[early ? 1 : 0];
+  if (smem > 48 * 1024 && smem > cfg) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cfg = smem;
+  }
+  kern<<<(items + 3) / 4, 128, smem, st>>>(uniq, seg, perm, sinv, hrow, U_dev, L, OG, PS, cnt, d, world, ns, sw,
+                                           wbytes, ent, m, v, grad_out, lr, hy, bc, flags, apply, skip_key);
+  ++g_launches;
 }
 
 // Phase 2 for the relation rows: RGU[u] = sum of the occurrence rows of relation u.

@@ -22,7 +22,8 @@ constexpr int kDedupThreads = 1024;
 template <int ITEMS>
 __global__ void __launch_bounds__(kDedupThreads) dedup_kernel(const int64_t *ids64, const int32_t *ids32, int L,
                                                               int end_bit, int64_t *uniq, int32_t *inv,
-                                                              int32_t *perm, int32_t *seg, int32_t *U_out) {
+                                                              int32_t *perm, int32_t *seg, int32_t *U_out,
+                                                              int32_t *sinv, int32_t *hrow) {
   KG_GRID_DEP_WAIT();
   using Sort = cub::BlockRadixSort<uint32_t, kDedupThreads, ITEMS, uint32_t>;
   using Disc = cub::BlockDiscontinuity<uint32_t, kDedupThreads>;
@@ -49,8 +50,8 @@ __global__ void __launch_bounds__(kDedupThreads) dedup_kernel(const int64_t *ids
   Sort(temp.sort).Sort(keys, vals, 0, end_bit);
   __syncthreads();
 
-  int head[ITEMS];
-  Disc(temp.disc).FlagHeads(head, keys, cub::Inequality());
+  int head[ITEMS], tail[ITEMS];
+  Disc(temp.disc).FlagHeadsAndTails(head, tail, keys, cub::Inequality());
   __syncthreads();
 #pragma unroll
   for (int it = 0; it < ITEMS; ++it)
@@ -64,9 +65,13 @@ __global__ void __launch_bounds__(kDedupThreads) dedup_kernel(const int64_t *ids
     const int u = excl[it] + head[it] - 1;
     perm[s] = (int32_t)vals[it];
     inv[vals[it]] = u;
+    if (sinv) sinv[s] = u;   // sorted position -> distinct index (= inv[perm[s]])
     if (head[it]) {
       uniq[u] = (int64_t)keys[it];
       seg[u] = s;
+      // the single occurrence of a segment of length 1, else -1 (the next position is
+      // padding, p >= L, or another key)
+      if (hrow) hrow[u] = (tail[it] || s + 1 >= L) ? (int32_t)vals[it] : -1;
     }
   }
   if (threadIdx.x == 0) {
@@ -79,7 +84,8 @@ int dedup_capacity() { return kDedupThreads * 32; }
 
 template <int ITEMS>
 static void run_dedup(const int64_t *ids64, const int32_t *ids32, int L, int end_bit, int64_t *uniq, int32_t *inv,
-                      int32_t *perm, int32_t *seg, int32_t *U_out, cudaStream_t st) {
+                      int32_t *perm, int32_t *seg, int32_t *U_out, int32_t *sinv, int32_t *hrow,
+                      cudaStream_t st) {
   using Sort = cub::BlockRadixSort<uint32_t, kDedupThreads, ITEMS, uint32_t>;
   using Disc = cub::BlockDiscontinuity<uint32_t, kDedupThreads>;
   using Scan = cub::BlockScan<int, kDedupThreads>;
@@ -91,16 +97,16 @@ static void run_dedup(const int64_t *ids64, const int32_t *ids32, int L, int end
   static const bool configured =
       cudaFuncSetAttribute(dedup_kernel<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess;
   (void)configured;
-  { dedup_kernel<ITEMS><<<1, kDedupThreads, bytes, st>>>(ids64, ids32, L, end_bit, uniq, inv, perm, seg, U_out); ++g_launches; }
+  { dedup_kernel<ITEMS><<<1, kDedupThreads, bytes, st>>>(ids64, ids32, L, end_bit, uniq, inv, perm, seg, U_out, sinv, hrow); ++g_launches; }
 }
 
 void launch_dedup(const int64_t *ids64, const int32_t *ids32, int L, int end_bit, int64_t *uniq, int32_t *inv,
-                  int32_t *perm, int32_t *seg, int32_t *U_out, cudaStream_t st) {
+                  int32_t *perm, int32_t *seg, int32_t *U_out, cudaStream_t st, int32_t *sinv, int32_t *hrow) {
   if (end_bit < 1) end_bit = 1;
-  if (L <= kDedupThreads * 4) run_dedup<4>(ids64, ids32, L, end_bit, uniq, inv, perm, seg, U_out, st);
-  else if (L <= kDedupThreads * 8) run_dedup<8>(ids64, ids32, L, end_bit, uniq, inv, perm, seg, U_out, st);
-  else if (L <= kDedupThreads * 16) run_dedup<16>(ids64, ids32, L, end_bit, uniq, inv, perm, seg, U_out, st);
-  else run_dedup<32>(ids64, ids32, L, end_bit, uniq, inv, perm, seg, U_out, st);
+  if (L <= kDedupThreads * 4) run_dedup<4>(ids64, ids32, L, end_bit, uniq, inv, perm, seg, U_out, sinv, hrow, st);
+  else if (L <= kDedupThreads * 8) run_dedup<8>(ids64, ids32, L, end_bit, uniq, inv, perm, seg, U_out, sinv, hrow, st);
+  else if (L <= kDedupThreads * 16) run_dedup<16>(ids64, ids32, L, end_bit, uniq, inv, perm, seg, U_out, sinv, hrow, st);
+  else run_dedup<32>(ids64, ids32, L, end_bit, uniq, inv, perm, seg, U_out, sinv, hrow, st);
 }
 
 }  // namespace kg

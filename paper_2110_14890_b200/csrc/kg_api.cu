@@ -492,6 +492,8 @@ struct kg_handle {
   int32_t *rel_seg_map = nullptr;
   int64_t *rel_stamp = nullptr;
   float *OG = nullptr, *RG = nullptr, *RGU = nullptr, *Gc = nullptr, *gdense = nullptr, *PS = nullptr, *PSr = nullptr;
+  int32_t *pcnt = nullptr, *ocnt = nullptr, *sinv = nullptr, *osinv = nullptr, *hrow = nullptr,
+          *ohrow = nullptr;
   float *Q = nullptr, *dQ = nullptr, *C = nullptr, *Dmin = nullptr, *Dpos = nullptr, *loss_part = nullptr,
         *loss_pos = nullptr;
   float *F = nullptr, *Cv = nullptr, *QP = nullptr, *Cq = nullptr;
@@ -672,6 +674,8 @@ void carve(kg_handle *h, Arena &A) {
   h->uniq = A.take<int64_t>(h->Lx);
   h->inv = A.take<int32_t>(h->Lx);
   h->perm = A.take<int32_t>(h->Lx);
+  h->sinv = A.take<int32_t>(h->Lx);
+  h->hrow = A.take<int32_t>(h->Lx);
   h->seg = A.take<int32_t>(h->Lx + 1);
   {
     // the step's scalar results, contiguous so that one D2H copies them (layout = HostOut)
@@ -696,6 +700,7 @@ void carve(kg_handle *h, Arena &A) {
   h->OG = A.take<float>((int64_t)h->Lx * d);
   h->Gc = A.take<float>((int64_t)h->Lx * d);
   h->PS = A.take<float>((int64_t)h->Lx * d);
+  h->pcnt = A.take<int32_t>((int64_t)h->Lx * 16);   // piece arrival counters of the fused sparse Adam (self-resetting)
   h->PSr = A.take<float>((int64_t)h->Lrx * h->dr);
   h->gfull = A.take<float>(h->dense_size);
   h->gdense = h->gfull + h->w_off;
@@ -777,6 +782,8 @@ void carve(kg_handle *h, Arena &A) {
     h->ouniq = A.take<int64_t>(GL);
     h->oinv = A.take<int32_t>(GL);
     h->operm = A.take<int32_t>(GL);
+    h->osinv = A.take<int32_t>(GL);
+    h->ohrow = A.take<int32_t>(GL);
     h->oseg = A.take<int32_t>(GL + 1);
     h->oU = A.take<int32_t>(1);
     h->Xin = A.take<float>(SL * d);
@@ -784,6 +791,7 @@ void carve(kg_handle *h, Arena &A) {
     h->Gsend = A.take<float>(SL * d);
     h->Grecv = A.take<float>(GL * d);
     h->PSo = A.take<float>(GL * d);
+    h->ocnt = A.take<int32_t>(GL * 16);
     h->pp = reinterpret_cast<PeerPtrs *>(A.take<char>(sizeof(PeerPtrs)));
     h->p2p_flags = A.take<unsigned long long>(kMaxWorld + 1);
     h->p2p_epoch = h->p2p_flags ? h->p2p_flags + kMaxWorld : nullptr;
@@ -1589,7 +1597,7 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   launch_rel_occ(h->b_rels, M, nr, sl, p.nproj, h->R, h->rocc, h->flags + 1, st);
   CK(cudaEventRecord(h->ev_fork, st));
   CK(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
-  launch_dedup(h->ids, nullptr, L, h->ent_bits, h->uniq, h->inv, h->perm, h->seg, h->Udev, h->st2);
+  launch_dedup(h->ids, nullptr, L, h->ent_bits, h->uniq, h->inv, h->perm, h->seg, h->Udev, h->st2, h->sinv, h->hrow);
   launch_dedup(nullptr, h->rocc, Lr, h->rel_bits, h->runiq, h->rinv, h->rperm, h->rseg, h->rU, h->st2);
   CK(cudaEventRecord(h->ev_rel, h->st2));
 
@@ -1692,9 +1700,9 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
     CK(cudaEventRecord(h->ev_join, s2));
   }
   if (h->apply || h->keep_grads)
-    launch_sparse_adam(h->uniq, h->seg, h->perm, h->inv, h->Udev, L, h->OG, h->PS, d, h->world, h->t.ent, h->t.ent_m,
+    launch_sparse_adam(h->uniq, h->seg, h->perm, h->sinv, h->hrow, h->Udev, L, h->OG, h->PS, h->pcnt, d, h->world, h->t.ent, h->t.ent_m,
                        h->t.ent_v, h->keep_grads ? h->Gc : nullptr, h->lr_dev, h->cfg.beta1, h->cfg.beta2,
-                       h->cfg.eps, h->bc, h->flags, h->apply, st);
+                       h->cfg.eps, h->bc, h->flags, h->apply, st, -1, /*early=*/1);
   mark(h, 6);
   CK(cudaStreamWaitEvent(st, h->ev_join, 0));
   mark(h, 7);
@@ -1728,7 +1736,7 @@ kg_status step_dist(kg_handle *h, StepBufs &S) {
       if (p.n[ni].type == 0) sl.s[u++] = p.n[ni].rel;
   }
   launch_rel_occ(h->b_rels, M, nr, sl, p.nproj, h->R, h->rocc, h->flags + 1, st);
-  launch_dedup(h->ids, nullptr, L, h->ent_bits, h->uniq, h->inv, h->perm, h->seg, h->Udev, st);
+  launch_dedup(h->ids, nullptr, L, h->ent_bits, h->uniq, h->inv, h->perm, h->seg, h->Udev, st, h->sinv, h->hrow);
   launch_dedup(nullptr, h->rocc, Lr, h->rel_bits, h->runiq, h->rinv, h->rperm, h->rseg, h->rU, st);
   // a3: route the distinct ids to their owners (owner = id % G).  Buckets: every rank sends
   // `cap` slots to every owner (empty slots = -1), so no size is read on the host and the
@@ -1833,7 +1841,7 @@ kg_status step_dist(kg_handle *h, StepBufs &S) {
                         h->cfg.beta2, h->cfg.eps, h->bc, h->flags, h->st2);
   }
   // a12: merged row gradients of this rank (distinct-id order) -> send order -> owners
-  launch_sparse_adam(h->uniq, h->seg, h->perm, h->inv, h->Udev, L, h->OG, h->PS, d, 1, h->t.ent, h->t.ent_m,
+  launch_sparse_adam(h->uniq, h->seg, h->perm, h->sinv, h->hrow, h->Udev, L, h->OG, h->PS, h->pcnt, d, 1, h->t.ent, h->t.ent_m,
                      h->t.ent_v, h->Gc, h->lr_dev, h->cfg.beta1, h->cfg.beta2, h->cfg.eps, h->bc, h->flags,
                      /*apply=*/0, st);
   launch_reorder_rows(h->Gc, h->send_pos, h->Udev, L, d, h->Gsend, st);
@@ -1853,9 +1861,10 @@ kg_status step_dist(kg_handle *h, StepBufs &S) {
   // a13 at the owner: merge the contributions of all ranks (fixed order) + sparse Adam on local rows
   // empty bucket slots carry the key `shard` (one past the last local row), skipped by the update
   launch_local_rows(h->recv_ids, Rtot, G, h->recv_keys, st, h->shard);
-  launch_dedup(h->recv_keys, nullptr, Rtot, bits_for(h->shard + 1), h->ouniq, h->oinv, h->operm, h->oseg, h->oU, st);
+  launch_dedup(h->recv_keys, nullptr, Rtot, bits_for(h->shard + 1), h->ouniq, h->oinv, h->operm, h->oseg, h->oU, st,
+               h->osinv, h->ohrow);
   if (h->apply)
-    launch_sparse_adam(h->ouniq, h->oseg, h->operm, h->oinv, h->oU, Rtot, h->Grecv, h->PSo, d, 1, h->t.ent,
+    launch_sparse_adam(h->ouniq, h->oseg, h->operm, h->osinv, h->ohrow, h->oU, Rtot, h->Grecv, h->PSo, h->ocnt, d, 1, h->t.ent,
                        h->t.ent_m, h->t.ent_v, nullptr, h->lr_dev, h->cfg.beta1, h->cfg.beta2, h->cfg.eps, h->bc,
                        h->flags, 1, st, /*skip_key=*/h->shard);
   mark(h, 6);

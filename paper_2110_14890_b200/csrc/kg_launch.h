@@ -62,16 +62,19 @@ void launch_loss_finalize(const float *loss_pos, const float *loss_part, int M, 
 // positions), seg[U+1] (segment starts into perm), *U_out.
 int dedup_capacity();
 void launch_dedup(const int64_t *ids64, const int32_t *ids32, int L, int end_bit, int64_t *uniq, int32_t *inv,
-                  int32_t *perm, int32_t *seg, int32_t *U_out, cudaStream_t st);
+                  int32_t *perm, int32_t *seg, int32_t *U_out, cudaStream_t st, int32_t *sinv = nullptr,
+                  int32_t *hrow = nullptr);
 
 // k_adam.cu
 void launch_init_rows(float *p, int64_t rows, int d, int64_t row0, int64_t row_step, uint64_t seed, uint64_t stream,
                       float lo, float hi, cudaStream_t st);
 void launch_init_flat(float *p, int64_t n, uint64_t seed, uint64_t stream, float lo, float hi, cudaStream_t st);
-void launch_sparse_adam(const int64_t *uniq, const int32_t *seg, const int32_t *perm, const int32_t *inv,
-                        const int32_t *U_dev, int L, const float *OG, float *PS, int d, int world, float *ent,
-                        float *m, float *v, float *grad_out, const float *lr, double beta1, double beta2, double eps,
-                        const float *bc, const int *flags, int apply, cudaStream_t st, int64_t skip_key = -1);
+void launch_sparse_adam(const int64_t *uniq, const int32_t *seg, const int32_t *perm, const int32_t *sinv,
+                        const int32_t *hrow,
+                        const int32_t *U_dev, int L, const float *OG, float *PS, int32_t *cnt, int d, int world,
+                        float *ent, float *m, float *v, float *grad_out, const float *lr, double beta1, double beta2,
+                        double eps, const float *bc, const int *flags, int apply, cudaStream_t st,
+                        int64_t skip_key = -1, int early = 0);
 void launch_rel_reduce(const int32_t *seg, const int32_t *perm, const int32_t *inv, const int32_t *U_dev, int Lr,
                        const float *RG, float *PS, int dr, float *RGU, cudaStream_t st);
 void launch_rel_stamp(const int64_t *uniq_rel, const int32_t *U_dev, int Lmax, int32_t *rel_seg, int64_t *rel_stamp,
