@@ -367,7 +367,7 @@ def run_ours(args, world, rank, local):
         "config": workload_config(args, cfg, w, world),
         "e2e": e2e, "e2e_sampler": e2e_sampler, "roofline": roof,
         "gpu_launches": int(sum(kernels_of.get(st, info.kernels) for st in step_structs)),
-        "kernels_per_step": kernels_of, "cublas_gemms_per_step": gemms_of, "ms_per_step_by_structure": per_struct_ms,
+        "kernels_per_step": kernels_of, "tc_gemms_per_step": gemms_of, "ms_per_step_by_structure": per_struct_ms,
         "clocks": clk,
         "wall_s": round(wall, 3), "loss_last": info.loss,
     }
@@ -431,29 +431,45 @@ def sampler_e2e(args, gm, cfg, w, M, K, world, rank):
 
 # ------------------------------------------------------------------ oracle timing
 def oracle_time(cfg, batches, q_per_step, n_steps, seed):
-    """Time the CPU oracle, as it stands, on the first q_per_step queries of each batch (full pool)."""
+    """Time the CPU oracle, as it stands, on the first q_per_step queries of each batch (full pool).
+    Returns (queries/s over all steps, threads used, total seconds, per-step queries/s)."""
     import torch
     import oracle
     table = oracle.SparseTable(cfg, seed)
     done = 0
+    rates = []
     t0 = time.perf_counter()
     for s in range(n_steps):
         b = batches[s % len(batches)]
         q = q_per_step
         sub = dict(b, anchors=b["anchors"][:q], relations=b["relations"][:q], answers=b["answers"][:q],
                    mask=b["mask"][:q], M=q)
+        ts = time.perf_counter()
         oracle.oracle_step(cfg, table, [sub], 1e-4)
+        rates.append(q / (time.perf_counter() - ts))
         done += q
     dt = time.perf_counter() - t0
-    return done / dt, torch.get_num_threads(), dt
+    return done / dt, torch.get_num_threads(), dt, rates
 
 
 def cpu_baseline(cfg, batches, seed, budget_s=20.0):
+    """The oracle on all host threads (median over steps) and on one core."""
+    import torch
     # ~2 s per step of 16 queries on the 8-core dev box; sized to stay within ~budget_s
-    rate, cores, dt = oracle_time(cfg, batches, 16, 1, seed)
-    n = max(1, min(9, int(budget_s / max(dt, 1e-3))))
-    rate, cores, dt = oracle_time(cfg, batches, 16, n, seed)
+    rate, cores, dt, _ = oracle_time(cfg, batches, 16, 1, seed)
+    n = max(1, min(9, int(0.6 * budget_s / max(dt, 1e-3))))
+    rate, cores, dt, rates = oracle_time(cfg, batches, 16, n, seed)
+    nt = torch.get_num_threads()
+    torch.set_num_threads(1)
+    try:
+        r1, _, dt1, rates1 = oracle_time(cfg, batches, 4, max(1, min(3, int(0.4 * budget_s / max(4 * dt / n, 1e-3)))),
+                                         seed)
+    finally:
+        torch.set_num_threads(nt)
     return {"value": round(rate, 3), "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+            "median_step_value": round(float(np.median(rates)), 3),
+            "one_core": {"value": round(r1, 3), "median_step_value": round(float(np.median(rates1)), 3),
+                         "cores": 1, "sample": f"{len(rates1)} steps x 4 queries; {dt1:.1f} s"},
             "sample": f"{n} steps x 16 of the 512 queries (full K pool, full theta_D Adam), structures "
                       f"round-robin, fp64 torch CPU; {dt:.1f} s"}
 
@@ -471,7 +487,7 @@ def run_reference(args, world, rank):
     q = 4
     for s in range(min(args.warmup, 1)):
         oracle_time(cfg, batches, q, 1, args.seed)
-    rate, cores, dt = oracle_time(cfg, batches, q, args.steps if args.steps <= 60 else 60, args.seed)
+    rate, cores, dt, _ = oracle_time(cfg, batches, q, args.steps if args.steps <= 60 else 60, args.seed)
     steps_run = args.steps if args.steps <= 60 else 60
     return {"impl": "reference", "metric": METRIC, "value": round(rate, 3), "unit": UNIT, "n_gpus": 1,
             "steps": steps_run, "warmup": args.warmup, "ms_per_step": round(dt / steps_run * 1e3, 3),

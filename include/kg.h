@@ -133,7 +133,7 @@ typedef struct {
   int32_t n_touched;     /* distinct entity ids touched by this rank's batch (A16) */
   int64_t step;          /* Adam step counter t after the step */
   int32_t kernels;       /* kernels of this library enqueued by the step */
-  int32_t gemms;         /* cuBLAS SGEMM calls enqueued by the step (dense MLP layers) */
+  int32_t gemms;         /* tcgen05 tensor-core GEMM launches enqueued by the step (MLP layers, dot scores) */
   float stage_ms[10];    /* device time per stage when stage timing is on (kg_set_apply bit 2), else 0:
                             0 ingest + dedup, 1 DAG forward, 2 scoring forward + Eq. 1, 3 scoring backward,
                             4 DAG backward, 5 sparse update (segment reduce + sparse Adam), 6 what the dense

@@ -86,7 +86,7 @@ def build(verbose: bool = False, force: bool = False, out: str = None) -> str:
             raise RuntimeError(f"nvcc failed on {s}")
         if verbose and out:
             sys.stderr.write(out.decode())
-    cmd = [NVCC, *ARCH, "-shared", "-o", OUT_ + ".tmp", *objs, "-lcublas", "-ldl", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", OUT_ + ".tmp", *objs, "-ldl", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
     subprocess.run(cmd, check=True)
     os.replace(OUT_ + ".tmp", OUT_)
     return OUT_

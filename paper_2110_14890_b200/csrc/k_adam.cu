@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(128, 8) sparse_adam_fused_kernel(const int64_t
     }
     if (EARLY) KG_GRID_DEP_WAIT();
     if (lane == 0) bulk_g2s(sm + 3 * d4, X4 + (int64_t)r0 * d4, rb, bar);
-    const bool upd = apply && !flags[0];          // the step's go / no-go, after the wait
+    const bool upd = apply && !(flags[0] | flags[1]);          // the step's go / no-go, after the wait
     const float lr1 = *lr_dev * bc[0], ibc2 = bc[1];
     __syncwarp();
     bar_wait0(bar);
@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(128, 8) sparse_adam_fused_kernel(const int64_t
   __syncwarp();
   if (EARLY) KG_GRID_DEP_WAIT();
   if (rep) bulk_g2s(sm + lane * sw, X4 + (int64_t)pj * d4 + c0, sb, bar);   // slot j = position j
-  const bool upd = apply && !flags[0];
+  const bool upd = apply && !(flags[0] | flags[1]);
   const float lr1 = *lr_dev * bc[0], ibc2 = bc[1];
   bar_wait0(bar);
   SA_T(2);
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(256) dense_adam_rel_kernel(float4 *p, float4 *
                                                              AdamHyper hy, const float *bc, const int *flags,
                                                              int untouched_only) {
   KG_GRID_DEP_WAIT();
-  if (flags[0]) return;
+  if (flags[0] | flags[1]) return;   // flags[1]: a failure found after the loss check (p2p barrier)
   const float lr1 = *lr_dev * bc[0], ibc2 = bc[1];
   const int64_t stamp = *stamp_dev;
   const int w4 = (int)fw4.d;
@@ -525,7 +525,7 @@ __global__ void __launch_bounds__(256) dense_adam_rel_touched_kernel(float4 *p, 
                                                                      const float *lr_dev, AdamHyper hy,
                                                                      const float *bc, const int *flags) {
   KG_GRID_DEP_WAIT();
-  if (flags[0]) return;
+  if (flags[0] | flags[1]) return;   // flags[1]: a failure found after the loss check (p2p barrier)
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int per = nseg * w4;
   const int u = (int)(e / per);
@@ -545,7 +545,7 @@ __global__ void __launch_bounds__(256) dense_adam_kernel(float4 *p, float4 *m, f
                                                          const float *lr_dev, AdamHyper hy, const float *bc,
                                                          const int *flags) {
   KG_GRID_DEP_WAIT();
-  if (flags[0]) return;
+  if (flags[0] | flags[1]) return;   // flags[1]: a failure found after the loss check (p2p barrier)
   const float lr1 = *lr_dev * bc[0], ibc2 = bc[1];
   const int base = blockIdx.x * (256 * kE) + threadIdx.x;
   float4 P[kE], Mm[kE], V[kE], G[kE];

@@ -1063,7 +1063,7 @@ static void launch_bwd(ScoreArgs a, cudaStream_t st, cudaStream_t st2) {
   const int kt = (a.U + 31) / 32, jt = (a.K + JB - 1) / JB;
   a.JS = jt;                                   // dQ partials: one per j-block
   // Q2B unions: one pass per query over both disjunct rows (pair_bwd_union_box_kernel)
-  const bool union_box = std::is_same<Mdl, MBox>::value && a.NQ == 2 * a.M && !std::getenv("KG_UNION_ROWS");
+  const bool union_box = std::is_same<Mdl, MBox>::value && a.NQ == 2 * a.M;
   if (union_box) {
     const int chunks = (a.M + kICU - 1) / kICU;
     int is = (3 * 148) / (kt * jt);   // one wave of the 3 resident CTAs per SM (ncu: 5 splits were 1.17 waves)

@@ -4,7 +4,6 @@
 // App. A.3), the device workspace, pinned staging, cuBLAS, and the order in
 // which the sm_100a kernels of k_*.cu are enqueued for one training step
 // (§4.1, §4.2, §4.3).
-#include <cublas_v2.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
@@ -24,6 +23,7 @@
 #include <vector>
 
 #include "../../include/kg.h"
+#include <nvtx3/nvToolsExt.h>
 #include "kg_launch.h"
 
 using namespace kg;
@@ -475,7 +475,6 @@ struct kg_handle {
   int64_t dense_size = 0, w_off = 0;
   kg_tables t{};
   cudaStream_t st = nullptr;
-  cublasHandle_t blas = nullptr;
   int device = 0;
 
   // workspace
@@ -514,7 +513,6 @@ struct kg_handle {
   int64_t gsP_cap = 0;
   float *Dpart = nullptr, *partQ = nullptr, *partV = nullptr, *Cpart = nullptr, *Csum = nullptr;
   float *Eg = nullptr;     // dot-product scorers: the pool's rows, contiguous (GEMM operand)
-  bool gemm_scores = true; // dot-product scorers on the tensor-core GEMM; KG_GEMM_SCORES=0: pair kernels
   bool score_bf16 = false;  // kg_config.score_precision == KG_SCORE_BF16
   bool gemm_lowp = false;   // the GEMMs being enqueued take bf16-rounded operands (scoring, bf16 mode)
   int64_t cap_D = 0, cap_Q = 0, cap_V = 0;
@@ -530,10 +528,7 @@ struct kg_handle {
   };
   std::vector<GraphEntry> graphs;
   bool use_graphs = true;
-  bool gemm_cublas = false, gemm_drain = false, side = false, use_pdl = true;
-  cublasHandle_t blas2 = nullptr;
-  void *blas_ws2 = nullptr;
-  void *blas_ws = nullptr;
+  bool gemm_drain = true, side = false, use_pdl = true;
   // row-sharded exchange (world > 1, k_dist.cu)
   ncclComm_t comm = nullptr;
   ncclComm_t comm2 = nullptr;  // world > 1: the dense all-reduce's own communicator (on st2, overlapped)
@@ -600,13 +595,6 @@ kg_status fail(kg_handle *h, kg_status s, const std::string &msg) {
     ncclResult_t r_ = (call);                                                                    \
     if (r_ != ncclSuccess) return fail(h, KG_ENCCL, std::string(#call) + ": " + nccl().GetErrorString(r_)); \
   } while (0)
-#define CKB(call)                                                                              \
-  do {                                                                                         \
-    cublasStatus_t e_ = (call);                                                                \
-    if (e_ != CUBLAS_STATUS_SUCCESS)                                                           \
-      return fail(h, KG_ECUDA, std::string(#call) + ": cublas status " + std::to_string(e_));  \
-  } while (0)
-
 bool single_hop(int k) { return k == KG_TRANSE || k == KG_ROTATE || k == KG_DISTMULT || k == KG_COMPLEX; }
 int base_kind(int k) {
   return k == KG_ROTATE_M ? KG_ROTATE : (k == KG_DISTMULT_M ? KG_DISTMULT : (k == KG_COMPLEX_M ? KG_COMPLEX : k));
@@ -733,8 +721,6 @@ void carve(kg_handle *h, Arena &A) {
   }
   h->lr_dev = A.take<float>(4);
   h->stamp_dev = A.take<int64_t>(1);
-  h->blas_ws = A.take<char>(32 << 20);
-  h->blas_ws2 = A.take<char>(32 << 20);
   h->bc = A.take<float>(2);
   for (int i = 0; i < 6; ++i) {
     h->nval[i] = A.take<float>((int64_t)Mx * dq);
@@ -799,26 +785,21 @@ void carve(kg_handle *h, Arena &A) {
 }
 
 // Row-major GEMM: C[m x n] = op(A) op(B) + beta C, op(A) is [m x k]; tb: B given as [n x k].
-// The tcgen05 3xTF32 kernel (k_gemm.cu; drained accumulation for BetaE) or cuBLAS SGEMM; see kg_create.
+// Every contraction of the DAG runs on the tcgen05 3xTF32 kernel (k_gemm.cu; drained
+// accumulation, see kg_create); the side stream has its own split-K scratch.
 kg_status gemm(kg_handle *h, bool ta, bool tb, int m, int n, int k, const float *A, int lda, const float *B, int ldb,
                float beta, float *C, int ldc, const float *bias = nullptr, int relu = 0, float alpha = 1.f) {
   if (m <= 0 || n <= 0) return KG_OK;
-  // every contraction of the DAG goes to the tcgen05 kernel (measured faster than cuBLAS SGEMM
-  // from the d x d DeepSet / attention layers up to the BetaE MLP); the side stream has its
-  // own split-K scratch
-  if (!h->gemm_cublas) {
-    // the tensor-core kernel reads either operand layout directly ([k][m] / [k][n] = MN-major)
-    GemmArgs g;
-    g.A = A; g.B = B; g.C = C; g.M = m; g.N = n; g.K = k; g.lda = lda; g.ldb = ldb; g.ldc = ldc; g.beta = beta;
-    g.bias = bias; g.relu = relu; g.a_mn = ta; g.b_mn = !tb; g.drain = h->gemm_drain && !h->gemm_lowp;
-    g.lowp = h->gemm_lowp;
-    g.alpha = alpha;
-    if (k > 0 && launch_gemm_tc(g, h->side ? h->gsP2 : h->gsP, h->gsP_cap, h->st)) return KG_OK;
-  }
+  // the tensor-core kernel reads either operand layout directly ([k][m] / [k][n] = MN-major)
+  GemmArgs g;
+  g.A = A; g.B = B; g.C = C; g.M = m; g.N = n; g.K = k; g.lda = lda; g.ldb = ldb; g.ldc = ldc; g.beta = beta;
+  g.bias = bias; g.relu = relu; g.a_mn = ta; g.b_mn = !tb; g.drain = h->gemm_drain && !h->gemm_lowp;
+  g.lowp = h->gemm_lowp;
+  g.alpha = alpha;
+  if (k <= 0 || !launch_gemm_tc(g, h->side ? h->gsP2 : h->gsP, h->gsP_cap, h->st))
+    return fail(h, KG_EUNSUPPORTED, "tensor-core GEMM: operands must be 16-byte aligned with ld % 4 == 0 and K > 0 "
+                                    "(and cuTensorMapEncodeTiled available)");
   h->gemm_count++;
-  CKB(cublasSgemm(h->blas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, n, m, k, &alpha, B, ldb, A,
-                  lda, &beta, C, ldc));
-  if (bias || relu) launch_bias_act(C, bias, m, n, relu, h->st);   // (bias required when relu; ldc == n here)
   return KG_OK;
 }
 // Run the following GEMMs / kernels on another stream (restored on scope exit).
@@ -827,16 +808,12 @@ kg_status gemm(kg_handle *h, bool ta, bool tb, int m, int n, int k, const float 
 struct OnStream {
   kg_handle *h;
   cudaStream_t prev;
-  cublasHandle_t prev_blas;
-  OnStream(kg_handle *hh, cudaStream_t s) : h(hh), prev(hh->st), prev_blas(hh->blas) {
+  OnStream(kg_handle *hh, cudaStream_t s) : h(hh), prev(hh->st) {
     h->st = s;
-    h->blas = h->blas2;
-    cublasSetStream(h->blas, s);
     h->side = true;
   }
   ~OnStream() {
     h->st = prev;
-    h->blas = prev_blas;
     h->side = false;
   }
 };
@@ -1384,7 +1361,6 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
       cudaEventCreateWithFlags(&h->res_ev[1], cudaEventDisableTiming) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
   for (int i = 0; i < 12; ++i)
     if (cudaEventCreate(&h->sev[i]) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
-  if (cublasCreate(&h->blas) != CUBLAS_STATUS_SUCCESS) { kg_destroy(h); return KG_ECUDA; }
   if (cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->st_cap, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->st3, cudaStreamNonBlocking) != cudaSuccess ||
@@ -1397,9 +1373,6 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
       cudaEventCreateWithFlags(&h->ev_fork2, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
-  if (cublasSetWorkspace(h->blas, h->blas_ws, 32 << 20) != CUBLAS_STATUS_SUCCESS) { kg_destroy(h); return KG_ECUDA; }
-  if (cublasCreate(&h->blas2) != CUBLAS_STATUS_SUCCESS ||
-      cublasSetWorkspace(h->blas2, h->blas_ws2, 32 << 20) != CUBLAS_STATUS_SUCCESS) { kg_destroy(h); return KG_ECUDA; }
   if (c.world > 1) {
     ncclUniqueId id;
     std::memcpy(&id, c.nccl_id, sizeof(id));
@@ -1424,9 +1397,7 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
     kg_destroy(h);
     return KG_ECUDA;
   }
-  if (const char *e = std::getenv("KG_GEMM_SCORES")) h->gemm_scores = !(e[0] == '0');
   h->score_bf16 = c.score_precision == KG_SCORE_BF16;
-  if (h->score_bf16) h->gemm_scores = true;   // the bf16 mode lives on the scoring GEMMs
   if (const char *e = std::getenv("KG_DIST_GRAPH")) h->dist_graph = !(e[0] == '0');
   if (const char *e = std::getenv("KG_NCCL")) if (std::string(e) == "loopback") h->dist_graph = false;
   // DAG contractions (reading A24): the hand-written tcgen05 3xTF32 kernel
@@ -1435,19 +1406,7 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
   // (tools/gemm_precision.py), which BetaE's full-size gradients (K = 800 / 1600 contractions
   // feeding differences of digammas) amplify past the 1e-5 bar; drained, the error is SGEMM's.
   // GQE / Q2B would pass undrained too (1 % faster); one accurate path is kept for all.
-  // KG_GEMM=sgemm: cuBLAS SGEMM everywhere; =tc: undrained tcgen05 (A/B checks).
-  // (cuBLAS 12.9's BF16x9 fp32 emulation is faster and more accurate than SGEMM --
-  // tools/cublas_emu_probe.cu -- but torch 2.11 loads its own cuBLAS 12.8 into the process.)
-  h->gemm_cublas = false;
   h->gemm_drain = true;
-  if (const char *e = std::getenv("KG_GEMM")) {
-    const std::string v = e;
-    if (v == "sgemm") h->gemm_cublas = true;
-    if (v == "tc") h->gemm_drain = false;
-    if (v == "drain") h->gemm_drain = true;
-  }
-  cublasSetMathMode(h->blas, CUBLAS_PEDANTIC_MATH);
-  cublasSetMathMode(h->blas2, CUBLAS_PEDANTIC_MATH);
   // device scalars
   if (cudaMemset(h->ws, 0, h->ws_bytes) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
   if (cudaMemset(h->rel_stamp, 0xff, sizeof(int64_t) * h->R) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
@@ -1500,7 +1459,6 @@ kg_status kg_bind(kg_handle *h, const kg_tables *t, void *stream) {
   }
   h->t = tt;
   h->st = (cudaStream_t)stream;
-  CKB(cublasSetStream(h->blas, h->st));
   if (h->p2p) {
     if (h->host_tier) return fail(h, KG_EUNSUPPORTED, "KG_XCHG=p2p needs theta_E in device memory");
     kg_status s = map_peers(h);
@@ -1546,7 +1504,7 @@ struct LowpScope {
   LowpScope(kg_handle *hh, bool on) : h(hh) { h->gemm_lowp = on; }
   ~LowpScope() { h->gemm_lowp = false; }
 };
-bool gemm_scoring(const kg_handle *h) { return h->gemm_scores && (h->sk == KG_DISTMULT || h->sk == KG_COMPLEX); }
+bool gemm_scoring(const kg_handle *h) { return h->sk == KG_DISTMULT || h->sk == KG_COMPLEX; }
 kg_status score_forward(kg_handle *h, ScoreArgs &sa, int nout, bool train, const int64_t *neg_rows) {
   if (!gemm_scoring(h)) {
     launch_pair_fwd(h->sk, sa, nout, train, h->st);
@@ -1959,9 +1917,17 @@ kg_status fetch_rows(kg_handle *h, const int64_t *ids, int64_t n, const float *t
 
 }  // namespace
 
+// NVTX ranges on the host side of the public calls (enqueue, capture, H2D staging); the
+// device work of a step is one graph launch, its stage boundaries are the stage events.
+struct NvtxRange {
+  explicit NvtxRange(const char *n) { nvtxRangePushA(n); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 extern "C" {
 
 kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info) {
+  NvtxRange range("kg_step");
   kg_status s = check_state(h);
   if (s) return s;
   if (!b) return fail(h, KG_EINVAL, "null batch");
@@ -1976,7 +1942,10 @@ kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info)
   const Plan &p = S.plan;
   S.M = b->M; S.K = b->K; S.Kp = (int)align_up(std::max(b->K, 1), 64); S.NQ = p.nout * b->M;
   h->stamp++;
-  if ((s = ingest(h, b, true, p, lr)) != KG_OK) return s;
+  {
+    NvtxRange r2("kg_step: ingest (H2D staging)");
+    if ((s = ingest(h, b, true, p, lr)) != KG_OK) return s;
+  }
   h->last_M = S.M; h->last_K = S.K;
   // world > 1 is captured too when its exchange has fixed sizes (buckets) and the
   // communicator is NCCL (the loopback test communicator synchronises on the host)
@@ -1996,15 +1965,14 @@ kg_status kg_step(kg_handle *h, const kg_batch *b, float lr, kg_step_info *info)
       // capture once per (structure, M, K, flags) on the internal stream, then replay
       cudaStream_t user = h->st;
       h->st = h->st_cap;
-      CKB(cublasSetStream(h->blas, h->st_cap));
       const int64_t l0 = g_launches;
       h->gemm_count = 0;
+      NvtxRange r3("kg_step: graph capture + instantiate");
       CK(cudaStreamBeginCapture(h->st_cap, cudaStreamCaptureModeThreadLocal));
       s = h->world > 1 ? step_dist(h, S) : enqueue_step(h, S);
       cudaGraph_t graph = nullptr;
       cudaError_t ce = cudaStreamEndCapture(h->st_cap, &graph);
       h->st = user;
-      CKB(cublasSetStream(h->blas, user));
       if (h->world > 1 && (s != KG_OK || ce != cudaSuccess)) {
         // the collectives could not be captured: this and later steps run eagerly
         if (graph) cudaGraphDestroy(graph);
@@ -2127,6 +2095,7 @@ static kg_status embed_queries(kg_handle *h, const kg_batch *q, StepBufs &S, int
 }
 
 kg_status kg_score(kg_handle *h, const kg_batch *q, const int64_t *cand, int32_t n_cand, float *out_dist) {
+  NvtxRange range("kg_score");
   kg_status s = check_state(h);
   if (s) return s;
   if (!q || !cand || !out_dist) return fail(h, KG_EINVAL, "null argument");
@@ -2162,6 +2131,7 @@ kg_status kg_score(kg_handle *h, const kg_batch *q, const int64_t *cand, int32_t
 
 kg_status kg_eval(kg_handle *h, const kg_batch *q, const int64_t *ans_off, const int64_t *ans_ids, int32_t n_neg,
                   const int64_t *negatives, int32_t *ranks, float *metrics) {
+  NvtxRange range("kg_eval");
   kg_status s = check_state(h);
   if (s) return s;
   if (!q || !ans_off || !ans_ids || !ranks || !metrics || n_neg < 0 || (n_neg > 0 && !negatives))
@@ -2426,8 +2396,6 @@ void kg_destroy(kg_handle *h) {
   if (!h) return;
   if (h->st) cudaStreamSynchronize(h->st);
   else cudaDeviceSynchronize();
-  if (h->blas) cublasDestroy(h->blas);
-  if (h->blas2) cublasDestroy(h->blas2);
   if (h->st2) { cudaStreamSynchronize(h->st2); cudaStreamDestroy(h->st2); }
   if (h->st_cap) cudaStreamDestroy(h->st_cap);
   if (h->st3) { cudaStreamSynchronize(h->st3); cudaStreamDestroy(h->st3); }

@@ -54,42 +54,101 @@ def assert_close(x, ref, rtol=RTOL, what="", mask=None):
                              f"got {x[k]!r} ref {ref[k]!r}")
 
 
-def q2b_kink_allowance(cfg, table, b, M, K):
-    """(number of near-kink terms, largest jump 2|dL/dD| among them) for a Q2B batch."""
+def q2b_flip_allowance(cfg, table, b, M, K, rel=1e-6):
+    """Per-element allowance for Q2B's kinks, from the oracle itself (reading A28).
+
+    A term (query i, candidate j, unit k) within rel * (|c| + |o| + |v|) of a kink -- |t| = o
+    or t = 0, t = v - c -- may be decided the other way in fp32 (rel = 1e-6, ~16 ulp: the
+    GPU's query boxes carry the rounding of a few fp32 ops and of the intersection MLPs).  A flip changes dD/dv, dD/dc
+    and dD/do of that term by at most 1 (W in {0, alpha, 1}, dD/do = alpha - W), i.e. the
+    adjoints of v_jk, c_ik and o_ik by at most |dL/dD_ij| (Eq. 1: sigma(gamma - D)/(M n_i) for
+    a pool term, sigma(D+ - gamma)/M for the positive).  The candidate row's element (j, k)
+    gets that bound directly; the query side is propagated exactly through the query's DAG
+    with one vector-Jacobian product per flagged (i, k): allowance += w_ik |dc_ik/dtheta| +
+    w_ik |do_ik/dtheta| on the anchor rows, relation rows and operator weights of query i.
+    Every element no flagged term reaches gets no allowance (the plain 1e-5 bar).
+    Returns (allow_rows [len(uniq), d] aligned with the oracle's uniq, allow_dense, n_terms)."""
     import torch
-    from oracle.model import dense_views, query_disjuncts
+    import oracle.model as OM
+    d = cfg.dim
     na = kggen.N_ANCHORS[b["structure"]]
     ids = np.concatenate([b["anchors"].reshape(-1), b["answers"], b["negatives"]])
     uniq, inv = oracle.dedup(ids)
     X = torch.tensor(table.get(uniq)[0], dtype=torch.float64)
-    P = dense_views(cfg, torch.tensor(table.dense, dtype=torch.float64))
+    theta = torch.tensor(table.dense, dtype=torch.float64)
+    P = OM.dense_views(cfg, theta)
     ia = inv[:M * na].reshape(M, na)
-    anchors = [X[torch.as_tensor(ia[:, a])] for a in range(na)]
     rels = [torch.as_tensor(b["relations"][:, s].astype(np.int64)) for s in range(b["relations"].shape[1])]
-    d = cfg.dim
     with torch.no_grad():
-        qs = query_disjuncts(b["structure"], cfg.kind, anchors, rels, P)
+        qs = OM.query_disjuncts(b["structure"], cfg.kind, [X[torch.as_tensor(ia[:, a])] for a in range(na)], rels, P)
+    dpos, dneg, _ = oracle_forward(cfg, table, b, M, K)
+    bits = kggen.unpack_mask(b["mask"], K)
+    n_i = bits.sum(axis=1).astype(np.float64)
+    g = cfg.gamma
+    sig = lambda z: 1.0 / (1.0 + np.exp(-z))  # noqa: E731
+    c_pos = sig(dpos.min(axis=0) - g) / M                                       # [M]
+    c_neg = np.where(bits, sig(g - dneg.min(axis=0)) / (M * np.maximum(n_i, 1))[:, None], 0.0)   # [M, K]
+    arg_pos, arg_neg = dpos.argmin(axis=0), dneg.argmin(axis=0)
     vpos = X[torch.as_tensor(inv[M * na:M * na + M])]
     vneg = X[torch.as_tensor(inv[M * na + M:])]
-    n_i = kggen.unpack_mask(b["mask"], K).sum(axis=1)
-    jpos, jneg = 2.0 / M, 2.0 / (M * max(1, int(n_i[n_i > 0].min()) if (n_i > 0).any() else 1))
-    count, jump = 0, 0.0
-    for q in qs:
+    allow_rows = np.zeros((len(uniq), d))
+    w = np.zeros((len(qs), M, d))                  # query-side weight per (disjunct, i, k)
+    n_terms = 0
+    pos_u, neg_u = inv[M * na:M * na + M], inv[M * na + M:]
+    for t_, q in enumerate(qs):
         c, o = q[:, :d], q[:, d:]
-        for v, per_query, j in ((vpos, True, jpos), (vneg, False, jneg)):
-            for lo in range(0, M, 32):
-                cc, oo = c[lo:lo + 32], o[lo:lo + 32]
-                t = (v[lo:lo + 32] - cc) if per_query else (v[None, :, :] - cc[:, None, :])
-                if not per_query:
-                    oo = oo[:, None, :]
-                    cc = cc[:, None, :]
-                delta = 1e-5 * (cc.abs() + oo.abs() + (t + cc).abs())
-                near = ((t.abs() - oo).abs() <= delta) | (t.abs() <= delta)
-                n = int(near.sum())
-                if n:
-                    count += n
-                    jump = max(jump, j)
-    return count, jump
+        tt = vpos - c
+        near = (((tt.abs() - o).abs() <= rel * (c.abs() + o.abs() + vpos.abs())) | (tt.abs() <= rel * (c.abs() + vpos.abs())))
+        near = near.numpy() & (arg_pos == t_)[:, None]
+        ii, kk = np.nonzero(near)
+        n_terms += len(ii)
+        np.add.at(allow_rows, (pos_u[ii], kk), c_pos[ii])
+        np.add.at(w[t_], (ii, kk), c_pos[ii])
+        for lo in range(0, M, 16):
+            cc, oo = c[lo:lo + 16, None, :], o[lo:lo + 16, None, :]
+            tt = vneg[None] - cc
+            sc = rel * (cc.abs() + vneg[None].abs())
+            near = ((tt.abs() - oo).abs() <= sc + rel * oo.abs()) | (tt.abs() <= sc)
+            near = near.numpy() & ((arg_neg[lo:lo + 16] == t_) & bits[lo:lo + 16])[:, :, None]
+            ii, jj, kk = np.nonzero(near)
+            if len(ii):
+                n_terms += len(ii)
+                cw = c_neg[lo + ii, jj]
+                np.add.at(allow_rows, (neg_u[jj], kk), cw)
+                np.add.at(w[t_], (lo + ii, kk), cw)
+    # the query side, through each flagged query's DAG (exact vector-Jacobian products)
+    offs, total = kggen.dense_offsets(cfg)
+    allow_dense = np.zeros(total)
+    rel_names = [n for n in offs if n.startswith("rel")]
+    wnames = [n for n in offs if not n.startswith("rel")]
+    for t_ in range(len(qs)):
+        for i in np.nonzero(w[t_].any(axis=1))[0]:
+            rid = b["relations"][i].astype(np.int64)
+            ur, rinv = np.unique(rid, return_inverse=True)
+            leaves_a = [X[ia[i, a]].clone().view(1, d).requires_grad_(True) for a in range(na)]
+            Pi = {n: P[n].detach().clone().requires_grad_(True) for n in wnames}
+            leaves_r = {n: P[n][torch.as_tensor(ur)].detach().clone().requires_grad_(True) for n in rel_names}
+            Pi.update(leaves_r)
+            rels_i = [torch.as_tensor([int(rinv[s])]) for s in range(len(rid))]
+            q = OM.query_disjuncts(b["structure"], cfg.kind, leaves_a, rels_i, Pi)[t_]
+            leaves = leaves_a + [leaves_r[n] for n in rel_names] + [Pi[n] for n in wnames]
+            for k in np.nonzero(w[t_, i])[0]:
+                for col in (k, d + k):
+                    gr = torch.autograd.grad(q[0, col], leaves, retain_graph=True, allow_unused=True)
+                    for a in range(na):
+                        if gr[a] is not None:
+                            allow_rows[ia[i, a]] += w[t_, i, k] * gr[a].abs().numpy()[0]
+                    for n, gg in zip(rel_names, gr[na:na + len(rel_names)]):
+                        if gg is not None:
+                            o0, shape = offs[n]
+                            for r_, row in enumerate(ur):
+                                allow_dense[o0 + row * shape[1]:o0 + (row + 1) * shape[1]] += \
+                                    w[t_, i, k] * gg[r_].abs().numpy()
+                    for n, gg in zip(wnames, gr[na + len(rel_names):]):
+                        if gg is not None:
+                            o0, shape = offs[n]
+                            allow_dense[o0:o0 + gg.numel()] += w[t_, i, k] * gg.abs().reshape(-1).numpy()
+    return allow_rows, allow_dense, n_terms
 
 
 def oracle_forward(cfg, table, b, M, K, trace=False):
@@ -167,18 +226,19 @@ def well_conditioned_batch(cfg, table, structure, M, K, seed):
     return b, redrawn, masked
 
 
-def assert_close_allow(x, ref, what, n_allow, jump):
+def assert_close_allow(x, ref, what, allow):
+    """|x - ref| <= the plain bound + allow (elementwise; allow = 0 where no flagged term reaches)."""
     x = np.asarray(x, np.float64)
     ref = np.asarray(ref, np.float64)
     assert x.shape == ref.shape, (what, x.shape, ref.shape)
     err = np.abs(x - ref)
     tol = RTOL * np.abs(ref) + RTOL * np.abs(ref).max()
-    bad = err > tol
+    bad = err > tol + allow
     if bad.any():
-        assert bad.sum() <= n_allow and np.all(err[bad] <= tol[bad] + 2 * jump), (
-            f"{what}: {bad.sum()} elements out of tolerance (allowance {n_allow}), worst excess "
-            f"{float((err - tol)[bad].max()):.3g} vs jump {jump:.3g}")
-    return int(bad.sum())
+        k = np.unravel_index(np.argmax(np.where(bad, err - tol - allow, -np.inf)), err.shape)
+        raise AssertionError(f"{what}: {bad.sum()}/{bad.size} out of tolerance; worst at {k}: got {x[k]!r} ref "
+                             f"{ref[k]!r}, allowance {allow[k]!r}")
+    return int(((err > tol) & (allow > 0)).sum()), int((allow > 0).sum())
 
 
 CASES = [("C2", "ip", None), ("C2", "up", None), ("C2", "3i", "gqe"), ("C2", "pi", "distmult-m"),
@@ -205,8 +265,14 @@ def test_full_size_step(wl, structure, kind):
     b, redrawn, masked = well_conditioned_batch(cfg, table, structure, M, K, seed=3)
     print(f"{wl} {structure}: {redrawn} queries re-drawn, {masked} near-tie DNF pairs masked out")
     lr = 1e-3
-    n_kink, jump = q2b_kink_allowance(cfg, table, b, M, K) if cfg.kind == "q2b" else (0, 0.0)
+    assert redrawn <= 0.5 * M, f"{redrawn} of {M} queries re-drawn"
+    # (before oracle_step: it applies the update to `table`)
+    allow = q2b_flip_allowance(cfg, table, b, M, K) if cfg.kind == "q2b" else None
     ref = oracle.oracle_step(cfg, table, [b], lr, apply=True)
+    if allow is not None:
+        allow_rows, allow_dense, n_terms = allow
+    else:
+        allow_rows, allow_dense, n_terms = np.zeros_like(ref.grad_rows), np.zeros_like(ref.grad_dense), 0
     info = gm.step(gm.host_batch(b), lr)
     g = gm.last_grads(cap=4 * M + M + K + 8, M=M, K=K)
     assert abs(info.loss - ref.loss) <= RTOL * abs(ref.loss), (info.loss, ref.loss)
@@ -214,11 +280,42 @@ def test_full_size_step(wl, structure, kind):
     assert_close(g["d_neg"], ref.d_neg[0], what="D")
     np.testing.assert_array_equal(g["uniq"], ref.uniq)
     assert info.n_touched == len(ref.uniq)
-    n1 = assert_close_allow(g["grad_rows"], ref.grad_rows, "dL/dtheta_E rows", 8 * n_kink, jump)
-    n2 = assert_close_allow(g["grad_dense"], ref.grad_dense, "dL/dtheta_D", 8 * n_kink, jump)
-    print(f"{wl} {structure}: near-kink terms {n_kink}, outliers rows {n1} dense {n2}")
+    n1, a1 = assert_close_allow(g["grad_rows"], ref.grad_rows, "dL/dtheta_E rows", allow_rows)
+    n2, a2 = assert_close_allow(g["grad_dense"], ref.grad_dense, "dL/dtheta_D", allow_dense)
+    print(f"{wl} {structure}: {n_terms} terms within 1e-6 of a kink; elements with an allowance: rows {a1} of "
+          f"{allow_rows.size}, dense {a2} of {allow_dense.size}; beyond the plain bound: rows {n1}, dense {n2}")
     keep = np.abs(ref.m_new) >= 1e-4 * np.abs(ref.m_new).max()
     assert_close(gm.read_rows(ref.uniq), ref.rows_new, what="theta_E rows after the step", mask=keep)
     keepd = np.abs(ref.dense_m_new) >= 1e-4 * np.abs(ref.dense_m_new).max()
     assert_close(gm.read_dense(0), ref.dense_new, what="theta_D after the step", mask=keepd)
+    gm.close()
+
+
+UNCONDITIONED = [("C5-q2b", "pi"), ("C5-q2b", "3i"), ("C5-betae", "ip"), ("C4", "2in")]
+
+
+@pytest.mark.parametrize("wl,structure", UNCONDITIONED)
+def test_full_size_forward_unconditioned(wl, structure):
+    """The seeded batch exactly as bench.py draws it (no re-drawn queries, no masked pairs): the
+    forward outputs -- every D+ and D_ij and the loss -- are continuous in the fp32 rounding of
+    every discrete decision the forward takes (ReLU, clamp, min), so they meet the plain 1e-5 bar
+    with no conditioning; the touched-row set is bit-exact."""
+    from paper_2110_14890_b200 import KGModel
+    w = kggen.WORKLOADS[wl]
+    cfg = w.model_config()
+    if wl.startswith("C5"):
+        cfg.n_entities = kggen.shard_rows(w.n_entities, 8)
+    M, K = w.M, w.K
+    gm = KGModel(cfg, M, K)
+    gm.init_params(7)
+    gm.set_apply(False, keep_grads=True)
+    table = oracle.SparseTable(cfg, 7)
+    b = kggen.make_batch(cfg, structure, M, K, seed=11, step=0)
+    ref = oracle.oracle_step(cfg, table, [b], 1e-3, apply=False)
+    info = gm.step(gm.host_batch(b), 1e-3)
+    g = gm.last_grads(cap=4 * M + M + K + 8, M=M, K=K)
+    assert abs(info.loss - ref.loss) <= RTOL * abs(ref.loss), (info.loss, ref.loss)
+    assert_close(g["d_pos"], ref.d_pos[0], what="D+")
+    assert_close(g["d_neg"], ref.d_neg[0], what="D")
+    np.testing.assert_array_equal(g["uniq"], ref.uniq)
     gm.close()
