@@ -16,6 +16,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 
 #include "kg_common.cuh"
@@ -226,6 +227,25 @@ __device__ __forceinline__ void split_op(uint8_t *raw, uint8_t *hi, uint8_t *lo,
 // error of the TMEM accumulation grows with the number of MMAs chained into one accumulator
 // (tools/gemm_precision.py: 15-25x SGEMM's at K = 800-1600); chunks of 24 bring it to SGEMM's.
 constexpr int kDrainKB = 4;
+#ifdef KG_GEMM_TRACE
+// tools/gemm_trace.py: globaltimer stamps of CTA (0, 0, 0), per k-block: [0] producer issued the
+// loads, [1] split warp 2 saw full, [2] split warp 2 arrived conv, [3] MMA warp saw conv,
+// [4] MMA issued (before commit); [5] per chunk: drain begin / end
+__device__ unsigned long long g_gemm_trace[8][512];
+__device__ __forceinline__ unsigned long long gt_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define GT(k, i) do { if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (i) < 512) g_gemm_trace[k][i] = gt_now(); } while (0)
+}  // namespace kg
+extern "C" int gemm_trace_get(unsigned long long *out) {
+  return (int)cudaMemcpyFromSymbol(out, kg::g_gemm_trace, sizeof(unsigned long long) * 8 * 512);
+}
+namespace kg {
+#else
+#define GT(k, i) do {} while (0)
+#endif
 template <int BN, bool AMN, bool BMN, bool DRAIN, bool LOWP = false>
 __global__ void __launch_bounds__(G2T, 1)
     gemm_tf32x3_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
@@ -241,7 +261,9 @@ __global__ void __launch_bounds__(G2T, 1)
   static_assert(BN % 32 == 0 && kNeed <= 512 && G2CW % 4 == 0, "tile width / split warps");
   static_assert(!DRAIN || kCI <= 3, "the drained accumulator is held in registers");
   extern __shared__ uint8_t gsm_raw[];
-  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned (SWIZZLE tiles), derived from the shared-memory symbol itself so the
+  // compiler keeps the address space: LDS / STS in the split and the epilogue, not generic LD / ST
+  uint8_t *sm = gsm_raw + ((1024u - (su32(gsm_raw) & 1023u)) & 1023u);
   __shared__ __align__(8) uint64_t full_bar[S], conv_bar[S], empty_bar[S];
   __shared__ __align__(8) uint64_t done_bar, acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base;
@@ -285,6 +307,7 @@ __global__ void __launch_bounds__(G2T, 1)
         const int k0 = (kb0 + kb) * G2K;
         load_op<AMN, GBM>(&tmA, &full_bar[s], st, m0, k0);
         load_op<BMN, BN>(&tmB, &full_bar[s], st + Cfg::kA, n0, k0);
+        GT(0, kb);
       }
     }
   } else if (warp == 1) {
@@ -295,6 +318,7 @@ __global__ void __launch_bounds__(G2T, 1)
         const bool chunk0 = DRAIN ? (kb % kDrainKB == 0) : (kb == 0);
         if (DRAIN && chunk0 && c >= 2) mbar_wait(&acc_empty[c & 1], ((c >> 1) - 1) & 1);   // chunk c-2 drained
         mbar_wait(&conv_bar[s], (kb / S) & 1);
+        GT(3, kb);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t tm = DRAIN ? tmem + (uint32_t)((c & 1) * BN) : tmem;
         const uint32_t st = su32(sm + s * Cfg::kStage);
@@ -313,6 +337,7 @@ __global__ void __launch_bounds__(G2T, 1)
           mma_tf32_i<Cfg::kIdesc>(tm, dal, dbh, 1);
           mma_tf32_i<Cfg::kIdesc>(tm, dah, dbh, 1);
         }
+        GT(4, kb);
         mma_commit(&empty_bar[s]);
         if (DRAIN && (kb % kDrainKB == kDrainKB - 1 || kb == nkb - 1)) mma_commit(&acc_full[c & 1]);
       }
@@ -356,11 +381,13 @@ __global__ void __launch_bounds__(G2T, 1)
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % S;
       mbar_wait(&full_bar[s], (kb / S) & 1);
+      if (ct == 0) GT(1, kb);
       uint8_t *st = sm + s * Cfg::kStage;
       split_op<AMN, GBM, LOWP>(st, st + Cfg::oAhi, st + Cfg::oAlo, ct);
       split_op<BMN, BN, LOWP>(st + Cfg::kA, st + Cfg::oBhi, st + Cfg::oBlo, ct);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic stores -> tensor-core reads
       mbar_arrive(&conv_bar[s]);
+      if (ct == 0) GT(2, kb);
       // DRAIN: once chunk c's operands are all released, the previous chunk is drained
       if (DRAIN && (kb % kDrainKB == kDrainKB - 1 || kb == nkb - 1) && kb / kDrainKB >= 1) drain(kb / kDrainKB - 1);
     }
@@ -466,6 +493,7 @@ bool launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t s
   const int nkb = (g.K + G2K - 1) / G2K;
   // split K to fill the SMs while every split keeps >= 8 k-blocks (measured best of 8 / 16 / none)
   int splits = std::max(1, std::min(148 / std::max(tiles, 1), nkb / 8));
+  if (g0.force & 1) splits = 1;
   while (splits > 1 && (!part || (int64_t)splits * g.M * g.N > part_cap)) --splits;
   g.kbs = (nkb + splits - 1) / splits;
   splits = (nkb + g.kbs - 1) / g.kbs;
@@ -502,6 +530,17 @@ bool launch_gemm_tc(const GemmArgs &g, float *part, int64_t part_cap, cudaStream
   const int64_t t256 = (int64_t)((g.N + 255) / 256) * ((g.M + GBM - 1) / GBM);
   const bool wide = g.N > 128 && t256 >= 100;   // enough 128 x 256 tiles to fill the GPU
   if (g.lowp) return launch_v2_any<128, false, true>(g, part, part_cap, st);
+  if (g.force) {
+    const GemmArgs &f = g;
+    const int bn = (g.force >> 1) & 3;
+    auto go = [&](auto tag) -> bool {
+      constexpr int BN = decltype(tag)::value;
+      return f.drain ? launch_v2_any<BN, true>(f, part, part_cap, st) : launch_v2_any<BN, false>(f, part, part_cap, st);
+    };
+    if (bn == 1) return go(std::integral_constant<int, 64>());
+    if (bn == 3) return go(std::integral_constant<int, 160>());
+    return go(std::integral_constant<int, 128>());
+  }
   if (g.drain) {
     // wave quantisation: e.g. 1536 x 1600 is 156 tiles of 128 x 128 (two waves on 148 SMs) but
     // 120 tiles of 128 x 160 (one)

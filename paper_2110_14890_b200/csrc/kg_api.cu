@@ -2352,6 +2352,7 @@ kg_status kg_test_gemm(int32_t ta, int32_t tb, int32_t M, int32_t N, int32_t K, 
   GemmArgs g;
   g.A = A; g.B = B; g.C = C; g.bias = bias; g.M = M; g.N = N; g.K = K; g.lda = lda; g.ldb = ldb; g.ldc = ldc;
   g.relu = relu & 1; g.beta = beta; g.a_mn = ta != 0; g.b_mn = tb != 0; g.drain = (relu & 2) != 0;
+  g.force = relu >> 2;   // tile experiments (tools/gemm_tiles.py)
   if (!gemm_tc_accepts(g)) return KG_EINVAL;   // 16-byte aligned operands with ld % 4 == 0
   float *sP = nullptr;
   const int64_t pcap = 8LL * std::max(M, 1) * std::max(N, 1);

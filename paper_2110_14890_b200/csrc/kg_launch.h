@@ -105,6 +105,7 @@ struct GemmArgs {
   int kbs = 1 << 30;    // k-blocks per split
   bool drain = false;   // fp32-accurate accumulation: TMEM chunks of kDrainKB k-blocks summed in registers
   bool lowp = false;    // bf16 score mode: operands rounded to bf16, one MMA per K-step (no 3xTF32 split)
+  int force = 0;        // tile experiments (kg_test_gemm): bit 0 no split-K; bits 1-2 BN 1:64 2:128 3:160
 };
 bool gemm_tc_accepts(const GemmArgs &g);   // 16-byte aligned operands, ld % 4 == 0
 bool launch_gemm_tc(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st);   // false: not launched

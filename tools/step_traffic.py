@@ -44,7 +44,7 @@ def classify(name, kind, single_hop):
     return None
 
 
-def run(workload):
+def run(workload, only=None):
     import torch
     import kggen
     from paper_2110_14890_b200 import KGModel
@@ -56,7 +56,7 @@ def run(workload):
     gm.init_params(0)
     gm.set_apply(True)
     batches = [gm.device_batch(kggen.make_batch(cfg, s, w.M, w.K, seed=0, step=i))
-               for i, s in enumerate(w.structures)]
+               for i, s in enumerate(w.structures) if not only or s in only]
     for b in batches:                                  # warm-up: one graph per structure
         gm.step(b, 1e-4, sync=False, on_device=True)
     gm.sync()
@@ -120,10 +120,11 @@ def parse(paths, out):
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload")
+    ap.add_argument("--structures", default="", help="comma list: profile only these structures")
     ap.add_argument("--parse", nargs="*")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "ncu_traffic.json"))
     a = ap.parse_args()
     if a.parse:
         parse(a.parse, a.out)
     else:
-        run(a.workload)
+        run(a.workload, [x for x in a.structures.split(",") if x])
