@@ -100,14 +100,20 @@ __global__ void gemm_reduce_kernel(const float *__restrict__ P, int splits, int 
 #endif
 constexpr int G2CW = KG_G2CW;                          // split / epilogue warps
 constexpr int G2T = 64 + 32 * G2CW, G2K = 16;
-template <int BN, bool AMN, bool BMN> struct G2Cfg {
+// ATM (the fp32-accurate modes): A's hi / lo tiles go to tensor memory, so a stage holds
+// A raw, B raw, [B hi if BMN], B lo; otherwise (LOWP) A raw, B raw, [A hi], [B hi], A lo, B lo.
+// S stages (even) in G = S / 2 groups of k-blocks: the MMA warp commits once per group
+// (a tcgen05.commit drains the tensor pipe: ~200 cycles, tools/mma_probe.cu), and the
+// producer refills a group's stages when the group two back has completed.
+template <int BN, bool AMN, bool BMN, bool ATM = true> struct G2Cfg {
   static constexpr int kA = GBM * G2K * 4, kB = BN * G2K * 4;           // bytes of one tile
-  // stage: A raw, B raw, [A hi if AMN], [B hi if BMN], A lo, B lo
-  static constexpr int kStage = 2 * (kA + kB) + (AMN ? kA : 0) + (BMN ? kB : 0);
-  static constexpr int kStages = (196 * 1024) / kStage < 8 ? (196 * 1024) / kStage : 8;
+  static constexpr int kStage = ATM ? kA + kB + (BMN ? kB : 0) + kB : 2 * (kA + kB) + (AMN ? kA : 0) + (BMN ? kB : 0);
+  static constexpr int kFit = (196 * 1024) / kStage < 8 ? (196 * 1024) / kStage : 8;
+  static constexpr int kStages = kFit >= 2 ? (kFit / 2) * 2 : 2;
+  static constexpr int kGroup = kStages / 2;
   static constexpr int kSmem = kStages * kStage + 1024;
-  static constexpr int oAhi = kA + kB, oBhi = oAhi + (AMN ? kA : 0);
-  static constexpr int oAlo = oBhi + (BMN ? kB : 0), oBlo = oAlo + kA;
+  static constexpr int oAhi = kA + kB, oBhi = ATM ? kA + kB : oAhi + (AMN ? kA : 0);
+  static constexpr int oAlo = oBhi + (BMN ? kB : 0), oBlo = ATM ? oAlo : oAlo + kA;
   static constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                                      ((uint32_t)(GBM >> 4) << 24);
 };
@@ -139,6 +145,15 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap *tm, uint64_t *bar
           su32(dst)),
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(su32(bar)), "r"(x), "r"(y)
       : "memory");
+}
+// A operand from tensor memory ([a_tmem]: 128 lanes = rows, one 32-bit column per k), B from
+// shared memory: the MMA reads only B through the shared-memory port
+template <uint32_t IDESC>
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem, uint32_t a_tmem, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %3, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %4, p;\n}\n" ::"r"(tmem),
+      "r"(a_tmem), "l"(b), "r"(acc), "r"(IDESC));
 }
 template <uint32_t IDESC>
 __device__ __forceinline__ void mma_tf32_i(uint32_t tmem, uint64_t a, uint64_t b, uint32_t acc) {
@@ -221,22 +236,18 @@ __device__ __forceinline__ void split_op(uint8_t *raw, uint8_t *hi, uint8_t *lo,
   }
 }
 
-// DRAIN (fp32-accurate mode, reading A24): the tensor cores accumulate only kDrainKB k-blocks
-// (K = 64: 24 MMAs) into one of two TMEM accumulators; the split warps then drain that chunk
-// into fp32 registers (round-to-nearest adds) while the MMA warp fills the other one.  The
-// error of the TMEM accumulation grows with the number of MMAs chained into one accumulator
-// (tools/gemm_precision.py: 15-25x SGEMM's at K = 800-1600); chunks of 24 bring it to SGEMM's.
-constexpr int kDrainKB = 4;
+// DRAIN (fp32-accurate mode, reading A24): the tensor cores accumulate only one group of G
+// k-blocks (K = 16 G: 6 G MMAs) into one of two TMEM accumulators; the split warps then drain
+// that group into fp32 registers (round-to-nearest adds) while the MMA warp fills the other
+// one.  The error of the TMEM accumulation grows with the number of MMAs chained into one
+// accumulator (tools/gemm_precision.py: 15-25x SGEMM's at K = 800-1600); groups of <= 24 MMAs
+// bring it to SGEMM's.
 #ifdef KG_GEMM_TRACE
 // tools/gemm_trace.py: globaltimer stamps of CTA (0, 0, 0), per k-block: [0] producer issued the
 // loads, [1] split warp 2 saw full, [2] split warp 2 arrived conv, [3] MMA warp saw conv,
 // [4] MMA issued (before commit); [5] per chunk: drain begin / end
 __device__ unsigned long long g_gemm_trace[8][512];
-__device__ __forceinline__ unsigned long long gt_now() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
+__device__ __forceinline__ unsigned long long gt_now() { return (unsigned long long)clock64(); }   // SM cycles
 #define GT(k, i) do { if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (i) < 512) g_gemm_trace[k][i] = gt_now(); } while (0)
 }  // namespace kg
 extern "C" int gemm_trace_get(unsigned long long *out) {
@@ -250,11 +261,20 @@ template <int BN, bool AMN, bool BMN, bool DRAIN, bool LOWP = false>
 __global__ void __launch_bounds__(G2T, 1)
     gemm_tf32x3_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
   KG_GRID_DEP_WAIT();
-  using Cfg = G2Cfg<BN, AMN, BMN>;
-  constexpr int S = Cfg::kStages;
+  using Cfg = G2Cfg<BN, AMN, BMN, !LOWP>;
+  constexpr int S = Cfg::kStages, G = Cfg::kGroup;
   // TMEM columns: a power of 2 >= 32 holding one (or, drained, two) BN-column accumulators
   constexpr int kNeed = DRAIN ? 2 * BN : BN;
-  constexpr int kCols = kNeed <= 32 ? 32 : kNeed <= 64 ? 64 : kNeed <= 128 ? 128 : kNeed <= 256 ? 256 : 512;
+  // ATM (every fp32-accurate mode): the A operand's hi / lo tiles of each stage live in tensor
+  // memory (32 columns per stage after the accumulators), written by the split warps with
+  // tcgen05.st; the MMAs then read only B from shared memory.  Shared-memory traffic per
+  // k-block (128 x 128): TMA 16 KB + split 24 KB + MMA 24 KB = 64 KB instead of 96 KB (the
+  // split stage was bound by the 128 B/clk shared-memory port: tools/gemm_trace.py).
+  constexpr bool ATM = !LOWP;
+  constexpr int kACol = kNeed;
+  constexpr int kCols = ATM ? 512 : kNeed <= 32 ? 32 : kNeed <= 64 ? 64 : kNeed <= 128 ? 128 : kNeed <= 256 ? 256 : 512;
+  static_assert(!ATM || (kACol % 32 == 0 && kACol + 32 * S <= 512 && G2CW == 8), "TMEM A stages");
+  static_assert(S == 2 * G && G >= 1, "two groups of stages in flight");
   // 32-column chunks of the tile; the NG = G2CW / 4 warps of a TMEM lane quarter take the
   // chunks round-robin (chunk = grp + NG i)
   constexpr int NG = G2CW / 4, kChunks = BN / 32, kCI = (kChunks + NG - 1) / NG;
@@ -264,8 +284,11 @@ __global__ void __launch_bounds__(G2T, 1)
   // 1024-byte aligned (SWIZZLE tiles), derived from the shared-memory symbol itself so the
   // compiler keeps the address space: LDS / STS in the split and the epilogue, not generic LD / ST
   uint8_t *sm = gsm_raw + ((1024u - (su32(gsm_raw) & 1023u)) & 1023u);
-  __shared__ __align__(8) uint64_t full_bar[S], conv_bar[S], empty_bar[S];
-  __shared__ __align__(8) uint64_t done_bar, acc_full[2], acc_empty[2];
+  // full[s]: TMA landed; conv[s]: split done (one arrival per split warp); gdone[g & 1]: the
+  // MMAs of group g completed (one commit per group: frees its stages for the producer and
+  // hands its accumulator to the drain); acc_empty[g & 1]: the drain of group g is done
+  __shared__ __align__(8) uint64_t full_bar[S], conv_bar[S];
+  __shared__ __align__(8) uint64_t done_bar, gdone[2], acc_empty[2];
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * BN;
@@ -282,13 +305,12 @@ __global__ void __launch_bounds__(G2T, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     for (int s = 0; s < S; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&conv_bar[s], 32 * G2CW);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&conv_bar[s], G2CW);   // one arrival per split warp (256 single-thread arrivals serialise)
     }
     mbar_init(&done_bar, 1);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 32 * G2CW);
+      mbar_init(&gdone[b], 1);
+      mbar_init(&acc_empty[b], G2CW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
@@ -301,7 +323,10 @@ __global__ void __launch_bounds__(G2T, 1)
     if (lane == 0) {
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % S;
-        if (kb >= S) mbar_wait(&empty_bar[s], ((kb / S) - 1) & 1);
+        if (kb >= S) {   // the stage's previous k-block belongs to group kb / G - 2 (S = 2 G)
+          const int gw = kb / G - 2;
+          mbar_wait(&gdone[gw & 1], (gw >> 1) & 1);
+        }
         uint8_t *st = sm + s * Cfg::kStage;
         mbar_expect_tx(&full_bar[s], Cfg::kA + Cfg::kB);
         const int k0 = (kb0 + kb) * G2K;
@@ -312,34 +337,45 @@ __global__ void __launch_bounds__(G2T, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % S;
-        const int c = kb / kDrainKB;                      // DRAIN: chunk c -> accumulator c & 1
-        const bool chunk0 = DRAIN ? (kb % kDrainKB == 0) : (kb == 0);
-        if (DRAIN && chunk0 && c >= 2) mbar_wait(&acc_empty[c & 1], ((c >> 1) - 1) & 1);   // chunk c-2 drained
-        mbar_wait(&conv_bar[s], (kb / S) & 1);
-        GT(3, kb);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t tm = DRAIN ? tmem + (uint32_t)((c & 1) * BN) : tmem;
-        const uint32_t st = su32(sm + s * Cfg::kStage);
-        const uint32_t ah = AMN ? st + Cfg::oAhi : st, bh = BMN ? st + Cfg::oBhi : st + Cfg::kA;
-        const uint32_t al = st + Cfg::oAlo, bl = st + Cfg::oBlo;
+      const int ngr = (nkb + G - 1) / G;
+      for (int gi = 0; gi < ngr; ++gi) {
+        if (DRAIN && gi >= 2) mbar_wait(&acc_empty[gi & 1], ((gi >> 1) - 1) & 1);   // group gi-2 drained
+        GT(7, 256 + gi);
+        const uint32_t tm = DRAIN ? tmem + (uint32_t)((gi & 1) * BN) : tmem;
+        const int kbe = min(nkb, gi * G + G);
+        for (int kb = gi * G; kb < kbe; ++kb) {
+          const int s = kb % S;
+          const bool first = DRAIN ? (kb == gi * G) : (kb == 0);
+          mbar_wait(&conv_bar[s], (kb / S) & 1);
+          GT(3, kb);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t st = su32(sm + s * Cfg::kStage);
+          const uint32_t ah = AMN ? st + Cfg::oAhi : st, bh = BMN ? st + Cfg::oBhi : st + Cfg::kA;
+          const uint32_t al = st + Cfg::oAlo, bl = st + Cfg::oBlo;
+          const uint32_t ta = tmem + (uint32_t)(kACol + 32 * s);   // this stage's A: hi at +0, lo at +16
 #pragma unroll
-        for (int kk = 0; kk < G2K / 8; ++kk) {   // K = 8 tf32 per MMA
-          const uint64_t dah = kmajor_desc(ah, kk), dal = kmajor_desc(al, kk);
-          const uint64_t dbh = kmajor_desc(bh, kk), dbl = kmajor_desc(bl, kk);
-          if (LOWP) {   // bf16-rounded operands: one MMA
-            mma_tf32_i<Cfg::kIdesc>(tm, dah, dbh, !(chunk0 && kk == 0));
-            continue;
+          for (int kk = 0; kk < G2K / 8; ++kk) {   // K = 8 tf32 per MMA
+            const uint64_t dbh = kmajor_desc(bh, kk), dbl = kmajor_desc(bl, kk);
+            if (ATM) {
+              mma_tf32_ts<Cfg::kIdesc>(tm, ta + 8 * kk, dbl, !(first && kk == 0));        // hi.lo
+              mma_tf32_ts<Cfg::kIdesc>(tm, ta + 16 + 8 * kk, dbh, 1);                     // lo.hi
+              mma_tf32_ts<Cfg::kIdesc>(tm, ta + 8 * kk, dbh, 1);                          // hi.hi
+              continue;
+            }
+            const uint64_t dah = kmajor_desc(ah, kk), dal = kmajor_desc(al, kk);
+            if (LOWP) {   // bf16-rounded operands: one MMA
+              mma_tf32_i<Cfg::kIdesc>(tm, dah, dbh, !(first && kk == 0));
+              continue;
+            }
+            // small terms first: hi.lo, lo.hi, then hi.hi
+            mma_tf32_i<Cfg::kIdesc>(tm, dah, dbl, !(first && kk == 0));
+            mma_tf32_i<Cfg::kIdesc>(tm, dal, dbh, 1);
+            mma_tf32_i<Cfg::kIdesc>(tm, dah, dbh, 1);
           }
-          // small terms first: hi.lo, lo.hi, then hi.hi
-          mma_tf32_i<Cfg::kIdesc>(tm, dah, dbl, !(chunk0 && kk == 0));
-          mma_tf32_i<Cfg::kIdesc>(tm, dal, dbh, 1);
-          mma_tf32_i<Cfg::kIdesc>(tm, dah, dbh, 1);
+          GT(4, kb);
         }
-        GT(4, kb);
-        mma_commit(&empty_bar[s]);
-        if (DRAIN && (kb % kDrainKB == kDrainKB - 1 || kb == nkb - 1)) mma_commit(&acc_full[c & 1]);
+        mma_commit(&gdone[gi & 1]);
+        GT(6, 256 + gi);
       }
       mma_commit(&done_bar);
     }
@@ -357,7 +393,8 @@ __global__ void __launch_bounds__(G2T, 1)
         for (int j = 0; j < 32; ++j) acc[i][j] = 0.f;
     }
     auto drain = [&](int c) {
-      mbar_wait(&acc_full[c & 1], (c >> 1) & 1);
+      if (ct == 0) GT(6, c);
+      mbar_wait(&gdone[c & 1], (c >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
       for (int i = 0; i < (DRAIN ? kCI : 1); ++i) {
@@ -376,22 +413,62 @@ __global__ void __launch_bounds__(G2T, 1)
         for (int j = 0; j < 32; ++j) acc[i][j] += __uint_as_float(r[j]);
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
-      mbar_arrive(&acc_empty[c & 1]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[c & 1]);
+      if (ct == 0) GT(7, c);
     };
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % S;
       mbar_wait(&full_bar[s], (kb / S) & 1);
       if (ct == 0) GT(1, kb);
       uint8_t *st = sm + s * Cfg::kStage;
-      split_op<AMN, GBM, LOWP>(st, st + Cfg::oAhi, st + Cfg::oAlo, ct);
+      if (ATM) {
+        // A: row r = 32 q + lane of the tile (this warp's TMEM lane quarter), k half `half`:
+        // 8 values -> hi = trunc_tf32(x), lo = rna_tf32(x - hi) -> two tcgen05.st of 8 columns
+        const int r = 32 * q + lane;
+        float v[8];
+        if (!AMN) {
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj) {
+            const float4 x = *reinterpret_cast<const float4 *>(st + sw64_off(r, 2 * half + jj));
+            v[4 * jj + 0] = x.x; v[4 * jj + 1] = x.y; v[4 * jj + 2] = x.z; v[4 * jj + 3] = x.w;
+          }
+        } else {   // raw MN-major boxes [GBM / 32][16 k][32 rows]
+          const float *src = reinterpret_cast<const float *>(st + (r >> 5) * 2048) + (r & 31);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = src[(8 * half + i) * 32];
+        }
+        uint32_t hb[8], lb[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t h = __float_as_uint(v[i]) & 0xFFFFE000u;
+          hb[i] = h;
+          lb[i] = __float_as_uint(rna_tf32(v[i] - __uint_as_float(h)));
+        }
+        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(kACol + 32 * s + 8 * half);
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta),
+                     "r"(hb[0]), "r"(hb[1]), "r"(hb[2]), "r"(hb[3]), "r"(hb[4]), "r"(hb[5]), "r"(hb[6]), "r"(hb[7])
+                     : "memory");
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta + 16),
+                     "r"(lb[0]), "r"(lb[1]), "r"(lb[2]), "r"(lb[3]), "r"(lb[4]), "r"(lb[5]), "r"(lb[6]), "r"(lb[7])
+                     : "memory");
+      } else {
+        split_op<AMN, GBM, LOWP>(st, st + Cfg::oAhi, st + Cfg::oAlo, ct);
+      }
       split_op<BMN, BN, LOWP>(st + Cfg::kA, st + Cfg::oBhi, st + Cfg::oBlo, ct);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic stores -> tensor-core reads
-      mbar_arrive(&conv_bar[s]);
+      if (ATM) {
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&conv_bar[s]);
       if (ct == 0) GT(2, kb);
-      // DRAIN: once chunk c's operands are all released, the previous chunk is drained
-      if (DRAIN && (kb % kDrainKB == kDrainKB - 1 || kb == nkb - 1) && kb / kDrainKB >= 1) drain(kb / kDrainKB - 1);
+      if (ct == 32 * G2CW - 32) GT(5, kb);   // the last split warp
+      // DRAIN: once group c's operands are all split, the previous group is drained
+      if (DRAIN && (kb % G == G - 1 || kb == nkb - 1) && kb / G >= 1) drain(kb / G - 1);
     }
-    if (DRAIN && nkb > 0) drain((nkb - 1) / kDrainKB);
+    if (DRAIN && nkb > 0) drain((nkb - 1) / G);
     // ---- epilogue: TMEM -> registers (thread = accumulator row) -> per-warp 32 x 33 staging
     // tile in the (now idle) pipeline smem -> coalesced row stores (lane = column)
     mbar_wait(&done_bar, 0);
@@ -480,7 +557,7 @@ bool make_tmap(CUtensorMap *tm, const float *base, int rows, int K, int ld, int 
 
 template <int BN, bool AMN, bool BMN, bool DRAIN, bool LOWP = false>
 bool launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t st) {
-  using Cfg = G2Cfg<BN, AMN, BMN>;
+  using Cfg = G2Cfg<BN, AMN, BMN, !LOWP>;
   CUtensorMap ta, tb;
   if (!make_tmap(&ta, g0.A, g0.M, g0.K, g0.lda, GBM, AMN) || !make_tmap(&tb, g0.B, g0.N, g0.K, g0.ldb, BN, BMN))
     return false;

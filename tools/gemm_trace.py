@@ -34,6 +34,9 @@ lib.gemm_trace_get(C.c_void_p(tr.ctypes.data))
 t = tr.astype(np.int64)
 t0 = t[0, 0]
 n = int((t[0] > 0).sum())
-print("k-block  produce  split_saw_full  split_done  mma_saw_conv  mma_issued   (ns from the first load issue)")
+print("k-block  produce  split_saw_full  split_done  mma_saw_conv  mma_issued  lastwarp_done | chunk: drain_begin drain_end"
+      "   (SM cycles from the first load issue)")
 for kb in range(n):
-    print(f"{kb:4d} " + " ".join(f"{(t[r, kb] - t0):10d}" for r in range(5)))
+    extra = f" | {t[6, kb] - t0:8d} {t[7, kb] - t0:8d}" if t[6, kb] > 0 else " |"
+    extra += f" || group {kb}: mma start {t[7, 256 + kb] - t0:8d} committed {t[6, 256 + kb] - t0:8d}" if t[7, 256 + kb] > 0 else ""
+    print(f"{kb:4d} " + " ".join(f"{(t[r, kb] - t0):10d}" for r in (0, 1, 2, 3, 4, 5)) + extra)
