@@ -105,10 +105,14 @@ constexpr int G2T = 64 + 32 * G2CW, G2K = 16;
 // S stages (even) in G = S / 2 groups of k-blocks: the MMA warp commits once per group
 // (a tcgen05.commit drains the tensor pipe: ~200 cycles, tools/mma_probe.cu), and the
 // producer refills a group's stages when the group two back has completed.
-template <int BN, bool AMN, bool BMN, bool ATM = true> struct G2Cfg {
+template <int BN, bool AMN, bool BMN, bool ATM = true, bool DRAIN = true> struct G2Cfg {
   static constexpr int kA = GBM * G2K * 4, kB = BN * G2K * 4;           // bytes of one tile
   static constexpr int kStage = ATM ? kA + kB + (BMN ? kB : 0) + kB : 2 * (kA + kB) + (AMN ? kA : 0) + (BMN ? kB : 0);
-  static constexpr int kFit = (196 * 1024) / kStage < 8 ? (196 * 1024) / kStage : 8;
+  // stages: shared memory (224 KB budget), at most 8, and (ATM) 32 TMEM columns each after
+  // the accumulator(s)
+  static constexpr int kTmemFit = ATM ? (512 - (DRAIN ? 2 * BN : BN)) / 32 : 8;
+  static constexpr int kSmemFit = (224 * 1024) / kStage;
+  static constexpr int kFit = kSmemFit < 8 ? (kSmemFit < kTmemFit ? kSmemFit : kTmemFit) : (8 < kTmemFit ? 8 : kTmemFit);
   static constexpr int kStages = kFit >= 2 ? (kFit / 2) * 2 : 2;
   static constexpr int kGroup = kStages / 2;
   static constexpr int kSmem = kStages * kStage + 1024;
@@ -130,6 +134,23 @@ __device__ __forceinline__ uint32_t sw64_off(int r, int q) {
   return (uint32_t)((r >> 3) * 512 + (r & 7) * 64 + ((q ^ ((r >> 1) & 3)) << 4));
 }
 
+// Named (hardware) barriers between the split warps and the MMA warp.  The MMA warp must
+// not wait on an mbarrier (or poll shared memory) while its MMAs are in flight: that stalls
+// the tensor pipe ~200 cycles per wait (tools/mma_probe.cu, "pattern" rows: 592 vs 385
+// cycles per 16-deep k-block); a bar.sync does not (385).
+// k-block barriers: one split team (4 warps) + the MMA warp; drain barriers: both teams + MMA warp
+constexpr int kTeamBar = 32 * (G2CW / 2) + 32, kAllBar = 32 * G2CW + 32;
+template <int N> __device__ __forceinline__ void nbar_sync(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(N) : "memory");
+}
+template <int N> __device__ __forceinline__ void nbar_arrive(int id) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "n"(N) : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p = 0;
+  asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\nselp.u32 %0, 1, 0, e;\n}\n" : "=r"(p));
+  return p != 0;
+}
 __device__ __forceinline__ void mbar_init(uint64_t *b, int n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
 }
@@ -199,10 +220,10 @@ __device__ __forceinline__ float4 bf16r4(float4 v) { return make_float4(bf16r(v.
 // mode): the operand is rounded to bf16 (RNE) instead -- K-major in place, MN-major into hi --
 // and the one MMA per K-step multiplies bf16-exact values (exact products, fp32 accumulation)
 template <bool MN, int R, bool LOWP = false>
-__device__ __forceinline__ void split_op(uint8_t *raw, uint8_t *hi, uint8_t *lo, int ct) {
+__device__ __forceinline__ void split_op(uint8_t *raw, uint8_t *hi, uint8_t *lo, int ct, int nthr) {
   if (LOWP && !MN) {
 #pragma unroll 4
-    for (int c = ct; c < R * 4; c += 32 * G2CW) {
+    for (int c = ct; c < R * 4; c += nthr) {
       float4 *p = reinterpret_cast<float4 *>(raw + c * 16);
       *p = bf16r4(*p);
     }
@@ -210,13 +231,13 @@ __device__ __forceinline__ void split_op(uint8_t *raw, uint8_t *hi, uint8_t *lo,
   }
   if (!MN) {   // K-major: same (swizzled) offsets, lo only
 #pragma unroll 4
-    for (int c = ct; c < R * 4; c += 32 * G2CW) {
+    for (int c = ct; c < R * 4; c += nthr) {
       const float4 v = *reinterpret_cast<const float4 *>(raw + c * 16);
       *reinterpret_cast<float4 *>(lo + c * 16) = tf32_lo(v);
     }
   } else {     // MN-major raw [R/32][16 k][32 rows] -> K-major SW64 hi and lo, 4 k per chunk
 #pragma unroll 4
-    for (int c = ct; c < R * 4; c += 32 * G2CW) {
+    for (int c = ct; c < R * 4; c += nthr) {
       const int r = c % R, q = c / R;
       const float *src = reinterpret_cast<const float *>(raw + (r >> 5) * 2048) + (r & 31);
       float4 v;
@@ -261,7 +282,7 @@ template <int BN, bool AMN, bool BMN, bool DRAIN, bool LOWP = false>
 __global__ void __launch_bounds__(G2T, 1)
     gemm_tf32x3_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
   KG_GRID_DEP_WAIT();
-  using Cfg = G2Cfg<BN, AMN, BMN, !LOWP>;
+  using Cfg = G2Cfg<BN, AMN, BMN, !LOWP, DRAIN>;
   constexpr int S = Cfg::kStages, G = Cfg::kGroup;
   // TMEM columns: a power of 2 >= 32 holding one (or, drained, two) BN-column accumulators
   constexpr int kNeed = DRAIN ? 2 * BN : BN;
@@ -274,7 +295,8 @@ __global__ void __launch_bounds__(G2T, 1)
   constexpr int kACol = kNeed;
   constexpr int kCols = ATM ? 512 : kNeed <= 32 ? 32 : kNeed <= 64 ? 64 : kNeed <= 128 ? 128 : kNeed <= 256 ? 256 : 512;
   static_assert(!ATM || (kACol % 32 == 0 && kACol + 32 * S <= 512 && G2CW == 8), "TMEM A stages");
-  static_assert(S == 2 * G && G >= 1, "two groups of stages in flight");
+  static_assert(S == 2 * G && G >= 2 && S + 3 <= 16, "two groups of stages in flight, k-blocks of both split teams in "
+                "each; named barrier ids 1 .. S + 2");
   // 32-column chunks of the tile; the NG = G2CW / 4 warps of a TMEM lane quarter take the
   // chunks round-robin (chunk = grp + NG i)
   constexpr int NG = G2CW / 4, kChunks = BN / 32, kCI = (kChunks + NG - 1) / NG;
@@ -284,11 +306,12 @@ __global__ void __launch_bounds__(G2T, 1)
   // 1024-byte aligned (SWIZZLE tiles), derived from the shared-memory symbol itself so the
   // compiler keeps the address space: LDS / STS in the split and the epilogue, not generic LD / ST
   uint8_t *sm = gsm_raw + ((1024u - (su32(gsm_raw) & 1023u)) & 1023u);
-  // full[s]: TMA landed; conv[s]: split done (one arrival per split warp); gdone[g & 1]: the
-  // MMAs of group g completed (one commit per group: frees its stages for the producer and
-  // hands its accumulator to the drain); acc_empty[g & 1]: the drain of group g is done
-  __shared__ __align__(8) uint64_t full_bar[S], conv_bar[S];
-  __shared__ __align__(8) uint64_t done_bar, gdone[2], acc_empty[2];
+  // full[s]: TMA landed (mbarrier); split of k-block kb done: named barrier 1 + kb % S; gdone[g &
+  // 1]: the MMAs of group g completed (mbarrier, one commit per group: frees its stages for
+  // the producer and hands its accumulator to the drain); drain of group g done: named
+  // barrier 1 + S + (g & 1).  (Barrier ids <= 1 + 8 + 1 < 16; 0 is __syncthreads.)
+  __shared__ __align__(8) uint64_t full_bar[S];
+  __shared__ __align__(8) uint64_t done_bar, gdone[2];
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * BN;
@@ -303,15 +326,9 @@ __global__ void __launch_bounds__(G2T, 1)
   if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&conv_bar[s], G2CW);   // one arrival per split warp (256 single-thread arrivals serialise)
-    }
+    for (int s = 0; s < S; ++s) mbar_init(&full_bar[s], 1);
     mbar_init(&done_bar, 1);
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&gdone[b], 1);
-      mbar_init(&acc_empty[b], G2CW);
-    }
+    for (int b = 0; b < 2; ++b) mbar_init(&gdone[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -336,48 +353,54 @@ __global__ void __launch_bounds__(G2T, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    // the whole warp runs the loop (named barriers are warp-aligned); one elected lane issues
+    const bool leader = elect_one();
+    {
       const int ngr = (nkb + G - 1) / G;
       for (int gi = 0; gi < ngr; ++gi) {
-        if (DRAIN && gi >= 2) mbar_wait(&acc_empty[gi & 1], ((gi >> 1) - 1) & 1);   // group gi-2 drained
+        if (DRAIN && gi >= 2) nbar_sync<kAllBar>(1 + S + (gi & 1));   // group gi-2 drained
         GT(7, 256 + gi);
         const uint32_t tm = DRAIN ? tmem + (uint32_t)((gi & 1) * BN) : tmem;
         const int kbe = min(nkb, gi * G + G);
         for (int kb = gi * G; kb < kbe; ++kb) {
           const int s = kb % S;
           const bool first = DRAIN ? (kb == gi * G) : (kb == 0);
-          mbar_wait(&conv_bar[s], (kb / S) & 1);
+          nbar_sync<kTeamBar>(1 + s);                          // k-block kb split (team kb & 1)
           GT(3, kb);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t st = su32(sm + s * Cfg::kStage);
-          const uint32_t ah = AMN ? st + Cfg::oAhi : st, bh = BMN ? st + Cfg::oBhi : st + Cfg::kA;
-          const uint32_t al = st + Cfg::oAlo, bl = st + Cfg::oBlo;
-          const uint32_t ta = tmem + (uint32_t)(kACol + 32 * s);   // this stage's A: hi at +0, lo at +16
-#pragma unroll
-          for (int kk = 0; kk < G2K / 8; ++kk) {   // K = 8 tf32 per MMA
-            const uint64_t dbh = kmajor_desc(bh, kk), dbl = kmajor_desc(bl, kk);
-            if (ATM) {
-              mma_tf32_ts<Cfg::kIdesc>(tm, ta + 8 * kk, dbl, !(first && kk == 0));        // hi.lo
-              mma_tf32_ts<Cfg::kIdesc>(tm, ta + 16 + 8 * kk, dbh, 1);                     // lo.hi
-              mma_tf32_ts<Cfg::kIdesc>(tm, ta + 8 * kk, dbh, 1);                          // hi.hi
-              continue;
+          if (leader) {
+            const uint32_t st = su32(sm + s * Cfg::kStage);
+            const uint32_t ah = AMN ? st + Cfg::oAhi : st, bh = BMN ? st + Cfg::oBhi : st + Cfg::kA;
+            const uint32_t al = st + Cfg::oAlo, bl = st + Cfg::oBlo;
+            const uint32_t ta = tmem + (uint32_t)(kACol + 32 * s);   // this stage's A: hi at +0, lo at +16
+  #pragma unroll
+            for (int kk = 0; kk < G2K / 8; ++kk) {   // K = 8 tf32 per MMA
+              const uint64_t dbh = kmajor_desc(bh, kk), dbl = kmajor_desc(bl, kk);
+              if (ATM) {
+                mma_tf32_ts<Cfg::kIdesc>(tm, ta + 8 * kk, dbl, !(first && kk == 0));        // hi.lo
+                mma_tf32_ts<Cfg::kIdesc>(tm, ta + 16 + 8 * kk, dbh, 1);                     // lo.hi
+                mma_tf32_ts<Cfg::kIdesc>(tm, ta + 8 * kk, dbh, 1);                          // hi.hi
+                continue;
+              }
+              const uint64_t dah = kmajor_desc(ah, kk), dal = kmajor_desc(al, kk);
+              if (LOWP) {   // bf16-rounded operands: one MMA
+                mma_tf32_i<Cfg::kIdesc>(tm, dah, dbh, !(first && kk == 0));
+                continue;
+              }
+              // small terms first: hi.lo, lo.hi, then hi.hi
+              mma_tf32_i<Cfg::kIdesc>(tm, dah, dbl, !(first && kk == 0));
+              mma_tf32_i<Cfg::kIdesc>(tm, dal, dbh, 1);
+              mma_tf32_i<Cfg::kIdesc>(tm, dah, dbh, 1);
             }
-            const uint64_t dah = kmajor_desc(ah, kk), dal = kmajor_desc(al, kk);
-            if (LOWP) {   // bf16-rounded operands: one MMA
-              mma_tf32_i<Cfg::kIdesc>(tm, dah, dbh, !(first && kk == 0));
-              continue;
-            }
-            // small terms first: hi.lo, lo.hi, then hi.hi
-            mma_tf32_i<Cfg::kIdesc>(tm, dah, dbl, !(first && kk == 0));
-            mma_tf32_i<Cfg::kIdesc>(tm, dal, dbh, 1);
-            mma_tf32_i<Cfg::kIdesc>(tm, dah, dbh, 1);
+            GT(4, kb);
           }
-          GT(4, kb);
+          __syncwarp();
         }
-        mma_commit(&gdone[gi & 1]);
+        if (leader) mma_commit(&gdone[gi & 1]);
+        __syncwarp();
         GT(6, 256 + gi);
       }
-      mma_commit(&done_bar);
+      if (leader) mma_commit(&done_bar);
     }
   } else {
     // ---- split (and transpose the MN-major operands)
@@ -413,62 +436,73 @@ __global__ void __launch_bounds__(G2T, 1)
         for (int j = 0; j < 32; ++j) acc[i][j] += __uint_as_float(r[j]);
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[c & 1]);
+      nbar_arrive<kAllBar>(1 + S + (c & 1));
       if (ct == 0) GT(7, c);
     };
-    for (int kb = 0; kb < nkb; ++kb) {
+    // two teams of four warps (one per TMEM lane quarter: warps 2-5 and 6-9) split alternate
+    // k-blocks (S is even: a stage always belongs to the same team), so one k-block's split
+    // latency chain (loads, tcgen05.st, fences) overlaps the other's
+    const int team = half, tct = ct - 128 * team;
+    const int ngr = (nkb + G - 1) / G;
+    int dn = 0;   // next group this thread drains (DRAIN)
+    for (int kb = team; kb < nkb; kb += 2) {
       const int s = kb % S;
       mbar_wait(&full_bar[s], (kb / S) & 1);
       if (ct == 0) GT(1, kb);
       uint8_t *st = sm + s * Cfg::kStage;
       if (ATM) {
-        // A: row r = 32 q + lane of the tile (this warp's TMEM lane quarter), k half `half`:
-        // 8 values -> hi = trunc_tf32(x), lo = rna_tf32(x - hi) -> two tcgen05.st of 8 columns
+        // A: row r = 32 q + lane of the tile (this warp's TMEM lane quarter), all 16 k:
+        // hi = trunc_tf32(x), lo = rna_tf32(x - hi) -> two tcgen05.st of 16 columns
         const int r = 32 * q + lane;
-        float v[8];
+        float v[16];
         if (!AMN) {
 #pragma unroll
-          for (int jj = 0; jj < 2; ++jj) {
-            const float4 x = *reinterpret_cast<const float4 *>(st + sw64_off(r, 2 * half + jj));
+          for (int jj = 0; jj < 4; ++jj) {
+            const float4 x = *reinterpret_cast<const float4 *>(st + sw64_off(r, jj));
             v[4 * jj + 0] = x.x; v[4 * jj + 1] = x.y; v[4 * jj + 2] = x.z; v[4 * jj + 3] = x.w;
           }
         } else {   // raw MN-major boxes [GBM / 32][16 k][32 rows]
           const float *src = reinterpret_cast<const float *>(st + (r >> 5) * 2048) + (r & 31);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) v[i] = src[(8 * half + i) * 32];
+          for (int i = 0; i < 16; ++i) v[i] = src[i * 32];
         }
-        uint32_t hb[8], lb[8];
+        uint32_t hb[16], lb[16];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < 16; ++i) {
           const uint32_t h = __float_as_uint(v[i]) & 0xFFFFE000u;
           hb[i] = h;
           lb[i] = __float_as_uint(rna_tf32(v[i] - __uint_as_float(h)));
         }
-        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(kACol + 32 * s + 8 * half);
-        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta),
-                     "r"(hb[0]), "r"(hb[1]), "r"(hb[2]), "r"(hb[3]), "r"(hb[4]), "r"(hb[5]), "r"(hb[6]), "r"(hb[7])
-                     : "memory");
-        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta + 16),
-                     "r"(lb[0]), "r"(lb[1]), "r"(lb[2]), "r"(lb[3]), "r"(lb[4]), "r"(lb[5]), "r"(lb[6]), "r"(lb[7])
-                     : "memory");
+        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(kACol + 32 * s);
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta),
+            "r"(hb[0]), "r"(hb[1]), "r"(hb[2]), "r"(hb[3]), "r"(hb[4]), "r"(hb[5]), "r"(hb[6]), "r"(hb[7]), "r"(hb[8]),
+            "r"(hb[9]), "r"(hb[10]), "r"(hb[11]), "r"(hb[12]), "r"(hb[13]), "r"(hb[14]), "r"(hb[15])
+            : "memory");
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta + 16),
+            "r"(lb[0]), "r"(lb[1]), "r"(lb[2]), "r"(lb[3]), "r"(lb[4]), "r"(lb[5]), "r"(lb[6]), "r"(lb[7]), "r"(lb[8]),
+            "r"(lb[9]), "r"(lb[10]), "r"(lb[11]), "r"(lb[12]), "r"(lb[13]), "r"(lb[14]), "r"(lb[15])
+            : "memory");
       } else {
-        split_op<AMN, GBM, LOWP>(st, st + Cfg::oAhi, st + Cfg::oAlo, ct);
+        split_op<AMN, GBM, LOWP>(st, st + Cfg::oAhi, st + Cfg::oAlo, tct, 128);
       }
-      split_op<BMN, BN, LOWP>(st + Cfg::kA, st + Cfg::oBhi, st + Cfg::oBlo, ct);
+      split_op<BMN, BN, LOWP>(st + Cfg::kA, st + Cfg::oBhi, st + Cfg::oBlo, tct, 128);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic stores -> tensor-core reads
       if (ATM) {
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&conv_bar[s]);
+      nbar_arrive<kTeamBar>(1 + s);
       if (ct == 0) GT(2, kb);
       if (ct == 32 * G2CW - 32) GT(5, kb);   // the last split warp
-      // DRAIN: once group c's operands are all split, the previous group is drained
-      if (DRAIN && (kb % G == G - 1 || kb == nkb - 1) && kb / G >= 1) drain(kb / G - 1);
+      // DRAIN: once this team has split its part of group c, group c - 1 is drained
+      if (DRAIN) {
+        const int gnext = kb + 2 < nkb ? (kb + 2) / G : ngr;
+        while (dn < gnext - 1) drain(dn++);
+      }
     }
-    if (DRAIN && nkb > 0) drain((nkb - 1) / G);
+    if (DRAIN) while (dn < ngr) drain(dn++);
     // ---- epilogue: TMEM -> registers (thread = accumulator row) -> per-warp 32 x 33 staging
     // tile in the (now idle) pipeline smem -> coalesced row stores (lane = column)
     mbar_wait(&done_bar, 0);
@@ -557,7 +591,7 @@ bool make_tmap(CUtensorMap *tm, const float *base, int rows, int K, int ld, int 
 
 template <int BN, bool AMN, bool BMN, bool DRAIN, bool LOWP = false>
 bool launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t st) {
-  using Cfg = G2Cfg<BN, AMN, BMN, !LOWP>;
+  using Cfg = G2Cfg<BN, AMN, BMN, !LOWP, DRAIN>;
   CUtensorMap ta, tb;
   if (!make_tmap(&ta, g0.A, g0.M, g0.K, g0.lda, GBM, AMN) || !make_tmap(&tb, g0.B, g0.N, g0.K, g0.ldb, BN, BMN))
     return false;

@@ -718,9 +718,11 @@ __global__ void __launch_bounds__(kBW * 32, 3) pair_bwd_union_box_kernel(ScoreAr
           const float2 W = make_float2(fmaf(a.alpha, ax < ox ? 1.f : 0.f, ax > ox ? 1.f : 0.f),
                                        fmaf(a.alpha, ay < oy ? 1.f : 0.f, ay > oy ? 1.f : 0.f));
           const float2 cw = __fmul2_rn(cf, W);
-          const float2 cg = make_float2(
-              t.x == 0.f ? 0.f : __int_as_float(__float_as_int(cw.x) ^ (__float_as_int(t.x) & 0x80000000)),
-              t.y == 0.f ? 0.f : __int_as_float(__float_as_int(cw.y) ^ (__float_as_int(t.y) & 0x80000000)));
+          // sign(t) cw with 0 at t = 0 (A19): sign transfer (LOP3) x a 0/1 factor on the FMA
+          // pipe instead of a select (this loop's ALU pipe also carries the disjunct selects)
+          const float2 csg = make_float2(__int_as_float(__float_as_int(cw.x) ^ (__float_as_int(t.x) & 0x80000000)),
+                                         __int_as_float(__float_as_int(cw.y) ^ (__float_as_int(t.y) & 0x80000000)));
+          const float2 cg = __fmul2_rn(csg, make_float2(t.x != 0.f ? 1.f : 0.f, t.y != 0.f ? 1.f : 0.f));
           gA0 = __ffma2_rn(cg, nt, gA0);
           gB0 = __ffma2_rn(cg, tf, gB0);
           gA1 = __ffma2_rn(cw, nt, gA1);
