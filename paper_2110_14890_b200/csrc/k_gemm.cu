@@ -280,7 +280,8 @@ namespace kg {
 #endif
 template <int BN, bool AMN, bool BMN, bool DRAIN, bool LOWP = false>
 __global__ void __launch_bounds__(G2T, 1)
-    gemm_tf32x3_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
+    gemm_tf32x3_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                           const __grid_constant__ CUtensorMap tmBl, GemmArgs g) {
   KG_GRID_DEP_WAIT();
   using Cfg = G2Cfg<BN, AMN, BMN, !LOWP, DRAIN>;
   constexpr int S = Cfg::kStages, G = Cfg::kGroup;
@@ -315,6 +316,7 @@ __global__ void __launch_bounds__(G2T, 1)
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * BN;
+  const bool bpre = !BMN && !LOWP && g.B_lo != nullptr;   // B's lo plane comes from global memory
   const int nkb_all = (g.K + G2K - 1) / G2K;
   const int kb0 = blockIdx.z * g.kbs, nkb = min(nkb_all, kb0 + g.kbs) - kb0;   // split-K range
 
@@ -326,6 +328,7 @@ __global__ void __launch_bounds__(G2T, 1)
   if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    if (bpre) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmBl)) : "memory");
     for (int s = 0; s < S; ++s) mbar_init(&full_bar[s], 1);
     mbar_init(&done_bar, 1);
     for (int b = 0; b < 2; ++b) mbar_init(&gdone[b], 1);
@@ -345,10 +348,11 @@ __global__ void __launch_bounds__(G2T, 1)
           mbar_wait(&gdone[gw & 1], (gw >> 1) & 1);
         }
         uint8_t *st = sm + s * Cfg::kStage;
-        mbar_expect_tx(&full_bar[s], Cfg::kA + Cfg::kB);
+        mbar_expect_tx(&full_bar[s], Cfg::kA + Cfg::kB + (bpre ? Cfg::kB : 0));
         const int k0 = (kb0 + kb) * G2K;
         load_op<AMN, GBM>(&tmA, &full_bar[s], st, m0, k0);
         load_op<BMN, BN>(&tmB, &full_bar[s], st + Cfg::kA, n0, k0);
+        if (bpre) load_op<false, BN>(&tmBl, &full_bar[s], st + Cfg::oBlo, n0, k0);   // B's lo plane
         GT(0, kb);
       }
     }
@@ -487,7 +491,7 @@ __global__ void __launch_bounds__(G2T, 1)
       } else {
         split_op<AMN, GBM, LOWP>(st, st + Cfg::oAhi, st + Cfg::oAlo, tct, 128);
       }
-      split_op<BMN, BN, LOWP>(st + Cfg::kA, st + Cfg::oBhi, st + Cfg::oBlo, tct, 128);
+      if (!bpre) split_op<BMN, BN, LOWP>(st + Cfg::kA, st + Cfg::oBhi, st + Cfg::oBlo, tct, 128);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic stores -> tensor-core reads
       if (ATM) {
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -559,6 +563,43 @@ __global__ void __launch_bounds__(G2T, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
 }
 
+// Pre-split weights (B operands): for W [R][C], lo = rna_tf32(W - trunc_tf32(W)) in W's layout,
+// and the transposed pair WT = W^T [C][R], WT_lo = lo^T (the backward's dX = dY W reads W as a
+// K-major [in][out] operand).  32 x 32 tiles through shared memory; one launch for all jobs.
+__global__ void wsplit_kernel(WSplitJobs J, int part) {   // part 0: lo; 1: t, tlo
+  KG_GRID_DEP_WAIT();
+  const WSplitJob &jb = J.j[blockIdx.z];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  if (r0 >= jb.R || c0 >= jb.C) return;
+  __shared__ float th[32][33], tl[32][33];
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    const int r = r0 + y, c = c0 + threadIdx.x;
+    if (r < jb.R && c < jb.C) {
+      const float x = jb.w[(int64_t)r * jb.C + c];
+      const float l = rna_tf32(x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u));
+      if (part == 0) jb.lo[(int64_t)r * jb.C + c] = l;
+      th[y][threadIdx.x] = x;
+      tl[y][threadIdx.x] = l;
+    }
+  }
+  if (part == 0) return;
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    const int c = c0 + y, r = r0 + threadIdx.x;
+    if (c < jb.C && r < jb.R) {
+      jb.t[(int64_t)c * jb.R + r] = th[threadIdx.x][y];
+      jb.tlo[(int64_t)c * jb.R + r] = tl[threadIdx.x][y];
+    }
+  }
+}
+void launch_wsplit(const WSplitJobs &J, int part, cudaStream_t st) {
+  if (J.n <= 0) return;
+  int mr = 0, mc = 0;
+  for (int i = 0; i < J.n; ++i) { mr = std::max(mr, J.j[i].R); mc = std::max(mc, J.j[i].C); }
+  dim3 grid((mc + 31) / 32, (mr + 31) / 32, J.n), block(32, 8);
+  { wsplit_kernel<<<grid, block, 0, st>>>(J, part); ++g_launches; }
+}
+
 namespace {
 PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   // resolved once; a function-local static is initialised thread-safely (with a plain
@@ -592,9 +633,14 @@ bool make_tmap(CUtensorMap *tm, const float *base, int rows, int K, int ld, int 
 template <int BN, bool AMN, bool BMN, bool DRAIN, bool LOWP = false>
 bool launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t st) {
   using Cfg = G2Cfg<BN, AMN, BMN, !LOWP, DRAIN>;
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tbl;
   if (!make_tmap(&ta, g0.A, g0.M, g0.K, g0.lda, GBM, AMN) || !make_tmap(&tb, g0.B, g0.N, g0.K, g0.ldb, BN, BMN))
     return false;
+  if (g0.B_lo && !BMN && !LOWP) {
+    if (!make_tmap(&tbl, g0.B_lo, g0.N, g0.K, g0.ldb, BN, false)) return false;
+  } else {
+    tbl = tb;
+  }
   static const bool configured =   // thread-safe one-time attribute (concurrent host threads)
       cudaFuncSetAttribute(gemm_tf32x3_tma_kernel<BN, AMN, BMN, DRAIN, LOWP>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) == cudaSuccess;
@@ -610,7 +656,7 @@ bool launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t s
   splits = (nkb + g.kbs - 1) / g.kbs;
   g.P = splits > 1 ? part : nullptr;
   dim3 grid((g.N + BN - 1) / BN, (g.M + GBM - 1) / GBM, splits);
-  { gemm_tf32x3_tma_kernel<BN, AMN, BMN, DRAIN, LOWP><<<grid, G2T, Cfg::kSmem, st>>>(ta, tb, g); ++g_launches; }
+  { gemm_tf32x3_tma_kernel<BN, AMN, BMN, DRAIN, LOWP><<<grid, G2T, Cfg::kSmem, st>>>(ta, tb, tbl, g); ++g_launches; }
   if (splits > 1) {
     const int64_t n = (int64_t)g.M * g.N;
     { gemm_reduce_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(part, splits, g.M, g.N, g.C, g.ldc, g.bias, g.relu,
@@ -629,7 +675,8 @@ bool launch_v2_any(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_
 
 bool gemm_tc_accepts(const GemmArgs &g) {
   return g.M > 0 && g.N > 0 && g.K > 0 && !(reinterpret_cast<uintptr_t>(g.A) & 15) &&
-         !(reinterpret_cast<uintptr_t>(g.B) & 15) && !(g.lda & 3) && !(g.ldb & 3) && tmap_encoder() != nullptr;
+         !(reinterpret_cast<uintptr_t>(g.B) & 15) && !(reinterpret_cast<uintptr_t>(g.B_lo) & 15) &&
+         !(g.B_lo && g.b_mn) && !(g.lda & 3) && !(g.ldb & 3) && tmap_encoder() != nullptr;
 }
 
 // C = beta C + op(A) op(B)^T (+ bias) (ReLU) on the tensor cores.  A is [M][K] (a_mn: [K][M]),

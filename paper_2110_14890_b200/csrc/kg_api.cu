@@ -493,6 +493,12 @@ struct kg_handle {
   float *OG = nullptr, *RG = nullptr, *RGU = nullptr, *Gc = nullptr, *gdense = nullptr, *PS = nullptr, *PSr = nullptr;
   int32_t *pcnt = nullptr, *ocnt = nullptr, *sinv = nullptr, *osinv = nullptr, *hrow = nullptr,
           *ohrow = nullptr;
+  // pre-split weight planes of the MLP weights used as GEMM B operands (refreshed at the start of
+  // every DAG forward, on a side stream): lo (W's layout), t = W^T, tlo = lo^T
+  struct WPlanes { std::string name; float *lo = nullptr, *t = nullptr, *tlo = nullptr; };
+  std::vector<WPlanes> wpl;
+  cudaEvent_t ev_wsplit = nullptr, ev_wsplit_t = nullptr;   // lo planes / transposed planes refreshed
+  bool wsplit_issued = false;                               // this step's transposed planes are on their way
   float *Q = nullptr, *dQ = nullptr, *C = nullptr, *Dmin = nullptr, *Dpos = nullptr, *loss_part = nullptr,
         *loss_pos = nullptr;
   float *F = nullptr, *Cv = nullptr, *QP = nullptr, *Cq = nullptr;
@@ -647,6 +653,16 @@ const Seg *seg_of(const kg_handle *h, const char *name) {
   return nullptr;
 }
 float *dp(kg_handle *h, const char *name) { return h->t.dense + seg_of(h, name)->off; }
+const kg_handle::WPlanes *wplanes(const kg_handle *h, const char *name) {
+  for (auto &w : h->wpl)
+    if (w.name == name) return &w;
+  return nullptr;
+}
+// forward operand: B = W [out][in] (K-major) with its lo plane
+const float *wlo(const kg_handle *h, const char *name) { const auto *w = wplanes(h, name); return w ? w->lo : nullptr; }
+// backward operand of dX = dY W: W^T [in][out] (K-major, ld = out) and its lo plane
+const float *wt(const kg_handle *h, const char *name) { return wplanes(h, name)->t; }
+const float *wtlo(const kg_handle *h, const char *name) { return wplanes(h, name)->tlo; }
 float *gp(kg_handle *h, const char *name) { return h->gdense + (seg_of(h, name)->off - h->w_off); }
 
 void carve(kg_handle *h, Arena &A) {
@@ -753,6 +769,21 @@ void carve(kg_handle *h, Arena &A) {
     h->gsP = A.take<float>(h->gsP_cap);
     h->gsP2 = A.take<float>(h->gsP_cap);
   }
+  {
+    static const char *kWNames[] = {"prj_W1", "prj_W2", "prj_W0", "ds_W1", "ds_W2", "off_W1", "off_W2",
+                                    "att_W1", "att_W2", "att_U1", "att_U2"};
+    h->wpl.clear();
+    for (const char *n : kWNames) {
+      const Seg *sg = seg_of(h, n);
+      if (!sg) continue;
+      kg_handle::WPlanes w;
+      w.name = n;
+      w.lo = A.take<float>(sg->n);
+      w.t = A.take<float>(sg->n);
+      w.tlo = A.take<float>(sg->n);
+      h->wpl.push_back(w);
+    }
+  }
   if (h->world > 1) {
     const int64_t GL = (int64_t)h->world * h->Lx;
     // fixed-capacity exchange buckets: twice the mean share of distinct ids per
@@ -788,7 +819,8 @@ void carve(kg_handle *h, Arena &A) {
 // Every contraction of the DAG runs on the tcgen05 3xTF32 kernel (k_gemm.cu; drained
 // accumulation, see kg_create); the side stream has its own split-K scratch.
 kg_status gemm(kg_handle *h, bool ta, bool tb, int m, int n, int k, const float *A, int lda, const float *B, int ldb,
-               float beta, float *C, int ldc, const float *bias = nullptr, int relu = 0, float alpha = 1.f) {
+               float beta, float *C, int ldc, const float *bias = nullptr, int relu = 0, float alpha = 1.f,
+               const float *B_lo = nullptr, bool tb_t = false) {
   if (m <= 0 || n <= 0) return KG_OK;
   // the tensor-core kernel reads either operand layout directly ([k][m] / [k][n] = MN-major)
   GemmArgs g;
@@ -796,6 +828,8 @@ kg_status gemm(kg_handle *h, bool ta, bool tb, int m, int n, int k, const float 
   g.bias = bias; g.relu = relu; g.a_mn = ta; g.b_mn = !tb; g.drain = h->gemm_drain && !h->gemm_lowp;
   g.lowp = h->gemm_lowp;
   g.alpha = alpha;
+  if (B_lo) CK(cudaStreamWaitEvent(h->st, tb_t ? h->ev_wsplit_t : h->ev_wsplit, 0));   // this step's planes (st3)
+  g.B_lo = B_lo;
   if (k <= 0 || !launch_gemm_tc(g, h->side ? h->gsP2 : h->gsP, h->gsP_cap, h->st))
     return fail(h, KG_EUNSUPPORTED, "tensor-core GEMM: operands must be 16-byte aligned with ld % 4 == 0 and K > 0 "
                                     "(and cuTensorMapEncodeTiled available)");
@@ -884,6 +918,25 @@ struct StepBufs {
 };
 
 // -------------------------------------------------------------- forward DAG
+// The transposed pre-split planes of the MLP weights (W^T and its lo plane, the K-major B
+// operand of the backward's dX = dY W): one launch per step, issued where it interferes least --
+// at the start of a local step on the low-priority stream (st4, concurrent with the gathers and
+// the DAG forward), else on st3 at the start of the DAG backward.  The dX GEMMs wait ev_wsplit_t.
+bool needs_wplanes(const kg_handle *h, const Plan &p) { return !h->wpl.empty() && (h->kind == KG_BETAE || p.inter >= 0); }
+kg_status issue_wplanes(kg_handle *h, cudaStream_t from, cudaStream_t on) {
+  WSplitJobs J;
+  for (auto &w : h->wpl) {
+    const Seg *sg = seg_of(h, w.name.c_str());
+    J.j[J.n++] = WSplitJob{h->t.dense + sg->off, w.lo, w.t, w.tlo, sg->rows, sg->cols};
+  }
+  kg_status fs = fork(h, from, on);
+  if (fs) return fs;
+  launch_wsplit(J, 1, on);
+  CK(cudaEventRecord(h->ev_wsplit_t, on));
+  h->wsplit_issued = true;
+  return KG_OK;
+}
+
 kg_status dag_forward(kg_handle *h, StepBufs &S) {
   const Plan &p = S.plan;
   const int M = S.M, d = h->d, dq = h->dq, m = h->m, HH = h->H;
@@ -904,7 +957,7 @@ kg_status dag_forward(kg_handle *h, StepBufs &S) {
       }
       G(false, true, GM, HH, 2 * d, X, 2 * d, dp(h, "prj_W1"), 2 * d, 0.f, H1, HH, dp(h, "prj_b1"), 1);
       G(false, true, GM, HH, HH, H1, HH, dp(h, "prj_W2"), HH, 0.f, H2, HH, dp(h, "prj_b2"), 1);
-      G(false, true, GM, d, HH, H2, HH, dp(h, "prj_W0"), HH, 0.f, h->pZ, d);
+      G(false, true, GM, d, HH, H2, HH, dp(h, "prj_W0"), HH, 0.f, h->pZ, d, nullptr, 0);
       for (int k = ni; k < nj; ++k)
         launch_betae_proj_out(h->pZ + (int64_t)(k - ni) * M * d, dp(h, "prj_b0"), M, d,
                               h->pZp1 + (int64_t)(u + k - ni) * M * d, S.val[k], st);
@@ -964,6 +1017,11 @@ kg_status dag_forward(kg_handle *h, StepBufs &S) {
 // -------------------------------------------------------------- backward DAG
 kg_status dag_backward(kg_handle *h, StepBufs &S) {
   const Plan &p = S.plan;
+  if (needs_wplanes(h, p) && !h->wsplit_issued) {
+    kg_status ws = issue_wplanes(h, h->st, h->st3);
+    if (ws) return ws;
+  }
+  h->wsplit_issued = false;   // consumed by this backward (the next step issues its own)
   const int M = S.M, d = h->d, dq = h->dq, m = h->m, HH = h->H;
   cudaStream_t st = h->st;
   const float *ent = h->ent_src;
@@ -979,11 +1037,11 @@ kg_status dag_backward(kg_handle *h, StepBufs &S) {
             *dH1 = h->pdH1 + (int64_t)u0 * M * HH;
       for (int k = n0; k <= ni; ++k)
         launch_betae_proj_dz(S.grad[k], h->pZp1 + (int64_t)use[k] * M * d, M, d, h->pdZ + (int64_t)use[k] * M * d, st);
-      G(false, false, GM, HH, d, dZ, d, dp(h, "prj_W0"), HH, 0.f, dH2, HH);
+      G(false, true, GM, HH, d, dZ, d, wt(h, "prj_W0"), d, 0.f, dH2, HH, nullptr, 0, 1.f, wtlo(h, "prj_W0"), true);
       launch_relu_mask(dH2, h->pH2 + (int64_t)u0 * M * HH, GM, HH, st);
-      G(false, false, GM, HH, HH, dH2, HH, dp(h, "prj_W2"), HH, 0.f, dH1, HH);
+      G(false, true, GM, HH, HH, dH2, HH, wt(h, "prj_W2"), HH, 0.f, dH1, HH, nullptr, 0, 1.f, wtlo(h, "prj_W2"), true);
       launch_relu_mask(dH1, h->pH1 + (int64_t)u0 * M * HH, GM, HH, st);
-      G(false, false, GM, 2 * d, HH, dH1, HH, dp(h, "prj_W1"), 2 * d, 0.f, h->pdX, 2 * d);
+      G(false, true, GM, 2 * d, HH, dH1, HH, wt(h, "prj_W1"), HH, 0.f, h->pdX, 2 * d, nullptr, 0, 1.f, wtlo(h, "prj_W1"), true);
       for (int k = n0; k <= ni; ++k) {
         const PNode &nk = p.n[k];
         const int64_t *arows = nk.in < 0 ? h->rows + (int64_t)nk.anchor * M : nullptr;
@@ -1020,13 +1078,13 @@ kg_status dag_backward(kg_handle *h, StepBufs &S) {
       if (h->deepset) {
         // T0 = H, T1 = Mn (forward);  T7 = dMn, T8 = dH
         if (h->qnorm) launch_qnorm_bwd(S.grad[ni], S.val[ni], M, d, h->qnorm, h->qn + (int64_t)ni * 2 * h->Mx, st);
-        G(false, false, M, d, d, gout, d, dp(h, "ds_W2"), d, 0.f, T[7], d);
+        G(false, true, M, d, d, gout, d, wt(h, "ds_W2"), d, 0.f, T[7], d, nullptr, 0, 1.f, wtlo(h, "ds_W2"), true);
         G(true, false, d, d, M, gout, d, T[1], d, 0.f, gp(h, "ds_W2"), d);
         launch_colsum(gout, M, d, d, gp(h, "ds_b2"), st);
         launch_gqe_inter_dh(T[7], T[0], n, M, d, T[8], st);
         G(true, false, d, d, NR, T[8], d, h->stack_v, d, 0.f, gp(h, "ds_W1"), d);
         launch_colsum(T[8], NR, d, d, gp(h, "ds_b1"), st);
-        G(false, false, NR, d, d, T[8], d, dp(h, "ds_W1"), d, 0.f, h->stack_g, d);
+        G(false, true, NR, d, d, T[8], d, wt(h, "ds_W1"), d, 0.f, h->stack_g, d, nullptr, 0, 1.f, wtlo(h, "ds_W1"), true);
       } else if (h->kind == KG_Q2B) {
         // forward: T0 Hc, T1 Lg, T2 a, T3 Ho, T4 Mo, T5 Z, T6 sig.  backward: T7 dLg, T8 dHc, T9 dZ, T10 dMo, T11 dHo
         // offset branch on the second stream (writes the offset half of stack_g only)
@@ -1036,33 +1094,33 @@ kg_status dag_backward(kg_handle *h, StepBufs &S) {
           OnStream os(h, h->st3);
           cudaStream_t s3 = h->st3;
           launch_q2b_off_bwd(h->stack_v, T[6], h->amin, gout, n, M, d, T[9], h->stack_g, s3);
-          G(false, false, M, d, d, T[9], d, dp(h, "off_W2"), d, 0.f, T[10], d);
+          G(false, true, M, d, d, T[9], d, wt(h, "off_W2"), d, 0.f, T[10], d, nullptr, 0, 1.f, wtlo(h, "off_W2"), true);
           G(true, false, d, d, M, T[9], d, T[4], d, 0.f, gp(h, "off_W2"), d);
           launch_colsum(T[9], M, d, d, gp(h, "off_b2"), s3);
           launch_gqe_inter_dh(T[10], T[3], n, M, d, T[11], s3);
           G(true, false, d, d, NR, T[11], d, h->stack_v + d, 2 * d, 0.f, gp(h, "off_W1"), d);
           launch_colsum(T[11], NR, d, d, gp(h, "off_b1"), s3);
-          G(false, false, NR, d, d, T[11], d, dp(h, "off_W1"), d, 1.f, h->stack_g + d, 2 * d);
+          G(false, true, NR, d, d, T[11], d, wt(h, "off_W1"), d, 1.f, h->stack_g + d, 2 * d, nullptr, 0, 1.f, wtlo(h, "off_W1"), true);
         }
         launch_q2b_att_bwd(h->stack_v, T[2], gout, n, M, d, T[7], h->stack_g, st);
-        G(false, false, NR, d, d, T[7], d, dp(h, "att_W2"), d, 0.f, T[8], d);
+        G(false, true, NR, d, d, T[7], d, wt(h, "att_W2"), d, 0.f, T[8], d, nullptr, 0, 1.f, wtlo(h, "att_W2"), true);
         launch_relu_mask(T[8], T[0], NR, d, st);
         G(true, false, d, d, NR, T[7], d, T[0], d, 0.f, gp(h, "att_W2"), d);
         launch_colsum(T[7], NR, d, d, gp(h, "att_b2"), st);
         G(true, false, d, d, NR, T[8], d, h->stack_v, 2 * d, 0.f, gp(h, "att_W1"), d);
         launch_colsum(T[8], NR, d, d, gp(h, "att_b1"), st);
-        G(false, false, NR, d, d, T[8], d, dp(h, "att_W1"), d, 1.f, h->stack_g, 2 * d);
+        G(false, true, NR, d, d, T[8], d, wt(h, "att_W1"), d, 1.f, h->stack_g, 2 * d, nullptr, 0, 1.f, wtlo(h, "att_W1"), true);
         if ((fs = join(h, h->st3, st)) != KG_OK) return fs;
       } else if (h->kind == KG_BETAE) {
         // forward: T0 Hs, T1 Lg, T2 w.  backward: T7 dLg, T8 dHs
         launch_beta_att_bwd(h->stack_v, T[2], gout, n, M, d, T[7], h->stack_g, st);
-        G(false, false, NR, d, m, T[7], m, dp(h, "att_U2"), d, 0.f, T[8], d);
+        G(false, true, NR, d, m, T[7], m, wt(h, "att_U2"), m, 0.f, T[8], d, nullptr, 0, 1.f, wtlo(h, "att_U2"), true);
         launch_relu_mask(T[8], T[0], NR, d, st);
         G(true, false, m, d, NR, T[7], m, T[0], d, 0.f, gp(h, "att_U2"), d);
         launch_colsum(T[7], NR, m, m, gp(h, "att_c2"), st);
         G(true, false, d, d, NR, T[8], d, h->stack_v, d, 0.f, gp(h, "att_U1"), d);
         launch_colsum(T[8], NR, d, d, gp(h, "att_c1"), st);
-        G(false, false, NR, d, d, T[8], d, dp(h, "att_U1"), d, 1.f, h->stack_g, d);
+        G(false, true, NR, d, d, T[8], d, wt(h, "att_U1"), d, 1.f, h->stack_g, d, nullptr, 0, 1.f, wtlo(h, "att_U1"), true);
       }
     }
   }
@@ -1372,7 +1430,9 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
       cudaEventCreateWithFlags(&h->ev_i2, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork2, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
+      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_wsplit, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_wsplit_t, cudaEventDisableTiming) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
   if (c.world > 1) {
     ncclUniqueId id;
     std::memcpy(&id, c.nccl_id, sizeof(id));
@@ -1553,6 +1613,7 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
       if (p.n[ni].type == 0) sl.s[u++] = p.n[ni].rel;
   }
   launch_rel_occ(h->b_rels, M, nr, sl, p.nproj, h->R, h->rocc, h->flags + 1, st);
+  if (needs_wplanes(h, p) && (s = issue_wplanes(h, st, h->st4)) != KG_OK) return s;
   CK(cudaEventRecord(h->ev_fork, st));
   CK(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
   launch_dedup(h->ids, nullptr, L, h->ent_bits, h->uniq, h->inv, h->perm, h->seg, h->Udev, h->st2, h->sinv, h->hrow);

@@ -106,7 +106,13 @@ struct GemmArgs {
   bool drain = false;   // fp32-accurate accumulation: TMEM chunks of kDrainKB k-blocks summed in registers
   bool lowp = false;    // bf16 score mode: operands rounded to bf16, one MMA per K-step (no 3xTF32 split)
   int force = 0;        // tile experiments (kg_test_gemm): bit 0 no split-K; bits 1-2 BN 1:64 2:128 3:160
+  // pre-split B (K-major only): B_lo = rna_tf32(B - trunc_tf32(B)) in B's layout; the kernel
+  // loads it with TMA instead of splitting B in shared memory (weights: kg_api.cu wsplit)
+  const float *B_lo = nullptr;
 };
+struct WSplitJob { const float *w; float *lo, *t, *tlo; int R, C; };
+struct WSplitJobs { WSplitJob j[12]; int n = 0; };
+void launch_wsplit(const WSplitJobs &J, int part, cudaStream_t st);   // pre-split weight planes: 0 lo, 1 t + tlo
 bool gemm_tc_accepts(const GemmArgs &g);   // 16-byte aligned operands, ld % 4 == 0
 bool launch_gemm_tc(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st);   // false: not launched
 void launch_transpose(const float *in, int R, int Cc, int ld_in, float *out, int ld_out, cudaStream_t st);
