@@ -29,8 +29,11 @@ ReLU moves a whole row of dW by a few percent.  So the batch is conditioned: que
 fp64 pre-activations or argmin gaps sit within 2e-6 of the magnitude of the sum that
 produced them are re-drawn (same recipe, same pool), see well_conditioned_batch.
 """
+import contextlib
+
 import numpy as np
 import pytest
+import torch
 
 import kggen
 import oracle
@@ -151,6 +154,130 @@ def q2b_flip_allowance(cfg, table, b, M, K, rel=1e-6):
     return allow_rows, allow_dense, n_terms
 
 
+@contextlib.contextmanager
+def _decision_hooks(rec):
+    """Test-side hooks on the oracle's forward (no arithmetic change): every traced decision --
+    a ReLU pre-activation, the BetaE projection clamp, a Q2B offset-min gap -- is recorded in
+    call order as [margin, scale, post, kind] with the margin NOT detached and, for ReLU / clamp,
+    the tensor the decision produced (post), so a per-query re-run can differentiate both."""
+    import oracle.model as OM
+    saved = (OM._trace, OM._relu_lin, OM.project, OM.TRACE)
+
+    def tr(margin, scale):
+        rec.append([margin, scale, None, "gap"])
+
+    def rl(x, W, b_):
+        z = OM._linear(x, W, b_)
+        rec.append([z, x.abs() @ W.abs().T + b_.abs(), None, "relu"])
+        out = torch.relu(z)
+        if out.requires_grad:
+            out.retain_grad()
+        rec[-1][2] = out
+        return out
+
+    def pj(kind, q, r, P):
+        out = saved[2](kind, q, r, P)
+        if kind == "betae":              # project's last record is its clamp's margin
+            rec[-1][3] = "clamp"
+            if out.requires_grad:
+                out.retain_grad()
+            rec[-1][2] = out
+        return out
+
+    OM._trace, OM._relu_lin, OM.project, OM.TRACE = tr, rl, pj, []
+    try:
+        yield
+    finally:
+        OM._trace, OM._relu_lin, OM.project, OM.TRACE = saved
+
+
+def traced_flip_allowance(cfg, table, b, M, K, rel=2e-6):
+    """Per-element allowance for the forward's traced decisions taken on computed values (DESIGN.md
+    reading A28): a ReLU pre-activation or the BetaE projection clamp within rel x the magnitude
+    of the sum that produced it may fall the other way in fp32.  The value it produces moves by
+    at most that margin (continuous), but the gradient through it switches between passing and
+    blocking dL/d(post): the adjoint jump is |dL_i/d post| of the query's own loss term, and its
+    effect on every parameter is |dL_i/d post| x |d margin / d theta|, one vector-Jacobian product
+    per flagged (query, decision, unit) on the query's own DAG.  Q2B offset-min near-ties are not
+    covered here (their queries are re-drawn).  Returns (allow_rows [len(uniq), d], allow_dense,
+    number of flagged decisions)."""
+    import oracle.model as OM
+    d = cfg.dim
+    na = kggen.N_ANCHORS[b["structure"]]
+    ids = np.concatenate([b["anchors"].reshape(-1), b["answers"], b["negatives"]])
+    uniq, inv = oracle.dedup(ids)
+    X = torch.tensor(table.get(uniq)[0], dtype=torch.float64)
+    theta = torch.tensor(table.dense, dtype=torch.float64)
+    P = OM.dense_views(cfg, theta)
+    ia = inv[:M * na].reshape(M, na)
+    rels = [torch.as_tensor(b["relations"][:, s].astype(np.int64)) for s in range(b["relations"].shape[1])]
+    rec = []
+    with torch.no_grad(), _decision_hooks(rec):
+        OM.query_disjuncts(b["structure"], cfg.kind, [X[torch.as_tensor(ia[:, a])] for a in range(na)], rels, P)
+    flagged = {}   # query -> [(record index, index into the query's own tensor)]
+    for k, (margin, scale, _, kind) in enumerate(rec):
+        if kind == "gap":
+            continue
+        near = (margin.abs() <= rel * scale).numpy()
+        for idx in zip(*np.nonzero(near)):
+            if near.ndim == 2:          # [M, units]
+                i, qidx = int(idx[0]), (0, int(idx[1]))
+            else:                       # [n, M, units] (intersection inputs stacked)
+                i, qidx = int(idx[1]), (int(idx[0]), 0, int(idx[2]))
+            flagged.setdefault(i, []).append((k, qidx))
+    offs, total = kggen.dense_offsets(cfg)
+    allow_rows, allow_dense = np.zeros((len(uniq), d)), np.zeros(total)
+    rel_names = [n for n in offs if n.startswith("rel")]
+    wnames = [n for n in offs if not n.startswith("rel")]
+    bits = kggen.unpack_mask(b["mask"], K)
+    vpos_all = X[torch.as_tensor(inv[M * na:M * na + M])]
+    vneg = X[torch.as_tensor(inv[M * na + M:])]
+    g = cfg.gamma
+    sp = lambda z: torch.nn.functional.softplus(z)  # noqa: E731
+    n_flag = 0
+    for i, items in flagged.items():
+        rid = b["relations"][i].astype(np.int64)
+        ur, rinv = np.unique(rid, return_inverse=True)
+        leaves_a = [X[ia[i, a]].clone().view(1, d).requires_grad_(True) for a in range(na)]
+        Pi = {n: P[n].detach().clone().requires_grad_(True) for n in wnames}
+        leaves_r = {n: P[n][torch.as_tensor(ur)].detach().clone().requires_grad_(True) for n in rel_names}
+        Pi.update(leaves_r)
+        rels_i = [torch.as_tensor([int(rinv[s])]) for s in range(len(rid))]
+        rq = []
+        with _decision_hooks(rq):
+            qs = OM.query_disjuncts(b["structure"], cfg.kind, leaves_a, rels_i, Pi)
+        dp = torch.stack([OM.distance(cfg.kind, q, vpos_all[i:i + 1], cfg.box_alpha) for q in qs]).min(dim=0).values
+        dn = torch.stack([OM.distance(cfg.kind, q[:, None, :], vneg[None], cfg.box_alpha) for q in qs]).min(dim=0).values
+        mb = torch.as_tensor(bits[i], dtype=torch.float64)
+        n_i = float(bits[i].sum())
+        li = sp(dp - g).sum() + ((mb * sp(g - dn[0])).sum() / n_i if n_i > 0 else 0.0)
+        li = li / M
+        li.backward(retain_graph=True)
+        leaves = leaves_a + [leaves_r[n] for n in rel_names] + [Pi[n] for n in wnames]
+        for k, qidx in items:
+            margin, _, post, _ = rq[k]
+            if post is None or post.grad is None:
+                continue
+            jump = float(post.grad[qidx].abs())
+            if jump == 0.0:
+                continue
+            n_flag += 1
+            gr = torch.autograd.grad(margin[qidx], leaves, retain_graph=True, allow_unused=True)
+            for a in range(na):
+                if gr[a] is not None:
+                    allow_rows[ia[i, a]] += jump * gr[a].abs().numpy()[0]
+            for n, gg in zip(rel_names, gr[na:na + len(rel_names)]):
+                if gg is not None:
+                    o0, shape = offs[n]
+                    for r_, row in enumerate(ur):
+                        allow_dense[o0 + row * shape[1]:o0 + (row + 1) * shape[1]] += jump * gg[r_].abs().numpy()
+            for n, gg in zip(wnames, gr[na + len(rel_names):]):
+                if gg is not None:
+                    o0, shape = offs[n]
+                    allow_dense[o0:o0 + gg.numel()] += jump * gg.abs().reshape(-1).numpy()
+    return allow_rows, allow_dense, n_flag
+
+
 def oracle_forward(cfg, table, b, M, K, trace=False):
     """Oracle (fp64) forward of a batch: per-disjunct D+ [n, M], D [n, M, K], and the trace of
     the discrete decisions taken on computed values (oracle.model.TRACE) if asked."""
@@ -185,22 +312,42 @@ def _near(x, y):
     return (x != y) & (np.abs(x - y) <= 1e-5 * (np.abs(x) + np.abs(y)))
 
 
-def well_conditioned_batch(cfg, table, structure, M, K, seed):
-    """A batch whose discrete decisions are well away from fp32 rounding (reading A28).
+def _decision_kinds(cfg, table, b, M):
+    """The kind ("relu" / "clamp" / "gap") of every traced decision of the batch, in call order."""
+    import oracle.model as OM
+    na = kggen.N_ANCHORS[b["structure"]]
+    ids = np.concatenate([b["anchors"].reshape(-1), b["answers"], b["negatives"]])
+    uniq, inv = oracle.dedup(ids)
+    X = torch.tensor(table.get(uniq)[0], dtype=torch.float64)
+    P = OM.dense_views(cfg, torch.tensor(table.dense, dtype=torch.float64))
+    ia = inv[:M * na].reshape(M, na)
+    rels = [torch.as_tensor(b["relations"][:, s].astype(np.int64)) for s in range(b["relations"].shape[1])]
+    rec = []
+    with torch.no_grad(), _decision_hooks(rec):
+        OM.query_disjuncts(b["structure"], cfg.kind, [X[torch.as_tensor(ia[:, a])] for a in range(na)], rels, P)
+    return [r[3] for r in rec]
 
-    Queries with a ReLU / clamp pre-activation or an argmin gap within 2e-6 of the magnitude
-    of the sum that produced it (cuBLAS SGEMM's largest normalised error measured on B200 is
-    7e-7, tools/gemm_precision.py), or with a near-tie between the DNF disjuncts of their
-    positive, are re-drawn from another batch of the same recipe (same pool); pool entries
-    whose DNF disjunct distances nearly tie for a query are masked out for it (no loss term).
+
+def well_conditioned_batch(cfg, table, structure, M, K, seed):
+    """A batch whose argmin decisions are well away from fp32 rounding (reading A28).
+
+    Queries with a Q2B offset-min gap within 2e-6 of the magnitude of the values compared, or
+    with a near-tie between the DNF disjuncts of their positive, are re-drawn from another batch
+    of the same recipe (same pool); pool entries whose DNF disjunct distances nearly tie for a
+    query are masked out for it (no loss term).  ReLU / clamp decisions are not re-drawn: the
+    step is checked against their exact flip allowance (traced_flip_allowance).
     Returns (batch, number of re-drawn queries, number of masked pairs)."""
     b = {k: (v.copy() if isinstance(v, np.ndarray) else v)
          for k, v in kggen.make_batch(cfg, structure, M, K, seed=seed, step=0).items()}
     redrawn = 0
     for it in range(30):
         dpos, dneg, tr = oracle_forward(cfg, table, b, M, K, trace=True)
+        kinds = _decision_kinds(cfg, table, b, M)
+        assert len(kinds) == len(tr)
         bad = np.zeros(M, bool)
-        for margin, scale in tr:
+        for (margin, scale), kind in zip(tr, kinds):
+            if kind != "gap":   # ReLU / clamp decisions: covered by traced_flip_allowance instead
+                continue
             near = (margin.abs() <= 2e-6 * scale).numpy()
             bad |= near.reshape(-1, M, near.shape[-1]).any(axis=(0, 2)) if near.ndim >= 2 else near
         if len(dpos) == 2:
@@ -265,14 +412,17 @@ def test_full_size_step(wl, structure, kind):
     b, redrawn, masked = well_conditioned_batch(cfg, table, structure, M, K, seed=3)
     print(f"{wl} {structure}: {redrawn} queries re-drawn, {masked} near-tie DNF pairs masked out")
     lr = 1e-3
-    assert redrawn <= 0.5 * M, f"{redrawn} of {M} queries re-drawn"
+    assert redrawn <= 0.1 * M, f"{redrawn} of {M} queries re-drawn"
     # (before oracle_step: it applies the update to `table`)
     allow = q2b_flip_allowance(cfg, table, b, M, K) if cfg.kind == "q2b" else None
+    ta_rows, ta_dense, n_dec = traced_flip_allowance(cfg, table, b, M, K)
     ref = oracle.oracle_step(cfg, table, [b], lr, apply=True)
     if allow is not None:
         allow_rows, allow_dense, n_terms = allow
     else:
         allow_rows, allow_dense, n_terms = np.zeros_like(ref.grad_rows), np.zeros_like(ref.grad_dense), 0
+    allow_rows = allow_rows + ta_rows
+    allow_dense = allow_dense + ta_dense
     info = gm.step(gm.host_batch(b), lr)
     g = gm.last_grads(cap=4 * M + M + K + 8, M=M, K=K)
     assert abs(info.loss - ref.loss) <= RTOL * abs(ref.loss), (info.loss, ref.loss)
@@ -282,11 +432,14 @@ def test_full_size_step(wl, structure, kind):
     assert info.n_touched == len(ref.uniq)
     n1, a1 = assert_close_allow(g["grad_rows"], ref.grad_rows, "dL/dtheta_E rows", allow_rows)
     n2, a2 = assert_close_allow(g["grad_dense"], ref.grad_dense, "dL/dtheta_D", allow_dense)
+    print(f"{wl} {structure}: {n_dec} ReLU / clamp decisions within 2e-6 of their kink")
     print(f"{wl} {structure}: {n_terms} terms within 1e-6 of a kink; elements with an allowance: rows {a1} of "
           f"{allow_rows.size}, dense {a2} of {allow_dense.size}; beyond the plain bound: rows {n1}, dense {n2}")
-    keep = np.abs(ref.m_new) >= 1e-4 * np.abs(ref.m_new).max()
+    # after the step: an element whose gradient carries a flip allowance may take another Adam
+    # step (at t = 1 the update is ~ -lr sign(g)); those are checked through the gradients above
+    keep = (np.abs(ref.m_new) >= 1e-4 * np.abs(ref.m_new).max()) & (allow_rows <= 0.1 * np.abs(ref.grad_rows))
     assert_close(gm.read_rows(ref.uniq), ref.rows_new, what="theta_E rows after the step", mask=keep)
-    keepd = np.abs(ref.dense_m_new) >= 1e-4 * np.abs(ref.dense_m_new).max()
+    keepd = (np.abs(ref.dense_m_new) >= 1e-4 * np.abs(ref.dense_m_new).max()) & (allow_dense <= 0.1 * np.abs(ref.grad_dense))
     assert_close(gm.read_dense(0), ref.dense_new, what="theta_D after the step", mask=keepd)
     gm.close()
 
