@@ -512,6 +512,8 @@ struct kg_handle {
   int host_tier = 0;     // bit i: theta_E table i (ent, ent_m, ent_v) is pinned host memory
   float *T[12] = {};
   int8_t *amin = nullptr;
+  float *pXT = nullptr, *pH1T = nullptr, *pH2T = nullptr;   // BetaE MLP inputs transposed ([cols][rows]) for dW
+  cudaEvent_t ev_xt = nullptr;
   float *pX = nullptr, *pH1 = nullptr, *pH2 = nullptr, *pZp1 = nullptr, *pdZ = nullptr, *pdH2 = nullptr,
         *pdH1 = nullptr, *pZ = nullptr, *pdX = nullptr;
   float *Dscore = nullptr;
@@ -754,6 +756,9 @@ void carve(kg_handle *h, Arena &A) {
     h->pX = A.take<float>(P * 2 * d);
     h->pH1 = A.take<float>(P * H);
     h->pH2 = A.take<float>(P * H);
+    h->pXT = A.take<float>(align_up(P, 4) * 2 * d);
+    h->pH1T = A.take<float>(align_up(P, 4) * H);
+    h->pH2T = A.take<float>(align_up(P, 4) * H);
     h->pZp1 = A.take<float>(P * d);
     h->pdZ = A.take<float>(P * d);
     h->pdH2 = A.take<float>(P * H);
@@ -1011,6 +1016,18 @@ kg_status dag_forward(kg_handle *h, StepBufs &S) {
       }
     }
   }
+  if (h->kind == KG_BETAE && p.nproj > 0) {
+    // the MLP layers' inputs transposed ([cols][rows], ld = rows rounded up to 4) for the weight
+    // gradients dW = dY^T X of the backward: K-major B operands instead of MN-major ones the
+    // GEMM's split warps would transpose; on the low-priority stream, during the scoring
+    const int NR = p.nproj * M, ldT = (int)align_up(NR, 4);
+    kg_status fs = fork(h, st, h->st4);
+    if (fs) return fs;
+    launch_transpose(h->pX, NR, 2 * d, 2 * d, h->pXT, ldT, h->st4);
+    launch_transpose(h->pH1, NR, HH, HH, h->pH1T, ldT, h->st4);
+    launch_transpose(h->pH2, NR, HH, HH, h->pH2T, ldT, h->st4);
+    CK(cudaEventRecord(h->ev_xt, h->st4));
+  }
   return KG_OK;
 }
 
@@ -1126,12 +1143,13 @@ kg_status dag_backward(kg_handle *h, StepBufs &S) {
   }
   if (h->kind == KG_BETAE) {
     // projection-MLP weight gradients over all projection uses at once (A9)
-    const int NR = p.nproj * M;
-    G(true, false, d, HH, NR, h->pdZ, d, h->pH2, HH, 0.f, gp(h, "prj_W0"), HH);
+    const int NR = p.nproj * M, ldT = (int)align_up(NR, 4);
+    CK(cudaStreamWaitEvent(st, h->ev_xt, 0));   // the transposed inputs (DAG forward, st4)
+    G(true, true, d, HH, NR, h->pdZ, d, h->pH2T, ldT, 0.f, gp(h, "prj_W0"), HH);
     launch_colsum(h->pdZ, NR, d, d, gp(h, "prj_b0"), st);
-    G(true, false, HH, HH, NR, h->pdH2, HH, h->pH1, HH, 0.f, gp(h, "prj_W2"), HH);
+    G(true, true, HH, HH, NR, h->pdH2, HH, h->pH1T, ldT, 0.f, gp(h, "prj_W2"), HH);
     launch_colsum(h->pdH2, NR, HH, HH, gp(h, "prj_b2"), st);
-    G(true, false, HH, 2 * d, NR, h->pdH1, HH, h->pX, 2 * d, 0.f, gp(h, "prj_W1"), 2 * d);
+    G(true, true, HH, 2 * d, NR, h->pdH1, HH, h->pXT, ldT, 0.f, gp(h, "prj_W1"), 2 * d);
     launch_colsum(h->pdH1, NR, HH, HH, gp(h, "prj_b1"), st);
   }
   return KG_OK;
@@ -1432,7 +1450,8 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_wsplit, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&h->ev_wsplit_t, cudaEventDisableTiming) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
+      cudaEventCreateWithFlags(&h->ev_wsplit_t, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_xt, cudaEventDisableTiming) != cudaSuccess) { kg_destroy(h); return KG_ECUDA; }
   if (c.world > 1) {
     ncclUniqueId id;
     std::memcpy(&id, c.nccl_id, sizeof(id));
