@@ -62,21 +62,53 @@ void launch_transpose(const float *in, int R, int Cc, int ld_in, float *out, int
   { transpose_kernel<<<grid, block, 0, st>>>(in, R, Cc, ld_in, out, ld_out); ++g_launches; }
 }
 
-// C = beta C + alpha sum_z P[z] (+ bias) (ReLU): the fixed-order combine of the split-K partials.
+// C = beta C + alpha sum_z P[z] (+ bias) (ReLU) (masked): the fixed-order combine of the split-K
+// partials, 4 consecutive columns per thread (N % 4 == 0 and ldc % 4 == 0: float4 path).
 __global__ void gemm_reduce_kernel(const float *__restrict__ P, int splits, int M, int N, float *C, int ldc,
-                                   const float *bias, int relu, float beta, float alpha) {
+                                   const float *bias, int relu, float beta, float alpha, const float *mask) {
   KG_GRID_DEP_WAIT();
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4;
   if (e >= (int64_t)M * N) return;
   const int row = (int)(e / N), n = (int)(e - (int64_t)row * N);
-  float v = 0.f;
-  for (int z = 0; z < splits; ++z) v += P[(int64_t)z * M * N + e];
-  v *= alpha;
-  if (bias) v += bias[n];
-  if (relu) v = fmaxf(v, 0.f);
-  float *c = C + (int64_t)row * ldc + n;
-  if (beta != 0.f) v += beta * *c;
-  *c = v;
+  const int64_t MN = (int64_t)M * N;
+  const int64_t co = (int64_t)row * ldc + n;
+  if (!(N & 3) && !(ldc & 3)) {
+    float4 v = __ldcs(reinterpret_cast<const float4 *>(P + e));
+    for (int z = 1; z < splits; ++z) {
+      const float4 q = __ldcs(reinterpret_cast<const float4 *>(P + z * MN + e));
+      v.x += q.x; v.y += q.y; v.z += q.z; v.w += q.w;
+    }
+    v.x *= alpha; v.y *= alpha; v.z *= alpha; v.w *= alpha;
+    if (bias) { v.x += bias[n]; v.y += bias[n + 1]; v.z += bias[n + 2]; v.w += bias[n + 3]; }
+    if (relu) { v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f); }
+    float4 *c = reinterpret_cast<float4 *>(C + co);
+    if (beta != 0.f) {
+      const float4 o = *c;
+      v.x += beta * o.x; v.y += beta * o.y; v.z += beta * o.z; v.w += beta * o.w;
+    }
+    if (mask) {
+      const float4 y = *reinterpret_cast<const float4 *>(mask + co);
+      if (!(y.x > 0.f)) v.x = 0.f;
+      if (!(y.y > 0.f)) v.y = 0.f;
+      if (!(y.z > 0.f)) v.z = 0.f;
+      if (!(y.w > 0.f)) v.w = 0.f;
+    }
+    *c = v;
+    return;
+  }
+  for (int j = 0; j < 4 && e + j < MN; ++j) {   // generic: 4 consecutive flat elements
+    const int64_t f = e + j;
+    const int r = (int)(f / N), c = (int)(f - (int64_t)r * N);
+    float v = 0.f;
+    for (int z = 0; z < splits; ++z) v += P[z * MN + f];
+    v *= alpha;
+    if (bias) v += bias[c];
+    if (relu) v = fmaxf(v, 0.f);
+    float *o = C + (int64_t)r * ldc + c;
+    if (beta != 0.f) v += beta * *o;
+    if (mask && !(mask[(int64_t)r * ldc + c] > 0.f)) v = 0.f;
+    *o = v;
+  }
 }
 
 
@@ -658,9 +690,11 @@ bool launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t s
   dim3 grid((g.N + BN - 1) / BN, (g.M + GBM - 1) / GBM, splits);
   { gemm_tf32x3_tma_kernel<BN, AMN, BMN, DRAIN, LOWP><<<grid, G2T, Cfg::kSmem, st>>>(ta, tb, tbl, g); ++g_launches; }
   if (splits > 1) {
-    const int64_t n = (int64_t)g.M * g.N;
-    { gemm_reduce_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(part, splits, g.M, g.N, g.C, g.ldc, g.bias, g.relu,
-                                                                g.beta, g.alpha); ++g_launches; }
+    const int64_t n4 = ((int64_t)g.M * g.N + 3) / 4;
+    { gemm_reduce_kernel<<<(int)((n4 + 255) / 256), 256, 0, st>>>(part, splits, g.M, g.N, g.C, g.ldc, g.bias, g.relu,
+                                                                 g.beta, g.alpha, g.mask); ++g_launches; }
+  } else if (g.mask) {
+    launch_relu_mask(g.C, g.mask, g.M, g.N, st);
   }
   return true;
 }
@@ -676,7 +710,8 @@ bool launch_v2_any(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_
 bool gemm_tc_accepts(const GemmArgs &g) {
   return g.M > 0 && g.N > 0 && g.K > 0 && !(reinterpret_cast<uintptr_t>(g.A) & 15) &&
          !(reinterpret_cast<uintptr_t>(g.B) & 15) && !(reinterpret_cast<uintptr_t>(g.B_lo) & 15) &&
-         !(g.B_lo && g.b_mn) && !(g.lda & 3) && !(g.ldb & 3) && tmap_encoder() != nullptr;
+         !(g.B_lo && g.b_mn) && !(g.lda & 3) && !(g.ldb & 3) && !(g.mask && g.ldc != g.N) &&
+         tmap_encoder() != nullptr;
 }
 
 // C = beta C + op(A) op(B)^T (+ bias) (ReLU) on the tensor cores.  A is [M][K] (a_mn: [K][M]),

@@ -825,7 +825,7 @@ void carve(kg_handle *h, Arena &A) {
 // accumulation, see kg_create); the side stream has its own split-K scratch.
 kg_status gemm(kg_handle *h, bool ta, bool tb, int m, int n, int k, const float *A, int lda, const float *B, int ldb,
                float beta, float *C, int ldc, const float *bias = nullptr, int relu = 0, float alpha = 1.f,
-               const float *B_lo = nullptr, bool tb_t = false) {
+               const float *B_lo = nullptr, bool tb_t = false, const float *mask = nullptr) {
   if (m <= 0 || n <= 0) return KG_OK;
   // the tensor-core kernel reads either operand layout directly ([k][m] / [k][n] = MN-major)
   GemmArgs g;
@@ -835,6 +835,7 @@ kg_status gemm(kg_handle *h, bool ta, bool tb, int m, int n, int k, const float 
   g.alpha = alpha;
   if (B_lo) CK(cudaStreamWaitEvent(h->st, tb_t ? h->ev_wsplit_t : h->ev_wsplit, 0));   // this step's planes (st3)
   g.B_lo = B_lo;
+  g.mask = mask;
   if (k <= 0 || !launch_gemm_tc(g, h->side ? h->gsP2 : h->gsP, h->gsP_cap, h->st))
     return fail(h, KG_EUNSUPPORTED, "tensor-core GEMM: operands must be 16-byte aligned with ld % 4 == 0 and K > 0 "
                                     "(and cuTensorMapEncodeTiled available)");
@@ -1054,10 +1055,10 @@ kg_status dag_backward(kg_handle *h, StepBufs &S) {
             *dH1 = h->pdH1 + (int64_t)u0 * M * HH;
       for (int k = n0; k <= ni; ++k)
         launch_betae_proj_dz(S.grad[k], h->pZp1 + (int64_t)use[k] * M * d, M, d, h->pdZ + (int64_t)use[k] * M * d, st);
-      G(false, true, GM, HH, d, dZ, d, wt(h, "prj_W0"), d, 0.f, dH2, HH, nullptr, 0, 1.f, wtlo(h, "prj_W0"), true);
-      launch_relu_mask(dH2, h->pH2 + (int64_t)u0 * M * HH, GM, HH, st);
-      G(false, true, GM, HH, HH, dH2, HH, wt(h, "prj_W2"), HH, 0.f, dH1, HH, nullptr, 0, 1.f, wtlo(h, "prj_W2"), true);
-      launch_relu_mask(dH1, h->pH1 + (int64_t)u0 * M * HH, GM, HH, st);
+      G(false, true, GM, HH, d, dZ, d, wt(h, "prj_W0"), d, 0.f, dH2, HH, nullptr, 0, 1.f, wtlo(h, "prj_W0"), true,
+        h->pH2 + (int64_t)u0 * M * HH);   // ReLU backward folded into the GEMM's combine
+      G(false, true, GM, HH, HH, dH2, HH, wt(h, "prj_W2"), HH, 0.f, dH1, HH, nullptr, 0, 1.f, wtlo(h, "prj_W2"), true,
+        h->pH1 + (int64_t)u0 * M * HH);
       G(false, true, GM, 2 * d, HH, dH1, HH, wt(h, "prj_W1"), HH, 0.f, h->pdX, 2 * d, nullptr, 0, 1.f, wtlo(h, "prj_W1"), true);
       for (int k = n0; k <= ni; ++k) {
         const PNode &nk = p.n[k];
@@ -1120,8 +1121,8 @@ kg_status dag_backward(kg_handle *h, StepBufs &S) {
           G(false, true, NR, d, d, T[11], d, wt(h, "off_W1"), d, 1.f, h->stack_g + d, 2 * d, nullptr, 0, 1.f, wtlo(h, "off_W1"), true);
         }
         launch_q2b_att_bwd(h->stack_v, T[2], gout, n, M, d, T[7], h->stack_g, st);
-        G(false, true, NR, d, d, T[7], d, wt(h, "att_W2"), d, 0.f, T[8], d, nullptr, 0, 1.f, wtlo(h, "att_W2"), true);
-        launch_relu_mask(T[8], T[0], NR, d, st);
+        G(false, true, NR, d, d, T[7], d, wt(h, "att_W2"), d, 0.f, T[8], d, nullptr, 0, 1.f, wtlo(h, "att_W2"), true,
+          T[0]);
         G(true, false, d, d, NR, T[7], d, T[0], d, 0.f, gp(h, "att_W2"), d);
         launch_colsum(T[7], NR, d, d, gp(h, "att_b2"), st);
         G(true, false, d, d, NR, T[8], d, h->stack_v, 2 * d, 0.f, gp(h, "att_W1"), d);
@@ -1131,8 +1132,8 @@ kg_status dag_backward(kg_handle *h, StepBufs &S) {
       } else if (h->kind == KG_BETAE) {
         // forward: T0 Hs, T1 Lg, T2 w.  backward: T7 dLg, T8 dHs
         launch_beta_att_bwd(h->stack_v, T[2], gout, n, M, d, T[7], h->stack_g, st);
-        G(false, true, NR, d, m, T[7], m, wt(h, "att_U2"), m, 0.f, T[8], d, nullptr, 0, 1.f, wtlo(h, "att_U2"), true);
-        launch_relu_mask(T[8], T[0], NR, d, st);
+        G(false, true, NR, d, m, T[7], m, wt(h, "att_U2"), m, 0.f, T[8], d, nullptr, 0, 1.f, wtlo(h, "att_U2"), true,
+          T[0]);
         G(true, false, m, d, NR, T[7], m, T[0], d, 0.f, gp(h, "att_U2"), d);
         launch_colsum(T[7], NR, m, m, gp(h, "att_c2"), st);
         G(true, false, d, d, NR, T[8], d, h->stack_v, d, 0.f, gp(h, "att_U1"), d);

@@ -109,6 +109,9 @@ struct GemmArgs {
   // pre-split B (K-major only): B_lo = rna_tf32(B - trunc_tf32(B)) in B's layout; the kernel
   // loads it with TMA instead of splitting B in shared memory (weights: kg_api.cu wsplit)
   const float *B_lo = nullptr;
+  // ReLU backward folded in: C = 0 where !(mask > 0); mask has C's shape and leading dimension
+  // (ldc == N required).  Applied by the split-K combine, or by a mask pass after an unsplit GEMM.
+  const float *mask = nullptr;
 };
 struct WSplitJob { const float *w; float *lo, *t, *tlo; int R, C; };
 struct WSplitJobs { WSplitJob j[12]; int n = 0; };
