@@ -257,7 +257,8 @@ const char *kg_last_error(const kg_handle *h);
  * relu & 2 selects the drained (fp32-accurate) accumulation used for BetaE;
  * ta: A stored [K][lda] (else [M][lda]); tb: B stored [K][ldb] (else [N][ldb]); both layouts are
  * read in place by TMA.  tcgen05 kind::tf32 with a 3xTF32 split (fp32-level accuracy).  Needs
- * K >= 1, 16-byte aligned A / B and lda % 4 == ldb % 4 == 0 (else EINVAL).  Synchronises the stream. */
+ * K >= 1, 16-byte aligned A / B and lda % 4 == ldb % 4 == 0 (else EINVAL).  Synchronises the stream.
+ * Tool bits: (relu >> 2) & 63 forces a tile / split-K variant, relu >> 8 = back-to-back repetitions. */
 kg_status kg_test_gemm(int32_t ta, int32_t tb, int32_t M, int32_t N, int32_t K, const float *A, int32_t lda,
                        const float *B, int32_t ldb, float *C, int32_t ldc, const float *bias, int32_t relu, float beta,
                        void *stream);

@@ -619,5 +619,31 @@ __global__ void __launch_bounds__(1024) colsum_kernel(const float *X, int rows, 
 void launch_colsum(const float *X, int rows, int cols, int ld, float *out, cudaStream_t st) {
   { colsum_kernel<<<(cols + 31) / 32, 1024, 0, st>>>(X, rows, cols, ld, out); ++g_launches; }
 }
+// Every bias gradient of one DAG node in one launch (blockIdx.y = job): the same per-column
+// fixed-order sums as colsum_kernel.
+__global__ void __launch_bounds__(1024) colsum_multi_kernel(ColsumJobs J) {
+  KG_GRID_DEP_WAIT();
+  __shared__ float red[32][33];
+  const ColsumJob &jb = J.j[blockIdx.y];
+  const int cx = threadIdx.x & 31, ry = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + cx;
+  if (blockIdx.x * 32 >= jb.cols) return;
+  float s = 0.f;
+  if (c < jb.cols)
+    for (int r = ry; r < jb.rows; r += 32) s += jb.X[(int64_t)r * jb.ld + c];
+  red[ry][cx] = s;
+  __syncthreads();
+  if (ry == 0 && c < jb.cols) {
+    float t = 0.f;
+    for (int k = 0; k < 32; ++k) t += red[k][cx];
+    jb.out[c] = t;
+  }
+}
+void launch_colsum_multi(const ColsumJobs &J, cudaStream_t st) {
+  if (J.n <= 0) return;
+  int mc = 0;
+  for (int i = 0; i < J.n; ++i) mc = std::max(mc, J.j[i].cols);
+  { colsum_multi_kernel<<<dim3((mc + 31) / 32, J.n), 1024, 0, st>>>(J); ++g_launches; }
+}
 
 }  // namespace kg

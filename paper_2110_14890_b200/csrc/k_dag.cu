@@ -129,6 +129,13 @@ void launch_proj_bwd(int kind, int N, int d, const float *dout, const float *in,
 #undef ARGS
 }
 
+// sum of the raw split-K partial products [S][..] at element e, in ascending split order
+__device__ __forceinline__ float psum(const float *P, int S, int64_t zs, int64_t e) {
+  float v = P[e];
+  for (int z = 1; z < S; ++z) v += P[z * zs + e];
+  return v;
+}
+
 // ------------------------------------------------------------ BetaE MLP glue
 // X[i] = [e_q(i) ; y_r(i)]  (A9), e_q = node value or clamp(x_anchor + 1) (A8)
 __global__ void betae_proj_in_kernel(int N, int d, const float *in, const int64_t *anchor_rows, const float *ent,
@@ -169,6 +176,25 @@ __global__ void betae_proj_out_kernel(const float *Z, const float *b0, int rows,
 void launch_betae_proj_out(const float *Z, const float *b0, int rows, int d, float *Zp1, float *out,
                            cudaStream_t st) {
   { betae_proj_out_kernel<<<blocks((int64_t)rows * d), 256, 0, st>>>(Z, b0, rows, d, Zp1, out); ++g_launches; }
+}
+
+// the same from the raw split-K partials of Z = H2 W0^T over the rows of a projection group
+// (fused epilogue, k_dag.cu *_red): z = (sum_z P) + b0 + 1; projection g of the group (rows
+// [g M, (g + 1) M)) writes its node value out.p[g]
+__global__ void betae_proj_out_red_kernel(const float *P, int S, const float *b0, int rows, int M, int d, float *Zp1,
+                                          OutPtrs out) {
+  KG_GRID_DEP_WAIT();
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t n = (int64_t)rows * d;
+  if (e >= n) return;
+  const float z = psum(P, S, n, e) * 1.f + b0[e % d] + 1.f;
+  Zp1[e] = z;
+  const int64_t Md = (int64_t)M * d, g = e / Md;
+  out.p[g][e - g * Md] = fminf(fmaxf(z, kBetaLo), kBetaHi);
+}
+void launch_betae_proj_out_red(const float *P, int S, const float *b0, int rows, int M, int d, float *Zp1,
+                               const OutPtrs &out, cudaStream_t st) {
+  { betae_proj_out_red_kernel<<<blocks((int64_t)rows * d), 256, 0, st>>>(P, S, b0, rows, M, d, Zp1, out); ++g_launches; }
 }
 
 __global__ void betae_proj_dz_kernel(const float *dout, const float *Zp1, int rows, int d, float *dZ) {
@@ -294,6 +320,114 @@ __global__ void gqe_inter_dh_kernel(const float *dMn, const float *H, int n, int
 void launch_gqe_inter_dh(const float *dMn, const float *H, int n, int rows, int cols, float *dH, cudaStream_t st) {
   const int64_t rc = (int64_t)rows * cols;
   { gqe_inter_dh_kernel<<<blocks(rc * n), 256, 0, st>>>(dMn, H, n, rc, dH); ++g_launches; }
+}
+
+// ---- the intersection MLPs' GEMM epilogues fused with their consumers.  P holds the raw
+// split-K partial products [S][rows][d] of a GEMM (launch_gemm_tc_raw); each kernel sums them in
+// ascending split order and adds the bias exactly as gemm_reduce_kernel does, then applies the
+// node's pooling in the order of the kernels above it replaces (mean_stack, q2b_off_fwd,
+// q2b_att_fwd): the values are bitwise those of the unfused chain.
+// DeepSet layer 1 + mean pooling (A4): H_t = ReLU(P_t + b), Mn = (sum_t H_t) / n
+__global__ void mean_red_kernel(const float *P, int S, const float *b, int n, int M, int d, float *H, float *Mn) {
+  KG_GRID_DEP_WAIT();
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t Md = (int64_t)M * d;
+  if (e >= Md) return;
+  const int k = (int)(e % d);
+  const int64_t zs = (int64_t)n * Md;
+  float s = 0.f;
+  for (int t = 0; t < n; ++t) {
+    const float h = fmaxf(psum(P, S, zs, t * Md + e) * 1.f + b[k], 0.f);
+    H[t * Md + e] = h;
+    s += h;
+  }
+  Mn[e] = s / (float)n;
+}
+void launch_mean_red(const float *P, int S, const float *b, int n, int M, int d, float *H, float *Mn, cudaStream_t st) {
+  { mean_red_kernel<<<blocks((int64_t)M * d), 256, 0, st>>>(P, S, b, n, M, d, H, Mn); ++g_launches; }
+}
+// Q2B offset: Z = P + b, o = min_t o_t * sigmoid(Z) (Table 1), argmin ties -> lowest t (A19)
+__global__ void q2b_off_red_kernel(const float *P, int S, const float *b, const float *stack, int n, int M, int d,
+                                   float *sig, int8_t *amin, float *out) {
+  KG_GRID_DEP_WAIT();
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t Md = (int64_t)M * d;
+  if (e >= Md) return;
+  const int i = (int)(e / d), k = (int)(e - (int64_t)i * d);
+  float mn = stack[(int64_t)i * 2 * d + d + k];
+  int am = 0;
+  for (int t = 1; t < n; ++t) {
+    const float o = stack[((int64_t)t * M + i) * 2 * d + d + k];
+    if (o < mn) { mn = o; am = t; }
+  }
+  const float s = sigm_(psum(P, S, Md, e) * 1.f + b[k]);
+  sig[e] = s;
+  amin[e] = (int8_t)am;
+  out[(int64_t)i * 2 * d + d + k] = mn * s;
+}
+void launch_q2b_off_red(const float *P, int S, const float *b, const float *stack, int n, int M, int d, float *sig,
+                        int8_t *amin, float *out, cudaStream_t st) {
+  { q2b_off_red_kernel<<<blocks((int64_t)M * d), 256, 0, st>>>(P, S, b, stack, n, M, d, sig, amin, out); ++g_launches; }
+}
+// Q2B center attention: Lg_t = P_t + b, a_t = softmax_t(Lg_t) per (i, k), c = sum_t a_t c_t (A5)
+__global__ void q2b_att_red_kernel(const float *P, int S, const float *b, const float *stack, int n, int M, int d,
+                                   float *a, float *out) {
+  KG_GRID_DEP_WAIT();
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t Md = (int64_t)M * d;
+  if (e >= Md) return;
+  const int i = (int)(e / d), k = (int)(e - (int64_t)i * d);
+  const int64_t zs = (int64_t)n * Md;
+  float lg[3], mx = -INFINITY;
+  for (int t = 0; t < n; ++t) {
+    lg[t] = psum(P, S, zs, t * Md + e) * 1.f + b[k];
+    mx = fmaxf(mx, lg[t]);
+  }
+  float z = 0.f, ex[3];
+  for (int t = 0; t < n; ++t) { ex[t] = expf(lg[t] - mx); z += ex[t]; }
+  float c = 0.f;
+  for (int t = 0; t < n; ++t) {
+    const float at = ex[t] / z;
+    a[t * Md + e] = at;
+    c += at * stack[((int64_t)t * M + i) * 2 * d + k];
+  }
+  out[(int64_t)i * 2 * d + k] = c;
+}
+void launch_q2b_att_red(const float *P, int S, const float *b, const float *stack, int n, int M, int d, float *a,
+                        float *out, cudaStream_t st) {
+  { q2b_att_red_kernel<<<blocks((int64_t)M * d), 256, 0, st>>>(P, S, b, stack, n, M, d, a, out); ++g_launches; }
+}
+// BetaE attention: Lg_t = P_t + c2 (m per row), w = softmax_t(Lg_t), out = (sum w a_t, sum w b_t)
+__global__ void beta_att_red_kernel(const float *P, int S, const float *b, const float *stack, int n, int M, int d,
+                                    float *w, float *out) {
+  KG_GRID_DEP_WAIT();
+  const int m = d / 2;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t Mm = (int64_t)M * m;
+  if (e >= Mm) return;
+  const int i = (int)(e / m), k = (int)(e - (int64_t)i * m);
+  const int64_t zs = (int64_t)n * Mm;
+  float lg[3], mx = -INFINITY;
+  for (int t = 0; t < n; ++t) {
+    lg[t] = psum(P, S, zs, t * Mm + e) * 1.f + b[k];
+    mx = fmaxf(mx, lg[t]);
+  }
+  float z = 0.f, ex[3];
+  for (int t = 0; t < n; ++t) { ex[t] = expf(lg[t] - mx); z += ex[t]; }
+  float sa = 0.f, sb = 0.f;
+  for (int t = 0; t < n; ++t) {
+    const float wt = ex[t] / z;
+    w[t * Mm + e] = wt;
+    const float *row = stack + ((int64_t)t * M + i) * d;
+    sa += wt * row[k];
+    sb += wt * row[m + k];
+  }
+  out[(int64_t)i * d + k] = sa;
+  out[(int64_t)i * d + m + k] = sb;
+}
+void launch_beta_att_red(const float *P, int S, const float *b, const float *stack, int n, int M, int d, float *w,
+                         float *out, cudaStream_t st) {
+  { beta_att_red_kernel<<<blocks((int64_t)M * (d / 2)), 256, 0, st>>>(P, S, b, stack, n, M, d, w, out); ++g_launches; }
 }
 
 // Q2B center attention: a_t = softmax_t(Lg_t) per (i, k); c = sum_t a_t c_t (A5).

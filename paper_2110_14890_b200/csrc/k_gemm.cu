@@ -583,6 +583,7 @@ __global__ void __launch_bounds__(G2T, 1)
             v = fmaf(g.alpha, v, bn);
             if (g.relu) v = fmaxf(v, 0.f);
             if (g.beta != 0.f) v += g.beta * *c;
+            if (g.mask && !(g.mask[(int64_t)row * g.ldc + n] > 0.f)) v = 0.f;   // ReLU backward (ldc == N)
             *c = v;
           }
         }
@@ -662,14 +663,16 @@ bool make_tmap(CUtensorMap *tm, const float *base, int rows, int K, int ld, int 
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// returns the number of K splits (0: not launched); raw: the kernel writes the raw partial
+// products [splits][M][N] into `part` (even unsplit) and the caller's kernel combines them
 template <int BN, bool AMN, bool BMN, bool DRAIN, bool LOWP = false>
-bool launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t st) {
+int launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t st, bool raw = false) {
   using Cfg = G2Cfg<BN, AMN, BMN, !LOWP, DRAIN>;
   CUtensorMap ta, tb, tbl;
   if (!make_tmap(&ta, g0.A, g0.M, g0.K, g0.lda, GBM, AMN) || !make_tmap(&tb, g0.B, g0.N, g0.K, g0.ldb, BN, BMN))
-    return false;
+    return 0;
   if (g0.B_lo && !BMN && !LOWP) {
-    if (!make_tmap(&tbl, g0.B_lo, g0.N, g0.K, g0.ldb, BN, false)) return false;
+    if (!make_tmap(&tbl, g0.B_lo, g0.N, g0.K, g0.ldb, BN, false)) return 0;
   } else {
     tbl = tb;
   }
@@ -687,23 +690,26 @@ bool launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t s
   g.kbs = (nkb + splits - 1) / splits;
   splits = (nkb + g.kbs - 1) / g.kbs;
   g.P = splits > 1 ? part : nullptr;
+  if (raw) {
+    if (!part || (int64_t)splits * g.M * g.N > part_cap) return 0;
+    g.P = part;
+  }
   dim3 grid((g.N + BN - 1) / BN, (g.M + GBM - 1) / GBM, splits);
   { gemm_tf32x3_tma_kernel<BN, AMN, BMN, DRAIN, LOWP><<<grid, G2T, Cfg::kSmem, st>>>(ta, tb, tbl, g); ++g_launches; }
+  if (raw) return splits;
   if (splits > 1) {
     const int64_t n4 = ((int64_t)g.M * g.N + 3) / 4;
     { gemm_reduce_kernel<<<(int)((n4 + 255) / 256), 256, 0, st>>>(part, splits, g.M, g.N, g.C, g.ldc, g.bias, g.relu,
                                                                  g.beta, g.alpha, g.mask); ++g_launches; }
-  } else if (g.mask) {
-    launch_relu_mask(g.C, g.mask, g.M, g.N, st);
   }
-  return true;
+  return splits;
 }
 template <int BN, bool DRAIN, bool LOWP = false>
-bool launch_v2_any(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st) {
-  if (g.a_mn) return g.b_mn ? launch_v2<BN, true, true, DRAIN, LOWP>(g, part, part_cap, st)
-                            : launch_v2<BN, true, false, DRAIN, LOWP>(g, part, part_cap, st);
-  return g.b_mn ? launch_v2<BN, false, true, DRAIN, LOWP>(g, part, part_cap, st)
-                : launch_v2<BN, false, false, DRAIN, LOWP>(g, part, part_cap, st);
+int launch_v2_any(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st, bool raw = false) {
+  if (g.a_mn) return g.b_mn ? launch_v2<BN, true, true, DRAIN, LOWP>(g, part, part_cap, st, raw)
+                            : launch_v2<BN, true, false, DRAIN, LOWP>(g, part, part_cap, st, raw);
+  return g.b_mn ? launch_v2<BN, false, true, DRAIN, LOWP>(g, part, part_cap, st, raw)
+                : launch_v2<BN, false, false, DRAIN, LOWP>(g, part, part_cap, st, raw);
 }
 }  // namespace
 
@@ -718,17 +724,17 @@ bool gemm_tc_accepts(const GemmArgs &g) {
 // B is [N][K] (b_mn: [K][N]), 16-byte aligned with ld % 4 == 0 (gemm_tc_accepts).  When the
 // output has fewer tiles than SMs, K is split over blockIdx.z (at most one wave of CTAs: 192 KB
 // of shared memory per CTA) into `part` (capacity part_cap floats).
-bool launch_gemm_tc(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st) {
-  if (!gemm_tc_accepts(g)) return false;
+static int launch_gemm_sel(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st, bool raw) {
+  if (!gemm_tc_accepts(g)) return 0;
   const int64_t t256 = (int64_t)((g.N + 255) / 256) * ((g.M + GBM - 1) / GBM);
   const bool wide = g.N > 128 && t256 >= 100;   // enough 128 x 256 tiles to fill the GPU
-  if (g.lowp) return launch_v2_any<128, false, true>(g, part, part_cap, st);
+  if (g.lowp) return launch_v2_any<128, false, true>(g, part, part_cap, st, raw);
   if (g.force) {
     const GemmArgs &f = g;
     const int bn = (g.force >> 1) & 3;
-    auto go = [&](auto tag) -> bool {
+    auto go = [&](auto tag) -> int {
       constexpr int BN = decltype(tag)::value;
-      return f.drain ? launch_v2_any<BN, true>(f, part, part_cap, st) : launch_v2_any<BN, false>(f, part, part_cap, st);
+      return f.drain ? launch_v2_any<BN, true>(f, part, part_cap, st, raw) : launch_v2_any<BN, false>(f, part, part_cap, st, raw);
     };
     if (bn == 1) return go(std::integral_constant<int, 64>());
     if (bn == 3) return go(std::integral_constant<int, 160>());
@@ -739,15 +745,25 @@ bool launch_gemm_tc(const GemmArgs &g, float *part, int64_t part_cap, cudaStream
     // 120 tiles of 128 x 160 (one)
     const int64_t t128 = (int64_t)((g.N + 127) / 128) * ((g.M + GBM - 1) / GBM);
     const int64_t t160 = (int64_t)((g.N + 159) / 160) * ((g.M + GBM - 1) / GBM);
-    if (t128 > 148 && t160 <= 148) return launch_v2_any<160, true>(g, part, part_cap, st);
+    if (t128 > 148 && t160 <= 148) return launch_v2_any<160, true>(g, part, part_cap, st, raw);
     // under half the SMs with a K too short to split (>= 8 k-blocks per split): 128 x 64
     // tiles, twice the CTAs (e.g. the ComplEx scores S = Q E^T, 1024 x 1024 x 200: 64 -> 128)
     const int nkb = (g.K + G2K - 1) / G2K;
     const int64_t t64 = (int64_t)((g.N + 63) / 64) * ((g.M + GBM - 1) / GBM);
-    if (2 * t128 <= 148 && nkb < 16 && t64 <= 148 && t64 > t128) return launch_v2_any<64, true>(g, part, part_cap, st);
-    return launch_v2_any<128, true>(g, part, part_cap, st);
+    if (2 * t128 <= 148 && nkb < 16 && t64 <= 148 && t64 > t128) return launch_v2_any<64, true>(g, part, part_cap, st, raw);
+    return launch_v2_any<128, true>(g, part, part_cap, st, raw);
   }
-  return wide ? launch_v2_any<256, false>(g, part, part_cap, st) : launch_v2_any<128, false>(g, part, part_cap, st);
+  return wide ? launch_v2_any<256, false>(g, part, part_cap, st, raw) : launch_v2_any<128, false>(g, part, part_cap, st, raw);
+}
+
+bool launch_gemm_tc(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st) {
+  return launch_gemm_sel(g, part, part_cap, st, false) > 0;
+}
+// The raw partial products only: [splits][M][N] fp32 into part (bias / relu / beta / mask of g are
+// not applied); returns the number of splits (0: not launched).  The caller's kernel sums the
+// splits in ascending order (the sums of gemm_reduce_kernel) and applies its own epilogue.
+int launch_gemm_tc_raw(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st) {
+  return launch_gemm_sel(g, part, part_cap, st, true);
 }
 
 }  // namespace kg

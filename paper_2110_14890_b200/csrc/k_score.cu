@@ -174,8 +174,16 @@ __device__ __forceinline__ float4 ld4(const float *p) { return *reinterpret_cast
 // 16 staged in shared memory.  blockIdx.z selects a contiguous range of units
 // (split reduction: more CTAs than the 148 SMs even at B = 512); the raw partial
 // sums go to Dpart[z][t][i][j] and pair_epi_kernel adds them in the fixed order z.
+// resident CTAs per SM of pair_fwd (KG_FWD_OCC4=1: 4 for the single-output Q2B box kernel, i.e.
+// <= 64 registers; experiment)
+#ifndef KG_FWD_OCC4
+#define KG_FWD_OCC4 1
+#endif
+template <class Mdl, int NOUT> struct kFwdOcc {
+  static constexpr int v = (KG_FWD_OCC4 && NOUT == 1 && std::is_same<Mdl, MBox>::value) ? 4 : 1;
+};
 template <class Mdl, int NOUT>
-__global__ void __launch_bounds__(256) pair_fwd_kernel(ScoreArgs a) {
+__global__ void __launch_bounds__(256, kFwdOcc<Mdl, NOUT>::v) pair_fwd_kernel(ScoreArgs a) {
   KG_GRID_DEP_WAIT();
   // thread (tx, ty) owns queries i0 + 4*ty + x and candidates j0 + 4*tx + b (x, b < 4):
   // one 128-bit shared load per operand row per unit.

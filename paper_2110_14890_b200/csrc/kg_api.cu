@@ -517,7 +517,7 @@ struct kg_handle {
   float *pX = nullptr, *pH1 = nullptr, *pH2 = nullptr, *pZp1 = nullptr, *pdZ = nullptr, *pdH2 = nullptr,
         *pdH1 = nullptr, *pZ = nullptr, *pdX = nullptr;
   float *Dscore = nullptr;
-  float *gsP = nullptr, *gsP2 = nullptr;   // GEMM split-K scratch (main / side stream)
+  float *gsP = nullptr, *gsP2 = nullptr, *gsP3 = nullptr;   // GEMM split-K scratch (st / st3 / st5)
   int64_t gsP_cap = 0;
   float *Dpart = nullptr, *partQ = nullptr, *partV = nullptr, *Cpart = nullptr, *Csum = nullptr;
   float *Eg = nullptr;     // dot-product scorers: the pool's rows, contiguous (GEMM operand)
@@ -525,6 +525,11 @@ struct kg_handle {
   bool gemm_lowp = false;   // the GEMMs being enqueued take bf16-rounded operands (scoring, bf16 mode)
   int64_t cap_D = 0, cap_Q = 0, cap_V = 0;
   cudaStream_t st2 = nullptr, st_cap = nullptr, st3 = nullptr, st4 = nullptr;
+  // st5: the DAG backward's weight gradients (dW = dY^T X, bias column sums) -- they feed only the
+  // dense Adam, so they run beside the dX chain; w_used: st5 joined the step, ev_wjoin its end
+  cudaStream_t st5 = nullptr;
+  cudaEvent_t ev_wjoin = nullptr;
+  bool w_used = false;
   cudaEvent_t ev_rel = nullptr, ev_loss = nullptr, ev_early = nullptr;
   cudaEvent_t ev_i1 = nullptr, ev_i2 = nullptr;   // fork / join of the two Q2B intersection branches
   cudaEvent_t ev_fork = nullptr, ev_fork2 = nullptr, ev_join = nullptr;
@@ -536,7 +541,8 @@ struct kg_handle {
   };
   std::vector<GraphEntry> graphs;
   bool use_graphs = true;
-  bool gemm_drain = true, side = false, use_pdl = true;
+  bool gemm_drain = true, use_pdl = true;
+  int side = 0;   // the stream the GEMMs are enqueued on: 0 st, 1 st3, 2 st5 (split-K scratch)
   // row-sharded exchange (world > 1, k_dist.cu)
   ncclComm_t comm = nullptr;
   ncclComm_t comm2 = nullptr;  // world > 1: the dense all-reduce's own communicator (on st2, overlapped)
@@ -773,6 +779,7 @@ void carve(kg_handle *h, Arena &A) {
     h->gsP_cap = std::min<int64_t>(16LL << 20, 8LL * 4 * Mx * wide);
     h->gsP = A.take<float>(h->gsP_cap);
     h->gsP2 = A.take<float>(h->gsP_cap);
+    h->gsP3 = A.take<float>(h->gsP_cap);
   }
   {
     static const char *kWNames[] = {"prj_W1", "prj_W2", "prj_W0", "ds_W1", "ds_W2", "off_W1", "off_W2",
@@ -836,25 +843,45 @@ kg_status gemm(kg_handle *h, bool ta, bool tb, int m, int n, int k, const float 
   if (B_lo) CK(cudaStreamWaitEvent(h->st, tb_t ? h->ev_wsplit_t : h->ev_wsplit, 0));   // this step's planes (st3)
   g.B_lo = B_lo;
   g.mask = mask;
-  if (k <= 0 || !launch_gemm_tc(g, h->side ? h->gsP2 : h->gsP, h->gsP_cap, h->st))
+  float *scr = h->side == 2 ? h->gsP3 : h->side == 1 ? h->gsP2 : h->gsP;
+  if (k <= 0 || !launch_gemm_tc(g, scr, h->gsP_cap, h->st))
     return fail(h, KG_EUNSUPPORTED, "tensor-core GEMM: operands must be 16-byte aligned with ld % 4 == 0 and K > 0 "
                                     "(and cuTensorMapEncodeTiled available)");
   h->gemm_count++;
   return KG_OK;
 }
+// Y = X W^T (X [m][k] with ld lda, W [n][k]) as raw split-K partial products in the stream's
+// split-K scratch (*P, [splits][m][n]); returns the split count, 0 on failure.  The consumer
+// kernel (k_dag.cu *_red) sums the splits, adds the bias and pools (fused epilogue).
+int gemm_raw(kg_handle *h, int m, int n, int k, const float *A, int lda, const float *B, int ldb, const float **P) {
+  GemmArgs g;
+  g.A = A; g.B = B; g.M = m; g.N = n; g.K = k; g.lda = lda; g.ldb = ldb; g.ldc = n;
+  g.drain = h->gemm_drain && !h->gemm_lowp;
+  float *scr = h->side == 2 ? h->gsP3 : h->side == 1 ? h->gsP2 : h->gsP;
+  const int s = launch_gemm_tc_raw(g, scr, h->gsP_cap, h->st);
+  if (s > 0) h->gemm_count++;
+  *P = scr;
+  return s;
+}
+#define GR(var, ...)                                                                           \
+  do {                                                                                         \
+    var = gemm_raw(h, __VA_ARGS__);                                                            \
+    if (var <= 0) return fail(h, KG_EUNSUPPORTED, "tensor-core GEMM (raw partials) not launched"); \
+  } while (0)
 // Run the following GEMMs / kernels on another stream (restored on scope exit).
 // The side stream gets its own cuBLAS handle (own workspace) and its own tensor-core GEMM
 // split-K scratch, so the two branches cannot race on scratch memory.
 struct OnStream {
   kg_handle *h;
   cudaStream_t prev;
-  OnStream(kg_handle *hh, cudaStream_t s) : h(hh), prev(hh->st) {
+  int prev_side;
+  OnStream(kg_handle *hh, cudaStream_t s, int which = 1) : h(hh), prev(hh->st), prev_side(hh->side) {
     h->st = s;
-    h->side = true;
+    h->side = which;
   }
   ~OnStream() {
     h->st = prev;
-    h->side = false;
+    h->side = prev_side;
   }
 };
 // Programmatic dependent launch inside the step graph: every edge between two of this
@@ -911,9 +938,32 @@ kg_status join(kg_handle *h, cudaStream_t from, cudaStream_t to) {
   return KG_OK;
 }
 
+// Weight gradients on st5 (off the dX chain): wfork(from) makes st5 wait for everything enqueued
+// on `from` so far; the GEMMs enqueued inside a WOn scope go to st5 with its own split-K scratch.
+kg_status wfork(kg_handle *h, cudaStream_t from) {
+  h->w_used = true;
+  return fork(h, from, h->st5);
+}
+struct WOn : OnStream {
+  explicit WOn(kg_handle *hh) : OnStream(hh, hh->st5, 2) {}
+};
+// end of the DAG backward's st5 work: the stream that runs the dense Adam waits for ev_wjoin
+kg_status wjoin(kg_handle *h, cudaStream_t to) {
+  if (!h->w_used) return KG_OK;
+  h->w_used = false;
+  CK(cudaEventRecord(h->ev_wjoin, h->st5));
+  CK(cudaStreamWaitEvent(to, h->ev_wjoin, 0));
+  return KG_OK;
+}
+
 #define G(...)                                   \
   do {                                           \
     kg_status s_ = gemm(h, __VA_ARGS__);         \
+    if (s_ != KG_OK) return s_;                  \
+  } while (0)
+#define WF(from)                                 \
+  do {                                           \
+    kg_status s_ = wfork(h, from);               \
     if (s_ != KG_OK) return s_;                  \
   } while (0)
 
@@ -963,10 +1013,14 @@ kg_status dag_forward(kg_handle *h, StepBufs &S) {
       }
       G(false, true, GM, HH, 2 * d, X, 2 * d, dp(h, "prj_W1"), 2 * d, 0.f, H1, HH, dp(h, "prj_b1"), 1);
       G(false, true, GM, HH, HH, H1, HH, dp(h, "prj_W2"), HH, 0.f, H2, HH, dp(h, "prj_b2"), 1);
-      G(false, true, GM, d, HH, H2, HH, dp(h, "prj_W0"), HH, 0.f, h->pZ, d, nullptr, 0);
-      for (int k = ni; k < nj; ++k)
-        launch_betae_proj_out(h->pZ + (int64_t)(k - ni) * M * d, dp(h, "prj_b0"), M, d,
-                              h->pZp1 + (int64_t)(u + k - ni) * M * d, S.val[k], st);
+      {
+        const float *P = nullptr;
+        int sp = 0;
+        GR(sp, GM, d, HH, H2, HH, dp(h, "prj_W0"), HH, &P);   // Z, its epilogue fused below
+        OutPtrs op{};
+        for (int k = ni; k < nj; ++k) op.p[k - ni] = S.val[k];
+        launch_betae_proj_out_red(P, sp, dp(h, "prj_b0"), GM, M, d, h->pZp1 + (int64_t)u * M * d, op, st);
+      }
       u += nj - ni;
       ni = nj - 1;
       continue;
@@ -990,9 +1044,11 @@ kg_status dag_forward(kg_handle *h, StepBufs &S) {
       const int n = nd.nin, NR = n * M;
       float *out = S.val[ni];
       float **T = h->T;
+      const float *P = nullptr;
+      int sp = 0;
       if (h->deepset) {
-        G(false, true, NR, d, d, h->stack_v, d, dp(h, "ds_W1"), d, 0.f, T[0], d, dp(h, "ds_b1"), 1);   // H
-        launch_mean_stack(T[0], n, M, d, T[1], st);                                  // Mn
+        GR(sp, NR, d, d, h->stack_v, d, dp(h, "ds_W1"), d, &P);
+        launch_mean_red(P, sp, dp(h, "ds_b1"), n, M, d, T[0], T[1], st);              // H, Mn
         G(false, true, M, d, d, T[1], d, dp(h, "ds_W2"), d, 0.f, out, d, dp(h, "ds_b2"), 0);
         if (h->qnorm) launch_qnorm_fwd(out, M, d, h->qnorm, h->qn + (int64_t)ni * 2 * h->Mx, st);   // A27
       } else if (h->kind == KG_Q2B) {
@@ -1001,19 +1057,21 @@ kg_status dag_forward(kg_handle *h, StepBufs &S) {
         if (fs) return fs;
         {
           OnStream os(h, h->st3);
-          G(false, true, NR, d, d, h->stack_v + d, 2 * d, dp(h, "off_W1"), d, 0.f, T[3], d, dp(h, "off_b1"), 1);  // Ho
-          launch_mean_stack(T[3], n, M, d, T[4], h->st3);                                                         // Mo
-          G(false, true, M, d, d, T[4], d, dp(h, "off_W2"), d, 0.f, T[5], d, dp(h, "off_b2"), 0);                 // Z
-          launch_q2b_off_fwd(h->stack_v, T[5], n, M, d, T[6], h->amin, out, h->st3);  // sig, amin, offset
+          const float *P3 = nullptr;
+          int sp3 = 0;
+          GR(sp3, NR, d, d, h->stack_v + d, 2 * d, dp(h, "off_W1"), d, &P3);
+          launch_mean_red(P3, sp3, dp(h, "off_b1"), n, M, d, T[3], T[4], h->st3);                  // Ho, Mo
+          GR(sp3, M, d, d, T[4], d, dp(h, "off_W2"), d, &P3);
+          launch_q2b_off_red(P3, sp3, dp(h, "off_b2"), h->stack_v, n, M, d, T[6], h->amin, out, h->st3);  // sig, amin, offset
         }
         G(false, true, NR, d, d, h->stack_v, 2 * d, dp(h, "att_W1"), d, 0.f, T[0], d, dp(h, "att_b1"), 1);  // Hc
-        G(false, true, NR, d, d, T[0], d, dp(h, "att_W2"), d, 0.f, T[1], d, dp(h, "att_b2"), 0);           // Lg
-        launch_q2b_att_fwd(h->stack_v, T[1], n, M, d, T[2], out, st);                  // a, center
+        GR(sp, NR, d, d, T[0], d, dp(h, "att_W2"), d, &P);
+        launch_q2b_att_red(P, sp, dp(h, "att_b2"), h->stack_v, n, M, d, T[2], out, st);        // a, center
         if ((fs = join(h, h->st3, st)) != KG_OK) return fs;
       } else if (h->kind == KG_BETAE) {
         G(false, true, NR, d, d, h->stack_v, d, dp(h, "att_U1"), d, 0.f, T[0], d, dp(h, "att_c1"), 1);     // Hs
-        G(false, true, NR, m, d, T[0], d, dp(h, "att_U2"), d, 0.f, T[1], m, dp(h, "att_c2"), 0);           // Lg
-        launch_beta_att_fwd(h->stack_v, T[1], n, M, d, T[2], out, st);                 // w, out
+        GR(sp, NR, m, d, T[0], d, dp(h, "att_U2"), d, &P);
+        launch_beta_att_red(P, sp, dp(h, "att_c2"), h->stack_v, n, M, d, T[2], out, st);      // w, out
       }
     }
   }
@@ -1033,7 +1091,7 @@ kg_status dag_forward(kg_handle *h, StepBufs &S) {
 }
 
 // -------------------------------------------------------------- backward DAG
-kg_status dag_backward(kg_handle *h, StepBufs &S) {
+kg_status dag_backward(kg_handle *h, StepBufs &S, bool defer_wjoin = false) {
   const Plan &p = S.plan;
   if (needs_wplanes(h, p) && !h->wsplit_issued) {
     kg_status ws = issue_wplanes(h, h->st, h->st3);
@@ -1096,12 +1154,19 @@ kg_status dag_backward(kg_handle *h, StepBufs &S) {
       if (h->deepset) {
         // T0 = H, T1 = Mn (forward);  T7 = dMn, T8 = dH
         if (h->qnorm) launch_qnorm_bwd(S.grad[ni], S.val[ni], M, d, h->qnorm, h->qn + (int64_t)ni * 2 * h->Mx, st);
+        WF(st);
+        { WOn w(h); G(true, false, d, d, M, gout, d, T[1], d, 0.f, gp(h, "ds_W2"), d); }
         G(false, true, M, d, d, gout, d, wt(h, "ds_W2"), d, 0.f, T[7], d, nullptr, 0, 1.f, wtlo(h, "ds_W2"), true);
-        G(true, false, d, d, M, gout, d, T[1], d, 0.f, gp(h, "ds_W2"), d);
-        launch_colsum(gout, M, d, d, gp(h, "ds_b2"), st);
         launch_gqe_inter_dh(T[7], T[0], n, M, d, T[8], st);
-        G(true, false, d, d, NR, T[8], d, h->stack_v, d, 0.f, gp(h, "ds_W1"), d);
-        launch_colsum(T[8], NR, d, d, gp(h, "ds_b1"), st);
+        WF(st);
+        {
+          WOn w(h);
+          G(true, false, d, d, NR, T[8], d, h->stack_v, d, 0.f, gp(h, "ds_W1"), d);
+          ColsumJobs cj;
+          cj.add(gout, M, d, d, gp(h, "ds_b2"));
+          cj.add(T[8], NR, d, d, gp(h, "ds_b1"));
+          launch_colsum_multi(cj, h->st5);
+        }
         G(false, true, NR, d, d, T[8], d, wt(h, "ds_W1"), d, 0.f, h->stack_g, d, nullptr, 0, 1.f, wtlo(h, "ds_W1"), true);
       } else if (h->kind == KG_Q2B) {
         // forward: T0 Hc, T1 Lg, T2 a, T3 Ho, T4 Mo, T5 Z, T6 sig.  backward: T7 dLg, T8 dHc, T9 dZ, T10 dMo, T11 dHo
@@ -1112,32 +1177,49 @@ kg_status dag_backward(kg_handle *h, StepBufs &S) {
           OnStream os(h, h->st3);
           cudaStream_t s3 = h->st3;
           launch_q2b_off_bwd(h->stack_v, T[6], h->amin, gout, n, M, d, T[9], h->stack_g, s3);
+          WF(s3);
+          { WOn w(h); G(true, false, d, d, M, T[9], d, T[4], d, 0.f, gp(h, "off_W2"), d); }
           G(false, true, M, d, d, T[9], d, wt(h, "off_W2"), d, 0.f, T[10], d, nullptr, 0, 1.f, wtlo(h, "off_W2"), true);
-          G(true, false, d, d, M, T[9], d, T[4], d, 0.f, gp(h, "off_W2"), d);
-          launch_colsum(T[9], M, d, d, gp(h, "off_b2"), s3);
           launch_gqe_inter_dh(T[10], T[3], n, M, d, T[11], s3);
-          G(true, false, d, d, NR, T[11], d, h->stack_v + d, 2 * d, 0.f, gp(h, "off_W1"), d);
-          launch_colsum(T[11], NR, d, d, gp(h, "off_b1"), s3);
+          WF(s3);
+          { WOn w(h); G(true, false, d, d, NR, T[11], d, h->stack_v + d, 2 * d, 0.f, gp(h, "off_W1"), d); }
           G(false, true, NR, d, d, T[11], d, wt(h, "off_W1"), d, 1.f, h->stack_g + d, 2 * d, nullptr, 0, 1.f, wtlo(h, "off_W1"), true);
         }
         launch_q2b_att_bwd(h->stack_v, T[2], gout, n, M, d, T[7], h->stack_g, st);
+        WF(st);
+        { WOn w(h); G(true, false, d, d, NR, T[7], d, T[0], d, 0.f, gp(h, "att_W2"), d); }
         G(false, true, NR, d, d, T[7], d, wt(h, "att_W2"), d, 0.f, T[8], d, nullptr, 0, 1.f, wtlo(h, "att_W2"), true,
           T[0]);
-        G(true, false, d, d, NR, T[7], d, T[0], d, 0.f, gp(h, "att_W2"), d);
-        launch_colsum(T[7], NR, d, d, gp(h, "att_b2"), st);
-        G(true, false, d, d, NR, T[8], d, h->stack_v, 2 * d, 0.f, gp(h, "att_W1"), d);
-        launch_colsum(T[8], NR, d, d, gp(h, "att_b1"), st);
+        WF(st);
+        {
+          // st5 already waits for the offset branch's dZ / dHo (forked from st3 above, enqueued first)
+          WOn w(h);
+          G(true, false, d, d, NR, T[8], d, h->stack_v, 2 * d, 0.f, gp(h, "att_W1"), d);
+          ColsumJobs cj;
+          cj.add(T[7], NR, d, d, gp(h, "att_b2"));
+          cj.add(T[8], NR, d, d, gp(h, "att_b1"));
+          cj.add(T[9], M, d, d, gp(h, "off_b2"));
+          cj.add(T[11], NR, d, d, gp(h, "off_b1"));
+          launch_colsum_multi(cj, h->st5);
+        }
         G(false, true, NR, d, d, T[8], d, wt(h, "att_W1"), d, 1.f, h->stack_g, 2 * d, nullptr, 0, 1.f, wtlo(h, "att_W1"), true);
         if ((fs = join(h, h->st3, st)) != KG_OK) return fs;
       } else if (h->kind == KG_BETAE) {
         // forward: T0 Hs, T1 Lg, T2 w.  backward: T7 dLg, T8 dHs
         launch_beta_att_bwd(h->stack_v, T[2], gout, n, M, d, T[7], h->stack_g, st);
+        WF(st);
+        { WOn w(h); G(true, false, m, d, NR, T[7], m, T[0], d, 0.f, gp(h, "att_U2"), d); }
         G(false, true, NR, d, m, T[7], m, wt(h, "att_U2"), m, 0.f, T[8], d, nullptr, 0, 1.f, wtlo(h, "att_U2"), true,
           T[0]);
-        G(true, false, m, d, NR, T[7], m, T[0], d, 0.f, gp(h, "att_U2"), d);
-        launch_colsum(T[7], NR, m, m, gp(h, "att_c2"), st);
-        G(true, false, d, d, NR, T[8], d, h->stack_v, d, 0.f, gp(h, "att_U1"), d);
-        launch_colsum(T[8], NR, d, d, gp(h, "att_c1"), st);
+        WF(st);
+        {
+          WOn w(h);
+          G(true, false, d, d, NR, T[8], d, h->stack_v, d, 0.f, gp(h, "att_U1"), d);
+          ColsumJobs cj;
+          cj.add(T[7], NR, m, m, gp(h, "att_c2"));
+          cj.add(T[8], NR, d, d, gp(h, "att_c1"));
+          launch_colsum_multi(cj, h->st5);
+        }
         G(false, true, NR, d, d, T[8], d, wt(h, "att_U1"), d, 1.f, h->stack_g, d, nullptr, 0, 1.f, wtlo(h, "att_U1"), true);
       }
     }
@@ -1145,14 +1227,21 @@ kg_status dag_backward(kg_handle *h, StepBufs &S) {
   if (h->kind == KG_BETAE) {
     // projection-MLP weight gradients over all projection uses at once (A9)
     const int NR = p.nproj * M, ldT = (int)align_up(NR, 4);
-    CK(cudaStreamWaitEvent(st, h->ev_xt, 0));   // the transposed inputs (DAG forward, st4)
+    WF(st);
+    WOn w(h);
+    CK(cudaStreamWaitEvent(h->st5, h->ev_xt, 0));   // the transposed inputs (DAG forward, st4)
     G(true, true, d, HH, NR, h->pdZ, d, h->pH2T, ldT, 0.f, gp(h, "prj_W0"), HH);
-    launch_colsum(h->pdZ, NR, d, d, gp(h, "prj_b0"), st);
     G(true, true, HH, HH, NR, h->pdH2, HH, h->pH1T, ldT, 0.f, gp(h, "prj_W2"), HH);
-    launch_colsum(h->pdH2, NR, HH, HH, gp(h, "prj_b2"), st);
     G(true, true, HH, 2 * d, NR, h->pdH1, HH, h->pXT, ldT, 0.f, gp(h, "prj_W1"), 2 * d);
-    launch_colsum(h->pdH1, NR, HH, HH, gp(h, "prj_b1"), st);
+    ColsumJobs cj;
+    cj.add(h->pdZ, NR, d, d, gp(h, "prj_b0"));
+    cj.add(h->pdH2, NR, HH, HH, gp(h, "prj_b2"));
+    cj.add(h->pdH1, NR, HH, HH, gp(h, "prj_b1"));
+    launch_colsum_multi(cj, h->st5);
   }
+  // the weight gradients on st5 join `st` here, or (defer_wjoin) the caller joins them into
+  // the stream of the dense Adam (wjoin)
+  if (!defer_wjoin) return wjoin(h, st);
   return KG_OK;
 }
 
@@ -1441,6 +1530,8 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
   if (cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->st_cap, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->st3, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&h->st5, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_wjoin, cudaEventDisableTiming) != cudaSuccess ||
       cudaStreamCreateWithPriority(&h->st4, cudaStreamNonBlocking, kLowPriority()) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_rel, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_loss, cudaEventDisableTiming) != cudaSuccess ||
@@ -1634,6 +1725,13 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   }
   launch_rel_occ(h->b_rels, M, nr, sl, p.nproj, h->R, h->rocc, h->flags + 1, st);
   if (needs_wplanes(h, p) && (s = issue_wplanes(h, st, h->st4)) != KG_OK) return s;
+  const int64_t *neg_rows = h->rows + (int64_t)na * M + M;
+  if (h->kind == KG_BETAE && K > 0) {
+    // the pool's Beta features (digamma / trigamma planes) depend only on the gathered rows:
+    // on st3 beside the DAG forward, joined before the scoring
+    if ((s = fork(h, st, h->st3)) != KG_OK) return s;
+    launch_beta_entity(h->ent_src, neg_rows, K, h->m, h->F, h->Cv, h->st3);
+  }
   CK(cudaEventRecord(h->ev_fork, st));
   CK(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
   launch_dedup(h->ids, nullptr, L, h->ent_bits, h->uniq, h->inv, h->perm, h->seg, h->Udev, h->st2, h->sinv, h->hrow);
@@ -1648,17 +1746,21 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
 
   // a8-a10: scoring, Eq. 1, scoring backward
   const int U = (h->sk == KG_BETAE || h->sk == KG_ROTATE || h->sk == KG_COMPLEX) ? h->m : d;
-  const int64_t *neg_rows = h->rows + (int64_t)na * M + M;
   const float scale = 1.f / (float)((double)M * h->world);
   if (h->kind == KG_BETAE) {
     launch_beta_query(h->Q, S.NQ, h->m, h->QP, h->Cq, st);
-    launch_beta_entity(h->ent_src, neg_rows, K, h->m, h->F, h->Cv, st);
+    if (K > 0 && (s = join(h, h->st3, st)) != KG_OK) return s;   // beta_entity (st3)
   }
   PosArgs pa;
   pa.M = M; pa.U = U; pa.d = d; pa.ent = h->ent_src; pa.ans_rows = h->rows + (int64_t)na * M; pa.Q = h->Q;
   pa.alpha = h->cfg.box_alpha; pa.gamma = h->cfg.gamma; pa.scale = scale; pa.Cq = h->Cq; pa.QP = h->QP;
   pa.loss_pos = h->loss_pos; pa.Dpos = h->Dpos; pa.dQ = h->dQ; pa.dV = h->OG + (int64_t)na * M * d;
-  launch_pos(h->sk, pa, p.nout, st);
+  // the positive term (D+, its adjoint and gradients: per query): BetaE's (digamma / lgamma
+  // per unit) beside the pool scoring on st3; the light ones in order (run beside pair_fwd they
+  // slowed it more than they took: C5-q2b scoring forward 57 -> 62 us)
+  const bool pos_side = h->kind == KG_BETAE;
+  if (pos_side && (s = fork(h, st, h->st3)) != KG_OK) return s;
+  launch_pos(h->sk, pa, p.nout, pos_side ? h->st3 : st);
   ScoreArgs sa;
   sa.Q = h->Q; sa.NQ = S.NQ; sa.M = M; sa.K = K; sa.Kp = S.Kp; sa.U = U; sa.d = d;
   if (h->kind == KG_BETAE) { sa.E = h->F; sa.eidx = nullptr; sa.estride = 9LL * h->m; }
@@ -1671,6 +1773,7 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   sa.dV = h->OG + (int64_t)(na * M + M) * d;
   const int njt = K > 0 ? 1 : 0;
   if (K > 0 && (s = score_forward(h, sa, p.nout, true, neg_rows)) != KG_OK) return s;
+  if (pos_side && (s = join(h, h->st3, st)) != KG_OK) return s;
   launch_loss_finalize(h->loss_pos, h->loss_part, M, njt, 1.0 / ((double)M * h->world), h->loss_dev, h->flags,
                        h->t_dev, h->bc, h->cfg.beta1, h->cfg.beta2, h->apply, st);
   mark(h, 3);
@@ -1700,8 +1803,8 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   CK(cudaEventRecord(h->ev_join, h->st2));
   mark(h, 4);
 
-  // a11: DAG backward
-  if ((s = dag_backward(h, S)) != KG_OK) return s;
+  // a11: DAG backward (its weight gradients join the dense Adam's stream below)
+  if ((s = dag_backward(h, S, /*defer_wjoin=*/true)) != KG_OK) return s;
   if (p.inter < 0 && h->kind != KG_BETAE && h->w_off < h->dense_size)
     CK(cudaMemsetAsync(h->gdense, 0, sizeof(float) * (h->dense_size - h->w_off), st));
   if (p.inter < 0 && h->kind == KG_BETAE) {   // attention weights unused by this structure
@@ -1720,6 +1823,7 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   {
     cudaStream_t s2 = h->st2;
     mark(h, 8, s2);
+    if ((s = wjoin(h, s2)) != KG_OK) return s;
     launch_rel_reduce(h->rseg, h->rperm, h->rinv, h->rU, Lr, h->RG, h->PSr, h->dr, h->RGU, s2);
     if (h->apply) {
       const double b1 = h->cfg.beta1, b2 = h->cfg.beta2, eps = h->cfg.eps;
@@ -2433,12 +2537,14 @@ kg_status kg_test_gemm(int32_t ta, int32_t tb, int32_t M, int32_t N, int32_t K, 
   GemmArgs g;
   g.A = A; g.B = B; g.C = C; g.bias = bias; g.M = M; g.N = N; g.K = K; g.lda = lda; g.ldb = ldb; g.ldc = ldc;
   g.relu = relu & 1; g.beta = beta; g.a_mn = ta != 0; g.b_mn = tb != 0; g.drain = (relu & 2) != 0;
-  g.force = relu >> 2;   // tile experiments (tools/gemm_tiles.py)
+  g.force = (relu >> 2) & 63;   // tile experiments (tools/gemm_tiles.py, tools/gemm_events.py)
+  const int reps = std::max(1, relu >> 8);   // back-to-back launches (event timing, tools/gemm_events.py)
   if (!gemm_tc_accepts(g)) return KG_EINVAL;   // 16-byte aligned operands with ld % 4 == 0
   float *sP = nullptr;
   const int64_t pcap = 8LL * std::max(M, 1) * std::max(N, 1);
   if (cudaMalloc(&sP, sizeof(float) * pcap) != cudaSuccess) return KG_ENOMEM;
-  const bool launched = launch_gemm_tc(g, sP, pcap, st);
+  bool launched = true;
+  for (int r = 0; r < reps && launched; ++r) launched = launch_gemm_tc(g, sP, pcap, st);
   const cudaError_t e = cudaStreamSynchronize(st);
   cudaFree(sP);
   if (!launched) return KG_EUNSUPPORTED;   // tensor map encoding failed
@@ -2482,6 +2588,8 @@ void kg_destroy(kg_handle *h) {
   if (h->st_cap) cudaStreamDestroy(h->st_cap);
   if (h->st3) { cudaStreamSynchronize(h->st3); cudaStreamDestroy(h->st3); }
   if (h->st4) { cudaStreamSynchronize(h->st4); cudaStreamDestroy(h->st4); }
+  if (h->st5) { cudaStreamSynchronize(h->st5); cudaStreamDestroy(h->st5); }
+  if (h->ev_wjoin) cudaEventDestroy(h->ev_wjoin);
   if (h->ev_i1) cudaEventDestroy(h->ev_i1);
   if (h->ev_i2) cudaEventDestroy(h->ev_i2);
   for (auto &g : h->graphs) cudaGraphExecDestroy(g.exec);

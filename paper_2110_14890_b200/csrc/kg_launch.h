@@ -89,6 +89,13 @@ void launch_dense_adam_rel_touched(float *p, float *m, float *v, int R, int widt
 void launch_dense_adam(float *p, float *m, float *v, const float *g, int64_t n, const float *lr, double beta1,
                        double beta2, double eps, const float *bc, const int *flags, cudaStream_t st);
 void launch_colsum(const float *X, int rows, int cols, int ld, float *out, cudaStream_t st);
+struct ColsumJob { const float *X; int rows, cols, ld; float *out; };
+struct ColsumJobs {
+  ColsumJob j[6];
+  int n = 0;
+  void add(const float *X, int rows, int cols, int ld, float *out) { j[n++] = ColsumJob{X, rows, cols, ld, out}; }
+};
+void launch_colsum_multi(const ColsumJobs &J, cudaStream_t st);   // out_i[c] = sum_r X_i[r][c], one launch
 
 // k_gemm.cu: C[M][N] = beta C + op(A) op(B)^T (+ bias) (ReLU), op(A) [M][K], op(B) [N][K];
 // tcgen05 kind::tf32 with a 3xTF32 split; A stored [M][lda], B stored [N][ldb] (K-major).
@@ -118,6 +125,18 @@ struct WSplitJobs { WSplitJob j[12]; int n = 0; };
 void launch_wsplit(const WSplitJobs &J, int part, cudaStream_t st);   // pre-split weight planes: 0 lo, 1 t + tlo
 bool gemm_tc_accepts(const GemmArgs &g);   // 16-byte aligned operands, ld % 4 == 0
 bool launch_gemm_tc(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st);   // false: not launched
+int launch_gemm_tc_raw(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st);   // splits, 0: not launched
+// k_dag.cu: GEMM epilogues fused with the intersection's pooling (P = raw partials [S][rows][d])
+void launch_mean_red(const float *P, int S, const float *b, int n, int M, int d, float *H, float *Mn, cudaStream_t st);
+void launch_q2b_off_red(const float *P, int S, const float *b, const float *stack, int n, int M, int d, float *sig,
+                        int8_t *amin, float *out, cudaStream_t st);
+void launch_q2b_att_red(const float *P, int S, const float *b, const float *stack, int n, int M, int d, float *a,
+                        float *out, cudaStream_t st);
+struct OutPtrs { float *p[4]; };
+void launch_betae_proj_out_red(const float *P, int S, const float *b0, int rows, int M, int d, float *Zp1,
+                               const OutPtrs &out, cudaStream_t st);
+void launch_beta_att_red(const float *P, int S, const float *b, const float *stack, int n, int M, int d, float *w,
+                         float *out, cudaStream_t st);
 void launch_transpose(const float *in, int R, int Cc, int ld_in, float *out, int ld_out, cudaStream_t st);
 
 // k_eval.cu (evaluation path, App. F)
