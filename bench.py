@@ -117,8 +117,10 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ algorithmic work
 def pair_flops_per_unit(kind):
-    """FP32 ops per (query, candidate, unit) of the distance, forward; backward counted as 2x."""
-    return {"q2b": 7, "betae": 6, "gqe": 3, "transe": 3, "rotate": 8, "distmult": 2, "complex": 4}[kind]
+    """FP32 ops per (query, candidate, unit) of the distance, forward; backward counted as 2x.
+    Q2B: 6 (t = v - c, |t|, |t| - o, ReLU, min(|t|, o), + alpha * min: SURVEY §8(d)'s 9.0 MFLOP
+    per C5 query = 3 x 6 x K x d x the DNF mix 11/9)."""
+    return {"q2b": 6, "betae": 6, "gqe": 3, "transe": 3, "rotate": 8, "distmult": 2, "complex": 4}[kind]
 
 
 def stage_work(cfg, M, K, structure, U, d):

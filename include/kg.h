@@ -203,6 +203,18 @@ kg_status kg_result(kg_handle *h, kg_step_info *info);
 kg_status kg_score(kg_handle *h, const kg_batch *queries, const int64_t *cand, int32_t n_cand,
                    float *out_dist);
 
+/* Per-query candidates (SURVEY §8(b) sketch, `shared = 0`): Dist(f(q_i), f(v)) of every
+ * query of `queries` (forward DAG only) to ITS OWN candidates: cand host [M][n_cand] (row i =
+ * query i's candidates, any ids in [0, n_entities), duplicates allowed), out_dist host
+ * [M][n_cand], lower = closer, unions = DNF min (A11).  n_cand >= 1 and n_cand * M <= 2^31.
+ * One CTA per query (k_eval.cu score_each_kernel: a row gather of n_cand rows per query plus
+ * the distance arithmetic -- nothing is shared across queries, so no pair tiling); the
+ * distances equal kg_score's up to fp32 summation order.  world > 1: collective as kg_score
+ * (candidate rows fetched from their owners).  Errors: EINVAL (pointer / size / id),
+ * EUNSUPPORTED (structure not valid for the kind).  Synchronises the stream. */
+kg_status kg_score_each(kg_handle *h, const kg_batch *queries, const int64_t *cand, int32_t n_cand,
+                        float *out_dist);
+
 /* Evaluation path (App. F, reading A26): filtered rank of every missing
  * answer of every query and the per-query metrics.  queries: structure, M (<= max_M),
  * anchors, relations (host or device per on_device).  ans_off host [M+1] (ans_off[0] = 0,

@@ -38,11 +38,11 @@ paper" for their exact architecture).
 """
 from .model import (anchor_query, embed_entity, project, intersect, distance, negate,
                     query_disjuncts, dense_views)
-from .step import (dedup, adam, SparseTable, oracle_step, oracle_score, StepResult,
+from .step import (dedup, adam, SparseTable, oracle_step, oracle_score, oracle_score_each, StepResult,
                    softplus, query_loss_terms)
 from .eval import ranks_from_distances, metrics_from_ranks, oracle_eval
 
 __all__ = ["anchor_query", "embed_entity", "project", "intersect", "distance", "negate",
            "query_disjuncts", "dense_views", "dedup", "adam", "SparseTable",
-           "oracle_step", "oracle_score", "StepResult", "softplus", "query_loss_terms",
+           "oracle_step", "oracle_score", "oracle_score_each", "StepResult", "softplus", "query_loss_terms",
            "ranks_from_distances", "metrics_from_ranks", "oracle_eval"]

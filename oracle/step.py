@@ -217,3 +217,28 @@ def oracle_score(cfg: kggen.ModelConfig, table: SparseTable, batch: dict, cand) 
                              for q in qs]).min(dim=0).values
             out[lo:hi] = D.numpy()
     return out
+
+
+def oracle_score_each(cfg: kggen.ModelConfig, table: SparseTable, batch: dict, cand) -> np.ndarray:
+    """Per-query candidates (SURVEY §8(b) kg_score with shared = 0): D[i, c] = Dist(f(q_i),
+    f(v_{cand[i, c]})) with the DNF min over q_i's disjuncts (A11); cand [M][n_cand].
+    Written out query by query (a plain loop over i), no tiling."""
+    structure = batch["structure"]
+    cand = np.asarray(cand, np.int64)
+    M, n = cand.shape
+    with torch.no_grad():
+        theta = torch.tensor(table.dense, dtype=F64)
+        P = dense_views(cfg, theta)
+        anchors_ids = np.asarray(batch["anchors"], np.int64)
+        anchors = [torch.tensor(table.get(anchors_ids[:, a])[0], dtype=F64)
+                   for a in range(anchors_ids.shape[1])]
+        rels = np.asarray(batch["relations"])
+        rel = [torch.as_tensor(rels[:, s].astype(np.int64)) for s in range(rels.shape[1])]
+        qs = query_disjuncts(structure, cfg.kind, anchors, rel, P)
+        out = np.empty((M, n))
+        for i in range(M):
+            V = torch.tensor(table.get(cand[i])[0], dtype=F64)          # this query's candidates
+            D = torch.stack([distance(cfg.kind, q[i:i + 1], V, cfg.box_alpha) for q in qs]).min(dim=0).values
+            out[i] = D.numpy()
+    return out
+

@@ -99,6 +99,42 @@ __global__ void __launch_bounds__(256) eval_rank_kernel(EvalArgs a) {
   }
 }
 
+// kg_score_each: out[i][c] = D(q_i, v_cand[i][c]) (DNF min over the disjuncts, A11); one CTA per
+// query, one warp per candidate (the distance of eval_rank_kernel)
+template <int KIND, int NOUT>
+__global__ void __launch_bounds__(256) score_each_kernel(EvalArgs a) {
+  KG_GRID_DEP_WAIT();
+  const int i = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int nc = a.n_neg;
+  const int qstride = (KIND == KG_Q2B ? 2 : 1) * a.d;
+  for (int c = warp; c < nc; c += nw) {
+    const float *e = a.ent + a.negatives[(int64_t)i * nc + c] * a.d;
+    float D = warp_dist<KIND>(a.Q + (int64_t)i * qstride, e, a.U, a.alpha, lane);
+#pragma unroll
+    for (int t = 1; t < NOUT; ++t)
+      D = fminf(D, warp_dist<KIND>(a.Q + ((int64_t)t * a.M + i) * qstride, e, a.U, a.alpha, lane));
+    if (lane == 0) a.metrics[(int64_t)i * nc + c] = D;
+  }
+}
+template <int KIND>
+static void launch_score_each_k(const EvalArgs &a, int nout, cudaStream_t st) {
+  if (nout == 2) score_each_kernel<KIND, 2><<<a.M, 256, 0, st>>>(a);
+  else score_each_kernel<KIND, 1><<<a.M, 256, 0, st>>>(a);
+  ++g_launches;
+}
+void launch_score_each(int kind, const EvalArgs &a, int nout, cudaStream_t st) {
+  if (a.M <= 0 || a.n_neg <= 0) return;
+  switch (kind) {
+    case KG_GQE: launch_score_each_k<KG_GQE>(a, nout, st); break;
+    case KG_Q2B: launch_score_each_k<KG_Q2B>(a, nout, st); break;
+    case KG_BETAE: launch_score_each_k<KG_BETAE>(a, nout, st); break;
+    case KG_TRANSE: launch_score_each_k<KG_TRANSE>(a, nout, st); break;
+    case KG_ROTATE: launch_score_each_k<KG_ROTATE>(a, nout, st); break;
+    case KG_DISTMULT: launch_score_each_k<KG_DISTMULT>(a, nout, st); break;
+    default: launch_score_each_k<KG_COMPLEX>(a, nout, st); break;
+  }
+}
+
 template <int KIND>
 static void launch_eval_k(const EvalArgs &a, int nout, size_t smem, cudaStream_t st) {
   if (nout == 2) {

@@ -583,7 +583,6 @@ __global__ void __launch_bounds__(G2T, 1)
             v = fmaf(g.alpha, v, bn);
             if (g.relu) v = fmaxf(v, 0.f);
             if (g.beta != 0.f) v += g.beta * *c;
-            if (g.mask && !(g.mask[(int64_t)row * g.ldc + n] > 0.f)) v = 0.f;   // ReLU backward (ldc == N)
             *c = v;
           }
         }
@@ -701,6 +700,10 @@ int launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t st
     const int64_t n4 = ((int64_t)g.M * g.N + 3) / 4;
     { gemm_reduce_kernel<<<(int)((n4 + 255) / 256), 256, 0, st>>>(part, splits, g.M, g.N, g.C, g.ldc, g.bias, g.relu,
                                                                  g.beta, g.alpha, g.mask); ++g_launches; }
+  } else if (g.mask) {
+    // a separate pass: a dependent global load per element in the epilogue's row loop was
+    // latency-bound (C5-betae 2u DAG backward 0.10 -> 0.15 ms)
+    launch_relu_mask(g.C, g.mask, g.M, g.N, st);
   }
   return splits;
 }

@@ -174,13 +174,20 @@ __device__ __forceinline__ float4 ld4(const float *p) { return *reinterpret_cast
 // 16 staged in shared memory.  blockIdx.z selects a contiguous range of units
 // (split reduction: more CTAs than the 148 SMs even at B = 512); the raw partial
 // sums go to Dpart[z][t][i][j] and pair_epi_kernel adds them in the fixed order z.
+// (A balanced one-wave schedule -- each CTA an equal run of (tile, chunk) items, a tile's
+// partials in a variable number of slots -- measured slower: C5-q2b 40 -> 47 us; likewise
+// for pair_bwd_kernel, 0.142 -> 0.147 ms per step.)
 // resident CTAs per SM of pair_fwd (KG_FWD_OCC4=1: 4 for the single-output Q2B box kernel, i.e.
-// <= 64 registers; experiment)
+// <= 64 registers: measured slower, C5-q2b scoring forward 57 -> 59 us, as was 3 per SM at 79
+// registers, 54 -> 54.4 us; the default lets the compiler take 102 registers, 2 per SM)
 #ifndef KG_FWD_OCC4
-#define KG_FWD_OCC4 1
+#define KG_FWD_OCC4 0
 #endif
 template <class Mdl, int NOUT> struct kFwdOcc {
-  static constexpr int v = (KG_FWD_OCC4 && NOUT == 1 && std::is_same<Mdl, MBox>::value) ? 4 : 1;
+  // the two-output (DNF union) Q2B kernel: 2 per SM (<= 128 registers, no spills) instead of the
+  // compiler's 132 registers at 1 per SM (8 warps per SM)
+  static constexpr int v = (KG_FWD_OCC4 && NOUT == 1 && std::is_same<Mdl, MBox>::value) ? 4
+                           : (NOUT == 2 && std::is_same<Mdl, MBox>::value) ? 2 : 1;
 };
 template <class Mdl, int NOUT>
 __global__ void __launch_bounds__(256, kFwdOcc<Mdl, NOUT>::v) pair_fwd_kernel(ScoreArgs a) {
@@ -1097,6 +1104,8 @@ static void launch_bwd(ScoreArgs a, cudaStream_t st, cudaStream_t st2) {
   const int slots = BwdOcc<Mdl>::v * 148;
   int is = std::max(1, slots / (kt * jt));
   if ((int64_t)is * kt * jt * 100 < 85LL * slots) is = (slots + kt * jt - 1) / (kt * jt);
+  // (measured at C5-q2b: 5 splits 0.136 ms, 8: 0.136, 11: 0.146, 16: 0.150 -- the finer splits'
+  // extra dV partials cost more than the better balance of 3 vs 4 CTAs per SM saves)
   is = std::max(1, std::min(is, std::min(16, chunks)));
   while (is > 1 && (int64_t)is * a.K * Mdl::AV * a.U > a.cap_V) --is;
   a.rps = ((chunks + is - 1) / is) * kIC;

@@ -1104,6 +1104,15 @@ kg_status dag_backward(kg_handle *h, StepBufs &S, bool defer_wjoin = false) {
   // projection-use index of each node
   int use[6], u = 0;
   for (int ni = 0; ni < p.nn; ++ni) use[ni] = p.n[ni].type == 0 ? u++ : -1;
+  // BetaE: the projection MLP's weight gradients group by group on st5 (beside the dX chain of
+  // the earlier groups), accumulated over the groups; one group (or row offsets TMA cannot
+  // address: M % 4 != 0): all groups at once after the chain
+  int ngroups = 0;
+  for (int ni = 0; ni < p.nn; ni = p.n[ni].type == 0 && h->kind == KG_BETAE ? p.ge[ni] : ni + 1)
+    if (p.n[ni].type == 0 && h->kind == KG_BETAE) ++ngroups;
+  const bool dw_by_group = h->kind == KG_BETAE && ngroups > 1 && (M & 3) == 0;
+  const int ldT = (int)align_up(p.nproj * M, 4);
+  bool dw_first = true;
   for (int ni = p.nn - 1; ni >= 0; --ni) {
     const PNode &nd = p.n[ni];
     if (nd.type == 0 && h->kind == KG_BETAE) {
@@ -1117,6 +1126,17 @@ kg_status dag_backward(kg_handle *h, StepBufs &S, bool defer_wjoin = false) {
         h->pH2 + (int64_t)u0 * M * HH);   // ReLU backward folded into the GEMM's combine
       G(false, true, GM, HH, HH, dH2, HH, wt(h, "prj_W2"), HH, 0.f, dH1, HH, nullptr, 0, 1.f, wtlo(h, "prj_W2"), true,
         h->pH1 + (int64_t)u0 * M * HH);
+      if (dw_by_group) {
+        WF(st);
+        WOn w(h);
+        if (dw_first) CK(cudaStreamWaitEvent(h->st5, h->ev_xt, 0));   // the transposed inputs (st4)
+        const float beta = dw_first ? 0.f : 1.f;
+        const int64_t c0 = (int64_t)u0 * M;   // this group's rows = columns of the transposed inputs
+        G(true, true, d, HH, GM, dZ, d, h->pH2T + c0, ldT, beta, gp(h, "prj_W0"), HH);
+        G(true, true, HH, HH, GM, dH2, HH, h->pH1T + c0, ldT, beta, gp(h, "prj_W2"), HH);
+        G(true, true, HH, 2 * d, GM, dH1, HH, h->pXT + c0, ldT, beta, gp(h, "prj_W1"), 2 * d);
+        dw_first = false;
+      }
       G(false, true, GM, 2 * d, HH, dH1, HH, wt(h, "prj_W1"), HH, 0.f, h->pdX, 2 * d, nullptr, 0, 1.f, wtlo(h, "prj_W1"), true);
       for (int k = n0; k <= ni; ++k) {
         const PNode &nk = p.n[k];
@@ -1226,13 +1246,15 @@ kg_status dag_backward(kg_handle *h, StepBufs &S, bool defer_wjoin = false) {
   }
   if (h->kind == KG_BETAE) {
     // projection-MLP weight gradients over all projection uses at once (A9)
-    const int NR = p.nproj * M, ldT = (int)align_up(NR, 4);
+    const int NR = p.nproj * M;
     WF(st);
     WOn w(h);
-    CK(cudaStreamWaitEvent(h->st5, h->ev_xt, 0));   // the transposed inputs (DAG forward, st4)
-    G(true, true, d, HH, NR, h->pdZ, d, h->pH2T, ldT, 0.f, gp(h, "prj_W0"), HH);
-    G(true, true, HH, HH, NR, h->pdH2, HH, h->pH1T, ldT, 0.f, gp(h, "prj_W2"), HH);
-    G(true, true, HH, 2 * d, NR, h->pdH1, HH, h->pXT, ldT, 0.f, gp(h, "prj_W1"), 2 * d);
+    if (!dw_by_group) {
+      CK(cudaStreamWaitEvent(h->st5, h->ev_xt, 0));   // the transposed inputs (DAG forward, st4)
+      G(true, true, d, HH, NR, h->pdZ, d, h->pH2T, ldT, 0.f, gp(h, "prj_W0"), HH);
+      G(true, true, HH, HH, NR, h->pdH2, HH, h->pH1T, ldT, 0.f, gp(h, "prj_W2"), HH);
+      G(true, true, HH, 2 * d, NR, h->pdH1, HH, h->pXT, ldT, 0.f, gp(h, "prj_W1"), 2 * d);
+    }
     ColsumJobs cj;
     cj.add(h->pdZ, NR, d, d, gp(h, "prj_b0"));
     cj.add(h->pdH2, NR, HH, HH, gp(h, "prj_b2"));
@@ -1767,21 +1789,25 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   else { sa.E = h->ent_src; sa.eidx = neg_rows; sa.estride = d; }
   sa.mask = h->b_mask; sa.W = (K + 31) / 32; sa.Cq = h->Cq; sa.Cv = h->Cv; sa.QP = h->QP;
   sa.gamma = h->cfg.gamma; sa.alpha = h->cfg.box_alpha; sa.scale = scale;
-  sa.C = h->C; sa.Dmin = h->Dmin; sa.loss_part = h->loss_part; sa.dQ = h->dQ;
+  sa.C = h->C; sa.Dmin = h->keep_grads ? h->Dmin : nullptr; sa.loss_part = h->loss_part; sa.dQ = h->dQ;   // D only for kg_last_grads
   sa.Dpart = h->Dpart; sa.partQ = h->partQ; sa.partV = h->partV; sa.Cpart = h->Cpart; sa.Csum = h->Csum;
   sa.cap_D = h->cap_D; sa.cap_Q = h->cap_Q; sa.cap_V = h->cap_V;
   sa.dV = h->OG + (int64_t)(na * M + M) * d;
   const int njt = K > 0 ? 1 : 0;
   if (K > 0 && (s = score_forward(h, sa, p.nout, true, neg_rows)) != KG_OK) return s;
   if (pos_side && (s = join(h, h->st3, st)) != KG_OK) return s;
+  // Eq. 1's loss, the step's fate (flags) and Adam's bias corrections: one CTA on st3, off the
+  // scoring backward's path (only the updates need it: the early dense Adam waits for ev_loss,
+  // the sparse update joins st3 before it)
+  if ((s = fork(h, st, h->st3)) != KG_OK) return s;
   launch_loss_finalize(h->loss_pos, h->loss_part, M, njt, 1.0 / ((double)M * h->world), h->loss_dev, h->flags,
-                       h->t_dev, h->bc, h->cfg.beta1, h->cfg.beta2, h->apply, st);
+                       h->t_dev, h->bc, h->cfg.beta1, h->cfg.beta2, h->apply, h->st3);
+  CK(cudaEventRecord(h->ev_loss, h->st3));
   mark(h, 3);
   // a14 (first part): the relation rows this step does not use take their Adam update with
   // g = 0 (A17) as soon as the step's fate (flags, bias corrections) is known -- a 300 MB
   // stream overlapped with the ALU-bound scoring backward; the used rows follow at the end.
   if (h->apply) {
-    CK(cudaEventRecord(h->ev_loss, st));
     CK(cudaStreamWaitEvent(h->st4, h->ev_loss, 0));
     CK(cudaStreamWaitEvent(h->st4, h->ev_rel, 0));
     mark(h, 10, h->st4);
@@ -1817,6 +1843,7 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   // theta_D (a streaming, HBM-bound pass) on the side stream; joined before the outputs.
   // Stage 5-6 = the sparse path, stage 6-7 = what the dense path adds after it.
   CK(cudaStreamWaitEvent(st, h->ev_join, 0));
+  CK(cudaStreamWaitEvent(st, h->ev_loss, 0));   // loss_finalize (st3): flags, bias corrections
   mark(h, 5);
   CK(cudaEventRecord(h->ev_fork2, st));
   CK(cudaStreamWaitEvent(h->st2, h->ev_fork2, 0));
@@ -1947,7 +1974,7 @@ kg_status step_dist(kg_handle *h, StepBufs &S) {
   else { sa.E = h->ent_src; sa.eidx = neg_rows; sa.estride = d; }
   sa.mask = h->b_mask; sa.W = (K + 31) / 32; sa.Cq = h->Cq; sa.Cv = h->Cv; sa.QP = h->QP;
   sa.gamma = h->cfg.gamma; sa.alpha = h->cfg.box_alpha; sa.scale = scale;
-  sa.C = h->C; sa.Dmin = h->Dmin; sa.loss_part = h->loss_part; sa.dQ = h->dQ;
+  sa.C = h->C; sa.Dmin = h->keep_grads ? h->Dmin : nullptr; sa.loss_part = h->loss_part; sa.dQ = h->dQ;   // D only for kg_last_grads
   sa.Dpart = h->Dpart; sa.partQ = h->partQ; sa.partV = h->partV; sa.Cpart = h->Cpart; sa.Csum = h->Csum;
   sa.cap_D = h->cap_D; sa.cap_Q = h->cap_Q; sa.cap_V = h->cap_V;
   sa.dV = h->OG + (int64_t)(na * M + M) * d;
@@ -2310,6 +2337,50 @@ kg_status kg_score(kg_handle *h, const kg_batch *q, const int64_t *cand, int32_t
   launch_pair_fwd(h->sk, sa, p.nout, false, st);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out_dist, h->Dscore, sizeof(float) * (size_t)M * n_cand, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return KG_OK;
+}
+
+kg_status kg_score_each(kg_handle *h, const kg_batch *q, const int64_t *cand, int32_t n_cand, float *out_dist) {
+  NvtxRange range("kg_score_each");
+  kg_status s = check_state(h);
+  if (s) return s;
+  if (!q || !cand || !out_dist) return fail(h, KG_EINVAL, "null argument");
+  const int M = q->M;
+  if (M < 1 || M > h->Mx) return fail(h, KG_EINVAL, "M out of range [1, max_M]");
+  if (n_cand < 1 || (int64_t)n_cand * M > (1LL << 31)) return fail(h, KG_EINVAL, "n_cand out of range");
+  const int64_t nc = (int64_t)M * n_cand;
+  for (int64_t k = 0; k < nc; ++k)
+    if (cand[k] < 0 || cand[k] >= h->n_ent) return fail(h, KG_EINVAL, "candidate id out of range");
+  StepBufs S;
+  CallBufs B(h);
+  if ((s = embed_queries(h, q, S, 0, B)) != KG_OK) return s;
+  cudaStream_t st = h->st;
+  const float *ent = h->ent_src;
+  std::vector<int64_t> pos_ids;
+  if (h->world > 1) {   // the candidate rows from their owners (collective), read by position
+    float *X = B.get<float>(nc * h->d);
+    if (!X) return fail(h, KG_ENOMEM, "score row buffer");
+    if ((s = fetch_rows(h, cand, nc, h->t.ent, X, B)) != KG_OK) return s;
+    pos_ids.resize(nc);
+    for (int64_t i = 0; i < nc; ++i) pos_ids[i] = i;
+    cand = pos_ids.data();
+    ent = X;
+  }
+  int64_t *d_cand = nullptr;
+  float *d_out = nullptr;
+  CK(cudaMallocAsync(&d_cand, sizeof(int64_t) * nc, st));
+  CK(cudaMallocAsync(&d_out, sizeof(float) * nc, st));
+  CK(cudaMemcpyAsync(d_cand, cand, sizeof(int64_t) * nc, cudaMemcpyHostToDevice, st));
+  EvalArgs a;
+  a.Q = h->Q; a.ent = ent; a.negatives = d_cand; a.metrics = d_out;
+  a.M = M; a.d = h->d; a.U = (h->sk == KG_BETAE || h->sk == KG_ROTATE || h->sk == KG_COMPLEX) ? h->m : h->d;
+  a.n_neg = n_cand; a.alpha = h->cfg.box_alpha;
+  launch_score_each(h->sk, a, S.plan.nout, st);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out_dist, d_out, sizeof(float) * nc, cudaMemcpyDeviceToHost, st));
+  CK(cudaFreeAsync(d_cand, st));
+  CK(cudaFreeAsync(d_out, st));
   CK(cudaStreamSynchronize(st));
   return KG_OK;
 }

@@ -149,6 +149,8 @@ struct EvalArgs {
   int32_t *ranks = nullptr;
   float *metrics = nullptr;       // [M][4]
 };
+// per-query candidates (kg_score_each): a.negatives = cand [M][n_neg], a.metrics = out [M][n_neg]
+void launch_score_each(int kind, const EvalArgs &a, int nout, cudaStream_t st);
 void launch_eval(int kind, const EvalArgs &a, int nout, cudaStream_t st);
 
 // k_dist.cu (world > 1)

@@ -65,6 +65,7 @@ _sig = {
     "kg_sync": (C.c_int, [_H, C.POINTER(kg_step_info)]),
     "kg_result": (C.c_int, [_H, C.POINTER(kg_step_info)]),
     "kg_score": (C.c_int, [_H, C.POINTER(kg_batch), C.c_void_p, C.c_int32, C.c_void_p]),
+    "kg_score_each": (C.c_int, [_H, C.POINTER(kg_batch), C.c_void_p, C.c_int32, C.c_void_p]),
     "kg_eval": (C.c_int, [_H, C.POINTER(kg_batch), C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                           C.c_void_p]),
     "kg_read_rows": (C.c_int, [_H, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
@@ -223,6 +224,15 @@ class KGModel:
         bs = self.batch_struct(dict(b, K=0, answers=None, negatives=None, mask=None))
         out = np.empty((int(b["M"]), len(cand)), np.float32)
         check(kg_score(self.h, C.byref(bs), cand.ctypes.data, len(cand), out.ctypes.data), self.h)
+        return out
+
+    def score_each(self, b, cand):
+        """kg_score_each: cand [M][n_cand] per-query candidates -> distances [M][n_cand]."""
+        cand = np.ascontiguousarray(cand, np.int64)
+        assert cand.ndim == 2 and cand.shape[0] == int(b["M"])
+        bs = self.batch_struct(dict(b, K=0, answers=None, negatives=None, mask=None))
+        out = np.empty(cand.shape, np.float32)
+        check(kg_score_each(self.h, C.byref(bs), cand.ctypes.data, cand.shape[1], out.ctypes.data), self.h)
         return out
 
     def eval(self, b, ans_off, ans_ids, negatives):

@@ -142,6 +142,42 @@ def test_union_score_is_dnf_min():
     np.testing.assert_allclose(D[0], [ex["d_pos"], ex["d_neg"]], rtol=1e-14)
 
 
+def test_score_each_per_query_candidates():
+    # kg_score_each's oracle (per-query candidates, SURVEY §8(b) shared = 0) on the same worked
+    # 2u example: each query row scores only its own candidates, with the DNF min (A11);
+    # a second query with the candidates swapped gets the swapped distances
+    ex = GOLD["union_gradient"]["2u"]
+    cfg = kggen.ModelConfig("gqe", 2, 10, 2, gamma=ex["gamma"])
+    _, n = kggen.dense_offsets(cfg)
+    dense = np.zeros(n, np.float32)
+    _set(cfg, dense, "rel", ex["relations"])
+    t = oracle.SparseTable(cfg, 0, dense=dense)
+    rows = np.array(ex["anchors"] + [ex["positive"], ex["negative"]], np.float32)
+    t.set([0, 1, POS, NEG], rows, np.zeros_like(rows), np.zeros_like(rows))
+    b = dict(structure="2u", anchors=np.array([[0, 1], [0, 1]], np.int64), relations=np.array([[0, 1], [0, 1]], np.int32))
+    D = oracle.oracle_score_each(cfg, t, b, np.array([[POS, NEG], [NEG, POS]]))
+    np.testing.assert_allclose(D, [[ex["d_pos"], ex["d_neg"]], [ex["d_neg"], ex["d_pos"]]], rtol=1e-14)
+
+
+@pytest.mark.parametrize("kind,structure", [("q2b", "pi"), ("betae", "2in"), ("rotate", "1p"), ("gqe", "up")])
+def test_score_each_rows_equal_shared_scores(kind, structure):
+    # with every query given the same candidate list the per-query scores reduce to the
+    # shared-candidate scores (oracle_score, pinned above), row by row
+    cfg = kggen.ModelConfig(kind, 8, 50, 5, hidden=16 if kind == "betae" else None)
+    t = oracle.SparseTable(cfg, 3)
+    b = kggen.make_batch(cfg, structure, 4, 6, seed=5)
+    cand = np.array([3, 17, 17, 0, 49])
+    shared = oracle.oracle_score(cfg, t, b, cand)
+    each = oracle.oracle_score_each(cfg, t, b, np.tile(cand, (4, 1)))
+    np.testing.assert_allclose(each, shared, rtol=1e-13, atol=0)
+    # and a permutation of one query's candidates permutes only that query's row
+    perm = np.tile(cand, (4, 1))
+    perm[2] = cand[::-1]
+    each2 = oracle.oracle_score_each(cfg, t, b, perm)
+    np.testing.assert_allclose(each2[2], shared[2][::-1], rtol=1e-13, atol=0)
+    np.testing.assert_allclose(np.delete(each2, 2, 0), np.delete(shared, 2, 0), rtol=1e-13, atol=0)
+
+
 def _partial_mask_run():
     ex = GOLD["partial_mask"]
     cfg = kggen.ModelConfig("gqe", 2, 20, 1, gamma=ex["gamma"])

@@ -133,6 +133,28 @@ def test_score_parity(kind, structure):
     gm.close()
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,structure", [("gqe", "2i"), ("q2b", "up"), ("q2b", "pi"), ("betae", "ip"),
+                                            ("betae", "pin"), ("rotate", "1p"), ("distmult", "1p"),
+                                            ("complex", "1p"), ("transe", "1p"), ("complex-m", "2u")])
+def test_score_each_parity(kind, structure):
+    """kg_score_each (per-query candidates, SURVEY §8(b) shared = 0) against the oracle, with
+    duplicate ids inside a row and n_cand not a multiple of the warp count."""
+    cfg = kggen.ModelConfig(kind, 40, 300, 7, hidden=24)
+    gm = _model(cfg, 70, 100, max_cand=90)
+    table = oracle.SparseTable(cfg, 5)
+    b = kggen.make_batch(cfg, structure, 70, 100, seed=3)
+    cand = np.random.default_rng(1).integers(0, 300, size=(70, 37))
+    cand[:, 5] = cand[:, 4]
+    assert_close(gm.score_each(gm.host_batch(b), cand), oracle.oracle_score_each(cfg, table, b, cand),
+                 what="kg_score_each")
+    with pytest.raises(Exception):
+        bad = cand.copy()
+        bad[3, 3] = 300
+        gm.score_each(gm.host_batch(b), bad)
+    gm.close()
+
+
 def test_determinism_bitwise():
     cfg = kggen.ModelConfig("q2b", 40, 300, 7)
     outs = []
