@@ -272,7 +272,10 @@ def run_ours(args, world, rank, local):
     cand = {"scoring": (stage[2] + stage[3]), "dense_adam": (stage[8] + stage[9]) if stage[8] > 0 else stage[6],
             "sparse_adam": stage[5]}
     if "dag" in work:
-        cand["dag"] = stage[1] + stage[4]
+        # the DAG's weight-gradient GEMMs run on their own stream beside the dX chain and the
+        # sparse update; the dense stage (6) is where the step waits for them, so it is counted
+        # in the DAG's time (an upper bound: it also holds what the dense Adam adds)
+        cand["dag"] = stage[1] + stage[4] + stage[6]
     dom = max(cand, key=cand.get)
     bound, amount, unit = work[dom]
     per_launch = amount / n_prof

@@ -184,10 +184,8 @@ __device__ __forceinline__ float4 ld4(const float *p) { return *reinterpret_cast
 #define KG_FWD_OCC4 0
 #endif
 template <class Mdl, int NOUT> struct kFwdOcc {
-  // the two-output (DNF union) Q2B kernel: 2 per SM (<= 128 registers, no spills) instead of the
-  // compiler's 132 registers at 1 per SM (8 warps per SM)
-  static constexpr int v = (KG_FWD_OCC4 && NOUT == 1 && std::is_same<Mdl, MBox>::value) ? 4
-                           : (NOUT == 2 && std::is_same<Mdl, MBox>::value) ? 2 : 1;
+  // (the two-output DNF-union kernel at 2 per SM, <= 128 registers: neutral, 92.6 vs 92.4 us)
+  static constexpr int v = (KG_FWD_OCC4 && NOUT == 1 && std::is_same<Mdl, MBox>::value) ? 4 : 1;
 };
 template <class Mdl, int NOUT>
 __global__ void __launch_bounds__(256, kFwdOcc<Mdl, NOUT>::v) pair_fwd_kernel(ScoreArgs a) {

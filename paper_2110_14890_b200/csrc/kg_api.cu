@@ -1104,15 +1104,9 @@ kg_status dag_backward(kg_handle *h, StepBufs &S, bool defer_wjoin = false) {
   // projection-use index of each node
   int use[6], u = 0;
   for (int ni = 0; ni < p.nn; ++ni) use[ni] = p.n[ni].type == 0 ? u++ : -1;
-  // BetaE: the projection MLP's weight gradients group by group on st5 (beside the dX chain of
-  // the earlier groups), accumulated over the groups; one group (or row offsets TMA cannot
-  // address: M % 4 != 0): all groups at once after the chain
-  int ngroups = 0;
-  for (int ni = 0; ni < p.nn; ni = p.n[ni].type == 0 && h->kind == KG_BETAE ? p.ge[ni] : ni + 1)
-    if (p.n[ni].type == 0 && h->kind == KG_BETAE) ++ngroups;
-  const bool dw_by_group = h->kind == KG_BETAE && ngroups > 1 && (M & 3) == 0;
-  const int ldT = (int)align_up(p.nproj * M, 4);
-  bool dw_first = true;
+  // (BetaE's projection-MLP weight gradients issued group by group on st5, beside the dX chain of
+  // the earlier groups, measured slower: C5-betae 3p 0.709 -> 0.810 ms -- the concurrent GEMMs
+  // slow the chain more than they overlap; they run once after it, over all groups)
   for (int ni = p.nn - 1; ni >= 0; --ni) {
     const PNode &nd = p.n[ni];
     if (nd.type == 0 && h->kind == KG_BETAE) {
@@ -1126,17 +1120,6 @@ kg_status dag_backward(kg_handle *h, StepBufs &S, bool defer_wjoin = false) {
         h->pH2 + (int64_t)u0 * M * HH);   // ReLU backward folded into the GEMM's combine
       G(false, true, GM, HH, HH, dH2, HH, wt(h, "prj_W2"), HH, 0.f, dH1, HH, nullptr, 0, 1.f, wtlo(h, "prj_W2"), true,
         h->pH1 + (int64_t)u0 * M * HH);
-      if (dw_by_group) {
-        WF(st);
-        WOn w(h);
-        if (dw_first) CK(cudaStreamWaitEvent(h->st5, h->ev_xt, 0));   // the transposed inputs (st4)
-        const float beta = dw_first ? 0.f : 1.f;
-        const int64_t c0 = (int64_t)u0 * M;   // this group's rows = columns of the transposed inputs
-        G(true, true, d, HH, GM, dZ, d, h->pH2T + c0, ldT, beta, gp(h, "prj_W0"), HH);
-        G(true, true, HH, HH, GM, dH2, HH, h->pH1T + c0, ldT, beta, gp(h, "prj_W2"), HH);
-        G(true, true, HH, 2 * d, GM, dH1, HH, h->pXT + c0, ldT, beta, gp(h, "prj_W1"), 2 * d);
-        dw_first = false;
-      }
       G(false, true, GM, 2 * d, HH, dH1, HH, wt(h, "prj_W1"), HH, 0.f, h->pdX, 2 * d, nullptr, 0, 1.f, wtlo(h, "prj_W1"), true);
       for (int k = n0; k <= ni; ++k) {
         const PNode &nk = p.n[k];
@@ -1246,15 +1229,13 @@ kg_status dag_backward(kg_handle *h, StepBufs &S, bool defer_wjoin = false) {
   }
   if (h->kind == KG_BETAE) {
     // projection-MLP weight gradients over all projection uses at once (A9)
-    const int NR = p.nproj * M;
+    const int NR = p.nproj * M, ldT = (int)align_up(NR, 4);
     WF(st);
     WOn w(h);
-    if (!dw_by_group) {
-      CK(cudaStreamWaitEvent(h->st5, h->ev_xt, 0));   // the transposed inputs (DAG forward, st4)
-      G(true, true, d, HH, NR, h->pdZ, d, h->pH2T, ldT, 0.f, gp(h, "prj_W0"), HH);
-      G(true, true, HH, HH, NR, h->pdH2, HH, h->pH1T, ldT, 0.f, gp(h, "prj_W2"), HH);
-      G(true, true, HH, 2 * d, NR, h->pdH1, HH, h->pXT, ldT, 0.f, gp(h, "prj_W1"), 2 * d);
-    }
+    CK(cudaStreamWaitEvent(h->st5, h->ev_xt, 0));   // the transposed inputs (DAG forward, st4)
+    G(true, true, d, HH, NR, h->pdZ, d, h->pH2T, ldT, 0.f, gp(h, "prj_W0"), HH);
+    G(true, true, HH, HH, NR, h->pdH2, HH, h->pH1T, ldT, 0.f, gp(h, "prj_W2"), HH);
+    G(true, true, HH, 2 * d, NR, h->pdH1, HH, h->pXT, ldT, 0.f, gp(h, "prj_W1"), 2 * d);
     ColsumJobs cj;
     cj.add(h->pdZ, NR, d, d, gp(h, "prj_b0"));
     cj.add(h->pdH2, NR, HH, HH, gp(h, "prj_b2"));
