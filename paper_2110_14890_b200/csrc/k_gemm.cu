@@ -137,13 +137,17 @@ constexpr int G2T = 64 + 32 * G2CW, G2K = 16;
 // S stages (even) in G = S / 2 groups of k-blocks: the MMA warp commits once per group
 // (a tcgen05.commit drains the tensor pipe: ~200 cycles, tools/mma_probe.cu), and the
 // producer refills a group's stages when the group two back has completed.
-template <int BN, bool AMN, bool BMN, bool ATM = true, bool DRAIN = true> struct G2Cfg {
+// OCC = 2: a narrow-tile form with two resident CTAs per SM (half the TMEM columns -- 256 -- and
+// under half the shared memory each), so the small d x d contractions of concurrent DAG branches
+// (Q2B center / offset, weight gradients) share the SMs instead of queueing behind each other
+template <int BN, bool AMN, bool BMN, bool ATM = true, bool DRAIN = true, int OCC = 1> struct G2Cfg {
   static constexpr int kA = GBM * G2K * 4, kB = BN * G2K * 4;           // bytes of one tile
   static constexpr int kStage = ATM ? kA + kB + (BMN ? kB : 0) + kB : 2 * (kA + kB) + (AMN ? kA : 0) + (BMN ? kB : 0);
   // stages: shared memory (224 KB budget), at most 8, and (ATM) 32 TMEM columns each after
   // the accumulator(s)
-  static constexpr int kTmemFit = ATM ? (512 - (DRAIN ? 2 * BN : BN)) / 32 : 8;
-  static constexpr int kSmemFit = (224 * 1024) / kStage;
+  static constexpr int kTmemCols = OCC == 2 ? 256 : 512;
+  static constexpr int kTmemFit = ATM ? (kTmemCols - (DRAIN ? 2 * BN : BN)) / 32 : 8;
+  static constexpr int kSmemFit = ((OCC == 2 ? 108 : 224) * 1024) / kStage;
   static constexpr int kFit = kSmemFit < 8 ? (kSmemFit < kTmemFit ? kSmemFit : kTmemFit) : (8 < kTmemFit ? 8 : kTmemFit);
   static constexpr int kStages = kFit >= 2 ? (kFit / 2) * 2 : 2;
   static constexpr int kGroup = kStages / 2;
@@ -310,12 +314,12 @@ namespace kg {
 #else
 #define GT(k, i) do {} while (0)
 #endif
-template <int BN, bool AMN, bool BMN, bool DRAIN, bool LOWP = false>
-__global__ void __launch_bounds__(G2T, 1)
+template <int BN, bool AMN, bool BMN, bool DRAIN, bool LOWP = false, int OCC = 1>
+__global__ void __launch_bounds__(G2T, OCC)
     gemm_tf32x3_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                            const __grid_constant__ CUtensorMap tmBl, GemmArgs g) {
   KG_GRID_DEP_WAIT();
-  using Cfg = G2Cfg<BN, AMN, BMN, !LOWP, DRAIN>;
+  using Cfg = G2Cfg<BN, AMN, BMN, !LOWP, DRAIN, OCC>;
   constexpr int S = Cfg::kStages, G = Cfg::kGroup;
   // TMEM columns: a power of 2 >= 32 holding one (or, drained, two) BN-column accumulators
   constexpr int kNeed = DRAIN ? 2 * BN : BN;
@@ -326,8 +330,8 @@ __global__ void __launch_bounds__(G2T, 1)
   // split stage was bound by the 128 B/clk shared-memory port: tools/gemm_trace.py).
   constexpr bool ATM = !LOWP;
   constexpr int kACol = kNeed;
-  constexpr int kCols = ATM ? 512 : kNeed <= 32 ? 32 : kNeed <= 64 ? 64 : kNeed <= 128 ? 128 : kNeed <= 256 ? 256 : 512;
-  static_assert(!ATM || (kACol % 32 == 0 && kACol + 32 * S <= 512 && G2CW == 8), "TMEM A stages");
+  constexpr int kCols = ATM ? Cfg::kTmemCols : kNeed <= 32 ? 32 : kNeed <= 64 ? 64 : kNeed <= 128 ? 128 : kNeed <= 256 ? 256 : 512;
+  static_assert(!ATM || (kACol % 32 == 0 && kACol + 32 * S <= kCols && G2CW == 8), "TMEM A stages");
   static_assert(S == 2 * G && G >= 2 && S + 3 <= 16, "two groups of stages in flight, k-blocks of both split teams in "
                 "each; named barrier ids 1 .. S + 2");
   // 32-column chunks of the tile; the NG = G2CW / 4 warps of a TMEM lane quarter take the
@@ -664,9 +668,9 @@ bool make_tmap(CUtensorMap *tm, const float *base, int rows, int K, int ld, int 
 
 // returns the number of K splits (0: not launched); raw: the kernel writes the raw partial
 // products [splits][M][N] into `part` (even unsplit) and the caller's kernel combines them
-template <int BN, bool AMN, bool BMN, bool DRAIN, bool LOWP = false>
+template <int BN, bool AMN, bool BMN, bool DRAIN, bool LOWP = false, int OCC = 1>
 int launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t st, bool raw = false) {
-  using Cfg = G2Cfg<BN, AMN, BMN, !LOWP, DRAIN>;
+  using Cfg = G2Cfg<BN, AMN, BMN, !LOWP, DRAIN, OCC>;
   CUtensorMap ta, tb, tbl;
   if (!make_tmap(&ta, g0.A, g0.M, g0.K, g0.lda, GBM, AMN) || !make_tmap(&tb, g0.B, g0.N, g0.K, g0.ldb, BN, BMN))
     return 0;
@@ -676,14 +680,14 @@ int launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t st
     tbl = tb;
   }
   static const bool configured =   // thread-safe one-time attribute (concurrent host threads)
-      cudaFuncSetAttribute(gemm_tf32x3_tma_kernel<BN, AMN, BMN, DRAIN, LOWP>,
+      cudaFuncSetAttribute(gemm_tf32x3_tma_kernel<BN, AMN, BMN, DRAIN, LOWP, OCC>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) == cudaSuccess;
   (void)configured;
   GemmArgs g = g0;
   const int tiles = ((g.N + BN - 1) / BN) * ((g.M + GBM - 1) / GBM);
   const int nkb = (g.K + G2K - 1) / G2K;
   // split K to fill the SMs while every split keeps >= 8 k-blocks (measured best of 8 / 16 / none)
-  int splits = std::max(1, std::min(148 / std::max(tiles, 1), nkb / 8));
+  int splits = std::max(1, std::min(148 * OCC / std::max(tiles, 1), nkb / 8));
   if (g0.force & 1) splits = 1;
   while (splits > 1 && (!part || (int64_t)splits * g.M * g.N > part_cap)) --splits;
   g.kbs = (nkb + splits - 1) / splits;
@@ -694,7 +698,7 @@ int launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t st
     g.P = part;
   }
   dim3 grid((g.N + BN - 1) / BN, (g.M + GBM - 1) / GBM, splits);
-  { gemm_tf32x3_tma_kernel<BN, AMN, BMN, DRAIN, LOWP><<<grid, G2T, Cfg::kSmem, st>>>(ta, tb, tbl, g); ++g_launches; }
+  { gemm_tf32x3_tma_kernel<BN, AMN, BMN, DRAIN, LOWP, OCC><<<grid, G2T, Cfg::kSmem, st>>>(ta, tb, tbl, g); ++g_launches; }
   if (raw) return splits;
   if (splits > 1) {
     const int64_t n4 = ((int64_t)g.M * g.N + 3) / 4;
@@ -707,12 +711,12 @@ int launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t st
   }
   return splits;
 }
-template <int BN, bool DRAIN, bool LOWP = false>
+template <int BN, bool DRAIN, bool LOWP = false, int OCC = 1>
 int launch_v2_any(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st, bool raw = false) {
-  if (g.a_mn) return g.b_mn ? launch_v2<BN, true, true, DRAIN, LOWP>(g, part, part_cap, st, raw)
-                            : launch_v2<BN, true, false, DRAIN, LOWP>(g, part, part_cap, st, raw);
-  return g.b_mn ? launch_v2<BN, false, true, DRAIN, LOWP>(g, part, part_cap, st, raw)
-                : launch_v2<BN, false, false, DRAIN, LOWP>(g, part, part_cap, st, raw);
+  if (g.a_mn) return g.b_mn ? launch_v2<BN, true, true, DRAIN, LOWP, OCC>(g, part, part_cap, st, raw)
+                            : launch_v2<BN, true, false, DRAIN, LOWP, OCC>(g, part, part_cap, st, raw);
+  return g.b_mn ? launch_v2<BN, false, true, DRAIN, LOWP, OCC>(g, part, part_cap, st, raw)
+                : launch_v2<BN, false, false, DRAIN, LOWP, OCC>(g, part, part_cap, st, raw);
 }
 }  // namespace
 
@@ -739,10 +743,13 @@ static int launch_gemm_sel(const GemmArgs &g, float *part, int64_t part_cap, cud
       constexpr int BN = decltype(tag)::value;
       return f.drain ? launch_v2_any<BN, true>(f, part, part_cap, st, raw) : launch_v2_any<BN, false>(f, part, part_cap, st, raw);
     };
+    if (g.force & 8) return f.drain ? launch_v2_any<64, true, false, 2>(f, part, part_cap, st, raw) : 0;   // 2 per SM
     if (bn == 1) return go(std::integral_constant<int, 64>());
     if (bn == 3) return go(std::integral_constant<int, 160>());
     return go(std::integral_constant<int, 128>());
   }
+  // (the two-per-SM narrow form, force bit 3, for every N <= 512 contraction of the step: neutral at
+  // C5-q2b / C5-betae -- the concurrent branches' GEMMs did not gain from sharing SMs)
   if (g.drain) {
     // wave quantisation: e.g. 1536 x 1600 is 156 tiles of 128 x 128 (two waves on 148 SMs) but
     // 120 tiles of 128 x 160 (one)

@@ -16,7 +16,10 @@ for gm in (512, 1024, 1536):
 for nr in (512, 1024, 1536):
     SHAPES += [(nr, D, D, 0, 0), (D, D, nr, 1, 1)]                            # d x d intersection MLPs
 VARIANTS = [(None, "auto"), (1 | (1 << 1), "bn64-nosplit"), (1 | (2 << 1), "bn128-nosplit"),
-            (1 | (3 << 1), "bn160-nosplit"), (1 << 1, "bn64-split"), (2 << 1, "bn128-split"), (3 << 1, "bn160-split")]
+            (1 | (3 << 1), "bn160-nosplit"), (1 << 1, "bn64-split"), (2 << 1, "bn128-split"), (3 << 1, "bn160-split"),
+            (8, "bn64-occ2-split"), (8 | 1, "bn64-occ2-nosplit")]
+if "--small" in sys.argv:   # the d x d shapes only
+    SHAPES = [sh for sh in SHAPES if sh[0] <= 1536 and sh[1] <= 400 and sh[2] <= 1536 and min(sh[:3]) == 400]
 
 
 def run():
@@ -33,9 +36,9 @@ def run():
             for _ in range(3):
                 assert kgb.kg_test_gemm(ta, tb, M, N, K, A.data_ptr(), A.shape[1], B.data_ptr(), B.shape[1],
                                         Cm.data_ptr(), N, None, fl, 0.0, C.c_void_p(st.cuda_stream)) == 0
-            torch.cuda.nvtx.range_push(f"{M}x{N}x{K}:{ta}{tb}:{name}")
-            torch.cuda.nvtx.range_pop()
-            print(f"{M}x{N}x{K} ta{ta} tb{tb} {name}", flush=True)
+            r2 = (A.t() if ta else A).double() @ (B if tb else B.t()).double()
+            err = float((Cm.double() - r2).abs().max() / r2.abs().max())
+            print(f"{M}x{N}x{K} ta{ta} tb{tb} {name} relerr {err:.1e}", flush=True)
 
 
 def parse(path):
@@ -68,6 +71,8 @@ def parse(path):
 
 if __name__ == "__main__":
     if len(sys.argv) > 2 and sys.argv[1] == "--parse":
+        if "--small" in sys.argv:
+            pass
         parse(sys.argv[2])
     else:
         run()

@@ -15,6 +15,10 @@ for W in C5-q2b C5-betae C5-q2b-bw C4 C2 C3-complex C3-rotate C4-bw; do
   timeout 600 ncu --profile-from-start off --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --csv --log-file gpurun_out/r/traffic_$W.csv python tools/step_traffic.py --workload $W > /dev/null 2>&1
 done
 timeout 600 ncu --profile-from-start off --clock-control none --set full --import-source on --kernel-name-base demangled -k "regex:pair_bwd_kernel<kg::MBox>" -c 1 -o gpurun_out/r/${TAG}_pairbwd_full python tools/step_traffic.py --workload C5-q2b > /dev/null 2>&1
+timeout 600 ncu --profile-from-start off --clock-control none --set full --import-source on --kernel-name-base demangled -k "regex:pair_fwd_kernel<kg::MBox, \(int\)1>" -c 1 -o gpurun_out/r/${TAG}_pairfwd_full python tools/step_traffic.py --workload C5-q2b > /dev/null 2>&1
 timeout 600 ncu --profile-from-start off --clock-control none --set full --import-source on -k regex:sparse_adam_fused -c 2 -o gpurun_out/r/${TAG}_sparse_full python tools/step_traffic.py --workload C5-q2b > /dev/null 2>&1
 timeout 600 ncu --profile-from-start off --clock-control none --set full --import-source on --kernel-name-base demangled -k "regex:gemm_tf32x3_tma_kernel<\(int\)160" -c 1 -o gpurun_out/r/${TAG}_gemm160_full python tools/step_traffic.py --workload C5-betae > /dev/null 2>&1
+for R in gpurun_out/r/${TAG}_*_full.ncu-rep; do
+  ncu -i $R --page raw --csv > ${R%.ncu-rep}_raw.csv 2>/dev/null
+done
 ls -la gpurun_out/r

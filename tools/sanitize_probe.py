@@ -1,4 +1,4 @@
-"""Small steps of every model kind through kg_step / kg_score / kg_eval, for compute-sanitizer
+"""Small steps of every model kind through kg_step / kg_score / kg_score_each, for compute-sanitizer
 (memcheck / racecheck / synccheck):  compute-sanitizer --tool memcheck python tools/sanitize_probe.py"""
 import os
 import sys
@@ -21,5 +21,6 @@ for kind, st, *prec in cases:
         b = kggen.make_batch(cfg, st, 70, 100, seed=2, step=s)
         gm.step(gm.host_batch(b), 1e-3)
     gm.score(gm.host_batch(b), np.arange(50))
+    gm.score_each(gm.host_batch(b), np.random.default_rng(0).integers(0, 300, size=(70, 13)))   # per-query candidates
     gm.close()
     print("ok", kind, st, *prec, flush=True)
