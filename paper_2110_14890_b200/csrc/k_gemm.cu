@@ -132,6 +132,9 @@ __global__ void gemm_reduce_kernel(const float *__restrict__ P, int splits, int 
 #endif
 constexpr int G2CW = KG_G2CW;                          // split / epilogue warps
 constexpr int G2T = 64 + 32 * G2CW, G2K = 16;
+#ifndef KG_GEMM_KB32
+#define KG_GEMM_KB32 1
+#endif
 // ATM (the fp32-accurate modes): A's hi / lo tiles go to tensor memory, so a stage holds
 // A raw, B raw, [B hi if BMN], B lo; otherwise (LOWP) A raw, B raw, [A hi], [B hi], A lo, B lo.
 // S stages (even) in G = S / 2 groups of k-blocks: the MMA warp commits once per group
@@ -140,32 +143,47 @@ constexpr int G2T = 64 + 32 * G2CW, G2K = 16;
 // OCC = 2: a narrow-tile form with two resident CTAs per SM (half the TMEM columns -- 256 -- and
 // under half the shared memory each), so the small d x d contractions of concurrent DAG branches
 // (Q2B center / offset, weight gradients) share the SMs instead of queueing behind each other
-template <int BN, bool AMN, bool BMN, bool ATM = true, bool DRAIN = true, int OCC = 1> struct G2Cfg {
-  static constexpr int kA = GBM * G2K * 4, kB = BN * G2K * 4;           // bytes of one tile
+// KB: k-block depth, 16 (SWIZZLE_64B rows of 64 B) or 32 (SWIZZLE_128B rows of 128 B: half the
+// TMA row requests, handshakes and commits per MMA; K-major operands only)
+template <int BN, bool AMN, bool BMN, bool ATM = true, bool DRAIN = true, int OCC = 1, int KB = 16> struct G2Cfg {
+  static constexpr int kA = GBM * KB * 4, kB = BN * KB * 4;           // bytes of one tile
   static constexpr int kStage = ATM ? kA + kB + (BMN ? kB : 0) + kB : 2 * (kA + kB) + (AMN ? kA : 0) + (BMN ? kB : 0);
   // stages: shared memory (224 KB budget), at most 8, and (ATM) 32 TMEM columns each after
   // the accumulator(s)
   static constexpr int kTmemCols = OCC == 2 ? 256 : 512;
-  static constexpr int kTmemFit = ATM ? (kTmemCols - (DRAIN ? 2 * BN : BN)) / 32 : 8;
+  static constexpr int kTmemFit = ATM ? (kTmemCols - (DRAIN ? 2 * BN : BN)) / (2 * KB) : 8;   // A hi + lo per stage
   static constexpr int kSmemFit = ((OCC == 2 ? 108 : 224) * 1024) / kStage;
   static constexpr int kFit = kSmemFit < 8 ? (kSmemFit < kTmemFit ? kSmemFit : kTmemFit) : (8 < kTmemFit ? 8 : kTmemFit);
   static constexpr int kStages = kFit >= 2 ? (kFit / 2) * 2 : 2;
   static constexpr int kGroup = kStages / 2;
-  static constexpr int kSmem = kStages * kStage + 1024;
+  // shared-memory stages (TMA destinations) beyond the TMEM A stages (drained fp32 mode): the
+  // producer refills a stage once the group holding its previous k-block has completed, so
+  // kSmemStages - kStages extra stages let the loads run that many k-blocks further ahead of the
+  // split (tools/gemm_trace.py: ~1,000 cycles from TMA issue to landed, against ~750 cycles per
+  // k-block of MMA work at 128 x 160)
+  static constexpr int kSmemStages0 = kSmemFit < kStages + kGroup ? kSmemFit : kStages + kGroup;
+  static constexpr int kSmemStages = (ATM && DRAIN && kSmemStages0 > kStages) ? kSmemStages0 : kStages;
+  static constexpr int kSmem = kSmemStages * kStage + 1024;
   static constexpr int oAhi = kA + kB, oBhi = ATM ? kA + kB : oAhi + (AMN ? kA : 0);
   static constexpr int oAlo = oBhi + (BMN ? kB : 0), oBlo = ATM ? oAlo : oAlo + kA;
   static constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                                      ((uint32_t)(GBM >> 4) << 24);
 };
+template <int KB = 16>
 __device__ __forceinline__ uint64_t kmajor_desc(uint32_t saddr, int kk) {
-  uint64_t d = (uint64_t)(((saddr + kk * 32) >> 4) & 0x3FFF);   // K-step = 32 B inside the 64 B row
+  uint64_t d = (uint64_t)(((saddr + kk * 32) >> 4) & 0x3FFF);   // K-step = 32 B inside the KB * 4 B row
   d |= (uint64_t)1 << 16;
-  d |= (uint64_t)(512 >> 4) << 32;                              // 8-row groups 512 B apart
+  d |= (uint64_t)((8 * KB * 4) >> 4) << 32;                     // 8-row groups 512 / 1024 B apart
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)4 << 61;                                       // SWIZZLE_64B
+  d |= (uint64_t)(KB == 32 ? 2 : 4) << 61;                      // SWIZZLE_128B / SWIZZLE_64B
   return d;
 }
 // byte offset of 16-byte chunk q (k = 4q .. 4q+3) of row r in a K-major SWIZZLE_64B tile
+template <int KB = 16>
+__device__ __forceinline__ uint32_t sw_off(int r, int q) {
+  if (KB == 32) return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((q ^ (r & 7)) << 4));   // SWIZZLE_128B
+  return (uint32_t)((r >> 3) * 512 + (r & 7) * 64 + ((q ^ ((r >> 1) & 3)) << 4));
+}
 __device__ __forceinline__ uint32_t sw64_off(int r, int q) {
   return (uint32_t)((r >> 3) * 512 + (r & 7) * 64 + ((q ^ ((r >> 1) & 3)) << 4));
 }
@@ -221,11 +239,11 @@ __device__ __forceinline__ void mma_tf32_i(uint32_t tmem, uint64_t a, uint64_t b
 }
 // one operand tile (rows r0 .. r0 + R, k0 .. k0 + 16) into dst: K-major one SWIZZLE_64B box;
 // MN-major R / 32 unswizzled boxes of 32 (rows) x 16 (k), 2048 B each ([k][32 rows])
-template <bool MN, int R>
+template <bool MN, int R, int KB = 16>
 __device__ __forceinline__ void load_op(const CUtensorMap *tm, uint64_t *bar, uint8_t *dst, int r0, int k0) {
   if (MN) {
 #pragma unroll
-    for (int c = 0; c < R / 32; ++c) tma_load_2d(tm, bar, dst + c * 2048, r0 + 32 * c, k0);
+    for (int c = 0; c < R / 32; ++c) tma_load_2d(tm, bar, dst + c * (32 * KB * 4), r0 + 32 * c, k0);
   } else {
     tma_load_2d(tm, bar, dst, k0, r0);
   }
@@ -255,11 +273,12 @@ __device__ __forceinline__ float4 bf16r4(float4 v) { return make_float4(bf16r(v.
 // split one landed operand tile of R rows (32 G2CW threads, ct = 0 ..).  LOWP (the bf16 score
 // mode): the operand is rounded to bf16 (RNE) instead -- K-major in place, MN-major into hi --
 // and the one MMA per K-step multiplies bf16-exact values (exact products, fp32 accumulation)
-template <bool MN, int R, bool LOWP = false>
+template <bool MN, int R, bool LOWP = false, int KB = 16>
 __device__ __forceinline__ void split_op(uint8_t *raw, uint8_t *hi, uint8_t *lo, int ct, int nthr) {
+  constexpr int Q = KB / 4;   // 16-byte chunks per row
   if (LOWP && !MN) {
 #pragma unroll 4
-    for (int c = ct; c < R * 4; c += nthr) {
+    for (int c = ct; c < R * Q; c += nthr) {
       float4 *p = reinterpret_cast<float4 *>(raw + c * 16);
       *p = bf16r4(*p);
     }
@@ -267,21 +286,21 @@ __device__ __forceinline__ void split_op(uint8_t *raw, uint8_t *hi, uint8_t *lo,
   }
   if (!MN) {   // K-major: same (swizzled) offsets, lo only
 #pragma unroll 4
-    for (int c = ct; c < R * 4; c += nthr) {
+    for (int c = ct; c < R * Q; c += nthr) {
       const float4 v = *reinterpret_cast<const float4 *>(raw + c * 16);
       *reinterpret_cast<float4 *>(lo + c * 16) = tf32_lo(v);
     }
   } else {     // MN-major raw [R/32][16 k][32 rows] -> K-major SW64 hi and lo, 4 k per chunk
 #pragma unroll 4
-    for (int c = ct; c < R * 4; c += nthr) {
+    for (int c = ct; c < R * Q; c += nthr) {
       const int r = c % R, q = c / R;
-      const float *src = reinterpret_cast<const float *>(raw + (r >> 5) * 2048) + (r & 31);
+      const float *src = reinterpret_cast<const float *>(raw + (r >> 5) * (32 * KB * 4)) + (r & 31);
       float4 v;
       v.x = src[(4 * q + 0) * 32];
       v.y = src[(4 * q + 1) * 32];
       v.z = src[(4 * q + 2) * 32];
       v.w = src[(4 * q + 3) * 32];
-      const uint32_t o = sw64_off(r, q);
+      const uint32_t o = sw_off<KB>(r, q);
       if (LOWP) {
         *reinterpret_cast<float4 *>(hi + o) = bf16r4(v);
         continue;
@@ -314,13 +333,15 @@ namespace kg {
 #else
 #define GT(k, i) do {} while (0)
 #endif
-template <int BN, bool AMN, bool BMN, bool DRAIN, bool LOWP = false, int OCC = 1>
+template <int BN, bool AMN, bool BMN, bool DRAIN, bool LOWP = false, int OCC = 1, int KB = 16>
 __global__ void __launch_bounds__(G2T, OCC)
     gemm_tf32x3_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                            const __grid_constant__ CUtensorMap tmBl, GemmArgs g) {
   KG_GRID_DEP_WAIT();
-  using Cfg = G2Cfg<BN, AMN, BMN, !LOWP, DRAIN, OCC>;
-  constexpr int S = Cfg::kStages, G = Cfg::kGroup;
+  using Cfg = G2Cfg<BN, AMN, BMN, !LOWP, DRAIN, OCC, KB>;
+  static_assert(KB == 16 || (KB == 32 && !AMN && !BMN && !LOWP), "32-deep k-blocks: K-major operands");
+  constexpr int S = Cfg::kStages, G = Cfg::kGroup, SM = Cfg::kSmemStages;
+  static_assert(SM >= S && SM <= S + G, "shared-memory stages");
   // TMEM columns: a power of 2 >= 32 holding one (or, drained, two) BN-column accumulators
   constexpr int kNeed = DRAIN ? 2 * BN : BN;
   // ATM (every fp32-accurate mode): the A operand's hi / lo tiles of each stage live in tensor
@@ -331,7 +352,7 @@ __global__ void __launch_bounds__(G2T, OCC)
   constexpr bool ATM = !LOWP;
   constexpr int kACol = kNeed;
   constexpr int kCols = ATM ? Cfg::kTmemCols : kNeed <= 32 ? 32 : kNeed <= 64 ? 64 : kNeed <= 128 ? 128 : kNeed <= 256 ? 256 : 512;
-  static_assert(!ATM || (kACol % 32 == 0 && kACol + 32 * S <= kCols && G2CW == 8), "TMEM A stages");
+  static_assert(!ATM || (kACol % 32 == 0 && kACol + 2 * KB * S <= kCols && G2CW == 8), "TMEM A stages");
   static_assert(S == 2 * G && G >= 2 && S + 3 <= 16, "two groups of stages in flight, k-blocks of both split teams in "
                 "each; named barrier ids 1 .. S + 2");
   // 32-column chunks of the tile; the NG = G2CW / 4 warps of a TMEM lane quarter take the
@@ -347,13 +368,15 @@ __global__ void __launch_bounds__(G2T, OCC)
   // 1]: the MMAs of group g completed (mbarrier, one commit per group: frees its stages for
   // the producer and hands its accumulator to the drain); drain of group g done: named
   // barrier 1 + S + (g & 1).  (Barrier ids <= 1 + 8 + 1 < 16; 0 is __syncthreads.)
-  __shared__ __align__(8) uint64_t full_bar[S];
-  __shared__ __align__(8) uint64_t done_bar, gdone[2];
+  // gdone[g & 3]: four group barriers -- the producer waits for a group up to three behind the
+  // one it loads for (SM <= S + G), so the bucket of a group cannot have moved on a full phase
+  __shared__ __align__(8) uint64_t full_bar[SM];
+  __shared__ __align__(8) uint64_t done_bar, gdone[4];
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * BN;
   const bool bpre = !BMN && !LOWP && g.B_lo != nullptr;   // B's lo plane comes from global memory
-  const int nkb_all = (g.K + G2K - 1) / G2K;
+  const int nkb_all = (g.K + KB - 1) / KB;
   const int kb0 = blockIdx.z * g.kbs, nkb = min(nkb_all, kb0 + g.kbs) - kb0;   // split-K range
 
   if (warp == 1) {
@@ -365,9 +388,9 @@ __global__ void __launch_bounds__(G2T, OCC)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     if (bpre) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmBl)) : "memory");
-    for (int s = 0; s < S; ++s) mbar_init(&full_bar[s], 1);
+    for (int s = 0; s < SM; ++s) mbar_init(&full_bar[s], 1);
     mbar_init(&done_bar, 1);
-    for (int b = 0; b < 2; ++b) mbar_init(&gdone[b], 1);
+    for (int b = 0; b < 4; ++b) mbar_init(&gdone[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -378,17 +401,17 @@ __global__ void __launch_bounds__(G2T, OCC)
   if (warp == 0) {
     if (lane == 0) {
       for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % S;
-        if (kb >= S) {   // the stage's previous k-block belongs to group kb / G - 2 (S = 2 G)
-          const int gw = kb / G - 2;
-          mbar_wait(&gdone[gw & 1], (gw >> 1) & 1);
+        const int s = kb % SM;
+        if (kb >= SM) {   // the stage's previous k-block kb - SM: its group has completed
+          const int gw = (kb - SM) / G;
+          mbar_wait(&gdone[gw & 3], (gw >> 2) & 1);
         }
         uint8_t *st = sm + s * Cfg::kStage;
         mbar_expect_tx(&full_bar[s], Cfg::kA + Cfg::kB + (bpre ? Cfg::kB : 0));
-        const int k0 = (kb0 + kb) * G2K;
-        load_op<AMN, GBM>(&tmA, &full_bar[s], st, m0, k0);
-        load_op<BMN, BN>(&tmB, &full_bar[s], st + Cfg::kA, n0, k0);
-        if (bpre) load_op<false, BN>(&tmBl, &full_bar[s], st + Cfg::oBlo, n0, k0);   // B's lo plane
+        const int k0 = (kb0 + kb) * KB;
+        load_op<AMN, GBM, KB>(&tmA, &full_bar[s], st, m0, k0);
+        load_op<BMN, BN, KB>(&tmB, &full_bar[s], st + Cfg::kA, n0, k0);
+        if (bpre) load_op<false, BN, KB>(&tmBl, &full_bar[s], st + Cfg::oBlo, n0, k0);   // B's lo plane
         GT(0, kb);
       }
     }
@@ -403,26 +426,26 @@ __global__ void __launch_bounds__(G2T, OCC)
         const uint32_t tm = DRAIN ? tmem + (uint32_t)((gi & 1) * BN) : tmem;
         const int kbe = min(nkb, gi * G + G);
         for (int kb = gi * G; kb < kbe; ++kb) {
-          const int s = kb % S;
+          const int s = kb % S, sms = kb % SM;   // TMEM A stage, shared-memory stage
           const bool first = DRAIN ? (kb == gi * G) : (kb == 0);
           nbar_sync<kTeamBar>(1 + s);                          // k-block kb split (team kb & 1)
           GT(3, kb);
           asm volatile("tcgen05.fence::after_thread_sync;");
           if (leader) {
-            const uint32_t st = su32(sm + s * Cfg::kStage);
+            const uint32_t st = su32(sm + sms * Cfg::kStage);
             const uint32_t ah = AMN ? st + Cfg::oAhi : st, bh = BMN ? st + Cfg::oBhi : st + Cfg::kA;
             const uint32_t al = st + Cfg::oAlo, bl = st + Cfg::oBlo;
-            const uint32_t ta = tmem + (uint32_t)(kACol + 32 * s);   // this stage's A: hi at +0, lo at +16
+            const uint32_t ta = tmem + (uint32_t)(kACol + 2 * KB * s);   // this stage's A: hi at +0, lo at +KB
   #pragma unroll
-            for (int kk = 0; kk < G2K / 8; ++kk) {   // K = 8 tf32 per MMA
-              const uint64_t dbh = kmajor_desc(bh, kk), dbl = kmajor_desc(bl, kk);
+            for (int kk = 0; kk < KB / 8; ++kk) {   // K = 8 tf32 per MMA
+              const uint64_t dbh = kmajor_desc<KB>(bh, kk), dbl = kmajor_desc<KB>(bl, kk);
               if (ATM) {
                 mma_tf32_ts<Cfg::kIdesc>(tm, ta + 8 * kk, dbl, !(first && kk == 0));        // hi.lo
-                mma_tf32_ts<Cfg::kIdesc>(tm, ta + 16 + 8 * kk, dbh, 1);                     // lo.hi
+                mma_tf32_ts<Cfg::kIdesc>(tm, ta + KB + 8 * kk, dbh, 1);                     // lo.hi
                 mma_tf32_ts<Cfg::kIdesc>(tm, ta + 8 * kk, dbh, 1);                          // hi.hi
                 continue;
               }
-              const uint64_t dah = kmajor_desc(ah, kk), dal = kmajor_desc(al, kk);
+              const uint64_t dah = kmajor_desc<KB>(ah, kk), dal = kmajor_desc<KB>(al, kk);
               if (LOWP) {   // bf16-rounded operands: one MMA
                 mma_tf32_i<Cfg::kIdesc>(tm, dah, dbh, !(first && kk == 0));
                 continue;
@@ -436,7 +459,7 @@ __global__ void __launch_bounds__(G2T, OCC)
           }
           __syncwarp();
         }
-        if (leader) mma_commit(&gdone[gi & 1]);
+        if (leader) mma_commit(&gdone[gi & 3]);
         __syncwarp();
         GT(6, 256 + gi);
       }
@@ -457,7 +480,7 @@ __global__ void __launch_bounds__(G2T, OCC)
     }
     auto drain = [&](int c) {
       if (ct == 0) GT(6, c);
-      mbar_wait(&gdone[c & 1], (c >> 1) & 1);
+      mbar_wait(&gdone[c & 3], (c >> 2) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
       for (int i = 0; i < (DRAIN ? kCI : 1); ++i) {
@@ -486,48 +509,53 @@ __global__ void __launch_bounds__(G2T, OCC)
     const int ngr = (nkb + G - 1) / G;
     int dn = 0;   // next group this thread drains (DRAIN)
     for (int kb = team; kb < nkb; kb += 2) {
-      const int s = kb % S;
-      mbar_wait(&full_bar[s], (kb / S) & 1);
+      // TMEM stage s was last used by k-block kb - S (group g - 2): drained by this thread
+      // before this iteration (DRAIN), so its MMAs are complete
+      const int s = kb % S, sms = kb % SM;
+      mbar_wait(&full_bar[sms], (kb / SM) & 1);
       if (ct == 0) GT(1, kb);
-      uint8_t *st = sm + s * Cfg::kStage;
+      uint8_t *st = sm + sms * Cfg::kStage;
       if (ATM) {
-        // A: row r = 32 q + lane of the tile (this warp's TMEM lane quarter), all 16 k:
-        // hi = trunc_tf32(x), lo = rna_tf32(x - hi) -> two tcgen05.st of 16 columns
+        // A: row r = 32 q + lane of the tile (this warp's TMEM lane quarter), all KB k in halves
+        // of 16: hi = trunc_tf32(x), lo = rna_tf32(x - hi) -> tcgen05.st of 16 columns each
         const int r = 32 * q + lane;
-        float v[16];
-        if (!AMN) {
+        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(kACol + 2 * KB * s);
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const float4 x = *reinterpret_cast<const float4 *>(st + sw64_off(r, jj));
-            v[4 * jj + 0] = x.x; v[4 * jj + 1] = x.y; v[4 * jj + 2] = x.z; v[4 * jj + 3] = x.w;
+        for (int h16 = 0; h16 < KB / 16; ++h16) {
+          float v[16];
+          if (!AMN) {
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              const float4 x = *reinterpret_cast<const float4 *>(st + sw_off<KB>(r, 4 * h16 + jj));
+              v[4 * jj + 0] = x.x; v[4 * jj + 1] = x.y; v[4 * jj + 2] = x.z; v[4 * jj + 3] = x.w;
+            }
+          } else {   // raw MN-major boxes [GBM / 32][KB k][32 rows]
+            const float *src = reinterpret_cast<const float *>(st + (r >> 5) * (32 * KB * 4)) + (r & 31);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = src[(16 * h16 + i) * 32];
           }
-        } else {   // raw MN-major boxes [GBM / 32][16 k][32 rows]
-          const float *src = reinterpret_cast<const float *>(st + (r >> 5) * 2048) + (r & 31);
+          uint32_t hb[16], lb[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = src[i * 32];
+          for (int i = 0; i < 16; ++i) {
+            const uint32_t hh = __float_as_uint(v[i]) & 0xFFFFE000u;
+            hb[i] = hh;
+            lb[i] = __float_as_uint(rna_tf32(v[i] - __uint_as_float(hh)));
+          }
+          asm volatile(
+              "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta + 16 * h16),
+              "r"(hb[0]), "r"(hb[1]), "r"(hb[2]), "r"(hb[3]), "r"(hb[4]), "r"(hb[5]), "r"(hb[6]), "r"(hb[7]), "r"(hb[8]),
+              "r"(hb[9]), "r"(hb[10]), "r"(hb[11]), "r"(hb[12]), "r"(hb[13]), "r"(hb[14]), "r"(hb[15])
+              : "memory");
+          asm volatile(
+              "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta + KB + 16 * h16),
+              "r"(lb[0]), "r"(lb[1]), "r"(lb[2]), "r"(lb[3]), "r"(lb[4]), "r"(lb[5]), "r"(lb[6]), "r"(lb[7]), "r"(lb[8]),
+              "r"(lb[9]), "r"(lb[10]), "r"(lb[11]), "r"(lb[12]), "r"(lb[13]), "r"(lb[14]), "r"(lb[15])
+              : "memory");
         }
-        uint32_t hb[16], lb[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const uint32_t h = __float_as_uint(v[i]) & 0xFFFFE000u;
-          hb[i] = h;
-          lb[i] = __float_as_uint(rna_tf32(v[i] - __uint_as_float(h)));
-        }
-        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(kACol + 32 * s);
-        asm volatile(
-            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta),
-            "r"(hb[0]), "r"(hb[1]), "r"(hb[2]), "r"(hb[3]), "r"(hb[4]), "r"(hb[5]), "r"(hb[6]), "r"(hb[7]), "r"(hb[8]),
-            "r"(hb[9]), "r"(hb[10]), "r"(hb[11]), "r"(hb[12]), "r"(hb[13]), "r"(hb[14]), "r"(hb[15])
-            : "memory");
-        asm volatile(
-            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta + 16),
-            "r"(lb[0]), "r"(lb[1]), "r"(lb[2]), "r"(lb[3]), "r"(lb[4]), "r"(lb[5]), "r"(lb[6]), "r"(lb[7]), "r"(lb[8]),
-            "r"(lb[9]), "r"(lb[10]), "r"(lb[11]), "r"(lb[12]), "r"(lb[13]), "r"(lb[14]), "r"(lb[15])
-            : "memory");
       } else {
-        split_op<AMN, GBM, LOWP>(st, st + Cfg::oAhi, st + Cfg::oAlo, tct, 128);
+        split_op<AMN, GBM, LOWP, KB>(st, st + Cfg::oAhi, st + Cfg::oAlo, tct, 128);
       }
-      if (!bpre) split_op<BMN, BN, LOWP>(st + Cfg::kA, st + Cfg::oBhi, st + Cfg::oBlo, tct, 128);
+      if (!bpre) split_op<BMN, BN, LOWP, KB>(st + Cfg::kA, st + Cfg::oBhi, st + Cfg::oBlo, tct, 128);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic stores -> tensor-core reads
       if (ATM) {
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -654,40 +682,42 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 // fp32 operand with `rows` GEMM rows (M or N) and K columns, stored with leading dimension ld:
 //   K-major  [rows][ld]: dims {K, rows}, box {16, box_rows}, SWIZZLE_64B
 //   MN-major [K][ld]:    dims {rows, K}, box {32, 16},       no swizzle (one box per 32 rows)
-bool make_tmap(CUtensorMap *tm, const float *base, int rows, int K, int ld, int box_rows, bool mn) {
+bool make_tmap(CUtensorMap *tm, const float *base, int rows, int K, int ld, int box_rows, bool mn, int kb = 16) {
   auto enc = tmap_encoder();
   if (!enc) return false;
   const cuuint64_t dims[2] = {(cuuint64_t)(mn ? rows : K), (cuuint64_t)(mn ? K : rows)};
   const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-  const cuuint32_t box[2] = {mn ? 32u : (cuuint32_t)G2K, mn ? (cuuint32_t)G2K : (cuuint32_t)box_rows};
+  const cuuint32_t box[2] = {mn ? 32u : (cuuint32_t)kb, mn ? (cuuint32_t)kb : (cuuint32_t)box_rows};
   const cuuint32_t es[2] = {1, 1};
   return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, mn ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_64B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE,
+             mn ? CU_TENSOR_MAP_SWIZZLE_NONE : (kb == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B),
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // returns the number of K splits (0: not launched); raw: the kernel writes the raw partial
 // products [splits][M][N] into `part` (even unsplit) and the caller's kernel combines them
-template <int BN, bool AMN, bool BMN, bool DRAIN, bool LOWP = false, int OCC = 1>
+template <int BN, bool AMN, bool BMN, bool DRAIN, bool LOWP = false, int OCC = 1, int KB = 16>
 int launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t st, bool raw = false) {
-  using Cfg = G2Cfg<BN, AMN, BMN, !LOWP, DRAIN, OCC>;
+  using Cfg = G2Cfg<BN, AMN, BMN, !LOWP, DRAIN, OCC, KB>;
   CUtensorMap ta, tb, tbl;
-  if (!make_tmap(&ta, g0.A, g0.M, g0.K, g0.lda, GBM, AMN) || !make_tmap(&tb, g0.B, g0.N, g0.K, g0.ldb, BN, BMN))
+  if (!make_tmap(&ta, g0.A, g0.M, g0.K, g0.lda, GBM, AMN, KB) || !make_tmap(&tb, g0.B, g0.N, g0.K, g0.ldb, BN, BMN, KB))
     return 0;
   if (g0.B_lo && !BMN && !LOWP) {
-    if (!make_tmap(&tbl, g0.B_lo, g0.N, g0.K, g0.ldb, BN, false)) return 0;
+    if (!make_tmap(&tbl, g0.B_lo, g0.N, g0.K, g0.ldb, BN, false, KB)) return 0;
   } else {
     tbl = tb;
   }
   static const bool configured =   // thread-safe one-time attribute (concurrent host threads)
-      cudaFuncSetAttribute(gemm_tf32x3_tma_kernel<BN, AMN, BMN, DRAIN, LOWP, OCC>,
+      cudaFuncSetAttribute(gemm_tf32x3_tma_kernel<BN, AMN, BMN, DRAIN, LOWP, OCC, KB>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) == cudaSuccess;
   (void)configured;
   GemmArgs g = g0;
   const int tiles = ((g.N + BN - 1) / BN) * ((g.M + GBM - 1) / GBM);
-  const int nkb = (g.K + G2K - 1) / G2K;
-  // split K to fill the SMs while every split keeps >= 8 k-blocks (measured best of 8 / 16 / none)
-  int splits = std::max(1, std::min(148 * OCC / std::max(tiles, 1), nkb / 8));
+  const int nkb = (g.K + KB - 1) / KB;
+  // split K to fill the SMs while every split keeps >= 128 of K (8 16-deep k-blocks; measured
+  // best of 8 / 16 / none)
+  int splits = std::max(1, std::min(148 * OCC / std::max(tiles, 1), nkb / (128 / KB)));
   if (g0.force & 1) splits = 1;
   while (splits > 1 && (!part || (int64_t)splits * g.M * g.N > part_cap)) --splits;
   g.kbs = (nkb + splits - 1) / splits;
@@ -698,7 +728,7 @@ int launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t st
     g.P = part;
   }
   dim3 grid((g.N + BN - 1) / BN, (g.M + GBM - 1) / GBM, splits);
-  { gemm_tf32x3_tma_kernel<BN, AMN, BMN, DRAIN, LOWP, OCC><<<grid, G2T, Cfg::kSmem, st>>>(ta, tb, tbl, g); ++g_launches; }
+  { gemm_tf32x3_tma_kernel<BN, AMN, BMN, DRAIN, LOWP, OCC, KB><<<grid, G2T, Cfg::kSmem, st>>>(ta, tb, tbl, g); ++g_launches; }
   if (raw) return splits;
   if (splits > 1) {
     const int64_t n4 = ((int64_t)g.M * g.N + 3) / 4;
@@ -711,12 +741,17 @@ int launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t st
   }
   return splits;
 }
+// 32-deep k-blocks (SWIZZLE_128B) where both operands are K-major and the TMEM budget keeps two
+// groups of >= 2 stages: the drained fp32 mode, one CTA per SM, 64 / 128-wide tiles
+template <int BN, bool DRAIN, bool LOWP, int OCC> constexpr bool kUseKB32() {
+  return KG_GEMM_KB32 && DRAIN && !LOWP && OCC == 1 && (BN == 64 || BN == 128);
+}
 template <int BN, bool DRAIN, bool LOWP = false, int OCC = 1>
 int launch_v2_any(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st, bool raw = false) {
   if (g.a_mn) return g.b_mn ? launch_v2<BN, true, true, DRAIN, LOWP, OCC>(g, part, part_cap, st, raw)
                             : launch_v2<BN, true, false, DRAIN, LOWP, OCC>(g, part, part_cap, st, raw);
-  return g.b_mn ? launch_v2<BN, false, true, DRAIN, LOWP, OCC>(g, part, part_cap, st, raw)
-                : launch_v2<BN, false, false, DRAIN, LOWP, OCC>(g, part, part_cap, st, raw);
+  if (g.b_mn) return launch_v2<BN, false, true, DRAIN, LOWP, OCC>(g, part, part_cap, st, raw);
+  return launch_v2<BN, false, false, DRAIN, LOWP, OCC, kUseKB32<BN, DRAIN, LOWP, OCC>() ? 32 : 16>(g, part, part_cap, st, raw);
 }
 }  // namespace
 
@@ -761,6 +796,14 @@ static int launch_gemm_sel(const GemmArgs &g, float *part, int64_t part_cap, cud
     const int nkb = (g.K + G2K - 1) / G2K;
     const int64_t t64 = (int64_t)((g.N + 63) / 64) * ((g.M + GBM - 1) / GBM);
     if (2 * t128 <= 148 && nkb < 16 && t64 <= 148 && t64 > t128) return launch_v2_any<64, true>(g, part, part_cap, st, raw);
+    // short K (<= 512, K-major operands: 32-deep k-blocks) with one wave of 128 x 64 tiles: those,
+    // unsplit (tools/gemm_variants.py, ncu GEMM + combine: 1024 x 400 x 400 11.3 -> 9.8 us,
+    // 512 x 1600 x 400 13.6 -> 10.5 us, 1536 x 400 x 400 12.5 -> 10.4 us)
+    if (kUseKB32<64, true, false, 1>() && !g.a_mn && !g.b_mn && g.K <= 512 && t64 <= 148) {
+      GemmArgs u = g;
+      u.force |= 1;   // no split-K
+      return launch_v2_any<64, true>(u, part, part_cap, st, raw);
+    }
     return launch_v2_any<128, true>(g, part, part_cap, st, raw);
   }
   return wide ? launch_v2_any<256, false>(g, part, part_cap, st, raw) : launch_v2_any<128, false>(g, part, part_cap, st, raw);

@@ -11,11 +11,12 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SO = os.path.join(ROOT, "tools", "libgemm_trace.so")
 SRC = os.path.join(ROOT, "paper_2110_14890_b200", "csrc", "k_gemm.cu")
+SRC2 = os.path.join(ROOT, "paper_2110_14890_b200", "csrc", "k_dag.cu")   # launch_relu_mask
 WRAP = os.path.join(ROOT, "tools", "gemm_trace.cu")
 if not os.path.exists(SO) or os.path.getmtime(SO) < max(os.path.getmtime(SRC), os.path.getmtime(WRAP)):
     subprocess.run(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
                     "-DKG_GEMM_TRACE", "-Xcompiler", "-fPIC", "-shared", "-lcuda", "-I", os.path.join(ROOT, "include"),
-                    WRAP, SRC, "-o", SO], check=True)
+                    WRAP, SRC, SRC2, "-o", SO], check=True)
 lib = C.CDLL(SO)
 M, N, K, ta, tb = (int(x) for x in sys.argv[1:6])
 force = int(sys.argv[6]) if len(sys.argv) > 6 else 0

@@ -56,7 +56,7 @@ def parse(path):
     for name, t in launches:
         if 'gemm_tf32x3' in name:
             calls.append([t, 1])
-        elif calls:
+        elif calls and ('gemm_reduce' in name or 'relu_mask' in name):   # the call's combine / mask pass
             calls[-1][0] += t
             calls[-1][1] += 1
     i = 0
