@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(G2T, OCC)
                            const __grid_constant__ CUtensorMap tmBl, GemmArgs g) {
   KG_GRID_DEP_WAIT();
   using Cfg = G2Cfg<BN, AMN, BMN, !LOWP, DRAIN, OCC, KB>;
-  static_assert(KB == 16 || (KB == 32 && !AMN && !BMN && !LOWP), "32-deep k-blocks: K-major operands");
+  static_assert(KB == 16 || (KB == 32 && !BMN && !LOWP), "32-deep k-blocks: K-major B (A K- or MN-major)");
   constexpr int S = Cfg::kStages, G = Cfg::kGroup, SM = Cfg::kSmemStages;
   static_assert(SM >= S && SM <= S + G, "shared-memory stages");
   // TMEM columns: a power of 2 >= 32 holding one (or, drained, two) BN-column accumulators
@@ -749,7 +749,8 @@ template <int BN, bool DRAIN, bool LOWP, int OCC> constexpr bool kUseKB32() {
 template <int BN, bool DRAIN, bool LOWP = false, int OCC = 1>
 int launch_v2_any(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st, bool raw = false) {
   if (g.a_mn) return g.b_mn ? launch_v2<BN, true, true, DRAIN, LOWP, OCC>(g, part, part_cap, st, raw)
-                            : launch_v2<BN, true, false, DRAIN, LOWP, OCC>(g, part, part_cap, st, raw);
+                            : launch_v2<BN, true, false, DRAIN, LOWP, OCC, kUseKB32<BN, DRAIN, LOWP, OCC>() ? 32 : 16>(
+                                  g, part, part_cap, st, raw);
   if (g.b_mn) return launch_v2<BN, false, true, DRAIN, LOWP, OCC>(g, part, part_cap, st, raw);
   return launch_v2<BN, false, false, DRAIN, LOWP, OCC, kUseKB32<BN, DRAIN, LOWP, OCC>() ? 32 : 16>(g, part, part_cap, st, raw);
 }

@@ -80,7 +80,12 @@ def test_gemm_rejects_unaligned_leading_dimension():
                                          (False, False, 1536, 800, 1600),   # dX = dH1 W1
                                          (False, True, 200, 72, 40), (True, False, 70, 130, 33),
                                          (False, True, 1024, 1024, 200),    # S = Q E^T (ComplEx C3): 128 x 64
-                                         (True, True, 300, 200, 120)])
+                                         (True, True, 300, 200, 120),
+                                         # 32-deep k-blocks (K-major B): the unsplit 128 x 64 short-K form,
+                                         # 128 x 128 with split K, and MN-major A (dW = dY^T X with X^T stored)
+                                         (False, False, 1024, 400, 400), (False, False, 512, 1600, 400),
+                                         (False, False, 1024, 1600, 1600), (True, False, 400, 1600, 1024),
+                                         (True, False, 1600, 800, 512), (True, False, 100, 60, 70)])
 def test_gemm_drained_accumulation(ta, tb, M, N, K):
     """The drained form (fp32-accurate, the default; 128 x 128, 128 x 160 or, for few tiles and a
     short K, 128 x 64 tiles)."""

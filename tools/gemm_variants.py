@@ -15,6 +15,10 @@ for gm in (512, 1024, 1536):
                (D, H, gm, 1, 1), (H, H, gm, 1, 1), (H, 2 * D, gm, 1, 1)]     # dW = dY^T X
 for nr in (512, 1024, 1536):
     SHAPES += [(nr, D, D, 0, 0), (D, D, nr, 1, 1)]                            # d x d intersection MLPs
+DW = [(D, H, nr, 1, 0) for nr in (512, 1024, 1536)] + [(H, H, nr, 1, 0) for nr in (512, 1024, 1536)] + \
+     [(H, 2 * D, nr, 1, 0) for nr in (512, 1024, 1536)]                     # BetaE dW = dY^T X, X^T stored
+if "--dw" in sys.argv:
+    SHAPES = DW
 VARIANTS = [(None, "auto"), (1 | (1 << 1), "bn64-nosplit"), (1 | (2 << 1), "bn128-nosplit"),
             (1 | (3 << 1), "bn160-nosplit"), (1 << 1, "bn64-split"), (2 << 1, "bn128-split"), (3 << 1, "bn160-split"),
             (8, "bn64-occ2-split"), (8 | 1, "bn64-occ2-nosplit")]
