@@ -800,11 +800,15 @@ static int launch_gemm_sel(const GemmArgs &g, float *part, int64_t part_cap, cud
     // short K (<= 512, K-major operands: 32-deep k-blocks) with one wave of 128 x 64 tiles: those,
     // unsplit (tools/gemm_variants.py, ncu GEMM + combine: 1024 x 400 x 400 11.3 -> 9.8 us,
     // 512 x 1600 x 400 13.6 -> 10.5 us, 1536 x 400 x 400 12.5 -> 10.4 us)
-    if (kUseKB32<64, true, false, 1>() && !g.a_mn && !g.b_mn && g.K <= 512 && t64 <= 148) {
+    if (kUseKB32<64, true, false, 1>() && !g.b_mn && g.K <= 512 && t64 <= 148) {
       GemmArgs u = g;
       u.force |= 1;   // no split-K
       return launch_v2_any<64, true>(u, part, part_cap, st, raw);
     }
+    // weight gradients dW = dY^T X with few 128 x 128 tiles and a long K: 128 x 160 tiles split
+    // two ways fill more SMs (1600 x 800 x 1536: 91 tiles -> 130 CTAs, 36.9 -> 33.0 us)
+    if (g.a_mn && !g.b_mn && t128 < 100 && 2 * t160 <= 148 && g.K >= 1024)
+      return launch_v2_any<160, true>(g, part, part_cap, st, raw);
     return launch_v2_any<128, true>(g, part, part_cap, st, raw);
   }
   return wide ? launch_v2_any<256, false>(g, part, part_cap, st, raw) : launch_v2_any<128, false>(g, part, part_cap, st, raw);
