@@ -800,7 +800,9 @@ static int launch_gemm_sel(const GemmArgs &g, float *part, int64_t part_cap, cud
     // short K (<= 512, K-major operands: 32-deep k-blocks) with one wave of 128 x 64 tiles: those,
     // unsplit (tools/gemm_variants.py, ncu GEMM + combine: 1024 x 400 x 400 11.3 -> 9.8 us,
     // 512 x 1600 x 400 13.6 -> 10.5 us, 1536 x 400 x 400 12.5 -> 10.4 us)
-    if (kUseKB32<64, true, false, 1>() && !g.b_mn && g.K <= 512 && t64 <= 148) {
+    // (and K <= 1024 where the 128 x 64 tiles alone fill two thirds of the SMs: 512 x 1600 x 800
+    // 17.7 -> 16.0 us)
+    if (kUseKB32<64, true, false, 1>() && !g.b_mn && t64 <= 148 && (g.K <= 512 || (g.K <= 1024 && t64 >= 96))) {
       GemmArgs u = g;
       u.force |= 1;   // no split-K
       return launch_v2_any<64, true>(u, part, part_cap, st, raw);
