@@ -744,7 +744,7 @@ int launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t st
 // 32-deep k-blocks (SWIZZLE_128B) where both operands are K-major and the TMEM budget keeps two
 // groups of >= 2 stages: the drained fp32 mode, one CTA per SM, 64 / 128-wide tiles
 template <int BN, bool DRAIN, bool LOWP, int OCC> constexpr bool kUseKB32() {
-  return KG_GEMM_KB32 && DRAIN && !LOWP && OCC == 1 && (BN == 64 || BN == 128);
+  return KG_GEMM_KB32 && DRAIN && !LOWP && OCC == 1 && (BN == 64 || BN == 96 || BN == 128);
 }
 template <int BN, bool DRAIN, bool LOWP = false, int OCC = 1>
 int launch_v2_any(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st, bool raw = false) {
@@ -780,6 +780,7 @@ static int launch_gemm_sel(const GemmArgs &g, float *part, int64_t part_cap, cud
       return f.drain ? launch_v2_any<BN, true>(f, part, part_cap, st, raw) : launch_v2_any<BN, false>(f, part, part_cap, st, raw);
     };
     if (g.force & 8) return f.drain ? launch_v2_any<64, true, false, 2>(f, part, part_cap, st, raw) : 0;   // 2 per SM
+    if (g.force & 16) return f.drain ? launch_v2_any<96, true>(f, part, part_cap, st, raw) : 0;           // 96 wide
     if (bn == 1) return go(std::integral_constant<int, 64>());
     if (bn == 3) return go(std::integral_constant<int, 160>());
     return go(std::integral_constant<int, 128>());
@@ -811,6 +812,15 @@ static int launch_gemm_sel(const GemmArgs &g, float *part, int64_t part_cap, cud
     // two ways fill more SMs (1600 x 800 x 1536: 91 tiles -> 130 CTAs, 36.9 -> 33.0 us)
     if (g.a_mn && !g.b_mn && t128 < 100 && 2 * t160 <= 148 && g.K >= 1024)
       return launch_v2_any<160, true>(g, part, part_cap, st, raw);
+    // SM coverage: 96-wide tiles when they give a markedly fuller single wave than 128-wide ones
+    // (e.g. 512 x 1600 x 1600: 52 tiles x 2 splits = 104 CTAs -> 68 x 2 = 136), K-major B
+    if (kUseKB32<96, true, false, 1>() && !g.b_mn) {
+      const int nkb32 = (g.K + 31) / 32;
+      const int64_t t96 = (int64_t)((g.N + 95) / 96) * ((g.M + GBM - 1) / GBM);
+      const int64_t c128 = t128 * std::max<int64_t>(1, std::min<int64_t>(148 / std::max<int64_t>(t128, 1), nkb32 / 4));
+      const int64_t c96 = t96 * std::max<int64_t>(1, std::min<int64_t>(148 / std::max<int64_t>(t96, 1), nkb32 / 4));
+      if (t96 <= 148 && 20 * c96 > 23 * c128) return launch_v2_any<96, true>(g, part, part_cap, st, raw);
+    }
     return launch_v2_any<128, true>(g, part, part_cap, st, raw);
   }
   return wide ? launch_v2_any<256, false>(g, part, part_cap, st, raw) : launch_v2_any<128, false>(g, part, part_cap, st, raw);

@@ -12,7 +12,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _run(ta, tb, M, N, K, bias=False, relu=False, beta=0.0, seed=0, drain=False):
+def _run(ta, tb, M, N, K, bias=False, relu=False, beta=0.0, seed=0, drain=False, force=0):
     import torch
     import paper_2110_14890_b200 as kgb
     rng = np.random.default_rng(seed)
@@ -32,7 +32,7 @@ def _run(ta, tb, M, N, K, bias=False, relu=False, beta=0.0, seed=0, drain=False)
     tA, tB, tC, tb_ = (torch.from_numpy(x).to(dev) for x in (Ap, Bp, C0, b))
     st = torch.cuda.current_stream()
     s = kgb.kg_test_gemm(int(ta), int(tb), M, N, K, tA.data_ptr(), Ap.shape[1], tB.data_ptr(), Bp.shape[1],
-                         tC.data_ptr(), N, tb_.data_ptr() if bias else None, int(relu) | (2 if drain else 0), beta,
+                         tC.data_ptr(), N, tb_.data_ptr() if bias else None, int(relu) | (2 if drain else 0) | (force << 2), beta,
                          C.c_void_p(st.cuda_stream))
     assert s == 0
     opA = A.T.astype(np.float64) if ta else A.astype(np.float64)
@@ -90,3 +90,12 @@ def test_gemm_drained_accumulation(ta, tb, M, N, K):
     """The drained form (fp32-accurate, the default; 128 x 128, 128 x 160 or, for few tiles and a
     short K, 128 x 64 tiles)."""
     _run(ta, tb, M, N, K, bias=not ta, relu=not ta, drain=True)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ta,M,N,K", [(False, 512, 1600, 1600), (False, 200, 100, 70), (True, 400, 1600, 1024),
+                                      (False, 130, 96, 33)])
+def test_gemm_96_wide_tiles(ta, M, N, K):
+    """The 128 x 96 tile form (32-deep k-blocks, K-major B; chosen for fuller SM coverage), forced."""
+    _run(ta, False, M, N, K, bias=not ta, relu=not ta, drain=True, force=16)
+
