@@ -19,9 +19,11 @@ DW = [(D, H, nr, 1, 0) for nr in (512, 1024, 1536)] + [(H, H, nr, 1, 0) for nr i
      [(H, 2 * D, nr, 1, 0) for nr in (512, 1024, 1536)]                     # BetaE dW = dY^T X, X^T stored
 if "--dw" in sys.argv:
     SHAPES = DW
+if "--kmajor" in sys.argv:   # the K-major-B shapes of the BetaE step (forward, dX, dW on X^T)
+    SHAPES = [sh for sh in SHAPES if sh[4] == 0 and sh[3] == 0] + DW
 VARIANTS = [(None, "auto"), (1 | (1 << 1), "bn64-nosplit"), (1 | (2 << 1), "bn128-nosplit"),
             (1 | (3 << 1), "bn160-nosplit"), (1 << 1, "bn64-split"), (2 << 1, "bn128-split"), (3 << 1, "bn160-split"),
-            (8, "bn64-occ2-split"), (8 | 1, "bn64-occ2-nosplit")]
+            (8, "bn64-occ2-split"), (8 | 1, "bn64-occ2-nosplit"), (16, "bn96-split"), (16 | 1, "bn96-nosplit")]
 if "--small" in sys.argv:   # the d x d shapes only
     SHAPES = [sh for sh in SHAPES if sh[0] <= 1536 and sh[1] <= 400 and sh[2] <= 1536 and min(sh[:3]) == 400]
 
