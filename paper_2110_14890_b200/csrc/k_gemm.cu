@@ -151,7 +151,11 @@ template <int BN, bool AMN, bool BMN, bool ATM = true, bool DRAIN = true, int OC
   // stages: shared memory (224 KB budget), at most 8, and (ATM) 32 TMEM columns each after
   // the accumulator(s)
   static constexpr int kTmemCols = OCC == 2 ? 256 : 512;
-  static constexpr int kTmemFit = ATM ? (kTmemCols - (DRAIN ? 2 * BN : BN)) / (2 * KB) : 8;   // A hi + lo per stage
+  // SACC: one drained accumulator instead of two (160-wide, 32-deep: two 160-column accumulators
+  // would leave TMEM for only three 64-column A stages); the MMA of group g + 1 then waits for the
+  // drain of group g
+  static constexpr bool kSacc = DRAIN && KB == 32 && BN > 128;
+  static constexpr int kTmemFit = ATM ? (kTmemCols - (DRAIN && !kSacc ? 2 * BN : BN)) / (2 * KB) : 8;   // A hi + lo per stage
   static constexpr int kSmemFit = ((OCC == 2 ? 108 : 224) * 1024) / kStage;
   static constexpr int kFit = kSmemFit < 8 ? (kSmemFit < kTmemFit ? kSmemFit : kTmemFit) : (8 < kTmemFit ? 8 : kTmemFit);
   static constexpr int kStages = kFit >= 2 ? (kFit / 2) * 2 : 2;
@@ -343,7 +347,8 @@ __global__ void __launch_bounds__(G2T, OCC)
   constexpr int S = Cfg::kStages, G = Cfg::kGroup, SM = Cfg::kSmemStages;
   static_assert(SM >= S && SM <= S + G, "shared-memory stages");
   // TMEM columns: a power of 2 >= 32 holding one (or, drained, two) BN-column accumulators
-  constexpr int kNeed = DRAIN ? 2 * BN : BN;
+  constexpr bool SACC = Cfg::kSacc;
+  constexpr int kNeed = DRAIN && !SACC ? 2 * BN : BN;
   // ATM (every fp32-accurate mode): the A operand's hi / lo tiles of each stage live in tensor
   // memory (32 columns per stage after the accumulators), written by the split warps with
   // tcgen05.st; the MMAs then read only B from shared memory.  Shared-memory traffic per
@@ -421,9 +426,10 @@ __global__ void __launch_bounds__(G2T, OCC)
     {
       const int ngr = (nkb + G - 1) / G;
       for (int gi = 0; gi < ngr; ++gi) {
-        if (DRAIN && gi >= 2) nbar_sync<kAllBar>(1 + S + (gi & 1));   // group gi-2 drained
+        if (DRAIN && !SACC && gi >= 2) nbar_sync<kAllBar>(1 + S + (gi & 1));      // group gi-2 drained
+        if (DRAIN && SACC && gi >= 1) nbar_sync<kAllBar>(1 + S + ((gi - 1) & 1));  // group gi-1 drained
         GT(7, 256 + gi);
-        const uint32_t tm = DRAIN ? tmem + (uint32_t)((gi & 1) * BN) : tmem;
+        const uint32_t tm = DRAIN && !SACC ? tmem + (uint32_t)((gi & 1) * BN) : tmem;
         const int kbe = min(nkb, gi * G + G);
         for (int kb = gi * G; kb < kbe; ++kb) {
           const int s = kb % S, sms = kb % SM;   // TMEM A stage, shared-memory stage
@@ -493,7 +499,7 @@ __global__ void __launch_bounds__(G2T, OCC)
               "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
               "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
               "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-            : "r"(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((c & 1) * BN + 32 * (half + NG * i))));
+            : "r"(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((SACC ? 0 : (c & 1) * BN) + 32 * (half + NG * i))));
         asm volatile("tcgen05.wait::ld.sync.aligned;");
 #pragma unroll
         for (int j = 0; j < 32; ++j) acc[i][j] += __uint_as_float(r[j]);
@@ -744,7 +750,7 @@ int launch_v2(const GemmArgs &g0, float *part, int64_t part_cap, cudaStream_t st
 // 32-deep k-blocks (SWIZZLE_128B) where both operands are K-major and the TMEM budget keeps two
 // groups of >= 2 stages: the drained fp32 mode, one CTA per SM, 64 / 128-wide tiles
 template <int BN, bool DRAIN, bool LOWP, int OCC> constexpr bool kUseKB32() {
-  return KG_GEMM_KB32 && DRAIN && !LOWP && OCC == 1 && (BN == 64 || BN == 96 || BN == 128);
+  return KG_GEMM_KB32 && DRAIN && !LOWP && OCC == 1 && (BN == 64 || BN == 96 || BN == 128 || BN == 160);
 }
 template <int BN, bool DRAIN, bool LOWP = false, int OCC = 1>
 int launch_v2_any(const GemmArgs &g, float *part, int64_t part_cap, cudaStream_t st, bool raw = false) {
