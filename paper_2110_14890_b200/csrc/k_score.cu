@@ -656,7 +656,13 @@ __global__ void __launch_bounds__(kBW * 32, BwdOcc<Mdl>::v) pair_bwd_kernel(Scor
 // exact).  The terms and their fp32 arithmetic are those of pair_bwd_kernel<MBox>; it writes
 // the same partials (rows t M + i), so the combines are shared.
 constexpr int kICU = 8;   // query rows per staged chunk (two disjunct rows each; 52 KB of shared memory)
-__global__ void __launch_bounds__(kBW * 32, 3) pair_bwd_union_box_kernel(ScoreArgs a) {
+#ifndef KG_UNION_OCC
+#define KG_UNION_OCC 3
+#endif
+// resident CTAs per SM (4, at 64 registers with a small spill, measured slower: C5-q2b 2u scoring
+// backward 0.207 -> 0.232 ms)
+constexpr int kUnionOcc = KG_UNION_OCC;
+__global__ void __launch_bounds__(kBW * 32, kUnionOcc) pair_bwd_union_box_kernel(ScoreArgs a) {
   KG_GRID_DEP_WAIT();
   constexpr int JB = kBW * kJW;
   extern __shared__ __align__(16) float smem[];
@@ -1081,7 +1087,7 @@ static void launch_bwd(ScoreArgs a, cudaStream_t st, cudaStream_t st2) {
   const bool union_box = std::is_same<Mdl, MBox>::value && a.NQ == 2 * a.M;
   if (union_box) {
     const int chunks = (a.M + kICU - 1) / kICU;
-    int is = (3 * 148) / (kt * jt);   // one wave of the 3 resident CTAs per SM (ncu: 5 splits were 1.17 waves)
+    int is = (kUnionOcc * 148) / (kt * jt);   // one wave of the resident CTAs (ncu: 5 splits at 3 per SM were 1.17 waves)
     is = std::max(1, std::min(is, std::min(16, chunks)));
     while (is > 1 && (int64_t)is * a.K * a.U > a.cap_V) --is;
     a.rps = ((chunks + is - 1) / is) * kICU;
