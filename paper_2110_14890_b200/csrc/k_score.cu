@@ -474,6 +474,15 @@ __global__ void __launch_bounds__(256) pair_epi_kernel(ScoreArgs a) {
 // (row, j-block of NW*JW).  blockIdx.z splits the rows; all partial sums are
 // added by the combine kernels in a fixed order (deterministic, no atomics).
 constexpr int kBW = 8, kJW = 16, kIC = 16;
+// the t = 0 factor of the box backward from the FMA pipe (sat(|t| 2^126)) instead of a compare:
+// fewer instructions (80.6 -> 73.9 M per launch) but the FMA pipe becomes the limiter, C5-q2b
+// pair_bwd 120 -> 130 us, so off for the single-disjunct kernel; KG_UNION_NZ_SAT for the union one
+#ifndef KG_BOX_NZ_SAT
+#define KG_BOX_NZ_SAT 0
+#endif
+#ifndef KG_UNION_NZ_SAT
+#define KG_UNION_NZ_SAT 1
+#endif
 // resident CTAs per SM for the fused backward: 4 where the per-term state fits 64 registers
 // without spills (measured +4 % C5-q2b q/s over 2), 2 for the 2- / 4-feature models
 template <class Mdl> struct BwdOcc { static constexpr int v = (Mdl::BF == 1 && Mdl::AV == 1) ? 4 : 2; };
@@ -546,9 +555,18 @@ __global__ void __launch_bounds__(kBW * 32, BwdOcc<Mdl>::v) pair_bwd_kernel(Scor
             const float2 W = make_float2(fmaf(a.alpha, ax < o ? 1.f : 0.f, ax > o ? 1.f : 0.f),
                                          fmaf(a.alpha, ay < o ? 1.f : 0.f, ay > o ? 1.f : 0.f));
             const float2 cw = __fmul2_rn(cf, W);
+#if KG_BOX_NZ_SAT
+            // sign(t) cw, 0 at t = 0 (A19): unconditional sign transfer (LOP3) times a 0 / 1
+            // factor from the FMA pipe, sat(|t| 2^126) (1 for every normal |t|, 0 at t = 0),
+            // instead of a compare + predicated LOP3 on the ALU pipe (this loop's limiter)
+            const float2 csg = make_float2(__int_as_float(__float_as_int(cw.x) ^ (__float_as_int(t.x) & 0x80000000)),
+                                           __int_as_float(__float_as_int(cw.y) ^ (__float_as_int(t.y) & 0x80000000)));
+            const float2 cg = __fmul2_rn(csg, make_float2(__saturatef(ax * 0x1p126f), __saturatef(ay * 0x1p126f)));
+#else
             const float2 cg = make_float2(
                 t.x == 0.f ? 0.f : __int_as_float(__float_as_int(cw.x) ^ (__float_as_int(t.x) & 0x80000000)),
                 t.y == 0.f ? 0.f : __int_as_float(__float_as_int(cw.y) ^ (__float_as_int(t.y) & 0x80000000)));
+#endif
             gq0 = __fadd2_rn(gq0, cg);
             gq1 = __fadd2_rn(gq1, cw);
             const float2 dvp = __fadd2_rn(make_float2(dv[2 * jp][0], dv[2 * jp + 1][0]), cg);
@@ -741,7 +759,12 @@ __global__ void __launch_bounds__(kBW * 32, kUnionOcc) pair_bwd_union_box_kernel
           // pipe instead of a select (this loop's ALU pipe also carries the disjunct selects)
           const float2 csg = make_float2(__int_as_float(__float_as_int(cw.x) ^ (__float_as_int(t.x) & 0x80000000)),
                                          __int_as_float(__float_as_int(cw.y) ^ (__float_as_int(t.y) & 0x80000000)));
+#if KG_UNION_NZ_SAT
+          // the 0 / 1 factor from the FMA pipe: sat(|t| 2^126) (1 for every normal |t|, 0 at t = 0)
+          const float2 cg = __fmul2_rn(csg, make_float2(__saturatef(ax * 0x1p126f), __saturatef(ay * 0x1p126f)));
+#else
           const float2 cg = __fmul2_rn(csg, make_float2(t.x != 0.f ? 1.f : 0.f, t.y != 0.f ? 1.f : 0.f));
+#endif
           gA0 = __ffma2_rn(cg, nt, gA0);
           gB0 = __ffma2_rn(cg, tf, gB0);
           gA1 = __ffma2_rn(cw, nt, gA1);
