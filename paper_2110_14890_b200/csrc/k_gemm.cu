@@ -113,12 +113,14 @@ __global__ void gemm_reduce_kernel(const float *__restrict__ P, int splits, int 
 
 
 // ================================================================ v2: TMA + warp specialisation
-// Tile 128 (M) x BN (N) x 16 (K), 6 warps with fixed roles:
+// Tile 128 (M) x BN (N) x KB (K; KB = 16, or 32 for K-major B at 64- to 160-wide tiles), 10 warps
+// with fixed roles:
 //   warp 0      TMA producer: cp.async.bulk.tensor of the raw fp32 A / B tiles into stage s
 //               (zero fill out of bounds), completion on full[s];
-//   warp 1      TMEM allocator + MMA issuer: per k-block 2 K-steps x 3 tcgen05.mma
-//               (hi.hi, hi.lo, lo.hi), committed to empty[s];
-//   warps 2-5   split + epilogue: lo = x - trunc_tf32(x) of the landed tiles (kind::tf32 reads
+//   warp 1      TMEM allocator + MMA issuer: per k-block KB / 8 K-steps x 3 tcgen05.mma
+//               (hi.hi, hi.lo, lo.hi), one commit per group of k-blocks;
+//   warps 2-9   split + drain + epilogue (two teams on alternate k-blocks): lo = x - trunc_tf32(x)
+//               of the landed A tile into tensor memory (kind::tf32 reads
 //               the raw fp32 words of a K-major tile as hi = trunc_tf32(x)), then tcgen05.ld of
 //               the accumulator quarter their warp may access (lanes 32 (w % 4) ..) -> per-warp
 //               staging tile -> bias / ReLU / beta C -> coalesced row stores.
@@ -126,7 +128,8 @@ __global__ void gemm_reduce_kernel(const float *__restrict__ P, int splits, int 
 // an operand stored MN-major (A [K][M], B [K][N], e.g. both operands of dW = dY^T X) is
 // brought in as raw 32 x 16 boxes and the split warps transpose it while splitting, writing
 // hi and lo K-major tiles; no global transpose pass.
-// K-major smem tiles: rows of 16 fp32 (64 B), SWIZZLE_64B, 8-row groups 512 B apart.
+// K-major smem tiles: rows of KB fp32 (64 B, SWIZZLE_64B, 8-row groups 512 B apart; or 128 B,
+// SWIZZLE_128B, 1024 B apart).
 #ifndef KG_G2CW
 #define KG_G2CW 8
 #endif
