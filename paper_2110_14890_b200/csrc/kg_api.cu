@@ -1833,22 +1833,22 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   {
     cudaStream_t s2 = h->st2;
     mark(h, 8, s2);
-    if ((s = wjoin(h, s2)) != KG_OK) return s;
     launch_rel_reduce(h->rseg, h->rperm, h->rinv, h->rU, Lr, h->RG, h->PSr, h->dr, h->RGU, s2);
+    const double b1 = h->cfg.beta1, b2 = h->cfg.beta2, eps = h->cfg.eps;
+    const float *lr = h->lr_dev;
     if (h->apply) {
-      const double b1 = h->cfg.beta1, b2 = h->cfg.beta2, eps = h->cfg.eps;
-      const float *lr = h->lr_dev;
       CK(cudaStreamWaitEvent(s2, h->ev_early, 0));
-      {
-        // the relation rows used by this step: segs[0] (and segs[1] for Q2B: rel_offset right after)
-        const Seg &r = h->segs[0];
-        const int nseg = h->kind == KG_Q2B ? 2 : 1;
-        launch_dense_adam_rel_touched(h->t.dense + r.off, h->t.dense_m + r.off, h->t.dense_v + r.off, h->R, r.cols,
-                                      nseg, h->RGU, h->runiq, h->rU, Lr, lr, b1, b2, eps, h->bc, h->flags, s2);
-      }
+      // the relation rows used by this step: segs[0] (and segs[1] for Q2B: rel_offset right after)
+      const Seg &r = h->segs[0];
+      const int nseg = h->kind == KG_Q2B ? 2 : 1;
+      launch_dense_adam_rel_touched(h->t.dense + r.off, h->t.dense_m + r.off, h->t.dense_v + r.off, h->R, r.cols,
+                                    nseg, h->RGU, h->runiq, h->rU, Lr, lr, b1, b2, eps, h->bc, h->flags, s2);
+    }
+    // only the operator weights' Adam needs the weight gradients of st5 (the relation rows' do not)
+    if ((s = wjoin(h, s2)) != KG_OK) return s;
+    if (h->apply)
       launch_dense_adam(h->t.dense + h->w_off, h->t.dense_m + h->w_off, h->t.dense_v + h->w_off, h->gdense,
                         h->dense_size - h->w_off, lr, b1, b2, eps, h->bc, h->flags, s2);
-    }
     mark(h, 9, s2);
     CK(cudaEventRecord(h->ev_join, s2));
   }
