@@ -416,6 +416,53 @@ __global__ void __launch_bounds__(256) pair_epi_kernel(ScoreArgs a) {
 #pragma unroll
   for (int tt = 0; tt < NOUT; ++tt) csum[tt] = 0.f;
   const int jend = TRAIN ? a.Kp : K;
+  if (TRAIN && !Mdl::kBeta && !(K & 3) && !(a.Kp & 3) && (a.Dmin == nullptr)) {
+    // 4 consecutive candidates per thread (float4 loads of the partials and stores of C); the
+    // per-pair arithmetic is the scalar loop's below
+    const float4 *Dp = reinterpret_cast<const float4 *>(a.Dpart);
+    for (int j4 = threadIdx.x; j4 * 4 < jend; j4 += blockDim.x) {
+      const int j0 = j4 * 4;
+      float4 D4[NOUT];
+#pragma unroll
+      for (int tt = 0; tt < NOUT; ++tt) {
+        const size_t base = ((size_t)(tt * M + i) * a.Kp + j0) / 4;
+        float4 s4 = Dp[base];
+        for (int z = 1; z < a.KS; ++z) {
+          const float4 q = Dp[z * zs / 4 + base];
+          s4.x += q.x; s4.y += q.y; s4.z += q.z; s4.w += q.w;
+        }
+        D4[tt] = make_float4(Mdl::fin(s4.x, 0.f, 0.f), Mdl::fin(s4.y, 0.f, 0.f), Mdl::fin(s4.z, 0.f, 0.f),
+                             Mdl::fin(s4.w, 0.f, 0.f));
+      }
+      const uint32_t word = j0 < K ? a.mask[(size_t)i * a.W + (j0 >> 5)] : 0u;
+      float cf[NOUT][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = j0 + u;
+        float D[NOUT];
+#pragma unroll
+        for (int tt = 0; tt < NOUT; ++tt) D[tt] = u == 0 ? D4[tt].x : u == 1 ? D4[tt].y : u == 2 ? D4[tt].z : D4[tt].w;
+        int tm = 0;
+        float Dm = D[0];
+        if (NOUT == 2 && D[1] < D[0]) { tm = 1; Dm = D[1]; }   // DNF min, ties -> lowest (A11)
+        float c = 0.f;
+        if (j < K && ((word >> (j & 31)) & 1u)) {
+          c = -sigm_(a.gamma - Dm) * inv_n * a.scale;         // dl/dD_ij of Eq. 1 (A12)
+          lsum += softplusf_(a.gamma - Dm) * inv_n;
+        }
+#pragma unroll
+        for (int tt = 0; tt < NOUT; ++tt) {
+          float coef = (tt == tm) ? c : 0.f;
+          csum[tt] += coef;
+          if (Mdl::kL2) coef = (coef != 0.f && D[tt] > 0.f) ? coef / D[tt] : 0.f;
+          cf[tt][u] = coef;
+        }
+      }
+#pragma unroll
+      for (int tt = 0; tt < NOUT; ++tt)
+        *reinterpret_cast<float4 *>(a.C + (size_t)(tt * M + i) * a.Kp + j0) = make_float4(cf[tt][0], cf[tt][1], cf[tt][2], cf[tt][3]);
+    }
+  } else
   for (int j = threadIdx.x; j < jend; j += blockDim.x) {
     if (j >= K) {
 #pragma unroll
@@ -1145,7 +1192,7 @@ template <class F> static int gpu_slots(F kernel, int threads) {
 }
 
 template <class Mdl>
-static void launch_pair(ScoreArgs a, int nout, bool train, cudaStream_t st) {
+static void launch_pair(ScoreArgs a, int nout, bool train, cudaStream_t st, const std::function<void()> &between) {
   const int tiles = ((a.K + 63) / 64) * ((a.M + 63) / 64);
   const int chunks = (a.U + 15) / 16;
   static const int slots1 = gpu_slots(pair_fwd_kernel<Mdl, 1>, 256), slots2 = gpu_slots(pair_fwd_kernel<Mdl, 2>, 256);
@@ -1155,23 +1202,26 @@ static void launch_pair(ScoreArgs a, int nout, bool train, cudaStream_t st) {
   dim3 gf((a.K + 63) / 64, (a.M + 63) / 64, a.KS);
   if (nout == 1) {
     { pair_fwd_kernel<Mdl, 1><<<gf, 256, 0, st>>>(a); ++g_launches; }
+    if (between) between();
     if (train) { pair_epi_kernel<Mdl, 1, true><<<a.M, 256, 0, st>>>(a); ++g_launches; }
     else { pair_epi_kernel<Mdl, 1, false><<<a.M, 256, 0, st>>>(a); ++g_launches; }
   } else {
     { pair_fwd_kernel<Mdl, 2><<<gf, 256, 0, st>>>(a); ++g_launches; }
+    if (between) between();
     if (train) { pair_epi_kernel<Mdl, 2, true><<<a.M, 256, 0, st>>>(a); ++g_launches; }
     else { pair_epi_kernel<Mdl, 2, false><<<a.M, 256, 0, st>>>(a); ++g_launches; }
   }
 }
 
-void launch_pair_fwd(int kind, const ScoreArgs &a, int nout, bool train, cudaStream_t st) {
+void launch_pair_fwd(int kind, const ScoreArgs &a, int nout, bool train, cudaStream_t st,
+                     const std::function<void()> &between) {
   switch (kind) {
-    case GQE: case TRANSE: launch_pair<ML2>(a, nout, train, st); break;
-    case Q2B: launch_pair<MBox>(a, nout, train, st); break;
-    case BETAE: launch_pair<MBeta>(a, nout, train, st); break;
-    case ROTATE: launch_pair<MRot>(a, nout, train, st); break;
-    case DISTMULT: launch_pair<MDot>(a, nout, train, st); break;
-    case COMPLEX: launch_pair<MCpx>(a, nout, train, st); break;
+    case GQE: case TRANSE: launch_pair<ML2>(a, nout, train, st, between); break;
+    case Q2B: launch_pair<MBox>(a, nout, train, st, between); break;
+    case BETAE: launch_pair<MBeta>(a, nout, train, st, between); break;
+    case ROTATE: launch_pair<MRot>(a, nout, train, st, between); break;
+    case DISTMULT: launch_pair<MDot>(a, nout, train, st, between); break;
+    case COMPLEX: launch_pair<MCpx>(a, nout, train, st, between); break;
   }
 }
 
