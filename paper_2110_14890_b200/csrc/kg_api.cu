@@ -1679,11 +1679,13 @@ struct LowpScope {
   ~LowpScope() { h->gemm_lowp = false; }
 };
 bool gemm_scoring(const kg_handle *h) { return h->sk == KG_DISTMULT || h->sk == KG_COMPLEX; }
-kg_status score_forward(kg_handle *h, ScoreArgs &sa, int nout, bool train, const int64_t *neg_rows) {
+kg_status score_forward(kg_handle *h, ScoreArgs &sa, int nout, bool train, const int64_t *neg_rows,
+                        const std::function<void()> &between = {}) {
   if (!gemm_scoring(h)) {
-    launch_pair_fwd(h->sk, sa, nout, train, h->st);
+    launch_pair_fwd(h->sk, sa, nout, train, h->st, between);
     return KG_OK;
   }
+  if (between) between();
   launch_gather_rows(h->Eg, h->ent_src, neg_rows, sa.K, h->d, h->st);
   sa.KS = 1;
   LowpScope lp(h, train && h->score_bf16);
@@ -1761,9 +1763,17 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   // the positive term (D+, its adjoint and gradients: per query): BetaE's (digamma / lgamma
   // per unit) beside the pool scoring on st3; the light ones in order (run beside pair_fwd they
   // slowed it more than they took: C5-q2b scoring forward 57 -> 62 us)
+  // (pair kernels: on st3 beside the pair epilogue, forked once pair_fwd is enqueued -- beside
+  // pair_fwd itself it slowed that kernel more than it saved)
   const bool pos_side = h->kind == KG_BETAE;
+  const bool pos_between = !pos_side && !gemm_scoring(h) && K > 0;
   if (pos_side && (s = fork(h, st, h->st3)) != KG_OK) return s;
-  launch_pos(h->sk, pa, p.nout, pos_side ? h->st3 : st);
+  if (!pos_between) launch_pos(h->sk, pa, p.nout, pos_side ? h->st3 : st);
+  kg_status sb = KG_OK;
+  auto pos_beside_epi = [&]() {
+    sb = fork(h, st, h->st3);
+    launch_pos(h->sk, pa, p.nout, h->st3);
+  };
   ScoreArgs sa;
   sa.Q = h->Q; sa.NQ = S.NQ; sa.M = M; sa.K = K; sa.Kp = S.Kp; sa.U = U; sa.d = d;
   if (h->kind == KG_BETAE) { sa.E = h->F; sa.eidx = nullptr; sa.estride = 9LL * h->m; }
@@ -1775,8 +1785,11 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   sa.cap_D = h->cap_D; sa.cap_Q = h->cap_Q; sa.cap_V = h->cap_V;
   sa.dV = h->OG + (int64_t)(na * M + M) * d;
   const int njt = K > 0 ? 1 : 0;
-  if (K > 0 && (s = score_forward(h, sa, p.nout, true, neg_rows)) != KG_OK) return s;
-  if (pos_side && (s = join(h, h->st3, st)) != KG_OK) return s;
+  if (K > 0 && (s = score_forward(h, sa, p.nout, true, neg_rows,
+                                  pos_between ? std::function<void()>(pos_beside_epi) : std::function<void()>())) != KG_OK)
+    return s;
+  if (sb != KG_OK) return sb;
+  if ((pos_side || pos_between) && (s = join(h, h->st3, st)) != KG_OK) return s;
   // Eq. 1's loss, the step's fate (flags) and Adam's bias corrections: one CTA on st3, off the
   // scoring backward's path (only the updates need it: the early dense Adam waits for ev_loss,
   // the sparse update joins st3 before it)

@@ -1,5 +1,6 @@
 // kg_launch.h -- host-side launchers of the sm_100a kernels (internal to libkg.so).
 #pragma once
+#include <functional>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -45,7 +46,10 @@ struct PosArgs {
 };
 
 // k_score.cu
-void launch_pair_fwd(int kind, const ScoreArgs &a, int nout, bool train, cudaStream_t st);
+// between(): called after the pair kernel is enqueued and before its epilogue (kg_api.cu runs the
+// positive term there, on a side stream beside the epilogue)
+void launch_pair_fwd(int kind, const ScoreArgs &a, int nout, bool train, cudaStream_t st,
+                     const std::function<void()> &between = {});
 void launch_pair_bwd(int kind, const ScoreArgs &a, cudaStream_t st, cudaStream_t st2);
 // The dot-product scorers on the tensor-core GEMM (kg_api.cu): the pair epilogue over
 // Dpart (a.KS partials) and the dQ / dV combines over partQ / partV (a.JS / a.RS partials).
