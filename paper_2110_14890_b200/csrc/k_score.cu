@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(256) pair_epi_kernel(ScoreArgs a) {
 #pragma unroll
   for (int tt = 0; tt < NOUT; ++tt) csum[tt] = 0.f;
   const int jend = TRAIN ? a.Kp : K;
-  if (TRAIN && !Mdl::kBeta && !(K & 3) && !(a.Kp & 3) && (a.Dmin == nullptr)) {
+  if (TRAIN && !(K & 3) && !(a.Kp & 3) && (a.Dmin == nullptr)) {
     // 4 consecutive candidates per thread (float4 loads of the partials and stores of C); the
     // per-pair arithmetic is the scalar loop's below
     const float4 *Dp = reinterpret_cast<const float4 *>(a.Dpart);
@@ -431,8 +431,11 @@ __global__ void __launch_bounds__(256) pair_epi_kernel(ScoreArgs a) {
           const float4 q = Dp[z * zs / 4 + base];
           s4.x += q.x; s4.y += q.y; s4.z += q.z; s4.w += q.w;
         }
-        D4[tt] = make_float4(Mdl::fin(s4.x, 0.f, 0.f), Mdl::fin(s4.y, 0.f, 0.f), Mdl::fin(s4.z, 0.f, 0.f),
-                             Mdl::fin(s4.w, 0.f, 0.f));
+        const float cq = Mdl::kBeta ? a.Cq[tt * M + i] : 0.f;
+        float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (Mdl::kBeta && j0 < K) cv = *reinterpret_cast<const float4 *>(a.Cv + j0);   // K % 4 == 0
+        D4[tt] = make_float4(Mdl::fin(s4.x, cq, cv.x), Mdl::fin(s4.y, cq, cv.y), Mdl::fin(s4.z, cq, cv.z),
+                             Mdl::fin(s4.w, cq, cv.w));
       }
       const uint32_t word = j0 < K ? a.mask[(size_t)i * a.W + (j0 >> 5)] : 0u;
       float cf[NOUT][4];
