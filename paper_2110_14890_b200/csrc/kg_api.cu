@@ -528,7 +528,7 @@ struct kg_handle {
   // st5: the DAG backward's weight gradients (dW = dY^T X, bias column sums) -- they feed only the
   // dense Adam, so they run beside the dX chain; w_used: st5 joined the step, ev_wjoin its end
   cudaStream_t st5 = nullptr;
-  cudaEvent_t ev_wjoin = nullptr;
+  cudaEvent_t ev_wjoin = nullptr, ev_bent = nullptr;   // ev_bent: BetaE pool features done (st3)
   bool w_used = false;
   cudaEvent_t ev_rel = nullptr, ev_loss = nullptr, ev_early = nullptr;
   cudaEvent_t ev_i1 = nullptr, ev_i2 = nullptr;   // fork / join of the two Q2B intersection branches
@@ -1535,6 +1535,7 @@ kg_status kg_create(const kg_config *cfg, kg_handle **out) {
       cudaStreamCreateWithFlags(&h->st3, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->st5, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_wjoin, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_bent, cudaEventDisableTiming) != cudaSuccess ||
       cudaStreamCreateWithPriority(&h->st4, cudaStreamNonBlocking, kLowPriority()) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_rel, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_loss, cudaEventDisableTiming) != cudaSuccess ||
@@ -1736,6 +1737,7 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
     // on st3 beside the DAG forward, joined before the scoring
     if ((s = fork(h, st, h->st3)) != KG_OK) return s;
     launch_beta_entity(h->ent_src, neg_rows, K, h->m, h->F, h->Cv, h->st3);
+    CK(cudaEventRecord(h->ev_bent, h->st3));
   }
   CK(cudaEventRecord(h->ev_fork, st));
   CK(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
@@ -1753,8 +1755,11 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   const int U = (h->sk == KG_BETAE || h->sk == KG_ROTATE || h->sk == KG_COMPLEX) ? h->m : d;
   const float scale = 1.f / (float)((double)M * h->world);
   if (h->kind == KG_BETAE) {
-    launch_beta_query(h->Q, S.NQ, h->m, h->QP, h->Cq, st);
-    if (K > 0 && (s = join(h, h->st3, st)) != KG_OK) return s;   // beta_entity (st3)
+    // the query's Beta features (QP, Cq) and then the positive term on st3 beside pair_fwd
+    // (which reads only Q and the pool features); the pair epilogue joins st3
+    if ((s = fork(h, st, h->st3)) != KG_OK) return s;
+    launch_beta_query(h->Q, S.NQ, h->m, h->QP, h->Cq, h->st3);
+    if (K > 0) CK(cudaStreamWaitEvent(st, h->ev_bent, 0));   // pool features (st3, before the fork)
   }
   PosArgs pa;
   pa.M = M; pa.U = U; pa.d = d; pa.ent = h->ent_src; pa.ans_rows = h->rows + (int64_t)na * M; pa.Q = h->Q;
@@ -1765,15 +1770,15 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   // slowed it more than they took: C5-q2b scoring forward 57 -> 62 us)
   // (pair kernels: on st3 beside the pair epilogue, forked once pair_fwd is enqueued -- beside
   // pair_fwd itself it slowed that kernel more than it saved)
-  const bool pos_side = h->kind == KG_BETAE;
+  const bool pos_side = h->kind == KG_BETAE;   // st3 already forked (beta_query)
   const bool pos_between = !pos_side && !gemm_scoring(h) && K > 0;
-  if (pos_side && (s = fork(h, st, h->st3)) != KG_OK) return s;
   if (!pos_between) launch_pos(h->sk, pa, p.nout, pos_side ? h->st3 : st);
   kg_status sb = KG_OK;
   auto pos_beside_epi = [&]() {
     sb = fork(h, st, h->st3);
     launch_pos(h->sk, pa, p.nout, h->st3);
   };
+  auto join_before_epi = [&]() { sb = join(h, h->st3, st); };   // BetaE: QP / Cq / loss_pos (st3)
   ScoreArgs sa;
   sa.Q = h->Q; sa.NQ = S.NQ; sa.M = M; sa.K = K; sa.Kp = S.Kp; sa.U = U; sa.d = d;
   if (h->kind == KG_BETAE) { sa.E = h->F; sa.eidx = nullptr; sa.estride = 9LL * h->m; }
@@ -1786,7 +1791,9 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   sa.dV = h->OG + (int64_t)(na * M + M) * d;
   const int njt = K > 0 ? 1 : 0;
   if (K > 0 && (s = score_forward(h, sa, p.nout, true, neg_rows,
-                                  pos_between ? std::function<void()>(pos_beside_epi) : std::function<void()>())) != KG_OK)
+                                  pos_between ? std::function<void()>(pos_beside_epi)
+                                  : pos_side  ? std::function<void()>(join_before_epi)
+                                              : std::function<void()>())) != KG_OK)
     return s;
   if (sb != KG_OK) return sb;
   if ((pos_side || pos_between) && (s = join(h, h->st3, st)) != KG_OK) return s;
@@ -2657,6 +2664,7 @@ void kg_destroy(kg_handle *h) {
   if (h->st4) { cudaStreamSynchronize(h->st4); cudaStreamDestroy(h->st4); }
   if (h->st5) { cudaStreamSynchronize(h->st5); cudaStreamDestroy(h->st5); }
   if (h->ev_wjoin) cudaEventDestroy(h->ev_wjoin);
+  if (h->ev_bent) cudaEventDestroy(h->ev_bent);
   if (h->ev_i1) cudaEventDestroy(h->ev_i1);
   if (h->ev_i2) cudaEventDestroy(h->ev_i2);
   for (auto &g : h->graphs) cudaGraphExecDestroy(g.exec);
