@@ -632,6 +632,41 @@ void launch_ids_concat(const int64_t *anchors, int na, int M, const int64_t *ans
                                                  n_entities); ++g_launches; }
 }
 
+// Both of the step's index kernels in one launch: threads [0, L) do ids_concat_kernel's work,
+// threads [L, L + nproj M) rel_occ_kernel's (the same per-element code).
+__global__ void ids_rel_kernel(const int64_t *anchors, int na, int M, const int64_t *answers, int n_ans,
+                               const int64_t *negs, int K, int world, int64_t *ids, int64_t *rows_out,
+                               int64_t n_entities, const int32_t *relations, int nr, Slots4 slots, int nproj,
+                               int n_rel, int32_t *occ, int32_t *bad) {
+  KG_GRID_DEP_WAIT();
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nai = na * M, L = nai + n_ans + K;
+  if (p < L) {
+    int64_t id;
+    if (p < nai) { const int a = p / M, i = p - a * M; id = anchors[(int64_t)i * na + a]; }
+    else if (p < nai + n_ans) id = answers[p - nai];
+    else id = negs[p - nai - n_ans];
+    if (id < 0 || id >= n_entities) { bad[0] = 1; id = 0; }
+    ids[p] = id;
+    rows_out[p] = id / world;
+    return;
+  }
+  const int e = p - L;
+  if (e >= nproj * M) return;
+  const int u = e / M, i = e - u * M;
+  int r = relations[(int64_t)i * nr + slots.s[u]];
+  if (r < 0 || r >= n_rel) { bad[0] = 1; r = 0; }
+  occ[e] = r;
+}
+void launch_ids_rel(const int64_t *anchors, int na, int M, const int64_t *answers, int n_ans, const int64_t *negs,
+                    int K, int world, int64_t *ids, int64_t *rows_out, int64_t n_entities, const int32_t *relations,
+                    int nr, Slots4 slots, int nproj, int n_rel, int32_t *occ, int32_t *bad, cudaStream_t st) {
+  const int n = na * M + n_ans + K + nproj * M;
+  if (n > 0)
+    { ids_rel_kernel<<<blocks(n), 256, 0, st>>>(anchors, na, M, answers, n_ans, negs, K, world, ids, rows_out,
+                                              n_entities, relations, nr, slots, nproj, n_rel, occ, bad); ++g_launches; }
+}
+
 // occ[u*M + i] = relations[i][slot_u] (one relation occurrence per projection use).
 __global__ void rel_occ_kernel(const int32_t *relations, int M, int nr, Slots4 slots, int nproj, int n_rel,
                                int32_t *occ, int32_t *bad) {

@@ -169,7 +169,11 @@ template <int BN, bool AMN, bool BMN, bool ATM = true, bool DRAIN = true, int OC
   // split (tools/gemm_trace.py: ~1,000 cycles from TMA issue to landed, against ~750 cycles per
   // k-block of MMA work at 128 x 160)
   static constexpr int kSmemStages0 = kSmemFit < kStages + kGroup ? kSmemFit : kStages + kGroup;
-  static constexpr int kSmemStages = (ATM && DRAIN && kSmemStages0 > kStages) ? kSmemStages0 : kStages;
+#ifndef KG_GEMM_SMEM_STAGES_DECOUPLED
+#define KG_GEMM_SMEM_STAGES_DECOUPLED 1
+#endif
+  static constexpr int kSmemStages =
+      (KG_GEMM_SMEM_STAGES_DECOUPLED && ATM && DRAIN && kSmemStages0 > kStages) ? kSmemStages0 : kStages;
   static constexpr int kSmem = kSmemStages * kStage + 1024;
   static constexpr int oAhi = kA + kB, oBhi = ATM ? kA + kB : oAhi + (AMN ? kA : 0);
   static constexpr int oAlo = oBhi + (BMN ? kB : 0), oBlo = ATM ? oAlo : oAlo + kA;

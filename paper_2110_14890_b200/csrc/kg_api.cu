@@ -1721,15 +1721,14 @@ kg_status enqueue_step(kg_handle *h, StepBufs &S) {
   // a2: ids (fused gather indices) on the main stream; dedup of entities and relations
   // on the side stream -- only the sparse update at the end needs them
   CK(cudaMemsetAsync(h->flags, 0, 2 * sizeof(int), st));
-  launch_ids_concat(h->b_anchors, na, M, h->b_answers, M, h->b_negs, K, h->world, h->ids, h->rows, h->flags + 1,
-                    h->n_ent, st);
   Slots4 sl{{0, 0, 0, 0}};
   {
     int u = 0;
     for (int ni = 0; ni < p.nn; ++ni)
       if (p.n[ni].type == 0) sl.s[u++] = p.n[ni].rel;
   }
-  launch_rel_occ(h->b_rels, M, nr, sl, p.nproj, h->R, h->rocc, h->flags + 1, st);
+  launch_ids_rel(h->b_anchors, na, M, h->b_answers, M, h->b_negs, K, h->world, h->ids, h->rows, h->n_ent, h->b_rels,
+                 nr, sl, p.nproj, h->R, h->rocc, h->flags + 1, st);
   if (needs_wplanes(h, p) && (s = issue_wplanes(h, st, h->st4)) != KG_OK) return s;
   const int64_t *neg_rows = h->rows + (int64_t)na * M + M;
   if (h->kind == KG_BETAE && K > 0) {

@@ -223,6 +223,9 @@ void launch_scatter_rows(float *dst, const float *src, const int64_t *rows, int 
 void launch_ids_concat(const int64_t *anchors, int na, int M, const int64_t *answers, int n_ans, const int64_t *negs,
                        int K, int world, int64_t *ids, int64_t *rows_out, int32_t *bad, int64_t n_entities,
                        cudaStream_t st);
+void launch_ids_rel(const int64_t *anchors, int na, int M, const int64_t *answers, int n_ans, const int64_t *negs,
+                    int K, int world, int64_t *ids, int64_t *rows_out, int64_t n_entities, const int32_t *relations,
+                    int nr, Slots4 slots, int nproj, int n_rel, int32_t *occ, int32_t *bad, cudaStream_t st);
 void launch_rel_occ(const int32_t *relations, int M, int nr, Slots4 slots, int nproj, int n_rel, int32_t *occ,
                     int32_t *bad, cudaStream_t st);
 

@@ -13,8 +13,14 @@ os.environ["KG_NCCL"] = "loopback"
 # rank's peer-memory barrier kernel (KG_XCHG=p2p), which spins until this rank arrives.
 # Separate processes (the real deployment) have separate contexts; here everything is loaded
 # up front.
+# Likewise the ranks' streams (six per handle, up to 4 handles) share the device's hardware work
+# queues: with the default 8 connections a rank's kernel can sit in the same queue behind another
+# rank's spinning barrier kernel and never start (the barrier then times out after 20 s); 32
+# connections give every stream its own queue.  One rank per GPU (the deployment) never has a
+# kernel of another rank on its device to wait behind.
 if os.environ.get("KG_XCHG") == "p2p":     # (eager loading of torch's modules costs ~30 s)
     os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+    os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
