@@ -301,14 +301,13 @@ __global__ void __launch_bounds__(128, 8) sparse_adam_fused_kernel(const int64_t
   const unsigned start_mask = __ballot_sync(0xffffffffu, rep && (base + lane == s0j || lane == 0));
   const unsigned cont_mask = rep_mask & ~start_mask;
   const unsigned end_mask = rep_mask & ~(cont_mask >> 1);
-  // the p, m, v slices of the segments that finish in this piece (single-piece) to L2 now
-  if (apply && ((start_mask >> lane) & 1u)) {
-    const bool single = (s1j - 1) / kPiece == s0j / kPiece;
-    if (single) {
-      const int64_t off = (kj / world) * d4 + c0;
-      for (int k = 0; k < cw; k += 8) {           // 128-byte lines
-        prefetch_l2(E4 + off + k); prefetch_l2(M4 + off + k); prefetch_l2(V4 + off + k);
-      }
+  // the p, m, v slices of the segments starting in this piece to L2 now -- single-piece ones are
+  // updated here, multi-piece (hot) ones by the item completing their last piece, which then
+  // finds them in L2 instead of paying a DRAM round trip after the piece sums
+  if (apply && base + lane == s0j && ((start_mask >> lane) & 1u)) {
+    const int64_t off = (kj / world) * d4 + c0;
+    for (int k = 0; k < cw; k += 8) {           // 128-byte lines
+      prefetch_l2(E4 + off + k); prefetch_l2(M4 + off + k); prefetch_l2(V4 + off + k);
     }
   }
   const uint32_t sb = (uint32_t)cw * 16u;
